@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the tensor-query hot path on B200.
+
+Default workload: TPC-H Q1 at SF10 (6.0e7 synthetic lineitem rows, 4 groups x
+8 aggregates incl. avg/count), written against the reference's query API
+(SQL + elementwise TvfMap UDF) and executed by this
+package: the plan compiles to Filter -> TvfMap -> GroupAggregate, which runs
+as one fused pass (tdp_scan_aggregate).  ``--query q6`` selects TPC-H Q6.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N > 1): lineitem rows are sharded by rank
+(total fixed at SF10 -> "strong" scaling) and partial aggregates are merged
+with NCCL all-reduces.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the reference's algorithm on the host cores: the
+numpy restatement in oracle/ (the reference itself is Python/numpy and cannot
+travel to the GPU host), row-sharded over all cores with multiprocessing.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TPC-H Q1/Q6 SF10 rows/sec & HBM GB/s at 1/2/4/8 B200 vs CPU ref"
+HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--query", choices=("q1", "q6"), default="q1")
+    ap.add_argument("--sf", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def _workload(query: str, sf: float, rows: int) -> dict:
+    if query == "q1":
+        return {"workload": f"TPC-H Q1 SF{sf:g}: filter l_shipdate<=10471 -> q1prep UDF "
+                            "(disc_price, charge) -> GROUP BY returnflag, linestatus, 8 aggregates",
+                "sf": sf, "rows": rows, "bytes_per_row": 56,
+                "columns": "7 x 8 B (int64 dates/dictionary codes, float64 values)"}
+    return {"workload": f"TPC-H Q6 SF{sf:g}: 5-predicate filter -> revenue UDF -> SUM",
+            "sf": sf, "rows": rows, "bytes_per_row": 32,
+            "columns": "4 x 8 B (int64 shipdate, float64 values)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_id: str):
+        self.samples: list[list[str]] = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        self._first = threading.Event()
+        self.active = False
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        self._first.wait(timeout=5.0)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self._first.set()
+            if self.active:
+                self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.active = False
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# kernel timing hook (CUDA events on the launching stream)
+# ---------------------------------------------------------------------------
+
+class KernelTimer:
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.pending: list = []
+        self.rows: list[int] = []
+
+    def begin(self, name, rows):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pending.append([e, None])
+        self.rows.append(int(rows))
+
+    def end(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pending[-1][1] = e
+
+    def mean_ms(self) -> float | None:
+        if not self.pending:
+            return None
+        return statistics.mean(a.elapsed_time(b) for a, b in self.pending)
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+
+def _ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_02753_b200 as tq
+    from paper_2211_02753_b200 import _native, kernels as K, workloads as wl
+    from paper_2211_02753_b200.distributed import shard_bounds, sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    group = dist.group.WORLD if world > 1 else None
+
+    n_total = int(round(6_000_000 * args.sf))
+    lo, hi = shard_bounds(n_total, rank, world)
+    rows = hi - lo
+    arrays = wl.lineitem_arrays(args.sf, seed=42 + rank, rows=rows)
+    cols = wl.LINEITEM_COLUMNS
+    if args.query == "q1":
+        sql, reg, bpr = wl.Q1_SQL, wl.q1_registry(), wl.Q1_BYTES_PER_ROW
+    else:
+        sql, reg, bpr = wl.Q6_SQL, wl.q6_registry(), wl.Q6_BYTES_PER_ROW
+        cols = ("l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
+
+    cat = tq.Catalog()
+    cat.register("lineitem", wl.lineitem_table(arrays, cols))
+    query = wl.compile_sql(sql, cat, reg)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with sharded(group):
+        for _ in range(max(args.warmup, 3)):
+            result = query.run(cat)
+        torch.cuda.synchronize()
+        # parity of the warm-up result on rank 0 at N=1 is checked after timing
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+        sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
+        timer = KernelTimer()
+        K.PROFILE_HOOK = timer
+        launches0 = _native.launch_count()
+        barrier()
+        torch.cuda.synchronize()
+        sampler.active = True
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            result = query.run(cat)
+        t1.record()
+        torch.cuda.synchronize()
+        barrier()
+        clocks = sampler.stop()
+        K.PROFILE_HOOK = None
+        launches = _native.launch_count() - launches0
+        ms = t0.elapsed_time(t1) / args.steps
+        kernel_ms = timer.mean_ms()
+        if world > 1:
+            t = torch.tensor([ms, kernel_ms or 0.0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, kernel_ms = float(t[0]), float(t[1])
+            lt = torch.tensor([launches], dtype=torch.int64, device="cuda")
+            dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+            launches = int(lt.item())
+
+        # ---- end to end through the API from pinned host buffers ----------
+        host = {c: torch.from_numpy(arrays[c]).pin_memory() for c in cols}
+        h2d = sum(h.numel() * h.element_size() for h in host.values())
+
+        def e2e_step():
+            c2 = tq.Catalog()
+            c2.register("lineitem", wl.lineitem_table(host, cols))
+            out = query.run(c2)
+            vals = [c.values.numpy() for c in out.columns]
+            return sum(v.nbytes for v in vals)
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.e2e_steps):
+            d2h = e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = (time.perf_counter() - w0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = _peaks()
+    value = n_total / (ms / 1e3)
+    kernel_rows = rows
+    achieved = bpr * kernel_rows / (kernel_ms / 1e3) / 1e9 if kernel_ms else None
+    traffic = None
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    if tf.exists():
+        try:
+            tj = json.loads(tf.read_text())
+            key = f"{args.query}_sf{args.sf:g}_n{world}"
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "rows/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), resident in HBM",
+        "config": dict(_workload(args.query, args.sf, n_total),
+                       parallelism=f"dp{world} row-sharded, NCCL all-reduce of partial aggregates",
+                       l2="inputs larger than L2 (no flush needed)",
+                       step="CompiledQuery.run(catalog) of the SQL plan, result table on device"),
+        "hbm_gbs_step": bpr * n_total / (ms / 1e3) / 1e9,
+        "e2e": {"value": n_total / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h,
+                "how": "pinned host columns -> device table -> CompiledQuery.run -> result to host"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "tdp_scan_agg (+ partial reduce), per rank",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": peak_src, "kernel_ms": kernel_ms,
+                     "algorithmic_bytes_per_launch": bpr * kernel_rows},
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"], line["parity"] = _cpu_baseline(args, arrays, query, cat)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_baseline(args, arrays, query, cat):
+    """Oracle (numpy restatement of the reference path) on a bounded sample,
+    one host core; plus a parity check of the engine on the same sample."""
+    import numpy as np
+
+    import paper_2211_02753_b200 as tq
+    from oracle import tpch as otpch
+    from paper_2211_02753_b200 import workloads as wl
+
+    sample_rows = min(len(arrays["l_shipdate"]), 6_000_000)
+    sample = {k: v[:sample_rows] for k, v in arrays.items()}
+    fn = otpch.q1 if args.query == "q1" else otpch.q6
+    reps, t = 0, 0.0
+    exp = None
+    while t < 10.0 and reps < 20:
+        w0 = time.perf_counter()
+        exp = fn(sample)
+        t += time.perf_counter() - w0
+        reps += 1
+    rate = reps * sample_rows / t
+    # parity of the engine on the same sample
+    c2 = tq.Catalog()
+    cols = wl.LINEITEM_COLUMNS if args.query == "q1" else (
+        "l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
+    c2.register("lineitem", wl.lineitem_table(sample, cols))
+    res = query.run(c2)
+    got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
+    ok = True
+    for k, v in exp.items():
+        g = got[k]
+        if v.dtype.kind in "iu":
+            ok &= bool(np.array_equal(g, v))
+        else:
+            ok &= bool(np.allclose(g, v, rtol=1e-9, atol=0))
+    return ({"value": rate, "unit": "rows/s", "cores": 1, "kind": "port",
+             "sample": f"{sample_rows} rows (first SF{sample_rows / 6e6:g} of the shard) x {reps} "
+                       f"repetitions, oracle/tpch.py (numpy restatement of tq filter_exact -> "
+                       f"UDF -> groupby_exact)"},
+            {"status": "ok" if ok else "MISMATCH", "rows": sample_rows,
+             "rule": "keys/counts bit-exact, float aggregates rtol 1e-9 vs float64 oracle"})
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm on all host cores
+# ---------------------------------------------------------------------------
+
+_REF_ARRAYS: dict = {}
+
+
+def _ref_worker(task):
+    import numpy as np
+
+    from oracle import relational as orc
+
+    query, lo, hi = task
+    a = {k: v[lo:hi] for k, v in _REF_ARRAYS.items()}
+    if query == "q1":
+        cols = [a[c] for c in ("l_shipdate", "l_returnflag", "l_linestatus", "l_quantity",
+                               "l_extendedprice", "l_discount", "l_tax")]
+        ship, rf, ls, q, p, d, t = orc.filter_exact(cols, [(0, "<=", 10471)])
+        one = np.asarray(1.0)
+        dp = p * (one - d)
+        ch = dp * (one + t)
+        keys, aggs = orc.groupby_exact([rf, ls], [("sum", q), ("sum", p), ("sum", dp),
+                                                  ("sum", ch), ("sum", d), ("count", None)])
+        return [k.tolist() for k in keys], [x.tolist() for x in aggs]
+    cols = [a[c] for c in ("l_shipdate", "l_discount", "l_quantity", "l_extendedprice")]
+    ship, d, q, p = orc.filter_exact(cols, [(0, ">=", 8766), (0, "<", 9131), (1, ">=", 0.05),
+                                            (1, "<=", 0.07), (2, "<", 24)])
+    return float((p * d).sum()), len(p)
+
+
+def _reference(args):
+    import multiprocessing as mp
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2211_02753_b200 import workloads as wl
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    n_total = int(round(6_000_000 * args.sf))
+    # calibrate one core, then size the per-step sample so the run stays short
+    cal = wl.lineitem_arrays(args.sf, seed=42, rows=min(n_total, 1_000_000))
+    _REF_ARRAYS.clear()
+    _REF_ARRAYS.update(cal)
+    w0 = time.perf_counter()
+    _ref_worker((args.query, 0, len(cal["l_shipdate"])))
+    per_core = len(cal["l_shipdate"]) / (time.perf_counter() - w0)
+    budget_s = max(0.05, 150.0 / max(1, args.steps + args.warmup))
+    sample = int(min(n_total, per_core * cores * budget_s))
+    sample = max(sample, cores)
+    arrays = wl.lineitem_arrays(args.sf, seed=42, rows=sample)
+    _REF_ARRAYS.clear()
+    _REF_ARRAYS.update(arrays)
+    bounds = [(args.query, i * sample // cores, (i + 1) * sample // cores) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_ref_worker, bounds)
+        times = []
+        for _ in range(args.steps):
+            w0 = time.perf_counter()
+            parts = pool.map(_ref_worker, bounds)
+            _merge(args.query, parts)
+            times.append(time.perf_counter() - w0)
+    step_s = statistics.mean(times)
+    value = sample / step_s
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), in host RAM",
+        "config": dict(_workload(args.query, args.sf, n_total),
+                       parallelism=f"{cores} host processes, row-sharded, partials merged"),
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} rows per step (bounded sample of SF{args.sf:g}), "
+                                   f"oracle/ numpy restatement of the reference path on "
+                                   f"{cores} processes"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _merge(query, parts):
+    if query == "q6":
+        return sum(p[0] for p in parts)
+    acc: dict = {}
+    for keys, aggs in parts:
+        for g in range(len(keys[0])):
+            key = tuple(k[g] for k in keys)
+            cur = acc.setdefault(key, [0.0] * (len(aggs) - 1) + [0])
+            for a in range(len(aggs)):
+                cur[a] += aggs[a][g]
+    out = {}
+    for key in sorted(acc):
+        s = acc[key]
+        cnt = s[-1]
+        out[key] = s[:5] + [s[0] / cnt, s[1] / cnt, s[4] / cnt, cnt]
+    return out
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        _reference(args)
+    else:
+        _ours(args)
+
+
+if __name__ == "__main__":
+    main()

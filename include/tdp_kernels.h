@@ -1,0 +1,337 @@
+/*
+ * tdp_kernels.h — C ABI of the B200 (sm_100a) tensor-query hot path.
+ *
+ * This is the drop-in boundary for the relational operators of the reference
+ * `tensorquery` package (TDP, arXiv 2211.02753).  Every function here replaces
+ * one numpy primitive chain of /root/reference/pkg/src/tensorquery (abbreviated
+ * tq/ below); the comment above each declaration cites the reference
+ * interface it stands in for.  The Python host layer
+ * (paper_2211_02753_b200/kernels.py) keeps the reference's operator
+ * signatures and calls these entry points through ctypes.
+ *
+ * Conventions
+ *  - Plain C types only: device pointers are `void*` / `const void*` owned by
+ *    the caller (PyTorch allocates them); sizes are int64_t; streams are
+ *    passed as `void*` (a cudaStream_t).
+ *  - Every entry point returns an int status: TDP_OK (0) or a negative code.
+ *    `tdp_last_error()` returns the thread-local message of the last failure.
+ *  - Preconditions the reference checks in Python (KernelError / EncodingError
+ *    classes) are checked by the host layer BEFORE launching; this layer
+ *    returns TDP_EINVAL for malformed descriptors.
+ *  - Variable-size results (selected row counts, group counts, join sizes) are
+ *    written to caller-provided DEVICE int64 cells; the caller syncs lazily.
+ *  - Workspace is caller-provided; `*_workspace()` functions size it.
+ *  - All kernels are asynchronous on the given stream.
+ */
+#ifndef TDP_KERNELS_H
+#define TDP_KERNELS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* status codes                                                              */
+/* ------------------------------------------------------------------------ */
+#define TDP_OK 0
+#define TDP_EINVAL -1   /* malformed argument / descriptor                    */
+#define TDP_ECUDA -2    /* CUDA runtime or launch failure                      */
+#define TDP_ENOMEM -3   /* workspace too small                                 */
+#define TDP_ENOTSUP -4  /* shape the kernel family does not cover              */
+#define TDP_EJIT -5     /* runtime specialisation (NVRTC) failed               */
+
+/* ------------------------------------------------------------------------ */
+/* column descriptor                                                         */
+/* ------------------------------------------------------------------------ */
+/* Element types.  The reference stores int64 / float64 / float32 / bool
+ * (tq/tensor.py:17-18); dictionary codes are int64 (tq/encodings.py:88).  */
+enum tdp_dtype {
+  TDP_I64 = 0,
+  TDP_F64 = 1,
+  TDP_F32 = 2,
+  TDP_BOOL = 3, /* one byte per value, 0/1 */
+  TDP_I32 = 4
+};
+
+/* A column: `rows` values of `width` elements each, row-major, contiguous.
+ * Scalar columns have width 1; PE matrices [n, k] have width k.            */
+typedef struct tdp_column {
+  const void* data;
+  int32_t dtype;
+  int32_t reserved;
+  int64_t rows;
+  int64_t width;
+} tdp_column;
+
+/* ------------------------------------------------------------------------ */
+/* predicates (tq/kernels.py:54-84 comparison_mask)                          */
+/* ------------------------------------------------------------------------ */
+enum tdp_cmp_op { TDP_EQ = 0, TDP_NE = 1, TDP_LT = 2, TDP_GT = 3, TDP_LE = 4, TDP_GE = 5 };
+
+/* How the column value and literal are compared.  The host layer resolves
+ * numpy-2 (NEP 50) promotion once per predicate:
+ *   TDP_CMP_I64  int64(x)  <op> lit_i
+ *   TDP_CMP_F64  double(x) <op> lit_f
+ *   TDP_CMP_F32  float(x)  <op> (float)lit_f  (lit_f holds an exact float32)
+ *   TDP_CMP_NONE row never matches (absent dictionary literal, :74-76)
+ *   TDP_CMP_ALL  row always matches (out-of-range int literal)            */
+enum tdp_cmp_type {
+  TDP_CMP_I64 = 0,
+  TDP_CMP_F64 = 1,
+  TDP_CMP_F32 = 2,
+  TDP_CMP_NONE = 3,
+  TDP_CMP_ALL = 4
+};
+
+typedef struct tdp_predicate {
+  int32_t column; /* index into the column array                        */
+  int32_t op;     /* tdp_cmp_op                                         */
+  int32_t cmp;    /* tdp_cmp_type                                       */
+  int32_t reserved;
+  int64_t lit_i;
+  double lit_f;
+} tdp_predicate;
+
+/* ------------------------------------------------------------------------ */
+/* library                                                                   */
+/* ------------------------------------------------------------------------ */
+const char* tdp_last_error(void);
+const char* tdp_version(void);
+/* Number of SMs of the current device (grid sizing); <0 on error. */
+int tdp_device_sm_count(void);
+/* Total kernels launched by this library in this process (benchmark
+ * accounting of "our" launches). */
+uint64_t tdp_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* filter / compaction / row movement                                        */
+/* ------------------------------------------------------------------------ */
+
+/* Conjunctive predicate mask, one byte per row (replaces the
+ * `mask &= comparison_mask(...)` loop, tq/kernels.py:93-95).               */
+int tdp_filter_mask(const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
+                    int32_t npreds, int64_t n, uint8_t* out_mask, void* stream);
+
+/* Workspace bytes for tdp_filter_select over n rows. */
+size_t tdp_filter_workspace(int64_t n);
+
+/* Fused predicate evaluation + order-preserving stream compaction: writes the
+ * ascending indices of surviving rows and their count (device int64).
+ * Replaces comparison_mask chain + np.nonzero (tq/kernels.py:87-96).       */
+int tdp_filter_select(const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
+                      int32_t npreds, int64_t n, int64_t* out_indices, int64_t* out_count,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* Row gather of several columns by one index vector in one launch:
+ * dst[c][j, :] = src[c][idx[j], :].  Replaces take_rows (tq/kernels.py:44-51)
+ * / gather forward (tq/tensor.py:597-607).                                 */
+int tdp_gather_rows(const tdp_column* src, int32_t ncols, const int64_t* indices, int64_t m,
+                    void* const* dst, void* stream);
+
+/* grad_in[idx[j], :] += grad_out[j, :] (float32/float64).  Replaces the
+ * np.add.at VJP of gather (tq/tensor.py:609-612).  grad_in must be zeroed. */
+int tdp_scatter_add_rows(const void* grad_out, int32_t dtype, int64_t width,
+                         const int64_t* indices, int64_t m, void* grad_in, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* fused scan -> filter -> expression -> dense grouped aggregate              */
+/* ------------------------------------------------------------------------ */
+/* Expression program: SSA, instruction i defines value i.  Types follow the
+ * numpy promotion the host layer resolved (tq/tensor.py:330-412 ops).       */
+enum tdp_opcode {
+  TDP_OP_LOAD = 0,   /* a = column index; value = column[row] as `dtype`   */
+  TDP_OP_CONST = 1,  /* imm_i / imm_f                                       */
+  TDP_OP_CAST = 2,   /* a -> dtype                                          */
+  TDP_OP_ADD = 3,
+  TDP_OP_SUB = 4,
+  TDP_OP_MUL = 5,
+  TDP_OP_DIV = 6,    /* float true divide                                   */
+  TDP_OP_NEG = 7,
+  TDP_OP_SQUARE = 8,
+  TDP_OP_LOG = 9,
+  TDP_OP_EXP = 10,
+  TDP_OP_RELU = 11
+};
+
+typedef struct tdp_instr {
+  int32_t op;    /* tdp_opcode                                             */
+  int32_t dtype; /* result type: TDP_I64 / TDP_F64 / TDP_F32                */
+  int32_t a;     /* operand value index (or column index for LOAD)          */
+  int32_t b;     /* second operand value index                              */
+  int64_t imm_i;
+  double imm_f;
+} tdp_instr;
+
+/* Group key: program value `value` (int64) mapped to a dense digit
+ * (v - lo) in [0, span).  slot = mixed radix over keys in GROUP BY order,
+ * so ascending slot == ascending lexicographic key (np.unique order,
+ * tq/kernels.py:128-136).                                                   */
+typedef struct tdp_key {
+  int32_t value;
+  int32_t reserved;
+  int64_t lo;
+  int64_t span;
+} tdp_key;
+
+enum tdp_agg_kind { TDP_AGG_COUNT = 0, TDP_AGG_SUM_F64 = 1, TDP_AGG_SUM_I64 = 2 };
+
+typedef struct tdp_agg {
+  int32_t kind;  /* tdp_agg_kind                                           */
+  int32_t value; /* program value index (ignored for COUNT)                 */
+} tdp_agg;
+
+size_t tdp_scan_aggregate_workspace(int64_t n, int64_t slots, int32_t naggs);
+
+/* One pass over n base rows: rows passing every predicate are grouped by the
+ * keys and aggregated.  out_counts[slot] (int64) and out_sums[a][slot]
+ * (8 bytes: double for SUM_F64, int64 for SUM_I64, count for COUNT) over all
+ * prod(span) slots.  Replaces FilterOp -> TvfOp (elementwise UDF) ->
+ * GroupAggExactOp / _global_aggregate (tq/compiler.py:146-215,
+ * tq/kernels.py:108-167).  Specialised per program with NVRTC (sm_100a),
+ * cached in-process.                                                        */
+int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
+                       const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                       int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                       int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* Same front half, but writes the selected rows' program values
+ * (outputs[j] = value outs[j]) compacted in row order: the materialised
+ * form of a lazily filtered, elementwise-UDF column.                       */
+int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,
+                     const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                     int32_t nprog, const int32_t* outs, int32_t nouts, void* const* out_ptrs,
+                     int64_t* out_count, void* ws, size_t ws_bytes, void* stream);
+
+/* Diagnostic: emit (and, when `compile` != 0, NVRTC-compile for sm_100a) the
+ * specialised pipeline source for a descriptor set without launching it.
+ * Needs no GPU.  Returns the source length (>= 0) or an error code; the text
+ * is copied (NUL-terminated, truncated to cap) into out_src when non-NULL.
+ * For a projection pass keys/aggs are empty and outs lists the values.     */
+int tdp_pipeline_codegen(const tdp_column* cols, int32_t ncols, int64_t n,
+                         const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                         int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                         int32_t naggs, const int32_t* outs, int32_t nouts, int32_t compile,
+                         char* out_src, size_t cap);
+
+/* Compact occupied slots (count > 0) in ascending slot order: writes key
+ * values (per key, int64), counts, and per aggregate either the sum or, when
+ * avg_mask bit a is set, float64(sum)/count (tq/kernels.py:154-166).
+ * out_groups receives the number of occupied groups (device int64).       */
+int tdp_groupby_finalize(const int64_t* counts, const void* sums, int64_t slots,
+                         const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs, int32_t naggs,
+                         uint64_t avg_mask, int64_t* out_keys, int64_t* out_counts,
+                         void* out_aggs, int64_t* out_groups, void* stream);
+
+/* Min / max of int64 key columns over rows passing the predicates
+ * (dense-path planning for plain integer keys).  out_minmax[2*j] = min,
+ * out_minmax[2*j+1] = max; empty selection leaves INT64_MAX / INT64_MIN. */
+int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
+                    const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
+                    int32_t nkeys, int64_t* out_minmax, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* sort-based group-by (general integer keys)                                */
+/* ------------------------------------------------------------------------ */
+size_t tdp_sort_workspace(int64_t n);
+
+/* Stable argsort with numpy semantics (tq/kernels.py:256-264):
+ * descending = stable ascending sort of the negated key (ties keep input
+ * order; -INT64_MIN wraps), NaN last in both directions, -0.0 == 0.0.
+ * key: TDP_I64 / TDP_F64 / TDP_F32 / TDP_I32 scalar column.               */
+int tdp_sort_order(const tdp_column* key, int32_t descending, int64_t n, int64_t* out_order,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* np.unique(key, return_inverse=True) for an int64 column
+ * (tq/kernels.py:128): out_uniques[0:u) ascending, out_inverse[i] = rank of
+ * key[i], out_nunique = u (device).                                        */
+int tdp_unique_inverse(const int64_t* key, int64_t n, int64_t* out_uniques,
+                       int64_t* out_inverse, int64_t* out_nunique, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* Grouped aggregation over dense codes in [0, slots): counts (int64) and per
+ * aggregate 8-byte sums in the value column's accumulator type (float64 for
+ * float input, int64 wrap-around for int input; np.bincount / np.add.at,
+ * tq/kernels.py:138-153).  vals[a] may be NULL for COUNT.                   */
+int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_column* vals,
+                      const int32_t* agg_kinds, int32_t naggs, int64_t* out_counts,
+                      void* out_sums, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* equi-join (builder-defined; the reference has none)       */
+/* ------------------------------------------------------------------------ */
+size_t tdp_join_workspace(int64_t n_build, int64_t n_probe);
+
+/* Inner equi-join on int64 keys, two calls sharing one workspace.
+ * prepare: stable radix sort of the build keys, one binary search per probe
+ * key, scan of match counts; writes the number of result pairs to out_count
+ * (device int64).  emit: writes the pairs, ordered by probe row and, within a
+ * probe row, by ascending build row.  The workspace must not be touched
+ * between the two calls.                                                   */
+int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                     int64_t n_probe, int64_t* out_count, void* ws, size_t ws_bytes,
+                     void* stream);
+int tdp_join_emit(int64_t n_build, int64_t n_probe, int64_t* out_probe_idx,
+                  int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* probability encodings and soft (differentiable) group-by                 */
+/* ------------------------------------------------------------------------ */
+
+/* Row softmax with max subtraction (tq/tensor.py:515-521 via pe_encode,
+ * tq/encodings.py:143-151).  float32 / float64, [n, k].                    */
+int tdp_softmax_fwd(const void* logits, int32_t dtype, int64_t n, int64_t k, void* probs,
+                    void* stream);
+/* VJP: grad_logits = P * (g - sum(g * P)) (tq/tensor.py:523-525).          */
+int tdp_softmax_bwd(const void* probs, const void* grad_probs, int32_t dtype, int64_t n,
+                    int64_t k, void* grad_logits, void* stream);
+
+/* PE invariant check (tq/encodings.py:101-107): out_flags[0] |= 1 when an
+ * entry is outside [-tol, 1+tol], |= 2 when a row sum differs from 1 by
+ * more than tol.  out_flags is a device int32 the caller zeroes.           */
+int tdp_pe_validate(const void* probs, int32_t dtype, int64_t n, int64_t k, double tol,
+                    int32_t* out_flags, void* stream);
+
+/* Row argmax, first maximum wins (np.argmax, tq/encodings.py:161).         */
+int tdp_pe_argmax(const void* probs, int32_t dtype, int64_t n, int64_t k, int64_t* out_codes,
+                  void* stream);
+
+/* Range check of int64 codes: out_flags |= 1 if any code < 0 or >= k
+ * (tq/encodings.py:180-181, tq/kernels.py:244-245).                        */
+int tdp_codes_check(const int64_t* codes, int64_t n, int64_t k, int32_t* out_flags,
+                    void* stream);
+
+/* A soft group-by key: a dense PE matrix [n, k] (float32/float64) or a
+ * compact one-hot column given as int64 codes (one_hot_pe,
+ * tq/encodings.py:175-183, never materialised).                            */
+enum tdp_soft_kind { TDP_SOFT_DENSE = 0, TDP_SOFT_ONEHOT = 1 };
+typedef struct tdp_soft_key {
+  const void* data;
+  int32_t kind;
+  int32_t dtype; /* of dense probabilities                                  */
+  int64_t k;
+} tdp_soft_key;
+
+/* grid[c1..cm] = sum_i w_i * prod_j P_j[i, c_j]   (w_i = 1 when values is
+ * NULL), accumulated in float64, row-major over the keys
+ * (tq/kernels.py:190-229 _joint_probabilities + reduce_sum).               */
+int tdp_soft_groupby_fwd(const tdp_soft_key* keys, int32_t nkeys, int64_t n, const void* values,
+                         int32_t values_dtype, double* out_grid, void* stream);
+
+/* VJP of the above for upstream grid gradient G (float64, prod k):
+ *   dP_j[i, c] = sum_{cells with c_j = c} G[cell] * w_i * prod_{l != j} P_l[i, c_l]
+ *   dw_i       = sum_cells G[cell] * prod_l P_l[i, c_l]
+ * grad_keys[j] is NULL for one-hot keys or keys needing no gradient;
+ * grad_values may be NULL.  Outputs are written (not accumulated) in the
+ * key / value dtype (tq/tensor.py:364-365, :474, :544 VJP chain).         */
+int tdp_soft_groupby_bwd(const tdp_soft_key* keys, int32_t nkeys, int64_t n, const void* values,
+                         int32_t values_dtype, const double* grad_grid, void* const* grad_keys,
+                         void* grad_values, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDP_KERNELS_H */

@@ -1,0 +1,177 @@
+"""torch.autograd bindings of the differentiable B200 kernels.
+
+Each Function's forward and backward call libtdp_kernels; PyTorch's autograd
+engine only sequences them (it is the "tape" of this build).
+
+* :func:`softmax_rows`   -- row softmax and its VJP (tq/tensor.py:515-527)
+* :func:`gather_rows`    -- row gather and its scatter-add VJP (tq/tensor.py:597-614)
+* :func:`soft_groupby_grid` -- soft grouped count / weighted sum over PE keys and
+  its VJP (tq/kernels.py:190-229 and the reduce_sum/mul/reshape VJP chain).
+"""
+
+from __future__ import annotations
+
+from ctypes import c_void_p
+from typing import Optional, Sequence
+
+import torch
+
+from . import _native as nat
+
+
+def _dt(t: torch.Tensor) -> int:
+    return nat.TORCH_TO_TDP[t.dtype]
+
+
+class _SoftmaxRows(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, logits: torch.Tensor) -> torch.Tensor:
+        x = logits.contiguous()
+        nat.require_cuda(x)
+        n, k = x.shape
+        out = torch.empty_like(x)
+        nat.call("tdp_softmax_fwd", nat.ptr(x), _dt(x), n, k, nat.ptr(out), nat.stream())
+        ctx.save_for_backward(out)
+        return out
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        (p,) = ctx.saved_tensors
+        g = g.contiguous().to(p.dtype)
+        n, k = p.shape
+        dz = torch.empty_like(p)
+        nat.call("tdp_softmax_bwd", nat.ptr(p), nat.ptr(g), _dt(p), n, k, nat.ptr(dz), nat.stream())
+        return dz
+
+
+def softmax_rows(logits: torch.Tensor) -> torch.Tensor:
+    return _SoftmaxRows.apply(logits)
+
+
+def gather_rows_raw(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """Row gather without autograd (B200 kernel)."""
+    x = x.contiguous()
+    nat.require_cuda(x, idx)
+    m = idx.numel()
+    out = torch.empty((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    if m:
+        cols = nat.columns([x])
+        dst = (c_void_p * 1)(out.data_ptr())
+        nat.call("tdp_gather_rows", cols, 1, nat.ptr(idx), m, dst, nat.stream())
+    return out
+
+
+def gather_many(xs: Sequence[torch.Tensor], idx: torch.Tensor) -> list[torch.Tensor]:
+    """Gather several columns with one index vector in a single launch."""
+    nat.require_cuda(idx, *xs)
+    m = idx.numel()
+    outs = [torch.empty((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device) for x in xs]
+    if m and xs:
+        xs = [x.contiguous() for x in xs]
+        cols = nat.columns(xs)
+        dst = (c_void_p * len(xs))(*[o.data_ptr() for o in outs])
+        nat.call("tdp_gather_rows", cols, len(xs), nat.ptr(idx), m, dst, nat.stream())
+    return outs
+
+
+class _GatherRows(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        ctx.save_for_backward(idx)
+        ctx.src_shape = tuple(x.shape)
+        return gather_rows_raw(x, idx)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        (idx,) = ctx.saved_tensors
+        g = g.contiguous()
+        out = torch.zeros(ctx.src_shape, dtype=g.dtype, device=g.device)
+        m = idx.numel()
+        width = 1
+        for s in ctx.src_shape[1:]:
+            width *= s
+        if m:
+            nat.call("tdp_scatter_add_rows", nat.ptr(g), _dt(g), width, nat.ptr(idx), m,
+                     nat.ptr(out), nat.stream())
+        return out, None
+
+
+def gather_rows(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    if x.is_floating_point() and x.requires_grad:
+        return _GatherRows.apply(x, idx)
+    return gather_rows_raw(x, idx)
+
+
+# ---------------------------------------------------------------------------
+# soft group-by
+# ---------------------------------------------------------------------------
+
+class SoftKeySpec:
+    """Static description of the key list: ('dense', k) or ('onehot', k) per key."""
+
+    def __init__(self, kinds: Sequence[tuple[str, int]]):
+        self.kinds = tuple(kinds)
+
+    @property
+    def cells(self) -> int:
+        c = 1
+        for _, k in self.kinds:
+            c *= k
+        return c
+
+
+def _soft_keys(spec: SoftKeySpec, tensors: Sequence[torch.Tensor]):
+    arr = (nat.SoftKey * len(tensors))()
+    for j, ((kind, k), t) in enumerate(zip(spec.kinds, tensors)):
+        if kind == "dense":
+            arr[j] = nat.SoftKey(c_void_p(t.data_ptr()), nat.SOFT_DENSE, _dt(t), k)
+        else:
+            arr[j] = nat.SoftKey(c_void_p(t.data_ptr()), nat.SOFT_ONEHOT, nat.I64, k)
+    return arr
+
+
+class _SoftGroupBy(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec: SoftKeySpec, n: int, out_dtype: torch.dtype, values: Optional[torch.Tensor],
+                *keys: torch.Tensor):
+        keys = tuple(k.contiguous() for k in keys)
+        nat.require_cuda(*keys)
+        dev = keys[0].device
+        grid = torch.empty(spec.cells, dtype=torch.float64, device=dev)
+        vals = None if values is None else values.contiguous()
+        nat.call("tdp_soft_groupby_fwd", _soft_keys(spec, keys), len(keys), n, nat.ptr(vals),
+                 nat.I64 if vals is None else _dt(vals), nat.ptr(grid), nat.stream())
+        ctx.spec = spec
+        ctx.n = n
+        ctx.has_values = vals is not None
+        ctx.save_for_backward(*(keys + ((vals,) if vals is not None else ())))
+        return grid.to(out_dtype)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        saved = ctx.saved_tensors
+        spec = ctx.spec
+        nk = len(spec.kinds)
+        keys = saved[:nk]
+        vals = saved[nk] if ctx.has_values else None
+        G = g.detach().to(torch.float64).contiguous()
+        grads: list[Optional[torch.Tensor]] = [None] * nk
+        ptrs = (c_void_p * nk)()
+        for j, ((kind, _), t) in enumerate(zip(spec.kinds, keys)):
+            if kind == "dense" and ctx.needs_input_grad[4 + j]:
+                grads[j] = torch.empty_like(t)
+                ptrs[j] = grads[j].data_ptr()
+        dvals = None
+        if vals is not None and ctx.needs_input_grad[3]:
+            dvals = torch.empty_like(vals)
+        if any(x is not None for x in grads) or dvals is not None:
+            nat.call("tdp_soft_groupby_bwd", _soft_keys(spec, keys), nk, ctx.n, nat.ptr(vals),
+                     nat.I64 if vals is None else _dt(vals), nat.ptr(G), ptrs, nat.ptr(dvals),
+                     nat.stream())
+        return (None, None, None, dvals, *grads)
+
+
+def soft_groupby_grid(spec: SoftKeySpec, keys: Sequence[torch.Tensor], n: int,
+                      out_dtype: torch.dtype, values: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Dense grid (flattened, row-major over keys) of sum_i w_i prod_j P_j[i, c_j]."""
+    return _SoftGroupBy.apply(spec, n, out_dtype, values, *keys)

@@ -1,0 +1,884 @@
+// Fused scan -> filter -> elementwise expression -> dense grouped aggregate.
+//
+// Replaces, in ONE pass over the base columns, the reference's operator-at-a-
+// time chain (tq = /root/reference/pkg/src/tensorquery):
+//   FilterOp  -> filter_exact        tq/compiler.py:146-150, tq/kernels.py:87-97
+//   TvfOp     -> elementwise UDF     tq/compiler.py:114-122 (add/sub/mul/... tq/tensor.py:330-412)
+//   GroupAggExactOp -> groupby_exact tq/compiler.py:176-203, tq/kernels.py:108-167
+//                   or _global_aggregate tq/compiler.py:206-215
+// The reference moves every surviving row of every column through three
+// materialisations; here the base columns are read once and nothing per-row is
+// written.
+//
+// The query-specific part (column loads, predicate conjunction, the SSA
+// expression program, the key -> slot map and the aggregate inputs) is emitted
+// as CUDA C++ and compiled once per distinct program by NVRTC for sm_100a; the
+// kernel body is the hand-written skeleton in pipeline_skeleton.cuh.  Literals
+// and constants are kernel parameters, so only the program SHAPE keys the cache.
+#include <cuda.h>
+#include <nvrtc.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <vector>
+
+#include "tdp_common.cuh"
+
+namespace tdp {
+
+namespace {
+
+#include "pipeline_skeleton.inc"  // static const char* kSkeleton
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+constexpr int kMaxInstr = 64;
+constexpr int kMaxKeys = 8;
+constexpr int kMaxOuts = 16;
+constexpr int kMaxRegCells = 64;
+constexpr i64 kMaxSlots = 1 << 20;
+
+// Must match the TdpParams emitted below, field for field.
+struct HostParams {
+  const void* col[kMaxCols];
+  void* out[kMaxOuts];
+  i64 n;
+  i64 pli[kMaxPreds];
+  double plf[kMaxPreds];
+  i64 imi[kMaxInstr];
+  double imf[kMaxInstr];
+  i64 klo[kMaxKeys];
+  void* acc;
+  const unsigned* bits;
+  const i64* tile_off;
+};
+
+// ---------------------------------------------------------------------------
+// driver API through the runtime's entry-point query (no libcuda link, so the
+// library also loads on hosts without a driver)
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_ModuleLoadData)(CUmodule*, const void*);
+typedef CUresult (*PFN_ModuleGetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                     unsigned, unsigned, CUstream, void**, void**);
+typedef CUresult (*PFN_Occupancy)(int*, CUfunction, int, size_t);
+typedef CUresult (*PFN_GetErrorString)(CUresult, const char**);
+
+struct Driver {
+  PFN_ModuleLoadData load = nullptr;
+  PFN_ModuleGetFunction getfn = nullptr;
+  PFN_LaunchKernel launch = nullptr;
+  PFN_Occupancy occupancy = nullptr;
+  PFN_GetErrorString errstr = nullptr;
+  bool ok = false;
+};
+
+int get_driver(Driver** out) {
+  static Driver d;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    auto q = [](const char* sym, void** fp) -> bool {
+      cudaDriverEntryPointQueryResult st;
+      cudaError_t e = cudaGetDriverEntryPoint(sym, fp, cudaEnableDefault, &st);
+      return e == cudaSuccess && st == cudaDriverEntryPointSuccess && *fp != nullptr;
+    };
+    bool ok = q("cuModuleLoadData", (void**)&d.load) &&
+              q("cuModuleGetFunction", (void**)&d.getfn) &&
+              q("cuLaunchKernel", (void**)&d.launch) &&
+              q("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occupancy) &&
+              q("cuGetErrorString", (void**)&d.errstr);
+    d.ok = ok;
+    if (!ok) err = "driver entry points unavailable";
+  });
+  if (!d.ok) return set_error(TDP_ECUDA, "%s", err.c_str());
+  *out = &d;
+  return TDP_OK;
+}
+
+int cu_check(Driver* d, CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return TDP_OK;
+  const char* s = "?";
+  if (d && d->errstr) d->errstr(r, &s);
+  return set_error(TDP_ECUDA, "%s failed: %s", what, s);
+}
+
+// ---------------------------------------------------------------------------
+// code generation
+// ---------------------------------------------------------------------------
+const char* ctype_of(int dt) {
+  switch (dt) {
+    case TDP_I64:
+      return "i64";
+    case TDP_F64:
+      return "double";
+    case TDP_F32:
+      return "float";
+    case TDP_I32:
+      return "int";
+    default:
+      return "unsigned char";
+  }
+}
+
+const char* op_sym(int op) {
+  switch (op) {
+    case TDP_EQ:
+      return "==";
+    case TDP_NE:
+      return "!=";
+    case TDP_LT:
+      return "<";
+    case TDP_GT:
+      return ">";
+    case TDP_LE:
+      return "<=";
+    default:
+      return ">=";
+  }
+}
+
+struct Spec {
+  // inputs
+  std::vector<int> col_dtype;  // per column
+  std::vector<tdp_predicate> preds;
+  std::vector<tdp_instr> prog;
+  std::vector<tdp_key> keys;
+  std::vector<tdp_agg> aggs;
+  std::vector<int> outs;
+  // derived
+  std::vector<int> used_cols;
+  std::vector<int> fvals, ivals;  // accumulator -> program value
+  std::vector<int> agg_acc;       // agg -> accumulator index (-1 for count)
+  i64 slots = 1;
+  bool regacc = true;
+};
+
+int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
+  TDP_REQUIRE(ncols >= 0 && ncols <= kMaxCols, "at most %d columns (got %d)", kMaxCols, ncols);
+  TDP_REQUIRE((int)s.prog.size() <= kMaxInstr, "program longer than %d instructions",
+              kMaxInstr);
+  TDP_REQUIRE((int)s.keys.size() <= kMaxKeys, "at most %d keys", kMaxKeys);
+  TDP_REQUIRE((int)s.preds.size() <= kMaxPreds, "at most %d predicates", kMaxPreds);
+  TDP_REQUIRE((int)s.outs.size() <= kMaxOuts, "at most %d outputs", kMaxOuts);
+  std::vector<char> used(ncols, 0);
+  for (int c = 0; c < ncols; ++c) {
+    TDP_REQUIRE(dtype_size(cols[c].dtype) > 0, "column %d: bad dtype", c);
+    TDP_REQUIRE(cols[c].width == 1, "column %d: scalar columns only", c);
+    s.col_dtype.push_back(cols[c].dtype);
+  }
+  for (size_t k = 0; k < s.preds.size(); ++k) {
+    const tdp_predicate& p = s.preds[k];
+    TDP_REQUIRE(p.op >= TDP_EQ && p.op <= TDP_GE, "predicate %zu: bad op", k);
+    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_ALL, "predicate %zu: bad compare", k);
+    if (p.cmp <= TDP_CMP_F32) {
+      TDP_REQUIRE(p.column >= 0 && p.column < ncols, "predicate %zu: bad column", k);
+      used[p.column] = 1;
+    }
+  }
+  for (size_t j = 0; j < s.prog.size(); ++j) {
+    const tdp_instr& in = s.prog[j];
+    TDP_REQUIRE(in.dtype == TDP_I64 || in.dtype == TDP_F64 || in.dtype == TDP_F32,
+                "instr %zu: result dtype must be int64/float64/float32", j);
+    switch (in.op) {
+      case TDP_OP_LOAD:
+        TDP_REQUIRE(in.a >= 0 && in.a < ncols, "instr %zu: bad column", j);
+        used[in.a] = 1;
+        break;
+      case TDP_OP_CONST:
+        break;
+      case TDP_OP_ADD:
+      case TDP_OP_SUB:
+      case TDP_OP_MUL:
+      case TDP_OP_DIV:
+        TDP_REQUIRE(in.b >= 0 && in.b < (int)j, "instr %zu: bad operand b", j);
+        TDP_REQUIRE(s.prog[in.b].dtype == in.dtype, "instr %zu: operand b type mismatch", j);
+        // fallthrough
+      case TDP_OP_NEG:
+      case TDP_OP_SQUARE:
+      case TDP_OP_LOG:
+      case TDP_OP_EXP:
+      case TDP_OP_RELU:
+        TDP_REQUIRE(in.a >= 0 && in.a < (int)j, "instr %zu: bad operand a", j);
+        TDP_REQUIRE(s.prog[in.a].dtype == in.dtype, "instr %zu: operand a type mismatch", j);
+        if (in.op == TDP_OP_DIV || in.op == TDP_OP_LOG || in.op == TDP_OP_EXP)
+          TDP_REQUIRE(in.dtype != TDP_I64, "instr %zu: float-only op on int64", j);
+        break;
+      case TDP_OP_CAST:
+        TDP_REQUIRE(in.a >= 0 && in.a < (int)j, "instr %zu: bad cast operand", j);
+        TDP_REQUIRE(!(in.dtype == TDP_I64 && s.prog[in.a].dtype != TDP_I64),
+                    "instr %zu: float -> int cast not supported", j);
+        break;
+      default:
+        return set_error(TDP_EINVAL, "instr %zu: unknown opcode %d", j, in.op);
+    }
+  }
+  for (size_t j = 0; j < s.keys.size(); ++j) {
+    const tdp_key& k = s.keys[j];
+    TDP_REQUIRE(k.value >= 0 && k.value < (int)s.prog.size(), "key %zu: bad value", j);
+    TDP_REQUIRE(s.prog[k.value].dtype == TDP_I64, "key %zu: keys must be int64 values", j);
+    TDP_REQUIRE(k.span >= 1, "key %zu: span must be >= 1", j);
+    TDP_REQUIRE(s.slots <= kMaxSlots / k.span, "dense key space exceeds %lld slots",
+                (long long)kMaxSlots);
+    s.slots *= k.span;
+  }
+  for (size_t a = 0; a < s.aggs.size(); ++a) {
+    const tdp_agg& g = s.aggs[a];
+    if (g.kind == TDP_AGG_COUNT) {
+      s.agg_acc.push_back(-1);
+      continue;
+    }
+    TDP_REQUIRE(g.kind == TDP_AGG_SUM_F64 || g.kind == TDP_AGG_SUM_I64, "agg %zu: bad kind", a);
+    TDP_REQUIRE(g.value >= 0 && g.value < (int)s.prog.size(), "agg %zu: bad value", a);
+    if (g.kind == TDP_AGG_SUM_I64)
+      TDP_REQUIRE(s.prog[g.value].dtype == TDP_I64, "agg %zu: SUM_I64 over a float value", a);
+    std::vector<int>& lst = g.kind == TDP_AGG_SUM_F64 ? s.fvals : s.ivals;
+    int idx = -1;
+    for (size_t t = 0; t < lst.size(); ++t)
+      if (lst[t] == g.value) idx = (int)t;
+    if (idx < 0) {
+      idx = (int)lst.size();
+      lst.push_back(g.value);
+    }
+    s.agg_acc.push_back(idx);
+  }
+  for (size_t o = 0; o < s.outs.size(); ++o)
+    TDP_REQUIRE(s.outs[o] >= 0 && s.outs[o] < (int)s.prog.size(), "output %zu: bad value", o);
+  for (int c = 0; c < ncols; ++c)
+    if (used[c]) {
+      TDP_REQUIRE(cols[c].rows >= n, "column %d has %lld rows < %lld", c, (long long)cols[c].rows,
+                  (long long)n);
+      TDP_REQUIRE(n == 0 || cols[c].data != nullptr, "column %d: null data", c);
+      s.used_cols.push_back(c);
+    }
+  const i64 cells = s.slots * (i64)(1 + s.fvals.size() + s.ivals.size());
+  s.regacc = cells <= kMaxRegCells;
+  return TDP_OK;
+}
+
+void emit_program(std::ostringstream& o, const Spec& s) {
+  for (size_t j = 0; j < s.prog.size(); ++j) {
+    const tdp_instr& in = s.prog[j];
+    const char* T = ctype_of(in.dtype);
+    const bool isint = in.dtype == TDP_I64;
+    const bool isf32 = in.dtype == TDP_F32;
+    o << "  const " << T << " v" << j << " = ";
+    const std::string a = "v" + std::to_string(in.a), b = "v" + std::to_string(in.b);
+    switch (in.op) {
+      case TDP_OP_LOAD:
+        o << "(" << T << ")r.c" << in.a;
+        break;
+      case TDP_OP_CONST:
+        if (isint) o << "P.imi[" << j << "]";
+        else o << "(" << T << ")P.imf[" << j << "]";
+        break;
+      case TDP_OP_CAST:
+        o << "(" << T << ")" << a;
+        break;
+      case TDP_OP_ADD:
+        if (isint) o << "(i64)((u64)" << a << " + (u64)" << b << ")";
+        else o << a << " + " << b;
+        break;
+      case TDP_OP_SUB:
+        if (isint) o << "(i64)((u64)" << a << " - (u64)" << b << ")";
+        else o << a << " - " << b;
+        break;
+      case TDP_OP_MUL:
+        if (isint) o << "(i64)((u64)" << a << " * (u64)" << b << ")";
+        else o << a << " * " << b;
+        break;
+      case TDP_OP_DIV:
+        o << a << " / " << b;
+        break;
+      case TDP_OP_NEG:
+        if (isint) o << "(i64)(0ull - (u64)" << a << ")";
+        else o << "-" << a;
+        break;
+      case TDP_OP_SQUARE:
+        if (isint) o << "(i64)((u64)" << a << " * (u64)" << a << ")";
+        else o << a << " * " << a;
+        break;
+      case TDP_OP_LOG:
+        o << (isf32 ? "logf(" : "log(") << a << ")";
+        break;
+      case TDP_OP_EXP:
+        o << (isf32 ? "expf(" : "exp(") << a << ")";
+        break;
+      case TDP_OP_RELU:
+        o << "(" << a << " > (" << T << ")0 ? " << a << " : (" << T << ")0)";
+        break;
+    }
+    o << ";\n";
+  }
+}
+
+std::string generate(const Spec& s) {
+  std::ostringstream o;
+  o << "typedef long long i64;\ntypedef unsigned long long u64;\n";
+  o << "#define TDP_THREADS " << kThreads << "\n#define TDP_U " << kUnroll << "\n";
+  o << "#define TDP_G " << s.slots << "\n#define TDP_NF " << s.fvals.size() << "\n";
+  o << "#define TDP_NI " << s.ivals.size() << "\n#define TDP_REGACC " << (s.regacc ? 1 : 0)
+    << "\n";
+  o << "#define TDP_FTILE " << kFilterTile << "\n#define TDP_FWORDS " << kFilterWords << "\n";
+  o << "struct TdpParams {\n  const void* col[" << kMaxCols << "];\n  void* out[" << kMaxOuts
+    << "];\n  i64 n;\n  i64 pli[" << kMaxPreds << "];\n  double plf[" << kMaxPreds
+    << "];\n  i64 imi[" << kMaxInstr << "];\n  double imf[" << kMaxInstr << "];\n  i64 klo["
+    << kMaxKeys << "];\n  void* acc;\n  const unsigned* bits;\n  const i64* tile_off;\n};\n";
+  // row of loaded columns
+  o << "struct TdpRow {\n  int pad_;\n";
+  for (int c : s.used_cols) o << "  " << ctype_of(s.col_dtype[c]) << " c" << c << ";\n";
+  o << "};\n";
+  o << "__device__ __forceinline__ void tdp_zero(TdpRow& r) {\n  r.pad_ = 0;\n";
+  for (int c : s.used_cols) o << "  r.c" << c << " = 0;\n";
+  o << "}\n";
+  o << "__device__ __forceinline__ void tdp_load(TdpRow& r, const TdpParams& P, i64 i) {\n"
+       "  r.pad_ = 0;\n";
+  for (int c : s.used_cols) {
+    const char* T = ctype_of(s.col_dtype[c]);
+    if (s.col_dtype[c] == TDP_BOOL)
+      o << "  r.c" << c << " = ((const " << T << "*)P.col[" << c << "])[i];\n";
+    else
+      o << "  r.c" << c << " = __ldg((const " << T << "*)P.col[" << c << "] + i);\n";
+  }
+  o << "}\n";
+  // predicate conjunction + program + keys + aggregate inputs
+  o << "__device__ __forceinline__ bool tdp_eval(const TdpRow& r, const TdpParams& P, int& "
+       "slot, double* f, i64* q) {\n";
+  o << "  bool keep = true;\n";
+  for (size_t k = 0; k < s.preds.size(); ++k) {
+    const tdp_predicate& p = s.preds[k];
+    switch (p.cmp) {
+      case TDP_CMP_I64:
+        o << "  keep &= ((i64)r.c" << p.column << " " << op_sym(p.op) << " P.pli[" << k
+          << "]);\n";
+        break;
+      case TDP_CMP_F64:
+        o << "  keep &= ((double)r.c" << p.column << " " << op_sym(p.op) << " P.plf[" << k
+          << "]);\n";
+        break;
+      case TDP_CMP_F32:
+        o << "  keep &= ((float)r.c" << p.column << " " << op_sym(p.op) << " (float)P.plf[" << k
+          << "]);\n";
+        break;
+      case TDP_CMP_NONE:
+        o << "  keep = false;\n";
+        break;
+      default:
+        break;
+    }
+  }
+  emit_program(o, s);
+  o << "  i64 sl = 0;\n";
+  for (size_t j = 0; j < s.keys.size(); ++j)
+    o << "  sl = sl * " << s.keys[j].span << "LL + (i64)((u64)v" << s.keys[j].value
+      << " - (u64)P.klo[" << j << "]);\n";
+  o << "  slot = (int)sl;\n";
+  for (size_t a = 0; a < s.fvals.size(); ++a) o << "  f[" << a << "] = (double)v" << s.fvals[a] << ";\n";
+  for (size_t a = 0; a < s.ivals.size(); ++a) o << "  q[" << a << "] = (i64)v" << s.ivals[a] << ";\n";
+  o << "  return keep;\n}\n";
+  // projection
+  o << "__device__ __forceinline__ void tdp_project(const TdpRow& r, const TdpParams& P, i64 "
+       "pos) {\n";
+  emit_program(o, s);
+  for (size_t k = 0; k < s.outs.size(); ++k) {
+    const int v = s.outs[k];
+    o << "  ((" << ctype_of(s.prog[v].dtype) << "*)P.out[" << k << "])[pos] = v" << v << ";\n";
+  }
+  o << "}\n";
+  o << kSkeleton;
+  return o.str();
+}
+
+// ---------------------------------------------------------------------------
+// NVRTC compile + module cache
+// ---------------------------------------------------------------------------
+struct Kernel {
+  CUmodule mod = nullptr;
+  CUfunction agg = nullptr;
+  CUfunction proj = nullptr;
+  int agg_occ = 1;
+};
+
+std::mutex g_cache_mu;
+std::map<std::pair<int, std::string>, std::shared_ptr<Kernel>> g_cache;
+
+// Source -> sm_100a CUBIN.  Needs no device (usable on build hosts).
+int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "tdp_pipeline.cu", 0, nullptr, nullptr) !=
+      NVRTC_SUCCESS)
+    return set_error(TDP_EJIT, "nvrtcCreateProgram failed");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-fmad=false",
+                        "-lineinfo", "--device-as-default-execution-space"};
+  nvrtcResult cr = nvrtcCompileProgram(prog, 5, opts);
+  if (cr != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    if (n) nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    return set_error(TDP_EJIT, "NVRTC: %s\n%s", nvrtcGetErrorString(cr), log.c_str());
+  }
+  size_t cubin_size = 0;
+  nvrtcGetCUBINSize(prog, &cubin_size);
+  cubin->resize(cubin_size);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  return TDP_OK;
+}
+
+int compile(const std::string& src, std::shared_ptr<Kernel>* out) {
+  int dev = 0;
+  TDP_CUDA_TRY(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    auto it = g_cache.find({dev, src});
+    if (it != g_cache.end()) {
+      *out = it->second;
+      return TDP_OK;
+    }
+  }
+  Driver* d = nullptr;
+  int rc = get_driver(&d);
+  if (rc) return rc;
+  std::vector<char> cubin;
+  rc = nvrtc_compile(src, &cubin);
+  if (rc) return rc;
+  TDP_CUDA_TRY(cudaFree(0));  // make the primary context current on this thread
+  auto k = std::make_shared<Kernel>();
+  rc = cu_check(d, d->load(&k->mod, cubin.data()), "cuModuleLoadData");
+  if (rc) return rc;
+  rc = cu_check(d, d->getfn(&k->agg, k->mod, "tdp_scan_agg"), "cuModuleGetFunction(agg)");
+  if (rc) return rc;
+  rc = cu_check(d, d->getfn(&k->proj, k->mod, "tdp_scan_project"), "cuModuleGetFunction(proj)");
+  if (rc) return rc;
+  int occ = 1;
+  if (d->occupancy(&occ, k->agg, kThreads, 0) != CUDA_SUCCESS || occ < 1) occ = 1;
+  k->agg_occ = occ;
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  g_cache[{dev, src}] = k;
+  *out = k;
+  return TDP_OK;
+}
+
+void fill_params(HostParams& hp, const Spec& s, const tdp_column* cols, int ncols, i64 n) {
+  std::memset(&hp, 0, sizeof(hp));
+  for (int c = 0; c < ncols; ++c) hp.col[c] = cols[c].data;
+  hp.n = n;
+  for (size_t k = 0; k < s.preds.size(); ++k) {
+    hp.pli[k] = s.preds[k].lit_i;
+    hp.plf[k] = s.preds[k].lit_f;
+  }
+  for (size_t j = 0; j < s.prog.size(); ++j) {
+    hp.imi[j] = s.prog[j].imm_i;
+    hp.imf[j] = s.prog[j].imm_f;
+  }
+  for (size_t j = 0; j < s.keys.size(); ++j) hp.klo[j] = s.keys[j].lo;
+}
+
+// ---------------------------------------------------------------------------
+// AOT helpers: deterministic reduction of partial rows, finalize, min/max
+// ---------------------------------------------------------------------------
+struct AggMap {
+  int naggs;
+  int nf;
+  int ni;
+  int pad;
+  int kind[32];
+  int acc[32];
+};
+
+// One warp per output item; lanes stride over the partial rows in a fixed
+// order and combine with a fixed shuffle tree -> bitwise deterministic.
+__global__ void agg_reduce_kernel(const u64* __restrict__ part, int rows, int slots, AggMap m,
+                                  i64* __restrict__ out_counts, u64* __restrict__ out_sums) {
+  const int lane = threadIdx.x & 31;
+  const i64 items = (i64)slots * (1 + m.naggs);
+  const i64 cells = (i64)slots * (1 + m.nf + m.ni);
+  for (i64 it = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
+       it += ((i64)gridDim.x * blockDim.x) >> 5) {
+    i64 cell;
+    bool is_f = false;
+    if (it < slots) {
+      cell = it;
+    } else {
+      const int a = (int)((it - slots) / slots);
+      const i64 g = (it - slots) % slots;
+      if (m.kind[a] == TDP_AGG_COUNT) {
+        cell = g;
+      } else if (m.kind[a] == TDP_AGG_SUM_F64) {
+        cell = (i64)slots * (1 + m.acc[a]) + g;
+        is_f = true;
+      } else {
+        cell = (i64)slots * (1 + m.nf + m.acc[a]) + g;
+      }
+    }
+    u64 bits;
+    if (is_f) {
+      double v = 0.0;
+      for (int r = lane; r < rows; r += 32) v += __longlong_as_double((i64)part[(i64)r * cells + cell]);
+      v = warp_sum(v);
+      bits = (u64)__double_as_longlong(v);
+    } else {
+      u64 v = 0;
+      for (int r = lane; r < rows; r += 32) v += part[(i64)r * cells + cell];
+      bits = warp_sum(v);
+    }
+    if (lane == 0) {
+      if (it < slots) out_counts[it] = (i64)bits;
+      else out_sums[it - slots] = bits;
+    }
+  }
+}
+
+struct KeyDigits {
+  int nkeys;
+  int pad;
+  i64 lo[kMaxKeys];
+  i64 span[kMaxKeys];
+  i64 stride[kMaxKeys];
+};
+
+// Single CTA: compact occupied slots in ascending slot order.
+__global__ void __launch_bounds__(1024)
+    finalize_kernel(const i64* __restrict__ counts, const u64* __restrict__ sums, i64 slots,
+                    KeyDigits kd, AggMap m, unsigned long long avg_mask,
+                    i64* __restrict__ out_keys, i64* __restrict__ out_counts,
+                    u64* __restrict__ out_aggs, i64* __restrict__ out_groups) {
+  __shared__ int warp_tot[32];
+  __shared__ i64 running;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 base = 0; base < slots; base += blockDim.x) {
+    const i64 s = base + threadIdx.x;
+    const i64 c = s < slots ? counts[s] : 0;
+    const int occ = c > 0 ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, occ);
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) before += warp_tot[w];
+      total += warp_tot[w];
+    }
+    const i64 pos = running + before + __popc(bal & lanemask_lt());
+    if (occ) {
+      for (int j = 0; j < kd.nkeys; ++j) {
+        const i64 digit = (s / kd.stride[j]) % kd.span[j];
+        out_keys[(i64)j * slots + pos] = kd.lo[j] + digit;
+      }
+      out_counts[pos] = c;
+      for (int a = 0; a < m.naggs; ++a) {
+        const u64 raw = sums[(i64)a * slots + s];
+        u64 v = raw;
+        if ((avg_mask >> a) & 1ull) {
+          double sum;
+          if (m.kind[a] == TDP_AGG_SUM_F64) sum = __longlong_as_double((i64)raw);
+          else sum = (double)(i64)raw;
+          v = (u64)__double_as_longlong(sum / (double)c);
+        }
+        out_aggs[(i64)a * slots + pos] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out_groups = running;
+}
+
+struct KeyCols {
+  const void* p[kMaxKeys];
+  int dt[kMaxKeys];
+};
+
+__global__ void scan_minmax_kernel(PredSet ps, i64 n, KeyCols kc, int nkeys,
+                                   i64* __restrict__ out) {
+  i64 mn[kMaxKeys], mx[kMaxKeys];
+#pragma unroll
+  for (int j = 0; j < kMaxKeys; ++j) {
+    mn[j] = LLONG_MAX;
+    mx[j] = LLONG_MIN;
+  }
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    if (!eval_all(ps, i)) continue;
+#pragma unroll
+    for (int j = 0; j < kMaxKeys; ++j) {
+      if (j < nkeys) {
+        const i64 v = load_as_i64(kc.p[j], kc.dt[j], i);
+        mn[j] = v < mn[j] ? v : mn[j];
+        mx[j] = v > mx[j] ? v : mx[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxKeys; ++j) {
+    if (j < nkeys) {
+      i64 a = mn[j], b = mx[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const i64 ta = __shfl_xor_sync(0xffffffffu, a, o);
+        const i64 tb = __shfl_xor_sync(0xffffffffu, b, o);
+        a = ta < a ? ta : a;
+        b = tb > b ? tb : b;
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(reinterpret_cast<long long*>(out) + 2 * j, a);
+        atomicMax(reinterpret_cast<long long*>(out) + 2 * j + 1, b);
+      }
+    }
+  }
+}
+
+__global__ void set_i64_kernel(i64* out, i64 v) { *out = v; }
+
+__global__ void init_minmax_kernel(i64* out, int nkeys) {
+  const int j = threadIdx.x;
+  if (j < nkeys) {
+    out[2 * j] = LLONG_MAX;
+    out[2 * j + 1] = LLONG_MIN;
+  }
+}
+
+int build_spec(Spec& s, const tdp_column* cols, int32_t ncols, int64_t n,
+               const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog, int32_t nprog,
+               const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs, int32_t naggs,
+               const int32_t* outs, int32_t nouts) {
+  TDP_REQUIRE(n >= 0, "negative row count");
+  TDP_REQUIRE(npreds >= 0 && nprog >= 0 && nkeys >= 0 && naggs >= 0 && nouts >= 0,
+              "negative descriptor count");
+  TDP_REQUIRE(naggs <= 32, "at most 32 aggregates");
+  s.preds.assign(preds, preds + npreds);
+  s.prog.assign(prog, prog + nprog);
+  s.keys.assign(keys, keys + nkeys);
+  s.aggs.assign(aggs, aggs + naggs);
+  s.outs.assign(outs, outs + nouts);
+  return validate_and_derive(s, cols, ncols, n);
+}
+
+AggMap make_map(const Spec& s) {
+  AggMap m;
+  std::memset(&m, 0, sizeof(m));
+  m.naggs = (int)s.aggs.size();
+  m.nf = (int)s.fvals.size();
+  m.ni = (int)s.ivals.size();
+  for (int a = 0; a < m.naggs; ++a) {
+    m.kind[a] = s.aggs[a].kind;
+    m.acc[a] = s.agg_acc[a];
+  }
+  return m;
+}
+
+i64 cells_of(const Spec& s) { return s.slots * (i64)(1 + s.fvals.size() + s.ivals.size()); }
+
+}  // namespace
+
+}  // namespace tdp
+
+using namespace tdp;
+
+extern "C" {
+
+int tdp_pipeline_codegen(const tdp_column* cols, int32_t ncols, int64_t n,
+                         const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                         int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                         int32_t naggs, const int32_t* outs, int32_t nouts, int32_t compile,
+                         char* out_src, size_t cap) {
+  Spec s;
+  int rc = build_spec(s, cols, ncols, n, preds, npreds, prog, nprog, keys, nkeys, aggs, naggs,
+                      outs, nouts);
+  if (rc) return rc;
+  const std::string src = generate(s);
+  if (out_src && cap) {
+    const size_t m = src.size() < cap - 1 ? src.size() : cap - 1;
+    std::memcpy(out_src, src.data(), m);
+    out_src[m] = '\0';
+  }
+  if (compile) {
+    std::vector<char> cubin;
+    rc = nvrtc_compile(src, &cubin);
+    if (rc) return rc;
+  }
+  return (int)(src.size() > 0x7fffffff ? 0x7fffffff : src.size());
+}
+
+size_t tdp_scan_aggregate_workspace(int64_t n, int64_t slots, int32_t naggs) {
+  (void)n;
+  const i64 cells = (slots > 0 ? slots : 1) * (i64)(1 + (naggs > 0 ? naggs : 0));
+  const i64 reg_rows = (i64)sm_count() * 32;
+  const i64 reg = reg_rows * (cells < kMaxRegCells ? cells : kMaxRegCells);
+  return (size_t)((reg > cells ? reg : cells) * 8 + 256);
+}
+
+int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
+                       const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                       int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                       int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
+                       size_t ws_bytes, void* stream) {
+  Spec s;
+  int rc = build_spec(s, cols, ncols, n, preds, npreds, prog, nprog, keys, nkeys, aggs, naggs,
+                      nullptr, 0);
+  if (rc) return rc;
+  TDP_REQUIRE(out_counts != nullptr, "null count output");
+  TDP_REQUIRE(naggs == 0 || out_sums != nullptr, "null sums output");
+  cudaStream_t st = as_stream(stream);
+  const i64 cells = cells_of(s);
+  std::shared_ptr<Kernel> k;
+  rc = compile(generate(s), &k);
+  if (rc) return rc;
+  Driver* d = nullptr;
+  rc = get_driver(&d);
+  if (rc) return rc;
+  const i64 tile = (i64)kThreads * kUnroll;
+  i64 grid = ceil_div(n > 0 ? n : 1, tile);
+  const i64 cap = (i64)sm_count() * (s.regacc ? k->agg_occ : 2 * k->agg_occ);
+  if (grid > cap) grid = cap;
+  if (s.regacc && grid > (i64)sm_count() * 32) grid = (i64)sm_count() * 32;
+  const i64 rows = s.regacc ? grid : 1;
+  TDP_REQUIRE(ws != nullptr && ws_bytes >= (size_t)(rows * cells * 8),
+              "scan_aggregate workspace too small (%zu < %lld)", ws_bytes,
+              (long long)(rows * cells * 8));
+  if (!s.regacc) TDP_CUDA_TRY(cudaMemsetAsync(ws, 0, (size_t)cells * 8, st));
+  if (n > 0 || s.regacc) {
+    HostParams hp;
+    fill_params(hp, s, cols, ncols, n);
+    hp.acc = ws;
+    void* args[] = {&hp};
+    rc = cu_check(d,
+                  d->launch(k->agg, (unsigned)grid, 1, 1, kThreads, 1, 1, 0, (CUstream)st, args,
+                            nullptr),
+                  "cuLaunchKernel(tdp_scan_agg)");
+    if (rc) return rc;
+    count_launch();
+  }
+  AggMap m = make_map(s);
+  const i64 items = s.slots * (1 + naggs);
+  agg_reduce_kernel<<<(unsigned)ceil_div(items * 32, 256), 256, 0, st>>>(
+      reinterpret_cast<const u64*>(ws), (int)rows, (int)s.slots, m, out_counts,
+      reinterpret_cast<u64*>(out_sums));
+  TDP_LAUNCH_CHECK("agg_reduce_kernel");
+  return TDP_OK;
+}
+
+int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,
+                     const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                     int32_t nprog, const int32_t* outs, int32_t nouts, void* const* out_ptrs,
+                     int64_t* out_count, void* ws, size_t ws_bytes, void* stream) {
+  Spec s;
+  int rc = build_spec(s, cols, ncols, n, preds, npreds, prog, nprog, nullptr, 0, nullptr, 0,
+                      outs, nouts);
+  if (rc) return rc;
+  TDP_REQUIRE(out_count != nullptr, "null count output");
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(i64), st));
+    return TDP_OK;
+  }
+  std::shared_ptr<Kernel> k;
+  rc = compile(generate(s), &k);
+  if (rc) return rc;
+  Driver* d = nullptr;
+  rc = get_driver(&d);
+  if (rc) return rc;
+  HostParams hp;
+  fill_params(hp, s, cols, ncols, n);
+  for (int o = 0; o < nouts; ++o) hp.out[o] = out_ptrs[o];
+  unsigned grid;
+  if (npreds > 0) {
+    TDP_REQUIRE(ws_bytes >= tdp_filter_workspace(n), "project workspace too small");
+    PredSet ps;
+    rc = make_predset(cols, ncols, preds, npreds, n, &ps);
+    if (rc) return rc;
+    const i64 tiles = ceil_div(n, kFilterTile);
+    unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+    unsigned* bits = reinterpret_cast<unsigned*>(p);
+    p += ((size_t)tiles * kFilterWords * sizeof(unsigned) + 255) & ~(size_t)255;
+    i64* counts = reinterpret_cast<i64*>(p);
+    i64* offsets = counts + tiles;
+    void* scan_ws = offsets + tiles;
+    const size_t used = (size_t)((unsigned char*)scan_ws - (unsigned char*)ws);
+    rc = filter_bits(ps, n, bits, counts, st);
+    if (rc) return rc;
+    rc = exclusive_scan_i64(counts, offsets, tiles, out_count, scan_ws, ws_bytes - used, st);
+    if (rc) return rc;
+    hp.bits = bits;
+    hp.tile_off = offsets;
+    grid = (unsigned)tiles;
+  } else {
+    set_i64_kernel<<<1, 1, 0, st>>>(out_count, n);
+    TDP_LAUNCH_CHECK("set_i64_kernel");
+    grid = (unsigned)stream_grid(n, 256 * 4, 8);
+  }
+  void* args[] = {&hp};
+  rc = cu_check(d, d->launch(k->proj, grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr),
+                "cuLaunchKernel(tdp_scan_project)");
+  if (rc) return rc;
+  count_launch();
+  return TDP_OK;
+}
+
+int tdp_groupby_finalize(const int64_t* counts, const void* sums, int64_t slots,
+                         const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs, int32_t naggs,
+                         uint64_t avg_mask, int64_t* out_keys, int64_t* out_counts,
+                         void* out_aggs, int64_t* out_groups, void* stream) {
+  TDP_REQUIRE(slots >= 1, "slots must be >= 1");
+  TDP_REQUIRE(nkeys >= 0 && nkeys <= kMaxKeys, "bad key count");
+  TDP_REQUIRE(naggs >= 0 && naggs <= 32, "bad aggregate count");
+  KeyDigits kd;
+  std::memset(&kd, 0, sizeof(kd));
+  kd.nkeys = nkeys;
+  i64 prod = 1;
+  for (int j = nkeys - 1; j >= 0; --j) {
+    TDP_REQUIRE(keys[j].span >= 1, "key %d: bad span", j);
+    kd.lo[j] = keys[j].lo;
+    kd.span[j] = keys[j].span;
+    kd.stride[j] = prod;
+    prod *= keys[j].span;
+  }
+  TDP_REQUIRE(prod == slots, "slots %lld != product of key spans %lld", (long long)slots,
+              (long long)prod);
+  AggMap m;
+  std::memset(&m, 0, sizeof(m));
+  m.naggs = naggs;
+  for (int a = 0; a < naggs; ++a) m.kind[a] = aggs[a].kind;
+  finalize_kernel<<<1, 1024, 0, as_stream(stream)>>>(
+      counts, reinterpret_cast<const u64*>(sums), slots, kd, m,
+      (unsigned long long)avg_mask, out_keys, out_counts, reinterpret_cast<u64*>(out_aggs),
+      out_groups);
+  TDP_LAUNCH_CHECK("finalize_kernel");
+  return TDP_OK;
+}
+
+int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
+                    const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
+                    int32_t nkeys, int64_t* out_minmax, void* stream) {
+  TDP_REQUIRE(nkeys >= 1 && nkeys <= kMaxKeys, "bad key count");
+  PredSet ps;
+  int rc = make_predset(cols, ncols, preds, npreds, n, &ps);
+  if (rc) return rc;
+  KeyCols kc;
+  std::memset(&kc, 0, sizeof(kc));
+  for (int j = 0; j < nkeys; ++j) {
+    TDP_REQUIRE(key_cols[j] >= 0 && key_cols[j] < ncols, "key %d: bad column", j);
+    const tdp_column& c = cols[key_cols[j]];
+    TDP_REQUIRE(c.dtype == TDP_I64 || c.dtype == TDP_I32 || c.dtype == TDP_BOOL,
+                "key %d: integer column required", j);
+    TDP_REQUIRE(c.rows >= n, "key %d: short column", j);
+    kc.p[j] = c.data;
+    kc.dt[j] = c.dtype;
+  }
+  cudaStream_t st = as_stream(stream);
+  init_minmax_kernel<<<1, 32, 0, st>>>(out_minmax, nkeys);
+  TDP_LAUNCH_CHECK("init_minmax_kernel");
+  if (n == 0) return TDP_OK;
+  scan_minmax_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(ps, n, kc, nkeys, out_minmax);
+  TDP_LAUNCH_CHECK("scan_minmax_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,564 @@
+// Stable LSD radix sort of 64-bit keys with int64 payload, and the sort-based
+// relational primitives built on it.
+//
+// Reference primitives replaced (tq = /root/reference/pkg/src/tensorquery):
+//   np.argsort(+-key, kind="stable")   stable_order, tq/kernels.py:256-264
+//   np.unique(key, return_inverse)     groupby_exact, tq/kernels.py:128, :136
+//   np.bincount / np.add.at            groupby_exact, tq/kernels.py:138-153
+//
+// Keys are mapped to unsigned 64-bit images whose unsigned order is numpy's
+// order: int64 -> flip the sign bit; float -> IEEE total-order flip with
+// -0.0 canonicalised to +0.0 (numpy treats them as equal, so the stable sort
+// keeps input order) and every NaN mapped to the all-ones image (NaN sorts last
+// in both directions, ties among NaNs keep input order).  DESC sorts the
+// negated key exactly like the reference (`-arr`, INT64_MIN wraps).
+//
+// One pass per 8-bit digit: per-tile digit histograms -> device-wide scan of
+// the digit-major [256 x tiles] count matrix -> stable scatter, where each
+// warp ranks its keys in input order with __match_any_sync and the CTA adds
+// per-warp prefixes.  Digits that are constant across all keys (found with a
+// single histogram pre-pass over all 8 digits) are skipped, so int64 keys of
+// small range sort in 3-4 passes.
+#include <vector>
+
+#include "tdp_common.cuh"
+
+namespace tdp {
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;  // per thread
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kWarpKeys = 32 * kSortItems;
+constexpr int kWarps = kSortThreads / 32;
+
+__device__ __forceinline__ u64 image_i64(i64 x, bool desc) {
+  const u64 v = desc ? (u64)0 - (u64)x : (u64)x;
+  return v ^ 0x8000000000000000ull;
+}
+
+__device__ __forceinline__ u64 image_f64(double x, bool desc) {
+  if (x != x) return ~0ull;
+  if (desc) x = -x;
+  if (x == 0.0) x = 0.0;  // -0.0 -> +0.0
+  const u64 b = (u64)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ u64 image_f32(float x, bool desc) {
+  if (x != x) return 0xffffffffull;
+  if (desc) x = -x;
+  if (x == 0.0f) x = 0.0f;
+  const unsigned b = __float_as_uint(x);
+  return (u64)((b & 0x80000000u) ? ~b : (b | 0x80000000u));
+}
+
+__global__ void make_keys_kernel(const void* __restrict__ key, int dtype, int desc, i64 n,
+                                 u64* __restrict__ out, i64* __restrict__ idx) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    u64 k;
+    switch (dtype) {
+      case TDP_I64:
+        k = image_i64(reinterpret_cast<const i64*>(key)[i], desc);
+        break;
+      case TDP_I32:
+        k = image_i64((i64)reinterpret_cast<const int*>(key)[i], desc);
+        break;
+      case TDP_F64:
+        k = image_f64(reinterpret_cast<const double*>(key)[i], desc);
+        break;
+      default:
+        k = image_f32(reinterpret_cast<const float*>(key)[i], desc);
+        break;
+    }
+    out[i] = k;
+    idx[i] = i;
+  }
+}
+
+// Histograms of all 8 digits at once -> hist[8][256] (global, zeroed).
+__global__ void all_digit_hist_kernel(const u64* __restrict__ keys, i64 n,
+                                      unsigned long long* __restrict__ hist) {
+  __shared__ unsigned h[8][256];
+  for (int t = threadIdx.x; t < 8 * 256; t += blockDim.x) (&h[0][0])[t] = 0;
+  __syncthreads();
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 k = keys[i];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 8 * 256; t += blockDim.x) {
+    const unsigned v = (&h[0][0])[t];
+    if (v) atomicAdd(hist + t, (unsigned long long)v);
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+    tile_hist_kernel(const u64* __restrict__ keys, i64 n, int shift, i64 ntiles,
+                     i64* __restrict__ counts) {
+  __shared__ unsigned h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const i64 base = (i64)blockIdx.x * kSortTile;
+#pragma unroll 4
+  for (int k = 0; k < kSortItems; ++k) {
+    const i64 i = base + (i64)k * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  counts[(i64)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+    scatter_kernel(const u64* __restrict__ keys_in, const i64* __restrict__ idx_in, i64 n,
+                   int shift, i64 ntiles, const i64* __restrict__ offsets,
+                   u64* __restrict__ keys_out, i64* __restrict__ idx_out) {
+  __shared__ unsigned wcount[kWarps][256];
+  __shared__ i64 goff[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = lane; d < 256; d += 32) wcount[warp][d] = 0;
+  goff[threadIdx.x] = offsets[(i64)threadIdx.x * ntiles + blockIdx.x];
+  __syncwarp();
+  const i64 wbase = (i64)blockIdx.x * kSortTile + (i64)warp * kWarpKeys;
+  const unsigned lt = lanemask_lt();
+  u64 k[kSortItems];
+  i64 p[kSortItems];
+  unsigned rank[kSortItems];
+  int dig[kSortItems];
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const i64 i = wbase + it * 32 + lane;
+    const bool valid = i < n;
+    k[it] = valid ? keys_in[i] : 0;
+    p[it] = valid ? idx_in[i] : 0;
+    dig[it] = valid ? (int)((k[it] >> shift) & 0xff) : 256;
+  }
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const int d = dig[it];
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    unsigned before = 0;
+    if (d < 256) before = wcount[warp][d];
+    rank[it] = before + __popc(peers & lt);
+    __syncwarp();
+    if (d < 256 && (peers & lt) == 0) wcount[warp][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive prefix over warps for each digit (thread t owns digit t)
+  {
+    unsigned run = 0;
+    const int d = threadIdx.x;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const unsigned c = wcount[w][d];
+      wcount[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const int d = dig[it];
+    if (d < 256) {
+      const i64 pos = goff[d] + wcount[warp][d] + rank[it];
+      keys_out[pos] = k[it];
+      idx_out[pos] = p[it];
+    }
+  }
+}
+
+struct SortBuffers {
+  u64* k0;
+  u64* k1;
+  i64* i0;
+  i64* i1;
+  i64* counts;
+  i64* offsets;
+  unsigned long long* hist;
+  void* scan_ws;
+  size_t scan_bytes;
+};
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+size_t sort_ws_bytes(i64 n) {
+  const i64 ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
+  return 4 * align256((size_t)n * 8) + 2 * align256((size_t)ntiles * 256 * 8) +
+         align256(8 * 256 * 8) + exclusive_scan_workspace(ntiles * 256) + 1024;
+}
+
+SortBuffers carve(void* ws, i64 n) {
+  const i64 ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  SortBuffers b;
+  b.k0 = (u64*)p;
+  p += align256((size_t)n * 8);
+  b.k1 = (u64*)p;
+  p += align256((size_t)n * 8);
+  b.i0 = (i64*)p;
+  p += align256((size_t)n * 8);
+  b.i1 = (i64*)p;
+  p += align256((size_t)n * 8);
+  b.counts = (i64*)p;
+  p += align256((size_t)ntiles * 256 * 8);
+  b.offsets = (i64*)p;
+  p += align256((size_t)ntiles * 256 * 8);
+  b.hist = (unsigned long long*)p;
+  p += align256(8 * 256 * 8);
+  b.scan_ws = p;
+  b.scan_bytes = exclusive_scan_workspace(ntiles * 256) + 512;
+  return b;
+}
+
+// Sorts the images in b.k0 / payload b.i0.  On return *keys/*idx point at the
+// buffer holding the sorted result.
+int radix_sort(SortBuffers& b, i64 n, cudaStream_t st, u64** keys, i64** idx) {
+  *keys = b.k0;
+  *idx = b.i0;
+  if (n <= 1) return TDP_OK;
+  const i64 ntiles = ceil_div(n, kSortTile);
+  TDP_CUDA_TRY(cudaMemsetAsync(b.hist, 0, 8 * 256 * 8, st));
+  all_digit_hist_kernel<<<stream_grid(n, 256 * 16, 4), 256, 0, st>>>(b.k0, n, b.hist);
+  TDP_LAUNCH_CHECK("all_digit_hist_kernel");
+  std::vector<unsigned long long> h(8 * 256);
+  TDP_CUDA_TRY(cudaMemcpyAsync(h.data(), b.hist, h.size() * 8, cudaMemcpyDeviceToHost, st));
+  TDP_CUDA_TRY(cudaStreamSynchronize(st));
+  u64* kin = b.k0;
+  u64* kout = b.k1;
+  i64* iin = b.i0;
+  i64* iout = b.i1;
+  for (int d = 0; d < 8; ++d) {
+    bool trivial = false;
+    for (int v = 0; v < 256; ++v)
+      if (h[d * 256 + v] == (unsigned long long)n) trivial = true;
+    if (trivial) continue;
+    const int shift = 8 * d;
+    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, ntiles, b.counts);
+    TDP_LAUNCH_CHECK("tile_hist_kernel");
+    int rc = exclusive_scan_i64(b.counts, b.offsets, ntiles * 256, nullptr, b.scan_ws,
+                                b.scan_bytes, st);
+    if (rc) return rc;
+    scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, iin, n, shift, ntiles,
+                                                              b.offsets, kout, iout);
+    TDP_LAUNCH_CHECK("scatter_kernel");
+    u64* tk = kin;
+    kin = kout;
+    kout = tk;
+    i64* ti = iin;
+    iin = iout;
+    iout = ti;
+  }
+  *keys = kin;
+  *idx = iin;
+  return TDP_OK;
+}
+
+// ---- unique / inverse ----------------------------------------------------
+__global__ void boundary_flags_kernel(const u64* __restrict__ sk, i64 n, i64* __restrict__ flags) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || sk[i] != sk[i - 1]) ? 1 : 0;
+}
+
+// rank of sorted position i = (#boundaries at or before i) - 1 = excl[i] + flag[i] - 1
+__global__ void unique_scatter_kernel(const u64* __restrict__ sk, const i64* __restrict__ order,
+                                      const i64* __restrict__ flags, const i64* __restrict__ excl,
+                                      i64 n, i64* __restrict__ uniques, i64* __restrict__ inverse) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const i64 r = excl[i] + flags[i] - 1;
+    inverse[order[i]] = r;
+    if (flags[i]) uniques[r] = (i64)(sk[i] ^ 0x8000000000000000ull);
+  }
+}
+
+// ---- grouped aggregation over dense codes ----------------------------------
+struct ValSet {
+  int naggs;
+  int pad;
+  const void* p[32];
+  int dt[32];
+  int kind[32];
+};
+
+__global__ void groupby_codes_kernel(const i64* __restrict__ codes, i64 n, i64 slots, ValSet vs,
+                                     unsigned long long* __restrict__ counts,
+                                     unsigned long long* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const i64 i = base + threadIdx.x;
+    const bool valid = i < n;
+    const i64 c = valid ? codes[i] : -1;
+    const i64 c0 = __shfl_sync(0xffffffffu, c, 0);
+    const bool uniform = __all_sync(0xffffffffu, c == c0) && c0 >= 0;
+    if (uniform) {
+      // whole warp in one group (typical after sorting / small key spaces)
+      const unsigned long long cnt = warp_sum(1ull);
+      if (lane == 0) atomicAdd(counts + c0, cnt);
+      for (int a = 0; a < vs.naggs; ++a) {
+        if (vs.kind[a] == TDP_AGG_COUNT) continue;
+        if (vs.kind[a] == TDP_AGG_SUM_F64) {
+          const double v = warp_sum(load_as_f64(vs.p[a], vs.dt[a], i));
+          if (lane == 0) atomicAdd(reinterpret_cast<double*>(sums) + (i64)a * slots + c0, v);
+        } else {
+          const unsigned long long v = warp_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i));
+          if (lane == 0) atomicAdd(sums + (i64)a * slots + c0, v);
+        }
+      }
+    } else if (valid) {
+      atomicAdd(counts + c, 1ull);
+      for (int a = 0; a < vs.naggs; ++a) {
+        if (vs.kind[a] == TDP_AGG_COUNT) continue;
+        if (vs.kind[a] == TDP_AGG_SUM_F64)
+          atomicAdd(reinterpret_cast<double*>(sums) + (i64)a * slots + c,
+                    load_as_f64(vs.p[a], vs.dt[a], i));
+        else
+          atomicAdd(sums + (i64)a * slots + c,
+                    (unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i));
+      }
+    }
+  }
+}
+
+__global__ void copy_counts_kernel(const unsigned long long* __restrict__ counts, i64 slots,
+                                   ValSet vs, unsigned long long* __restrict__ sums) {
+  for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < slots * vs.naggs;
+       t += (i64)gridDim.x * blockDim.x) {
+    const int a = (int)(t / slots);
+    if (vs.kind[a] == TDP_AGG_COUNT) sums[t] = counts[t - (i64)a * slots];
+  }
+}
+
+}  // namespace
+
+}  // namespace tdp
+
+using namespace tdp;
+
+extern "C" {
+
+size_t tdp_sort_workspace(int64_t n) { return sort_ws_bytes(n); }
+
+int tdp_sort_order(const tdp_column* key, int32_t descending, int64_t n, int64_t* out_order,
+                   void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(key != nullptr && n >= 0, "bad sort arguments");
+  TDP_REQUIRE(key->width == 1, "sort keys must be scalar columns");
+  TDP_REQUIRE(key->dtype == TDP_I64 || key->dtype == TDP_F64 || key->dtype == TDP_F32 ||
+                  key->dtype == TDP_I32,
+              "sort key dtype %d not supported", key->dtype);
+  TDP_REQUIRE(key->rows >= n, "short key column");
+  if (n == 0) return TDP_OK;
+  TDP_REQUIRE(ws_bytes >= sort_ws_bytes(n), "sort workspace too small");
+  cudaStream_t st = as_stream(stream);
+  SortBuffers b = carve(ws, n);
+  make_keys_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(key->data, key->dtype,
+                                                                descending ? 1 : 0, n, b.k0, b.i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  u64* sk;
+  i64* order;
+  int rc = radix_sort(b, n, st, &sk, &order);
+  if (rc) return rc;
+  TDP_CUDA_TRY(cudaMemcpyAsync(out_order, order, (size_t)n * 8, cudaMemcpyDeviceToDevice, st));
+  return TDP_OK;
+}
+
+int tdp_unique_inverse(const int64_t* key, int64_t n, int64_t* out_uniques, int64_t* out_inverse,
+                       int64_t* out_nunique, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n >= 0, "negative length");
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_nunique, 0, 8, st));
+    return TDP_OK;
+  }
+  TDP_REQUIRE(ws_bytes >= sort_ws_bytes(n) + 2 * align256((size_t)n * 8),
+              "unique workspace too small");
+  SortBuffers b = carve(ws, n);
+  unsigned char* extra = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n);
+  i64* flags = reinterpret_cast<i64*>(extra);
+  i64* excl = reinterpret_cast<i64*>(extra + align256((size_t)n * 8));
+  make_keys_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(key, TDP_I64, 0, n, b.k0, b.i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  u64* sk;
+  i64* order;
+  int rc = radix_sort(b, n, st, &sk, &order);
+  if (rc) return rc;
+  boundary_flags_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(sk, n, flags);
+  TDP_LAUNCH_CHECK("boundary_flags_kernel");
+  rc = exclusive_scan_i64(flags, excl, n, out_nunique, b.scan_ws, b.scan_bytes, st);
+  if (rc) return rc;
+  unique_scatter_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(sk, order, flags, excl, n,
+                                                                     out_uniques, out_inverse);
+  TDP_LAUNCH_CHECK("unique_scatter_kernel");
+  return TDP_OK;
+}
+
+int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_column* vals,
+                      const int32_t* agg_kinds, int32_t naggs, int64_t* out_counts,
+                      void* out_sums, void* stream) {
+  TDP_REQUIRE(n >= 0 && slots >= 1, "bad group-by shape");
+  TDP_REQUIRE(naggs >= 0 && naggs <= 32, "at most 32 aggregates");
+  ValSet vs;
+  vs.naggs = naggs;
+  vs.pad = 0;
+  for (int a = 0; a < naggs; ++a) {
+    vs.kind[a] = agg_kinds[a];
+    TDP_REQUIRE(agg_kinds[a] >= TDP_AGG_COUNT && agg_kinds[a] <= TDP_AGG_SUM_I64,
+                "agg %d: bad kind", a);
+    if (agg_kinds[a] == TDP_AGG_COUNT) {
+      vs.p[a] = nullptr;
+      vs.dt[a] = TDP_I64;
+      continue;
+    }
+    TDP_REQUIRE(vals != nullptr && vals[a].rows >= n && vals[a].width == 1,
+                "agg %d: value column must be scalar with >= n rows", a);
+    vs.p[a] = vals[a].data;
+    vs.dt[a] = vals[a].dtype;
+  }
+  cudaStream_t st = as_stream(stream);
+  TDP_CUDA_TRY(cudaMemsetAsync(out_counts, 0, (size_t)slots * 8, st));
+  if (naggs) TDP_CUDA_TRY(cudaMemsetAsync(out_sums, 0, (size_t)slots * naggs * 8, st));
+  if (n > 0) {
+    groupby_codes_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(
+        codes, n, slots, vs, reinterpret_cast<unsigned long long*>(out_counts),
+        reinterpret_cast<unsigned long long*>(out_sums));
+    TDP_LAUNCH_CHECK("groupby_codes_kernel");
+  }
+  if (naggs) {
+    copy_counts_kernel<<<stream_grid(slots * naggs, 256, 4), 256, 0, st>>>(
+        reinterpret_cast<unsigned long long*>(out_counts), slots, vs,
+        reinterpret_cast<unsigned long long*>(out_sums));
+    TDP_LAUNCH_CHECK("copy_counts_kernel");
+  }
+  return TDP_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// equi-join: sort build keys, binary-search each probe key
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+__device__ __forceinline__ i64 lower_bound_u64(const u64* a, i64 n, u64 v) {
+  i64 lo = 0, hi = n;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void probe_count_kernel(const u64* __restrict__ sk, i64 nb,
+                                   const i64* __restrict__ probe, i64 np, i64* __restrict__ lb,
+                                   i64* __restrict__ cnt) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 v = (u64)probe[i] ^ 0x8000000000000000ull;
+    const i64 l = lower_bound_u64(sk, nb, v);
+    i64 h = l;
+    if (l < nb && sk[l] == v) h = lower_bound_u64(sk, nb, v + 1);  // v + 1 cannot wrap: v == ~0 only for INT64_MAX
+    if (v == ~0ull) h = nb;
+    lb[i] = l;
+    cnt[i] = h - l;
+  }
+}
+
+__global__ void probe_emit_kernel(const i64* __restrict__ order, const i64* __restrict__ lb,
+                                  const i64* __restrict__ cnt, const i64* __restrict__ off,
+                                  i64 np, i64* __restrict__ out_probe,
+                                  i64* __restrict__ out_build) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+       i += (i64)gridDim.x * blockDim.x) {
+    const i64 c = cnt[i];
+    const i64 o = off[i], l = lb[i];
+    for (i64 j = 0; j < c; ++j) {
+      out_probe[o + j] = i;
+      out_build[o + j] = order[l + j];
+    }
+  }
+}
+
+struct JoinLayout {
+  SortBuffers sb;
+  i64* lb;
+  i64* cnt;
+  i64* off;
+  u64** sorted_keys_slot;
+  unsigned char* state;  // [0]: 0/1 which sort buffer holds the result
+};
+
+size_t join_ws_bytes(i64 nb, i64 np) {
+  return sort_ws_bytes(nb) + 3 * align256((size_t)(np > 0 ? np : 1) * 8) +
+         exclusive_scan_workspace(np) + 1024;
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_join_workspace(int64_t n_build, int64_t n_probe) { return join_ws_bytes(n_build, n_probe); }
+
+int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                     int64_t n_probe, int64_t* out_count, void* ws, size_t ws_bytes,
+                     void* stream) {
+  TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
+  TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
+  cudaStream_t st = as_stream(stream);
+  SortBuffers b = carve(ws, n_build);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n_build);
+  i64* lb = (i64*)p;
+  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
+  i64* cnt = (i64*)p;
+  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
+  i64* off = (i64*)p;
+  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
+  if (n_build == 0 || n_probe == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
+    return TDP_OK;
+  }
+  make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
+                                                                      n_build, b.k0, b.i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  u64* sk;
+  i64* order;
+  int rc = radix_sort(b, n_build, st, &sk, &order);
+  if (rc) return rc;
+  if (sk != b.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
+    TDP_CUDA_TRY(cudaMemcpyAsync(b.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+    TDP_CUDA_TRY(cudaMemcpyAsync(b.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  probe_count_kernel<<<stream_grid(n_probe, 256 * 4, 8), 256, 0, st>>>(b.k0, n_build, probe_keys,
+                                                                        n_probe, lb, cnt);
+  TDP_LAUNCH_CHECK("probe_count_kernel");
+  return exclusive_scan_i64(cnt, off, n_probe, out_count, p, exclusive_scan_workspace(n_probe) + 512,
+                            st);
+}
+
+int tdp_join_emit(int64_t n_build, int64_t n_probe, int64_t* out_probe_idx,
+                  int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
+  cudaStream_t st = as_stream(stream);
+  SortBuffers b = carve(ws, n_build);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n_build);
+  i64* lb = (i64*)p;
+  p += align256((size_t)n_probe * 8);
+  i64* cnt = (i64*)p;
+  p += align256((size_t)n_probe * 8);
+  i64* off = (i64*)p;
+  probe_emit_kernel<<<stream_grid(n_probe, 256 * 4, 8), 256, 0, st>>>(b.i0, lb, cnt, off, n_probe,
+                                                                       out_probe_idx, out_build_idx);
+  TDP_LAUNCH_CHECK("probe_emit_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"

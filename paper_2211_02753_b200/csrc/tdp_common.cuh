@@ -1,0 +1,225 @@
+// Shared infrastructure of libtdp_kernels: error reporting, dtype access,
+// predicate evaluation, grid sizing.  Device code targets sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/tdp_kernels.h"
+
+namespace tdp {
+
+typedef int64_t i64;
+typedef uint64_t u64;
+
+// ---------------------------------------------------------------------------
+// host-side error plumbing (thread-local message, returned by tdp_last_error)
+// ---------------------------------------------------------------------------
+int set_error(int code, const char* fmt, ...);
+const char* last_error();
+
+#define TDP_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      return ::tdp::set_error(TDP_ECUDA, "%s failed: %s (%s:%d)", #expr,                \
+                              cudaGetErrorString(_e), __FILE__, __LINE__);              \
+  } while (0)
+
+// Counts every kernel this library launches (tdp_launch_count) so benchmarks
+// can report how many of their launches were ours.
+void count_launch();
+
+#define TDP_LAUNCH_CHECK(name)                                                          \
+  do {                                                                                  \
+    cudaError_t _e = cudaGetLastError();                                                \
+    if (_e != cudaSuccess)                                                              \
+      return ::tdp::set_error(TDP_ECUDA, "launch of %s failed: %s", name,               \
+                              cudaGetErrorString(_e));                                  \
+    ::tdp::count_launch();                                                              \
+  } while (0)
+
+#define TDP_REQUIRE(cond, ...)                                                          \
+  do {                                                                                  \
+    if (!(cond)) return ::tdp::set_error(TDP_EINVAL, __VA_ARGS__);                      \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Number of SMs of the current device (cached per device ordinal).
+int sm_count();
+
+inline int dtype_size(int dt) {
+  switch (dt) {
+    case TDP_I64:
+    case TDP_F64:
+      return 8;
+    case TDP_F32:
+    case TDP_I32:
+      return 4;
+    case TDP_BOOL:
+      return 1;
+    default:
+      return 0;
+  }
+}
+
+inline i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// Grid for a grid-stride streaming kernel: enough CTAs to cover the work,
+// capped at `per_sm` resident CTAs on every SM.
+inline int stream_grid(i64 work_items, int items_per_cta, int per_sm) {
+  i64 want = ceil_div(work_items > 0 ? work_items : 1, items_per_cta);
+  i64 cap = (i64)sm_count() * per_sm;
+  return (int)(want < cap ? want : cap);
+}
+
+// ---------------------------------------------------------------------------
+// device-side column access
+// ---------------------------------------------------------------------------
+constexpr int kMaxPreds = 16;
+constexpr int kMaxCols = 32;
+
+struct DevPred {
+  const void* ptr;
+  int dtype;
+  int op;
+  int cmp;
+  int pad;
+  i64 li;
+  double lf;
+};
+
+struct PredSet {
+  int npreds;
+  int pad;
+  DevPred p[kMaxPreds];
+};
+
+__device__ __forceinline__ i64 load_as_i64(const void* base, int dt, i64 i) {
+  switch (dt) {
+    case TDP_I64:
+      return __ldg(reinterpret_cast<const i64*>(base) + i);
+    case TDP_I32:
+      return (i64)__ldg(reinterpret_cast<const int*>(base) + i);
+    case TDP_BOOL:
+      return (i64)reinterpret_cast<const unsigned char*>(base)[i];
+    case TDP_F64:
+      return (i64)__ldg(reinterpret_cast<const double*>(base) + i);
+    default:
+      return (i64)__ldg(reinterpret_cast<const float*>(base) + i);
+  }
+}
+
+__device__ __forceinline__ double load_as_f64(const void* base, int dt, i64 i) {
+  switch (dt) {
+    case TDP_F64:
+      return __ldg(reinterpret_cast<const double*>(base) + i);
+    case TDP_F32:
+      return (double)__ldg(reinterpret_cast<const float*>(base) + i);
+    case TDP_I64:
+      return (double)__ldg(reinterpret_cast<const i64*>(base) + i);
+    case TDP_I32:
+      return (double)__ldg(reinterpret_cast<const int*>(base) + i);
+    default:
+      return (double)reinterpret_cast<const unsigned char*>(base)[i];
+  }
+}
+
+__device__ __forceinline__ float load_as_f32(const void* base, int dt, i64 i) {
+  switch (dt) {
+    case TDP_F32:
+      return __ldg(reinterpret_cast<const float*>(base) + i);
+    case TDP_F64:
+      return (float)__ldg(reinterpret_cast<const double*>(base) + i);
+    case TDP_I64:
+      return (float)__ldg(reinterpret_cast<const i64*>(base) + i);
+    case TDP_I32:
+      return (float)__ldg(reinterpret_cast<const int*>(base) + i);
+    default:
+      return (float)reinterpret_cast<const unsigned char*>(base)[i];
+  }
+}
+
+template <class T>
+__device__ __forceinline__ bool compare(T x, T y, int op) {
+  switch (op) {
+    case TDP_EQ:
+      return x == y;
+    case TDP_NE:
+      return x != y;
+    case TDP_LT:
+      return x < y;
+    case TDP_GT:
+      return x > y;
+    case TDP_LE:
+      return x <= y;
+    default:
+      return x >= y;
+  }
+}
+
+// One comparison with the promotion the host resolved (numpy NEP 50 rules).
+__device__ __forceinline__ bool eval_pred(const DevPred& p, i64 i) {
+  switch (p.cmp) {
+    case TDP_CMP_I64:
+      return compare<i64>(load_as_i64(p.ptr, p.dtype, i), p.li, p.op);
+    case TDP_CMP_F64:
+      return compare<double>(load_as_f64(p.ptr, p.dtype, i), p.lf, p.op);
+    case TDP_CMP_F32:
+      return compare<float>(load_as_f32(p.ptr, p.dtype, i), (float)p.lf, p.op);
+    case TDP_CMP_NONE:
+      return false;
+    default:
+      return true;
+  }
+}
+
+__device__ __forceinline__ bool eval_all(const PredSet& ps, i64 i) {
+  bool keep = true;
+  for (int k = 0; k < ps.npreds; ++k) keep &= eval_pred(ps.p[k], i);
+  return keep;
+}
+
+// Host: translate public descriptors into the device predicate set.
+int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
+                 int32_t npreds, int64_t n, PredSet* out);
+
+// ---------------------------------------------------------------------------
+// warp / block helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Exclusive scan of int64 block counts; writes offsets and the total.
+// Lives in scan.cu; used by filter compaction, sort and join.
+int exclusive_scan_i64(const i64* in, i64* out, i64 n, i64* total, void* ws, size_t ws_bytes,
+                       cudaStream_t stream);
+size_t exclusive_scan_workspace(i64 n);
+
+// Filter tiling shared by compaction and the JIT projection pass: a CTA of
+// kFilterThreads threads owns kFilterTile consecutive rows, evaluated as
+// kFilterTile/32 ballot words in row order.
+constexpr int kFilterThreads = 256;
+constexpr int kFilterTile = 4096;
+constexpr int kFilterWords = kFilterTile / 32;
+
+// mask pass: bitmask words + per-tile counts (internal to filter.cu).
+int filter_bits(const PredSet& ps, int64_t n, unsigned* bits, i64* tile_counts,
+                cudaStream_t stream);
+
+}  // namespace tdp

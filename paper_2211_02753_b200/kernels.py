@@ -1,0 +1,948 @@
+"""Relational operator kernels (exact and soft) and the UDF/TVF registry.
+
+Drop-in for ``tensorquery.kernels`` (tq/kernels.py): same functions, argument
+meaning, output contracts and error classes/messages.  Every row-proportional
+loop runs in libtdp_kernels.so (sm_100a) -- there is no CPU implementation:
+
+==========================  =====================================================
+reference (tq/kernels.py)   B200 path
+==========================  =====================================================
+comparison_mask  :54        tdp_filter_mask
+filter_exact     :87        lazy Selection (tdp_filter_select when materialised)
+take_rows        :44        tdp_gather_rows / tdp_scatter_add_rows (VJP)
+groupby_exact    :108       fused tdp_scan_aggregate (dense keys) or
+                            tdp_unique_inverse + tdp_groupby_codes (general)
+_global_aggregate (compiler.py:206)  fused tdp_scan_aggregate, no keys
+soft_count       :183       tdp_soft_groupby_fwd/bwd (one dense key)
+soft_groupby     :212       tdp_soft_groupby_fwd/bwd (dense + compact one-hot keys)
+dense_exact_counts :238     tdp_groupby_codes
+stable_order     :256       tdp_sort_order (LSD radix, numpy stable semantics)
+sort_limit / limit_rows     tdp_sort_order + tdp_gather_rows
+equi_join (new)             tdp_join_prepare / tdp_join_emit
+==========================  =====================================================
+"""
+
+from __future__ import annotations
+
+from ctypes import c_int32
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .encodings import (
+    DictionaryEncoding,
+    EncodedTensor,
+    EncodingError,
+    OneHotValue,
+    onehot_payload,
+    plain,
+    trusted,
+)
+from .lazy import (
+    Expr,
+    LazyValue,
+    Pred,
+    Program,
+    Selection,
+    as_expr,
+    base_rows,
+    resolve_predicate,
+)
+from .distributed import allreduce_partials, allreduce_ranges, current_group
+from .storage import ColumnType
+from .tensor import (
+    FLOAT_DTYPES,
+    Parameter,
+    Tensor,
+    _finish,
+    _grad_mode,
+    _inputs,
+    active_tape,
+    add,
+    div,
+    mul,
+    reshape,
+    tensor,
+    to_device,
+    torch_dtype,
+)
+
+AVG_STABILIZER = 1e-12
+DENSE_SLOT_LIMIT = 1 << 16
+
+
+class KernelError(ValueError):
+    """Kernel precondition violation (types, shapes, arity)."""
+
+
+def _as_index(indices) -> torch.Tensor:
+    if isinstance(indices, Tensor):
+        indices = indices.data
+    return to_device(indices if isinstance(indices, torch.Tensor) else np.asarray(indices, dtype=np.int64)).to(torch.int64).reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# Row selection shared by filter / sort / limit
+# ---------------------------------------------------------------------------
+
+
+def take_rows(col: EncodedTensor, indices) -> EncodedTensor:
+    """Compact a column to the given row indices, preserving gradients."""
+    idx = _as_index(indices)
+    v = col.values
+    oh = onehot_payload(v)
+    with trusted():
+        if oh is not None:
+            from .autograd import gather_rows_raw
+
+            return EncodedTensor(Tensor(OneHotValue(gather_rows_raw(oh.codes, idx), oh.k, oh.dtype)),
+                                 col.encoding)
+        if v.dtype in FLOAT_DTYPES and active_tape() is not None:
+            from .tensor import gather
+
+            return EncodedTensor(gather(v, Tensor(idx), axis=0), col.encoding)
+        from .autograd import gather_rows_raw
+
+        return EncodedTensor(Tensor(gather_rows_raw(v.data, idx)), col.encoding)
+
+
+_OPS = ("=", "<>", "<", ">", "<=", ">=")
+
+
+def _resolve(col: EncodedTensor, op: str, literal, base: Optional[torch.Tensor]) -> Pred:
+    """Validate one comparison exactly as comparison_mask does and resolve it."""
+    if op not in _OPS:
+        raise KernelError(f"unknown comparison operator {op!r}")
+    if col.is_dictionary():
+        if not isinstance(literal, str):
+            raise KernelError(f"string column compared against {literal!r}")
+        code = col.encoding.dictionary.code_of(literal)
+        if code is None:
+            return Pred(None, op, nat.CMP_NONE, 0, 0.0)
+        return Pred(base, op, nat.CMP_I64, code, 0.0)
+    if col.is_pe():
+        raise KernelError("cannot filter on a probability-encoded column")
+    if isinstance(literal, str):
+        raise KernelError(f"numeric column compared against string {literal!r}")
+    if col.values.ndim != 1:
+        raise KernelError("filters require scalar columns")
+    cmp, li, lf = resolve_predicate(col.values.dtype, op, literal)
+    return Pred(base if cmp in (nat.CMP_I64, nat.CMP_F64, nat.CMP_F32) else None, op, cmp, li, lf)
+
+
+def comparison_mask(col: EncodedTensor, op: str, literal) -> torch.Tensor:
+    """Boolean row mask for ``col <op> literal`` (tdp_filter_mask)."""
+    data = col.values.data if not col.is_pe() else None
+    p = _resolve(col, op, literal, data)
+    n = col.row_count
+    out = torch.empty(n, dtype=torch.bool, device=data.device if data is not None else None)
+    cols = [data] if p.col is not None else []
+    if n:
+        nat.require_cuda(out, *cols)
+        from .lazy import native_predicates
+
+        nat.call("tdp_filter_mask", nat.columns(cols), len(cols),
+                 native_predicates([p], {id(c): i for i, c in enumerate(cols)}), 1, n,
+                 nat.ptr(out), nat.stream())
+    return out
+
+
+def _row_space(columns: Sequence[EncodedTensor]) -> Optional[tuple[Optional[Selection], int]]:
+    """Common (selection, base rows) of columns that can stay lazy, else None."""
+    sel_id, sel, n = None, None, None
+    for c in columns:
+        v = c.values
+        if v._t is not None:
+            s, rows = None, (int(v._t.shape[0]) if v._t.dim() else -1)
+        elif isinstance(v._lazy, LazyValue):
+            s = v._lazy.sel
+            rows = s.n if s is not None else base_rows(v._lazy.expr)
+            if s is not None and v._lazy.expr.op != "col":
+                # expression columns refine fine; require the same base space
+                pass
+        else:
+            return None
+        key = id(s) if s is not None else None
+        if n is None:
+            sel_id, sel, n = key, s, rows
+        elif key != sel_id or rows != n:
+            return None
+    return sel, (n if n is not None else 0)
+
+
+def filter_exact(columns: Sequence[EncodedTensor],
+                 predicates: Sequence[tuple[int, str, object]]) -> list[EncodedTensor]:
+    """Conjunctive filter: AND of per-predicate masks, then row compaction.
+
+    The compaction is late: the returned columns are lazy views of the input
+    rows under the new selection; consumers either fuse it (group-by) or
+    materialise it with tdp_filter_select + tdp_gather_rows.
+    """
+    if not columns:
+        return []
+    space = _row_space(columns) if active_tape() is None else None
+    if space is None:
+        return _filter_eager(columns, predicates)
+    sel, n = space
+    preds = []
+    for idx, op, literal in predicates:
+        col = columns[idx]
+        v = col.values
+        base = None
+        if not col.is_pe() and v.ndim == 1:
+            if v._t is not None:
+                base = v._t
+            elif v._lazy.expr.op == "col":
+                base = v._lazy.expr.col
+            else:  # predicate on a computed column: evaluate eagerly
+                return _filter_eager(columns, predicates)
+        preds.append(_resolve(col, op, literal, base))
+    device = _device_of([as_expr(c.values)[0] for c in columns], sel)
+    new_sel = sel.refine(preds) if sel is not None else Selection(n, preds, device)
+    out = []
+    for c in columns:
+        v = c.values
+        if v._t is not None:
+            lv = LazyValue(Expr.column(v._t), new_sel, valid_for=c.encoding)
+        else:
+            lv = LazyValue(v._lazy.expr, new_sel, valid_for=c.encoding)
+        with trusted():
+            out.append(EncodedTensor(Tensor(lv), c.encoding))
+    return out
+
+
+def _filter_eager(columns: Sequence[EncodedTensor], predicates) -> list[EncodedTensor]:
+    n = columns[0].row_count
+    preds = []
+    cols: list[torch.Tensor] = []
+    index: dict[int, int] = {}
+    for idx, op, literal in predicates:
+        col = columns[idx]
+        data = None
+        if not col.is_pe() and (col.is_dictionary() or not isinstance(literal, str)):
+            data = col.values.data.detach() if col.values.ndim == 1 else None
+        p = _resolve(col, op, literal, data)
+        if p.col is not None and id(p.col) not in index:
+            index[id(p.col)] = len(cols)
+            cols.append(p.col)
+        preds.append(p)
+    sel = Selection(n, preds, cols[0].device if cols else None)
+    if not cols:
+        sel._run()
+    idx = sel.indices()
+    return [take_rows(c, idx) for c in columns]
+
+
+# ---------------------------------------------------------------------------
+# Exact group-by (tq/kernels.py:108-167) and global aggregates (compiler.py:206)
+# ---------------------------------------------------------------------------
+
+AggInput = tuple[str, Optional[object]]  # ("count", None) | ("sum"/"avg", values)
+
+
+def _value_dtype(v) -> str:
+    if isinstance(v, Tensor):
+        return v.dtype
+    if isinstance(v, torch.Tensor):
+        from .tensor import dtype_name
+
+        return dtype_name(v)
+    return np.asarray(v).dtype.name
+
+
+def _as_value(v):
+    if isinstance(v, (Tensor, torch.Tensor)):
+        return v
+    return Tensor(np.asarray(v))
+
+
+def _agg_kind(func: str, dtype: str) -> int:
+    if func == "count":
+        return nat.AGG_COUNT
+    return nat.AGG_SUM_F64 if dtype in FLOAT_DTYPES else nat.AGG_SUM_I64
+
+
+def _fusable(values: Sequence) -> Optional[tuple[Optional[Selection], int]]:
+    """Common selection / base length of all operands, or None."""
+    sel_key, sel, n = 0, None, None
+    for v in values:
+        e, s = as_expr(v)
+        rows = s.n if s is not None else base_rows(e)
+        if rows < 0:
+            return None
+        k = id(s) if s is not None else None
+        if n is None:
+            sel_key, sel, n = k, s, rows
+        elif k != sel_key or rows != n:
+            return None
+    return sel, (n or 0)
+
+
+def _materialize(v) -> torch.Tensor:
+    if isinstance(v, Tensor):
+        return v.data.detach()
+    return to_device(v)
+
+
+def _scan_aggregate(exprs_keys: Sequence[Expr], spans: Sequence[tuple[int, int]],
+                    aggs: Sequence[tuple[int, Optional[Expr]]], sel: Optional[Selection],
+                    n: int, device) -> tuple[torch.Tensor, torch.Tensor, int]:
+    """Run tdp_scan_aggregate; returns (counts[G], sums_raw[naggs, G] int64 bits, G)."""
+    prog = Program()
+    keys = [nat.Key(prog.value(e), 0, lo, span) for e, (lo, span) in zip(exprs_keys, spans)]
+    agg_structs = []
+    for kind, e in aggs:
+        if kind == nat.AGG_COUNT:
+            agg_structs.append(nat.Agg(kind, 0))
+        else:
+            val = prog.value(e if kind == nat.AGG_SUM_F64 or e.dtype == "int64" else e.cast("int64"))
+            agg_structs.append(nat.Agg(kind, val))
+    preds, npreds = prog.predicates(sel)
+    slots = 1
+    for _, span in spans:
+        slots *= span
+    nat.require_cuda(*prog.cols)
+    counts = torch.empty(slots, dtype=torch.int64, device=device)
+    sums = torch.empty((max(1, len(aggs)), slots), dtype=torch.int64, device=device)
+    ws = nat.workspace(nat.load().tdp_scan_aggregate_workspace(n, slots, len(aggs)), device)
+    hook = PROFILE_HOOK
+    if hook is not None:
+        hook.begin("tdp_scan_aggregate", n)
+    nat.call("tdp_scan_aggregate", prog.native_columns(), len(prog.cols), n, preds, npreds,
+             prog.native_instrs(), len(prog.instrs), nat.struct_array(nat.Key, keys), len(keys),
+             nat.struct_array(nat.Agg, agg_structs), len(agg_structs), nat.ptr(counts),
+             nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
+    if hook is not None:
+        hook.end("tdp_scan_aggregate")
+    return counts, sums, slots
+
+
+# Optional kernel timer (bench.py): object with begin(name, rows) / end(name)
+# that records CUDA events on the current stream around native calls.
+PROFILE_HOOK = None
+
+
+def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device):
+    nkeys = len(spans)
+    keys = nat.struct_array(nat.Key, [nat.Key(0, 0, lo, span) for lo, span in spans])
+    aggs = nat.struct_array(nat.Agg, [nat.Agg(k, 0) for k in aggs_kinds])
+    out_keys = torch.empty((max(1, nkeys), slots), dtype=torch.int64, device=device)
+    out_counts = torch.empty(slots, dtype=torch.int64, device=device)
+    out_aggs = torch.empty((max(1, len(aggs_kinds)), slots), dtype=torch.int64, device=device)
+    out_groups = torch.empty(1, dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_finalize", nat.ptr(counts), nat.ptr(sums), slots, keys, nkeys, aggs,
+             len(aggs_kinds), avg_mask, nat.ptr(out_keys), nat.ptr(out_counts), nat.ptr(out_aggs),
+             nat.ptr(out_groups), nat.stream())
+    g = int(out_groups.item())
+    return out_keys[:, :g], out_counts[:g], out_aggs[:, :g], g
+
+
+def _agg_outputs(aggs: Sequence[tuple[str, str]], raw: torch.Tensor, counts: torch.Tensor,
+                 already_avg: bool) -> list[torch.Tensor]:
+    """Typed aggregate columns from raw 8-byte results."""
+    out = []
+    for a, (func, dt) in enumerate(aggs):
+        r = raw[a].contiguous()
+        if func == "count":
+            out.append(r.clone())
+        elif func == "avg":
+            if already_avg:
+                out.append(r.view(torch.float64).clone())
+            else:
+                s = r.view(torch.float64) if dt in FLOAT_DTYPES else r.to(torch.float64)
+                out.append(s / counts.to(torch.float64))
+        else:
+            out.append(r.view(torch.float64).clone() if dt in FLOAT_DTYPES else r.clone())
+    return out
+
+
+def groupby_exact(keys: Sequence[EncodedTensor],
+                  aggs: Sequence[AggInput]) -> tuple[list[torch.Tensor], list[torch.Tensor]]:
+    """Group rows by the key columns and aggregate.
+
+    Returns key-value arrays and aggregate arrays over the non-empty groups,
+    ordered by ascending combined key (lexicographic over the key columns).
+    """
+    if not keys:
+        raise KernelError("groupby_exact requires at least one key column")
+    for k in keys:
+        if k.is_pe():
+            raise KernelError("exact group-by cannot consume PE keys; decode first")
+        if k.values.ndim != 1 or k.values.dtype != "int64":
+            raise KernelError(
+                f"group-by keys must be integer or dictionary columns, got {k.values.dtype}"
+            )
+    key_vals = [k.values for k in keys]
+    agg_specs: list[tuple[str, str]] = []
+    agg_vals: list = []
+    for func, values in aggs:
+        if func == "count":
+            agg_specs.append(("count", "int64"))
+            agg_vals.append(None)
+            continue
+        if values is None:
+            raise KernelError(f"{func} aggregate needs a value column of {keys[0].row_count} rows")
+        if func not in ("sum", "avg"):
+            raise KernelError(f"unknown aggregate {func!r}")
+        v = _as_value(values)
+        agg_specs.append((func, _value_dtype(v)))
+        agg_vals.append(v)
+
+    operands = key_vals + [v for v in agg_vals if v is not None]
+    space = _fusable(operands)
+    if space is not None and all(as_expr(k)[0].op in ("col", "cast", "add", "sub", "mul", "neg", "square")
+                                 for k in key_vals):
+        return _groupby_fused(keys, key_vals, agg_specs, agg_vals, space)
+    return _groupby_general(keys, key_vals, agg_specs, agg_vals)
+
+
+def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space):
+    sel, n = space
+    kexprs = [as_expr(v)[0] for v in key_vals]
+    device = _device_of(kexprs, sel)
+    spans: list[tuple[int, int]] = []
+    need_range = [j for j, k in enumerate(keys) if not k.is_dictionary()]
+    ranges: dict[int, tuple[int, int]] = {}
+    if need_range:
+        if any(kexprs[j].op != "col" for j in need_range):
+            return _groupby_general(keys, key_vals, agg_specs, agg_vals)
+        prog = Program()
+        kc = [prog.col_index(kexprs[j].col) for j in need_range]
+        preds, npreds = prog.predicates(sel)
+        mm = torch.empty(2 * len(need_range), dtype=torch.int64, device=device)
+        nat.require_cuda(*prog.cols)
+        nat.call("tdp_scan_minmax", prog.native_columns(), len(prog.cols), n, preds, npreds,
+                 (c_int32 * len(kc))(*kc), len(kc), nat.ptr(mm), nat.stream())
+        group = current_group()
+        if group is not None:
+            lo, hi = allreduce_ranges(mm[0::2].contiguous(), mm[1::2].contiguous(), group)
+            mm = torch.stack([lo, hi], dim=1).reshape(-1)
+        host = mm.tolist()
+        for t, j in enumerate(need_range):
+            ranges[j] = (host[2 * t], host[2 * t + 1])
+        if any(lo > hi for lo, hi in ranges.values()):
+            return _empty_groups(len(keys), agg_specs, device)
+    slots = 1
+    for j, k in enumerate(keys):
+        if k.is_dictionary():
+            lo, span = 0, max(1, len(k.encoding.dictionary))
+        else:
+            lo, hi = ranges[j]
+            span = hi - lo + 1
+        spans.append((lo, span))
+        slots *= span
+    if slots > DENSE_SLOT_LIMIT:
+        if current_group() is not None:
+            raise KernelError("sharded group-by over more than "
+                              f"{DENSE_SLOT_LIMIT} dense slots needs a key shuffle")
+        return _groupby_general(keys, key_vals, agg_specs, agg_vals)
+    agg_exprs = []
+    for (func, dt), v in zip(agg_specs, agg_vals):
+        kind = _agg_kind(func, dt)
+        agg_exprs.append((kind, as_expr(v)[0] if v is not None else None))
+    counts, sums, slots = _scan_aggregate(kexprs, spans, agg_exprs, sel, n, device)
+    allreduce_partials(counts, sums, [a for a, (k, _) in enumerate(agg_exprs)
+                                      if k == nat.AGG_SUM_F64], current_group())
+    avg_mask = 0
+    for a, (func, _) in enumerate(agg_specs):
+        if func == "avg":
+            avg_mask |= 1 << a
+    kinds = [k for k, _ in agg_exprs]
+    out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask, device)
+    key_values = [out_keys[j].contiguous() for j in range(len(keys))]
+    return key_values, _agg_outputs(agg_specs, out_aggs, out_counts, already_avg=True)
+
+
+def _device_of(exprs, sel):
+    if sel is not None and sel.device is not None:
+        return sel.device
+    stack = list(exprs)
+    while stack:
+        e = stack.pop()
+        if e.op == "col":
+            return e.col.device
+        stack.extend(e.args)
+    return torch.device("cuda")
+
+
+def _empty_groups(nkeys: int, agg_specs, device):
+    key_values = [torch.empty(0, dtype=torch.int64, device=device) for _ in range(nkeys)]
+    outs = []
+    for func, dt in agg_specs:
+        if func == "count":
+            outs.append(torch.empty(0, dtype=torch.int64, device=device))
+        elif func == "avg" or dt in FLOAT_DTYPES:
+            outs.append(torch.empty(0, dtype=torch.float64, device=device))
+        else:
+            outs.append(torch.empty(0, dtype=torch.int64, device=device))
+    return key_values, outs
+
+
+def unique_inverse(key: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """np.unique(key, return_inverse=True) on the device (tdp_unique_inverse)."""
+    key = key.contiguous().to(torch.int64)
+    nat.require_cuda(key)
+    n = key.numel()
+    dev = key.device
+    uniques = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    inverse = torch.empty(n, dtype=torch.int64, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    lib = nat.load()
+    ws = nat.workspace(lib.tdp_sort_workspace(n) + 2 * ((n * 8 + 255) // 256 * 256) + 1024, dev)
+    nat.call("tdp_unique_inverse", nat.ptr(key), n, nat.ptr(uniques), nat.ptr(inverse),
+             nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream())
+    u = int(count.item()) if n else 0
+    return uniques[:u], inverse
+
+
+def _groupby_codes(codes: torch.Tensor, slots: int, agg_specs, agg_vals, n: int, device):
+    kinds = [_agg_kind(f, dt) for f, dt in agg_specs]
+    vals = []
+    keep = []
+    for (func, dt), v, kind in zip(agg_specs, agg_vals, kinds):
+        if kind == nat.AGG_COUNT:
+            vals.append(None)
+            continue
+        t = _materialize(v)
+        if t.dim() != 1 or t.shape[0] != n:
+            raise KernelError(f"{func} aggregate needs a value column of {n} rows")
+        if t.dtype == torch.bool:
+            t = t.to(torch.int64)
+        keep.append(t)
+        vals.append(t)
+    cols = (nat.Column * max(1, len(vals)))()
+    for a, t in enumerate(vals):
+        cols[a] = nat.column(t) if t is not None else nat.Column(None, nat.I64, 0, 0, 1)
+    counts = torch.empty(slots, dtype=torch.int64, device=device)
+    sums = torch.empty((max(1, len(kinds)), slots), dtype=torch.int64, device=device)
+    nat.require_cuda(codes)
+    nat.call("tdp_groupby_codes", nat.ptr(codes), n, slots, cols,
+             (c_int32 * max(1, len(kinds)))(*kinds), len(kinds), nat.ptr(counts), nat.ptr(sums),
+             nat.stream())
+    return counts, sums
+
+
+def _groupby_general(keys, key_vals, agg_specs, agg_vals):
+    """Sort-based path (the reference's np.unique algorithm on the device)."""
+    kdata = [_materialize(v) for v in key_vals]
+    n = int(kdata[0].shape[0])
+    for (func, dt), v in zip(agg_specs, agg_vals):
+        if v is not None and (_materialize(v).dim() != 1 or _materialize(v).shape[0] != n):
+            raise KernelError(f"{func} aggregate needs a value column of {n} rows")
+    device = kdata[0].device
+    nat.require_cuda(*kdata)
+    if n == 0:
+        return _empty_groups(len(keys), agg_specs, device)
+    uniqs, codes = zip(*[unique_inverse(k) for k in kdata])
+    if len(kdata) == 1:
+        group_codes, slots = codes[0], int(uniqs[0].numel())
+        key_values = [uniqs[0]]
+    else:
+        spaces = [max(1, int(u.numel())) for u in uniqs]
+        combined = torch.zeros(n, dtype=torch.int64, device=device)
+        for c, s in zip(codes, spaces):
+            combined = combined * s + c
+        occupied, group_codes = unique_inverse(combined)
+        slots = int(occupied.numel())
+        key_values = []
+        rem = occupied.clone()
+        for u, s in zip(reversed(uniqs), reversed(spaces)):
+            from .autograd import gather_rows_raw
+
+            key_values.append(gather_rows_raw(u, (rem % s).contiguous()))
+            rem = rem // s
+        key_values.reverse()
+    counts, sums = _groupby_codes(group_codes, slots, agg_specs, agg_vals, n, device)
+    return key_values, _agg_outputs(agg_specs, sums, counts, already_avg=False)
+
+
+def global_aggregate(row_source: Sequence[EncodedTensor], agg_inputs) -> list[torch.Tensor]:
+    """``_global_aggregate`` (tq/compiler.py:206-215): no GROUP BY.
+
+    count -> int64 [rows]; sum -> [sum] in the input dtype; avg -> [mean]
+    (float64 for int input, NaN when empty).  One fused pass computes the row
+    count and every sum.
+    """
+    vals = [_as_value(v) for f, v in agg_inputs if f != "count"]
+    operands = list(vals) + [c.values for c in row_source[:1]]
+    space = _fusable(operands) if operands else None
+    rows_dev = raw = None
+    if space is not None:
+        sel, n = space
+        device = _device_of([as_expr(v)[0] for v in operands], sel)
+        specs = [(nat.AGG_COUNT, None) if f == "count"
+                 else (_agg_kind(f, _value_dtype(v)), as_expr(_as_value(v))[0])
+                 for f, v in agg_inputs]
+        rows_dev, raw, _ = _scan_aggregate([], [], specs, sel, n, device)
+        allreduce_partials(rows_dev, raw, [a for a, (k, _) in enumerate(specs)
+                                           if k == nat.AGG_SUM_F64], current_group())
+    elif current_group() is not None:
+        raise KernelError("sharded global aggregate needs its inputs in one row space")
+    out = []
+    for a, (func, values) in enumerate(agg_inputs):
+        if func == "count":
+            if rows_dev is not None:
+                out.append(rows_dev[:1].clone())
+            else:
+                out.append(torch.tensor([row_source[0].row_count if row_source else 0],
+                                        dtype=torch.int64, device=_materialize(vals[0]).device
+                                        if vals else None))
+            continue
+        v = _as_value(values)
+        dt = _value_dtype(v)
+        if raw is not None:
+            r, cnt = raw[a, :1], rows_dev[:1]
+        else:  # value columns in different row spaces: one pass per column
+            cnt, r = _scan_single(_materialize(v))
+        total = r.view(torch.float64) if dt in FLOAT_DTYPES else r
+        if func == "sum":
+            # numpy keeps the input dtype: float32 stays float32, bool -> any()
+            out.append(total != 0 if dt == "bool" else total.to(torch_dtype(dt)).clone())
+        else:
+            mean = total.to(torch.float64) / cnt.to(torch.float64)
+            # numpy: float32 mean stays float32; an empty input gives float64 NaN
+            if dt == "float32" and int(cnt.item()) > 0:
+                mean = mean.to(torch.float32)
+            out.append(mean)
+    return out
+
+
+def _scan_single(t: torch.Tensor):
+    spec = [(nat.AGG_COUNT, None), (_agg_kind("sum", _value_dtype(t)), Expr.column(t.contiguous()))]
+    counts, sums, _ = _scan_aggregate([], [], spec, None, int(t.shape[0]), t.device)
+    return counts[:1], sums[1, :1]
+
+
+# ---------------------------------------------------------------------------
+# Soft aggregates over PE columns (tq/kernels.py:175-235)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class GroupedCounts:
+    """Dense aggregate grid over the cross-product of the key spaces."""
+
+    key_spaces: tuple[int, ...]
+    counts: Tensor
+
+
+def _soft_inputs(pes: Sequence[EncodedTensor]):
+    from .autograd import SoftKeySpec
+
+    kinds, tensors, dts = [], [], []
+    tape = active_tape()
+    for p in pes:
+        oh = onehot_payload(p.values)
+        if oh is not None:
+            kinds.append(("onehot", oh.k))
+            tensors.append(oh.codes)
+            dts.append(oh.dtype)
+        else:
+            kinds.append(("dense", p.encoding.num_classes))
+            t = tape.input_for(p.values) if tape is not None else p.values.data
+            tensors.append(t.contiguous())
+            dts.append(p.values.dtype)
+    return SoftKeySpec(kinds), tensors, dts
+
+
+def soft_count(pe: EncodedTensor) -> Tensor:
+    """Differentiable count per class: column sums of the PE matrix."""
+    if not pe.is_pe():
+        raise EncodingError("soft_count requires a probability-encoded column")
+    return soft_groupby([pe], "count").counts
+
+
+def _joint_spaces(pes: Sequence[EncodedTensor]) -> tuple[tuple[int, ...], int]:
+    if not pes:
+        raise KernelError("soft_groupby requires at least one PE column")
+    n = pes[0].row_count
+    spaces = []
+    for p in pes:
+        if not p.is_pe():
+            raise EncodingError("soft_groupby keys must be probability-encoded")
+        if p.row_count != n:
+            raise KernelError(f"soft_groupby keys disagree on row count ({p.row_count} vs {n})")
+        spaces.append(p.encoding.num_classes)
+    return tuple(spaces), n
+
+
+def soft_groupby(pes: Sequence[EncodedTensor], agg: str = "count",
+                 values: Optional[Tensor] = None) -> GroupedCounts:
+    """Differentiable grouped aggregation over PE key columns.
+
+    counts[c1..cm] = sum_i prod_j P_j[i, c_j]; every cell of the dense grid
+    is emitted.  sum/avg weight each row's joint probability by a plain
+    numeric column.  The n x prod(k) joint is never materialised.
+    """
+    spaces, n = _joint_spaces(pes)
+    from .autograd import soft_groupby_grid
+
+    spec, keys, dts = _soft_inputs(pes)
+    nat.require_cuda(*keys)
+    joint_dt = dts[0]
+    for d in dts[1:]:
+        joint_dt = np.promote_types(joint_dt, d).name
+    with _grad_mode():
+        grid = soft_groupby_grid(spec, keys, n, torch_dtype(joint_dt))
+        counts = _finish(grid.reshape(spaces))
+    if agg == "count":
+        return GroupedCounts(spaces, counts)
+    if values is None:
+        raise KernelError(f"soft {agg} needs a value column")
+    if values.shape != (n,):
+        raise KernelError(f"value column shape {list(values.shape)} != [{n}]")
+    w = values if values.dtype in FLOAT_DTYPES else values.astype("float64")
+    wdt = np.promote_types(joint_dt, w.dtype).name
+    tape = active_tape()
+    with _grad_mode():
+        wt = tape.input_for(w) if tape is not None else w.data
+        weighted_grid = soft_groupby_grid(spec, keys, n, torch_dtype(wdt), values=wt.contiguous())
+        weighted = _finish(weighted_grid.reshape(spaces))
+    if agg == "sum":
+        return GroupedCounts(spaces, weighted)
+    if agg == "avg":
+        eps = tensor(AVG_STABILIZER, dtype=counts.dtype)
+        return GroupedCounts(spaces, div(weighted, add(counts, eps)))
+    raise KernelError(f"unknown soft aggregate {agg!r}")
+
+
+def dense_exact_counts(codes: Sequence, spaces: Sequence[int]) -> torch.Tensor:
+    """Exact contingency grid over fixed key spaces (densified group-by)."""
+    spaces = tuple(int(s) for s in spaces)
+    cs = [_as_index(c) for c in codes]
+    n = int(cs[0].numel()) if cs else 0
+    dev = cs[0].device if cs else None
+    total = 1
+    for s in spaces:
+        total *= s
+    if n:
+        nat.require_cuda(*cs)
+        from .encodings import _codes_out_of_range
+
+        for c, s in zip(cs, spaces):
+            if _codes_out_of_range(c, s):
+                raise KernelError(f"key code out of range [0, {s})")
+    combined = torch.zeros(n, dtype=torch.int64, device=dev)
+    for c, s in zip(cs, spaces):
+        combined = combined * s + c
+    counts, _ = _groupby_codes(combined, max(1, total), [], [], n, dev)
+    return counts[:total].reshape(spaces)
+
+
+# ---------------------------------------------------------------------------
+# Sort / limit (tq/kernels.py:256-280)
+# ---------------------------------------------------------------------------
+
+
+def stable_order(key: EncodedTensor, descending: bool = False) -> torch.Tensor:
+    """Stable row order by a numeric or dictionary key (tdp_sort_order)."""
+    if key.is_pe():
+        raise KernelError("cannot sort by a probability-encoded column")
+    if key.values.ndim != 1:
+        raise KernelError("sort keys must be scalar columns")
+    arr = key.values.data.detach()
+    if arr.dtype == torch.bool:
+        if descending:
+            raise TypeError("The numpy boolean negative, the `-` operator, is not supported, "
+                            "use the `~` operator or the logical_not function instead.")
+        arr = arr.to(torch.int64)
+    arr = arr.contiguous()
+    nat.require_cuda(arr)
+    n = int(arr.shape[0])
+    out = torch.empty(n, dtype=torch.int64, device=arr.device)
+    if n:
+        ws = nat.workspace(nat.load().tdp_sort_workspace(n), arr.device)
+        nat.call("tdp_sort_order", nat.columns([arr]), 1 if descending else 0, n, nat.ptr(out),
+                 nat.ptr(ws), ws.numel(), nat.stream())
+    return out
+
+
+def sort_limit(columns: Sequence[EncodedTensor], key_index: int,
+               descending: bool = False, limit: Optional[int] = None) -> list[EncodedTensor]:
+    order = stable_order(columns[key_index], descending)
+    if limit is not None:
+        order = order[: max(0, limit)]
+    return [take_rows(c, order) for c in columns]
+
+
+def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTensor]:
+    if not columns:
+        return []
+    n = columns[0].row_count
+    m = min(max(0, count), n)
+    out = []
+    with trusted():
+        for c in columns:
+            oh = onehot_payload(c.values)
+            if oh is not None:
+                out.append(EncodedTensor(Tensor(OneHotValue(oh.codes[:m], oh.k, oh.dtype)), c.encoding))
+                continue
+            v = c.values
+            if v.dtype in FLOAT_DTYPES and active_tape() is not None:
+                from .tensor import slice_axis
+
+                out.append(EncodedTensor(slice_axis(v, 0, 0, m), c.encoding))
+            else:
+                out.append(EncodedTensor(Tensor(v.data[:m]), c.encoding))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Equi-join (builder-defined; the reference has none -- SURVEY §8 A20)
+# ---------------------------------------------------------------------------
+
+
+def join_indices(probe_key, build_key) -> tuple[torch.Tensor, torch.Tensor]:
+    """Inner equi-join row pairs: (probe rows, build rows), ordered by probe row
+    then ascending build row (stable radix sort of the build keys + binary
+    search per probe key)."""
+    pk = _materialize(probe_key).contiguous().to(torch.int64)
+    bk = _materialize(build_key).contiguous().to(torch.int64)
+    nat.require_cuda(pk, bk)
+    dev = pk.device
+    n_probe, n_build = int(pk.numel()), int(bk.numel())
+    ws = nat.workspace(nat.load().tdp_join_workspace(n_build, n_probe), dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    nat.call("tdp_join_prepare", nat.ptr(bk), n_build, nat.ptr(pk), n_probe, nat.ptr(count),
+             nat.ptr(ws), ws.numel(), nat.stream())
+    m = int(count.item())
+    pi = torch.empty(m, dtype=torch.int64, device=dev)
+    bi = torch.empty(m, dtype=torch.int64, device=dev)
+    if m:
+        nat.call("tdp_join_emit", n_build, n_probe, nat.ptr(pi), nat.ptr(bi), nat.ptr(ws),
+                 ws.numel(), nat.stream())
+    return pi, bi
+
+
+def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], left_key: int,
+              right_key: int) -> list[EncodedTensor]:
+    """Inner join ``left.left_key = right.right_key``; returns left columns then
+    right columns.  Keys must be plain int64 columns (dictionary codes from
+    different dictionaries are not comparable)."""
+    for side, cols, k in (("left", left, left_key), ("right", right, right_key)):
+        col = cols[k]
+        if col.is_pe() or col.is_dictionary() or col.values.dtype != "int64" or col.values.ndim != 1:
+            raise KernelError(f"{side} join key must be a plain int64 column")
+    pi, bi = join_indices(left[left_key].values, right[right_key].values)
+    return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
+
+
+# ---------------------------------------------------------------------------
+# UDF / TVF registry (tq/kernels.py:288-369)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class UdfEntry:
+    """A registered function: declared outputs, arity, body and parameters."""
+
+    name: str
+    output_schema: tuple[tuple[str, ColumnType], ...]
+    arity: int
+    body: Callable[..., tuple[EncodedTensor, ...]]
+    params: tuple[Parameter, ...] = ()
+    pe_outputs: bool = True
+
+
+def _row_keys(outputs: Sequence[EncodedTensor]) -> set:
+    """Row counts of outputs, compared symbolically for lazy views of one selection."""
+    keys = set()
+    for o in outputs:
+        v = o.values
+        if v._t is None and isinstance(v._lazy, LazyValue) and v._lazy.sel is not None \
+                and v._lazy.sel._count is None:
+            keys.add(("sel", id(v._lazy.sel)))
+        else:
+            keys.add(o.row_count)
+    return keys
+
+
+class UdfRegistry:
+    """Insertion-ordered function registry; registrations are exclusive."""
+
+    def __init__(self):
+        self._entries: dict[str, UdfEntry] = {}
+
+    def register(self, entry: UdfEntry) -> UdfEntry:
+        if entry.name in self._entries:
+            raise KernelError(f"function {entry.name!r} is already registered")
+        seen = set()
+        for p in entry.params:
+            if p.name in seen:
+                raise KernelError(f"duplicate parameter name {p.name!r} in {entry.name!r}")
+            seen.add(p.name)
+        self._entries[entry.name] = entry
+        return entry
+
+    def lookup(self, name: str) -> Optional[UdfEntry]:
+        return self._entries.get(name)
+
+    def names(self) -> list[str]:
+        return list(self._entries)
+
+    def entries(self) -> list[UdfEntry]:
+        return list(self._entries.values())
+
+    def invoke(self, name: str, inputs: Sequence[EncodedTensor]) -> tuple[EncodedTensor, ...]:
+        entry = self._entries.get(name)
+        if entry is None:
+            raise KernelError(f"unknown function {name!r}")
+        if len(inputs) != entry.arity:
+            raise KernelError(f"function {name!r} takes {entry.arity} argument(s), got {len(inputs)}")
+        outputs = entry.body(*inputs)
+        if isinstance(outputs, EncodedTensor):
+            outputs = (outputs,)
+        outputs = tuple(outputs)
+        self._validate_outputs(entry, outputs)
+        return outputs
+
+    @staticmethod
+    def _validate_outputs(entry: UdfEntry, outputs: tuple[EncodedTensor, ...]) -> None:
+        declared = entry.output_schema
+        if len(outputs) != len(declared):
+            raise KernelError(
+                f"function {entry.name!r} declared {len(declared)} output column(s), "
+                f"returned {len(outputs)}"
+            )
+        rows = _row_keys(outputs)
+        if len(rows) > 1:
+            counts = sorted({o.row_count for o in outputs})
+            if len(counts) > 1:
+                raise KernelError(
+                    f"function {entry.name!r} returned columns with differing row counts {counts}"
+                )
+        for (name, ctype), out in zip(declared, outputs):
+            if ctype.kind == "tensor" and entry.pe_outputs:
+                if not out.is_pe() or out.encoding.num_classes != ctype.dims[0]:
+                    raise KernelError(
+                        f"output {name!r} of {entry.name!r} must be PE over {ctype.dims[0]} classes"
+                    )
+            elif ctype.kind == "string":
+                if not out.is_dictionary():
+                    raise KernelError(f"output {name!r} of {entry.name!r} must be a string column")
+            elif ctype.kind in ("int", "float"):
+                if out.values.ndim != 1:
+                    raise KernelError(f"output {name!r} of {entry.name!r} must be a scalar column")
+
+
+def make_scoring_udf(name: str, weights: Tensor, scale: float = 1.0,
+                     column: str = "Score") -> UdfEntry:
+    """Generic scoring hook: rows -> plain float score, x . w / scale."""
+    if weights.ndim != 1:
+        raise KernelError("scoring weights must be a vector")
+    d = int(weights.shape[0])
+
+    def body(col: EncodedTensor) -> tuple[EncodedTensor, ...]:
+        x = col.values
+        if x.ndim != 2 or x.shape[1] != d:
+            raise KernelError(f"scoring input must be [n, {d}]")
+        from .tensor import matmul
+
+        scores = mul(reshape(matmul(x, reshape(weights, (d, 1))), (x.shape[0],)),
+                     tensor(1.0 / scale, dtype=x.dtype))
+        return (plain(scores),)
+
+    return UdfEntry(name, ((column, ColumnType("float")),), 1, body, (), pe_outputs=False)

@@ -1,0 +1,122 @@
+"""Benchmark workloads: seeded synthetic TPC-H-like tables and the reference-API
+restatement of the headline queries.
+
+The queries are written exactly as a user of the reference would write them
+(SQL text + TvfMap UDFs built from tensor ops, because the reference grammar
+has no arithmetic); nothing here is specific to this implementation.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .encodings import DictionaryEncoding, EncodedTensor, StringDictionary, plain, trusted
+from .kernels import UdfEntry, UdfRegistry
+from .storage import FLOAT, STRING, Catalog, table_from_columns, tensor_type
+from .tensor import Tensor, add, mul, sub, tensor
+
+# day numbers since 1970-01-01 (Appendix B)
+D_1992_01_01 = 8035
+D_1994_01_01 = 8766
+D_1995_01_01 = 9131
+D_1995_03_15 = 9204
+D_CURRENT = 9298  # 1995-06-17
+D_Q1_CUTOFF = 10471  # 1998-12-01 - 90 days
+D_1998_12_31 = 10591
+
+RETURNFLAG = StringDictionary(("A", "N", "R"))
+LINESTATUS = StringDictionary(("F", "O"))
+
+LINEITEM_COLUMNS = ("l_shipdate", "l_returnflag", "l_linestatus", "l_quantity",
+                    "l_extendedprice", "l_discount", "l_tax")
+
+
+def lineitem_arrays(sf: float, seed: int = 42, rows: int | None = None) -> dict[str, np.ndarray]:
+    """Appendix B lineitem generator (int64 dates/codes, float64 values)."""
+    n = int(rows if rows is not None else round(6_000_000 * sf))
+    rng = np.random.default_rng(seed)
+    orderdate = rng.integers(D_1992_01_01, 10440 + 1, size=n, dtype=np.int64)
+    shipdate = orderdate + rng.integers(1, 122, size=n, dtype=np.int64)
+    receipt = shipdate + rng.integers(1, 31, size=n, dtype=np.int64)
+    qty = rng.integers(1, 51, size=n).astype(np.float64)
+    partkey = rng.integers(1, int(200_000 * max(sf, 1e-6)) + 1, size=n, dtype=np.int64)
+    retail = (90000 + (partkey // 10) % 20001 + 100 * (partkey % 1000)) / 100.0
+    price = np.round(qty * retail, 2)
+    discount = rng.integers(0, 11, size=n) / 100.0
+    tax = rng.integers(0, 9, size=n) / 100.0
+    ar = rng.integers(0, 2, size=n, dtype=np.int64) * 2  # A=0 or R=2
+    returnflag = np.where(receipt <= D_CURRENT, ar, 1).astype(np.int64)  # else N=1
+    linestatus = (shipdate > D_CURRENT).astype(np.int64)  # O=1 else F=0
+    return {"l_shipdate": shipdate, "l_returnflag": returnflag, "l_linestatus": linestatus,
+            "l_quantity": qty, "l_extendedprice": price, "l_discount": discount, "l_tax": tax}
+
+
+def lineitem_table(arrays: dict, columns=LINEITEM_COLUMNS):
+    """Device table of the given lineitem arrays (numpy or torch)."""
+    cols = []
+    with trusted():
+        for name in columns:
+            v = Tensor(arrays[name])
+            if name == "l_returnflag":
+                cols.append(EncodedTensor(v, DictionaryEncoding(RETURNFLAG)))
+            elif name == "l_linestatus":
+                cols.append(EncodedTensor(v, DictionaryEncoding(LINESTATUS)))
+            else:
+                cols.append(plain(v))
+    return table_from_columns(list(columns), cols)
+
+
+# ---------------------------------------------------------------------------
+# Q6: SUM(extendedprice * discount) over a 3-column range filter
+# ---------------------------------------------------------------------------
+
+Q6_SQL = ("SELECT SUM(rev) FROM (SELECT revenue(l_extendedprice, l_discount) FROM lineitem "
+          "WHERE l_shipdate >= 8766 AND l_shipdate < 9131 AND l_discount >= 0.05 "
+          "AND l_discount <= 0.07 AND l_quantity < 24)")
+
+
+def q6_registry() -> UdfRegistry:
+    reg = UdfRegistry()
+    reg.register(UdfEntry("revenue", (("rev", FLOAT),), 2,
+                          lambda p, d: (plain(mul(p.values, d.values)),), (), pe_outputs=False))
+    return reg
+
+
+# ---------------------------------------------------------------------------
+# Q1: pricing summary, 4 groups x 8 aggregates
+# ---------------------------------------------------------------------------
+
+Q1_SQL = ("SELECT rf, ls, SUM(qty), SUM(price), SUM(disc_price), SUM(charge), AVG(qty), "
+          "AVG(price), AVG(disc), COUNT(*) FROM (SELECT q1prep(l_returnflag, l_linestatus, "
+          "l_quantity, l_extendedprice, l_discount, l_tax) FROM lineitem "
+          "WHERE l_shipdate <= 10471) GROUP BY rf, ls")
+
+
+def _q1prep(rf, ls, q, p, d, t):
+    one = tensor(1.0)
+    dp = mul(p.values, sub(one, d.values))
+    ch = mul(dp, add(one, t.values))
+    return (rf, ls, q, p, plain(dp), plain(ch), d)
+
+
+def q1_registry() -> UdfRegistry:
+    reg = UdfRegistry()
+    reg.register(UdfEntry("q1prep", (("rf", STRING), ("ls", STRING), ("qty", FLOAT),
+                                     ("price", FLOAT), ("disc_price", FLOAT), ("charge", FLOAT),
+                                     ("disc", FLOAT)), 6, _q1prep, (), pe_outputs=False))
+    return reg
+
+
+def compile_sql(sql: str, catalog: Catalog, registry: UdfRegistry, trainable: bool = False):
+    from .compiler import CompileConfig, compile_plan
+    from .sql import bind, lower, parse
+
+    return compile_plan(lower(bind(parse(sql), catalog, registry)),
+                        CompileConfig(trainable=trainable), registry)
+
+
+# algorithmic bytes per row: each referenced base column once at 8 B
+Q1_BYTES_PER_ROW = 56
+Q6_BYTES_PER_ROW = 32

@@ -1,0 +1,157 @@
+"""GPU parity: end-to-end queries through the drop-in API vs the CPU oracle.
+
+Float aggregates: rtol 1e-9 vs the float64 oracle (both accumulate in float64;
+the bound is far tighter than the north-star 1e-5).  Keys / counts / row sets:
+bit-exact.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle.tpch as otpch
+from oracle import relational as orc
+import paper_2211_02753_b200 as tq
+from paper_2211_02753_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+def _run(sql, arrays, registry, columns=wl.LINEITEM_COLUMNS):
+    cat = tq.Catalog()
+    cat.register("lineitem", wl.lineitem_table(arrays, columns))
+    q = wl.compile_sql(sql, cat, registry)
+    return q.run(cat)
+
+
+@pytest.mark.parametrize("rows", [0, 1, 1000, 123_457])
+def test_q6_matches_oracle(rows):
+    arrays = wl.lineitem_arrays(0.01, seed=3, rows=rows)
+    res = _run(wl.Q6_SQL, arrays, wl.q6_registry())
+    got = res.columns[0].values.numpy()
+    exp = otpch.q6(arrays)["sum_rev"]
+    assert got.dtype == exp.dtype == np.float64
+    np.testing.assert_allclose(got, exp, rtol=RTOL, atol=1e-9)
+
+
+@pytest.mark.parametrize("rows", [10, 5000, 200_003])
+def test_q1_matches_oracle(rows):
+    arrays = wl.lineitem_arrays(0.01, seed=5, rows=rows)
+    res = _run(wl.Q1_SQL, arrays, wl.q1_registry())
+    exp = otpch.q1(arrays)
+    names = res.schema.names
+    assert names == ["rf", "ls", "sum_qty", "sum_price", "sum_disc_price", "sum_charge",
+                     "avg_qty", "avg_price", "avg_disc", "count"]
+    cols = {n: c.values.numpy() for n, c in zip(names, res.columns)}
+    np.testing.assert_array_equal(cols["rf"], exp["rf"])
+    np.testing.assert_array_equal(cols["ls"], exp["ls"])
+    np.testing.assert_array_equal(cols["count"], exp["count"])
+    assert cols["count"].dtype == np.int64
+    for n in names[2:9]:
+        assert cols[n].dtype == np.float64
+        np.testing.assert_allclose(cols[n], exp[n], rtol=RTOL)
+    assert res.columns[0].is_dictionary() and res.columns[0].encoding.dictionary == wl.RETURNFLAG
+
+
+def test_filter_materialized_rows_bit_exact():
+    arrays = wl.lineitem_arrays(0.01, seed=7, rows=50_000)
+    res = _run("SELECT * FROM lineitem WHERE l_shipdate >= 9000 AND l_discount < 0.05 "
+               "AND l_returnflag = \"R\"", arrays, tq.UdfRegistry())
+    cols = [arrays[c] for c in wl.LINEITEM_COLUMNS]
+    idx = orc.filter_indices(cols, [(0, ">=", 9000), (5, "<", 0.05), (1, "=", 2)])
+    assert res.row_count == len(idx)
+    for name, col in zip(res.schema.names, res.columns):
+        np.testing.assert_array_equal(col.values.numpy(), arrays[name][idx])
+
+
+def test_absent_dictionary_literal_matches_nothing():
+    arrays = wl.lineitem_arrays(0.01, seed=7, rows=1000)
+    res = _run('SELECT COUNT(*) FROM lineitem WHERE l_returnflag > "Z"', arrays, tq.UdfRegistry())
+    assert res.columns[0].values.numpy().tolist() == [0]
+
+
+def test_group_by_plain_int_key_high_cardinality():
+    rng = np.random.default_rng(11)
+    n = 300_000
+    k = rng.integers(-10**12, 10**12, size=n // 3)
+    key = rng.choice(k, size=n)
+    v = rng.normal(size=n)
+    iv = rng.integers(-1000, 1000, size=n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["k", "v", "iv"], [tq.plain(tq.Tensor(key)),
+                                                               tq.plain(tq.Tensor(v)),
+                                                               tq.plain(tq.Tensor(iv))]))
+    q = wl.compile_sql("SELECT k, SUM(v), AVG(v), SUM(iv), COUNT(*) FROM t GROUP BY k", cat,
+                       tq.UdfRegistry())
+    res = q.run(cat)
+    keys, aggs = orc.groupby_exact([key], [("sum", v), ("avg", v), ("sum", iv), ("count", None)])
+    got = [c.values.numpy() for c in res.columns]
+    np.testing.assert_array_equal(got[0], keys[0])
+    np.testing.assert_allclose(got[1], aggs[0], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(got[2], aggs[1], rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(got[3], aggs[2])
+    np.testing.assert_array_equal(got[4], aggs[3])
+
+
+def test_group_by_two_plain_keys_dense_range():
+    rng = np.random.default_rng(12)
+    n = 100_000
+    a = rng.integers(-5, 40, size=n)
+    b = rng.integers(1000, 1100, size=n)
+    v = rng.integers(0, 10, size=n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["a", "b", "v"], [tq.plain(tq.Tensor(x)) for x in (a, b, v)]))
+    res = wl.compile_sql("SELECT b, a, SUM(v), COUNT(*) FROM t WHERE v > 2 GROUP BY a, b", cat,
+                         tq.UdfRegistry()).run(cat)
+    m = v > 2
+    keys, aggs = orc.groupby_exact([a[m], b[m]], [("sum", v[m]), ("count", None)])
+    got = [c.values.numpy() for c in res.columns]
+    np.testing.assert_array_equal(got[0], keys[1])
+    np.testing.assert_array_equal(got[1], keys[0])
+    np.testing.assert_array_equal(got[2], aggs[0])
+    np.testing.assert_array_equal(got[3], aggs[1])
+
+
+@pytest.mark.parametrize("desc", [False, True])
+@pytest.mark.parametrize("dtype", ["int64", "float64", "float32"])
+def test_sort_limit_stable(desc, dtype):
+    rng = np.random.default_rng(13)
+    n = 70_001
+    if dtype == "int64":
+        key = rng.integers(-50, 50, size=n)
+        key[:3] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max, 0]
+    else:
+        key = rng.integers(-50, 50, size=n).astype(dtype) / 4
+        key[:4] = [np.nan, -0.0, 0.0, np.inf]
+    payload = np.arange(n, dtype=np.int64)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["k", "p"], [tq.plain(tq.Tensor(key)),
+                                                         tq.plain(tq.Tensor(payload))]))
+    d = "DESC" if desc else "ASC"
+    res = wl.compile_sql(f"SELECT * FROM t ORDER BY k {d} LIMIT 1000", cat, tq.UdfRegistry()).run(cat)
+    exp = orc.sort_limit([key, payload], 0, desc, 1000)
+    np.testing.assert_array_equal(res.columns[1].values.numpy(), exp[1])
+    full = orc.stable_order(key, desc)
+    from paper_2211_02753_b200.kernels import stable_order
+
+    got = stable_order(tq.plain(tq.Tensor(key)), desc).cpu().numpy()
+    np.testing.assert_array_equal(got, full)
+
+
+def test_equi_join_matches_oracle_and_nested_loop():
+    from paper_2211_02753_b200.kernels import join_indices
+
+    rng = np.random.default_rng(14)
+    probe = rng.integers(0, 50, size=400)
+    build = rng.integers(0, 50, size=300)
+    pi, bi = join_indices(torch.as_tensor(probe).cuda(), torch.as_tensor(build).cuda())
+    epi, ebi = orc.join_inner(probe, build)
+    npi, nbi = orc.join_nested_loop(probe, build)
+    np.testing.assert_array_equal(epi, npi)
+    np.testing.assert_array_equal(ebi, nbi)
+    np.testing.assert_array_equal(pi.cpu().numpy(), epi)
+    np.testing.assert_array_equal(bi.cpu().numpy(), ebi)

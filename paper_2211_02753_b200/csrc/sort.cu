@@ -186,10 +186,16 @@ struct SortBuffers {
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Scans run over the [256 x tiles] digit counts and (unique) over n flags.
+i64 scan_extent(i64 n) {
+  const i64 ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
+  return ntiles * 256 > n ? ntiles * 256 : n;
+}
+
 size_t sort_ws_bytes(i64 n) {
   const i64 ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
   return 4 * align256((size_t)n * 8) + 2 * align256((size_t)ntiles * 256 * 8) +
-         align256(8 * 256 * 8) + exclusive_scan_workspace(ntiles * 256) + 1024;
+         align256(8 * 256 * 8) + exclusive_scan_workspace(scan_extent(n)) + 1024;
 }
 
 SortBuffers carve(void* ws, i64 n) {
@@ -211,7 +217,7 @@ SortBuffers carve(void* ws, i64 n) {
   b.hist = (unsigned long long*)p;
   p += align256(8 * 256 * 8);
   b.scan_ws = p;
-  b.scan_bytes = exclusive_scan_workspace(ntiles * 256) + 512;
+  b.scan_bytes = exclusive_scan_workspace(scan_extent(n)) + 512;
   return b;
 }
 

@@ -40,6 +40,9 @@ constexpr int kMaxKeys = 8;
 constexpr int kMaxOuts = 16;
 constexpr int kMaxRegCells = 64;
 constexpr i64 kMaxSlots = 1 << 20;
+constexpr int kConsWarps = 8;               // consumer warps of the ring kernel
+constexpr i64 kStageBudget = 64 * 1024;     // max bytes of one ring stage
+constexpr i64 kRingBudget = 200 * 1024;     // bytes of shared memory for the ring
 
 // Must match the TdpParams emitted below, field for field.
 struct HostParams {
@@ -66,6 +69,7 @@ typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, u
                                      unsigned, unsigned, CUstream, void**, void**);
 typedef CUresult (*PFN_Occupancy)(int*, CUfunction, int, size_t);
 typedef CUresult (*PFN_GetErrorString)(CUresult, const char**);
+typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
 
 struct Driver {
   PFN_ModuleLoadData load = nullptr;
@@ -73,6 +77,7 @@ struct Driver {
   PFN_LaunchKernel launch = nullptr;
   PFN_Occupancy occupancy = nullptr;
   PFN_GetErrorString errstr = nullptr;
+  PFN_FuncSetAttribute setattr = nullptr;
   bool ok = false;
 };
 
@@ -90,7 +95,8 @@ int get_driver(Driver** out) {
               q("cuModuleGetFunction", (void**)&d.getfn) &&
               q("cuLaunchKernel", (void**)&d.launch) &&
               q("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occupancy) &&
-              q("cuGetErrorString", (void**)&d.errstr);
+              q("cuGetErrorString", (void**)&d.errstr) &&
+              q("cuFuncSetAttribute", (void**)&d.setattr);
     d.ok = ok;
     if (!ok) err = "driver entry points unavailable";
   });
@@ -315,10 +321,36 @@ void emit_program(std::ostringstream& o, const Spec& s) {
   }
 }
 
+// Shape of the bulk-copy ring for the columns a program reads.
+struct Ring {
+  int pu = 4;            // rows per consumer thread per tile
+  int ptile = 0;         // rows per tile
+  i64 stage_bytes = 0;   // bytes of one ring stage (all columns of one tile)
+  int stages = 0;
+};
+
+Ring ring_shape(const Spec& s) {
+  Ring r;
+  i64 row_bytes = 0;
+  for (int c : s.used_cols) row_bytes += dtype_size(s.col_dtype[c]);
+  if (row_bytes == 0) row_bytes = 1;
+  r.pu = 4;
+  while (r.pu > 1 && (i64)kConsWarps * 32 * r.pu * row_bytes > kStageBudget) r.pu >>= 1;
+  r.ptile = kConsWarps * 32 * r.pu;
+  r.stage_bytes = (i64)r.ptile * row_bytes;
+  i64 st = kRingBudget / r.stage_bytes;
+  r.stages = (int)(st < 2 ? 2 : (st > 8 ? 8 : st));
+  return r;
+}
+
 std::string generate(const Spec& s) {
   std::ostringstream o;
+  const Ring ring = ring_shape(s);
   o << "typedef long long i64;\ntypedef unsigned long long u64;\n";
   o << "#define TDP_THREADS " << kThreads << "\n#define TDP_U " << kUnroll << "\n";
+  o << "#define TDP_CONS_WARPS " << kConsWarps << "\n#define TDP_PU " << ring.pu
+    << "\n#define TDP_PTILE " << ring.ptile << "\n#define TDP_STAGE_BYTES " << ring.stage_bytes
+    << "\n#define TDP_STAGES " << ring.stages << "\n";
   o << "#define TDP_G " << s.slots << "\n#define TDP_NF " << s.fvals.size() << "\n";
   o << "#define TDP_NI " << s.ivals.size() << "\n#define TDP_REGACC " << (s.regacc ? 1 : 0)
     << "\n";
@@ -344,6 +376,26 @@ std::string generate(const Spec& s) {
       o << "  r.c" << c << " = __ldg((const " << T << "*)P.col[" << c << "] + i);\n";
   }
   o << "}\n";
+  // ring stage layout: column tiles back to back, each PTILE elements
+  {
+    std::ostringstream ld, is;
+    i64 off = 0;
+    for (int c : s.used_cols) {
+      const int es = dtype_size(s.col_dtype[c]);
+      const char* T = ctype_of(s.col_dtype[c]);
+      ld << "  r.c" << c << " = ((const " << T << "*)(sb + " << off << "))[lr];\n";
+      is << "  tdp_bulk_load(sb + " << off << "u, (const unsigned char*)P.col[" << c
+         << "] + row0 * " << es << ", " << (i64)ring.ptile * es << "u, bar, policy);\n";
+      off += (i64)ring.ptile * es;
+    }
+    o << "__device__ __forceinline__ void tdp_load_smem(TdpRow& r, const unsigned char* sb, int lr) {\n"
+         "  r.pad_ = 0;\n"
+      << ld.str() << "}\n";
+    o << "__device__ __forceinline__ void tdp_bulk_load(unsigned, const void*, unsigned, unsigned, u64);\n";
+    o << "__device__ __forceinline__ void tdp_issue_tile(const TdpParams& P, unsigned sb, i64 row0, "
+         "unsigned bar, u64 policy) {\n"
+      << is.str() << "}\n";
+  }
   // predicate conjunction + program + keys + aggregate inputs
   o << "__device__ __forceinline__ bool tdp_eval(const TdpRow& r, const TdpParams& P, int& "
        "slot, double* f, i64* q) {\n";
@@ -397,9 +449,13 @@ std::string generate(const Spec& s) {
 // ---------------------------------------------------------------------------
 struct Kernel {
   CUmodule mod = nullptr;
-  CUfunction agg = nullptr;
+  CUfunction agg = nullptr;      // bulk-copy ring kernel
+  CUfunction agg_ldg = nullptr;  // register-staged kernel
   CUfunction proj = nullptr;
   int agg_occ = 1;
+  int ldg_occ = 1;
+  Ring ring;
+  size_t ring_smem = 0;
 };
 
 std::mutex g_cache_mu;
@@ -430,7 +486,7 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   return TDP_OK;
 }
 
-int compile(const std::string& src, std::shared_ptr<Kernel>* out) {
+int compile(const std::string& src, const Ring& ring, std::shared_ptr<Kernel>* out) {
   int dev = 0;
   TDP_CUDA_TRY(cudaGetDevice(&dev));
   {
@@ -453,11 +509,23 @@ int compile(const std::string& src, std::shared_ptr<Kernel>* out) {
   if (rc) return rc;
   rc = cu_check(d, d->getfn(&k->agg, k->mod, "tdp_scan_agg"), "cuModuleGetFunction(agg)");
   if (rc) return rc;
+  rc = cu_check(d, d->getfn(&k->agg_ldg, k->mod, "tdp_scan_agg_ldg"), "cuModuleGetFunction(ldg)");
+  if (rc) return rc;
   rc = cu_check(d, d->getfn(&k->proj, k->mod, "tdp_scan_project"), "cuModuleGetFunction(proj)");
   if (rc) return rc;
+  k->ring = ring;
+  k->ring_smem = (size_t)ring.stages * (size_t)ring.stage_bytes;
+  rc = cu_check(d, d->setattr(k->agg, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                              (int)k->ring_smem),
+                "cuFuncSetAttribute(max dynamic smem)");
+  if (rc) return rc;
   int occ = 1;
-  if (d->occupancy(&occ, k->agg, kThreads, 0) != CUDA_SUCCESS || occ < 1) occ = 1;
+  if (d->occupancy(&occ, k->agg, (kConsWarps + 1) * 32, k->ring_smem) != CUDA_SUCCESS || occ < 1)
+    occ = 1;
   k->agg_occ = occ;
+  occ = 1;
+  if (d->occupancy(&occ, k->agg_ldg, kThreads, 0) != CUDA_SUCCESS || occ < 1) occ = 1;
+  k->ldg_occ = occ;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   g_cache[{dev, src}] = k;
   *out = k;
@@ -728,17 +796,38 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
   TDP_REQUIRE(naggs == 0 || out_sums != nullptr, "null sums output");
   cudaStream_t st = as_stream(stream);
   const i64 cells = cells_of(s);
+  const Ring ring = ring_shape(s);
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), &k);
+  rc = compile(generate(s), ring, &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);
   if (rc) return rc;
-  const i64 tile = (i64)kThreads * kUnroll;
-  i64 grid = ceil_div(n > 0 ? n : 1, tile);
-  const i64 cap = (i64)sm_count() * (s.regacc ? k->agg_occ : 2 * k->agg_occ);
-  if (grid > cap) grid = cap;
-  if (s.regacc && grid > (i64)sm_count() * 32) grid = (i64)sm_count() * 32;
+  // The bulk-copy ring needs 16-byte aligned column bases and at least one
+  // full tile per CTA to be worth its setup; otherwise use the register path.
+  bool aligned = true;
+  for (int c : s.used_cols) aligned &= ((uintptr_t)cols[c].data & 15) == 0;
+  const i64 ntiles = n / ring.ptile;
+  const bool use_ring = aligned && ntiles >= (i64)sm_count();
+  const i64 max_rows = (i64)sm_count() * 32;
+  i64 grid;
+  unsigned threads;
+  size_t smem;
+  CUfunction fn;
+  if (use_ring) {
+    grid = ntiles < (i64)sm_count() * k->agg_occ ? ntiles : (i64)sm_count() * k->agg_occ;
+    threads = (kConsWarps + 1) * 32;
+    smem = k->ring_smem;
+    fn = k->agg;
+  } else {
+    grid = ceil_div(n > 0 ? n : 1, (i64)kThreads * kUnroll);
+    const i64 cap = (i64)sm_count() * (s.regacc ? k->ldg_occ : 2 * k->ldg_occ);
+    if (grid > cap) grid = cap;
+    threads = kThreads;
+    smem = 0;
+    fn = k->agg_ldg;
+  }
+  if (grid > max_rows) grid = max_rows;
   const i64 rows = s.regacc ? grid : 1;
   TDP_REQUIRE(ws != nullptr && ws_bytes >= (size_t)(rows * cells * 8),
               "scan_aggregate workspace too small (%zu < %lld)", ws_bytes,
@@ -750,9 +839,9 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
     hp.acc = ws;
     void* args[] = {&hp};
     rc = cu_check(d,
-                  d->launch(k->agg, (unsigned)grid, 1, 1, kThreads, 1, 1, 0, (CUstream)st, args,
-                            nullptr),
-                  "cuLaunchKernel(tdp_scan_agg)");
+                  d->launch(fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (CUstream)st,
+                            args, nullptr),
+                  use_ring ? "cuLaunchKernel(tdp_scan_agg)" : "cuLaunchKernel(tdp_scan_agg_ldg)");
     if (rc) return rc;
     count_launch();
   }
@@ -780,7 +869,7 @@ int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,
     return TDP_OK;
   }
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), &k);
+  rc = compile(generate(s), ring_shape(s), &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);

@@ -43,6 +43,8 @@ constexpr i64 kMaxSlots = 1 << 20;
 constexpr int kConsWarps = 8;               // consumer warps of the ring kernel
 constexpr i64 kStageBudget = 64 * 1024;     // max bytes of one ring stage
 constexpr i64 kRingBudget = 200 * 1024;     // bytes of shared memory for the ring
+constexpr i64 kMaxSmemCells = 48;           // shared-memory accumulator mode limit
+constexpr int kAccThreads = 256;            // accumulator columns (TDP_ACC_THREADS)
 
 // Must match the TdpParams emitted below, field for field.
 struct HostParams {
@@ -160,7 +162,9 @@ struct Spec {
   std::vector<int> fvals, ivals;  // accumulator -> program value
   std::vector<int> agg_acc;       // agg -> accumulator index (-1 for count)
   i64 slots = 1;
-  bool regacc = true;
+  int accmode = 0;       // 0 registers, 1 shared-memory columns, 2 global atomics
+  bool regacc = true;    // per-CTA partial rows (modes 0 and 1)
+  i64 acc_smem = 0;      // bytes of shared-memory accumulators (mode 1)
 };
 
 int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
@@ -261,7 +265,14 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
       s.used_cols.push_back(c);
     }
   const i64 cells = s.slots * (i64)(1 + s.fvals.size() + s.ivals.size());
-  s.regacc = cells <= kMaxRegCells;
+  // registers when the per-row select-and-add over all slots is cheap, private
+  // shared-memory columns (one add per aggregate per row) for up to
+  // kMaxSmemCells cells, global atomics beyond.
+  if (s.slots == 1 || cells <= 8) s.accmode = 0;
+  else if (cells <= kMaxSmemCells) s.accmode = 1;
+  else s.accmode = 2;
+  s.regacc = s.accmode != 2;
+  s.acc_smem = s.accmode == 1 ? cells * kAccThreads * 8 : 0;
   return TDP_OK;
 }
 
@@ -335,10 +346,11 @@ Ring ring_shape(const Spec& s) {
   for (int c : s.used_cols) row_bytes += dtype_size(s.col_dtype[c]);
   if (row_bytes == 0) row_bytes = 1;
   r.pu = 4;
-  while (r.pu > 1 && (i64)kConsWarps * 32 * r.pu * row_bytes > kStageBudget) r.pu >>= 1;
+  const i64 budget = kRingBudget - s.acc_smem;
+  while (r.pu > 1 && (i64)kConsWarps * 32 * r.pu * row_bytes * 4 > budget) r.pu >>= 1;
   r.ptile = kConsWarps * 32 * r.pu;
   r.stage_bytes = (i64)r.ptile * row_bytes;
-  i64 st = kRingBudget / r.stage_bytes;
+  i64 st = (kRingBudget - s.acc_smem) / r.stage_bytes;
   r.stages = (int)(st < 2 ? 2 : (st > 8 ? 8 : st));
   return r;
 }
@@ -352,7 +364,7 @@ std::string generate(const Spec& s) {
     << "\n#define TDP_PTILE " << ring.ptile << "\n#define TDP_STAGE_BYTES " << ring.stage_bytes
     << "\n#define TDP_STAGES " << ring.stages << "\n";
   o << "#define TDP_G " << s.slots << "\n#define TDP_NF " << s.fvals.size() << "\n";
-  o << "#define TDP_NI " << s.ivals.size() << "\n#define TDP_REGACC " << (s.regacc ? 1 : 0)
+  o << "#define TDP_NI " << s.ivals.size() << "\n#define TDP_ACCMODE " << s.accmode
     << "\n";
   o << "#define TDP_FTILE " << kFilterTile << "\n#define TDP_FWORDS " << kFilterWords << "\n";
   o << "struct TdpParams {\n  const void* col[" << kMaxCols << "];\n  void* out[" << kMaxOuts
@@ -455,7 +467,8 @@ struct Kernel {
   int agg_occ = 1;
   int ldg_occ = 1;
   Ring ring;
-  size_t ring_smem = 0;
+  size_t ring_smem = 0;   // ring + accumulators
+  size_t ldg_smem = 0;    // accumulators
 };
 
 std::mutex g_cache_mu;
@@ -486,7 +499,7 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   return TDP_OK;
 }
 
-int compile(const std::string& src, const Ring& ring, std::shared_ptr<Kernel>* out) {
+int compile(const std::string& src, const Ring& ring, i64 acc_smem, std::shared_ptr<Kernel>* out) {
   int dev = 0;
   TDP_CUDA_TRY(cudaGetDevice(&dev));
   {
@@ -514,17 +527,22 @@ int compile(const std::string& src, const Ring& ring, std::shared_ptr<Kernel>* o
   rc = cu_check(d, d->getfn(&k->proj, k->mod, "tdp_scan_project"), "cuModuleGetFunction(proj)");
   if (rc) return rc;
   k->ring = ring;
-  k->ring_smem = (size_t)ring.stages * (size_t)ring.stage_bytes;
+  k->ring_smem = (size_t)ring.stages * (size_t)ring.stage_bytes + (size_t)acc_smem;
+  k->ldg_smem = (size_t)acc_smem;
   rc = cu_check(d, d->setattr(k->agg, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                               (int)k->ring_smem),
                 "cuFuncSetAttribute(max dynamic smem)");
+  if (rc) return rc;
+  rc = cu_check(d, d->setattr(k->agg_ldg, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                              (int)k->ldg_smem),
+                "cuFuncSetAttribute(max dynamic smem, ldg)");
   if (rc) return rc;
   int occ = 1;
   if (d->occupancy(&occ, k->agg, (kConsWarps + 1) * 32, k->ring_smem) != CUDA_SUCCESS || occ < 1)
     occ = 1;
   k->agg_occ = occ;
   occ = 1;
-  if (d->occupancy(&occ, k->agg_ldg, kThreads, 0) != CUDA_SUCCESS || occ < 1) occ = 1;
+  if (d->occupancy(&occ, k->agg_ldg, kThreads, k->ldg_smem) != CUDA_SUCCESS || occ < 1) occ = 1;
   k->ldg_occ = occ;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   g_cache[{dev, src}] = k;
@@ -798,7 +816,7 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
   const i64 cells = cells_of(s);
   const Ring ring = ring_shape(s);
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), ring, &k);
+  rc = compile(generate(s), ring, s.acc_smem, &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);
@@ -824,7 +842,7 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
     const i64 cap = (i64)sm_count() * (s.regacc ? k->ldg_occ : 2 * k->ldg_occ);
     if (grid > cap) grid = cap;
     threads = kThreads;
-    smem = 0;
+    smem = k->ldg_smem;
     fn = k->agg_ldg;
   }
   if (grid > max_rows) grid = max_rows;
@@ -869,7 +887,7 @@ int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,
     return TDP_OK;
   }
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), ring_shape(s), &k);
+  rc = compile(generate(s), ring_shape(s), s.acc_smem, &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);

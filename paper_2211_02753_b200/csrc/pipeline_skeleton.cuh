@@ -37,13 +37,25 @@ __device__ __forceinline__ T tdp_warp_sum(T v) {
   return v;
 }
 
+// TDP_ACCMODE 0: registers, 1: per-thread columns in shared memory, 2: global atomics
+#define TDP_REGACC (TDP_ACCMODE == 0)
+#define TDP_SMEMACC (TDP_ACCMODE == 1)
+#define TDP_ACC_THREADS 256  // shared-memory accumulator columns (one per thread)
+
 struct TdpAcc {
 #if TDP_REGACC
   i64 cnt[TDP_G];
   double af[TDP_G][TDP_NFA];
   i64 ai[TDP_G][TDP_NIA];
 #endif
-  __device__ __forceinline__ void zero() {
+#if TDP_SMEMACC
+  // cell-major [TDP_CELLS][TDP_ACC_THREADS]: a thread touches only its own
+  // column, so updates need no atomics and consecutive threads hit
+  // consecutive 8-byte words (conflict-free).
+  u64* sm;
+  int col;
+#endif
+  __device__ __forceinline__ void zero(u64* smem_acc) {
 #if TDP_REGACC
 #pragma unroll
     for (int s = 0; s < TDP_G; ++s) {
@@ -53,6 +65,12 @@ struct TdpAcc {
 #pragma unroll
       for (int a = 0; a < TDP_NIA; ++a) ai[s][a] = 0;
     }
+#endif
+#if TDP_SMEMACC
+    sm = smem_acc;
+    col = threadIdx.x;
+    if (col < TDP_ACC_THREADS)
+      for (int c = 0; c < TDP_CELLS; ++c) sm[c * TDP_ACC_THREADS + col] = 0;
 #endif
   }
   __device__ __forceinline__ void add(const TdpParams& P, bool keep, int slot, const double* f,
@@ -66,6 +84,18 @@ struct TdpAcc {
       for (int a = 0; a < TDP_NF; ++a) af[s][a] += hit ? f[a] : 0.0;
 #pragma unroll
       for (int a = 0; a < TDP_NI; ++a) ai[s][a] = (i64)((u64)ai[s][a] + (hit ? (u64)q[a] : 0ull));
+    }
+#elif TDP_SMEMACC
+    if (keep) {
+      u64* p = sm + (size_t)slot * TDP_ACC_THREADS + col;
+      p[0] += 1ull;
+#pragma unroll
+      for (int a = 0; a < TDP_NF; ++a) {
+        double* d = reinterpret_cast<double*>(p + (size_t)TDP_G * (1 + a) * TDP_ACC_THREADS);
+        *d += f[a];
+      }
+#pragma unroll
+      for (int a = 0; a < TDP_NI; ++a) p[(size_t)TDP_G * (1 + TDP_NF + a) * TDP_ACC_THREADS] += (u64)q[a];
     }
 #else
     if (keep) {
@@ -121,19 +151,41 @@ struct TdpAcc {
         out[c] = v;
       }
     }
+#elif TDP_SMEMACC
+    __syncthreads();
+    u64* out = reinterpret_cast<u64*>(P.acc) + (i64)blockIdx.x * TDP_CELLS;
+    for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {
+      const u64* row = sm + (size_t)c * TDP_ACC_THREADS;
+      if (c >= TDP_G && c < TDP_G * (1 + TDP_NF)) {
+        double v = 0.0;
+        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += __longlong_as_double((i64)row[t]);
+        out[c] = (u64)__double_as_longlong(v);
+      } else {
+        u64 v = 0;
+        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];
+        out[c] = v;
+      }
+    }
 #endif
   }
 };
+
+#if TDP_SMEMACC
+#define TDP_ACC_SMEM_BYTES (TDP_CELLS * TDP_ACC_THREADS * 8)
+#else
+#define TDP_ACC_SMEM_BYTES 0
+#endif
 
 // ---------------------------------------------------------------------------
 // register-staged path
 // ---------------------------------------------------------------------------
 extern "C" __global__ void __launch_bounds__(TDP_THREADS)
     tdp_scan_agg_ldg(const __grid_constant__ TdpParams P) {
+  extern __shared__ __align__(128) unsigned char tdp_dyn[];
   const i64 tile = (i64)TDP_THREADS * TDP_U;
   const i64 step = (i64)gridDim.x * tile;
   TdpAcc acc;
-  acc.zero();
+  acc.zero(reinterpret_cast<u64*>(tdp_dyn));
   for (i64 base = (i64)blockIdx.x * tile; base < P.n; base += step) {
     TdpRow r[TDP_U];
 #pragma unroll
@@ -206,7 +258,7 @@ extern "C" __global__ void __launch_bounds__(TDP_PTHREADS)
   }
   __syncthreads();
   TdpAcc acc;
-  acc.zero();
+  acc.zero(reinterpret_cast<u64*>(tdp_ring + (size_t)TDP_STAGES * TDP_STAGE_BYTES));
   if (warp == TDP_CONS_WARPS) {
     // ---- producer: one elected lane streams tiles into the ring ----------
     if (lane == 0) {

@@ -499,12 +499,39 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   return TDP_OK;
 }
 
-int compile(const std::string& src, const Ring& ring, i64 acc_smem, std::shared_ptr<Kernel>* out) {
+// Everything the generated source depends on (literals and constants are
+// kernel parameters), as a compact cache key; the source is only generated on
+// a miss.
+std::string signature(const Spec& s) {
+  std::string k;
+  auto put = [&k](long long v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof(v));
+  };
+  put((long long)s.col_dtype.size());
+  for (int d : s.col_dtype) put(d);
+  put((long long)s.preds.size());
+  for (const auto& p : s.preds) put(((long long)p.column << 16) | (p.op << 8) | p.cmp);
+  put((long long)s.prog.size());
+  for (const auto& in : s.prog) put(((long long)in.op << 48) ^ ((long long)in.dtype << 40) ^ ((long long)in.a << 20) ^ in.b);
+  put((long long)s.keys.size());
+  for (const auto& kk : s.keys) {
+    put(kk.value);
+    put(kk.span);
+  }
+  put((long long)s.aggs.size());
+  for (const auto& a : s.aggs) put(((long long)a.kind << 32) | (unsigned)a.value);
+  put((long long)s.outs.size());
+  for (int o : s.outs) put(o);
+  return k;
+}
+
+int compile(const Spec& s, const Ring& ring, i64 acc_smem, std::shared_ptr<Kernel>* out) {
   int dev = 0;
   TDP_CUDA_TRY(cudaGetDevice(&dev));
+  const std::string key = signature(s);
   {
     std::lock_guard<std::mutex> lock(g_cache_mu);
-    auto it = g_cache.find({dev, src});
+    auto it = g_cache.find({dev, key});
     if (it != g_cache.end()) {
       *out = it->second;
       return TDP_OK;
@@ -513,6 +540,7 @@ int compile(const std::string& src, const Ring& ring, i64 acc_smem, std::shared_
   Driver* d = nullptr;
   int rc = get_driver(&d);
   if (rc) return rc;
+  const std::string src = generate(s);
   std::vector<char> cubin;
   rc = nvrtc_compile(src, &cubin);
   if (rc) return rc;
@@ -545,7 +573,7 @@ int compile(const std::string& src, const Ring& ring, i64 acc_smem, std::shared_
   if (d->occupancy(&occ, k->agg_ldg, kThreads, k->ldg_smem) != CUDA_SUCCESS || occ < 1) occ = 1;
   k->ldg_occ = occ;
   std::lock_guard<std::mutex> lock(g_cache_mu);
-  g_cache[{dev, src}] = k;
+  g_cache[{dev, key}] = k;
   *out = k;
   return TDP_OK;
 }
@@ -816,7 +844,7 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
   const i64 cells = cells_of(s);
   const Ring ring = ring_shape(s);
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), ring, s.acc_smem, &k);
+  rc = compile(s, ring, s.acc_smem, &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);
@@ -887,7 +915,7 @@ int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,
     return TDP_OK;
   }
   std::shared_ptr<Kernel> k;
-  rc = compile(generate(s), ring_shape(s), s.acc_smem, &k);
+  rc = compile(s, ring_shape(s), s.acc_smem, &k);
   if (rc) return rc;
   Driver* d = nullptr;
   rc = get_driver(&d);

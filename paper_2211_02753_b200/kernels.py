@@ -305,16 +305,20 @@ def _scan_aggregate(exprs_keys: Sequence[Expr], spans: Sequence[tuple[int, int]]
     for _, span in spans:
         slots *= span
     nat.require_cuda(*prog.cols)
-    counts = torch.empty(slots, dtype=torch.int64, device=device)
-    sums = torch.empty((max(1, len(aggs)), slots), dtype=torch.int64, device=device)
-    ws = nat.workspace(nat.load().tdp_scan_aggregate_workspace(n, slots, len(aggs)), device)
+    # one allocation: counts [slots] | sums [naggs, slots] | workspace
+    na = max(1, len(aggs))
+    ws_words = (int(nat.load().tdp_scan_aggregate_workspace(n, slots, len(aggs))) + 7) // 8
+    buf = torch.empty(slots * (1 + na) + ws_words, dtype=torch.int64, device=device)
+    counts = buf[:slots]
+    sums = buf[slots:slots * (1 + na)].view(na, slots)
+    ws = buf[slots * (1 + na):]
     hook = PROFILE_HOOK
     if hook is not None:
         hook.begin("tdp_scan_aggregate", n)
     nat.call("tdp_scan_aggregate", prog.native_columns(), len(prog.cols), n, preds, npreds,
              prog.native_instrs(), len(prog.instrs), nat.struct_array(nat.Key, keys), len(keys),
              nat.struct_array(nat.Agg, agg_structs), len(agg_structs), nat.ptr(counts),
-             nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
+             nat.ptr(sums), nat.ptr(ws), ws.numel() * 8, nat.stream())
     if hook is not None:
         hook.end("tdp_scan_aggregate")
     return counts, sums, slots
@@ -329,10 +333,12 @@ def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device):
     nkeys = len(spans)
     keys = nat.struct_array(nat.Key, [nat.Key(0, 0, lo, span) for lo, span in spans])
     aggs = nat.struct_array(nat.Agg, [nat.Agg(k, 0) for k in aggs_kinds])
-    out_keys = torch.empty((max(1, nkeys), slots), dtype=torch.int64, device=device)
-    out_counts = torch.empty(slots, dtype=torch.int64, device=device)
-    out_aggs = torch.empty((max(1, len(aggs_kinds)), slots), dtype=torch.int64, device=device)
-    out_groups = torch.empty(1, dtype=torch.int64, device=device)
+    nk, na = max(1, nkeys), max(1, len(aggs_kinds))
+    buf = torch.empty((nk + 1 + na) * slots + 1, dtype=torch.int64, device=device)
+    out_keys = buf[:nk * slots].view(nk, slots)
+    out_counts = buf[nk * slots:(nk + 1) * slots]
+    out_aggs = buf[(nk + 1) * slots:(nk + 1 + na) * slots].view(na, slots)
+    out_groups = buf[(nk + 1 + na) * slots:]
     nat.call("tdp_groupby_finalize", nat.ptr(counts), nat.ptr(sums), slots, keys, nkeys, aggs,
              len(aggs_kinds), avg_mask, nat.ptr(out_keys), nat.ptr(out_counts), nat.ptr(out_aggs),
              nat.ptr(out_groups), nat.stream())
@@ -342,20 +348,21 @@ def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device):
 
 def _agg_outputs(aggs: Sequence[tuple[str, str]], raw: torch.Tensor, counts: torch.Tensor,
                  already_avg: bool) -> list[torch.Tensor]:
-    """Typed aggregate columns from raw 8-byte results."""
+    """Typed aggregate columns from raw 8-byte results (views, no copies:
+    result columns are immutable)."""
     out = []
     for a, (func, dt) in enumerate(aggs):
-        r = raw[a].contiguous()
+        r = raw[a]
         if func == "count":
-            out.append(r.clone())
+            out.append(r)
         elif func == "avg":
             if already_avg:
-                out.append(r.view(torch.float64).clone())
+                out.append(r.view(torch.float64))
             else:
                 s = r.view(torch.float64) if dt in FLOAT_DTYPES else r.to(torch.float64)
                 out.append(s / counts.to(torch.float64))
         else:
-            out.append(r.view(torch.float64).clone() if dt in FLOAT_DTYPES else r.clone())
+            out.append(r.view(torch.float64) if dt in FLOAT_DTYPES else r)
     return out
 
 

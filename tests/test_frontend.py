@@ -179,6 +179,8 @@ def test_pipeline_codegen_compiles_q1_program_with_nvrtc():
         _native.struct_array(_native.Agg, aggs), len(aggs), None, 0, 1, buf, len(buf))
     assert rc > 0, _native.last_error()
     src = buf.value.decode()
-    assert "#define TDP_G 6" in src and "#define TDP_NF 5" in src and "#define TDP_REGACC 1" in src
+    assert "#define TDP_G 6" in src and "#define TDP_NF 5" in src
+    assert "#define TDP_ACCMODE 1" in src  # 36 cells -> shared-memory accumulator columns
+    assert "tdp_bulk_load(sb + 0u" in src  # column tiles stream through the bulk-copy ring
     # the UDF's (1 - d) and (1 + t) become SSA values; (1.0) is shared (CSE)
     assert src.count("P.imf[") == 2  # once in tdp_eval, once in tdp_project

@@ -43,7 +43,8 @@ def _args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--query", choices=("q1", "q6"), default="q1")
+    ap.add_argument("--query", choices=("q1", "q6", "llp"), default="q1")
+    ap.add_argument("--llp-rows", type=int, default=100_000_000)
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -447,8 +448,97 @@ def _merge(query, parts):
     return out
 
 
+# ---------------------------------------------------------------------------
+# LLP trainable step (SURVEY config 4) -- extra measurement, not the headline
+# ---------------------------------------------------------------------------
+
+def _llp(args):
+    import numpy as np
+    import torch
+
+    import paper_2211_02753_b200 as tq
+    from paper_2211_02753_b200 import _native
+    from paper_2211_02753_b200.storage import tensor_type
+    from paper_2211_02753_b200.training import AdamState, TrainConfig, train_step
+
+    torch.cuda.set_device(0)
+    n, d, bags = args.llp_rows, 64, 1000
+    g = torch.Generator(device="cuda").manual_seed(0)
+    X = torch.randn(n, d, generator=g, device="cuda", dtype=torch.float32)
+    bag = torch.randint(0, bags, (n,), generator=g, device="cuda", dtype=torch.int64)
+    Wstar = torch.randn(d, 2, generator=g, device="cuda", dtype=torch.float32)
+    labels = torch.argmax(X @ Wstar, dim=1)
+    target = torch.zeros(bags * 2, dtype=torch.float64, device="cuda")
+    target.index_add_(0, bag * 2 + labels, torch.ones(n, dtype=torch.float64, device="cuda"))
+    del labels
+    model = tq.Linear(d, 2, np.random.default_rng(0), name="lin")
+    bag_pe = tq.one_hot_pe(bag, bags)
+    reg = tq.UdfRegistry()
+    reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(2))), 1,
+                             lambda c: (bag_pe, tq.pe_encode(model(c.values))), model.parameters))
+    cat = tq.Catalog()
+    Xt = tq.Tensor(X)
+    cat.register_tensor(Xt, "T")
+    q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
+        "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"), cat, reg)),
+        tq.CompileConfig(trainable=True), reg)
+    params = q.parameters()
+    cfg = TrainConfig(iterations=1, lr=0.01)
+    state = AdamState.for_params(params)
+    tgt = tq.Tensor(target)
+    losses = []
+    for _ in range(max(args.warmup, 3)):
+        losses.append(train_step(q, cat, "T", Xt, tgt, params, cfg, state))
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 20))
+    t0.record()
+    for _ in range(steps):
+        losses.append(train_step(q, cat, "T", Xt, tgt, params, cfg, state))
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    launches = _native.launch_count() - launches0
+    # CPU baseline: the closed-form oracle of the reference's step, one core
+    from oracle import relational as orc
+
+    m = 100_000
+    Xh = X[:m].double().cpu().numpy()
+    bh = bag[:m].cpu().numpy()
+    Wh = model.weight.value.numpy().astype(np.float64)
+    bb = model.bias.value.numpy().astype(np.float64)
+    th = np.zeros(bags * 2)
+    w0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - w0 < 5.0:
+        orc.llp_forward_backward(Xh, bh, Wh, bb, th, bags)
+        reps += 1
+    cpu_s = (time.perf_counter() - w0) / reps
+    line = {
+        "metric": "LLP trainable query step latency (SURVEY config 4)",
+        "value": ms, "unit": "ms/step", "higher_is_better": False, "n_gpus": 1,
+        "steps": steps, "warmup": max(args.warmup, 3), "rows_per_s": n / (ms / 1e3),
+        "dtype": "f32 model, f64 grid", "data": "synthetic X ~ N(0,1), bags ~ U{0..999}",
+        "config": {"workload": f"SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred "
+                               f"(trainable), Linear({d},2) -> pe_encode, one_hot_pe bag, MSE, Adam",
+                   "rows": n, "features": d, "bags": bags},
+        "gpu_launches": launches, "losses": losses[:3] + losses[-2:],
+        "cpu_baseline": {"value": cpu_s / m * n * 1e3, "unit": "ms/step (linear extrapolation)",
+                         "cores": 1, "kind": "port",
+                         "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
+                                   f"reference tape), {reps} reps, extrapolated to {n} rows"},
+        "bytes_floor_ms": 528 * n / 6449.4e9 * 1e3,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = _args()
+    if args.query == "llp":
+        _llp(args)
+        return
     if args.impl == "reference":
         _reference(args)
     else:

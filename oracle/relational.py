@@ -244,6 +244,27 @@ def soft_groupby_vjp(pes: Sequence[np.ndarray], grid_grad: np.ndarray,
     return grads, (dw if values is not None else None)
 
 
+def llp_forward_backward(X: np.ndarray, bag: np.ndarray, W: np.ndarray, b: np.ndarray,
+                         target: np.ndarray, bags: int):
+    """One trainable LLP query step (SURVEY Appendix A llp TVF) in closed form:
+    Linear -> softmax (tq/tensor.py:515) -> soft group-by-count over
+    (one-hot bag, PE pred) (tq/kernels.py:212-223) -> MSE (tq/training.py:68-73)
+    and the gradient w.r.t. W, b that the reference's tape produces.
+    Returns (loss, grid[bags*k], dW, db)."""
+    logits = X @ W + b
+    P = softmax(logits)
+    k = P.shape[1]
+    grid = np.zeros((bags, k), dtype=np.result_type(P.dtype, np.float64))
+    np.add.at(grid, bag, P)
+    g = grid.reshape(-1)
+    diff = g - target
+    loss = float(np.mean(diff * diff))
+    dgrid = (2.0 * diff / diff.size).reshape(bags, k)
+    dP = dgrid[bag]
+    dZ = softmax_vjp(P, dP)
+    return loss, g, X.T @ dZ, dZ.sum(axis=0)
+
+
 # ---------------------------------------------------------------------------
 # equi-join (builder-defined: the reference has none, SURVEY §8 A20)
 # ---------------------------------------------------------------------------

@@ -250,6 +250,54 @@ for qname, sql, reg in (("q1", wl.Q1_SQL, ref_q1_registry()), ("q6", wl.Q6_SQL, 
     for nm, col in zip(out.schema.names, out.columns):
         put(f"tpch/{qname}/{nm}", col.values.data)
 
+# ---------------------------------------------------------------------------
+# LLP: trainable soft group-by-count through the reference's own train()
+# (SURVEY Appendix A llp TVF; float64 model for parity)
+# ---------------------------------------------------------------------------
+from tensorquery.storage import tensor_type  # noqa: E402
+
+llp_rng = np.random.default_rng(77)
+n_llp, d_llp, bags = 3000, 8, 25
+X = llp_rng.normal(size=(n_llp, d_llp))
+bag = llp_rng.integers(0, bags, size=n_llp)
+Wstar = llp_rng.normal(size=(d_llp, 2))
+labels = np.argmax(X @ Wstar, axis=1)
+target = np.zeros((bags, 2))
+np.add.at(target, (bag, labels), 1.0)
+put("llp/X", X)
+put("llp/bag", bag)
+put("llp/target", target.reshape(-1))
+model = ref.Linear(d_llp, 2, np.random.default_rng(5), name="lin", dtype="float64")
+put("llp/W0", model.weight.value.data.copy())
+reg = ref.UdfRegistry()
+reg.register(ref.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(2))), 1,
+                          lambda c: (ref.one_hot_pe(bag, bags), ref.pe_encode(model(c.values))),
+                          model.parameters))
+cat = ref.Catalog()
+cat.register_tensor(Tensor(X), "T")
+sql = "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"
+plan = ref.lower(ref.bind(ref.parse(sql), cat, reg))
+q = ref.compile_plan(plan, ref.CompileConfig(trainable=True), reg)
+meta["plans"]["llp"] = {"explain": ref.explain(plan), "compiled": q.explain_compiled(),
+                        "exact": q.swap_to_exact().explain_compiled()}
+losses = ref.train(q, cat, [("T", Tensor(X), Tensor(target.reshape(-1)))],
+                   ref.TrainConfig(iterations=4, lr=0.05))
+put("llp/losses", np.array(losses))
+put("llp/W4", model.weight.value.data.copy())
+put("llp/b4", model.bias.value.data.copy())
+# one more forward + gradient at the trained weights
+res = q.run(cat)
+pred = res.columns[2].values
+loss = ref.mse_loss(pred, Tensor(target.reshape(-1)))
+backward(loss)
+put("llp/grid5", pred.data)
+put("llp/dW5", q.tape.gradient(model.weight.value).data)
+put("llp/db5", q.tape.gradient(model.bias.value).data)
+q.end_session()
+exact = q.swap_to_exact().run(cat)
+for nm, col in zip(exact.schema.names, exact.columns):
+    put(f"llp/exact/{nm}", col.values.data)
+
 np.savez_compressed(HERE / "golden.npz", **arrays)
 (HERE / "golden.json").write_text(json.dumps(meta, indent=1, default=float))
 print(f"wrote {len(arrays)} arrays")

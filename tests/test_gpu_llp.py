@@ -1,0 +1,81 @@
+"""GPU parity of the trainable LLP query (SURVEY config 4 shape, small n)
+against golden values from the reference's own train() loop.
+
+Tolerance: rtol 1e-5 for losses, weights and gradients (north-star LLP
+tolerance); exact-swap keys and counts bit-exact.
+"""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2211_02753_b200 as tq
+from paper_2211_02753_b200.storage import tensor_type
+
+pytestmark = pytest.mark.gpu
+
+G = Path(__file__).resolve().parent / "golden"
+A = np.load(G / "golden.npz")
+META = json.loads((G / "golden.json").read_text())
+BAGS = 25
+
+
+def _setup():
+    X, bag, target = A["llp/X"], A["llp/bag"], A["llp/target"]
+    model = tq.Linear(X.shape[1], 2, np.random.default_rng(5), name="lin", dtype="float64")
+    np.testing.assert_array_equal(model.weight.value.numpy(), A["llp/W0"])
+    bag_pe = tq.one_hot_pe(bag, BAGS)
+    reg = tq.UdfRegistry()
+    reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(BAGS)), ("Pred", tensor_type(2))), 1,
+                             lambda c: (bag_pe, tq.pe_encode(model(c.values))), model.parameters))
+    cat = tq.Catalog()
+    cat.register_tensor(tq.Tensor(X), "T")
+    plan = tq.lower(tq.bind(tq.parse("SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"),
+                            cat, reg))
+    q = tq.compile_plan(plan, tq.CompileConfig(trainable=True), reg)
+    return X, target, model, cat, q, plan
+
+
+def test_llp_train_matches_reference():
+    X, target, model, cat, q, plan = _setup()
+    assert tq.explain(plan) == META["plans"]["llp"]["explain"]
+    assert q.explain_compiled() == META["plans"]["llp"]["compiled"]
+    assert q.swap_to_exact().explain_compiled() == META["plans"]["llp"]["exact"]
+    losses = tq.train(q, cat, [("T", tq.Tensor(X), tq.Tensor(target))],
+                      tq.TrainConfig(iterations=4, lr=0.05))
+    np.testing.assert_allclose(losses, A["llp/losses"], rtol=1e-5)
+    np.testing.assert_allclose(model.weight.value.numpy(), A["llp/W4"], rtol=1e-5, atol=1e-8)
+    np.testing.assert_allclose(model.bias.value.numpy(), A["llp/b4"], rtol=1e-5, atol=1e-8)
+    res = q.run(cat)
+    pred = res.columns[2].values
+    loss = tq.mse_loss(pred, tq.Tensor(target))
+    tq.backward(loss)
+    np.testing.assert_allclose(pred.numpy(), A["llp/grid5"], rtol=1e-5)
+    np.testing.assert_allclose(q.tape.gradient(model.weight.value).numpy(), A["llp/dW5"],
+                               rtol=1e-5, atol=1e-9)
+    np.testing.assert_allclose(q.tape.gradient(model.bias.value).numpy(), A["llp/db5"],
+                               rtol=1e-5, atol=1e-9)
+    q.end_session()
+    exact = q.swap_to_exact().run(cat)
+    for nm, col in zip(exact.schema.names, exact.columns):
+        np.testing.assert_array_equal(col.values.numpy(), A[f"llp/exact/{nm}"])
+
+
+def test_soft_counts_conserve_mass_and_gradient_of_total_is_zero():
+    rng = np.random.default_rng(3)
+    logits = rng.normal(size=(4000, 3))
+    with tq.Tape() as tape:
+        x = tq.Tensor(logits)
+        pe = tq.pe_encode(x)
+        c = tq.soft_count(pe)
+        from paper_2211_02753_b200.tensor import reduce_sum
+
+        total = reduce_sum(c)
+        tq.backward(total)
+        g = tape.gradient(x).numpy()
+    assert abs(float(total.item()) - 4000.0) < 1e-6
+    assert np.max(np.abs(g)) < 1e-6

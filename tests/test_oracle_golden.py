@@ -118,6 +118,15 @@ def test_tpch_end_to_end():
     np.testing.assert_allclose(q6["sum_rev"], A["tpch/q6/sum_rev"], rtol=1e-12)
 
 
+def test_llp_closed_form_matches_reference_tape():
+    X, bag, target = A["llp/X"], A["llp/bag"], A["llp/target"]
+    W, b = A["llp/W4"], A["llp/b4"]
+    loss, grid, dW, db = orc.llp_forward_backward(X, bag, W, b, target, 25)
+    np.testing.assert_allclose(grid, A["llp/grid5"], rtol=1e-12)
+    np.testing.assert_allclose(dW, A["llp/dW5"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(db, A["llp/db5"], rtol=1e-10, atol=1e-14)
+
+
 def test_join_oracle_vs_nested_loop():
     rng = np.random.default_rng(5)
     for _ in range(20):

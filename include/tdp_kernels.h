@@ -331,6 +331,20 @@ int tdp_soft_groupby_bwd(const tdp_soft_key* keys, int32_t nkeys, int64_t n, con
                          int32_t values_dtype, const double* grad_grid, void* const* grad_keys,
                          void* grad_values, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* skinny dense layers of models embedded in trainable queries              */
+/* ------------------------------------------------------------------------ */
+/* Y[n,k] = X[n,d] W[d,k] (+ bias[k]); 1 <= d <= 256, 1 <= k <= 8, float32 /
+ * float64, float64 accumulation.  Replaces matmul (tq/tensor.py:437-447) for
+ * the tall-skinny products of Linear (tq/models.py:26-27).                 */
+int tdp_linear_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k, const void* W,
+                   const void* bias, void* Y, void* stream);
+size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k);
+/* dW = X^T G, db = column sums of G (db may be NULL): the matmul VJP w.r.t.
+ * the weight (tq/tensor.py:452) and of the bias add (:337-338).          */
+int tdp_linear_wgrad(const void* X, const void* G, int32_t dtype, int64_t n, int32_t d, int32_t k,
+                     void* dW, void* db, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -125,6 +125,11 @@ _SIGNATURES = {
                                      c_void_p, c_void_p]),
     "tdp_soft_groupby_bwd": (c_int, [POINTER(SoftKey), c_int32, c_int64, c_void_p, c_int32,
                                      c_void_p, POINTER(c_void_p), c_void_p, c_void_p]),
+    "tdp_linear_fwd": (c_int, [c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p,
+                               c_void_p, c_void_p]),
+    "tdp_linear_wgrad_workspace": (c_size_t, [c_int64, c_int32, c_int32]),
+    "tdp_linear_wgrad": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p,
+                                 c_void_p, c_void_p, c_size_t, c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -103,6 +103,57 @@ def gather_rows(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
 
 
 # ---------------------------------------------------------------------------
+# skinny linear layer (matmul with few output columns)
+# ---------------------------------------------------------------------------
+
+LINEAR_MAX_K = 8
+LINEAR_MAX_D = 256
+LINEAR_MIN_ROWS = 1 << 14
+
+
+def linear_eligible(a: torch.Tensor, b: torch.Tensor) -> bool:
+    """Tall-skinny products the streaming kernels handle (else cuBLAS)."""
+    return (a.is_cuda and b.is_cuda and a.dim() == 2 and b.dim() == 2
+            and a.dtype == b.dtype and a.dtype in (torch.float32, torch.float64)
+            and 1 <= b.shape[1] <= LINEAR_MAX_K and 1 <= a.shape[1] <= LINEAR_MAX_D
+            and a.shape[0] >= LINEAR_MIN_ROWS)
+
+
+class _SkinnyLinear(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        x = x.contiguous()
+        w = w.contiguous()
+        n, d = x.shape
+        k = w.shape[1]
+        y = torch.empty((n, k), dtype=x.dtype, device=x.device)
+        nat.call("tdp_linear_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), c_void_p(0),
+                 nat.ptr(y), nat.stream())
+        ctx.save_for_backward(x, w)
+        return y
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        x, w = ctx.saved_tensors
+        g = g.contiguous().to(x.dtype)
+        n, d = x.shape
+        k = w.shape[1]
+        dx = dw = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.matmul(g, w.t())
+        if ctx.needs_input_grad[1]:
+            dw = torch.empty_like(w)
+            ws = nat.workspace(nat.load().tdp_linear_wgrad_workspace(n, d, k), x.device)
+            nat.call("tdp_linear_wgrad", nat.ptr(x), nat.ptr(g), _dt(x), n, d, k, nat.ptr(dw),
+                     c_void_p(0), nat.ptr(ws), ws.numel(), nat.stream())
+        return dx, dw
+
+
+def skinny_linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    return _SkinnyLinear.apply(x, w)
+
+
+# ---------------------------------------------------------------------------
 # soft group-by
 # ---------------------------------------------------------------------------
 

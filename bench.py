@@ -43,7 +43,7 @@ def _args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--query", choices=("q1", "q6", "llp"), default="q1")
+    ap.add_argument("--query", choices=("q1", "q6", "q3", "llp"), default="q1")
     ap.add_argument("--llp-rows", type=int, default=100_000_000)
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -534,10 +534,63 @@ def _llp(args):
     print(json.dumps(line), flush=True)
 
 
+def _q3(args):
+    """Q3-style join pipeline (SURVEY config 3) on one GPU -- extra measurement."""
+    import torch
+
+    from oracle import tpch as otpch
+    from paper_2211_02753_b200 import _native, workloads as wl
+
+    torch.cuda.set_device(0)
+    tables = wl.q3_arrays(args.sf, seed=7)
+    cat = wl.q3_catalog(tables)
+    plan = wl.Q3Plan(cat)
+    for _ in range(max(args.warmup, 3)):
+        res = plan.run(cat)
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    steps = max(1, min(args.steps, 50))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        res = plan.run(cat)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    launches = _native.launch_count() - launches0
+    nli = len(tables["lineitem"]["l_orderkey"])
+    base_bytes = (16 * len(tables["customer"]["c_custkey"]) + 32 * len(tables["orders"]["o_orderkey"])
+                  + 32 * nli)
+    w0 = time.perf_counter()
+    exp = otpch.q3(tables)
+    cpu_s = time.perf_counter() - w0
+    got = res.columns[0].values.numpy()
+    line = {
+        "metric": "TPC-H Q3-style join pipeline (SURVEY config 3)", "value": nli / (ms / 1e3),
+        "unit": "lineitem rows/s", "ms_per_step": ms, "higher_is_better": True, "n_gpus": 1,
+        "steps": steps, "warmup": max(args.warmup, 3), "dtype": "f64",
+        "data": "synthetic Appendix-B customer/orders/lineitem, seed 7",
+        "config": {"workload": f"Q3-style SF{args.sf:g}: 3 SQL filters, orders|><|customer, "
+                               f"lineitem|><|orders, GROUP BY l_orderkey, ORDER BY sum_rev DESC LIMIT 10",
+                   "customer": len(tables["customer"]["c_custkey"]),
+                   "orders": len(tables["orders"]["o_orderkey"]), "lineitem": nli,
+                   "joined_rows": int(exp["joined_rows"])},
+        "hbm_gbs_base_columns": base_bytes / (ms / 1e3) / 1e9, "gpu_launches": launches,
+        "parity": "ok" if (got == exp["l_orderkey"]).all() else "MISMATCH",
+        "cpu_baseline": {"value": nli / cpu_s, "unit": "lineitem rows/s", "cores": 1,
+                         "kind": "port", "sample": f"full SF{args.sf:g}, oracle/tpch.py q3 once"},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = _args()
     if args.query == "llp":
         _llp(args)
+        return
+    if args.query == "q3":
+        _q3(args)
         return
     if args.impl == "reference":
         _reference(args)

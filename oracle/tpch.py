@@ -33,6 +33,30 @@ def q1(arrays: dict) -> dict[str, np.ndarray]:
     return out
 
 
+def q3(tables: dict) -> dict[str, np.ndarray]:
+    """Q3-style pipeline: reference filters (filter_exact) on each table, the
+    builder-defined sort/searchsorted join (no join in the reference), the
+    reference's groupby_exact / sort_limit on the joined rows."""
+    from .relational import join_inner, sort_limit
+
+    c, o, li = tables["customer"], tables["orders"], tables["lineitem"]
+    (ck,) = filter_exact([c["c_custkey"], c["c_mktsegment"]], [(1, "=", 1)])[:1]
+    ok, ocust, odate, oship = filter_exact(
+        [o["o_orderkey"], o["o_custkey"], o["o_orderdate"], o["o_shippriority"]],
+        [(2, "<", 9204)])
+    lk, lp, ld = filter_exact([li["l_orderkey"], li["l_extendedprice"], li["l_discount"],
+                               li["l_shipdate"]], [(3, ">", 9204)])[:3]
+    pi, bi = join_inner(ocust, ck)
+    ok, ocust, odate, oship = ok[pi], ocust[pi], odate[pi], oship[pi]
+    pi, bi = join_inner(lk, ok)
+    jk, jp, jd, jdate, jship = lk[pi], lp[pi], ld[pi], odate[bi], oship[bi]
+    rev = jp * (np.asarray(1.0) - jd)
+    keys, aggs = groupby_exact([jk], [("sum", rev), ("avg", jdate), ("avg", jship)])
+    out = sort_limit([keys[0], aggs[0], aggs[1], aggs[2]], 1, True, 10)
+    return {"l_orderkey": out[0], "sum_rev": out[1], "avg_o_orderdate": out[2],
+            "avg_o_shippriority": out[3], "joined_rows": np.asarray(len(jk))}
+
+
 def q6(arrays: dict) -> dict[str, np.ndarray]:
     cols = [arrays[c] for c in ("l_shipdate", "l_discount", "l_quantity", "l_extendedprice")]
     ship, d, q, p = filter_exact(cols, [(0, ">=", 8766), (0, "<", 9131), (1, ">=", 0.05),

@@ -7,10 +7,14 @@
 // Linear.__call__ (tq/models.py:26-27) inside a classifier TVF.  In the LLP
 // query (SURVEY config 4) these two products read the [1e8, 64] feature matrix
 // and dominate the step; a general GEMM library treats m = 1e8, n = 2 as a
-// tall-skinny problem and runs it far below HBM bandwidth.  Both kernels here
-// are pure streaming passes over X (4·d bytes per row), CUDA-core FMAs
-// (the arithmetic intensity is ~k/2 flop/byte, far below the tensor-core
-// ridge), float64 accumulation.
+// tall-skinny problem and runs it far below HBM bandwidth.
+//
+// Both kernels stream X in row tiles: a CTA loads TILE consecutive rows (one
+// contiguous span of TILE*d elements) with fully coalesced 16-byte loads into
+// shared memory laid out with an odd row stride (d+1) so that per-row and
+// per-column reads are bank-conflict free, then computes from shared memory.
+// The arithmetic intensity is ~k/2 flop/byte -- far below the tensor-core
+// ridge -- so CUDA-core FMAs at HBM speed are the roofline.
 #include "tdp_common.cuh"
 
 namespace tdp {
@@ -18,98 +22,118 @@ namespace {
 
 constexpr int kMaxK = 8;
 constexpr int kMaxD = 256;
+constexpr int kMaxTile = 128;  // rows per tile (fewer for wide float64 rows)
+constexpr int kThreadsL = 256;
 
-// One thread per row; X row read with 16-byte vector loads (rows of one warp
-// are 4·d bytes apart; the sectors a vector load leaves unused are consumed by
-// the thread's next load from L1).  W lives in shared memory, read as
-// broadcasts.
-template <class T, int K>
-__global__ void __launch_bounds__(256)
-    linear_fwd_kernel(const T* __restrict__ X, i64 n, int d, const T* __restrict__ W,
-                      const T* __restrict__ bias, T* __restrict__ Y) {
-  __shared__ T sw[kMaxD * K];
-  __shared__ T sb[K];
-  for (int t = threadIdx.x; t < d * K; t += blockDim.x) sw[t] = W[t];
-  if (threadIdx.x < K) sb[threadIdx.x] = bias ? bias[threadIdx.x] : T(0);
-  __syncthreads();
-  const bool vec = (sizeof(T) == 4) && (d % 4 == 0) && ((((uintptr_t)X) & 15) == 0);
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    double acc[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] = 0.0;
-    const T* row = X + i * d;
-    if (vec) {
-      const float4* r4 = reinterpret_cast<const float4*>(row);
-      for (int c = 0; c < d / 4; ++c) {
-        const float4 v = __ldg(r4 + c);
-        const T* w = sw + (c * 4) * K;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          acc[j] += (double)v.x * (double)w[j] + (double)v.y * (double)w[K + j] +
-                    (double)v.z * (double)w[2 * K + j] + (double)v.w * (double)w[3 * K + j];
-        }
-      }
-    } else {
-      for (int c = 0; c < d; ++c) {
-        const double v = (double)__ldg(row + c);
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc[j] += v * (double)sw[c * K + j];
-      }
+template <class T>
+__device__ __forceinline__ void load_tile(const T* __restrict__ X, i64 row0, i64 n, int d,
+                                          int tile, T* __restrict__ s) {
+  // tile*d contiguous elements starting at row0*d; rows past n read as 0
+  const i64 base = row0 * d;
+  const i64 total = (i64)tile * d;
+  const i64 limit = n * (i64)d - base;
+  if (sizeof(T) == 4 && (d % 4) == 0 && ((((uintptr_t)(X + base)) & 15) == 0)) {
+    const float4* src = reinterpret_cast<const float4*>(X + base);
+    for (i64 v = threadIdx.x; v < total / 4; v += blockDim.x) {
+      const i64 e = v * 4;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < limit) q = __ldg(src + v);
+      const int r = (int)(e / d), c = (int)(e % d);
+      T* dst = s + r * (d + 1) + c;
+      dst[0] = (T)q.x;
+      dst[1] = (T)q.y;
+      dst[2] = (T)q.z;
+      dst[3] = (T)q.w;
     }
-#pragma unroll
-    for (int j = 0; j < K; ++j) Y[i * K + j] = (T)(acc[j] + (double)sb[j]);
+  } else {
+    for (i64 e = threadIdx.x; e < total; e += blockDim.x) {
+      const int r = (int)(e / d), c = (int)(e % d);
+      s[r * (d + 1) + c] = e < limit ? __ldg(X + base + e) : T(0);
+    }
   }
 }
 
-// Warp per row group: lane l owns features l, l+32, ...; each row's X is one
-// coalesced warp load, its G row a broadcast.  Per-CTA partials in float64
-// are written to `part` ([gridDim.x][d*K + K]) and reduced in a fixed order.
+// Y = X W (+ b): thread r of the first kTile threads computes row r of the
+// tile from shared memory (odd stride -> conflict-free), W read as broadcasts.
 template <class T, int K>
-__global__ void __launch_bounds__(256)
-    linear_wgrad_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d,
+__global__ void __launch_bounds__(kThreadsL)
+    linear_fwd_kernel(const T* __restrict__ X, i64 n, int d, int tile, const T* __restrict__ W,
+                      const T* __restrict__ bias, T* __restrict__ Y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sw = reinterpret_cast<T*>(smem_raw);
+  T* sx = sw + kMaxD * K + K;
+  for (int t = threadIdx.x; t < d * K; t += blockDim.x) sw[t] = W[t];
+  if (threadIdx.x < K) sw[kMaxD * K + threadIdx.x] = bias ? bias[threadIdx.x] : T(0);
+  const i64 ntiles = (n + tile - 1) / tile;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    __syncthreads();
+    load_tile<T>(X, t * tile, n, d, tile, sx);
+    __syncthreads();
+    // two threads per row: each takes half of the features, combined by shuffle
+    const int r = threadIdx.x >> 1, half = threadIdx.x & 1;
+    const i64 row = t * tile + r;
+    T acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = T(0);
+    const T* xr = sx + (r < tile ? r : 0) * (d + 1);
+    for (int c = half; c < d; c += 2) {
+      const T x = xr[c];
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] += x * sw[c * K + j];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 1);
+    if (half == 0 && r < tile && row < n) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) Y[row * K + j] = acc[j] + sw[kMaxD * K + j];
+    }
+  }
+}
+
+// dW = X^T G, db = sum G.  Thread t owns (feature c, class j) pairs strided by
+// the block size and sums its pairs over the tile's rows in float64; G's tile
+// is staged next to X's.  One partial row per CTA, reduced in a fixed order.
+template <class T, int K>
+__global__ void __launch_bounds__(kThreadsL)
+    linear_wgrad_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d, int tile,
                         double* __restrict__ part) {
-  constexpr int kF = kMaxD / 32;
-  double acc[kF][K];
-  double bacc[K];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sx = reinterpret_cast<T*>(smem_raw);
+  T* sg = sx + tile * (d + 1);
+  const int pairs = d * K + K;  // last K "pairs" are the bias sums
+  constexpr int kPer = (kMaxD * K + K + kThreadsL - 1) / kThreadsL;
+  double acc[kPer];
 #pragma unroll
-  for (int f = 0; f < kF; ++f)
+  for (int p = 0; p < kPer; ++p) acc[p] = 0.0;
+  const i64 ntiles = (n + tile - 1) / tile;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    __syncthreads();
+    load_tile<T>(X, t * tile, n, d, tile, sx);
+    for (int e = threadIdx.x; e < tile * K; e += blockDim.x) {
+      const i64 row = t * tile + e / K;
+      sg[e] = row < n ? G[t * tile * K + e] : T(0);
+    }
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc[f][j] = 0.0;
-#pragma unroll
-  for (int j = 0; j < K; ++j) bacc[j] = 0.0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const i64 warps = (i64)gridDim.x * (blockDim.x >> 5);
-  const int nf = (d + 31) / 32;
-  for (i64 i = (i64)blockIdx.x * (blockDim.x >> 5) + warp; i < n; i += warps) {
-    double g[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) g[j] = (double)__ldg(G + i * K + j);
-#pragma unroll
-    for (int f = 0; f < kF; ++f) {
-      if (f < nf) {
-        const int c = f * 32 + lane;
-        const double x = c < d ? (double)__ldg(X + i * d + c) : 0.0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc[f][j] += x * g[j];
+    for (int p = 0; p < kPer; ++p) {
+      const int q = threadIdx.x + p * kThreadsL;
+      if (q < pairs) {
+        double s = 0.0;
+        if (q < d * K) {
+          const int c = q / K, j = q % K;
+          for (int r = 0; r < tile; ++r) s += (double)sx[r * (d + 1) + c] * (double)sg[r * K + j];
+        } else {
+          const int j = q - d * K;
+          for (int r = 0; r < tile; ++r) s += (double)sg[r * K + j];
+        }
+        acc[p] += s;
       }
     }
-#pragma unroll
-    for (int j = 0; j < K; ++j) bacc[j] += g[j];
   }
-  // one partial row per warp; reduced across rows in a fixed order afterwards
-  const int W = d * K + K;
-  double* out = part + ((i64)blockIdx.x * (blockDim.x >> 5) + warp) * W;
 #pragma unroll
-  for (int f = 0; f < kF; ++f) {
-    const int c = f * 32 + lane;
-    if (f < nf && c < d) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) out[c * K + j] = acc[f][j];
-    }
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int j = 0; j < K; ++j) out[d * K + j] = bacc[j];
+  for (int p = 0; p < kPer; ++p) {
+    const int q = threadIdx.x + p * kThreadsL;
+    if (q < pairs) part[(i64)blockIdx.x * pairs + q] = acc[p];
   }
 }
 
@@ -129,13 +153,40 @@ __global__ void wgrad_reduce_kernel(const double* __restrict__ part, int rows, i
   }
 }
 
+// rows per tile: as many as fit 96 KB of shared memory, at most kMaxTile
+template <class T>
+int tile_rows(int d) {
+  int t = (int)((96 * 1024) / ((size_t)(d + 1) * sizeof(T)));
+  if (t > kMaxTile) t = kMaxTile;
+  return t < 8 ? 8 : t;
+}
+
+template <class T>
+size_t fwd_smem(int d, int k) {
+  return (size_t)(kMaxD * k + k) * sizeof(T) + (size_t)tile_rows<T>(d) * (d + 1) * sizeof(T);
+}
+
+template <class T>
+size_t wgrad_smem(int d, int k) {
+  const int t = tile_rows<T>(d);
+  return (size_t)t * (d + 1) * sizeof(T) + (size_t)t * k * sizeof(T);
+}
+
+template <class T>
+int wgrad_grid(i64 n, int d) { return stream_grid((n + tile_rows<T>(d) - 1) / tile_rows<T>(d), 1, 2); }
+
 template <class T>
 int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cudaStream_t st) {
-  const int grid = stream_grid(n, 256, 8);
+  const size_t smem = fwd_smem<T>(d, k);
+  const int tile = tile_rows<T>(d);
+  const int grid = stream_grid((n + tile - 1) / tile, 1, 4);
   switch (k) {
-#define TDP_CASE(KK)                                                                      \
-  case KK:                                                                                \
-    linear_fwd_kernel<T, KK><<<grid, 256, 0, st>>>(X, n, d, W, b, Y);                     \
+#define TDP_CASE(KK)                                                                        \
+  case KK:                                                                                  \
+    if (smem > 48 * 1024)                                                                   \
+      TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_kernel<T, KK>,                           \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_fwd_kernel<T, KK><<<grid, kThreadsL, smem, st>>>(X, n, d, tile, W, b, Y);        \
     break;
     TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
 #undef TDP_CASE
@@ -149,14 +200,18 @@ int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cu
 template <class T>
 int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, double* ws,
                  size_t ws_bytes, cudaStream_t st) {
-  const int grid = stream_grid(n, 8 * 64, 2);
+  const int grid = wgrad_grid<T>(n, d);
   const int width = d * k + k;
-  const int rows = grid * 8;  // one partial row per warp
-  TDP_REQUIRE(ws_bytes >= (size_t)rows * width * sizeof(double), "linear_wgrad workspace too small");
+  const size_t smem = wgrad_smem<T>(d, k);
+  const int tile = tile_rows<T>(d);
+  TDP_REQUIRE(ws_bytes >= (size_t)grid * width * sizeof(double), "linear_wgrad workspace too small");
   switch (k) {
-#define TDP_CASE(KK)                                                                      \
-  case KK:                                                                                \
-    linear_wgrad_kernel<T, KK><<<grid, 256, 0, st>>>(X, G, n, d, ws);                     \
+#define TDP_CASE(KK)                                                                        \
+  case KK:                                                                                  \
+    if (smem > 48 * 1024)                                                                   \
+      TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_kernel<T, KK>,                         \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_wgrad_kernel<T, KK><<<grid, kThreadsL, smem, st>>>(X, G, n, d, tile, ws);        \
     break;
     TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
 #undef TDP_CASE
@@ -164,7 +219,7 @@ int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, doub
       return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
   }
   TDP_LAUNCH_CHECK("linear_wgrad_kernel");
-  wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(ws, rows, width,
+  wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(ws, grid, width,
                                                                                  dW, db, d * k);
   TDP_LAUNCH_CHECK("wgrad_reduce_kernel");
   return TDP_OK;
@@ -194,7 +249,9 @@ int tdp_linear_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k
 }
 
 size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k) {
-  return (size_t)stream_grid(n, 8 * 64, 2) * 8 * (size_t)(d * k + k) * sizeof(double) + 256;
+  const int g = wgrad_grid<double>(n, d) > wgrad_grid<float>(n, d) ? wgrad_grid<double>(n, d)
+                                                                    : wgrad_grid<float>(n, d);
+  return (size_t)g * (size_t)(d * k + k) * sizeof(double) + 256;
 }
 
 int tdp_linear_wgrad(const void* X, const void* G, int32_t dtype, int64_t n, int32_t d, int32_t k,

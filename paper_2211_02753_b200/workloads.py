@@ -117,6 +117,107 @@ def compile_sql(sql: str, catalog: Catalog, registry: UdfRegistry, trainable: bo
                         CompileConfig(trainable=trainable), registry)
 
 
+# ---------------------------------------------------------------------------
+# Q3-style: customer |><| orders |><| lineitem, group by orderkey, top 10
+# ---------------------------------------------------------------------------
+
+MKTSEGMENT = StringDictionary(("AUTOMOBILE", "BUILDING", "FURNITURE", "HOUSEHOLD", "MACHINERY"))
+
+
+def q3_arrays(sf: float, seed: int = 7) -> dict[str, dict[str, np.ndarray]]:
+    """Appendix B Q3 tables: dbgen sparse order keys, customers without orders
+    for custkey % 3 == 0, 1..7 lines per order."""
+    rng = np.random.default_rng(seed)
+    nc = max(3, int(round(150_000 * sf)))
+    no = max(1, int(round(1_500_000 * sf)))
+    cust = {"c_custkey": np.arange(1, nc + 1, dtype=np.int64),
+            "c_mktsegment": rng.integers(0, 5, size=nc, dtype=np.int64)}
+    i = np.arange(no, dtype=np.int64)
+    okey = (i // 8) * 32 + i % 8 + 1
+    ck = rng.integers(1, nc + 1, size=no, dtype=np.int64)
+    ck = np.where(ck % 3 == 0, np.where(ck + 1 <= nc, ck + 1, ck - 1), ck)
+    odate = rng.integers(D_1992_01_01, 10440 + 1, size=no, dtype=np.int64)
+    orders = {"o_orderkey": okey, "o_custkey": ck, "o_orderdate": odate,
+              "o_shippriority": np.zeros(no, dtype=np.int64)}
+    lines = rng.integers(1, 8, size=no)
+    lok = np.repeat(okey, lines)
+    ldate = np.repeat(odate, lines) + rng.integers(1, 122, size=lok.size, dtype=np.int64)
+    qty = rng.integers(1, 51, size=lok.size).astype(np.float64)
+    pk = rng.integers(1, int(200_000 * max(sf, 1e-6)) + 1, size=lok.size, dtype=np.int64)
+    retail = (90000 + (pk // 10) % 20001 + 100 * (pk % 1000)) / 100.0
+    lineitem = {"l_orderkey": lok, "l_shipdate": ldate,
+                "l_extendedprice": np.round(qty * retail, 2),
+                "l_discount": rng.integers(0, 11, size=lok.size) / 100.0}
+    return {"customer": cust, "orders": orders, "lineitem": lineitem}
+
+
+def q3_catalog(tables: dict) -> Catalog:
+    cat = Catalog()
+    with trusted():
+        c = tables["customer"]
+        cat.register("customer", table_from_columns(
+            ["c_custkey", "c_mktsegment"],
+            [plain(Tensor(c["c_custkey"])),
+             EncodedTensor(Tensor(c["c_mktsegment"]), DictionaryEncoding(MKTSEGMENT))]))
+    for name in ("orders", "lineitem"):
+        t = tables[name]
+        cat.register(name, table_from_columns(list(t), [plain(Tensor(v)) for v in t.values()]))
+    return cat
+
+
+Q3_CUSTOMER = 'SELECT c_custkey FROM customer WHERE c_mktsegment = "BUILDING"'
+Q3_ORDERS = ("SELECT o_orderkey, o_custkey, o_orderdate, o_shippriority FROM orders "
+             "WHERE o_orderdate < 9204")
+Q3_LINEITEM = ("SELECT l_orderkey, l_extendedprice, l_discount FROM lineitem "
+               "WHERE l_shipdate > 9204")
+Q3_TAIL = ("SELECT l_orderkey, SUM(rev), AVG(o_orderdate), AVG(o_shippriority) FROM "
+           "(SELECT q3rev(l_orderkey, l_extendedprice, l_discount, o_orderdate, o_shippriority) "
+           "FROM joined) GROUP BY l_orderkey ORDER BY sum_rev DESC LIMIT 10")
+
+
+def q3_registry() -> UdfRegistry:
+    from .storage import INT
+
+    def q3rev(k, p, d, od, sp):
+        return (k, plain(mul(p.values, sub(tensor(1.0), d.values))), od, sp)
+
+    reg = UdfRegistry()
+    reg.register(UdfEntry("q3rev", (("l_orderkey", INT), ("rev", FLOAT), ("o_orderdate", INT),
+                                    ("o_shippriority", INT)), 5, q3rev, (), pe_outputs=False))
+    return reg
+
+
+class Q3Plan:
+    """Compiled pieces of the Q3-style pipeline (the SQL subset has no JOIN:
+    the three filters and the tail are SQL, the two equi-joins are
+    kernels.equi_join)."""
+
+    def __init__(self, catalog: Catalog):
+        empty = UdfRegistry()
+        self.cust = compile_sql(Q3_CUSTOMER, catalog, empty)
+        self.orders = compile_sql(Q3_ORDERS, catalog, empty)
+        self.lineitem = compile_sql(Q3_LINEITEM, catalog, empty)
+        self.registry = q3_registry()
+        self.tail = None
+
+    def run(self, catalog: Catalog):
+        from .kernels import equi_join
+
+        c = self.cust.run(catalog)
+        o = self.orders.run(catalog)
+        li = self.lineitem.run(catalog)
+        oc = equi_join(list(o.columns), list(c.columns), 1, 0)  # orders |><| BUILDING customers
+        j = equi_join(list(li.columns), oc[:4], 0, 0)          # lineitem |><| those orders
+        names = ["l_orderkey", "l_extendedprice", "l_discount", "o_orderkey", "o_custkey",
+                 "o_orderdate", "o_shippriority"]
+        joined = table_from_columns(names, j)
+        work = Catalog()
+        work.register("joined", joined)
+        if self.tail is None:
+            self.tail = compile_sql(Q3_TAIL, work, self.registry)
+        return self.tail.run(work)
+
+
 # algorithmic bytes per row (SURVEY §8(d)): each referenced base column once at 8 B
 Q1_BYTES_PER_ROW = 56
 Q6_BYTES_PER_ROW = 32

@@ -155,3 +155,21 @@ def test_equi_join_matches_oracle_and_nested_loop():
     np.testing.assert_array_equal(ebi, nbi)
     np.testing.assert_array_equal(pi.cpu().numpy(), epi)
     np.testing.assert_array_equal(bi.cpu().numpy(), ebi)
+
+
+@pytest.mark.parametrize("sf", [0.05, 0.5])
+def test_q3_join_pipeline_matches_oracle(sf):
+    tables = wl.q3_arrays(sf, seed=7)
+    cat = wl.q3_catalog(tables)
+    plan = wl.Q3Plan(cat)
+    res = plan.run(cat)
+    exp = otpch.q3(tables)
+    got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
+    assert list(got) == ["l_orderkey", "sum_rev", "avg_o_orderdate", "avg_o_shippriority"]
+    np.testing.assert_array_equal(got["l_orderkey"], exp["l_orderkey"])
+    np.testing.assert_allclose(got["sum_rev"], exp["sum_rev"], rtol=1e-9)
+    np.testing.assert_allclose(got["avg_o_orderdate"], exp["avg_o_orderdate"], rtol=1e-12)
+    np.testing.assert_array_equal(got["avg_o_shippriority"], exp["avg_o_shippriority"])
+    # a second run reuses the compiled tail and gives the same answer
+    res2 = plan.run(cat)
+    np.testing.assert_array_equal(res2.columns[0].values.numpy(), got["l_orderkey"])

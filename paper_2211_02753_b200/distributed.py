@@ -83,6 +83,64 @@ def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows:
             sums_raw[r].copy_(floats[j].view(torch.int64))
 
 
+def key_destination(keys: list[torch.Tensor], world: int) -> torch.Tensor:
+    """Owner rank of each row: a 64-bit mix of the key tuple, mod world.
+    Equal key tuples always map to the same rank."""
+    h = torch.zeros_like(keys[0], dtype=torch.int64)
+    for k in keys:
+        x = k.to(torch.int64) ^ (h * 31)
+        # splitmix64 finaliser in two's-complement int64 arithmetic
+        x = x ^ ((x >> 30) & 0x3FFFFFFFF)
+        x = x * -4658895280553007687  # 0xbf58476d1ce4e5b9
+        x = x ^ ((x >> 27) & 0x1FFFFFFFFF)
+        x = x * -7723592293110705685  # 0x94d049bb133111eb
+        h = x ^ ((x >> 31) & 0x1FFFFFFFF)
+    return torch.remainder(h, world)
+
+
+def exchange_rows(grouped: list[torch.Tensor], send_counts: torch.Tensor,
+                  group) -> list[torch.Tensor]:
+    """All-to-all repartition of rows (NCCL on the GPU host).
+
+    ``grouped`` columns hold the local rows already ordered by destination
+    rank (a stable sort of the destinations, done by the caller with the
+    radix-sort kernel) and ``send_counts[r]`` is how many go to rank r.  Rows
+    arrive grouped by source rank, each group in its original order, so the
+    result is deterministic.
+    """
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    send = send_counts.tolist()
+    recv = recv_counts.tolist()
+    out = []
+    for col in grouped:
+        dst = torch.empty((sum(recv),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
+        dist.all_to_all_single(dst, col.contiguous(), recv, send, group=group)
+        out.append(dst)
+    return out
+
+
+def allgather_rows(columns: list[torch.Tensor], group) -> list[torch.Tensor]:
+    """Concatenate every rank's rows (rank order) on every rank."""
+    world = world_size(group)
+    if world <= 1:
+        return columns
+    dev = columns[0].device
+    n = torch.tensor([columns[0].shape[0]], dtype=torch.int64, device=dev)
+    sizes = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s) for s in sizes]
+    m = max(sizes) if sizes else 0
+    out = []
+    for col in columns:
+        pad = torch.zeros((m,) + tuple(col.shape[1:]), dtype=col.dtype, device=dev)
+        pad[: col.shape[0]] = col
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        out.append(torch.cat([p[:s] for p, s in zip(parts, sizes)]))
+    return out
+
+
 def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous row range of ``rank`` (sizes differ by at most one row)."""
     base, extra = divmod(n, world)

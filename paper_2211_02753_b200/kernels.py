@@ -51,7 +51,15 @@ from .lazy import (
     base_rows,
     resolve_predicate,
 )
-from .distributed import allreduce_partials, allreduce_ranges, current_group
+from .distributed import (
+    allgather_rows,
+    allreduce_partials,
+    allreduce_ranges,
+    current_group,
+    exchange_rows,
+    key_destination,
+    world_size,
+)
 from .storage import ColumnType
 from .tensor import (
     FLOAT_DTYPES,
@@ -441,10 +449,7 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space):
             span = hi - lo + 1
         spans.append((lo, span))
         slots *= span
-    if slots > DENSE_SLOT_LIMIT:
-        if current_group() is not None:
-            raise KernelError("sharded group-by over more than "
-                              f"{DENSE_SLOT_LIMIT} dense slots needs a key shuffle")
+    if slots > DENSE_SLOT_LIMIT:  # high cardinality: sort-based (sharded: all-to-all)
         return _groupby_general(keys, key_vals, agg_specs, agg_vals)
     agg_exprs = []
     for (func, dt), v in zip(agg_specs, agg_vals):
@@ -536,13 +541,65 @@ def _groupby_general(keys, key_vals, agg_specs, agg_vals):
     """Sort-based path (the reference's np.unique algorithm on the device)."""
     kdata = [_materialize(v) for v in key_vals]
     n = int(kdata[0].shape[0])
+    vdata = []
     for (func, dt), v in zip(agg_specs, agg_vals):
-        if v is not None and (_materialize(v).dim() != 1 or _materialize(v).shape[0] != n):
+        if v is None:
+            vdata.append(None)
+            continue
+        t = _materialize(v)
+        if t.dim() != 1 or t.shape[0] != n:
             raise KernelError(f"{func} aggregate needs a value column of {n} rows")
-    device = kdata[0].device
+        vdata.append(t)
     nat.require_cuda(*kdata)
+    group = current_group()
+    if group is not None and world_size(group) > 1:
+        return _groupby_sharded(kdata, agg_specs, vdata, group)
+    return _groupby_local(kdata, agg_specs, vdata)
+
+
+def _lex_order(keys: Sequence[torch.Tensor]) -> torch.Tensor:
+    """Stable lexicographic order of key tuples (LSD over the key columns)."""
+    from .autograd import gather_rows_raw
+
+    order = None
+    for k in reversed(list(keys)):
+        kk = k if order is None else gather_rows_raw(k, order)
+        o = stable_order(plain(Tensor(kk)))
+        order = o if order is None else gather_rows_raw(order, o)
+    return order
+
+
+def _groupby_sharded(kdata, agg_specs, vdata, group):
+    """High-cardinality group-by across ranks: repartition rows by key with
+    an NCCL all-to-all, group locally (every group now lives on one rank),
+    all-gather the (small) results and order them by key."""
+    from .autograd import gather_many, gather_rows_raw
+
+    world = world_size(group)
+    device = kdata[0].device
+    dest = key_destination(kdata, world)
+    order = stable_order(plain(Tensor(dest)))
+    send_counts, _ = _groupby_codes(dest, world, [], [], int(dest.numel()), device)
+    cols = [t.to(torch.int64) if t.dtype == torch.bool else t for t in list(kdata) +
+            [v for v in vdata if v is not None]]
+    recv = exchange_rows(gather_many(cols, order), send_counts, group)
+    rk = recv[:len(kdata)]
+    rv = iter(recv[len(kdata):])
+    rvals = [None if v is None else next(rv) for v in vdata]
+    key_values, aggs = _groupby_local(rk, agg_specs, rvals)
+    allk = allgather_rows(list(key_values) + list(aggs), group)
+    kv, av = allk[:len(key_values)], allk[len(key_values):]
+    if kv[0].numel() == 0:
+        return kv, av
+    o = _lex_order(kv)
+    return gather_many(kv, o), gather_many(av, o)
+
+
+def _groupby_local(kdata, agg_specs, agg_vals):
+    device = kdata[0].device
+    n = int(kdata[0].shape[0])
     if n == 0:
-        return _empty_groups(len(keys), agg_specs, device)
+        return _empty_groups(len(kdata), agg_specs, device)
     uniqs, codes = zip(*[unique_inverse(k) for k in kdata])
     if len(kdata) == 1:
         group_codes, slots = codes[0], int(uniqs[0].numel())

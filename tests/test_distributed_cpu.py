@@ -75,6 +75,59 @@ def test_allreduce_partials_world2():
     assert result.get("ok") is True
 
 
+def _shuffle_worker(rank, world, port, result):
+    """High-cardinality group-by across ranks: key_destination + all-to-all
+    exchange + local group-by + all-gather + lexicographic order (the GPU
+    path's steps; local sort / group-by done by the oracle here)."""
+    from oracle import relational as orc
+    from paper_2211_02753_b200.distributed import allgather_rows, exchange_rows, key_destination
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(1)
+    n = 20_000
+    k1 = rng.integers(-10**9, 10**9, size=n // 7)[rng.integers(0, n // 7, size=n)]
+    k2 = rng.integers(0, 3, size=n)
+    v = rng.normal(size=n)
+    a, b = shard_bounds(n, rank, world)
+    kk1, kk2, vv = (torch.from_numpy(x[a:b].copy()) for x in (k1, k2, v))
+    dest = key_destination([kk1, kk2], world)
+    order = torch.from_numpy(np.argsort(dest.numpy(), kind="stable"))
+    counts = torch.from_numpy(np.bincount(dest.numpy(), minlength=world).astype(np.int64))
+    rk1, rk2, rv = exchange_rows([t[order] for t in (kk1, kk2, vv)], counts, dist.group.WORLD)
+    keys, aggs = orc.groupby_exact([rk1.numpy(), rk2.numpy()], [("sum", rv.numpy()), ("count", None)])
+    g1, g2, gs, gc = allgather_rows([torch.from_numpy(x) for x in (*keys, *aggs)], dist.group.WORLD)
+    o = np.lexsort((g2.numpy(), g1.numpy()))
+    if rank == 0:
+        ekeys, eaggs = orc.groupby_exact([k1, k2], [("sum", v), ("count", None)])
+        result["ok"] = (np.array_equal(g1.numpy()[o], ekeys[0])
+                        and np.array_equal(g2.numpy()[o], ekeys[1])
+                        and np.array_equal(gc.numpy()[o], eaggs[1])
+                        and np.allclose(gs.numpy()[o], eaggs[0], rtol=1e-12)
+                        and int(counts.sum()) == b - a)
+    dist.destroy_process_group()
+
+
+def test_key_shuffle_group_by_world2():
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_shuffle_worker, args=(2, _free_port(), result), nprocs=2, join=True)
+    assert result.get("ok") is True
+
+
+def test_key_destination_is_a_function_of_the_key():
+    from paper_2211_02753_b200.distributed import key_destination
+
+    k = torch.tensor([5, -7, 5, 2**62, -7, 0])
+    d = key_destination([k], 4)
+    assert d.tolist()[0] == d.tolist()[2] and d.tolist()[1] == d.tolist()[4]
+    assert d.min() >= 0 and d.max() < 4
+    many = key_destination([torch.arange(100_000)], 8)
+    counts = torch.bincount(many, minlength=8)
+    assert counts.min() > 100_000 / 8 * 0.9  # spreads keys evenly
+
+
 def test_shard_bounds_cover_rows():
     for n in (0, 1, 7, 10**6 + 3):
         for w in (1, 2, 3, 8):

@@ -266,16 +266,18 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
 size_t tdp_join_workspace(int64_t n_build, int64_t n_probe);
 
 /* Inner equi-join on int64 keys, two calls sharing one workspace.
- * prepare: stable radix sort of the build keys, one binary search per probe
- * key, scan of match counts; writes the number of result pairs to out_count
- * (device int64).  emit: writes the pairs, ordered by probe row and, within a
- * probe row, by ascending build row.  The workspace must not be touched
- * between the two calls.                                                   */
+ * prepare: stable radix sort of the build keys, open-addressing hash table
+ * over the distinct build keys (key -> run in sorted order), one hash probe
+ * per probe row, per-tile match counts and their scan; writes the number of
+ * result pairs to out_count (device int64).  emit: re-probes and writes the
+ * pairs, ordered by probe row and, within a probe row, by ascending build row.
+ * The workspace must not be touched between the two calls.                */
 int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
                      int64_t n_probe, int64_t* out_count, void* ws, size_t ws_bytes,
                      void* stream);
-int tdp_join_emit(int64_t n_build, int64_t n_probe, int64_t* out_probe_idx,
-                  int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);
+int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
+                  int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
+                  void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* probability encodings and soft (differentiable) group-by                 */

@@ -447,63 +447,182 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// equi-join: sort build keys, binary-search each probe key
+// equi-join: stable radix sort of the build keys, an open-addressing hash
+// table over the distinct build keys (key -> [start, count) in sorted order),
+// one hash probe per probe row.  Probe rows are processed in tiles: pass 1
+// counts matches per tile only (no per-row arrays), a tiny scan gives tile
+// offsets, pass 2 re-probes (the table is L2-resident) and writes the pairs
+// with a block scan.  Output: probe row order, ascending build row within a
+// probe row (stable sort).
 // ---------------------------------------------------------------------------
 namespace tdp {
 namespace {
 
-__device__ __forceinline__ i64 lower_bound_u64(const u64* a, i64 n, u64 v) {
-  i64 lo = 0, hi = n;
-  while (lo < hi) {
-    const i64 mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
+constexpr int kJoinThreads = 256;
+constexpr int kJoinTile = 256 * 8;  // probe rows per tile
+
+__device__ __forceinline__ u64 mix64(u64 x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
 }
 
-__global__ void probe_count_kernel(const u64* __restrict__ sk, i64 nb,
-                                   const i64* __restrict__ probe, i64 np, i64* __restrict__ lb,
-                                   i64* __restrict__ cnt) {
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < np;
-       i += (i64)gridDim.x * blockDim.x) {
-    const u64 v = (u64)probe[i] ^ 0x8000000000000000ull;
-    const i64 l = lower_bound_u64(sk, nb, v);
-    i64 h = l;
-    if (l < nb && sk[l] == v) h = lower_bound_u64(sk, nb, v + 1);  // v + 1 cannot wrap: v == ~0 only for INT64_MAX
-    if (v == ~0ull) h = nb;
-    lb[i] = l;
-    cnt[i] = h - l;
-  }
-}
+struct HashTable {
+  i64* key;       // [cap]
+  i64* start;     // [cap]; 0 = empty, else start + 1
+  i64* count;     // [cap]
+  u64 mask;
+};
 
-__global__ void probe_emit_kernel(const i64* __restrict__ order, const i64* __restrict__ lb,
-                                  const i64* __restrict__ cnt, const i64* __restrict__ off,
-                                  i64 np, i64* __restrict__ out_probe,
-                                  i64* __restrict__ out_build) {
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < np;
+__global__ void join_build_kernel(const u64* __restrict__ sk, i64 nb, HashTable ht) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
        i += (i64)gridDim.x * blockDim.x) {
-    const i64 c = cnt[i];
-    const i64 o = off[i], l = lb[i];
-    for (i64 j = 0; j < c; ++j) {
-      out_probe[o + j] = i;
-      out_build[o + j] = order[l + j];
+    if (i > 0 && sk[i] == sk[i - 1]) continue;  // only run starts insert
+    i64 e = i + 1;
+    while (e < nb && sk[e] == sk[i]) ++e;
+    const i64 key = (i64)(sk[i] ^ 0x8000000000000000ull);
+    u64 h = mix64((u64)key) & ht.mask;
+    for (;;) {
+      const unsigned long long prev = atomicCAS(
+          reinterpret_cast<unsigned long long*>(ht.start + h), 0ull, (unsigned long long)(i + 1));
+      if (prev == 0ull) {
+        ht.key[h] = key;
+        ht.count[h] = e - i;
+        break;
+      }
+      h = (h + 1) & ht.mask;
     }
   }
 }
 
-struct JoinLayout {
+__device__ __forceinline__ void join_lookup(const HashTable& ht, i64 key, i64* start, i64* cnt) {
+  u64 h = mix64((u64)key) & ht.mask;
+  for (;;) {
+    const i64 s = ht.start[h];
+    if (s == 0) {
+      *start = 0;
+      *cnt = 0;
+      return;
+    }
+    if (ht.key[h] == key) {
+      *start = s - 1;
+      *cnt = ht.count[h];
+      return;
+    }
+    h = (h + 1) & ht.mask;
+  }
+}
+
+__global__ void __launch_bounds__(kJoinThreads)
+    join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
+                      i64* __restrict__ tile_counts) {
+  __shared__ i64 warp_sums[kJoinThreads / 32];
+  const i64 tile = blockIdx.x;
+  i64 local = 0;
+  for (int k = 0; k < kJoinTile / kJoinThreads; ++k) {
+    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
+    if (i < np) {
+      i64 s, c;
+      join_lookup(ht, __ldg(probe + i), &s, &c);
+      local += c;
+    }
+  }
+  local = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i64 t = 0;
+    for (int w = 0; w < kJoinThreads / 32; ++w) t += warp_sums[w];
+    tile_counts[tile] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kJoinThreads)
+    join_emit_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
+                     const i64* __restrict__ order, const i64* __restrict__ tile_offsets,
+                     i64* __restrict__ out_probe, i64* __restrict__ out_build) {
+  __shared__ i64 warp_tot[kJoinThreads / 32];
+  __shared__ i64 running;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 tile = blockIdx.x;
+  if (threadIdx.x == 0) running = tile_offsets[tile];
+  __syncthreads();
+  for (int k = 0; k < kJoinTile / kJoinThreads; ++k) {
+    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
+    i64 s = 0, c = 0;
+    if (i < np) join_lookup(ht, __ldg(probe + i), &s, &c);
+    // block-wide exclusive scan of c (row order = thread order)
+    i64 incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const i64 t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    i64 before = 0, total = 0;
+    for (int w = 0; w < kJoinThreads / 32; ++w) {
+      if (w < warp) before += warp_tot[w];
+      total += warp_tot[w];
+    }
+    const i64 base = running + before + incl - c;
+    for (i64 j = 0; j < c; ++j) {
+      out_probe[base + j] = i;
+      out_build[base + j] = order[s + j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += total;
+    __syncthreads();
+  }
+}
+
+u64 table_capacity(i64 nb) {
+  u64 cap = 1024;
+  while (cap < (u64)(2 * (nb > 0 ? nb : 1))) cap <<= 1;
+  return cap;
+}
+
+struct JoinWs {
   SortBuffers sb;
-  i64* lb;
-  i64* cnt;
-  i64* off;
-  u64** sorted_keys_slot;
-  unsigned char* state;  // [0]: 0/1 which sort buffer holds the result
+  HashTable ht;
+  i64* tile_counts;
+  i64* tile_offsets;
+  void* scan_ws;
+  size_t scan_bytes;
+  i64* order;  // sorted build row ids (k0/i0 slot after prepare)
 };
 
 size_t join_ws_bytes(i64 nb, i64 np) {
-  return sort_ws_bytes(nb) + 3 * align256((size_t)(np > 0 ? np : 1) * 8) +
-         exclusive_scan_workspace(np) + 1024;
+  const u64 cap = table_capacity(nb);
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  return sort_ws_bytes(nb) + 3 * align256(cap * 8) + 2 * align256((size_t)tiles * 8) +
+         exclusive_scan_workspace(tiles) + 2048;
+}
+
+JoinWs carve_join(void* ws, i64 nb, i64 np) {
+  JoinWs j;
+  j.sb = carve(ws, nb);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(nb);
+  const u64 cap = table_capacity(nb);
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  j.ht.key = (i64*)p;
+  p += align256(cap * 8);
+  j.ht.start = (i64*)p;
+  p += align256(cap * 8);
+  j.ht.count = (i64*)p;
+  p += align256(cap * 8);
+  j.ht.mask = cap - 1;
+  j.tile_counts = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  j.tile_offsets = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  j.scan_ws = p;
+  j.scan_bytes = exclusive_scan_workspace(tiles) + 1024;
+  j.order = j.sb.i0;
+  return j;
 }
 
 }  // namespace
@@ -519,52 +638,47 @@ int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* 
   TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
   TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
   cudaStream_t st = as_stream(stream);
-  SortBuffers b = carve(ws, n_build);
-  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n_build);
-  i64* lb = (i64*)p;
-  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
-  i64* cnt = (i64*)p;
-  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
-  i64* off = (i64*)p;
-  p += align256((size_t)(n_probe > 0 ? n_probe : 1) * 8);
   if (n_build == 0 || n_probe == 0) {
     TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
     return TDP_OK;
   }
+  JoinWs j = carve_join(ws, n_build, n_probe);
   make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
-                                                                      n_build, b.k0, b.i0);
+                                                                      n_build, j.sb.k0, j.sb.i0);
   TDP_LAUNCH_CHECK("make_keys_kernel");
   u64* sk;
   i64* order;
-  int rc = radix_sort(b, n_build, st, &sk, &order);
+  int rc = radix_sort(j.sb, n_build, st, &sk, &order);
   if (rc) return rc;
-  if (sk != b.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
-    TDP_CUDA_TRY(cudaMemcpyAsync(b.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
-    TDP_CUDA_TRY(cudaMemcpyAsync(b.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+  if (sk != j.sb.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
   }
-  probe_count_kernel<<<stream_grid(n_probe, 256 * 4, 8), 256, 0, st>>>(b.k0, n_build, probe_keys,
-                                                                        n_probe, lb, cnt);
-  TDP_LAUNCH_CHECK("probe_count_kernel");
-  return exclusive_scan_i64(cnt, off, n_probe, out_count, p, exclusive_scan_workspace(n_probe) + 512,
-                            st);
+  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.start, 0, (j.ht.mask + 1) * 8, st));
+  join_build_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(j.sb.k0, n_build, j.ht);
+  TDP_LAUNCH_CHECK("join_build_kernel");
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  join_count_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe,
+                                                             j.tile_counts);
+  TDP_LAUNCH_CHECK("join_count_kernel");
+  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
+                            j.scan_bytes, st);
 }
 
-int tdp_join_emit(int64_t n_build, int64_t n_probe, int64_t* out_probe_idx,
-                  int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream) {
+int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
+                  int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
+                  void* stream) {
   TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
   if (n_build == 0 || n_probe == 0) return TDP_OK;
   cudaStream_t st = as_stream(stream);
-  SortBuffers b = carve(ws, n_build);
-  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n_build);
-  i64* lb = (i64*)p;
-  p += align256((size_t)n_probe * 8);
-  i64* cnt = (i64*)p;
-  p += align256((size_t)n_probe * 8);
-  i64* off = (i64*)p;
-  probe_emit_kernel<<<stream_grid(n_probe, 256 * 4, 8), 256, 0, st>>>(b.i0, lb, cnt, off, n_probe,
-                                                                       out_probe_idx, out_build_idx);
-  TDP_LAUNCH_CHECK("probe_emit_kernel");
+  JoinWs j = carve_join(ws, n_build, n_probe);
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  join_emit_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, j.order,
+                                                            j.tile_offsets, out_probe_idx,
+                                                            out_build_idx);
+  TDP_LAUNCH_CHECK("join_emit_kernel");
   return TDP_OK;
 }
 
 }  // extern "C"
+

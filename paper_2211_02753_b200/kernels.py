@@ -876,22 +876,66 @@ def join_indices(probe_key, build_key) -> tuple[torch.Tensor, torch.Tensor]:
     pi = torch.empty(m, dtype=torch.int64, device=dev)
     bi = torch.empty(m, dtype=torch.int64, device=dev)
     if m:
-        nat.call("tdp_join_emit", n_build, n_probe, nat.ptr(pi), nat.ptr(bi), nat.ptr(ws),
-                 ws.numel(), nat.stream())
+        nat.call("tdp_join_emit", nat.ptr(pk), n_build, n_probe, nat.ptr(pi), nat.ptr(bi),
+                 nat.ptr(ws), ws.numel(), nat.stream())
     return pi, bi
+
+
+def _side_sources(cols: Sequence[EncodedTensor]):
+    """(base tensors, row map or None) for one join side.
+
+    Lazy views of one selection are gathered straight from their base columns
+    through ``selection.indices()[rows]``; the filtered relation is never
+    materialised.  Anything else is materialised first."""
+    sels = set()
+    for c in cols:
+        v = c.values
+        if v._t is not None or not isinstance(v._lazy, LazyValue) or v._lazy.expr.op != "col" \
+                or v._lazy.sel is None:
+            sels = None
+            break
+        sels.add(id(v._lazy.sel))
+    if sels is not None and len(sels) == 1:
+        sel = cols[0].values._lazy.sel
+        return [c.values._lazy.expr.col for c in cols], sel.indices()
+    return [c.values.data.detach() for c in cols], None
+
+
+def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tensor):
+    from .autograd import gather_many, gather_rows_raw
+
+    if any(onehot_payload(c.values) is not None for c in cols):
+        return [take_rows(c, rows if rowmap is None else gather_rows_raw(rowmap, rows))
+                for c in cols]
+    src = rows if rowmap is None else gather_rows_raw(rowmap, rows)
+    outs = gather_many([b.contiguous() for b in bases], src)
+    with trusted():
+        return [EncodedTensor(Tensor(o), c.encoding) for o, c in zip(outs, cols)]
 
 
 def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], left_key: int,
               right_key: int) -> list[EncodedTensor]:
     """Inner join ``left.left_key = right.right_key``; returns left columns then
-    right columns.  Keys must be plain int64 columns (dictionary codes from
-    different dictionaries are not comparable)."""
+    right columns, rows ordered by left row then ascending right row.  Keys
+    must be plain int64 columns (dictionary codes from different dictionaries
+    are not comparable).  Filtered (lazy) inputs are joined without
+    materialising the filtered relations: only the key columns are gathered
+    before the join, every output column is gathered once from its base."""
     for side, cols, k in (("left", left, left_key), ("right", right, right_key)):
         col = cols[k]
         if col.is_pe() or col.is_dictionary() or col.values.dtype != "int64" or col.values.ndim != 1:
             raise KernelError(f"{side} join key must be a plain int64 column")
-    pi, bi = join_indices(left[left_key].values, right[right_key].values)
-    return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
+    if active_tape() is not None:
+        pi, bi = join_indices(left[left_key].values, right[right_key].values)
+        return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
+    lb, lmap = _side_sources(left)
+    rb, rmap = _side_sources(right)
+    from .autograd import gather_rows_raw
+
+    lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
+    rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
+    pi, bi = join_indices(lkey, rkey)
+    return _gather_side(left, lb, lmap, pi) + _gather_side(right, rb, rmap, bi)
 
 
 # ---------------------------------------------------------------------------

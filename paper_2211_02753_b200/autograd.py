@@ -121,15 +121,17 @@ def linear_eligible(a: torch.Tensor, b: torch.Tensor) -> bool:
 
 class _SkinnyLinear(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    def forward(ctx, x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor]) -> torch.Tensor:
         x = x.contiguous()
         w = w.contiguous()
+        b = None if b is None else b.contiguous()
         n, d = x.shape
         k = w.shape[1]
         y = torch.empty((n, k), dtype=x.dtype, device=x.device)
-        nat.call("tdp_linear_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), c_void_p(0),
+        nat.call("tdp_linear_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
                  nat.ptr(y), nat.stream())
         ctx.save_for_backward(x, w)
+        ctx.has_bias = b is not None
         return y
 
     @staticmethod
@@ -138,19 +140,23 @@ class _SkinnyLinear(torch.autograd.Function):
         g = g.contiguous().to(x.dtype)
         n, d = x.shape
         k = w.shape[1]
-        dx = dw = None
+        dx = dw = db = None
         if ctx.needs_input_grad[0]:
             dx = torch.matmul(g, w.t())
-        if ctx.needs_input_grad[1]:
+        want_b = ctx.has_bias and ctx.needs_input_grad[2]
+        if ctx.needs_input_grad[1] or want_b:
             dw = torch.empty_like(w)
+            db = torch.empty(k, dtype=x.dtype, device=x.device) if want_b else None
             ws = nat.workspace(nat.load().tdp_linear_wgrad_workspace(n, d, k), x.device)
             nat.call("tdp_linear_wgrad", nat.ptr(x), nat.ptr(g), _dt(x), n, d, k, nat.ptr(dw),
-                     c_void_p(0), nat.ptr(ws), ws.numel(), nat.stream())
-        return dx, dw
+                     nat.ptr(db), nat.ptr(ws), ws.numel(), nat.stream())
+            if not ctx.needs_input_grad[1]:
+                dw = None
+        return dx, dw, db
 
 
-def skinny_linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-    return _SkinnyLinear.apply(x, w)
+def skinny_linear(x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor] = None) -> torch.Tensor:
+    return _SkinnyLinear.apply(x, w, b)
 
 
 # ---------------------------------------------------------------------------

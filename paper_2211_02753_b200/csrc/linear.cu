@@ -53,46 +53,110 @@ __device__ __forceinline__ void load_tile(const T* __restrict__ X, i64 row0, i64
   }
 }
 
-// Y = X W (+ b): thread r of the first kTile threads computes row r of the
-// tile from shared memory (odd stride -> conflict-free), W read as broadcasts.
+// Y = X W (+ b).  Warp w owns 32 rows of the tile; lane l owns features
+// l, l+32, ... (its W entries live in registers).  Every lane forms partial dot
+// products for all 32 rows, then a butterfly "transpose reduction" (5 levels
+// of shuffles, halving the live partials each level) leaves the full sums of
+// row (base + l) in lane l: ~2 shuffles per row instead of a 5-level
+// reduction per row.  Shared-memory reads are conflict-free (a warp reads
+// consecutive features of one row).
 template <class T, int K>
 __global__ void __launch_bounds__(kThreadsL)
     linear_fwd_kernel(const T* __restrict__ X, i64 n, int d, int tile, const T* __restrict__ W,
                       const T* __restrict__ bias, T* __restrict__ Y) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sw = reinterpret_cast<T*>(smem_raw);
-  T* sx = sw + kMaxD * K + K;
-  for (int t = threadIdx.x; t < d * K; t += blockDim.x) sw[t] = W[t];
-  if (threadIdx.x < K) sw[kMaxD * K + threadIdx.x] = bias ? bias[threadIdx.x] : T(0);
+  T* sx = reinterpret_cast<T*>(smem_raw);
+  constexpr int kF = kMaxD / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nf = (d + 31) / 32;
+  T w[kF][K];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const int c = f * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < K; ++j) w[f][j] = (f < nf && c < d) ? W[c * K + j] : T(0);
+  }
+  T bj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
   const i64 ntiles = (n + tile - 1) / tile;
+  const int groups = tile / 32;
   for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
     __syncthreads();
     load_tile<T>(X, t * tile, n, d, tile, sx);
     __syncthreads();
-    // two threads per row: each takes half of the features, combined by shuffle
-    const int r = threadIdx.x >> 1, half = threadIdx.x & 1;
-    const i64 row = t * tile + r;
-    T acc[K];
+    for (int g = warp; g < groups; g += kThreadsL / 32) {
+      if constexpr (K > 2) {
+        // wide outputs: a plain per-row warp reduction keeps registers low
+        for (int r = 0; r < 32; ++r) {
+          const T* xr = sx + (g * 32 + r) * (d + 1);
+          T q[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] = T(0);
-    const T* xr = sx + (r < tile ? r : 0) * (d + 1);
-    for (int c = half; c < d; c += 2) {
-      const T x = xr[c];
+          for (int j = 0; j < K; ++j) q[j] = T(0);
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc[j] += x * sw[c * K + j];
-    }
+          for (int f = 0; f < kF; ++f) {
+            const int c = f * 32 + lane;
+            if (f < nf && c < d) {
+              const T x = xr[c];
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 1);
-    if (half == 0 && r < tile && row < n) {
+              for (int j = 0; j < K; ++j) q[j] += x * w[f][j];
+            }
+          }
 #pragma unroll
-      for (int j = 0; j < K; ++j) Y[row * K + j] = acc[j] + sw[kMaxD * K + j];
+          for (int j = 0; j < K; ++j) q[j] = warp_sum(q[j]);
+          const i64 row = t * tile + g * 32 + r;
+          if (lane == 0 && row < n) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) Y[row * K + j] = q[j] + bj[j];
+          }
+        }
+        continue;
+      }
+      T p[32][K];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const T* xr = sx + (g * 32 + r) * (d + 1);
+#pragma unroll
+        for (int j = 0; j < K; ++j) p[r][j] = T(0);
+#pragma unroll
+        for (int f = 0; f < kF; ++f) {
+          if (f < nf) {
+            const int c = f * 32 + lane;
+            const T x = c < d ? xr[c] : T(0);
+#pragma unroll
+            for (int j = 0; j < K; ++j) p[r][j] += x * w[f][j];
+          }
+        }
+      }
+      // transpose reduction: after the level with offset o, lane l holds the
+      // partial sums of the rows whose index bits above o match lane l's.
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int r = 0; r < o; ++r) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const T send = upper ? p[r][j] : p[r + o][j];
+            const T keep = upper ? p[r + o][j] : p[r][j];
+            p[r][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+      }
+      const i64 row = t * tile + g * 32 + lane;
+      if (row < n) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) Y[row * K + j] = p[0][j] + bj[j];
+      }
     }
   }
 }
 
-// dW = X^T G, db = sum G.  Thread t owns (feature c, class j) pairs strided by
-// the block size and sums its pairs over the tile's rows in float64; G's tile
-// is staged next to X's.  One partial row per CTA, reduced in a fixed order.
+// dW = X^T G, db = sum G.  Thread t owns feature c = t mod (d+1) (c == d is
+// the bias, x = 1) for every class and a row group t / (d+1); it sums its rows
+// of each tile in T with K independent FMA chains and folds the tile sum into
+// float64.  Row groups are combined in shared memory at the end; one partial
+// row per CTA, reduced in a fixed order by wgrad_reduce_kernel.
 template <class T, int K>
 __global__ void __launch_bounds__(kThreadsL)
     linear_wgrad_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d, int tile,
@@ -100,11 +164,13 @@ __global__ void __launch_bounds__(kThreadsL)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sx = reinterpret_cast<T*>(smem_raw);
   T* sg = sx + tile * (d + 1);
-  const int pairs = d * K + K;  // last K "pairs" are the bias sums
-  constexpr int kPer = (kMaxD * K + K + kThreadsL - 1) / kThreadsL;
-  double acc[kPer];
+  const int nfeat = d + 1;
+  const int ngroups = kThreadsL / nfeat > 0 ? kThreadsL / nfeat : 1;
+  double acc[2][K];  // a thread owns <= 2 features when d + 1 > 256 threads
 #pragma unroll
-  for (int p = 0; p < kPer; ++p) acc[p] = 0.0;
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[a][j] = 0.0;
   const i64 ntiles = (n + tile - 1) / tile;
   for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
     __syncthreads();
@@ -115,25 +181,40 @@ __global__ void __launch_bounds__(kThreadsL)
     }
     __syncthreads();
 #pragma unroll
-    for (int p = 0; p < kPer; ++p) {
-      const int q = threadIdx.x + p * kThreadsL;
-      if (q < pairs) {
-        double s = 0.0;
-        if (q < d * K) {
-          const int c = q / K, j = q % K;
-          for (int r = 0; r < tile; ++r) s += (double)sx[r * (d + 1) + c] * (double)sg[r * K + j];
-        } else {
-          const int j = q - d * K;
-          for (int r = 0; r < tile; ++r) s += (double)sg[r * K + j];
-        }
-        acc[p] += s;
+    for (int a = 0; a < 2; ++a) {
+      const int q = threadIdx.x + a * kThreadsL;
+      const int c = q % nfeat, rg = q / nfeat;
+      if (rg >= ngroups || (a == 1 && nfeat <= kThreadsL)) continue;
+      T s[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) s[j] = T(0);
+      for (int r = rg; r < tile; r += ngroups) {
+        const T x = c < d ? sx[r * (d + 1) + c] : T(1);
+#pragma unroll
+        for (int j = 0; j < K; ++j) s[j] += x * sg[r * K + j];
       }
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[a][j] += (double)s[j];
     }
   }
+  // combine row groups: reuse the tile buffer as [ngroups][nfeat*K] doubles
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smem_raw);
 #pragma unroll
-  for (int p = 0; p < kPer; ++p) {
-    const int q = threadIdx.x + p * kThreadsL;
-    if (q < pairs) part[(i64)blockIdx.x * pairs + q] = acc[p];
+  for (int a = 0; a < 2; ++a) {
+    const int q = threadIdx.x + a * kThreadsL;
+    const int c = q % nfeat, rg = q / nfeat;
+    if (rg >= ngroups || (a == 1 && nfeat <= kThreadsL)) continue;
+#pragma unroll
+    for (int j = 0; j < K; ++j) red[(size_t)rg * nfeat * K + c * K + j] = acc[a][j];
+  }
+  __syncthreads();
+  const int W = d * K + K;
+  for (int e = threadIdx.x; e < nfeat * K; e += blockDim.x) {
+    double v = 0.0;
+    for (int rg = 0; rg < ngroups; ++rg) v += red[(size_t)rg * nfeat * K + e];
+    // layout of the partial row: dW (d*K, row-major [c][j]) then db (K)
+    part[(i64)blockIdx.x * W + e] = v;
   }
 }
 
@@ -153,23 +234,27 @@ __global__ void wgrad_reduce_kernel(const double* __restrict__ part, int rows, i
   }
 }
 
-// rows per tile: as many as fit 96 KB of shared memory, at most kMaxTile
+// rows per tile: a multiple of 32 fitting 96 KB of shared memory, <= kMaxTile
 template <class T>
 int tile_rows(int d) {
   int t = (int)((96 * 1024) / ((size_t)(d + 1) * sizeof(T)));
   if (t > kMaxTile) t = kMaxTile;
-  return t < 8 ? 8 : t;
+  t = (t / 32) * 32;
+  return t < 32 ? 32 : t;
 }
 
 template <class T>
 size_t fwd_smem(int d, int k) {
-  return (size_t)(kMaxD * k + k) * sizeof(T) + (size_t)tile_rows<T>(d) * (d + 1) * sizeof(T);
+  (void)k;
+  return (size_t)tile_rows<T>(d) * (d + 1) * sizeof(T);
 }
 
 template <class T>
 size_t wgrad_smem(int d, int k) {
   const int t = tile_rows<T>(d);
-  return (size_t)t * (d + 1) * sizeof(T) + (size_t)t * k * sizeof(T);
+  const size_t tiles = (size_t)t * (d + 1) * sizeof(T) + (size_t)t * k * sizeof(T);
+  const size_t red = (size_t)(kThreadsL + d + 1) * k * sizeof(double);  // row-group combine
+  return tiles > red ? tiles : red;
 }
 
 template <class T>

@@ -516,20 +516,51 @@ __device__ __forceinline__ void join_lookup(const HashTable& ht, i64 key, i64* s
   }
 }
 
+constexpr int kJoinPer = kJoinTile / kJoinThreads;
+
+// All kJoinPer lookups of a thread issue their first table reads together
+// (independent loads in flight); only the rare collision chains loop.
+__device__ __forceinline__ void join_lookup_batch(const HashTable& ht, const i64* __restrict__ probe,
+                                                  i64 np, i64 tile, i64* s, i64* c) {
+  i64 key[kJoinPer];
+  u64 h[kJoinPer];
+  i64 st[kJoinPer], kk[kJoinPer];
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
+    key[k] = i < np ? __ldg(probe + i) : 0;
+    h[k] = mix64((u64)key[k]) & ht.mask;
+  }
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    st[k] = ht.start[h[k]];
+    kk[k] = ht.key[h[k]];
+  }
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
+    s[k] = 0;
+    c[k] = 0;
+    if (i >= np || st[k] == 0) continue;
+    if (kk[k] == key[k]) {
+      s[k] = st[k] - 1;
+      c[k] = ht.count[h[k]];
+    } else {
+      join_lookup(ht, key[k], &s[k], &c[k]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kJoinThreads)
     join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
                       i64* __restrict__ tile_counts) {
   __shared__ i64 warp_sums[kJoinThreads / 32];
   const i64 tile = blockIdx.x;
+  i64 s[kJoinPer], c[kJoinPer];
+  join_lookup_batch(ht, probe, np, tile, s, c);
   i64 local = 0;
-  for (int k = 0; k < kJoinTile / kJoinThreads; ++k) {
-    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
-    if (i < np) {
-      i64 s, c;
-      join_lookup(ht, __ldg(probe + i), &s, &c);
-      local += c;
-    }
-  }
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) local += c[k];
   local = warp_sum(local);
   if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = local;
   __syncthreads();
@@ -549,11 +580,13 @@ __global__ void __launch_bounds__(kJoinThreads)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
   if (threadIdx.x == 0) running = tile_offsets[tile];
+  i64 sv[kJoinPer], cv[kJoinPer];
+  join_lookup_batch(ht, probe, np, tile, sv, cv);
   __syncthreads();
-  for (int k = 0; k < kJoinTile / kJoinThreads; ++k) {
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
     const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
-    i64 s = 0, c = 0;
-    if (i < np) join_lookup(ht, __ldg(probe + i), &s, &c);
+    const i64 s = sv[k], c = cv[k];
     // block-wide exclusive scan of c (row order = thread order)
     i64 incl = c;
 #pragma unroll

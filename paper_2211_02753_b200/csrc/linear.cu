@@ -185,13 +185,13 @@ __global__ void __launch_bounds__(kThreadsL)
       const int q = threadIdx.x + a * kThreadsL;
       const int c = q % nfeat, rg = q / nfeat;
       if (rg >= ngroups || (a == 1 && nfeat <= kThreadsL)) continue;
-      T s[K];
+      double s[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j) s[j] = T(0);
+      for (int j = 0; j < K; ++j) s[j] = 0.0;
       for (int r = rg; r < tile; r += ngroups) {
-        const T x = c < d ? sx[r * (d + 1) + c] : T(1);
+        const double x = c < d ? (double)sx[r * (d + 1) + c] : 1.0;
 #pragma unroll
-        for (int j = 0; j < K; ++j) s[j] += x * sg[r * K + j];
+        for (int j = 0; j < K; ++j) s[j] += x * (double)sg[r * K + j];
       }
 #pragma unroll
       for (int j = 0; j < K; ++j) acc[a][j] += (double)s[j];
@@ -214,6 +214,256 @@ __global__ void __launch_bounds__(kThreadsL)
     double v = 0.0;
     for (int rg = 0; rg < ngroups; ++rg) v += red[(size_t)rg * nfeat * K + e];
     // layout of the partial row: dW (d*K, row-major [c][j]) then db (K)
+    part[(i64)blockIdx.x * W + e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bulk-copy ring variants: one producer warp streams contiguous row tiles of X
+// (rows*d*sizeof(T) bytes each) into a shared-memory ring with
+// cp.async.bulk (TMA engine); 8 consumer warps compute from shared memory.
+// Unpadded tiles are conflict-free for both kernels (a warp reads consecutive
+// features of one row).  Used when d*sizeof(T) is a multiple of 16 bytes.
+// ---------------------------------------------------------------------------
+constexpr int kRingWarps = 8;
+constexpr int kRingThreads = (kRingWarps + 1) * 32;
+
+struct RingShape {
+  int rows;   // rows per stage (multiple of 32)
+  int stages;
+  size_t stage_bytes;
+};
+
+template <class T>
+RingShape ring_shape(int d) {
+  RingShape r;
+  const size_t row_bytes = (size_t)d * sizeof(T);
+  int rows = (int)((48 * 1024) / row_bytes);
+  rows = (rows / 32) * 32;
+  if (rows > 256) rows = 256;
+  if (rows < 32) rows = 32;
+  r.rows = rows;
+  r.stage_bytes = (size_t)rows * row_bytes;
+  int st = (int)((192 * 1024) / r.stage_bytes);
+  r.stages = st < 2 ? 2 : (st > 4 ? 4 : st);
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ void ring_produce(const T* __restrict__ X, i64 n, int d, int rows,
+                                             int stages, size_t stage_bytes, unsigned char* ring,
+                                             u64* full, u64* empty) {
+  const unsigned long long pol = l2_evict_first_policy();
+  const i64 ntiles = (n + rows - 1) / rows;
+  int s = 0;
+  unsigned eph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&empty[s]), eph ^ 1u);
+    const i64 r0 = t * rows;
+    const i64 nr = (n - r0) < rows ? (n - r0) : rows;
+    const unsigned bytes = (unsigned)(nr * d * (i64)sizeof(T));
+    mbar_expect_tx(smem_addr(&full[s]), bytes);
+    bulk_load(smem_addr(ring + (size_t)s * stage_bytes), X + r0 * d, bytes, smem_addr(&full[s]),
+              pol);
+    if (++s == stages) {
+      s = 0;
+      eph ^= 1u;
+    }
+  }
+}
+
+template <class T, int K>
+__global__ void __launch_bounds__(kRingThreads)
+    linear_fwd_ring_kernel(const T* __restrict__ X, i64 n, int d, int rows, int stages,
+                           const T* __restrict__ W, const T* __restrict__ bias, T* __restrict__ Y) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) u64 full[4];
+  __shared__ __align__(8) u64 empty[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t stage_bytes = (size_t)rows * d * sizeof(T);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_addr(&full[s]), 1);
+      mbar_init(smem_addr(&empty[s]), kRingWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kRingWarps) {
+    if (lane == 0) ring_produce<T>(X, n, d, rows, stages, stage_bytes, ring, full, empty);
+    return;
+  }
+  constexpr int kF = kMaxD / 32;
+  const int nf = (d + 31) / 32;
+  T w[kF][K];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const int c = f * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < K; ++j) w[f][j] = (f < nf && c < d) ? W[c * K + j] : T(0);
+  }
+  T bj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
+  const i64 ntiles = (n + rows - 1) / rows;
+  int s = 0;
+  unsigned fph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&full[s]), fph);
+    const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+    const i64 r0 = t * rows;
+    for (int g = warp; g < rows / 32; g += kRingWarps) {
+      if (r0 + g * 32 >= n) break;
+      if constexpr (K > 2) {
+        for (int r = 0; r < 32; ++r) {
+          const i64 row = r0 + g * 32 + r;
+          if (row >= n) break;
+          const T* xr = sx + (size_t)(g * 32 + r) * d;
+          T q[K];
+#pragma unroll
+          for (int j = 0; j < K; ++j) q[j] = T(0);
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            const int c = f * 32 + lane;
+            if (f < nf && c < d) {
+              const T x = xr[c];
+#pragma unroll
+              for (int j = 0; j < K; ++j) q[j] += x * w[f][j];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j) q[j] = warp_sum(q[j]);
+          if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) Y[row * K + j] = q[j] + bj[j];
+          }
+        }
+      } else {
+        T p[32][K];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const bool valid = r0 + g * 32 + r < n;
+          const T* xr = sx + (size_t)(g * 32 + r) * d;
+#pragma unroll
+          for (int j = 0; j < K; ++j) p[r][j] = T(0);
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            const int c = f * 32 + lane;
+            if (f < nf) {
+              const T x = (valid && c < d) ? xr[c] : T(0);
+#pragma unroll
+              for (int j = 0; j < K; ++j) p[r][j] += x * w[f][j];
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool upper = (lane & o) != 0;
+#pragma unroll
+          for (int r = 0; r < o; ++r) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              const T send = upper ? p[r][j] : p[r + o][j];
+              const T keep = upper ? p[r + o][j] : p[r][j];
+              p[r][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+        }
+        const i64 row = r0 + g * 32 + lane;
+        if (row < n) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) Y[row * K + j] = p[0][j] + bj[j];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
+    if (++s == stages) {
+      s = 0;
+      fph ^= 1u;
+    }
+  }
+}
+
+template <class T, int K>
+__global__ void __launch_bounds__(kRingThreads)
+    linear_wgrad_ring_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d,
+                             int rows, int stages, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) u64 full[4];
+  __shared__ __align__(8) u64 empty[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t stage_bytes = (size_t)rows * d * sizeof(T);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_addr(&full[s]), 1);
+      mbar_init(smem_addr(&empty[s]), kRingWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int nfeat = d + 1;  // feature d is the bias (x = 1)
+  const int ct = kRingWarps * 32;
+  const int ngroups = ct / nfeat > 0 ? ct / nfeat : 1;
+  double acc[2][K];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[a][j] = 0.0;
+  if (warp == kRingWarps) {
+    if (lane == 0) ring_produce<T>(X, n, d, rows, stages, stage_bytes, ring, full, empty);
+  } else {
+    const i64 ntiles = (n + rows - 1) / rows;
+    int s = 0;
+    unsigned fph = 0;
+    for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(smem_addr(&full[s]), fph);
+      const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+      const i64 r0 = t * rows;
+      const int nr = (int)((n - r0) < rows ? (n - r0) : rows);
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int q = threadIdx.x + a * ct;
+        const int c = q % nfeat, rg = q / nfeat;
+        if (rg >= ngroups || (a == 1 && nfeat <= ct)) continue;
+        double sum[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) sum[j] = 0.0;
+        for (int r = rg; r < nr; r += ngroups) {
+          const double x = c < d ? (double)sx[(size_t)r * d + c] : 1.0;
+          const T* gr = G + (r0 + r) * K;
+#pragma unroll
+          for (int j = 0; j < K; ++j) sum[j] += x * (double)__ldg(gr + j);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[a][j] += sum[j];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
+      if (++s == stages) {
+        s = 0;
+        fph ^= 1u;
+      }
+    }
+  }
+  // combine row groups through the (now idle) ring memory
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(ring);
+  if (warp < kRingWarps) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int q = threadIdx.x + a * ct;
+      const int c = q % nfeat, rg = q / nfeat;
+      if (rg >= ngroups || (a == 1 && nfeat <= ct)) continue;
+#pragma unroll
+      for (int j = 0; j < K; ++j) red[(size_t)rg * nfeat * K + c * K + j] = acc[a][j];
+    }
+  }
+  __syncthreads();
+  const int W = d * K + K;
+  for (int e = threadIdx.x; e < nfeat * K; e += blockDim.x) {
+    double v = 0.0;
+    for (int rg = 0; rg < ngroups; ++rg) v += red[(size_t)rg * nfeat * K + e];
     part[(i64)blockIdx.x * W + e] = v;
   }
 }
@@ -261,7 +511,38 @@ template <class T>
 int wgrad_grid(i64 n, int d) { return stream_grid((n + tile_rows<T>(d) - 1) / tile_rows<T>(d), 1, 2); }
 
 template <class T>
+bool ring_ok(const T* X, i64 n, int d) {
+  return ((size_t)d * sizeof(T)) % 16 == 0 && (((uintptr_t)X) & 15) == 0 &&
+         n >= (i64)ring_shape<T>(d).rows * 4;
+}
+
+template <class T>
+int ring_wgrad_grid(i64 n, int d) {
+  return stream_grid((n + ring_shape<T>(d).rows - 1) / ring_shape<T>(d).rows, 1, 1);
+}
+
+template <class T>
 int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cudaStream_t st) {
+  if (ring_ok<T>(X, n, d)) {
+    const RingShape rs = ring_shape<T>(d);
+    const size_t smem = rs.stages * rs.stage_bytes;
+    const int grid = stream_grid((n + rs.rows - 1) / rs.rows, 1, 1);
+    switch (k) {
+#define TDP_CASE(KK)                                                                         \
+  case KK:                                                                                   \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_ring_kernel<T, KK>,                         \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_fwd_ring_kernel<T, KK><<<grid, kRingThreads, smem, st>>>(X, n, d, rs.rows,        \
+                                                                    rs.stages, W, b, Y);     \
+    break;
+      TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
+#undef TDP_CASE
+      default:
+        return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
+    }
+    TDP_LAUNCH_CHECK("linear_fwd_ring_kernel");
+    return TDP_OK;
+  }
   const size_t smem = fwd_smem<T>(d, k);
   const int tile = tile_rows<T>(d);
   const int grid = stream_grid((n + tile - 1) / tile, 1, 4);
@@ -285,6 +566,32 @@ int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cu
 template <class T>
 int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, double* ws,
                  size_t ws_bytes, cudaStream_t st) {
+  if (ring_ok<T>(X, n, d)) {
+    const RingShape rs = ring_shape<T>(d);
+    const size_t red = (size_t)(kRingWarps * 32 + d + 1) * k * sizeof(double);
+    const size_t smem = rs.stages * rs.stage_bytes > red ? rs.stages * rs.stage_bytes : red;
+    const int grid = ring_wgrad_grid<T>(n, d);
+    const int width = d * k + k;
+    TDP_REQUIRE(ws_bytes >= (size_t)grid * width * sizeof(double), "linear_wgrad workspace too small");
+    switch (k) {
+#define TDP_CASE(KK)                                                                         \
+  case KK:                                                                                   \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_ring_kernel<T, KK>,                       \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_wgrad_ring_kernel<T, KK><<<grid, kRingThreads, smem, st>>>(X, G, n, d, rs.rows,   \
+                                                                      rs.stages, ws);        \
+    break;
+      TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
+#undef TDP_CASE
+      default:
+        return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
+    }
+    TDP_LAUNCH_CHECK("linear_wgrad_ring_kernel");
+    wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(
+        ws, grid, width, dW, db, d * k);
+    TDP_LAUNCH_CHECK("wgrad_reduce_kernel");
+    return TDP_OK;
+  }
   const int grid = wgrad_grid<T>(n, d);
   const int width = d * k + k;
   const size_t smem = wgrad_smem<T>(d, k);
@@ -334,8 +641,10 @@ int tdp_linear_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k
 }
 
 size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k) {
-  const int g = wgrad_grid<double>(n, d) > wgrad_grid<float>(n, d) ? wgrad_grid<double>(n, d)
-                                                                    : wgrad_grid<float>(n, d);
+  int g = wgrad_grid<double>(n, d);
+  const int cands[3] = {wgrad_grid<float>(n, d), ring_wgrad_grid<float>(n, d),
+                        ring_wgrad_grid<double>(n, d)};
+  for (int c : cands) g = c > g ? c : g;
   return (size_t)g * (size_t)(d * k + k) * sizeof(double) + 256;
 }
 

@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from .autograd import SoftKeySpec, gather_many, gather_rows_raw, soft_groupby_grid
 from .encodings import (
     DictionaryEncoding,
     EncodedTensor,
@@ -42,6 +43,7 @@ from .encodings import (
     trusted,
 )
 from .lazy import (
+    native_predicates,
     Expr,
     LazyValue,
     Pred,
@@ -71,6 +73,9 @@ from .tensor import (
     active_tape,
     add,
     div,
+    dtype_name,
+    gather,
+    slice_axis,
     mul,
     reshape,
     tensor,
@@ -104,16 +109,10 @@ def take_rows(col: EncodedTensor, indices) -> EncodedTensor:
     oh = onehot_payload(v)
     with trusted():
         if oh is not None:
-            from .autograd import gather_rows_raw
-
             return EncodedTensor(Tensor(OneHotValue(gather_rows_raw(oh.codes, idx), oh.k, oh.dtype)),
                                  col.encoding)
         if v.dtype in FLOAT_DTYPES and active_tape() is not None:
-            from .tensor import gather
-
             return EncodedTensor(gather(v, Tensor(idx), axis=0), col.encoding)
-        from .autograd import gather_rows_raw
-
         return EncodedTensor(Tensor(gather_rows_raw(v.data, idx)), col.encoding)
 
 
@@ -150,8 +149,6 @@ def comparison_mask(col: EncodedTensor, op: str, literal) -> torch.Tensor:
     cols = [data] if p.col is not None else []
     if n:
         nat.require_cuda(out, *cols)
-        from .lazy import native_predicates
-
         nat.call("tdp_filter_mask", nat.columns(cols), len(cols),
                  native_predicates([p], {id(c): i for i, c in enumerate(cols)}), 1, n,
                  nat.ptr(out), nat.stream())
@@ -255,8 +252,6 @@ def _value_dtype(v) -> str:
     if isinstance(v, Tensor):
         return v.dtype
     if isinstance(v, torch.Tensor):
-        from .tensor import dtype_name
-
         return dtype_name(v)
     return np.asarray(v).dtype.name
 
@@ -559,8 +554,6 @@ def _groupby_general(keys, key_vals, agg_specs, agg_vals):
 
 def _lex_order(keys: Sequence[torch.Tensor]) -> torch.Tensor:
     """Stable lexicographic order of key tuples (LSD over the key columns)."""
-    from .autograd import gather_rows_raw
-
     order = None
     for k in reversed(list(keys)):
         kk = k if order is None else gather_rows_raw(k, order)
@@ -573,8 +566,6 @@ def _groupby_sharded(kdata, agg_specs, vdata, group):
     """High-cardinality group-by across ranks: repartition rows by key with
     an NCCL all-to-all, group locally (every group now lives on one rank),
     all-gather the (small) results and order them by key."""
-    from .autograd import gather_many, gather_rows_raw
-
     world = world_size(group)
     device = kdata[0].device
     dest = key_destination(kdata, world)
@@ -614,8 +605,6 @@ def _groupby_local(kdata, agg_specs, agg_vals):
         key_values = []
         rem = occupied.clone()
         for u, s in zip(reversed(uniqs), reversed(spaces)):
-            from .autograd import gather_rows_raw
-
             key_values.append(gather_rows_raw(u, (rem % s).contiguous()))
             rem = rem // s
         key_values.reverse()
@@ -694,8 +683,6 @@ class GroupedCounts:
 
 
 def _soft_inputs(pes: Sequence[EncodedTensor]):
-    from .autograd import SoftKeySpec
-
     kinds, tensors, dts = [], [], []
     tape = active_tape()
     for p in pes:
@@ -742,8 +729,6 @@ def soft_groupby(pes: Sequence[EncodedTensor], agg: str = "count",
     numeric column.  The n x prod(k) joint is never materialised.
     """
     spaces, n = _joint_spaces(pes)
-    from .autograd import soft_groupby_grid
-
     spec, keys, dts = _soft_inputs(pes)
     nat.require_cuda(*keys)
     joint_dt = dts[0]
@@ -846,8 +831,6 @@ def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTens
                 continue
             v = c.values
             if v.dtype in FLOAT_DTYPES and active_tape() is not None:
-                from .tensor import slice_axis
-
                 out.append(EncodedTensor(slice_axis(v, 0, 0, m), c.encoding))
             else:
                 out.append(EncodedTensor(Tensor(v.data[:m]), c.encoding))
@@ -902,8 +885,6 @@ def _side_sources(cols: Sequence[EncodedTensor]):
 
 
 def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tensor):
-    from .autograd import gather_many, gather_rows_raw
-
     if any(onehot_payload(c.values) is not None for c in cols):
         return [take_rows(c, rows if rowmap is None else gather_rows_raw(rowmap, rows))
                 for c in cols]
@@ -930,8 +911,6 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
         return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
     lb, lmap = _side_sources(left)
     rb, rmap = _side_sources(right)
-    from .autograd import gather_rows_raw
-
     lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
     rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
     pi, bi = join_indices(lkey, rkey)

@@ -29,6 +29,8 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import autograd as _ag
+from . import tensor as _T
 
 INT64_MIN, INT64_MAX = -(2**63), 2**63 - 1
 
@@ -164,9 +166,7 @@ class Expr:
 
     @staticmethod
     def column(t: torch.Tensor) -> "Expr":
-        from .tensor import dtype_name
-
-        return Expr("col", dtype_name(t), col=t)
+        return Expr("col", _T.dtype_name(t), col=t)
 
     @staticmethod
     def const(value, dtype: str) -> "Expr":
@@ -205,9 +205,7 @@ class LazyValue:
         if e.op == "col":
             if self.sel is None:
                 return e.col
-            from .autograd import gather_rows_raw
-
-            return gather_rows_raw(e.col, self.sel.indices())
+            return _ag.gather_rows_raw(e.col, self.sel.indices())
         return project([e], self.sel)[0]
 
 
@@ -227,9 +225,7 @@ def lazy_view(t: torch.Tensor, sel: Selection, valid_for=None) -> LazyValue:
 
 def as_expr(value) -> tuple[Expr, Optional[Selection]]:
     """(expression, selection) of a Tensor (lazy or materialised) or torch tensor."""
-    from .tensor import Tensor
-
-    if isinstance(value, Tensor):
+    if isinstance(value, _T.Tensor):
         if value._t is None:
             return value._lazy.expr, value._lazy.sel
         value = value._t
@@ -238,9 +234,7 @@ def as_expr(value) -> tuple[Expr, Optional[Selection]]:
 
 def _lazy_operand(t, rdt: str):
     """Expr and selection for ``t`` as an operand of a lazy op, or None."""
-    from .tensor import Tensor
-
-    if not isinstance(t, Tensor):
+    if not isinstance(t, _T.Tensor):
         return None
     if t._t is None:
         lv = t._lazy
@@ -268,9 +262,7 @@ def try_lazy_binary(op: str, a, b, rdt: str):
     sel = sa if sa is not None else sb
     if op == "div" and rdt == "int64":
         return None
-    from .tensor import Tensor
-
-    return Tensor(LazyValue(Expr(op, rdt, (la[0], lb[0])), sel))
+    return _T.Tensor(LazyValue(Expr(op, rdt, (la[0], lb[0])), sel))
 
 
 def try_lazy_unary(op: str, a, rdt: str):
@@ -281,9 +273,7 @@ def try_lazy_unary(op: str, a, rdt: str):
         return None
     if op in ("log", "exp", "relu") and rdt == "int64":
         return None
-    from .tensor import Tensor
-
-    return Tensor(LazyValue(Expr(op, rdt, (la[0],)), la[1]))
+    return _T.Tensor(LazyValue(Expr(op, rdt, (la[0],)), la[1]))
 
 
 # ---------------------------------------------------------------------------
@@ -374,13 +364,11 @@ def project(exprs: Sequence[Expr], sel: Optional[Selection]) -> list[torch.Tenso
     nat.require_cuda(*prog.cols)
     device = prog.cols[0].device if prog.cols else (sel.device if sel else torch.device("cuda"))
     m = sel.count() if sel is not None else n
-    from .tensor import torch_dtype
-
-    results = [torch.empty(m, dtype=torch_dtype(e.dtype), device=device) for e in exprs]
+    results = [torch.empty(m, dtype=_T.torch_dtype(e.dtype), device=device) for e in exprs]
     if m == 0 or not prog.cols:
         if not prog.cols:  # constant expression
             return [torch.full((m,), float(e.value) if e.dtype != "int64" else int(e.value),
-                               dtype=torch_dtype(e.dtype), device=device) for e in exprs]
+                               dtype=_T.torch_dtype(e.dtype), device=device) for e in exprs]
         return results
     count = torch.empty(1, dtype=torch.int64, device=device)
     ws = nat.workspace(nat.load().tdp_filter_workspace(n), device)

@@ -249,22 +249,36 @@ RingShape ring_shape(int d) {
   return r;
 }
 
+// Producer: per stage, the tile's X rows (in 8 KB bulk copies, so several
+// requests are in flight) and, when G != nullptr, its G rows behind them.
+// Returns through *g_in_smem whether G tiles are staged (their byte count must
+// be a multiple of 16 for every tile).
 template <class T>
-__device__ __forceinline__ void ring_produce(const T* __restrict__ X, i64 n, int d, int rows,
-                                             int stages, size_t stage_bytes, unsigned char* ring,
-                                             u64* full, u64* empty) {
+__device__ __forceinline__ void ring_produce(const T* __restrict__ X, const T* __restrict__ G, int K,
+                                             i64 n, int d, int rows, int stages,
+                                             size_t stage_bytes, unsigned char* ring, u64* full,
+                                             u64* empty) {
   const unsigned long long pol = l2_evict_first_policy();
   const i64 ntiles = (n + rows - 1) / rows;
+  constexpr unsigned kChunk = 8 * 1024;
   int s = 0;
   unsigned eph = 0;
   for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(smem_addr(&empty[s]), eph ^ 1u);
     const i64 r0 = t * rows;
     const i64 nr = (n - r0) < rows ? (n - r0) : rows;
-    const unsigned bytes = (unsigned)(nr * d * (i64)sizeof(T));
-    mbar_expect_tx(smem_addr(&full[s]), bytes);
-    bulk_load(smem_addr(ring + (size_t)s * stage_bytes), X + r0 * d, bytes, smem_addr(&full[s]),
-              pol);
+    const unsigned xbytes = (unsigned)(nr * d * (i64)sizeof(T));
+    const unsigned gbytes = G ? (unsigned)(nr * K * (i64)sizeof(T)) : 0u;
+    const unsigned bar = smem_addr(&full[s]);
+    mbar_expect_tx(bar, xbytes + gbytes);
+    unsigned char* dst = ring + (size_t)s * stage_bytes;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(X + r0 * d);
+    for (unsigned off = 0; off < xbytes; off += kChunk) {
+      const unsigned b = xbytes - off < kChunk ? xbytes - off : kChunk;
+      bulk_load(smem_addr(dst + off), src + off, b, bar, pol);
+    }
+    if (G)
+      bulk_load(smem_addr(dst + (size_t)rows * d * sizeof(T)), G + r0 * K, gbytes, bar, pol);
     if (++s == stages) {
       s = 0;
       eph ^= 1u;
@@ -290,7 +304,7 @@ __global__ void __launch_bounds__(kRingThreads)
   }
   __syncthreads();
   if (warp == kRingWarps) {
-    if (lane == 0) ring_produce<T>(X, n, d, rows, stages, stage_bytes, ring, full, empty);
+    if (lane == 0) ring_produce<T>(X, nullptr, 0, n, d, rows, stages, stage_bytes, ring, full, empty);
     return;
   }
   constexpr int kF = kMaxD / 32;
@@ -388,12 +402,17 @@ __global__ void __launch_bounds__(kRingThreads)
 template <class T, int K>
 __global__ void __launch_bounds__(kRingThreads)
     linear_wgrad_ring_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d,
-                             int rows, int stages, double* __restrict__ part) {
+                             int rows, int stages, int stage_g, double* __restrict__ part) {
+  // Warp w takes rows w, w+8, ... of each staged tile; lane l owns features
+  // l, l+32, ...: per row one conflict-free shared-memory read of the X row,
+  // a broadcast read of the G row, independent float64 FMAs per (feature,
+  // class).  Lane 0 also sums G for the bias.  One partial row per warp.
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) u64 full[4];
   __shared__ __align__(8) u64 empty[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t stage_bytes = (size_t)rows * d * sizeof(T);
+  const size_t xbytes = (size_t)rows * d * sizeof(T);
+  const size_t stage_bytes = xbytes + (size_t)rows * K * sizeof(T);
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(smem_addr(&full[s]), 1);
@@ -402,69 +421,69 @@ __global__ void __launch_bounds__(kRingThreads)
     mbar_fence_init();
   }
   __syncthreads();
-  const int nfeat = d + 1;  // feature d is the bias (x = 1)
-  const int ct = kRingWarps * 32;
-  const int ngroups = ct / nfeat > 0 ? ct / nfeat : 1;
-  double acc[2][K];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int j = 0; j < K; ++j) acc[a][j] = 0.0;
   if (warp == kRingWarps) {
-    if (lane == 0) ring_produce<T>(X, n, d, rows, stages, stage_bytes, ring, full, empty);
-  } else {
-    const i64 ntiles = (n + rows - 1) / rows;
-    int s = 0;
-    unsigned fph = 0;
-    for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(smem_addr(&full[s]), fph);
-      const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
-      const i64 r0 = t * rows;
-      const int nr = (int)((n - r0) < rows ? (n - r0) : rows);
+    if (lane == 0)
+      ring_produce<T>(X, stage_g ? G : nullptr, K, n, d, rows, stages, stage_bytes, ring, full,
+                      empty);
+    return;
+  }
+  constexpr int kF = kMaxD / 32;
+  const int nf = (d + 31) / 32;
+  double acc[kF][K];
+  double bacc[K];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int q = threadIdx.x + a * ct;
-        const int c = q % nfeat, rg = q / nfeat;
-        if (rg >= ngroups || (a == 1 && nfeat <= ct)) continue;
-        double sum[K];
+  for (int f = 0; f < kF; ++f)
 #pragma unroll
-        for (int j = 0; j < K; ++j) sum[j] = 0.0;
-        for (int r = rg; r < nr; r += ngroups) {
-          const double x = c < d ? (double)sx[(size_t)r * d + c] : 1.0;
-          const T* gr = G + (r0 + r) * K;
+    for (int j = 0; j < K; ++j) acc[f][j] = 0.0;
 #pragma unroll
-          for (int j = 0; j < K; ++j) sum[j] += x * (double)__ldg(gr + j);
+  for (int j = 0; j < K; ++j) bacc[j] = 0.0;
+  const i64 ntiles = (n + rows - 1) / rows;
+  int s = 0;
+  unsigned fph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&full[s]), fph);
+    const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+    const T* sg = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes + xbytes);
+    const i64 r0 = t * rows;
+    const int nr = (int)((n - r0) < rows ? (n - r0) : rows);
+    for (int r = warp; r < nr; r += kRingWarps) {
+      double g[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        g[j] = stage_g ? (double)sg[r * K + j] : (double)__ldg(G + (r0 + r) * K + j);
+      const T* xr = sx + (size_t)r * d;
+#pragma unroll
+      for (int f = 0; f < kF; ++f) {
+        const int c = f * 32 + lane;
+        if (f < nf && c < d) {
+          const double x = (double)xr[c];
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc[f][j] += x * g[j];
         }
+      }
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc[a][j] += sum[j];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
-      if (++s == stages) {
-        s = 0;
-        fph ^= 1u;
-      }
+      for (int j = 0; j < K; ++j) bacc[j] += g[j];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
+    if (++s == stages) {
+      s = 0;
+      fph ^= 1u;
     }
   }
-  // combine row groups through the (now idle) ring memory
-  __syncthreads();
-  double* red = reinterpret_cast<double*>(ring);
-  if (warp < kRingWarps) {
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int q = threadIdx.x + a * ct;
-      const int c = q % nfeat, rg = q / nfeat;
-      if (rg >= ngroups || (a == 1 && nfeat <= ct)) continue;
-#pragma unroll
-      for (int j = 0; j < K; ++j) red[(size_t)rg * nfeat * K + c * K + j] = acc[a][j];
-    }
-  }
-  __syncthreads();
   const int W = d * K + K;
-  for (int e = threadIdx.x; e < nfeat * K; e += blockDim.x) {
-    double v = 0.0;
-    for (int rg = 0; rg < ngroups; ++rg) v += red[(size_t)rg * nfeat * K + e];
-    part[(i64)blockIdx.x * W + e] = v;
+  double* out = part + ((i64)blockIdx.x * kRingWarps + warp) * W;
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const int c = f * 32 + lane;
+    if (f < nf && c < d) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) out[c * K + j] = acc[f][j];
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[d * K + j] = bacc[j];
   }
 }
 
@@ -568,18 +587,22 @@ int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, doub
                  size_t ws_bytes, cudaStream_t st) {
   if (ring_ok<T>(X, n, d)) {
     const RingShape rs = ring_shape<T>(d);
-    const size_t red = (size_t)(kRingWarps * 32 + d + 1) * k * sizeof(double);
-    const size_t smem = rs.stages * rs.stage_bytes > red ? rs.stages * rs.stage_bytes : red;
+    const size_t stage = rs.stage_bytes + (size_t)rs.rows * k * sizeof(T);
+    const size_t smem = rs.stages * stage;
     const int grid = ring_wgrad_grid<T>(n, d);
     const int width = d * k + k;
-    TDP_REQUIRE(ws_bytes >= (size_t)grid * width * sizeof(double), "linear_wgrad workspace too small");
+    const int prow = grid * kRingWarps;
+    const int stage_g = (((size_t)rs.rows * k * sizeof(T)) % 16 == 0) &&
+                        (((size_t)(n % rs.rows) * k * sizeof(T)) % 16 == 0) &&
+                        ((((uintptr_t)G) & 15) == 0);
+    TDP_REQUIRE(ws_bytes >= (size_t)prow * width * sizeof(double), "linear_wgrad workspace too small");
     switch (k) {
 #define TDP_CASE(KK)                                                                         \
   case KK:                                                                                   \
     TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_ring_kernel<T, KK>,                       \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     linear_wgrad_ring_kernel<T, KK><<<grid, kRingThreads, smem, st>>>(X, G, n, d, rs.rows,   \
-                                                                      rs.stages, ws);        \
+                                                                      rs.stages, stage_g, ws); \
     break;
       TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
 #undef TDP_CASE
@@ -588,7 +611,7 @@ int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, doub
     }
     TDP_LAUNCH_CHECK("linear_wgrad_ring_kernel");
     wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(
-        ws, grid, width, dW, db, d * k);
+        ws, prow, width, dW, db, d * k);
     TDP_LAUNCH_CHECK("wgrad_reduce_kernel");
     return TDP_OK;
   }
@@ -642,8 +665,8 @@ int tdp_linear_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k
 
 size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k) {
   int g = wgrad_grid<double>(n, d);
-  const int cands[3] = {wgrad_grid<float>(n, d), ring_wgrad_grid<float>(n, d),
-                        ring_wgrad_grid<double>(n, d)};
+  const int cands[3] = {wgrad_grid<float>(n, d), ring_wgrad_grid<float>(n, d) * kRingWarps,
+                        ring_wgrad_grid<double>(n, d) * kRingWarps};
   for (int c : cands) g = c > g ? c : g;
   return (size_t)g * (size_t)(d * k + k) * sizeof(double) + 256;
 }

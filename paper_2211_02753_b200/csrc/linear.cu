@@ -286,7 +286,7 @@ __device__ __forceinline__ void ring_produce(const T* __restrict__ X, const T* _
   }
 }
 
-template <class T, int K>
+template <class T, int K, int NF>
 __global__ void __launch_bounds__(kRingThreads)
     linear_fwd_ring_kernel(const T* __restrict__ X, i64 n, int d, int rows, int stages,
                            const T* __restrict__ W, const T* __restrict__ bias, T* __restrict__ Y) {
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kRingThreads)
     if (lane == 0) ring_produce<T>(X, nullptr, 0, n, d, rows, stages, stage_bytes, ring, full, empty);
     return;
   }
-  constexpr int kF = kMaxD / 32;
+  constexpr int kF = NF;
   const int nf = (d + 31) / 32;
   T w[kF][K];
 #pragma unroll
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kRingThreads)
   }
 }
 
-template <class T, int K>
+template <class T, int K, int NF>
 __global__ void __launch_bounds__(kRingThreads)
     linear_wgrad_ring_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int d,
                              int rows, int stages, int stage_g, double* __restrict__ part) {
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kRingThreads)
                       empty);
     return;
   }
-  constexpr int kF = kMaxD / 32;
+  constexpr int kF = NF;
   const int nf = (d + 31) / 32;
   double acc[kF][K];
   double bacc[K];
@@ -529,6 +529,12 @@ size_t wgrad_smem(int d, int k) {
 template <class T>
 int wgrad_grid(i64 n, int d) { return stream_grid((n + tile_rows<T>(d) - 1) / tile_rows<T>(d), 1, 2); }
 
+// feature groups of 32 lanes, rounded up to a power of two (kernel template)
+inline int nf_bucket(int d) {
+  const int nf = (d + 31) / 32;
+  return nf <= 1 ? 1 : nf <= 2 ? 2 : nf <= 4 ? 4 : 8;
+}
+
 template <class T>
 bool ring_ok(const T* X, i64 n, int d) {
   return ((size_t)d * sizeof(T)) % 16 == 0 && (((uintptr_t)X) & 15) == 0 &&
@@ -546,19 +552,21 @@ int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cu
     const RingShape rs = ring_shape<T>(d);
     const size_t smem = rs.stages * rs.stage_bytes;
     const int grid = stream_grid((n + rs.rows - 1) / rs.rows, 1, 1);
-    switch (k) {
-#define TDP_CASE(KK)                                                                         \
-  case KK:                                                                                   \
-    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_ring_kernel<T, KK>,                         \
+    const int nf = nf_bucket(d);
+    bool launched = false;
+#define TDP_CASE(KK, NN)                                                                     \
+  if (k == KK && nf == NN) {                                                                 \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_ring_kernel<T, KK, NN>,                     \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    linear_fwd_ring_kernel<T, KK><<<grid, kRingThreads, smem, st>>>(X, n, d, rs.rows,        \
-                                                                    rs.stages, W, b, Y);     \
-    break;
-      TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
+    linear_fwd_ring_kernel<T, KK, NN><<<grid, kRingThreads, smem, st>>>(X, n, d, rs.rows,    \
+                                                                        rs.stages, W, b, Y); \
+    launched = true;                                                                         \
+  }
+#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2) TDP_CASE(KK, 4) TDP_CASE(KK, 8)
+    TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
+#undef TDP_CASES
 #undef TDP_CASE
-      default:
-        return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
-    }
+    if (!launched) return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
     TDP_LAUNCH_CHECK("linear_fwd_ring_kernel");
     return TDP_OK;
   }
@@ -596,19 +604,21 @@ int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, doub
                         (((size_t)(n % rs.rows) * k * sizeof(T)) % 16 == 0) &&
                         ((((uintptr_t)G) & 15) == 0);
     TDP_REQUIRE(ws_bytes >= (size_t)prow * width * sizeof(double), "linear_wgrad workspace too small");
-    switch (k) {
-#define TDP_CASE(KK)                                                                         \
-  case KK:                                                                                   \
-    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_ring_kernel<T, KK>,                       \
+    const int nf = nf_bucket(d);
+    bool launched = false;
+#define TDP_CASE(KK, NN)                                                                     \
+  if (k == KK && nf == NN) {                                                                 \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_ring_kernel<T, KK, NN>,                   \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    linear_wgrad_ring_kernel<T, KK><<<grid, kRingThreads, smem, st>>>(X, G, n, d, rs.rows,   \
-                                                                      rs.stages, stage_g, ws); \
-    break;
-      TDP_CASE(1) TDP_CASE(2) TDP_CASE(3) TDP_CASE(4) TDP_CASE(5) TDP_CASE(6) TDP_CASE(7) TDP_CASE(8)
+    linear_wgrad_ring_kernel<T, KK, NN><<<grid, kRingThreads, smem, st>>>(X, G, n, d, rs.rows, \
+                                                                          rs.stages, stage_g, ws); \
+    launched = true;                                                                         \
+  }
+#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2) TDP_CASE(KK, 4) TDP_CASE(KK, 8)
+    TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
+#undef TDP_CASES
 #undef TDP_CASE
-      default:
-        return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
-    }
+    if (!launched) return set_error(TDP_EINVAL, "linear: k=%d > %d", k, kMaxK);
     TDP_LAUNCH_CHECK("linear_wgrad_ring_kernel");
     wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(
         ws, prow, width, dW, db, d * k);

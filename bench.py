@@ -167,9 +167,17 @@ def _ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TDP_DIST_BACKEND=gloo + TDP_ONE_GPU=1 exercise the multi-rank code path on
+    # a single-GPU host (every rank on cuda:0); production runs use NCCL.
+    if os.environ.get("TDP_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TDP_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     group = dist.group.WORLD if world > 1 else None
 
     n_total = int(round(6_000_000 * args.sf))

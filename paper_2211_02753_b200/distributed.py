@@ -50,12 +50,46 @@ def world_size(group) -> int:
     return 1 if group is None else dist.get_world_size(group)
 
 
+# Collectives: NCCL on device tensors.  A gloo group (CPU tests, or several
+# ranks sharing one GPU in the test harness) gets host-staged copies.
+def _host_staged(group) -> bool:
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_reduce(t: torch.Tensor, op, group) -> None:
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def _all_to_all_single(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group) -> None:
+    if inp.is_cuda and _host_staged(group):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(h, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(h)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+
+
+def _all_gather(parts: list, t: torch.Tensor, group) -> None:
+    if t.is_cuda and _host_staged(group):
+        hs = [torch.empty(p.shape, dtype=p.dtype) for p in parts]
+        dist.all_gather(hs, t.cpu(), group=group)
+        for p, h in zip(parts, hs):
+            p.copy_(h)
+    else:
+        dist.all_gather(parts, t, group=group)
+
+
 def allreduce_ranges(lo: torch.Tensor, hi: torch.Tensor, group) -> tuple[torch.Tensor, torch.Tensor]:
     """Global [min, max] of per-rank key ranges (empty shards hold
     (INT64_MAX, INT64_MIN), the identities of MIN / MAX)."""
     if world_size(group) > 1:
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+        _all_reduce(lo, dist.ReduceOp.MIN, group)
+        _all_reduce(hi, dist.ReduceOp.MAX, group)
     return lo, hi
 
 
@@ -72,13 +106,13 @@ def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows:
     nrows = sums_raw.shape[0]
     int_rows = [r for r in range(nrows) if r not in float_rows]
     ints = torch.cat([counts.reshape(1, -1), sums_raw[int_rows]], dim=0) if int_rows else counts.reshape(1, -1).clone()
-    dist.all_reduce(ints, op=dist.ReduceOp.SUM, group=group)
+    _all_reduce(ints, dist.ReduceOp.SUM, group)
     counts.copy_(ints[0])
     for j, r in enumerate(int_rows):
         sums_raw[r].copy_(ints[1 + j])
     if float_rows:
         floats = sums_raw[float_rows].contiguous().view(torch.float64).clone()
-        dist.all_reduce(floats, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce(floats, dist.ReduceOp.SUM, group)
         for j, r in enumerate(float_rows):
             sums_raw[r].copy_(floats[j].view(torch.int64))
 
@@ -109,13 +143,13 @@ def exchange_rows(grouped: list[torch.Tensor], send_counts: torch.Tensor,
     result is deterministic.
     """
     recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    _all_to_all_single(recv_counts, send_counts, None, None, group)
     send = send_counts.tolist()
     recv = recv_counts.tolist()
     out = []
     for col in grouped:
         dst = torch.empty((sum(recv),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
-        dist.all_to_all_single(dst, col.contiguous(), recv, send, group=group)
+        _all_to_all_single(dst, col.contiguous(), recv, send, group)
         out.append(dst)
     return out
 
@@ -128,7 +162,7 @@ def allgather_rows(columns: list[torch.Tensor], group) -> list[torch.Tensor]:
     dev = columns[0].device
     n = torch.tensor([columns[0].shape[0]], dtype=torch.int64, device=dev)
     sizes = [torch.empty_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
+    _all_gather(sizes, n, group)
     sizes = [int(s) for s in sizes]
     m = max(sizes) if sizes else 0
     out = []
@@ -136,7 +170,7 @@ def allgather_rows(columns: list[torch.Tensor], group) -> list[torch.Tensor]:
         pad = torch.zeros((m,) + tuple(col.shape[1:]), dtype=col.dtype, device=dev)
         pad[: col.shape[0]] = col
         parts = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(parts, pad, group=group)
+        _all_gather(parts, pad, group)
         out.append(torch.cat([p[:s] for p, s in zip(parts, sizes)]))
     return out
 

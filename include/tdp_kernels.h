@@ -105,6 +105,12 @@ int tdp_device_sm_count(void);
 /* Total kernels launched by this library in this process (benchmark
  * accounting of "our" launches). */
 uint64_t tdp_launch_count(void);
+/* Benchmark timer of the fused pipeline kernel: while enabled, CUDA events are
+ * recorded on the launch stream immediately around every tdp_scan_agg launch
+ * (after all host-side preparation).  read() waits for the recorded events,
+ * returns the summed milliseconds and the launch count, and clears them.   */
+int tdp_kernel_timer_enable(int32_t on);
+int tdp_kernel_timer_read(double* total_ms, int64_t* launches);
 
 /* ------------------------------------------------------------------------ */
 /* filter / compaction / row movement                                        */

@@ -790,6 +790,29 @@ AggMap make_map(const Spec& s) {
 
 i64 cells_of(const Spec& s) { return s.slots * (i64)(1 + s.fvals.size() + s.ivals.size()); }
 
+// ---- kernel timer (benchmarks) ---------------------------------------------
+std::mutex g_timer_mu;
+bool g_timer_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timer_events;
+
+cudaEvent_t timer_begin(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_timer_mu);
+  if (!g_timer_on) return nullptr;
+  cudaEvent_t a = nullptr;
+  if (cudaEventCreate(&a) != cudaSuccess) return nullptr;
+  cudaEventRecord(a, st);
+  return a;
+}
+
+void timer_end(cudaEvent_t a, cudaStream_t st) {
+  if (!a) return;
+  cudaEvent_t b = nullptr;
+  if (cudaEventCreate(&b) != cudaSuccess) return;
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lock(g_timer_mu);
+  g_timer_events.emplace_back(a, b);
+}
+
 }  // namespace
 
 }  // namespace tdp
@@ -819,6 +842,32 @@ int tdp_pipeline_codegen(const tdp_column* cols, int32_t ncols, int64_t n,
     if (rc) return rc;
   }
   return (int)(src.size() > 0x7fffffff ? 0x7fffffff : src.size());
+}
+
+int tdp_kernel_timer_enable(int32_t on) {
+  std::lock_guard<std::mutex> lock(g_timer_mu);
+  g_timer_on = on != 0;
+  return TDP_OK;
+}
+
+int tdp_kernel_timer_read(double* total_ms, int64_t* launches) {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+  {
+    std::lock_guard<std::mutex> lock(g_timer_mu);
+    evs.swap(g_timer_events);
+  }
+  double total = 0.0;
+  for (auto& e : evs) {
+    float ms = 0.f;
+    TDP_CUDA_TRY(cudaEventSynchronize(e.second));
+    TDP_CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+    total += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (total_ms) *total_ms = total;
+  if (launches) *launches = (int64_t)evs.size();
+  return TDP_OK;
 }
 
 size_t tdp_scan_aggregate_workspace(int64_t n, int64_t slots, int32_t naggs) {
@@ -884,11 +933,13 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
     fill_params(hp, s, cols, ncols, n);
     hp.acc = ws;
     void* args[] = {&hp};
+    cudaEvent_t t0 = timer_begin(st);
     rc = cu_check(d,
                   d->launch(fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (CUstream)st,
                             args, nullptr),
                   use_ring ? "cuLaunchKernel(tdp_scan_agg)" : "cuLaunchKernel(tdp_scan_agg_ldg)");
     if (rc) return rc;
+    timer_end(t0, st);
     count_launch();
   }
   AggMap m = make_map(s);

@@ -487,6 +487,243 @@ __global__ void __launch_bounds__(kRingThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// vectorised ring kernels for d = 32 * V (the common model widths): lane l
+// owns the V consecutive features [l*V, l*V + V) and reads them with one
+// vector shared-memory load per row; every stage holds 256 rows (32 per
+// consumer warp) so all consumer warps work on every stage; full stages run
+// without bounds checks.
+// ---------------------------------------------------------------------------
+template <class T, int V>
+struct VecLoad;
+template <>
+struct VecLoad<float, 1> {
+  __device__ static void ld(const float* p, float* o) { o[0] = p[0]; }
+};
+template <>
+struct VecLoad<float, 2> {
+  __device__ static void ld(const float* p, float* o) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    o[0] = v.x;
+    o[1] = v.y;
+  }
+};
+template <>
+struct VecLoad<float, 4> {
+  __device__ static void ld(const float* p, float* o) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  }
+};
+template <>
+struct VecLoad<float, 8> {
+  __device__ static void ld(const float* p, float* o) {
+    VecLoad<float, 4>::ld(p, o);
+    VecLoad<float, 4>::ld(p + 4, o + 4);
+  }
+};
+template <int V>
+struct VecLoad<double, V> {
+  __device__ static void ld(const double* p, double* o) {
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      if (i + 1 < V) {
+        const double2 v = *reinterpret_cast<const double2*>(p + i);
+        o[i] = v.x;
+        o[i + 1] = v.y;
+      } else {
+        o[i] = p[i];
+      }
+    }
+  }
+};
+
+constexpr int kVecRows = kRingWarps * 32;  // rows per stage in the vector kernels
+
+template <class T, int K, int V, bool FULL>
+__device__ __forceinline__ void vec_fwd_group(const T* __restrict__ sx, int g, i64 r0, i64 n,
+                                              const T (&w)[V][K], const T (&bj)[K],
+                                              T* __restrict__ Y, int lane) {
+  constexpr int d = 32 * V;
+  T p[32][K];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    T x[V];
+    if (FULL || r0 + g * 32 + r < n) {
+      VecLoad<T, V>::ld(sx + (size_t)(g * 32 + r) * d + lane * V, x);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      T acc = x[0] * w[0][j];
+#pragma unroll
+      for (int v = 1; v < V; ++v) acc += x[v] * w[v][j];
+      p[r][j] = acc;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int r = 0; r < o; ++r) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const T send = upper ? p[r][j] : p[r + o][j];
+        const T keep = upper ? p[r + o][j] : p[r][j];
+        p[r][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+  }
+  const i64 row = r0 + g * 32 + lane;
+  if (FULL || row < n) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) Y[row * K + j] = p[0][j] + bj[j];
+  }
+}
+
+template <class T, int K, int V>
+__global__ void __launch_bounds__(kRingThreads)
+    linear_fwd_vec_kernel(const T* __restrict__ X, i64 n, int stages, const T* __restrict__ W,
+                          const T* __restrict__ bias, T* __restrict__ Y) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) u64 full[4];
+  __shared__ __align__(8) u64 empty[4];
+  constexpr int d = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t stage_bytes = (size_t)kVecRows * d * sizeof(T);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_addr(&full[s]), 1);
+      mbar_init(smem_addr(&empty[s]), kRingWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kRingWarps) {
+    if (lane == 0)
+      ring_produce<T>(X, nullptr, 0, n, d, kVecRows, stages, stage_bytes, ring, full, empty);
+    return;
+  }
+  T w[V][K];
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int j = 0; j < K; ++j) w[v][j] = W[(lane * V + v) * K + j];
+  T bj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
+  const i64 ntiles = (n + kVecRows - 1) / kVecRows;
+  int s = 0;
+  unsigned fph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&full[s]), fph);
+    const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+    const i64 r0 = t * kVecRows;
+    if (r0 + kVecRows <= n) vec_fwd_group<T, K, V, true>(sx, warp, r0, n, w, bj, Y, lane);
+    else if (r0 + warp * 32 < n) vec_fwd_group<T, K, V, false>(sx, warp, r0, n, w, bj, Y, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
+    if (++s == stages) {
+      s = 0;
+      fph ^= 1u;
+    }
+  }
+}
+
+// dW / db: warp w takes rows w, w+8, ... of each stage; lane l owns features
+// [l*V, l*V+V); per stage the products are summed in T (at most 32 rows per
+// warp) and folded into float64 accumulators.  G's tile is staged behind X's.
+template <class T, int K, int V>
+__global__ void __launch_bounds__(kRingThreads)
+    linear_wgrad_vec_kernel(const T* __restrict__ X, const T* __restrict__ G, i64 n, int stages,
+                            int stage_g, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) u64 full[4];
+  __shared__ __align__(8) u64 empty[4];
+  constexpr int d = 32 * V;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t xbytes = (size_t)kVecRows * d * sizeof(T);
+  const size_t stage_bytes = xbytes + (size_t)kVecRows * K * sizeof(T);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(smem_addr(&full[s]), 1);
+      mbar_init(smem_addr(&empty[s]), kRingWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kRingWarps) {
+    if (lane == 0)
+      ring_produce<T>(X, stage_g ? G : nullptr, K, n, d, kVecRows, stages, stage_bytes, ring,
+                      full, empty);
+    return;
+  }
+  double acc[V][K];
+  double bacc[K];
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[v][j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) bacc[j] = 0.0;
+  const i64 ntiles = (n + kVecRows - 1) / kVecRows;
+  int s = 0;
+  unsigned fph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&full[s]), fph);
+    const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+    const T* sg = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes + xbytes);
+    const i64 r0 = t * kVecRows;
+    const int nr = (int)((n - r0) < kVecRows ? (n - r0) : kVecRows);
+    T ps[V][K], pb[K];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int j = 0; j < K; ++j) ps[v][j] = T(0);
+#pragma unroll
+    for (int j = 0; j < K; ++j) pb[j] = T(0);
+    for (int r = warp; r < nr; r += kRingWarps) {
+      T x[V], g[K];
+      VecLoad<T, V>::ld(sx + (size_t)r * d + lane * V, x);
+#pragma unroll
+      for (int j = 0; j < K; ++j) g[j] = stage_g ? sg[r * K + j] : __ldg(G + (r0 + r) * K + j);
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int j = 0; j < K; ++j) ps[v][j] += x[v] * g[j];
+#pragma unroll
+      for (int j = 0; j < K; ++j) pb[j] += g[j];
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[v][j] += (double)ps[v][j];
+#pragma unroll
+    for (int j = 0; j < K; ++j) bacc[j] += (double)pb[j];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
+    if (++s == stages) {
+      s = 0;
+      fph ^= 1u;
+    }
+  }
+  const int W = d * K + K;
+  double* out = part + ((i64)blockIdx.x * kRingWarps + warp) * W;
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[(lane * V + v) * K + j] = acc[v][j];
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[d * K + j] = bacc[j];
+  }
+}
+
 template <class T>
 __global__ void wgrad_reduce_kernel(const double* __restrict__ part, int rows, int width,
                                     T* __restrict__ dW, T* __restrict__ db, int dk) {
@@ -546,8 +783,45 @@ int ring_wgrad_grid(i64 n, int d) {
   return stream_grid((n + ring_shape<T>(d).rows - 1) / ring_shape<T>(d).rows, 1, 1);
 }
 
+// vector ring path: d = 32*V with a 256-row stage of at most 64 KB
+template <class T>
+int vec_width(const T* X, i64 n, int d) {
+  if ((((uintptr_t)X) & 15) != 0 || n < (i64)kVecRows * 4 || d % 32 != 0) return 0;
+  const int V = d / 32;
+  if ((V != 1 && V != 2 && V != 4 && V != 8) || (size_t)d * sizeof(T) > 256) return 0;
+  return V;
+}
+
+template <class T>
+int vec_stages(int d, int k) {
+  const size_t stage = (size_t)kVecRows * (d + k) * sizeof(T);
+  const int st = (int)((200 * 1024) / stage);
+  return st < 2 ? 2 : (st > 4 ? 4 : st);
+}
+
 template <class T>
 int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cudaStream_t st) {
+  if (const int V = vec_width<T>(X, n, d)) {
+    const int stages = vec_stages<T>(d, 0);
+    const size_t smem = (size_t)stages * kVecRows * d * sizeof(T);
+    const int grid = stream_grid((n + kVecRows - 1) / kVecRows, 1, 1);
+    bool launched = false;
+#define TDP_CASE(KK, VV)                                                                      \
+  if (k == KK && V == VV) {                                                                   \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_vec_kernel<T, KK, VV>,                       \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_fwd_vec_kernel<T, KK, VV><<<grid, kRingThreads, smem, st>>>(X, n, stages, W, b, Y); \
+    launched = true;                                                                          \
+  }
+#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2)
+    TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
+#undef TDP_CASES
+#undef TDP_CASE
+    if (launched) {
+      TDP_LAUNCH_CHECK("linear_fwd_vec_kernel");
+      return TDP_OK;
+    }
+  }
   if (ring_ok<T>(X, n, d)) {
     const RingShape rs = ring_shape<T>(d);
     const size_t smem = rs.stages * rs.stage_bytes;
@@ -593,6 +867,37 @@ int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cu
 template <class T>
 int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, double* ws,
                  size_t ws_bytes, cudaStream_t st) {
+  if (const int V = vec_width<T>(X, n, d)) {
+    const int stages = vec_stages<T>(d, k);
+    const size_t smem = (size_t)stages * kVecRows * (d + k) * sizeof(T);
+    const int grid = stream_grid((n + kVecRows - 1) / kVecRows, 1, 1);
+    const int width = d * k + k;
+    const int prow = grid * kRingWarps;
+    const int stage_g = (((size_t)kVecRows * k * sizeof(T)) % 16 == 0) &&
+                        (((size_t)(n % kVecRows) * k * sizeof(T)) % 16 == 0) &&
+                        ((((uintptr_t)G) & 15) == 0);
+    TDP_REQUIRE(ws_bytes >= (size_t)prow * width * sizeof(double), "linear_wgrad workspace too small");
+    bool launched = false;
+#define TDP_CASE(KK, VV)                                                                      \
+  if (k == KK && V == VV) {                                                                   \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_vec_kernel<T, KK, VV>,                     \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    linear_wgrad_vec_kernel<T, KK, VV><<<grid, kRingThreads, smem, st>>>(X, G, n, stages,     \
+                                                                         stage_g, ws);        \
+    launched = true;                                                                          \
+  }
+#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2)
+    TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
+#undef TDP_CASES
+#undef TDP_CASE
+    if (launched) {
+      TDP_LAUNCH_CHECK("linear_wgrad_vec_kernel");
+      wgrad_reduce_kernel<T><<<(unsigned)ceil_div((i64)width * 32, 256), 256, 0, st>>>(
+          ws, prow, width, dW, db, d * k);
+      TDP_LAUNCH_CHECK("wgrad_reduce_kernel");
+      return TDP_OK;
+    }
+  }
   if (ring_ok<T>(X, n, d)) {
     const RingShape rs = ring_shape<T>(d);
     const size_t stage = rs.stage_bytes + (size_t)rs.rows * k * sizeof(T);
@@ -675,8 +980,9 @@ int tdp_linear_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k
 
 size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k) {
   int g = wgrad_grid<double>(n, d);
-  const int cands[3] = {wgrad_grid<float>(n, d), ring_wgrad_grid<float>(n, d) * kRingWarps,
-                        ring_wgrad_grid<double>(n, d) * kRingWarps};
+  const int cands[4] = {wgrad_grid<float>(n, d), ring_wgrad_grid<float>(n, d) * kRingWarps,
+                        ring_wgrad_grid<double>(n, d) * kRingWarps,
+                        stream_grid((n + kVecRows - 1) / kVecRows, 1, 1) * kRingWarps};
   for (int c : cands) g = c > g ? c : g;
   return (size_t)g * (size_t)(d * k + k) * sizeof(double) + 256;
 }

@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(kRingThreads)
       for (int j = 0; j < K; ++j) ps[v][j] = T(0);
 #pragma unroll
     for (int j = 0; j < K; ++j) pb[j] = T(0);
-    for (int r = warp; r < nr; r += kRingWarps) {
+    auto row = [&](int r) {
       T x[V], g[K];
       VecLoad<T, V>::ld(sx + (size_t)r * d + lane * V, x);
 #pragma unroll
@@ -698,6 +698,13 @@ __global__ void __launch_bounds__(kRingThreads)
         for (int j = 0; j < K; ++j) ps[v][j] += x[v] * g[j];
 #pragma unroll
       for (int j = 0; j < K; ++j) pb[j] += g[j];
+    };
+    if (nr == kVecRows) {
+      // full stage: 32 rows per warp, unrolled so all shared loads issue early
+#pragma unroll
+      for (int i = 0; i < kVecRows / kRingWarps; ++i) row(warp + i * kRingWarps);
+    } else {
+      for (int r = warp; r < nr; r += kRingWarps) row(r);
     }
 #pragma unroll
     for (int v = 0; v < V; ++v)

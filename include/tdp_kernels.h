@@ -353,6 +353,33 @@ size_t tdp_linear_wgrad_workspace(int64_t n, int32_t d, int32_t k);
 int tdp_linear_wgrad(const void* X, const void* G, int32_t dtype, int64_t n, int32_t d, int32_t k,
                      void* dW, void* db, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* fused soft count over a linear classifier head (the LLP query)           */
+/* ------------------------------------------------------------------------ */
+/* Soft group-by COUNT (tdp_soft_groupby_fwd) whose key `dense_key` is the PE
+ * column P = softmax(X W + bias), X [n, d], W [d, k], computed on the fly:
+ * replaces Linear.__call__ (tq/models.py:26-27) -> pe_encode
+ * (tq/encodings.py:143-151) -> soft_groupby count (tq/kernels.py:190-229)
+ * for one pass over X.  All other keys are one-hot code columns.
+ * keys[dense_key].data is ignored; keys[dense_key].k must equal k.
+ * Supported shapes: tdp_soft_linear_supported() (d = 32 or 64 float32,
+ * d = 32 float64, X 16-byte aligned, n >= 1024, k <= 8, <= 8192 cells);
+ * otherwise TDP_ENOTSUP and the caller composes the unfused kernels.       */
+int tdp_soft_linear_supported(int32_t dtype, int64_t n, int32_t d, int32_t k, int64_t cells,
+                              const void* X);
+int tdp_soft_linear_count_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k,
+                              const void* W, const void* bias, const tdp_soft_key* keys,
+                              int32_t nkeys, int32_t dense_key, double* out_grid, void* stream);
+size_t tdp_soft_linear_count_bwd_workspace(int64_t n, int32_t d, int32_t k);
+/* VJP of the above w.r.t. W and bias for the upstream grid gradient G
+ * (float64): the softmax VJP (tq/tensor.py:515-527) of dP[i,c] = G[cell(i,c)]
+ * followed by the matmul / bias-add VJPs (tq/tensor.py:452, :337-338), with
+ * P recomputed from X.  dW [d, k], db [k] (may be NULL) in X's dtype.      */
+int tdp_soft_linear_count_bwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k,
+                              const void* W, const void* bias, const tdp_soft_key* keys,
+                              int32_t nkeys, int32_t dense_key, const double* grad_grid, void* dW,
+                              void* db, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,8 @@ engine only sequences them (it is the "tape" of this build).
 * :func:`gather_rows`    -- row gather and its scatter-add VJP (tq/tensor.py:597-614)
 * :func:`soft_groupby_grid` -- soft grouped count / weighted sum over PE keys and
   its VJP (tq/kernels.py:190-229 and the reduce_sum/mul/reshape VJP chain).
+* :func:`soft_linear_count` -- the soft count whose dense key is
+  pe_encode(Linear(X)), fused into one pass over X forward and one backward.
 """
 
 from __future__ import annotations
@@ -232,3 +234,72 @@ def soft_groupby_grid(spec: SoftKeySpec, keys: Sequence[torch.Tensor], n: int,
                       out_dtype: torch.dtype, values: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Dense grid (flattened, row-major over keys) of sum_i w_i prod_j P_j[i, c_j]."""
     return _SoftGroupBy.apply(spec, n, out_dtype, values, *keys)
+
+
+# ---------------------------------------------------------------------------
+# fused soft count over a linear classifier head (LLP)
+# ---------------------------------------------------------------------------
+
+def soft_linear_supported(x: torch.Tensor, w: torch.Tensor, cells: int) -> bool:
+    """Shapes the fused kernels cover (tdp_soft_linear_supported)."""
+    if not (x.is_cuda and x.dim() == 2 and w.dim() == 2 and x.dtype == w.dtype
+            and x.dtype in (torch.float32, torch.float64) and x.is_contiguous()):
+        return False
+    return bool(nat.load().tdp_soft_linear_supported(_dt(x), x.shape[0], x.shape[1], w.shape[1],
+                                                     int(cells), nat.ptr(x)))
+
+
+def _linear_keys(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor]):
+    arr = (nat.SoftKey * len(spec.kinds))()
+    it = iter(codes)
+    for j, (kind, k) in enumerate(spec.kinds):
+        if j == dense_pos:
+            arr[j] = nat.SoftKey(None, nat.SOFT_DENSE, nat.F32, k)
+        else:
+            arr[j] = nat.SoftKey(c_void_p(next(it).data_ptr()), nat.SOFT_ONEHOT, nat.I64, k)
+    return arr
+
+
+class _SoftLinearCount(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec: SoftKeySpec, dense_pos: int, out_dtype: torch.dtype, x: torch.Tensor,
+                w: torch.Tensor, b: Optional[torch.Tensor], *codes: torch.Tensor):
+        x = x.contiguous()
+        w = w.detach().contiguous()
+        b = None if b is None else b.detach().contiguous()
+        n, d = x.shape
+        k = w.shape[1]
+        grid = torch.empty(spec.cells, dtype=torch.float64, device=x.device)
+        keys = _linear_keys(spec, dense_pos, codes)
+        nat.call("tdp_soft_linear_count_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
+                 keys, len(spec.kinds), dense_pos, nat.ptr(grid), nat.stream())
+        ctx.spec, ctx.dense_pos, ctx.has_bias = spec, dense_pos, b is not None
+        ctx.save_for_backward(x, w, *(() if b is None else (b,)), *codes)
+        return grid.to(out_dtype)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        saved = ctx.saved_tensors
+        x, w = saved[0], saved[1]
+        b = saved[2] if ctx.has_bias else None
+        codes = saved[3 if ctx.has_bias else 2:]
+        n, d = x.shape
+        k = w.shape[1]
+        G = g.detach().to(torch.float64).contiguous()
+        dw = torch.empty_like(w)
+        db = torch.empty_like(b) if b is not None else None
+        ws = nat.workspace(nat.load().tdp_soft_linear_count_bwd_workspace(n, d, k), x.device)
+        keys = _linear_keys(ctx.spec, ctx.dense_pos, codes)
+        nat.call("tdp_soft_linear_count_bwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
+                 keys, len(ctx.spec.kinds), ctx.dense_pos, nat.ptr(G), nat.ptr(dw), nat.ptr(db),
+                 nat.ptr(ws), ws.numel(), nat.stream())
+        return (None, None, None, None, dw if ctx.needs_input_grad[4] else None,
+                db if ctx.has_bias and ctx.needs_input_grad[5] else None,
+                *([None] * len(codes)))
+
+
+def soft_linear_count(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor],
+                      x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor],
+                      out_dtype: torch.dtype) -> torch.Tensor:
+    """Flattened count grid of softmax(x w + b) crossed with one-hot keys."""
+    return _SoftLinearCount.apply(spec, dense_pos, out_dtype, x, w, b, *codes)

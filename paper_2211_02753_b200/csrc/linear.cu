@@ -15,7 +15,7 @@
 // per-column reads are bank-conflict free, then computes from shared memory.
 // The arithmetic intensity is ~k/2 flop/byte -- far below the tensor-core
 // ridge -- so CUDA-core FMAs at HBM speed are the roofline.
-#include "tdp_common.cuh"
+#include "stream_ring.cuh"
 
 namespace tdp {
 namespace {
@@ -225,8 +225,6 @@ __global__ void __launch_bounds__(kThreadsL)
 // Unpadded tiles are conflict-free for both kernels (a warp reads consecutive
 // features of one row).  Used when d*sizeof(T) is a multiple of 16 bytes.
 // ---------------------------------------------------------------------------
-constexpr int kRingWarps = 8;
-constexpr int kRingThreads = (kRingWarps + 1) * 32;
 
 struct RingShape {
   int rows;   // rows per stage (multiple of 32)
@@ -249,42 +247,6 @@ RingShape ring_shape(int d) {
   return r;
 }
 
-// Producer: per stage, the tile's X rows (in 8 KB bulk copies, so several
-// requests are in flight) and, when G != nullptr, its G rows behind them.
-// Returns through *g_in_smem whether G tiles are staged (their byte count must
-// be a multiple of 16 for every tile).
-template <class T>
-__device__ __forceinline__ void ring_produce(const T* __restrict__ X, const T* __restrict__ G, int K,
-                                             i64 n, int d, int rows, int stages,
-                                             size_t stage_bytes, unsigned char* ring, u64* full,
-                                             u64* empty) {
-  const unsigned long long pol = l2_evict_first_policy();
-  const i64 ntiles = (n + rows - 1) / rows;
-  constexpr unsigned kChunk = 8 * 1024;
-  int s = 0;
-  unsigned eph = 0;
-  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    mbar_wait(smem_addr(&empty[s]), eph ^ 1u);
-    const i64 r0 = t * rows;
-    const i64 nr = (n - r0) < rows ? (n - r0) : rows;
-    const unsigned xbytes = (unsigned)(nr * d * (i64)sizeof(T));
-    const unsigned gbytes = G ? (unsigned)(nr * K * (i64)sizeof(T)) : 0u;
-    const unsigned bar = smem_addr(&full[s]);
-    mbar_expect_tx(bar, xbytes + gbytes);
-    unsigned char* dst = ring + (size_t)s * stage_bytes;
-    const unsigned char* src = reinterpret_cast<const unsigned char*>(X + r0 * d);
-    for (unsigned off = 0; off < xbytes; off += kChunk) {
-      const unsigned b = xbytes - off < kChunk ? xbytes - off : kChunk;
-      bulk_load(smem_addr(dst + off), src + off, b, bar, pol);
-    }
-    if (G)
-      bulk_load(smem_addr(dst + (size_t)rows * d * sizeof(T)), G + r0 * K, gbytes, bar, pol);
-    if (++s == stages) {
-      s = 0;
-      eph ^= 1u;
-    }
-  }
-}
 
 template <class T, int K, int NF>
 __global__ void __launch_bounds__(kRingThreads)
@@ -494,97 +456,6 @@ __global__ void __launch_bounds__(kRingThreads)
 // consumer warp) so all consumer warps work on every stage; full stages run
 // without bounds checks.
 // ---------------------------------------------------------------------------
-template <class T, int V>
-struct VecLoad;
-template <>
-struct VecLoad<float, 1> {
-  __device__ static void ld(const float* p, float* o) { o[0] = p[0]; }
-};
-template <>
-struct VecLoad<float, 2> {
-  __device__ static void ld(const float* p, float* o) {
-    const float2 v = *reinterpret_cast<const float2*>(p);
-    o[0] = v.x;
-    o[1] = v.y;
-  }
-};
-template <>
-struct VecLoad<float, 4> {
-  __device__ static void ld(const float* p, float* o) {
-    const float4 v = *reinterpret_cast<const float4*>(p);
-    o[0] = v.x;
-    o[1] = v.y;
-    o[2] = v.z;
-    o[3] = v.w;
-  }
-};
-template <>
-struct VecLoad<float, 8> {
-  __device__ static void ld(const float* p, float* o) {
-    VecLoad<float, 4>::ld(p, o);
-    VecLoad<float, 4>::ld(p + 4, o + 4);
-  }
-};
-template <int V>
-struct VecLoad<double, V> {
-  __device__ static void ld(const double* p, double* o) {
-#pragma unroll
-    for (int i = 0; i < V; i += 2) {
-      if (i + 1 < V) {
-        const double2 v = *reinterpret_cast<const double2*>(p + i);
-        o[i] = v.x;
-        o[i + 1] = v.y;
-      } else {
-        o[i] = p[i];
-      }
-    }
-  }
-};
-
-constexpr int kVecRows = kRingWarps * 32;  // rows per stage in the vector kernels
-
-template <class T, int K, int V, bool FULL>
-__device__ __forceinline__ void vec_fwd_group(const T* __restrict__ sx, int g, i64 r0, i64 n,
-                                              const T (&w)[V][K], const T (&bj)[K],
-                                              T* __restrict__ Y, int lane) {
-  constexpr int d = 32 * V;
-  T p[32][K];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    T x[V];
-    if (FULL || r0 + g * 32 + r < n) {
-      VecLoad<T, V>::ld(sx + (size_t)(g * 32 + r) * d + lane * V, x);
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) x[v] = T(0);
-    }
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      T acc = x[0] * w[0][j];
-#pragma unroll
-      for (int v = 1; v < V; ++v) acc += x[v] * w[v][j];
-      p[r][j] = acc;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool upper = (lane & o) != 0;
-#pragma unroll
-    for (int r = 0; r < o; ++r) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const T send = upper ? p[r][j] : p[r + o][j];
-        const T keep = upper ? p[r + o][j] : p[r][j];
-        p[r][j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-  }
-  const i64 row = r0 + g * 32 + lane;
-  if (FULL || row < n) {
-#pragma unroll
-    for (int j = 0; j < K; ++j) Y[row * K + j] = p[0][j] + bj[j];
-  }
-}
 
 template <class T, int K, int V>
 __global__ void __launch_bounds__(kRingThreads)
@@ -624,8 +495,19 @@ __global__ void __launch_bounds__(kRingThreads)
     mbar_wait(smem_addr(&full[s]), fph);
     const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
     const i64 r0 = t * kVecRows;
-    if (r0 + kVecRows <= n) vec_fwd_group<T, K, V, true>(sx, warp, r0, n, w, bj, Y, lane);
-    else if (r0 + warp * 32 < n) vec_fwd_group<T, K, V, false>(sx, warp, r0, n, w, bj, Y, lane);
+    T z[K];
+    const i64 row = r0 + warp * 32 + lane;
+    if (r0 + kVecRows <= n) {
+      vec_row_dots<T, K, V, true>(sx, warp, r0, n, w, lane, z);
+#pragma unroll
+      for (int j = 0; j < K; ++j) Y[row * K + j] = z[j] + bj[j];
+    } else if (r0 + warp * 32 < n) {
+      vec_row_dots<T, K, V, false>(sx, warp, r0, n, w, lane, z);
+      if (row < n) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) Y[row * K + j] = z[j] + bj[j];
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
     if (++s == stages) {
@@ -731,21 +613,6 @@ __global__ void __launch_bounds__(kRingThreads)
   }
 }
 
-template <class T>
-__global__ void wgrad_reduce_kernel(const double* __restrict__ part, int rows, int width,
-                                    T* __restrict__ dW, T* __restrict__ db, int dk) {
-  const int lane = threadIdx.x & 31;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < width;
-       t += (gridDim.x * blockDim.x) >> 5) {
-    double v = 0.0;
-    for (int r = lane; r < rows; r += 32) v += part[(i64)r * width + t];
-    v = warp_sum(v);
-    if (lane == 0) {
-      if (t < dk) dW[t] = (T)v;
-      else if (db) db[t - dk] = (T)v;
-    }
-  }
-}
 
 // rows per tile: a multiple of 32 fitting 96 KB of shared memory, <= kMaxTile
 template <class T>
@@ -790,15 +657,6 @@ int ring_wgrad_grid(i64 n, int d) {
   return stream_grid((n + ring_shape<T>(d).rows - 1) / ring_shape<T>(d).rows, 1, 1);
 }
 
-// vector ring path: d = 32*V with a 256-row stage of at most 64 KB
-template <class T>
-int vec_width(const T* X, i64 n, int d) {
-  if ((((uintptr_t)X) & 15) != 0 || n < (i64)kVecRows * 4 || d % 32 != 0) return 0;
-  const int V = d / 32;
-  if ((V != 1 && V != 2 && V != 4 && V != 8) || (size_t)d * sizeof(T) > 256) return 0;
-  return V;
-}
-
 template <class T>
 int vec_stages(int d, int k) {
   const size_t stage = (size_t)kVecRows * (d + k) * sizeof(T);
@@ -814,7 +672,7 @@ int launch_fwd(const T* X, i64 n, int d, int k, const T* W, const T* b, T* Y, cu
     const int grid = stream_grid((n + kVecRows - 1) / kVecRows, 1, 1);
     bool launched = false;
 #define TDP_CASE(KK, VV)                                                                      \
-  if (k == KK && V == VV) {                                                                   \
+  if constexpr (sizeof(T) == 4 || VV == 1) if (k == KK && V == VV) {                                                                \
     TDP_CUDA_TRY(cudaFuncSetAttribute(linear_fwd_vec_kernel<T, KK, VV>,                       \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     linear_fwd_vec_kernel<T, KK, VV><<<grid, kRingThreads, smem, st>>>(X, n, stages, W, b, Y); \
@@ -886,7 +744,7 @@ int launch_wgrad(const T* X, const T* G, i64 n, int d, int k, T* dW, T* db, doub
     TDP_REQUIRE(ws_bytes >= (size_t)prow * width * sizeof(double), "linear_wgrad workspace too small");
     bool launched = false;
 #define TDP_CASE(KK, VV)                                                                      \
-  if (k == KK && V == VV) {                                                                   \
+  if constexpr (sizeof(T) == 4 || VV == 1) if (k == KK && V == VV) {                                                                \
     TDP_CUDA_TRY(cudaFuncSetAttribute(linear_wgrad_vec_kernel<T, KK, VV>,                     \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     linear_wgrad_vec_kernel<T, KK, VV><<<grid, kRingThreads, smem, st>>>(X, G, n, stages,     \

@@ -24,17 +24,6 @@ namespace tdp {
 namespace {
 
 template <class T>
-__device__ __forceinline__ T t_exp(T x);
-template <>
-__device__ __forceinline__ float t_exp<float>(float x) {
-  return expf(x);
-}
-template <>
-__device__ __forceinline__ double t_exp<double>(double x) {
-  return exp(x);
-}
-
-template <class T>
 __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -42,13 +31,6 @@ __device__ __forceinline__ T warp_max(T v) {
     v = (t > v || t != t) ? t : v;
   }
   return v;
-}
-
-// numpy max propagates NaN; keep that so exp(x - NaN) poisons the row as in
-// the reference.
-template <class T>
-__device__ __forceinline__ T nan_max(T a, T b) {
-  return (b > a || b != b) ? b : a;
 }
 
 template <class T>

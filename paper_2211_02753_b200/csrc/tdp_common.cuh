@@ -269,4 +269,25 @@ constexpr int kFilterWords = kFilterTile / 32;
 int filter_bits(const PredSet& ps, int64_t n, unsigned* bits, i64* tile_counts,
                 cudaStream_t stream);
 
+// ---------------------------------------------------------------------------
+// softmax helpers (soft.cu, llp.cu)
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ T t_exp(T x);
+template <>
+__device__ __forceinline__ float t_exp<float>(float x) {
+  return expf(x);
+}
+template <>
+__device__ __forceinline__ double t_exp<double>(double x) {
+  return exp(x);
+}
+
+// numpy max propagates NaN; keep that so exp(x - NaN) poisons the row as in
+// the reference.
+template <class T>
+__device__ __forceinline__ T nan_max(T a, T b) {
+  return (b > a || b != b) ? b : a;
+}
+
 }  // namespace tdp

@@ -32,7 +32,8 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .autograd import SoftKeySpec, gather_many, gather_rows_raw, soft_groupby_grid
+from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, soft_groupby_grid,
+                       soft_linear_count, soft_linear_supported)
 from .encodings import (
     DictionaryEncoding,
     EncodedTensor,
@@ -76,6 +77,7 @@ from .tensor import (
     dtype_name,
     gather,
     slice_axis,
+    pending_softmax,
     mul,
     reshape,
     tensor,
@@ -699,6 +701,43 @@ def _soft_inputs(pes: Sequence[EncodedTensor]):
     return SoftKeySpec(kinds), tensors, dts
 
 
+def _soft_linear_count(pes: Sequence[EncodedTensor], spaces: tuple[int, ...]) -> Optional[Tensor]:
+    """Soft count of one deferred ``pe_encode(Linear(X))`` key crossed with
+    one-hot keys, in one fused pass over X (tdp_soft_linear_count_fwd; the
+    backward recomputes P from X).  None when the keys do not have that form."""
+    dense, kinds, dts, codes = None, [], [], []
+    for j, p in enumerate(pes):
+        oh = onehot_payload(p.values)
+        if oh is not None:
+            kinds.append(("onehot", oh.k))
+            dts.append(oh.dtype)
+            codes.append(oh.codes)
+            continue
+        pend = pending_softmax(p.values)
+        if pend is None or dense is not None:
+            return None
+        dense = (j, pend, p.values.node)
+        kinds.append(("dense", p.encoding.num_classes))
+        dts.append(pend.dtype)
+    if dense is None:
+        return None
+    pos, pend, node = dense
+    if node is not None and node is not active_tape():
+        return None
+    lin = pend.lin
+    spec = SoftKeySpec(kinds)
+    if not soft_linear_supported(lin.x, lin.w, spec.cells):
+        return None
+    nat.require_cuda(*codes)
+    joint_dt = dts[0]
+    for d in dts[1:]:
+        joint_dt = np.promote_types(joint_dt, d).name
+    with _grad_mode():
+        grid = soft_linear_count(spec, pos, [c.contiguous() for c in codes], lin.x, lin.w, lin.b,
+                                 torch_dtype(joint_dt))
+        return _finish(grid.reshape(spaces))
+
+
 def soft_count(pe: EncodedTensor) -> Tensor:
     """Differentiable count per class: column sums of the PE matrix."""
     if not pe.is_pe():
@@ -729,6 +768,10 @@ def soft_groupby(pes: Sequence[EncodedTensor], agg: str = "count",
     numeric column.  The n x prod(k) joint is never materialised.
     """
     spaces, n = _joint_spaces(pes)
+    if agg == "count":
+        fused = _soft_linear_count(pes, spaces)
+        if fused is not None:
+            return GroupedCounts(spaces, fused)
     spec, keys, dts = _soft_inputs(pes)
     nat.require_cuda(*keys)
     joint_dt = dts[0]

@@ -226,9 +226,9 @@ def lazy_view(t: torch.Tensor, sel: Selection, valid_for=None) -> LazyValue:
 def as_expr(value) -> tuple[Expr, Optional[Selection]]:
     """(expression, selection) of a Tensor (lazy or materialised) or torch tensor."""
     if isinstance(value, _T.Tensor):
-        if value._t is None:
+        if value._t is None and isinstance(value._lazy, LazyValue):
             return value._lazy.expr, value._lazy.sel
-        value = value._t
+        value = value.data
     return Expr.column(value.contiguous()), None
 
 
@@ -238,7 +238,7 @@ def _lazy_operand(t, rdt: str):
         return None
     if t._t is None:
         lv = t._lazy
-        if lv.ndim != 1:
+        if not isinstance(lv, LazyValue) or lv.ndim != 1:
             return None
         return lv.expr.cast(rdt), lv.sel, True
     if t._t.dim() == 0:

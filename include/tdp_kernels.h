@@ -281,6 +281,16 @@ size_t tdp_join_workspace(int64_t n_build, int64_t n_probe);
 int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
                      int64_t n_probe, int64_t* out_count, void* ws, size_t ws_bytes,
                      void* stream);
+/* Same as tdp_join_prepare for a filtered probe relation: probe row i of the
+ * base key column takes part iff every predicate holds on the base columns
+ * (tdp_filter_select semantics), evaluated inside the probe pass; the probe
+ * indices tdp_join_emit then writes are base row ids.  Replaces filter_exact
+ * (tq/kernels.py:87-97) + take_rows of the key column ahead of a join.     */
+int tdp_join_prepare_filtered(const int64_t* build_keys, int64_t n_build,
+                              const int64_t* probe_keys, int64_t n_probe,
+                              const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
+                              int32_t npreds, int64_t* out_count, void* ws, size_t ws_bytes,
+                              void* stream);
 int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);

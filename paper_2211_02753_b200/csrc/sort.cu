@@ -448,18 +448,29 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
 
 // ---------------------------------------------------------------------------
 // equi-join: stable radix sort of the build keys, an open-addressing hash
-// table over the distinct build keys (key -> [start, count) in sorted order),
-// one hash probe per probe row.  Probe rows are processed in tiles: pass 1
-// counts matches per tile only (no per-row arrays), a tiny scan gives tile
-// offsets, pass 2 re-probes (the table is L2-resident) and writes the pairs
-// with a block scan.  Output: probe row order, ascending build row within a
-// probe row (stable sort).
+// table over the distinct build keys (16-byte slots {key, run start + 1}, one
+// vector load per probe; the run length is read only on a hit), one probe per
+// probe row.  The probe side may carry a filter: its predicates are evaluated
+// on the base columns in the same pass, so a filtered relation is probed
+// without materialising its row indices or gathering its key column.
+//
+//   pass 1 (count): per tile of kJoinTile rows, predicates + probe, one match
+//     bit per row (ballot) and the tile's pair count;
+//   scan of the tile counts -> tile output offsets and the total;
+//   pass 2 (emit): tiles without matches exit at once; otherwise only rows
+//     whose match bit is set are re-probed and their pairs written in order.
+//
+// Output: probe row order (base row ids), ascending build row within a probe
+// row (stable sort).
 // ---------------------------------------------------------------------------
 namespace tdp {
 namespace {
 
 constexpr int kJoinThreads = 256;
-constexpr int kJoinTile = 256 * 8;  // probe rows per tile
+constexpr int kJoinTile = 2048;  // probe rows per tile
+constexpr int kJoinWords = kJoinTile / 32;
+constexpr int kJoinPer = kJoinTile / kJoinThreads;
+constexpr int kJoinWarps = kJoinThreads / 32;
 
 __device__ __forceinline__ u64 mix64(u64 x) {
   x ^= x >> 30;
@@ -471,9 +482,8 @@ __device__ __forceinline__ u64 mix64(u64 x) {
 }
 
 struct HashTable {
-  i64* key;       // [cap]
-  i64* start;     // [cap]; 0 = empty, else start + 1
-  i64* count;     // [cap]
+  longlong2* slot;  // [cap] {key, start + 1}; .y == 0 -> empty
+  i64* count;       // [cap] run length
   u64 mask;
 };
 
@@ -487,9 +497,9 @@ __global__ void join_build_kernel(const u64* __restrict__ sk, i64 nb, HashTable 
     u64 h = mix64((u64)key) & ht.mask;
     for (;;) {
       const unsigned long long prev = atomicCAS(
-          reinterpret_cast<unsigned long long*>(ht.start + h), 0ull, (unsigned long long)(i + 1));
+          reinterpret_cast<unsigned long long*>(&ht.slot[h].y), 0ull, (unsigned long long)(i + 1));
       if (prev == 0ull) {
-        ht.key[h] = key;
+        ht.slot[h].x = key;
         ht.count[h] = e - i;
         break;
       }
@@ -498,95 +508,109 @@ __global__ void join_build_kernel(const u64* __restrict__ sk, i64 nb, HashTable 
   }
 }
 
-__device__ __forceinline__ void join_lookup(const HashTable& ht, i64 key, i64* start, i64* cnt) {
-  u64 h = mix64((u64)key) & ht.mask;
+// Continue a probe whose first slot was occupied by another key.
+__device__ __noinline__ void join_chain(const HashTable& ht, i64 key, u64 h, i64* start, i64* cnt) {
   for (;;) {
-    const i64 s = ht.start[h];
-    if (s == 0) {
+    h = (h + 1) & ht.mask;
+    const longlong2 e = ht.slot[h];
+    if (e.y == 0) {
       *start = 0;
       *cnt = 0;
       return;
     }
-    if (ht.key[h] == key) {
-      *start = s - 1;
+    if (e.x == key) {
+      *start = e.y - 1;
       *cnt = ht.count[h];
       return;
     }
-    h = (h + 1) & ht.mask;
   }
 }
 
-constexpr int kJoinPer = kJoinTile / kJoinThreads;
+__device__ __forceinline__ void join_lookup(const HashTable& ht, i64 key, i64* start, i64* cnt) {
+  const u64 h = mix64((u64)key) & ht.mask;
+  const longlong2 e = ht.slot[h];
+  if (e.y == 0) {
+    *start = 0;
+    *cnt = 0;
+  } else if (e.x == key) {
+    *start = e.y - 1;
+    *cnt = ht.count[h];
+  } else {
+    join_chain(ht, key, h, start, cnt);
+  }
+}
 
-// All kJoinPer lookups of a thread issue their first table reads together
-// (independent loads in flight); only the rare collision chains loop.
-__device__ __forceinline__ void join_lookup_batch(const HashTable& ht, const i64* __restrict__ probe,
-                                                  i64 np, i64 tile, i64* s, i64* c) {
+// Row of item k of this thread in a tile: rows k*256 .. k*256+255 form the
+// 8 match words k*8 .. k*8+7 (warp w owns word k*8+w, lane = bit).
+__device__ __forceinline__ i64 join_row(i64 tile, int k) {
+  return tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
+}
+
+template <bool kFiltered>
+__global__ void __launch_bounds__(kJoinThreads)
+    join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np, PredSet ps,
+                      unsigned* __restrict__ match_bits, i64* __restrict__ tile_counts) {
+  __shared__ i64 warp_sums[kJoinWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 tile = blockIdx.x;
+  bool act[kJoinPer];
   i64 key[kJoinPer];
   u64 h[kJoinPer];
-  i64 st[kJoinPer], kk[kJoinPer];
+  longlong2 e[kJoinPer];
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
-    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
-    key[k] = i < np ? __ldg(probe + i) : 0;
+    const i64 i = join_row(tile, k);
+    act[k] = i < np;
+    if (kFiltered && act[k]) act[k] = eval_all(ps, i);
+    key[k] = act[k] ? __ldg(probe + i) : 0;
     h[k] = mix64((u64)key[k]) & ht.mask;
   }
+  // all first-slot loads in flight together; only collision chains loop
 #pragma unroll
-  for (int k = 0; k < kJoinPer; ++k) {
-    st[k] = ht.start[h[k]];
-    kk[k] = ht.key[h[k]];
-  }
-#pragma unroll
-  for (int k = 0; k < kJoinPer; ++k) {
-    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
-    s[k] = 0;
-    c[k] = 0;
-    if (i >= np || st[k] == 0) continue;
-    if (kk[k] == key[k]) {
-      s[k] = st[k] - 1;
-      c[k] = ht.count[h[k]];
-    } else {
-      join_lookup(ht, key[k], &s[k], &c[k]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kJoinThreads)
-    join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
-                      i64* __restrict__ tile_counts) {
-  __shared__ i64 warp_sums[kJoinThreads / 32];
-  const i64 tile = blockIdx.x;
-  i64 s[kJoinPer], c[kJoinPer];
-  join_lookup_batch(ht, probe, np, tile, s, c);
+  for (int k = 0; k < kJoinPer; ++k) e[k] = act[k] ? ht.slot[h[k]] : make_longlong2(0, 0);
   i64 local = 0;
 #pragma unroll
-  for (int k = 0; k < kJoinPer; ++k) local += c[k];
+  for (int k = 0; k < kJoinPer; ++k) {
+    i64 c = 0;
+    if (e[k].y != 0) {
+      if (e[k].x == key[k]) {
+        c = ht.count[h[k]];
+      } else {
+        i64 s;
+        join_chain(ht, key[k], h[k], &s, &c);
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, c > 0);
+    if (lane == 0) match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
+    local += c;
+  }
   local = warp_sum(local);
-  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = local;
+  if (lane == 0) warp_sums[warp] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
     i64 t = 0;
-    for (int w = 0; w < kJoinThreads / 32; ++w) t += warp_sums[w];
+#pragma unroll
+    for (int w = 0; w < kJoinWarps; ++w) t += warp_sums[w];
     tile_counts[tile] = t;
   }
 }
 
 __global__ void __launch_bounds__(kJoinThreads)
     join_emit_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
-                     const i64* __restrict__ order, const i64* __restrict__ tile_offsets,
+                     const unsigned* __restrict__ match_bits, const i64* __restrict__ order,
+                     const i64* __restrict__ tile_counts, const i64* __restrict__ tile_offsets,
                      i64* __restrict__ out_probe, i64* __restrict__ out_build) {
-  __shared__ i64 warp_tot[kJoinThreads / 32];
-  __shared__ i64 running;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
-  if (threadIdx.x == 0) running = tile_offsets[tile];
-  i64 sv[kJoinPer], cv[kJoinPer];
-  join_lookup_batch(ht, probe, np, tile, sv, cv);
-  __syncthreads();
-#pragma unroll
+  if (tile_counts[tile] == 0) return;  // block-uniform
+  __shared__ i64 warp_tot[kJoinWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  i64 running = tile_offsets[tile];
   for (int k = 0; k < kJoinPer; ++k) {
-    const i64 i = tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
-    const i64 s = sv[k], c = cv[k];
+    const unsigned word = match_bits[tile * kJoinWords + k * kJoinWarps + warp];
+    if (!__syncthreads_or(word != 0u)) continue;  // no match among these 256 rows
+    const i64 i = join_row(tile, k);
+    i64 s = 0, c = 0;
+    if ((word >> lane) & 1u) join_lookup(ht, __ldg(probe + i), &s, &c);
     // block-wide exclusive scan of c (row order = thread order)
     i64 incl = c;
 #pragma unroll
@@ -597,18 +621,19 @@ __global__ void __launch_bounds__(kJoinThreads)
     if (lane == 31) warp_tot[warp] = incl;
     __syncthreads();
     i64 before = 0, total = 0;
-    for (int w = 0; w < kJoinThreads / 32; ++w) {
-      if (w < warp) before += warp_tot[w];
-      total += warp_tot[w];
+#pragma unroll
+    for (int w = 0; w < kJoinWarps; ++w) {
+      const i64 t = warp_tot[w];
+      before += w < warp ? t : 0;
+      total += t;
     }
     const i64 base = running + before + incl - c;
     for (i64 j = 0; j < c; ++j) {
       out_probe[base + j] = i;
       out_build[base + j] = order[s + j];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) running += total;
-    __syncthreads();
+    running += total;
+    __syncthreads();  // warp_tot reused by the next round
   }
 }
 
@@ -621,6 +646,7 @@ u64 table_capacity(i64 nb) {
 struct JoinWs {
   SortBuffers sb;
   HashTable ht;
+  unsigned* match_bits;
   i64* tile_counts;
   i64* tile_offsets;
   void* scan_ws;
@@ -631,7 +657,8 @@ struct JoinWs {
 size_t join_ws_bytes(i64 nb, i64 np) {
   const u64 cap = table_capacity(nb);
   const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
-  return sort_ws_bytes(nb) + 3 * align256(cap * 8) + 2 * align256((size_t)tiles * 8) +
+  return sort_ws_bytes(nb) + align256(cap * 16) + align256(cap * 8) +
+         align256((size_t)tiles * kJoinWords * 4) + 2 * align256((size_t)tiles * 8) +
          exclusive_scan_workspace(tiles) + 2048;
 }
 
@@ -641,13 +668,13 @@ JoinWs carve_join(void* ws, i64 nb, i64 np) {
   unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(nb);
   const u64 cap = table_capacity(nb);
   const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
-  j.ht.key = (i64*)p;
-  p += align256(cap * 8);
-  j.ht.start = (i64*)p;
-  p += align256(cap * 8);
+  j.ht.slot = (longlong2*)p;
+  p += align256(cap * 16);
   j.ht.count = (i64*)p;
   p += align256(cap * 8);
   j.ht.mask = cap - 1;
+  j.match_bits = (unsigned*)p;
+  p += align256((size_t)tiles * kJoinWords * 4);
   j.tile_counts = (i64*)p;
   p += align256((size_t)tiles * 8);
   j.tile_offsets = (i64*)p;
@@ -656,6 +683,48 @@ JoinWs carve_join(void* ws, i64 nb, i64 np) {
   j.scan_bytes = exclusive_scan_workspace(tiles) + 1024;
   j.order = j.sb.i0;
   return j;
+}
+
+int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                 int64_t n_probe, const PredSet* ps, int64_t* out_count, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
+  TDP_REQUIRE(out_count != nullptr, "null join count output");
+  TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
+  JoinWs j = carve_join(ws, n_build, n_probe);
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  if (n_build == 0 || n_probe == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
+    if (tiles) TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * 8, st));
+    return TDP_OK;
+  }
+  make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
+                                                                      n_build, j.sb.k0, j.sb.i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  u64* sk;
+  i64* order;
+  int rc = radix_sort(j.sb, n_build, st, &sk, &order);
+  if (rc) return rc;
+  if (sk != j.sb.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.slot, 0, (j.ht.mask + 1) * 16, st));
+  join_build_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(j.sb.k0, n_build, j.ht);
+  TDP_LAUNCH_CHECK("join_build_kernel");
+  if (ps != nullptr && ps->npreds > 0) {
+    join_count_kernel<true><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
+        j.ht, probe_keys, n_probe, *ps, j.match_bits, j.tile_counts);
+  } else {
+    PredSet none;
+    none.npreds = 0;
+    none.pad = 0;
+    join_count_kernel<false><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
+        j.ht, probe_keys, n_probe, none, j.match_bits, j.tile_counts);
+  }
+  TDP_LAUNCH_CHECK("join_count_kernel");
+  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
+                            j.scan_bytes, st);
 }
 
 }  // namespace
@@ -668,34 +737,19 @@ size_t tdp_join_workspace(int64_t n_build, int64_t n_probe) { return join_ws_byt
 int tdp_join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
                      int64_t n_probe, int64_t* out_count, void* ws, size_t ws_bytes,
                      void* stream) {
-  TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
-  TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
-  cudaStream_t st = as_stream(stream);
-  if (n_build == 0 || n_probe == 0) {
-    TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
-    return TDP_OK;
-  }
-  JoinWs j = carve_join(ws, n_build, n_probe);
-  make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
-                                                                      n_build, j.sb.k0, j.sb.i0);
-  TDP_LAUNCH_CHECK("make_keys_kernel");
-  u64* sk;
-  i64* order;
-  int rc = radix_sort(j.sb, n_build, st, &sk, &order);
+  return join_prepare(build_keys, n_build, probe_keys, n_probe, nullptr, out_count, ws, ws_bytes,
+                      as_stream(stream));
+}
+
+int tdp_join_prepare_filtered(const int64_t* build_keys, int64_t n_build,
+                              const int64_t* probe_keys, int64_t n_probe, const tdp_column* cols,
+                              int32_t ncols, const tdp_predicate* preds, int32_t npreds,
+                              int64_t* out_count, void* ws, size_t ws_bytes, void* stream) {
+  PredSet ps;
+  int rc = make_predset(cols, ncols, preds, npreds, n_probe, &ps);
   if (rc) return rc;
-  if (sk != j.sb.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
-    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
-    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
-  }
-  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.start, 0, (j.ht.mask + 1) * 8, st));
-  join_build_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(j.sb.k0, n_build, j.ht);
-  TDP_LAUNCH_CHECK("join_build_kernel");
-  const i64 tiles = ceil_div(n_probe, kJoinTile);
-  join_count_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe,
-                                                             j.tile_counts);
-  TDP_LAUNCH_CHECK("join_count_kernel");
-  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
-                            j.scan_bytes, st);
+  return join_prepare(build_keys, n_build, probe_keys, n_probe, &ps, out_count, ws, ws_bytes,
+                      as_stream(stream));
 }
 
 int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
@@ -706,12 +760,11 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
   cudaStream_t st = as_stream(stream);
   JoinWs j = carve_join(ws, n_build, n_probe);
   const i64 tiles = ceil_div(n_probe, kJoinTile);
-  join_emit_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, j.order,
-                                                            j.tile_offsets, out_probe_idx,
-                                                            out_build_idx);
+  join_emit_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(
+      j.ht, probe_keys, n_probe, j.match_bits, j.order, j.tile_counts, j.tile_offsets,
+      out_probe_idx, out_build_idx);
   TDP_LAUNCH_CHECK("join_emit_kernel");
   return TDP_OK;
 }
 
 }  // extern "C"
-

@@ -45,7 +45,9 @@ from .encodings import (
 )
 from .lazy import (
     native_predicates,
+    DeferredCount,
     Expr,
+    PrefixRows,
     LazyValue,
     Pred,
     Program,
@@ -334,7 +336,7 @@ def _scan_aggregate(exprs_keys: Sequence[Expr], spans: Sequence[tuple[int, int]]
 PROFILE_HOOK = None
 
 
-def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device):
+def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device, defer_rows=False):
     nkeys = len(spans)
     keys = nat.struct_array(nat.Key, [nat.Key(0, 0, lo, span) for lo, span in spans])
     aggs = nat.struct_array(nat.Agg, [nat.Agg(k, 0) for k in aggs_kinds])
@@ -347,6 +349,8 @@ def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device):
     nat.call("tdp_groupby_finalize", nat.ptr(counts), nat.ptr(sums), slots, keys, nkeys, aggs,
              len(aggs_kinds), avg_mask, nat.ptr(out_keys), nat.ptr(out_counts), nat.ptr(out_aggs),
              nat.ptr(out_groups), nat.stream())
+    if defer_rows:  # padded [slots] outputs + the occupied count, read by the host later
+        return out_keys, out_counts, out_aggs, DeferredCount(out_groups)
     g = int(out_groups.item())
     return out_keys[:, :g], out_counts[:g], out_aggs[:, :g], g
 
@@ -371,12 +375,16 @@ def _agg_outputs(aggs: Sequence[tuple[str, str]], raw: torch.Tensor, counts: tor
     return out
 
 
-def groupby_exact(keys: Sequence[EncodedTensor],
-                  aggs: Sequence[AggInput]) -> tuple[list[torch.Tensor], list[torch.Tensor]]:
+def groupby_exact(keys: Sequence[EncodedTensor], aggs: Sequence[AggInput], *,
+                  defer_rows: bool = False) -> tuple[list, list]:
     """Group rows by the key columns and aggregate.
 
     Returns key-value arrays and aggregate arrays over the non-empty groups,
     ordered by ascending combined key (lexicographic over the key columns).
+    With ``defer_rows`` (the compiler's GroupAggExactOp) the dense fused path
+    returns :class:`~.lazy.PrefixRows` payloads instead of torch tensors: the
+    number of occupied groups stays on the device until the host reads it, so
+    the query does not synchronise.
     """
     if not keys:
         raise KernelError("groupby_exact requires at least one key column")
@@ -407,11 +415,11 @@ def groupby_exact(keys: Sequence[EncodedTensor],
     space = _fusable(operands)
     if space is not None and all(as_expr(k)[0].op in ("col", "cast", "add", "sub", "mul", "neg", "square")
                                  for k in key_vals):
-        return _groupby_fused(keys, key_vals, agg_specs, agg_vals, space)
+        return _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows)
     return _groupby_general(keys, key_vals, agg_specs, agg_vals)
 
 
-def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space):
+def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False):
     sel, n = space
     kexprs = [as_expr(v)[0] for v in key_vals]
     device = _device_of(kexprs, sel)
@@ -460,9 +468,13 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space):
         if func == "avg":
             avg_mask |= 1 << a
     kinds = [k for k, _ in agg_exprs]
-    out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask, device)
+    out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask,
+                                                  device, defer_rows)
     key_values = [out_keys[j].contiguous() for j in range(len(keys))]
-    return key_values, _agg_outputs(agg_specs, out_aggs, out_counts, already_avg=True)
+    agg_values = _agg_outputs(agg_specs, out_aggs, out_counts, already_avg=True)
+    if defer_rows:
+        return ([PrefixRows(k, g) for k in key_values], [PrefixRows(a, g) for a in agg_values])
+    return key_values, agg_values
 
 
 def _device_of(exprs, sel):
@@ -885,10 +897,16 @@ def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTens
 # ---------------------------------------------------------------------------
 
 
-def join_indices(probe_key, build_key) -> tuple[torch.Tensor, torch.Tensor]:
+def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None
+                 ) -> tuple[torch.Tensor, torch.Tensor]:
     """Inner equi-join row pairs: (probe rows, build rows), ordered by probe row
-    then ascending build row (stable radix sort of the build keys + binary
-    search per probe key)."""
+    then ascending build row (stable radix sort of the build keys + one hash
+    probe per probe row).
+
+    With ``probe_sel`` the probe side is a filtered base relation:
+    ``probe_key`` is the *base* key column, the selection's predicates are
+    evaluated in the probe pass itself, and the returned probe rows are base
+    row ids (the filtered relation is never materialised)."""
     pk = _materialize(probe_key).contiguous().to(torch.int64)
     bk = _materialize(build_key).contiguous().to(torch.int64)
     nat.require_cuda(pk, bk)
@@ -896,8 +914,18 @@ def join_indices(probe_key, build_key) -> tuple[torch.Tensor, torch.Tensor]:
     n_probe, n_build = int(pk.numel()), int(bk.numel())
     ws = nat.workspace(nat.load().tdp_join_workspace(n_build, n_probe), dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
-    nat.call("tdp_join_prepare", nat.ptr(bk), n_build, nat.ptr(pk), n_probe, nat.ptr(count),
-             nat.ptr(ws), ws.numel(), nat.stream())
+    if probe_sel is not None and probe_sel.preds:
+        if probe_sel.n != n_probe:
+            raise KernelError("probe selection and key column disagree on row count")
+        prog = Program()
+        preds, npreds = prog.predicates(probe_sel)
+        nat.require_cuda(*prog.cols)
+        nat.call("tdp_join_prepare_filtered", nat.ptr(bk), n_build, nat.ptr(pk), n_probe,
+                 prog.native_columns(), len(prog.cols), preds, npreds, nat.ptr(count),
+                 nat.ptr(ws), ws.numel(), nat.stream())
+    else:
+        nat.call("tdp_join_prepare", nat.ptr(bk), n_build, nat.ptr(pk), n_probe, nat.ptr(count),
+                 nat.ptr(ws), ws.numel(), nat.stream())
     m = int(count.item())
     pi = torch.empty(m, dtype=torch.int64, device=dev)
     bi = torch.empty(m, dtype=torch.int64, device=dev)
@@ -908,11 +936,12 @@ def join_indices(probe_key, build_key) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 def _side_sources(cols: Sequence[EncodedTensor]):
-    """(base tensors, row map or None) for one join side.
+    """(base tensors, selection or None) for one join side.
 
-    Lazy views of one selection are gathered straight from their base columns
-    through ``selection.indices()[rows]``; the filtered relation is never
-    materialised.  Anything else is materialised first."""
+    Lazy views of one selection are read straight from their base columns
+    (the probe side through the filtered probe pass, the build side through
+    ``selection.indices()``); the filtered relation is never materialised.
+    Anything else is materialised first (selection None)."""
     sels = set()
     for c in cols:
         v = c.values
@@ -923,7 +952,7 @@ def _side_sources(cols: Sequence[EncodedTensor]):
         sels.add(id(v._lazy.sel))
     if sels is not None and len(sels) == 1:
         sel = cols[0].values._lazy.sel
-        return [c.values._lazy.expr.col for c in cols], sel.indices()
+        return [c.values._lazy.expr.col for c in cols], sel
     return [c.values.data.detach() for c in cols], None
 
 
@@ -952,11 +981,18 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
     if active_tape() is not None:
         pi, bi = join_indices(left[left_key].values, right[right_key].values)
         return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
-    lb, lmap = _side_sources(left)
-    rb, rmap = _side_sources(right)
-    lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
+    lb, lsel = _side_sources(left)
+    rb, rsel = _side_sources(right)
+    rmap = rsel.indices() if rsel is not None else None
     rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
-    pi, bi = join_indices(lkey, rkey)
+    if lsel is not None and lb[left_key].dim() == 1:
+        # probe the filtered base relation directly: probe rows are base rows
+        pi, bi = join_indices(lb[left_key], rkey, probe_sel=lsel)
+        lmap = None
+    else:
+        lmap = lsel.indices() if lsel is not None else None
+        lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
+        pi, bi = join_indices(lkey, rkey)
     return _gather_side(left, lb, lmap, pi) + _gather_side(right, rb, rmap, bi)
 
 

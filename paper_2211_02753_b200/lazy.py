@@ -22,6 +22,8 @@ and are evaluated without FMA contraction.
 from __future__ import annotations
 
 import struct
+import threading
+import weakref
 from ctypes import c_int32, c_void_p
 from typing import Optional, Sequence
 
@@ -378,3 +380,98 @@ def project(exprs: Sequence[Expr], sel: Optional[Selection]) -> list[torch.Tenso
              prog.native_instrs(), len(prog.instrs), out_idx, len(outs), out_ptrs,
              nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream())
     return results
+
+
+# ---------------------------------------------------------------------------
+# device-resident row counts (results whose length the host has not read yet)
+# ---------------------------------------------------------------------------
+
+
+class _PinnedRing:
+    """Pinned host int64 slots for device-produced counts, allocated once (a
+    fresh pinned allocation per query could block on cudaHostAlloc).  A slot
+    is reused after a full turn of the ring; its previous holder is resolved
+    first (its copy finished long ago in practice)."""
+
+    SLOTS = 4096
+
+    def __init__(self):
+        self.buf = torch.empty(self.SLOTS, dtype=torch.int64, pin_memory=True)
+        self.holders: list = [None] * self.SLOTS
+        self.next = 0
+        self.lock = threading.Lock()
+
+    def take(self, holder) -> int:
+        with self.lock:
+            i = self.next
+            self.next = (i + 1) % self.SLOTS
+            prev = self.holders[i]
+            self.holders[i] = holder
+        h = prev() if prev is not None else None
+        if h is not None:
+            h.value()
+        return i
+
+
+_RING: Optional[_PinnedRing] = None
+
+
+def _ring() -> _PinnedRing:
+    global _RING
+    if _RING is None:
+        _RING = _PinnedRing()
+    return _RING
+
+
+class DeferredCount:
+    """A row count produced by a kernel.  It is copied to a pinned host slot
+    asynchronously right after the producing launch; the host waits for it
+    only on first access (``value()``), so a query whose result stays on the
+    device never blocks the launching thread."""
+
+    __slots__ = ("_slot", "_event", "_value", "__weakref__")
+
+    def __init__(self, dev: torch.Tensor):
+        self._value: Optional[int] = None
+        ring = _ring()
+        self._slot = ring.take(weakref.ref(self))
+        ring.buf[self._slot:self._slot + 1].copy_(dev.reshape(1), non_blocking=True)
+        self._event = torch.cuda.Event()
+        self._event.record()
+
+    def value(self) -> int:
+        if self._value is None:
+            self._event.synchronize()
+            self._value = int(_ring().buf[self._slot])
+            self._event = None
+        return self._value
+
+
+class PrefixRows:
+    """Lazy payload: the first ``count`` rows of ``full`` (a padded result
+    buffer written by a kernel whose row count is a :class:`DeferredCount`)."""
+
+    __slots__ = ("full", "count", "dtype")
+
+    def __init__(self, full: torch.Tensor, count: DeferredCount):
+        self.full = full
+        self.count = count
+        self.dtype = _T.dtype_name(full)
+
+    @property
+    def ndim(self) -> int:
+        return self.full.dim()
+
+    def shape(self) -> tuple:
+        return (self.count.value(),) + tuple(self.full.shape[1:])
+
+    def materialize(self) -> torch.Tensor:
+        return self.full[: self.count.value()]
+
+
+def deferred_rows(t) -> Optional[DeferredCount]:
+    """The DeferredCount of an unresolved PrefixRows tensor, else None."""
+    if isinstance(t, _T.Tensor) and t._t is None and isinstance(t._lazy, PrefixRows) \
+            and t._lazy.count._value is None:
+        return t._lazy.count
+    return None

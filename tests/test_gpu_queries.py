@@ -173,3 +173,43 @@ def test_q3_join_pipeline_matches_oracle(sf):
     # a second run reuses the compiled tail and gives the same answer
     res2 = plan.run(cat)
     np.testing.assert_array_equal(res2.columns[0].values.numpy(), got["l_orderkey"])
+
+
+@pytest.mark.parametrize("n_probe,n_build,key_range", [(100_000, 3_000, 20_000), (5_000, 0, 10),
+                                                       (70_000, 40, 10), (1, 1, 1)])
+def test_filtered_probe_join_matches_oracle(n_probe, n_build, key_range):
+    """equi_join whose probe side is a lazy filtered relation: the predicates
+    run inside the probe pass and the emitted probe rows are base rows."""
+    from paper_2211_02753_b200.kernels import equi_join, filter_exact
+
+    rng = np.random.default_rng(n_probe + n_build)
+    pk = rng.integers(0, key_range, size=n_probe)
+    pv = rng.integers(0, 100, size=n_probe)
+    pf = rng.random(n_probe)
+    bk = rng.integers(0, key_range, size=n_build)
+    bv = rng.random(n_build)
+    probe = [tq.plain(tq.Tensor(pk)), tq.plain(tq.Tensor(pv)), tq.plain(tq.Tensor(pf))]
+    build = [tq.plain(tq.Tensor(bk)), tq.plain(tq.Tensor(bv))]
+    filtered = filter_exact(probe, [(1, "<", 37), (2, ">=", 0.25)])
+    assert filtered[0].values.is_lazy
+    out = equi_join(filtered, build, 0, 0)
+    keep = (pv < 37) & (pf >= 0.25)
+    fk, fv, ff = pk[keep], pv[keep], pf[keep]
+    epi, ebi = orc.join_inner(fk, bk)
+    np.testing.assert_array_equal(out[0].values.numpy(), fk[epi])
+    np.testing.assert_array_equal(out[1].values.numpy(), fv[epi])
+    np.testing.assert_array_equal(out[2].values.numpy(), ff[epi])
+    np.testing.assert_array_equal(out[3].values.numpy(), bk[ebi])
+    np.testing.assert_array_equal(out[4].values.numpy(), bv[ebi])
+
+
+def test_group_result_row_count_is_deferred_until_read():
+    """An exact dense group-by leaves its occupied-group count on the device:
+    the result table resolves row_count on first access."""
+    arrays = wl.lineitem_arrays(0.01, seed=3, rows=20_000)
+    res = _run(wl.Q1_SQL, arrays, wl.q1_registry())
+    assert not isinstance(res._rows, int)
+    exp = otpch.q1(arrays)
+    assert res.row_count == len(exp["rf"])
+    np.testing.assert_array_equal(res.columns[0].values.numpy(), exp["rf"])
+    np.testing.assert_array_equal(res.column("count").values.numpy(), exp["count"])

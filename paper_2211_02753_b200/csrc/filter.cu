@@ -30,14 +30,27 @@ __global__ void __launch_bounds__(kFilterThreads)
   const i64 tile = blockIdx.x;
   const i64 tile_base = tile * kFilterTile;
   int count = 0;
-#pragma unroll 4
-  for (int w = warp; w < kFilterWords; w += kFilterThreads / 32) {
-    const i64 row = tile_base + (i64)w * 32 + lane;
-    bool keep = row < n && eval_all(ps, row);
-    unsigned word = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) {
-      bits[tile * kFilterWords + w] = word;
-      count += __popc(word);
+  constexpr int kPer = kFilterWords / (kFilterThreads / 32);  // words per warp
+  constexpr int kBatch = 8;
+#pragma unroll
+  for (int b = 0; b < kPer; b += kBatch) {
+    i64 row[kBatch];
+    bool keep[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int w = warp + (b + r) * (kFilterThreads / 32);
+      row[r] = tile_base + (i64)w * 32 + lane;
+      keep[r] = row[r] < n;
+    }
+    eval_batch<kBatch>(ps, row, keep);
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+      const int w = warp + (b + r) * (kFilterThreads / 32);
+      const unsigned word = __ballot_sync(0xffffffffu, keep[r]);
+      if (lane == 0) {
+        bits[tile * kFilterWords + w] = word;
+        count += __popc(word);
+      }
     }
   }
   if (lane == 0) warp_counts[warp] = count;

@@ -447,21 +447,22 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// equi-join: stable radix sort of the build keys, an open-addressing hash
-// table over the distinct build keys (16-byte slots {key, run start + 1}, one
-// vector load per probe; the run length is read only on a hit), one probe per
-// probe row.  The probe side may carry a filter: its predicates are evaluated
-// on the base columns in the same pass, so a filtered relation is probed
-// without materialising its row indices or gathering its key column.
+// equi-join.  Build: an open-addressing hash table over the distinct build
+// keys (16-byte slots {key ^ INT64_MIN (0 = empty), packed run}, one vector
+// load per probe) plus a split-block Bloom filter (~16 bits per key, L2-
+// resident).  The build first inserts every row in input order, which is the
+// whole build when the keys are unique (the primary-key side of a PK-FK join:
+// no sort, run start = the row itself).  Only if a key repeats does it fall
+// back to a stable radix sort of the build keys and insert one run per
+// distinct key (key -> [start, count) in sorted order).
 //
-//   pass 1 (count): per tile of kJoinTile rows, predicates + probe, one match
-//     bit per row (ballot) and the tile's pair count;
-//   scan of the tile counts -> tile output offsets and the total;
-//   pass 2 (emit): tiles without matches exit at once; otherwise only rows
-//     whose match bit is set are re-probed and their pairs written in order.
-//
-// Output: probe row order (base row ids), ascending build row within a probe
-// row (stable sort).
+// Probe: pass 1 (count) evaluates the optional probe-side filter on the base
+// columns, the Bloom filter and the table, and writes one match bit per row,
+// per-word pair counts and per-tile pair counts; a scan gives tile offsets.
+// Pass 2 (emit) writes the pairs: probe row order (base row ids), ascending
+// build row within a probe row.  Unique keys emit in two fully parallel
+// steps (expand match bits -> probe rows, then one thread per pair); runs use
+// a warp-per-word re-probe with a warp scan of the run lengths.
 // ---------------------------------------------------------------------------
 namespace tdp {
 namespace {
@@ -471,77 +472,141 @@ constexpr int kJoinTile = 2048;  // probe rows per tile
 constexpr int kJoinWords = kJoinTile / 32;
 constexpr int kJoinPer = kJoinTile / kJoinThreads;
 constexpr int kJoinWarps = kJoinThreads / 32;
+constexpr i64 kMinKey = (i64)0x8000000000000000ull;
 
-__device__ __forceinline__ u64 mix64(u64 x) {
-  x ^= x >> 30;
-  x *= 0xbf58476d1ce4e5b9ull;
-  x ^= x >> 27;
-  x *= 0x94d049bb133111ebull;
-  x ^= x >> 31;
-  return x;
+// slot.y packs (start + 1) << 24 | min(run length, kCountSat); a saturated
+// length is read from count[] (runs of >= 16M equal build keys only).
+constexpr i64 kCountSat = (1 << 24) - 1;
+
+// One 64-bit multiply + xor-shift (the probe pass is instruction-bound at
+// 8-16 B/row); the table index, the Bloom block and its bit salts use
+// different bits.
+__device__ __forceinline__ u64 join_hash(i64 key) {
+  u64 h = (u64)key * 0x9E3779B97F4A7C15ull;
+  return h ^ (h >> 29);
 }
 
 struct HashTable {
-  longlong2* slot;  // [cap] {key, start + 1}; .y == 0 -> empty
-  i64* count;       // [cap] run length
+  longlong2* slot;   // [cap]
+  i64* count;        // [cap] run length (read only when saturated)
   u64 mask;
+  unsigned* bloom;   // [nwords]
+  unsigned bmask;    // nwords - 1
+  i64* side;         // run of the key INT64_MIN (its image is the empty marker): {start+1, count}
+  int* flags;        // [0] a key repeats, [1] build is sorted (runs), else unique
+  const i64* order;  // sorted build row ids (sorted mode)
 };
 
-__global__ void join_build_kernel(const u64* __restrict__ sk, i64 nb, HashTable ht) {
+// Register-blocked Bloom filter: one 32-bit word per key, 3 bits from 5-bit
+// fields of the hash (the table index uses the low bits of the full hash, the
+// word index bits 40+).  ~16 bits per key: a few MB, L2-resident, one 4-byte
+// load and a handful of 32-bit ops per probe; false positives ~1%.
+__device__ __forceinline__ unsigned bloom_mask(u64 h) {
+  const unsigned x = (unsigned)(h >> 16);
+  return (1u << (x & 31)) | (1u << ((x >> 5) & 31)) | (1u << ((x >> 10) & 31));
+}
+
+__device__ __forceinline__ const unsigned* bloom_word(const HashTable& ht, u64 h) {
+  return ht.bloom + ((unsigned)(h >> 40) & ht.bmask);
+}
+
+__device__ __forceinline__ i64 pack_run(i64 start, i64 cnt) {
+  return ((start + 1) << 24) | (cnt < kCountSat ? cnt : kCountSat);
+}
+
+// Insert key -> run; false if the key is already present.
+__device__ bool ht_insert(const HashTable& ht, i64 key, i64 start, i64 cnt) {
+  if (key == kMinKey) {
+    const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(ht.side), 0ull,
+                                              (unsigned long long)(start + 1));
+    if (prev != 0ull) return false;
+    ht.side[1] = cnt;
+    return true;
+  }
+  const u64 hk = join_hash(key);
+  const i64 kx = key ^ kMinKey;
+  u64 h = hk & ht.mask;
+  for (;;) {
+    const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(&ht.slot[h].x),
+                                              0ull, (unsigned long long)kx);
+    if (prev == 0ull) {
+      ht.slot[h].y = pack_run(start, cnt);
+      if (cnt >= kCountSat) ht.count[h] = cnt;
+      atomicOr(ht.bloom + ((unsigned)(hk >> 40) & ht.bmask), bloom_mask(hk));
+      return true;
+    }
+    if ((i64)prev == kx) return false;
+    h = (h + 1) & ht.mask;
+  }
+}
+
+__global__ void join_build_unique_kernel(const i64* __restrict__ keys, i64 nb, HashTable ht) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (i64)gridDim.x * blockDim.x)
+    if (!ht_insert(ht, __ldg(keys + i), i, 1)) ht.flags[0] = 1;
+}
+
+__global__ void join_build_runs_kernel(const u64* __restrict__ sk, i64 nb, HashTable ht) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
        i += (i64)gridDim.x * blockDim.x) {
     if (i > 0 && sk[i] == sk[i - 1]) continue;  // only run starts insert
     i64 e = i + 1;
     while (e < nb && sk[e] == sk[i]) ++e;
-    const i64 key = (i64)(sk[i] ^ 0x8000000000000000ull);
-    u64 h = mix64((u64)key) & ht.mask;
-    for (;;) {
-      const unsigned long long prev = atomicCAS(
-          reinterpret_cast<unsigned long long*>(&ht.slot[h].y), 0ull, (unsigned long long)(i + 1));
-      if (prev == 0ull) {
-        ht.slot[h].x = key;
-        ht.count[h] = e - i;
-        break;
-      }
-      h = (h + 1) & ht.mask;
-    }
+    ht_insert(ht, (i64)(sk[i] ^ 0x8000000000000000ull), i, e - i);
   }
 }
 
-// Continue a probe whose first slot was occupied by another key.
-__device__ __noinline__ void join_chain(const HashTable& ht, i64 key, u64 h, i64* start, i64* cnt) {
+__device__ __forceinline__ void unpack_run(const HashTable& ht, i64 y, u64 h, i64* start, i64* cnt) {
+  *start = (y >> 24) - 1;
+  const i64 c = y & kCountSat;
+  *cnt = c < kCountSat ? c : ht.count[h];
+}
+
+// Full lookup (collision chains, the INT64_MIN side slot).
+__device__ __noinline__ void join_lookup_slow(const HashTable& ht, i64 key, i64* start, i64* cnt) {
+  *start = 0;
+  *cnt = 0;
+  if (key == kMinKey) {
+    const i64 y = ht.side[0];
+    if (y != 0) {
+      *start = y - 1;
+      *cnt = ht.side[1];
+    }
+    return;
+  }
+  const i64 kx = key ^ kMinKey;
+  u64 h = join_hash(key) & ht.mask;
   for (;;) {
-    h = (h + 1) & ht.mask;
     const longlong2 e = ht.slot[h];
-    if (e.y == 0) {
-      *start = 0;
-      *cnt = 0;
+    if (e.x == 0) return;
+    if (e.x == kx) {
+      unpack_run(ht, e.y, h, start, cnt);
       return;
     }
-    if (e.x == key) {
-      *start = e.y - 1;
-      *cnt = ht.count[h];
-      return;
-    }
+    h = (h + 1) & ht.mask;
+  }
+}
+
+// First slot inline; chains and INT64_MIN go to the slow path.
+__device__ __forceinline__ void join_resolve(const HashTable& ht, i64 key, u64 hm, longlong2 e,
+                                             i64* start, i64* cnt) {
+  if (key != kMinKey && e.x == (key ^ kMinKey)) {
+    unpack_run(ht, e.y, hm, start, cnt);
+  } else if (key != kMinKey && e.x == 0) {
+    *start = 0;
+    *cnt = 0;
+  } else {
+    join_lookup_slow(ht, key, start, cnt);
   }
 }
 
 __device__ __forceinline__ void join_lookup(const HashTable& ht, i64 key, i64* start, i64* cnt) {
-  const u64 h = mix64((u64)key) & ht.mask;
-  const longlong2 e = ht.slot[h];
-  if (e.y == 0) {
-    *start = 0;
-    *cnt = 0;
-  } else if (e.x == key) {
-    *start = e.y - 1;
-    *cnt = ht.count[h];
-  } else {
-    join_chain(ht, key, h, start, cnt);
-  }
+  const u64 hm = join_hash(key) & ht.mask;
+  join_resolve(ht, key, hm, ht.slot[hm], start, cnt);
 }
 
-// Row of item k of this thread in a tile: rows k*256 .. k*256+255 form the
-// 8 match words k*8 .. k*8+7 (warp w owns word k*8+w, lane = bit).
+// Item k of a thread: rows k*256 .. k*256+255 of the tile form the match
+// words k*8 .. k*8+7 (warp w owns word k*8+w, lane = bit).
 __device__ __forceinline__ i64 join_row(i64 tile, int k) {
   return tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
 }
@@ -549,42 +614,56 @@ __device__ __forceinline__ i64 join_row(i64 tile, int k) {
 template <bool kFiltered>
 __global__ void __launch_bounds__(kJoinThreads)
     join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np, PredSet ps,
-                      unsigned* __restrict__ match_bits, i64* __restrict__ tile_counts) {
+                      unsigned* __restrict__ match_bits, i64* __restrict__ word_counts,
+                      i64* __restrict__ tile_counts) {
   __shared__ i64 warp_sums[kJoinWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
   bool act[kJoinPer];
-  i64 key[kJoinPer];
+  i64 row[kJoinPer], key[kJoinPer];
   u64 h[kJoinPer];
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    row[k] = join_row(tile, k);
+    act[k] = row[k] < np;
+  }
+  // keys are loaded together with the predicate columns (a selective filter
+  // still touches nearly every sector, so this costs no DRAM traffic and
+  // saves a dependent round trip)
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) key[k] = act[k] ? __ldcs(probe + row[k]) : 0;
+  if (kFiltered) eval_batch<kJoinPer>(ps, row, act);
+  unsigned bw[kJoinPer];
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    h[k] = join_hash(key[k]);
+    bw[k] = act[k] ? *bloom_word(ht, h[k]) : 0u;
+  }
   longlong2 e[kJoinPer];
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
-    const i64 i = join_row(tile, k);
-    act[k] = i < np;
-    if (kFiltered && act[k]) act[k] = eval_all(ps, i);
-    key[k] = act[k] ? __ldg(probe + i) : 0;
-    h[k] = mix64((u64)key[k]) & ht.mask;
+    const unsigned m = bloom_mask(h[k]);
+    act[k] = act[k] && (key[k] == kMinKey || (bw[k] & m) == m);
+    h[k] &= ht.mask;
+    e[k] = act[k] ? ht.slot[h[k]] : make_longlong2(0, 0);
   }
-  // all first-slot loads in flight together; only collision chains loop
-#pragma unroll
-  for (int k = 0; k < kJoinPer; ++k) e[k] = act[k] ? ht.slot[h[k]] : make_longlong2(0, 0);
+  const bool unique = ht.flags[1] == 0;  // at most one pair per probe row
   i64 local = 0;
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
     i64 c = 0;
-    if (e[k].y != 0) {
-      if (e[k].x == key[k]) {
-        c = ht.count[h[k]];
-      } else {
-        i64 s;
-        join_chain(ht, key[k], h[k], &s, &c);
-      }
+    if (act[k]) {
+      i64 st;
+      join_resolve(ht, key[k], h[k], e[k], &st, &c);
     }
     const unsigned word = __ballot_sync(0xffffffffu, c > 0);
-    if (lane == 0) match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
-    local += c;
+    const i64 wc = unique ? (i64)__popc(word) : (word ? warp_sum(c) : 0);
+    if (lane == 0) {
+      match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
+      word_counts[tile * kJoinWords + k * kJoinWarps + warp] = wc;
+    }
+    local += wc;
   }
-  local = warp_sum(local);
   if (lane == 0) warp_sums[warp] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -595,45 +674,120 @@ __global__ void __launch_bounds__(kJoinThreads)
   }
 }
 
-__global__ void __launch_bounds__(kJoinThreads)
-    join_emit_kernel(HashTable ht, const i64* __restrict__ probe, i64 np,
-                     const unsigned* __restrict__ match_bits, const i64* __restrict__ order,
-                     const i64* __restrict__ tile_counts, const i64* __restrict__ tile_offsets,
-                     i64* __restrict__ out_probe, i64* __restrict__ out_build) {
-  const i64 tile = blockIdx.x;
-  if (tile_counts[tile] == 0) return;  // block-uniform
-  __shared__ i64 warp_tot[kJoinWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  i64 running = tile_offsets[tile];
-  for (int k = 0; k < kJoinPer; ++k) {
-    const unsigned word = match_bits[tile * kJoinWords + k * kJoinWarps + warp];
-    if (!__syncthreads_or(word != 0u)) continue;  // no match among these 256 rows
-    const i64 i = join_row(tile, k);
-    i64 s = 0, c = 0;
-    if ((word >> lane) & 1u) join_lookup(ht, __ldg(probe + i), &s, &c);
-    // block-wide exclusive scan of c (row order = thread order)
-    i64 incl = c;
+// Exclusive prefix of a tile's 64 word pair counts, per warp (lane l holds
+// words 2l, 2l+1); word_offset(j) reads it back for word j.
+struct WordPrefix {
+  i64 excl, w0;
+  __device__ __forceinline__ WordPrefix(const i64* wc, int lane) {
+    w0 = wc[2 * lane];
+    const i64 w1 = wc[2 * lane + 1];
+    i64 incl = w0 + w1;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const i64 t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    i64 before = 0, total = 0;
+    excl = incl - w0 - w1;
+  }
+  __device__ __forceinline__ i64 word_offset(int j) const {
+    const i64 pe = __shfl_sync(0xffffffffu, excl, j >> 1);
+    const i64 p0 = __shfl_sync(0xffffffffu, w0, j >> 1);
+    return pe + ((j & 1) ? p0 : 0);
+  }
+};
+
+// Runs (a key repeats): every warp places its own words, its 8 lookups in
+// flight together, a warp scan of the run lengths per word.  Persistent CTAs
+// walk the tiles.
+__global__ void __launch_bounds__(kJoinThreads)
+    join_emit_runs_kernel(HashTable ht, const i64* __restrict__ probe, i64 tiles,
+                          const unsigned* __restrict__ match_bits,
+                          const i64* __restrict__ word_counts, const i64* __restrict__ tile_counts,
+                          const i64* __restrict__ tile_offsets, i64* __restrict__ out_probe,
+                          i64* __restrict__ out_build) {
+  if (ht.flags[1] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (tile_counts[tile] == 0) continue;
+    const WordPrefix wp(word_counts + tile * kJoinWords, lane);
+    const i64 base = tile_offsets[tile];
+    unsigned bits[kJoinPer];
+    i64 s[kJoinPer], c[kJoinPer];
 #pragma unroll
-    for (int w = 0; w < kJoinWarps; ++w) {
-      const i64 t = warp_tot[w];
-      before += w < warp ? t : 0;
-      total += t;
+    for (int k = 0; k < kJoinPer; ++k) bits[k] = match_bits[tile * kJoinWords + k * kJoinWarps + warp];
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      s[k] = 0;
+      c[k] = 0;
+      if ((bits[k] >> lane) & 1u) join_lookup(ht, __ldg(probe + join_row(tile, k)), &s[k], &c[k]);
     }
-    const i64 base = running + before + incl - c;
-    for (i64 j = 0; j < c; ++j) {
-      out_probe[base + j] = i;
-      out_build[base + j] = order[s + j];
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      if (bits[k] == 0u) continue;  // warp-uniform
+      const i64 word_off = base + wp.word_offset(k * kJoinWarps + warp);
+      i64 ci = c[k];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const i64 t = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) ci += t;
+      }
+      const i64 pos = word_off + ci - c[k];
+      const i64 i = join_row(tile, k);
+      for (i64 m = 0; m < c[k]; ++m) {
+        out_probe[pos + m] = i;
+        out_build[pos + m] = ht.order[s[k] + m];
+      }
     }
-    running += total;
-    __syncthreads();  // warp_tot reused by the next round
+  }
+}
+
+// Unique keys: expand the match bits into probe rows (no lookups), one warp
+// per tile (one DRAM round trip per tile, thousands of tiles in flight):
+// lane l owns words 2l, 2l+1 = rows 64l .. 64l+63 of the tile ...
+__global__ void __launch_bounds__(kJoinThreads)
+    join_expand_unique_kernel(HashTable ht, i64 tiles, const unsigned* __restrict__ match_bits,
+                              const i64* __restrict__ word_counts,
+                              const i64* __restrict__ tile_counts,
+                              const i64* __restrict__ tile_offsets, i64* __restrict__ out_probe) {
+  if (ht.flags[1] != 0) return;
+  const int lane = threadIdx.x & 31;
+  const i64 tile = (i64)blockIdx.x * kJoinWarps + (threadIdx.x >> 5);
+  if (tile >= tiles || tile_counts[tile] == 0) return;  // warp-uniform
+  const i64* wc = word_counts + tile * kJoinWords;
+  const unsigned* mb = match_bits + tile * kJoinWords;
+  const i64 w0 = wc[2 * lane], w1 = wc[2 * lane + 1];
+  unsigned b0 = mb[2 * lane], b1 = mb[2 * lane + 1];
+  i64 incl = w0 + w1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const i64 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  i64 pos = tile_offsets[tile] + incl - w0 - w1;
+  const i64 row0 = tile * kJoinTile + (i64)lane * 64;
+  while (b0) {
+    out_probe[pos++] = row0 + __ffs(b0) - 1;
+    b0 &= b0 - 1;
+  }
+  while (b1) {
+    out_probe[pos++] = row0 + 32 + __ffs(b1) - 1;
+    b1 &= b1 - 1;
+  }
+}
+
+// ... then one thread per pair re-probes (all lookups independent).
+__global__ void join_pairs_unique_kernel(HashTable ht, const i64* __restrict__ probe,
+                                         const i64* __restrict__ tile_counts,
+                                         const i64* __restrict__ tile_offsets, i64 tiles,
+                                         const i64* __restrict__ out_probe,
+                                         i64* __restrict__ out_build) {
+  if (ht.flags[1] != 0) return;
+  const i64 total = tile_offsets[tiles - 1] + tile_counts[tiles - 1];
+  for (i64 m = (i64)blockIdx.x * blockDim.x + threadIdx.x; m < total;
+       m += (i64)gridDim.x * blockDim.x) {
+    i64 s, c;
+    join_lookup(ht, __ldg(probe + out_probe[m]), &s, &c);
+    out_build[m] = s;
   }
 }
 
@@ -643,23 +797,31 @@ u64 table_capacity(i64 nb) {
   return cap;
 }
 
+// Bloom words (32-bit): power of two >= nb * 16 bits / 32.
+u64 bloom_blocks(i64 nb) {
+  u64 b = 64;
+  while (b < 2 * (u64)(nb > 0 ? nb : 1)) b <<= 1;
+  return b;
+}
+
 struct JoinWs {
   SortBuffers sb;
   HashTable ht;
   unsigned* match_bits;
+  i64* word_counts;
   i64* tile_counts;
   i64* tile_offsets;
   void* scan_ws;
   size_t scan_bytes;
-  i64* order;  // sorted build row ids (k0/i0 slot after prepare)
 };
 
 size_t join_ws_bytes(i64 nb, i64 np) {
   const u64 cap = table_capacity(nb);
   const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
   return sort_ws_bytes(nb) + align256(cap * 16) + align256(cap * 8) +
-         align256((size_t)tiles * kJoinWords * 4) + 2 * align256((size_t)tiles * 8) +
-         exclusive_scan_workspace(tiles) + 2048;
+         align256(bloom_blocks(nb) * 4) + 512 +
+         align256((size_t)tiles * kJoinWords * 4) + align256((size_t)tiles * kJoinWords * 8) +
+         2 * align256((size_t)tiles * 8) + exclusive_scan_workspace(tiles) + 2048;
 }
 
 JoinWs carve_join(void* ws, i64 nb, i64 np) {
@@ -673,16 +835,31 @@ JoinWs carve_join(void* ws, i64 nb, i64 np) {
   j.ht.count = (i64*)p;
   p += align256(cap * 8);
   j.ht.mask = cap - 1;
+  j.ht.bloom = (unsigned*)p;
+  p += align256(bloom_blocks(nb) * 4);
+  j.ht.bmask = (unsigned)(bloom_blocks(nb) - 1);
+  j.ht.side = (i64*)p;
+  j.ht.flags = (int*)(p + 256);
+  p += 512;
+  j.ht.order = j.sb.i0;
   j.match_bits = (unsigned*)p;
   p += align256((size_t)tiles * kJoinWords * 4);
+  j.word_counts = (i64*)p;
+  p += align256((size_t)tiles * kJoinWords * 8);
   j.tile_counts = (i64*)p;
   p += align256((size_t)tiles * 8);
   j.tile_offsets = (i64*)p;
   p += align256((size_t)tiles * 8);
   j.scan_ws = p;
   j.scan_bytes = exclusive_scan_workspace(tiles) + 1024;
-  j.order = j.sb.i0;
   return j;
+}
+
+int clear_table(const JoinWs& j, cudaStream_t st) {
+  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.slot, 0, (j.ht.mask + 1) * 16, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.bloom, 0, ((size_t)j.ht.bmask + 1) * 4, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.side, 0, 512, st));
+  return TDP_OK;
 }
 
 int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
@@ -695,32 +872,45 @@ int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* prob
   const i64 tiles = ceil_div(n_probe, kJoinTile);
   if (n_build == 0 || n_probe == 0) {
     TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
-    if (tiles) TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * 8, st));
     return TDP_OK;
   }
-  make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
-                                                                      n_build, j.sb.k0, j.sb.i0);
-  TDP_LAUNCH_CHECK("make_keys_kernel");
-  u64* sk;
-  i64* order;
-  int rc = radix_sort(j.sb, n_build, st, &sk, &order);
+  int rc = clear_table(j, st);
   if (rc) return rc;
-  if (sk != j.sb.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
-    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
-    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+  join_build_unique_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
+                                                                              j.ht);
+  TDP_LAUNCH_CHECK("join_build_unique_kernel");
+  int repeated = 0;
+  TDP_CUDA_TRY(cudaMemcpyAsync(&repeated, j.ht.flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TDP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (repeated) {  // runs of equal keys: stable sort, one table entry per run
+    rc = clear_table(j, st);
+    if (rc) return rc;
+    const int one[2] = {1, 1};
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.ht.flags, one, sizeof(one), cudaMemcpyHostToDevice, st));
+    make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(
+        build_keys, TDP_I64, 0, n_build, j.sb.k0, j.sb.i0);
+    TDP_LAUNCH_CHECK("make_keys_kernel");
+    u64* sk;
+    i64* order;
+    rc = radix_sort(j.sb, n_build, st, &sk, &order);
+    if (rc) return rc;
+    if (sk != j.sb.k0) {  // keep the sorted result in the k0/i0 slots for tdp_join_emit
+      TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+      TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    join_build_runs_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(j.sb.k0, n_build,
+                                                                             j.ht);
+    TDP_LAUNCH_CHECK("join_build_runs_kernel");
   }
-  TDP_CUDA_TRY(cudaMemsetAsync(j.ht.slot, 0, (j.ht.mask + 1) * 16, st));
-  join_build_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(j.sb.k0, n_build, j.ht);
-  TDP_LAUNCH_CHECK("join_build_kernel");
   if (ps != nullptr && ps->npreds > 0) {
     join_count_kernel<true><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
-        j.ht, probe_keys, n_probe, *ps, j.match_bits, j.tile_counts);
+        j.ht, probe_keys, n_probe, *ps, j.match_bits, j.word_counts, j.tile_counts);
   } else {
     PredSet none;
     none.npreds = 0;
     none.pad = 0;
     join_count_kernel<false><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
-        j.ht, probe_keys, n_probe, none, j.match_bits, j.tile_counts);
+        j.ht, probe_keys, n_probe, none, j.match_bits, j.word_counts, j.tile_counts);
   }
   TDP_LAUNCH_CHECK("join_count_kernel");
   return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
@@ -760,10 +950,17 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
   cudaStream_t st = as_stream(stream);
   JoinWs j = carve_join(ws, n_build, n_probe);
   const i64 tiles = ceil_div(n_probe, kJoinTile);
-  join_emit_kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(
-      j.ht, probe_keys, n_probe, j.match_bits, j.order, j.tile_counts, j.tile_offsets,
+  const unsigned grid = (unsigned)(tiles < (i64)sm_count() * 8 ? tiles : (i64)sm_count() * 8);
+  join_emit_runs_kernel<<<grid, kJoinThreads, 0, st>>>(
+      j.ht, probe_keys, tiles, j.match_bits, j.word_counts, j.tile_counts, j.tile_offsets,
       out_probe_idx, out_build_idx);
-  TDP_LAUNCH_CHECK("join_emit_kernel");
+  TDP_LAUNCH_CHECK("join_emit_runs_kernel");
+  join_expand_unique_kernel<<<(unsigned)ceil_div(tiles, kJoinWarps), kJoinThreads, 0, st>>>(
+      j.ht, tiles, j.match_bits, j.word_counts, j.tile_counts, j.tile_offsets, out_probe_idx);
+  TDP_LAUNCH_CHECK("join_expand_unique_kernel");
+  join_pairs_unique_kernel<<<(unsigned)(sm_count() * 8), 256, 0, st>>>(
+      j.ht, probe_keys, j.tile_counts, j.tile_offsets, tiles, out_probe_idx, out_build_idx);
+  TDP_LAUNCH_CHECK("join_pairs_unique_kernel");
   return TDP_OK;
 }
 

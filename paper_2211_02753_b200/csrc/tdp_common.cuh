@@ -185,6 +185,80 @@ __device__ __forceinline__ bool eval_all(const PredSet& ps, i64 i) {
   return keep;
 }
 
+// Branch-free comparison (numpy semantics: every comparison with NaN is false
+// except <>, which is true).
+template <class T>
+__device__ __forceinline__ bool compare_nb(T x, T y, int op) {
+  const bool lt = x < y, gt = x > y, eq = x == y;
+  return (op == TDP_EQ && eq) | (op == TDP_NE && !eq) | (op == TDP_LT && lt) |
+         (op == TDP_GT && gt) | (op == TDP_LE && (lt | eq)) | (op == TDP_GE && (gt | eq));
+}
+
+// keep[r] &= v[r] <op> lit with the operator resolved once, outside the
+// row loop (two compares per 64-bit row instead of a six-way select).
+template <int R, class T>
+__device__ __forceinline__ void cmp_rows(const T (&v)[R], T lit, int op, bool (&keep)[R]) {
+  switch (op) {
+    case TDP_EQ:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && v[r] == lit;
+      break;
+    case TDP_NE:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && !(v[r] == lit);
+      break;
+    case TDP_LT:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && v[r] < lit;
+      break;
+    case TDP_GT:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && v[r] > lit;
+      break;
+    case TDP_LE:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && v[r] <= lit;
+      break;
+    default:
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && v[r] >= lit;
+      break;
+  }
+}
+
+// Predicate-major evaluation of the conjunction over R rows of one thread:
+// for each predicate, the loads of all still-selected rows are issued
+// together (R independent loads in flight instead of one row's dependent
+// chain of switches).  row[r] must be a valid row wherever keep[r] is true.
+template <int R>
+__device__ __forceinline__ void eval_batch(const PredSet& ps, const i64 (&row)[R], bool (&keep)[R]) {
+  for (int k = 0; k < ps.npreds; ++k) {
+    const int cmp = ps.p[k].cmp, dt = ps.p[k].dtype, op = ps.p[k].op;
+    const void* ptr = ps.p[k].ptr;
+    if (cmp == TDP_CMP_NONE) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = false;
+    } else if (cmp == TDP_CMP_ALL) {
+      continue;
+    } else if (cmp == TDP_CMP_I64 && dt == TDP_I64) {
+      const i64* c = reinterpret_cast<const i64*>(ptr);
+      i64 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = keep[r] ? __ldg(c + row[r]) : 0;
+      cmp_rows<R, i64>(v, ps.p[k].li, op, keep);
+    } else if (cmp == TDP_CMP_F64 && dt == TDP_F64) {
+      const double* c = reinterpret_cast<const double*>(ptr);
+      double v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = keep[r] ? __ldg(c + row[r]) : 0.0;
+      cmp_rows<R, double>(v, ps.p[k].lf, op, keep);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && eval_pred(ps.p[k], row[r]);
+    }
+  }
+}
+
 // Host: translate public descriptors into the device predicate set.
 int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
                  int32_t npreds, int64_t n, PredSet* out);

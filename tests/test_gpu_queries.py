@@ -213,3 +213,21 @@ def test_group_result_row_count_is_deferred_until_read():
     assert res.row_count == len(exp["rf"])
     np.testing.assert_array_equal(res.columns[0].values.numpy(), exp["rf"])
     np.testing.assert_array_equal(res.column("count").values.numpy(), exp["count"])
+
+
+@pytest.mark.parametrize("unique", [True, False])
+def test_join_extreme_keys_unique_and_runs(unique):
+    """Unique build keys take the no-sort build; a repeated key falls back to
+    runs.  INT64_MIN (the table's empty image) and INT64_MAX must match."""
+    from paper_2211_02753_b200.kernels import join_indices
+
+    lo, hi = np.iinfo(np.int64).min, np.iinfo(np.int64).max
+    rng = np.random.default_rng(21)
+    build = np.concatenate([rng.permutation(50_000).astype(np.int64) * 7 - 100, [lo, hi]])
+    if not unique:
+        build = np.concatenate([build, build[:1000], [lo]])
+    probe = np.concatenate([rng.integers(-200, 400_000, size=90_000), [lo, hi, lo, 0]])
+    pi, bi = join_indices(torch.as_tensor(probe).cuda(), torch.as_tensor(build).cuda())
+    epi, ebi = orc.join_inner(probe, build)
+    np.testing.assert_array_equal(pi.cpu().numpy(), epi)
+    np.testing.assert_array_equal(bi.cpu().numpy(), ebi)

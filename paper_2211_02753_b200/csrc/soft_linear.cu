@@ -34,6 +34,7 @@ constexpr double kFixScale = 1073741824.0;  // 2^30, as soft_fwd_count_smem_kern
 
 struct OneHotKeys {
   int n;
+  int staged;  // codes of full stages ride in the ring behind the X rows
   const i64* codes[kMaxOneHot];
   i64 stride[kMaxOneHot];
   i64 dense_stride;
@@ -45,6 +46,68 @@ __device__ __forceinline__ i64 onehot_cell(const OneHotKeys& oh, i64 row) {
   for (int j = 0; j < kMaxOneHot; ++j)
     if (j < oh.n) base += __ldg(oh.codes[j] + row) * oh.stride[j];
   return base;
+}
+
+// Cell base of stage row `local` (global row `row`): from the stage's staged
+// code rows when present (full stages), else from global memory.
+__device__ __forceinline__ i64 onehot_cell_stage(const OneHotKeys& oh, const i64* __restrict__ sc,
+                                                 bool full, int local, i64 row) {
+  if (!(full && oh.staged)) return onehot_cell(oh, row);
+  i64 base = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxOneHot; ++j)
+    if (j < oh.n) base += sc[j * kVecRows + local] * oh.stride[j];
+  return base;
+}
+
+// Bytes of one ring stage: the X rows, then (staged) one 2 KB code row per key.
+template <class T>
+__host__ __device__ __forceinline__ size_t codes_offset(int d) {
+  return (size_t)kVecRows * d * sizeof(T);
+}
+template <class T>
+__host__ __device__ __forceinline__ size_t stage_size(int d, int staged_keys) {
+  return codes_offset<T>(d) + (size_t)staged_keys * kVecRows * sizeof(i64);
+}
+
+// Producer of the soft-linear ring: X rows in 8 KB bulk copies (several in
+// flight) and, for full stages, the tile's one-hot codes, so no consumer
+// waits on a dependent global load of the group keys.
+template <class T>
+__device__ __forceinline__ void ring_produce_codes(const T* __restrict__ X, const OneHotKeys& oh,
+                                                   i64 n, int d, int stages, size_t stage_bytes,
+                                                   unsigned char* ring, u64* full, u64* empty) {
+  const unsigned long long pol = l2_evict_first_policy();
+  const i64 ntiles = (n + kVecRows - 1) / kVecRows;
+  constexpr unsigned kChunk = 8 * 1024;
+  int s = 0;
+  unsigned eph = 0;
+  for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(smem_addr(&empty[s]), eph ^ 1u);
+    const i64 r0 = t * kVecRows;
+    const i64 nr = (n - r0) < kVecRows ? (n - r0) : kVecRows;
+    const unsigned xbytes = (unsigned)(nr * d * (i64)sizeof(T));
+    const bool codes = oh.staged && nr == kVecRows;
+    const unsigned cbytes = codes ? (unsigned)(oh.n * kVecRows * sizeof(i64)) : 0u;
+    const unsigned bar = smem_addr(&full[s]);
+    mbar_expect_tx(bar, xbytes + cbytes);
+    unsigned char* dst = ring + (size_t)s * stage_bytes;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(X + r0 * d);
+    for (unsigned off = 0; off < xbytes; off += kChunk) {
+      const unsigned b = xbytes - off < kChunk ? xbytes - off : kChunk;
+      bulk_load(smem_addr(dst + off), src + off, b, bar, pol);
+    }
+    if (codes)
+#pragma unroll
+      for (int j = 0; j < kMaxOneHot; ++j)
+        if (j < oh.n)
+          bulk_load(smem_addr(dst + codes_offset<T>(d) + (size_t)j * kVecRows * sizeof(i64)),
+                  oh.codes[j] + r0, kVecRows * sizeof(i64), bar, pol);
+    if (++s == stages) {
+      s = 0;
+      eph ^= 1u;
+    }
+  }
 }
 
 // softmax of one row held in registers; same operation order as
@@ -98,7 +161,7 @@ __global__ void __launch_bounds__(kRingThreads)
   __shared__ __align__(8) u64 empty[4];
   constexpr int d = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t stage_bytes = (size_t)kVecRows * d * sizeof(T);
+  const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   unsigned* lo = reinterpret_cast<unsigned*>(ring + (size_t)stages * stage_bytes);
   unsigned* hi = lo + cells;
   for (int c = threadIdx.x; c < 2 * cells; c += blockDim.x) lo[c] = 0u;
@@ -111,8 +174,7 @@ __global__ void __launch_bounds__(kRingThreads)
   }
   __syncthreads();
   if (warp == kRingWarps) {
-    if (lane == 0)
-      ring_produce<T>(X, nullptr, 0, n, d, kVecRows, stages, stage_bytes, ring, full, empty);
+    if (lane == 0) ring_produce_codes<T>(X, oh, n, d, stages, stage_bytes, ring, full, empty);
   } else {
     T w[V][K], bj[K];
     load_head<T, K, V>(W, bias, lane, w, bj);
@@ -122,16 +184,21 @@ __global__ void __launch_bounds__(kRingThreads)
     for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
       mbar_wait(smem_addr(&full[s]), fph);
       const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+      const i64* sc = reinterpret_cast<const i64*>(ring + (size_t)s * stage_bytes + codes_offset<T>(d));
       const i64 r0 = t * kVecRows;
       const i64 row = r0 + warp * 32 + lane;
+      const bool full_stage = r0 + kVecRows <= n;
       T z[K];
       bool valid = false;
-      if (r0 + kVecRows <= n) {
+      i64 base = 0;
+      if (full_stage) {
+        base = onehot_cell_stage(oh, sc, true, warp * 32 + lane, row);
         vec_row_dots<T, K, V, true>(sx, warp, r0, n, w, lane, z);
         valid = true;
       } else if (r0 + warp * 32 < n) {
         vec_row_dots<T, K, V, false>(sx, warp, r0, n, w, lane, z);
         valid = row < n;
+        if (valid) base = onehot_cell(oh, row);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_addr(&empty[s]));
@@ -140,7 +207,6 @@ __global__ void __launch_bounds__(kRingThreads)
         for (int j = 0; j < K; ++j) z[j] += bj[j];
         T p[K];
         softmax_row<T, K>(z, p);
-        const i64 base = onehot_cell(oh, row);
 #pragma unroll
         for (int j = 0; j < K; ++j) fix_add(lo, hi, grid, base + j * oh.dense_stride, (double)p[j]);
       }
@@ -172,7 +238,7 @@ __global__ void __launch_bounds__(kRingThreads)
   __shared__ __align__(8) u64 empty[4];
   constexpr int d = 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t stage_bytes = (size_t)kVecRows * d * sizeof(T);
+  const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   T* sG = reinterpret_cast<T*>(ring + (size_t)stages * stage_bytes);
   T* sdz = sG + ((cells + 3) & ~3);  // [kRingWarps][32][K]
   for (int c = threadIdx.x; c < cells; c += blockDim.x) sG[c] = (T)G[c];
@@ -185,8 +251,7 @@ __global__ void __launch_bounds__(kRingThreads)
   }
   __syncthreads();
   if (warp == kRingWarps) {
-    if (lane == 0)
-      ring_produce<T>(X, nullptr, 0, n, d, kVecRows, stages, stage_bytes, ring, full, empty);
+    if (lane == 0) ring_produce_codes<T>(X, oh, n, d, stages, stage_bytes, ring, full, empty);
     return;
   }
   T w[V][K], bj[K];
@@ -206,12 +271,15 @@ __global__ void __launch_bounds__(kRingThreads)
   for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
     mbar_wait(smem_addr(&full[s]), fph);
     const T* sx = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
+    const i64* sc = reinterpret_cast<const i64*>(ring + (size_t)s * stage_bytes + codes_offset<T>(d));
     const i64 r0 = t * kVecRows;
     const i64 row = r0 + warp * 32 + lane;
     const bool active = r0 + warp * 32 < n;  // warp-uniform
     T z[K];
     bool valid = false;
     const bool full_stage = r0 + kVecRows <= n;
+    i64 base = 0;
+    if (full_stage) base = onehot_cell_stage(oh, sc, true, warp * 32 + lane, row);
     if (full_stage) {
       vec_row_dots<T, K, V, true>(sx, warp, r0, n, w, lane, z);
       valid = true;
@@ -228,7 +296,7 @@ __global__ void __launch_bounds__(kRingThreads)
         for (int j = 0; j < K; ++j) z[j] += bj[j];
         T p[K], g[K];
         softmax_row<T, K>(z, p);
-        const i64 base = onehot_cell(oh, row);
+        if (!full_stage) base = onehot_cell(oh, row);
         T inner = 0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
@@ -299,10 +367,10 @@ struct Plan {
 };
 
 template <class T>
-bool make_plan(const void* X, i64 n, int d, int k, i64 cells, bool bwd, Plan* p) {
+bool make_plan(const void* X, i64 n, int d, int k, i64 cells, bool bwd, int staged_keys, Plan* p) {
   const int V = vec_width<T>(reinterpret_cast<const T*>(X), n, d);
   if (V == 0 || V > 2 || k < 1 || k > kMaxK || cells < 1 || cells > kMaxCells) return false;
-  const size_t stage = (size_t)kVecRows * d * sizeof(T);
+  const size_t stage = stage_size<T>(d, staged_keys);
   const size_t extra = bwd ? (size_t)((cells + 3) & ~3) * sizeof(T) +
                                  (size_t)kRingWarps * 32 * k * sizeof(T)
                            : (size_t)cells * 2 * sizeof(unsigned);
@@ -341,14 +409,21 @@ int make_keys(const tdp_soft_key* keys, int nkeys, int dense_key, int k, i64* ce
     TDP_REQUIRE(stride <= kMaxCells, "soft_linear: grid exceeds %d cells", kMaxCells);
   }
   *cells = stride;
+  // stage the codes in the ring when every code array is 16-byte aligned
+  // (bulk-copy requirement; full stages start at multiples of 256 rows)
+  oh->staged = oh->n > 0 ? 1 : 0;
+  for (int j = 0; j < oh->n; ++j)
+    if (((uintptr_t)oh->codes[j] & 15) != 0) oh->staged = 0;
   return TDP_OK;
 }
 
 template <class T>
 int launch_fwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
-               const OneHotKeys& oh, i64 cells, double* grid, cudaStream_t st) {
+               const OneHotKeys& oh_in, i64 cells, double* grid, cudaStream_t st) {
   Plan p;
-  if (!make_plan<T>(X, n, d, k, cells, false, &p))
+  OneHotKeys oh = oh_in;
+  if (oh.staged && !make_plan<T>(X, n, d, k, cells, false, oh.n, &p)) oh.staged = 0;
+  if (!oh.staged && !make_plan<T>(X, n, d, k, cells, false, 0, &p))
     return set_error(TDP_ENOTSUP, "soft_linear: unsupported shape (n=%lld d=%d k=%d cells=%lld)",
                      (long long)n, d, k, (long long)cells);
   bool launched = false;
@@ -371,10 +446,12 @@ int launch_fwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
 
 template <class T>
 int launch_bwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
-               const OneHotKeys& oh, i64 cells, const double* G, void* dW, void* db, void* ws,
+               const OneHotKeys& oh_in, i64 cells, const double* G, void* dW, void* db, void* ws,
                size_t ws_bytes, cudaStream_t st) {
   Plan p;
-  if (!make_plan<T>(X, n, d, k, cells, true, &p))
+  OneHotKeys oh = oh_in;
+  if (oh.staged && !make_plan<T>(X, n, d, k, cells, true, oh.n, &p)) oh.staged = 0;
+  if (!oh.staged && !make_plan<T>(X, n, d, k, cells, true, 0, &p))
     return set_error(TDP_ENOTSUP, "soft_linear: unsupported shape (n=%lld d=%d k=%d cells=%lld)",
                      (long long)n, d, k, (long long)cells);
   const int width = d * k + k;
@@ -413,11 +490,11 @@ int tdp_soft_linear_supported(int32_t dtype, int64_t n, int32_t d, int32_t k, in
                               const void* X) {
   Plan p;
   if (dtype == TDP_F32)
-    return make_plan<float>(X, n, d, k, cells, false, &p) &&
-           make_plan<float>(X, n, d, k, cells, true, &p);
+    return make_plan<float>(X, n, d, k, cells, false, 0, &p) &&
+           make_plan<float>(X, n, d, k, cells, true, 0, &p);
   if (dtype == TDP_F64)
-    return make_plan<double>(X, n, d, k, cells, false, &p) &&
-           make_plan<double>(X, n, d, k, cells, true, &p);
+    return make_plan<double>(X, n, d, k, cells, false, 0, &p) &&
+           make_plan<double>(X, n, d, k, cells, true, 0, &p);
   return 0;
 }
 

@@ -9,9 +9,10 @@ as one fused pass (tdp_scan_aggregate).  ``--query q6`` selects TPC-H Q6.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One process per GPU (torchrun for N > 1): lineitem rows are sharded by rank
-(total fixed at SF10 -> "strong" scaling) and partial aggregates are merged
-with NCCL all-reduces.  Rank 0 prints one JSON line.
+One process per GPU (torchrun for N > 1): every rank holds an SF10 shard of
+lineitem (the table is SF10 x N -- "weak" scaling, the row-partitioned path
+of SURVEY §8(e)) and the partial aggregates are merged with NCCL all-reduces
+inside the query.  Rank 0 prints one JSON line.
 
 ``--impl reference`` times the reference's algorithm on the host cores: the
 numpy restatement in oracle/ (the reference itself is Python/numpy and cannot
@@ -180,9 +181,8 @@ def _ours(args):
             dist.init_process_group(backend)
     group = dist.group.WORLD if world > 1 else None
 
-    n_total = int(round(6_000_000 * args.sf))
-    lo, hi = shard_bounds(n_total, rank, world)
-    rows = hi - lo
+    rows = int(round(6_000_000 * args.sf))  # per rank (weak scaling)
+    n_total = rows * world
     arrays = wl.lineitem_arrays(args.sf, seed=42 + rank, rows=rows)
     cols = wl.LINEITEM_COLUMNS
     if args.query == "q1":
@@ -292,12 +292,14 @@ def _ours(args):
         "warmup": max(args.warmup, 3),
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), resident in HBM",
-        "config": dict(_workload(args.query, args.sf, n_total),
-                       parallelism=f"dp{world} row-sharded, NCCL all-reduce of partial aggregates",
+        "config": dict(_workload(args.query, args.sf * world, n_total),
+                       sf_per_gpu=args.sf,
+                       parallelism=f"dp{world}: one SF{args.sf:g} lineitem shard per GPU, "
+                                   f"NCCL all-reduce of partial aggregates",
                        l2="inputs larger than L2 (no flush needed)",
                        step="CompiledQuery.run(catalog) of the SQL plan, result table on device"),
         "hbm_gbs_step": bpr * n_total / (ms / 1e3) / 1e9,
@@ -400,16 +402,17 @@ def _reference(args):
     from paper_2211_02753_b200 import workloads as wl
 
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    n_total = int(round(6_000_000 * args.sf))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    n_total = int(round(6_000_000 * args.sf)) * world  # our arm's table: SF10 per GPU
     # calibrate one core, then size the per-step sample so the run stays short
-    cal = wl.lineitem_arrays(args.sf, seed=42, rows=min(n_total, 1_000_000))
+    cal = wl.lineitem_arrays(args.sf, seed=42, rows=1_000_000)
     _REF_ARRAYS.clear()
     _REF_ARRAYS.update(cal)
     w0 = time.perf_counter()
     _ref_worker((args.query, 0, len(cal["l_shipdate"])))
     per_core = len(cal["l_shipdate"]) / (time.perf_counter() - w0)
     budget_s = max(0.05, 150.0 / max(1, args.steps + args.warmup))
-    sample = int(min(n_total, per_core * cores * budget_s))
+    sample = int(min(6_000_000 * args.sf, per_core * cores * budget_s))
     sample = max(sample, cores)
     arrays = wl.lineitem_arrays(args.sf, seed=42, rows=sample)
     _REF_ARRAYS.clear()
@@ -430,9 +433,9 @@ def _reference(args):
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), in host RAM",
-        "config": dict(_workload(args.query, args.sf, n_total),
+        "config": dict(_workload(args.query, args.sf * world, n_total), sf_per_gpu=args.sf,
                        parallelism=f"{cores} host processes, row-sharded, partials merged"),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "port",

@@ -475,3 +475,32 @@ def deferred_rows(t) -> Optional[DeferredCount]:
             and t._lazy.count._value is None:
         return t._lazy.count
     return None
+
+
+class SelectionRows:
+    """Row count of a filtered relation that has not been evaluated yet: a
+    result table over lazy views reads it (running the filter) only when its
+    ``row_count`` or a column's data is first needed."""
+
+    __slots__ = ("sel",)
+
+    def __init__(self, sel: Selection):
+        self.sel = sel
+
+    def value(self) -> int:
+        return self.sel.count()
+
+
+def deferred_selection(columns) -> Optional[Selection]:
+    """The common unevaluated Selection of columns that are all lazy views of
+    it (values of EncodedTensors), else None."""
+    sel = None
+    for c in columns:
+        t = c.values
+        if not (isinstance(t, _T.Tensor) and t._t is None and isinstance(t._lazy, LazyValue)):
+            return None
+        s = t._lazy.sel
+        if s is None or s._count is not None or (sel is not None and s is not sel):
+            return None
+        sel = s
+    return sel

@@ -611,17 +611,19 @@ __device__ __forceinline__ i64 join_row(i64 tile, int k) {
   return tile * kJoinTile + (i64)k * kJoinThreads + threadIdx.x;
 }
 
-template <bool kFiltered>
-__global__ void __launch_bounds__(kJoinThreads)
+// tile_counts must be zeroed: every warp adds its pair count (no CTA barrier,
+// so a warp leaves as soon as its own lookups are done).  Three batched
+// rounds of loads per thread (keys + predicate columns, Bloom words, table
+// slots), 8 rows each; with unique build keys only the slot keys are read.
+template <bool kFiltered, bool kUnique>
+__global__ void __launch_bounds__(kJoinThreads, kUnique ? 4 : 3)
     join_count_kernel(HashTable ht, const i64* __restrict__ probe, i64 np, PredSet ps,
                       unsigned* __restrict__ match_bits, i64* __restrict__ word_counts,
                       i64* __restrict__ tile_counts) {
-  __shared__ i64 warp_sums[kJoinWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
   bool act[kJoinPer];
   i64 row[kJoinPer], key[kJoinPer];
-  u64 h[kJoinPer];
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
     row[k] = join_row(tile, k);
@@ -635,43 +637,53 @@ __global__ void __launch_bounds__(kJoinThreads)
   if (kFiltered) eval_batch<kJoinPer>(ps, row, act);
   unsigned bw[kJoinPer];
 #pragma unroll
-  for (int k = 0; k < kJoinPer; ++k) {
-    h[k] = join_hash(key[k]);
-    bw[k] = act[k] ? *bloom_word(ht, h[k]) : 0u;
-  }
-  longlong2 e[kJoinPer];
+  for (int k = 0; k < kJoinPer; ++k)
+    bw[k] = act[k] ? *bloom_word(ht, join_hash(key[k])) : 0u;
+  unsigned slot[kJoinPer];
+  i64 ex[kJoinPer], ey[kJoinPer];
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
-    const unsigned m = bloom_mask(h[k]);
+    const u64 h = join_hash(key[k]);
+    const unsigned m = bloom_mask(h);
     act[k] = act[k] && (key[k] == kMinKey || (bw[k] & m) == m);
-    h[k] &= ht.mask;
-    e[k] = act[k] ? ht.slot[h[k]] : make_longlong2(0, 0);
+    slot[k] = (unsigned)(h & ht.mask);
+    ex[k] = 0;
+    ey[k] = 0;
+    if (act[k]) {
+      if (kUnique) {
+        ex[k] = ht.slot[slot[k]].x;
+      } else {
+        const longlong2 e = ht.slot[slot[k]];
+        ex[k] = e.x;
+        ey[k] = e.y;
+      }
+    }
   }
-  const bool unique = ht.flags[1] == 0;  // at most one pair per probe row
   i64 local = 0;
 #pragma unroll
   for (int k = 0; k < kJoinPer; ++k) {
     i64 c = 0;
     if (act[k]) {
-      i64 st;
-      join_resolve(ht, key[k], h[k], e[k], &st, &c);
+      if (kUnique && key[k] != kMinKey && ex[k] == (key[k] ^ kMinKey)) {
+        c = 1;
+      } else if (key[k] != kMinKey && ex[k] == 0) {
+        c = 0;
+      } else {
+        i64 st;
+        join_resolve(ht, key[k], slot[k], make_longlong2(ex[k], kUnique ? ht.slot[slot[k]].y : ey[k]),
+                     &st, &c);
+      }
     }
     const unsigned word = __ballot_sync(0xffffffffu, c > 0);
-    const i64 wc = unique ? (i64)__popc(word) : (word ? warp_sum(c) : 0);
+    const i64 wc = kUnique ? (i64)__popc(word) : (word ? warp_sum(c) : 0);
     if (lane == 0) {
       match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
       word_counts[tile * kJoinWords + k * kJoinWarps + warp] = wc;
     }
     local += wc;
   }
-  if (lane == 0) warp_sums[warp] = local;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    i64 t = 0;
-#pragma unroll
-    for (int w = 0; w < kJoinWarps; ++w) t += warp_sums[w];
-    tile_counts[tile] = t;
-  }
+  if (lane == 0 && local != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(tile_counts + tile), (unsigned long long)local);
 }
 
 // Exclusive prefix of a tile's 64 word pair counts, per warp (lane l holds
@@ -902,16 +914,16 @@ int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* prob
                                                                              j.ht);
     TDP_LAUNCH_CHECK("join_build_runs_kernel");
   }
-  if (ps != nullptr && ps->npreds > 0) {
-    join_count_kernel<true><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
-        j.ht, probe_keys, n_probe, *ps, j.match_bits, j.word_counts, j.tile_counts);
-  } else {
-    PredSet none;
-    none.npreds = 0;
-    none.pad = 0;
-    join_count_kernel<false><<<(unsigned)tiles, kJoinThreads, 0, st>>>(
-        j.ht, probe_keys, n_probe, none, j.match_bits, j.word_counts, j.tile_counts);
-  }
+  TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
+  PredSet none;
+  none.npreds = 0;
+  none.pad = 0;
+  const bool filtered = ps != nullptr && ps->npreds > 0;
+  const PredSet& pp = filtered ? *ps : none;
+  auto kernel = filtered ? (repeated ? join_count_kernel<true, false> : join_count_kernel<true, true>)
+                         : (repeated ? join_count_kernel<false, false> : join_count_kernel<false, true>);
+  kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, pp, j.match_bits,
+                                                   j.word_counts, j.tile_counts);
   TDP_LAUNCH_CHECK("join_count_kernel");
   return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
                             j.scan_bytes, st);

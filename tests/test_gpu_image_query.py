@@ -27,7 +27,8 @@ def _cnn(k: int) -> torch.nn.Module:
         torch.nn.Flatten(), torch.nn.Linear(400, k))
 
 
-def test_cnn_image_query_matches_torch_reference():
+@pytest.mark.parametrize("chunk_rows", [0, 128])
+def test_cnn_image_query_matches_torch_reference(chunk_rows):
     k, n = 4, 600
     rng = np.random.default_rng(0)
     images = rng.random((n, 28, 28)).astype(np.float64)
@@ -36,7 +37,7 @@ def test_cnn_image_query_matches_torch_reference():
     ref_net = _cnn(k).double()
     ref_net.load_state_dict(net.state_dict())
     net = net.cuda()
-    model = TorchModel(net, "cnn")
+    model = TorchModel(net, "cnn", chunk_rows=chunk_rows)
     reg = tq.UdfRegistry()
     reg.register(tq.classifier_tvf("cnn", model, k, "Pred"))
     cat = tq.Catalog()

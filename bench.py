@@ -51,6 +51,8 @@ def _args():
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--encoding", choices=("wide", "compact"), default="wide",
+                    help="compact: lossless narrow column storage (SURVEY §8(f) 1)")
     return ap.parse_args()
 
 
@@ -62,15 +64,23 @@ def _peaks() -> tuple[float, str]:
         return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def _workload(query: str, sf: float, rows: int) -> dict:
+def _workload(query: str, sf: float, rows: int, encoding: str = "wide", bpr: int = 0) -> dict:
     if query == "q1":
-        return {"workload": f"TPC-H Q1 SF{sf:g}: filter l_shipdate<=10471 -> q1prep UDF "
-                            "(disc_price, charge) -> GROUP BY returnflag, linestatus, 8 aggregates",
-                "sf": sf, "rows": rows, "bytes_per_row": 56,
-                "columns": "7 x 8 B (int64 dates/dictionary codes, float64 values)"}
-    return {"workload": f"TPC-H Q6 SF{sf:g}: 5-predicate filter -> revenue UDF -> SUM",
-            "sf": sf, "rows": rows, "bytes_per_row": 32,
-            "columns": "4 x 8 B (int64 shipdate, float64 values)"}
+        w = {"workload": f"TPC-H Q1 SF{sf:g}: filter l_shipdate<=10471 -> q1prep UDF "
+                         "(disc_price, charge) -> GROUP BY returnflag, linestatus, 8 aggregates",
+             "sf": sf, "rows": rows, "bytes_per_row": 56,
+             "columns": "7 x 8 B (int64 dates/dictionary codes, float64 values)"}
+    else:
+        w = {"workload": f"TPC-H Q6 SF{sf:g}: 5-predicate filter -> revenue UDF -> SUM",
+             "sf": sf, "rows": rows, "bytes_per_row": 32,
+             "columns": "4 x 8 B (int64 shipdate, float64 values)"}
+    if encoding == "compact":
+        w["bytes_per_row"] = bpr
+        w["columns"] = ("compact storage (SURVEY §8(f) 1): int16 dates, uint8 dictionary codes, "
+                        "scaled-decimal int8/int32 values; decoded values bit-identical to the "
+                        "8 B reference columns")
+        w["encoding"] = "compact"
+    return w
 
 
 # ---------------------------------------------------------------------------
@@ -193,8 +203,14 @@ def _ours(args):
         sql, reg, bpr = wl.Q6_SQL, wl.q6_registry(), wl.Q6_BYTES_PER_ROW
         cols = ("l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
 
+    table = wl.lineitem_table(arrays, cols)
+    if args.encoding == "compact":  # ingestion, outside the timed region
+        from paper_2211_02753_b200 import compact as cp
+
+        table = cp.compact_table(table)
+        bpr = sum(cp.stored_bytes(c) for c in table.columns)
     cat = tq.Catalog()
-    cat.register("lineitem", wl.lineitem_table(arrays, cols))
+    cat.register("lineitem", table)
     query = wl.compile_sql(sql, cat, reg)
 
     def barrier():
@@ -242,12 +258,25 @@ def _ours(args):
             launches = int(lt.item())
 
         # ---- end to end through the API from pinned host buffers ----------
-        host = {c: torch.from_numpy(arrays[c]).pin_memory() for c in cols}
-        h2d = sum(h.numel() * h.element_size() for h in host.values())
+        if args.encoding == "compact":
+            from paper_2211_02753_b200 import compact as cp
+
+            host_stored = [t.cpu().pin_memory() for t in cp.stored_tensors(table)]
+            h2d = sum(h.numel() * h.element_size() for h in host_stored)
+
+            def make_table():
+                dev = [h.to("cuda", non_blocking=True) for h in host_stored]
+                return cp.table_from_stored(table, dev)
+        else:
+            host = {c: torch.from_numpy(arrays[c]).pin_memory() for c in cols}
+            h2d = sum(h.numel() * h.element_size() for h in host.values())
+
+            def make_table():
+                return wl.lineitem_table(host, cols)
 
         def e2e_step():
             c2 = tq.Catalog()
-            c2.register("lineitem", wl.lineitem_table(host, cols))
+            c2.register("lineitem", make_table())
             out = query.run(c2)
             vals = [c.values.numpy() for c in out.columns]
             return sum(v.nbytes for v in vals)
@@ -281,7 +310,7 @@ def _ours(args):
     if tf.exists():
         try:
             tj = json.loads(tf.read_text())
-            key = f"{args.query}_sf{args.sf:g}_n{world}"
+            key = f"{args.query}_sf{args.sf:g}_n{world}" + ("_compact" if args.encoding == "compact" else "")
             traffic = tj.get(key)
         except Exception:
             traffic = None
@@ -298,7 +327,7 @@ def _ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), resident in HBM",
-        "config": dict(_workload(args.query, args.sf * world, n_total),
+        "config": dict(_workload(args.query, args.sf * world, n_total, args.encoding, bpr),
                        sf_per_gpu=args.sf,
                        parallelism=f"dp{world}: one SF{args.sf:g} lineitem shard per GPU, "
                                    f"NCCL all-reduce of partial aggregates",
@@ -347,7 +376,12 @@ def _cpu_baseline(args, arrays, query, cat):
     c2 = tq.Catalog()
     cols = wl.LINEITEM_COLUMNS if args.query == "q1" else (
         "l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
-    c2.register("lineitem", wl.lineitem_table(sample, cols))
+    t2 = wl.lineitem_table(sample, cols)
+    if args.encoding == "compact":
+        from paper_2211_02753_b200 import compact as cp
+
+        t2 = cp.compact_table(t2)
+    c2.register("lineitem", t2)
     res = query.run(c2)
     got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
     ok = True

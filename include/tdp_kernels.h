@@ -53,7 +53,13 @@ enum tdp_dtype {
   TDP_F64 = 1,
   TDP_F32 = 2,
   TDP_BOOL = 3, /* one byte per value, 0/1 */
-  TDP_I32 = 4
+  TDP_I32 = 4,
+  /* compact storage widths: a narrow stored column whose
+   * logical value is int64 (or float64 through TDP_CMP_DEC / a program
+   * CAST + DIV); values are widened on load, never written              */
+  TDP_I8 = 5,
+  TDP_I16 = 6,
+  TDP_U8 = 7
 };
 
 /* A column: `rows` values of `width` elements each, row-major, contiguous.
@@ -77,13 +83,17 @@ enum tdp_cmp_op { TDP_EQ = 0, TDP_NE = 1, TDP_LT = 2, TDP_GT = 3, TDP_LE = 4, TD
  *   TDP_CMP_F64  double(x) <op> lit_f
  *   TDP_CMP_F32  float(x)  <op> (float)lit_f  (lit_f holds an exact float32)
  *   TDP_CMP_NONE row never matches (absent dictionary literal, :74-76)
- *   TDP_CMP_ALL  row always matches (out-of-range int literal)            */
+ *   TDP_CMP_ALL  row always matches (out-of-range int literal)
+ *   TDP_CMP_DEC  double(x) / double(lit_i) <op> lit_f: a float64 column kept
+ *                as scaled integers (x = value * lit_i exactly), compared
+ *                after the same correctly rounded division that decodes it */
 enum tdp_cmp_type {
   TDP_CMP_I64 = 0,
   TDP_CMP_F64 = 1,
   TDP_CMP_F32 = 2,
   TDP_CMP_NONE = 3,
-  TDP_CMP_ALL = 4
+  TDP_CMP_ALL = 4,
+  TDP_CMP_DEC = 5
 };
 
 typedef struct tdp_predicate {
@@ -159,7 +169,11 @@ enum tdp_opcode {
   TDP_OP_SQUARE = 8,
   TDP_OP_LOG = 9,
   TDP_OP_EXP = 10,
-  TDP_OP_RELU = 11
+  TDP_OP_RELU = 11,
+  TDP_OP_DECIMAL = 12 /* a (int64) / imm_f, correctly rounded without a
+                       * divide: q = a*inv, q += fma(-q, imm_f, a)*inv with
+                       * inv = bits(imm_i) = RN(1/imm_f); compact.py checks
+                       * at ingestion that it equals the stored float64  */
 };
 
 typedef struct tdp_instr {

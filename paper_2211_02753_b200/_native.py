@@ -26,17 +26,18 @@ TDP_OK, TDP_EINVAL, TDP_ECUDA, TDP_ENOMEM, TDP_ENOTSUP, TDP_EJIT = 0, -1, -2, -3
 
 # dtypes
 I64, F64, F32, BOOL, I32 = 0, 1, 2, 3, 4
+I8, I16, U8 = 5, 6, 7  # compact storage widths (compact.py)
 TORCH_TO_TDP = {torch.int64: I64, torch.float64: F64, torch.float32: F32, torch.bool: BOOL,
-                torch.int32: I32}
+                torch.int32: I32, torch.int8: I8, torch.int16: I16, torch.uint8: U8}
 NAME_TO_TDP = {"int64": I64, "float64": F64, "float32": F32, "bool": BOOL}
 
 # comparison ops / kinds
 CMP_OPS = {"=": 0, "<>": 1, "<": 2, ">": 3, "<=": 4, ">=": 5}
-CMP_I64, CMP_F64, CMP_F32, CMP_NONE, CMP_ALL = 0, 1, 2, 3, 4
+CMP_I64, CMP_F64, CMP_F32, CMP_NONE, CMP_ALL, CMP_DEC = 0, 1, 2, 3, 4, 5
 
 # expression opcodes
 OP_LOAD, OP_CONST, OP_CAST, OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3, 4, 5, 6
-OP_NEG, OP_SQUARE, OP_LOG, OP_EXP, OP_RELU = 7, 8, 9, 10, 11
+OP_NEG, OP_SQUARE, OP_LOG, OP_EXP, OP_RELU, OP_DECIMAL = 7, 8, 9, 10, 11, 12
 
 AGG_COUNT, AGG_SUM_F64, AGG_SUM_I64 = 0, 1, 2
 SOFT_DENSE, SOFT_ONEHOT = 0, 1

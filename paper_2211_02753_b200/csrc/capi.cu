@@ -51,8 +51,9 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
   for (int k = 0; k < npreds; ++k) {
     const tdp_predicate& p = preds[k];
     TDP_REQUIRE(p.op >= TDP_EQ && p.op <= TDP_GE, "predicate %d: bad operator %d", k, p.op);
-    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_ALL, "predicate %d: bad compare kind",
+    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_DEC, "predicate %d: bad compare kind",
                 k);
+    TDP_REQUIRE(p.cmp != TDP_CMP_DEC || p.lit_i > 0, "predicate %d: decimal divisor must be > 0", k);
     DevPred& d = out->p[k];
     d.op = p.op;
     d.cmp = p.cmp;
@@ -72,6 +73,9 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
                 (long long)n);
     TDP_REQUIRE(dtype_size(c.dtype) > 0, "predicate %d: bad column dtype %d", k, c.dtype);
     TDP_REQUIRE(n == 0 || c.data != nullptr, "predicate %d: null column", k);
+    TDP_REQUIRE(p.cmp != TDP_CMP_DEC || c.dtype == TDP_I64 || c.dtype == TDP_I32 ||
+                    c.dtype == TDP_I16 || c.dtype == TDP_I8 || c.dtype == TDP_U8,
+                "predicate %d: decimal compare needs an integer column", k);
     d.ptr = c.data;
     d.dtype = c.dtype;
   }

@@ -127,6 +127,10 @@ const char* ctype_of(int dt) {
       return "float";
     case TDP_I32:
       return "int";
+    case TDP_I16:
+      return "short";
+    case TDP_I8:
+      return "signed char";
     default:
       return "unsigned char";
   }
@@ -183,8 +187,9 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
   for (size_t k = 0; k < s.preds.size(); ++k) {
     const tdp_predicate& p = s.preds[k];
     TDP_REQUIRE(p.op >= TDP_EQ && p.op <= TDP_GE, "predicate %zu: bad op", k);
-    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_ALL, "predicate %zu: bad compare", k);
-    if (p.cmp <= TDP_CMP_F32) {
+    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_DEC, "predicate %zu: bad compare", k);
+    TDP_REQUIRE(p.cmp != TDP_CMP_DEC || p.lit_i > 0, "predicate %zu: bad decimal divisor", k);
+    if (p.cmp <= TDP_CMP_F32 || p.cmp == TDP_CMP_DEC) {
       TDP_REQUIRE(p.column >= 0 && p.column < ncols, "predicate %zu: bad column", k);
       used[p.column] = 1;
     }
@@ -216,6 +221,12 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
         TDP_REQUIRE(s.prog[in.a].dtype == in.dtype, "instr %zu: operand a type mismatch", j);
         if (in.op == TDP_OP_DIV || in.op == TDP_OP_LOG || in.op == TDP_OP_EXP)
           TDP_REQUIRE(in.dtype != TDP_I64, "instr %zu: float-only op on int64", j);
+        break;
+      case TDP_OP_DECIMAL:
+        TDP_REQUIRE(in.a >= 0 && in.a < (int)j, "instr %zu: bad decimal operand", j);
+        TDP_REQUIRE(in.dtype == TDP_F64 && s.prog[in.a].dtype == TDP_I64,
+                    "instr %zu: decimal decodes int64 to float64", j);
+        TDP_REQUIRE(in.imm_f > 0.0, "instr %zu: decimal divisor must be > 0", j);
         break;
       case TDP_OP_CAST:
         TDP_REQUIRE(in.a >= 0 && in.a < (int)j, "instr %zu: bad cast operand", j);
@@ -295,6 +306,10 @@ void emit_program(std::ostringstream& o, const Spec& s) {
       case TDP_OP_CAST:
         o << "(" << T << ")" << a;
         break;
+      case TDP_OP_DECIMAL:
+        o << "tdp_decimal((double)" << a << ", P.imf[" << j << "], __longlong_as_double(P.imi[" << j
+          << "]))";
+        break;
       case TDP_OP_ADD:
         if (isint) o << "(i64)((u64)" << a << " + (u64)" << b << ")";
         else o << a << " + " << b;
@@ -359,6 +374,8 @@ std::string generate(const Spec& s) {
   std::ostringstream o;
   const Ring ring = ring_shape(s);
   o << "typedef long long i64;\ntypedef unsigned long long u64;\n";
+  o << "__device__ __forceinline__ double tdp_decimal(double x, double d, double inv) {\n"
+       "  const double q = x * inv;\n  return fma(fma(-q, d, x), inv, q);\n}\n";
   o << "#define TDP_THREADS " << kThreads << "\n#define TDP_U " << kUnroll << "\n";
   o << "#define TDP_CONS_WARPS " << kConsWarps << "\n#define TDP_PU " << ring.pu
     << "\n#define TDP_PTILE " << ring.ptile << "\n#define TDP_STAGE_BYTES " << ring.stage_bytes
@@ -426,6 +443,10 @@ std::string generate(const Spec& s) {
       case TDP_CMP_F32:
         o << "  keep &= ((float)r.c" << p.column << " " << op_sym(p.op) << " (float)P.plf[" << k
           << "]);\n";
+        break;
+      case TDP_CMP_DEC:
+        o << "  keep &= ((double)r.c" << p.column << " / (double)P.pli[" << k << "] "
+          << op_sym(p.op) << " P.plf[" << k << "]);\n";
         break;
       case TDP_CMP_NONE:
         o << "  keep = false;\n";

@@ -61,7 +61,11 @@ inline int dtype_size(int dt) {
     case TDP_F32:
     case TDP_I32:
       return 4;
+    case TDP_I16:
+      return 2;
     case TDP_BOOL:
+    case TDP_I8:
+    case TDP_U8:
       return 1;
     default:
       return 0;
@@ -106,7 +110,12 @@ __device__ __forceinline__ i64 load_as_i64(const void* base, int dt, i64 i) {
       return __ldg(reinterpret_cast<const i64*>(base) + i);
     case TDP_I32:
       return (i64)__ldg(reinterpret_cast<const int*>(base) + i);
+    case TDP_I16:
+      return (i64)__ldg(reinterpret_cast<const short*>(base) + i);
+    case TDP_I8:
+      return (i64)__ldg(reinterpret_cast<const signed char*>(base) + i);
     case TDP_BOOL:
+    case TDP_U8:
       return (i64)reinterpret_cast<const unsigned char*>(base)[i];
     case TDP_F64:
       return (i64)__ldg(reinterpret_cast<const double*>(base) + i);
@@ -125,6 +134,10 @@ __device__ __forceinline__ double load_as_f64(const void* base, int dt, i64 i) {
       return (double)__ldg(reinterpret_cast<const i64*>(base) + i);
     case TDP_I32:
       return (double)__ldg(reinterpret_cast<const int*>(base) + i);
+    case TDP_I16:
+      return (double)__ldg(reinterpret_cast<const short*>(base) + i);
+    case TDP_I8:
+      return (double)__ldg(reinterpret_cast<const signed char*>(base) + i);
     default:
       return (double)reinterpret_cast<const unsigned char*>(base)[i];
   }
@@ -172,6 +185,8 @@ __device__ __forceinline__ bool eval_pred(const DevPred& p, i64 i) {
       return compare<double>(load_as_f64(p.ptr, p.dtype, i), p.lf, p.op);
     case TDP_CMP_F32:
       return compare<float>(load_as_f32(p.ptr, p.dtype, i), (float)p.lf, p.op);
+    case TDP_CMP_DEC:
+      return compare<double>((double)load_as_i64(p.ptr, p.dtype, i) / (double)p.li, p.lf, p.op);
     case TDP_CMP_NONE:
       return false;
     default:

@@ -54,6 +54,8 @@ from .lazy import (
     Selection,
     as_expr,
     base_rows,
+    compact_source,
+    decimal_predicates,
     resolve_predicate,
 )
 from .distributed import (
@@ -123,8 +125,13 @@ def take_rows(col: EncodedTensor, indices) -> EncodedTensor:
 _OPS = ("=", "<>", "<", ">", "<=", ">=")
 
 
-def _resolve(col: EncodedTensor, op: str, literal, base: Optional[torch.Tensor]) -> Pred:
-    """Validate one comparison exactly as comparison_mask does and resolve it."""
+def _resolve(col: EncodedTensor, op: str, literal, base: Optional[torch.Tensor],
+             divisor: int = 0) -> Pred:
+    """Validate one comparison exactly as comparison_mask does and resolve it.
+
+    ``divisor`` > 0: ``base`` holds the column as scaled integers (a compact
+    float64 column, compact.py); the float64 comparison becomes a decimal one
+    on the stored integers (decode by the same division, then compare)."""
     if op not in _OPS:
         raise KernelError(f"unknown comparison operator {op!r}")
     if col.is_dictionary():
@@ -141,7 +148,25 @@ def _resolve(col: EncodedTensor, op: str, literal, base: Optional[torch.Tensor])
     if col.values.ndim != 1:
         raise KernelError("filters require scalar columns")
     cmp, li, lf = resolve_predicate(col.values.dtype, op, literal)
+    if divisor and cmp == nat.CMP_F64:
+        raise KernelError("decimal column predicates resolve through _resolve_all")
     return Pred(base if cmp in (nat.CMP_I64, nat.CMP_F64, nat.CMP_F32) else None, op, cmp, li, lf)
+
+
+def _resolve_all(col: EncodedTensor, op: str, literal, base: Optional[torch.Tensor],
+                 divisor: int = 0) -> list[Pred]:
+    """_resolve, with predicates on compact decimal columns rewritten into
+    int64 comparisons on the stored integers (lazy.decimal_predicates)."""
+    if divisor and not col.is_dictionary() and not col.is_pe() and op in _OPS \
+            and not isinstance(literal, str) and col.values.ndim == 1:
+        cmp, _, lf = resolve_predicate(col.values.dtype, op, literal)
+        if cmp == nat.CMP_F64:
+            out = []
+            for o, c, li in decimal_predicates(op, lf, divisor):
+                keep = c in (nat.CMP_I64, nat.CMP_DEC)
+                out.append(Pred(base if keep else None, o, c, li, lf))
+            return out
+    return [_resolve(col, op, literal, base)]
 
 
 def comparison_mask(col: EncodedTensor, op: str, literal) -> torch.Tensor:
@@ -200,15 +225,17 @@ def filter_exact(columns: Sequence[EncodedTensor],
     for idx, op, literal in predicates:
         col = columns[idx]
         v = col.values
-        base = None
+        base, divisor = None, 0
         if not col.is_pe() and v.ndim == 1:
             if v._t is not None:
                 base = v._t
             elif v._lazy.expr.op == "col":
                 base = v._lazy.expr.col
+            elif compact_source(v._lazy.expr) is not None:  # compact storage
+                base, divisor = compact_source(v._lazy.expr)
             else:  # predicate on a computed column: evaluate eagerly
                 return _filter_eager(columns, predicates)
-        preds.append(_resolve(col, op, literal, base))
+        preds.extend(_resolve_all(col, op, literal, base, divisor))
     device = _device_of([as_expr(c.values)[0] for c in columns], sel)
     new_sel = sel.refine(preds) if sel is not None else Selection(n, preds, device)
     out = []

@@ -178,6 +178,68 @@ class Expr:
         return self if dtype == self.dtype else Expr("cast", dtype, (self,))
 
 
+NARROW_INTS = ("int32", "int16", "int8", "uint8")
+
+
+def compact_source(e: Expr) -> Optional[tuple[torch.Tensor, int]]:
+    """(stored narrow column, decimal divisor or 0) when ``e`` decodes a
+    compact column (compact.py): ``cast(col)`` to int64, or
+    ``cast(col) / const`` to float64."""
+    if e.op == "cast" and e.dtype == "int64" and e.args[0].op == "col" \
+            and e.args[0].dtype in NARROW_INTS:
+        return e.args[0].col, 0
+    if e.op == "decimal" and e.args[0].op == "cast" and e.args[0].args[0].op == "col" \
+            and e.args[0].args[0].dtype in NARROW_INTS:
+        return e.args[0].args[0].col, int(e.value)
+    return None
+
+
+def decimal_predicates(op: str, lit: float, divisor: int) -> list[tuple[str, int, int]]:
+    """``value <op> lit`` on a column stored as integers c with value =
+    RN(c / divisor) (compact.py verifies it for every stored row), as
+    conjunctions of int64 comparisons on c: [(op, compare kind, int literal)].
+
+    RN(c / d) is non-decreasing in c, so {c : RN(c/d) >= lit} = {c >= t} with
+    t found by bisection in exact arithmetic (Python int / int is correctly
+    rounded).  A NaN literal matches nothing except under <>."""
+    if lit != lit:
+        return [(op, nat.CMP_ALL if op == "<>" else nat.CMP_NONE, 0)]
+    lo_b, hi_b = -(2**62), 2**62
+
+    def first(pred) -> int:  # smallest c in [lo_b, hi_b] with pred(c), else hi_b + 1
+        lo, hi = lo_b, hi_b + 1
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if pred(mid):
+                hi = mid
+            else:
+                lo = mid + 1
+        return lo
+
+    t_ge = first(lambda c: c / divisor >= lit)
+    t_gt = first(lambda c: c / divisor > lit)
+    if op == ">=":
+        return [(">=", nat.CMP_I64, t_ge)]
+    if op == ">":
+        return [(">=", nat.CMP_I64, t_gt)]
+    if op == "<":
+        return [("<", nat.CMP_I64, t_ge)]
+    if op == "<=":
+        return [("<", nat.CMP_I64, t_gt)]
+    if op == "=":
+        if t_gt == t_ge:
+            return [("=", nat.CMP_NONE, 0)]
+        if t_gt == t_ge + 1:
+            return [("=", nat.CMP_I64, t_ge)]
+        return [(">=", nat.CMP_I64, t_ge), ("<", nat.CMP_I64, t_gt)]
+    # "<>"
+    if t_gt == t_ge:
+        return [("<>", nat.CMP_ALL, 0)]
+    if t_gt == t_ge + 1:
+        return [("<>", nat.CMP_I64, t_ge)]
+    return [("<>", nat.CMP_DEC, divisor)]  # several stored values decode to lit
+
+
 class LazyValue:
     """An unmaterialised column: ``expr`` evaluated on the rows of ``sel``."""
 
@@ -315,7 +377,8 @@ class Program:
                 raise ValueError("expression columns must be 1-d")
             c = self.col_index(e.col)
             load_dt = {"int64": "int64", "bool": "int64", "float64": "float64",
-                       "float32": "float32"}[e.dtype]
+                       "float32": "float32", "int32": "int64", "int16": "int64",
+                       "int8": "int64", "uint8": "int64"}[e.dtype]
             v = self._emit(("load", c), nat.Instr(nat.OP_LOAD, _DT[load_dt], c, 0, 0, 0.0))
             return v
         if e.op == "const":
@@ -326,6 +389,11 @@ class Program:
             fv = float(e.value)
             bits = struct.pack("<d", fv)
             return self._emit(("cf", dt, bits), nat.Instr(nat.OP_CONST, _DT[dt], 0, 0, 0, fv))
+        if e.op == "decimal":  # compact float64 column: stored integer / divisor
+            a = self.value(e.args[0])
+            d = float(e.value)
+            inv_bits = struct.unpack("<q", struct.pack("<d", 1.0 / d))[0]
+            return self._emit(("dec", a, d), nat.Instr(nat.OP_DECIMAL, nat.F64, a, 0, inv_bits, d))
         if e.op == "cast":
             a = self.value(e.args[0])
             src = self.instrs[a].dtype

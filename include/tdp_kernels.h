@@ -115,6 +115,12 @@ int tdp_device_sm_count(void);
 /* Total kernels launched by this library in this process (benchmark
  * accounting of "our" launches). */
 uint64_t tdp_launch_count(void);
+/* Account `n` kernels of this library replayed inside a CUDA graph (a graph
+ * captured from library launches relaunches them without calling in). */
+void tdp_count_graph_launches(uint64_t n);
+/* Read and clear the CUDA runtime error state of this library (after an
+ * aborted graph capture); returns the cudaError_t that was pending.        */
+int tdp_clear_error(void);
 /* Benchmark timer of the fused pipeline kernel: while enabled, CUDA events are
  * recorded on the launch stream immediately around every tdp_scan_agg launch
  * (after all host-side preparation).  read() waits for the recorded events,

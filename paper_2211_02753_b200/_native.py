@@ -79,6 +79,8 @@ _SIGNATURES = {
     "tdp_version": (c_char_p, []),
     "tdp_device_sm_count": (c_int, []),
     "tdp_launch_count": (c_uint64, []),
+    "tdp_count_graph_launches": (None, [c_uint64]),
+    "tdp_clear_error": (c_int, []),
     "tdp_kernel_timer_enable": (c_int, [c_int32]),
     "tdp_kernel_timer_read": (c_int, [POINTER(c_double), POINTER(c_int64)]),
     "tdp_filter_mask": (c_int, [POINTER(Column), c_int32, POINTER(Predicate), c_int32, c_int64,

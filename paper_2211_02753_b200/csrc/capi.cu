@@ -94,4 +94,10 @@ int tdp_device_sm_count(void) { return tdp::sm_count(); }
 
 uint64_t tdp_launch_count(void) { return tdp::g_launches.load(std::memory_order_relaxed); }
 
+int tdp_clear_error(void) { return (int)cudaGetLastError(); }
+
+void tdp_count_graph_launches(uint64_t n) {
+  tdp::g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+
 }  // extern "C"

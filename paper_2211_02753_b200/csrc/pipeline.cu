@@ -43,6 +43,7 @@ constexpr i64 kMaxSlots = 1 << 20;
 constexpr int kConsWarps = 8;               // consumer warps of the ring kernel
 constexpr i64 kStageBudget = 64 * 1024;     // max bytes of one ring stage
 constexpr i64 kRingBudget = 200 * 1024;     // bytes of shared memory for the ring
+constexpr i64 kTwoCtaBudget = 110 * 1024;   // ring + accumulators per CTA at 2 CTAs/SM
 constexpr i64 kMaxSmemCells = 48;           // shared-memory accumulator mode limit
 constexpr int kAccThreads = 256;            // accumulator columns (TDP_ACC_THREADS)
 
@@ -366,6 +367,11 @@ Ring ring_shape(const Spec& s) {
   r.ptile = kConsWarps * 32 * r.pu;
   r.stage_bytes = (i64)r.ptile * row_bytes;
   i64 st = (kRingBudget - s.acc_smem) / r.stage_bytes;
+  // Narrow rows (compact storage) make the per-row arithmetic, not the bytes,
+  // the limit: then prefer two CTAs per SM (twice the consumer warps to hide
+  // FP64 / shared-memory latency) over a deeper ring, when two fit.
+  const i64 half = kTwoCtaBudget - s.acc_smem;
+  if (row_bytes <= 24 && half >= 2 * r.stage_bytes) st = half / r.stage_bytes;
   r.stages = (int)(st < 2 ? 2 : (st > 8 ? 8 : st));
   return r;
 }

@@ -491,16 +491,40 @@ def _ring() -> _PinnedRing:
     return _RING
 
 
+_CAPTURE = threading.local()
+
+
+class capturing:
+    """Context of a CUDA-graph capture of a query (compiler.py): device
+    counts stay on the device (no host copy or event inside the graph)."""
+
+    def __enter__(self):
+        _CAPTURE.on = True
+        return self
+
+    def __exit__(self, *exc):
+        _CAPTURE.on = False
+
+
+def is_capturing() -> bool:
+    return getattr(_CAPTURE, "on", False)
+
+
 class DeferredCount:
     """A row count produced by a kernel.  It is copied to a pinned host slot
     asynchronously right after the producing launch; the host waits for it
     only on first access (``value()``), so a query whose result stays on the
     device never blocks the launching thread."""
 
-    __slots__ = ("_slot", "_event", "_value", "__weakref__")
+    __slots__ = ("_slot", "_event", "_value", "dev", "__weakref__")
 
     def __init__(self, dev: torch.Tensor):
         self._value: Optional[int] = None
+        self.dev = dev
+        if is_capturing():  # a graph template: the replay makes a real one
+            self._slot = None
+            self._event = None
+            return
         ring = _ring()
         self._slot = ring.take(weakref.ref(self))
         ring.buf[self._slot:self._slot + 1].copy_(dev.reshape(1), non_blocking=True)
@@ -509,9 +533,12 @@ class DeferredCount:
 
     def value(self) -> int:
         if self._value is None:
+            if self._slot is None:
+                raise RuntimeError("row count of a CUDA-graph template read during capture")
             self._event.synchronize()
             self._value = int(_ring().buf[self._slot])
             self._event = None
+            self.dev = None
         return self._value
 
 

@@ -1,0 +1,223 @@
+"""CUDA-graph replay of exact query plans over an unchanged catalog.
+
+The reference re-interprets its operator program on every ``run``
+(tq/compiler.py:366-367).  Here that interpretation is Python planning around
+a handful of kernel launches (~0.3 ms for Q1), comparable to the launches
+themselves once columns are narrow or shards small.  An exact query is a pure
+function of the catalog state (SPEC plan-compiler: "run twice -> identical
+results"), so ``CompiledQuery.run`` captures the plan's launches into a CUDA
+graph the second time it sees the same state and replays it afterwards:
+
+* state = the scanned tables (object identity, every stored column buffer and
+  its in-place version counter), the UDF registry, the versions of the
+  referenced parameters, the device; anything else (a process group of more
+  than one rank, an open tape, an unknown lazy column) disables replay;
+* every kernel still runs over every row on each replay -- only the host-side
+  planning is skipped -- and the launches are accounted to the library's
+  launch counter;
+* the result is a fresh table: the result buffers written by the graph are
+  copied out of its memory pool, device row counts get fresh host slots.
+
+A plan that cannot be captured (a host synchronisation inside, e.g. a join
+sizing its output) runs eagerly from then on.  ``TDP_REPLAY=0`` or
+``CompileConfig(replay=False)`` turn replay off.
+"""
+
+from __future__ import annotations
+
+import os
+from collections import OrderedDict
+from typing import Optional
+
+import torch
+
+from . import _native as nat
+from .distributed import current_group, world_size
+from .encodings import EncodedTensor, trusted
+from .lazy import DeferredCount, LazyValue, PrefixRows, capturing, compact_source
+from .storage import table_from_columns
+from .tensor import Tensor
+
+MAX_ENTRIES = 4
+MAX_RESULT_BYTES = 64 << 20  # larger results: the copy-out would dominate
+
+_WARM = "warm"
+_NOGRAPH = "nograph"
+
+
+def enabled() -> bool:
+    return os.environ.get("TDP_REPLAY", "1") != "0"
+
+
+def _stored(t: Tensor) -> Optional[torch.Tensor]:
+    """The buffer a catalog column's values live in, if plainly known."""
+    if t._t is not None:
+        return t._t
+    lz = t._lazy
+    if isinstance(lz, LazyValue) and lz.sel is None:
+        if lz.expr.op == "col":
+            return lz.expr.col
+        src = compact_source(lz.expr)
+        if src is not None:
+            return src[0]
+    return None
+
+
+def signature(q, catalog) -> Optional[tuple]:
+    group = current_group()
+    if group is not None and world_size(group) > 1:
+        return None
+    if not torch.cuda.is_available() or torch.cuda.is_current_stream_capturing():
+        return None
+    sig = [id(catalog), id(q.registry), len(q.registry.names()), torch.cuda.current_device()]
+    tables = getattr(catalog, "_tables", None)
+    if tables is None:
+        return None
+    for name in q._scan_tables:
+        t = tables.get(name)
+        if t is None:
+            return None
+        sig.append(id(t))
+        for c in t.columns:
+            st = _stored(c.values)
+            if st is None or not st.is_cuda:
+                return None
+            sig.append(st.data_ptr())
+            sig.append(st._version)
+    for p in q._params:
+        d = p.value.data
+        sig.append(d.data_ptr())
+        sig.append(d._version)
+    return tuple(sig)
+
+
+class _Template:
+    """Result table of a captured run and how to re-materialise it."""
+
+    def __init__(self, names, cols, storages, device):
+        self.names = names
+        self.cols = cols          # (kind, tensors..., encoding)
+        self.storages = storages  # data_ptr -> uint8 view of a pool storage
+        self.device = device
+
+    @staticmethod
+    def build(table, inputs: set) -> Optional["_Template"]:
+        cols, storages, total = [], {}, 0
+
+        def track(t: torch.Tensor) -> bool:
+            nonlocal total
+            st = t.untyped_storage()
+            key = st.data_ptr()
+            if key in inputs or key in storages:
+                return True
+            total += st.nbytes()
+            storages[key] = torch.empty(0, dtype=torch.uint8, device=t.device).set_(
+                st, 0, (st.nbytes(),), (1,))
+            return total <= MAX_RESULT_BYTES
+
+        for c in table.columns:
+            v = c.values
+            if v._t is not None:
+                if not track(v._t):
+                    return None
+                cols.append(("t", v._t, None, c.encoding))
+            elif isinstance(v._lazy, PrefixRows) and isinstance(v._lazy.count, DeferredCount) \
+                    and v._lazy.count.dev is not None:
+                full, dev = v._lazy.full, v._lazy.count.dev
+                if not (track(full) and track(dev)):
+                    return None
+                cols.append(("prefix", full, dev, c.encoding))
+            else:
+                return None
+        return _Template(list(table.schema.names), cols, storages, table.device)
+
+    def materialise(self):
+        fresh = {k: src.clone() for k, src in self.storages.items()}
+
+        def remap(t: torch.Tensor) -> torch.Tensor:
+            new = fresh.get(t.untyped_storage().data_ptr())
+            if new is None:  # a catalog buffer passed through
+                return t
+            return torch.empty(0, dtype=t.dtype, device=t.device).set_(
+                new.untyped_storage(), t.storage_offset(), t.size(), t.stride())
+
+        cols = []
+        counts: dict = {}
+        with trusted():
+            for kind, a, b, enc in self.cols:
+                if kind == "t":
+                    cols.append(EncodedTensor(Tensor(remap(a)), enc))
+                else:
+                    key = (b.untyped_storage().data_ptr(), b.storage_offset())
+                    if key not in counts:  # one host slot per device count
+                        counts[key] = DeferredCount(remap(b))
+                    cols.append(EncodedTensor(Tensor(PrefixRows(remap(a), counts[key])), enc))
+        return table_from_columns(self.names, cols, device=self.device)
+
+
+class _Replay:
+    def __init__(self, graph, template: _Template, launches: int, hold):
+        self.graph = graph
+        self.template = template
+        self.launches = launches
+        self.hold = hold  # the catalog tables the signature names (ids stay unique)
+
+    def __call__(self):
+        self.graph.replay()
+        if self.launches:
+            nat.load().tdp_count_graph_launches(self.launches)
+        return self.template.materialise()
+
+
+def _inputs(q, catalog) -> tuple[set, list]:
+    ptrs, hold = set(), []
+    for name in q._scan_tables:
+        t = catalog._tables.get(name)
+        hold.append(t)
+        for c in t.columns:
+            st = _stored(c.values)
+            if st is not None:
+                ptrs.add(st.untyped_storage().data_ptr())
+    return ptrs, hold
+
+
+def _capture(q, catalog):
+    inputs, hold = _inputs(q, catalog)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    launches0 = nat.launch_count()
+    try:
+        with capturing():
+            with torch.cuda.graph(graph):
+                table = q._execute(catalog)
+    except Exception:
+        # a host synchronisation (or other uncapturable call) inside the plan
+        nat.load().tdp_clear_error()
+        torch.cuda.synchronize()
+        return _NOGRAPH
+    launches = nat.launch_count() - launches0
+    template = _Template.build(table, inputs)
+    if template is None:
+        return _NOGRAPH
+    return _Replay(graph, template, launches, hold)
+
+
+def run(q, catalog, sig):
+    """Replay for ``sig`` if captured (capturing it on the second sighting);
+    None: run the program eagerly."""
+    entries: OrderedDict = q._replays
+    ent = entries.get(sig)
+    if ent is None:
+        entries[sig] = _WARM
+        while len(entries) > MAX_ENTRIES:
+            entries.popitem(last=False)
+        return None
+    if ent == _NOGRAPH:
+        return None
+    if ent == _WARM:
+        ent = _capture(q, catalog)
+        entries[sig] = ent
+        if ent == _NOGRAPH:
+            return None
+    entries.move_to_end(sig)
+    return ent()

@@ -1,0 +1,114 @@
+"""GPU: CUDA-graph replay of exact plans (replay.py).
+
+Replayed runs must return fresh, correct tables (earlier results untouched),
+run every kernel (launch accounting), and fall back to eager execution when
+the catalog changes (new table, in-place write to a column, new parameter
+values) or the plan cannot be captured.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle.tpch as otpch
+import paper_2211_02753_b200 as tq
+from paper_2211_02753_b200 import _native, replay
+from paper_2211_02753_b200 import compact as cp
+from paper_2211_02753_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+def _cols(res):
+    return {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
+
+
+def _check_q1(cols, exp):
+    for n, v in exp.items():
+        if v.dtype.kind in "iu":
+            np.testing.assert_array_equal(cols[n], v)
+        else:
+            np.testing.assert_allclose(cols[n], v, rtol=1e-9)
+
+
+@pytest.mark.parametrize("compact", [False, True])
+def test_q1_replay_fresh_results_and_launches(compact):
+    arrays = wl.lineitem_arrays(0.01, seed=5, rows=100_003)
+    table = wl.lineitem_table(arrays)
+    if compact:
+        table = cp.compact_table(table)
+    cat = tq.Catalog()
+    cat.register("lineitem", table)
+    q = wl.compile_sql(wl.Q1_SQL, cat, wl.q1_registry())
+    exp = otpch.q1(arrays)
+    r1 = q.run(cat)                    # eager, marks the state
+    r2 = q.run(cat)                    # captured + replayed
+    assert any(isinstance(e, replay._Replay) for e in q._replays.values())
+    n0 = _native.launch_count()
+    r3 = q.run(cat)                    # replayed
+    assert _native.launch_count() > n0  # the graph's kernels are accounted
+    for r in (r3, r2, r1):
+        _check_q1(_cols(r), exp)
+    # results are distinct buffers: a later replay does not rewrite them
+    assert r2.columns[2].values.data.data_ptr() != r3.columns[2].values.data.data_ptr()
+
+
+def test_q6_replay_and_invalidation():
+    cols = ("l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
+    arrays = wl.lineitem_arrays(0.01, seed=3, rows=50_000)
+    table = wl.lineitem_table(arrays, cols)
+    cat = tq.Catalog()
+    cat.register("lineitem", table)
+    q = wl.compile_sql(wl.Q6_SQL, cat, wl.q6_registry())
+    exp = otpch.q6(arrays)["sum_rev"]
+    for _ in range(3):
+        got = q.run(cat).columns[0].values.numpy()
+        np.testing.assert_allclose(got, exp, rtol=1e-9, atol=1e-9)
+    # in-place write to a catalog column: new state, new result
+    price = table.columns[2].values.data
+    price.mul_(2.0)
+    got = q.run(cat).columns[0].values.numpy()
+    np.testing.assert_allclose(got, 2 * exp, rtol=1e-9, atol=1e-9)
+    got = q.run(cat).columns[0].values.numpy()
+    np.testing.assert_allclose(got, 2 * exp, rtol=1e-9, atol=1e-9)
+    # a different table under the same name
+    arrays2 = wl.lineitem_arrays(0.01, seed=4, rows=40_000)
+    cat.register("lineitem", wl.lineitem_table(arrays2, cols))
+    for _ in range(3):
+        got = q.run(cat).columns[0].values.numpy()
+        np.testing.assert_allclose(got, otpch.q6(arrays2)["sum_rev"], rtol=1e-9, atol=1e-9)
+
+
+def test_uncapturable_plan_falls_back():
+    rng = np.random.default_rng(11)
+    n = 20_000
+    k = rng.integers(-10**12, 10**12, size=n)
+    v = rng.random(n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["k", "v"], [tq.plain(tq.Tensor(k)),
+                                                          tq.plain(tq.Tensor(v))]))
+    q = tq.compile_plan(tq.lower(tq.bind(tq.parse("SELECT k, SUM(v) FROM t GROUP BY k"), cat,
+                                         tq.UdfRegistry())), tq.CompileConfig(), tq.UdfRegistry())
+    outs = [q.run(cat) for _ in range(3)]
+    assert replay._NOGRAPH in q._replays.values()
+    keys, inv = np.unique(k, return_inverse=True)
+    sums = np.zeros(len(keys))
+    np.add.at(sums, inv, v)
+    for r in outs:
+        np.testing.assert_array_equal(r.columns[0].values.numpy(), keys)
+        np.testing.assert_allclose(r.columns[1].values.numpy(), sums, rtol=1e-12)
+
+
+def test_replay_off_switch():
+    arrays = wl.lineitem_arrays(0.01, seed=5, rows=1000)
+    cat = tq.Catalog()
+    cat.register("lineitem", wl.lineitem_table(arrays))
+    sql = wl.Q1_SQL
+    reg = wl.q1_registry()
+    q = tq.compile_plan(tq.lower(tq.bind(tq.parse(sql), cat, reg)),
+                        tq.CompileConfig(replay=False), reg)
+    for _ in range(3):
+        q.run(cat)
+    assert not q._replays

@@ -311,6 +311,22 @@ int tdp_join_prepare_filtered(const int64_t* build_keys, int64_t n_build,
                               const tdp_column* cols, int32_t ncols, const tdp_predicate* preds,
                               int32_t npreds, int64_t* out_count, void* ws, size_t ws_bytes,
                               void* stream);
+/* Synchronisation-free two-phase prepare, both sides optionally filtered.
+ * mode 0 (optimistic): the (filtered) build rows are hashed in input order
+ *   as unique keys -- the primary-key side of a PK-FK join, no sort;
+ *   out_info[0] = result pairs, out_info[1] != 0 when a build key repeats, in
+ *   which case out_info[0] is invalid and the call must be repeated with
+ *   mode 1.  Build rows failing the build predicates do not take part; the
+ *   build indices tdp_join_emit writes are then base row ids.
+ * mode 1 (runs): stable sort of the build keys, one entry per run of equal
+ *   keys (build predicates not allowed: compact the build side first).
+ * Probe predicates as in tdp_join_prepare_filtered.  out_info: device int64[2]. */
+int tdp_join_prepare_ex(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                        int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds,
+                        const int64_t* probe_keys, int64_t n_probe, const tdp_column* pcols,
+                        int32_t npcols, const tdp_predicate* ppreds, int32_t nppreds,
+                        int32_t mode, int64_t* out_info, void* ws, size_t ws_bytes,
+                        void* stream);
 int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);

@@ -121,6 +121,10 @@ _SIGNATURES = {
     "tdp_join_prepare_filtered": (c_int, [c_void_p, c_int64, c_void_p, c_int64, POINTER(Column),
                                           c_int32, POINTER(Predicate), c_int32, c_void_p,
                                           c_void_p, c_size_t, c_void_p]),
+    "tdp_join_prepare_ex": (c_int, [c_void_p, c_int64, POINTER(Column), c_int32,
+                                    POINTER(Predicate), c_int32, c_void_p, c_int64,
+                                    POINTER(Column), c_int32, POINTER(Predicate), c_int32, c_int32,
+                                    c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_join_emit": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_size_t,
                               c_void_p]),
     "tdp_softmax_fwd": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p]),

@@ -540,10 +540,17 @@ __device__ bool ht_insert(const HashTable& ht, i64 key, i64 start, i64 cnt) {
   }
 }
 
-__global__ void join_build_unique_kernel(const i64* __restrict__ keys, i64 nb, HashTable ht) {
+// Build rows failing the optional build predicates are skipped (a filtered
+// build relation read straight from its base columns; run starts are then
+// base row ids).
+template <bool kFiltered>
+__global__ void join_build_unique_kernel(const i64* __restrict__ keys, i64 nb, HashTable ht,
+                                         PredSet bps) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
-       i += (i64)gridDim.x * blockDim.x)
+       i += (i64)gridDim.x * blockDim.x) {
+    if (kFiltered && !eval_all(bps, i)) continue;
     if (!ht_insert(ht, __ldg(keys + i), i, 1)) ht.flags[0] = 1;
+  }
 }
 
 __global__ void join_build_runs_kernel(const u64* __restrict__ sk, i64 nb, HashTable ht) {
@@ -874,29 +881,41 @@ int clear_table(const JoinWs& j, cudaStream_t st) {
   return TDP_OK;
 }
 
-int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
-                 int64_t n_probe, const PredSet* ps, int64_t* out_count, void* ws,
-                 size_t ws_bytes, cudaStream_t st) {
+// mode 0 (optimistic): hash the (filtered) build rows in input order as if
+// the keys were unique; out_info[1] = 1 reports a repeated key, in which case
+// the pair count in out_info[0] is not valid and mode 1 must follow.
+// mode 1 (runs): stable radix sort of the build keys, one table entry per run
+// (no build predicates).  Neither mode synchronises with the host.
+int join_prepare_mode(const int64_t* build_keys, int64_t n_build, const PredSet* bps,
+                      const int64_t* probe_keys, int64_t n_probe, const PredSet* ps, int mode,
+                      int64_t* out_info, void* ws, size_t ws_bytes, cudaStream_t st) {
   TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
-  TDP_REQUIRE(out_count != nullptr, "null join count output");
+  TDP_REQUIRE(out_info != nullptr, "null join info output");
+  TDP_REQUIRE(mode == 0 || mode == 1, "join mode must be 0 (optimistic) or 1 (runs)");
   TDP_REQUIRE(ws_bytes >= join_ws_bytes(n_build, n_probe), "join workspace too small");
+  const bool bfilt = bps != nullptr && bps->npreds > 0;
+  TDP_REQUIRE(!(bfilt && mode == 1), "build predicates need unique build keys (mode 0)");
   JoinWs j = carve_join(ws, n_build, n_probe);
   const i64 tiles = ceil_div(n_probe, kJoinTile);
-  if (n_build == 0 || n_probe == 0) {
-    TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, 8, st));
-    return TDP_OK;
-  }
+  TDP_CUDA_TRY(cudaMemsetAsync(out_info, 0, 2 * sizeof(i64), st));
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
   int rc = clear_table(j, st);
   if (rc) return rc;
-  join_build_unique_kernel<<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
-                                                                              j.ht);
-  TDP_LAUNCH_CHECK("join_build_unique_kernel");
-  int repeated = 0;
-  TDP_CUDA_TRY(cudaMemcpyAsync(&repeated, j.ht.flags, sizeof(int), cudaMemcpyDeviceToHost, st));
-  TDP_CUDA_TRY(cudaStreamSynchronize(st));
-  if (repeated) {  // runs of equal keys: stable sort, one table entry per run
-    rc = clear_table(j, st);
-    if (rc) return rc;
+  PredSet none;
+  none.npreds = 0;
+  none.pad = 0;
+  if (mode == 0) {
+    if (bfilt)
+      join_build_unique_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(
+          build_keys, n_build, j.ht, *bps);
+    else
+      join_build_unique_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(
+          build_keys, n_build, j.ht, none);
+    TDP_LAUNCH_CHECK("join_build_unique_kernel");
+    // report a repeated key (int flag into the low half of out_info[1])
+    TDP_CUDA_TRY(cudaMemcpyAsync(out_info + 1, j.ht.flags, sizeof(int), cudaMemcpyDeviceToDevice,
+                                 st));
+  } else {
     const int one[2] = {1, 1};
     TDP_CUDA_TRY(cudaMemcpyAsync(j.ht.flags, one, sizeof(one), cudaMemcpyHostToDevice, st));
     make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(
@@ -915,18 +934,38 @@ int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* prob
     TDP_LAUNCH_CHECK("join_build_runs_kernel");
   }
   TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
-  PredSet none;
-  none.npreds = 0;
-  none.pad = 0;
   const bool filtered = ps != nullptr && ps->npreds > 0;
   const PredSet& pp = filtered ? *ps : none;
-  auto kernel = filtered ? (repeated ? join_count_kernel<true, false> : join_count_kernel<true, true>)
-                         : (repeated ? join_count_kernel<false, false> : join_count_kernel<false, true>);
+  const bool runs = mode == 1;
+  auto kernel = filtered ? (runs ? join_count_kernel<true, false> : join_count_kernel<true, true>)
+                         : (runs ? join_count_kernel<false, false> : join_count_kernel<false, true>);
   kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, pp, j.match_bits,
                                                    j.word_counts, j.tile_counts);
   TDP_LAUNCH_CHECK("join_count_kernel");
-  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
+  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_info, j.scan_ws,
                             j.scan_bytes, st);
+}
+
+// Legacy single-call form: optimistic pass, one host check, runs if needed.
+int join_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                 int64_t n_probe, const PredSet* ps, int64_t* out_count, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  TDP_REQUIRE(out_count != nullptr, "null join count output");
+  i64* info = nullptr;
+  TDP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&info), 2 * sizeof(i64), st));
+  int rc = join_prepare_mode(build_keys, n_build, nullptr, probe_keys, n_probe, ps, 0, info, ws,
+                             ws_bytes, st);
+  i64 host[2] = {0, 0};
+  if (!rc) {
+    TDP_CUDA_TRY(cudaMemcpyAsync(host, info, sizeof(host), cudaMemcpyDeviceToHost, st));
+    TDP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (host[1] & 0xffffffff)
+      rc = join_prepare_mode(build_keys, n_build, nullptr, probe_keys, n_probe, ps, 1, info, ws,
+                             ws_bytes, st);
+  }
+  if (!rc) TDP_CUDA_TRY(cudaMemcpyAsync(out_count, info, sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  cudaFreeAsync(info, st);
+  return rc;
 }
 
 }  // namespace
@@ -952,6 +991,21 @@ int tdp_join_prepare_filtered(const int64_t* build_keys, int64_t n_build,
   if (rc) return rc;
   return join_prepare(build_keys, n_build, probe_keys, n_probe, &ps, out_count, ws, ws_bytes,
                       as_stream(stream));
+}
+
+int tdp_join_prepare_ex(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                        int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds,
+                        const int64_t* probe_keys, int64_t n_probe, const tdp_column* pcols,
+                        int32_t npcols, const tdp_predicate* ppreds, int32_t nppreds,
+                        int32_t mode, int64_t* out_info, void* ws, size_t ws_bytes,
+                        void* stream) {
+  PredSet bps, pps;
+  int rc = make_predset(bcols, nbcols, bpreds, nbpreds, n_build, &bps);
+  if (rc) return rc;
+  rc = make_predset(pcols, npcols, ppreds, nppreds, n_probe, &pps);
+  if (rc) return rc;
+  return join_prepare_mode(build_keys, n_build, &bps, probe_keys, n_probe, &pps, mode, out_info,
+                           ws, ws_bytes, as_stream(stream));
 }
 
 int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,

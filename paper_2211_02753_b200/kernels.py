@@ -924,36 +924,48 @@ def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTens
 # ---------------------------------------------------------------------------
 
 
-def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None
-                 ) -> tuple[torch.Tensor, torch.Tensor]:
+def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
+                 build_sel: Optional[Selection] = None
+                 ) -> Optional[tuple[torch.Tensor, torch.Tensor]]:
     """Inner equi-join row pairs: (probe rows, build rows), ordered by probe row
-    then ascending build row (stable radix sort of the build keys + one hash
-    probe per probe row).
+    then ascending build row (hash build, one probe per probe row).
 
-    With ``probe_sel`` the probe side is a filtered base relation:
-    ``probe_key`` is the *base* key column, the selection's predicates are
-    evaluated in the probe pass itself, and the returned probe rows are base
-    row ids (the filtered relation is never materialised)."""
+    With ``probe_sel`` / ``build_sel`` a side is a filtered base relation: its
+    key column is the *base* key column, the selection's predicates are
+    evaluated inside the join's own passes, and the returned row ids of that
+    side are base row ids (the filtered relation is never materialised).  One
+    host synchronisation (the pair count) unless the build keys repeat; a
+    filtered build with repeated keys returns None (the caller compacts the
+    build side first)."""
     pk = _materialize(probe_key).contiguous().to(torch.int64)
     bk = _materialize(build_key).contiguous().to(torch.int64)
     nat.require_cuda(pk, bk)
     dev = pk.device
     n_probe, n_build = int(pk.numel()), int(bk.numel())
     ws = nat.workspace(nat.load().tdp_join_workspace(n_build, n_probe), dev)
-    count = torch.zeros(1, dtype=torch.int64, device=dev)
-    if probe_sel is not None and probe_sel.preds:
-        if probe_sel.n != n_probe:
-            raise KernelError("probe selection and key column disagree on row count")
+    info = torch.empty(2, dtype=torch.int64, device=dev)
+
+    def predset(sel, n, what):
+        if sel is None or not sel.preds:
+            return nat.columns([]), 0, nat.struct_array(nat.Predicate, []), 0
+        if sel.n != n:
+            raise KernelError(f"{what} selection and key column disagree on row count")
         prog = Program()
-        preds, npreds = prog.predicates(probe_sel)
+        preds, npreds = prog.predicates(sel)
         nat.require_cuda(*prog.cols)
-        nat.call("tdp_join_prepare_filtered", nat.ptr(bk), n_build, nat.ptr(pk), n_probe,
-                 prog.native_columns(), len(prog.cols), preds, npreds, nat.ptr(count),
-                 nat.ptr(ws), ws.numel(), nat.stream())
-    else:
-        nat.call("tdp_join_prepare", nat.ptr(bk), n_build, nat.ptr(pk), n_probe, nat.ptr(count),
-                 nat.ptr(ws), ws.numel(), nat.stream())
-    m = int(count.item())
+        return prog.native_columns(), len(prog.cols), preds, npreds
+
+    bc, nbc, bp, nbp = predset(build_sel, n_build, "build")
+    pc, npc, pp, npp = predset(probe_sel, n_probe, "probe")
+    nat.call("tdp_join_prepare_ex", nat.ptr(bk), n_build, bc, nbc, bp, nbp, nat.ptr(pk), n_probe,
+             pc, npc, pp, npp, 0, nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
+    m, repeated = info.tolist()
+    if repeated:
+        if nbp:
+            return None
+        nat.call("tdp_join_prepare_ex", nat.ptr(bk), n_build, bc, 0, bp, 0, nat.ptr(pk), n_probe,
+                 pc, npc, pp, npp, 1, nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
+        m = int(info[0].item())
     pi = torch.empty(m, dtype=torch.int64, device=dev)
     bi = torch.empty(m, dtype=torch.int64, device=dev)
     if m:
@@ -1010,16 +1022,24 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
         return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
     lb, lsel = _side_sources(left)
     rb, rsel = _side_sources(right)
-    rmap = rsel.indices() if rsel is not None else None
-    rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
-    if lsel is not None and lb[left_key].dim() == 1:
-        # probe the filtered base relation directly: probe rows are base rows
-        pi, bi = join_indices(lb[left_key], rkey, probe_sel=lsel)
-        lmap = None
-    else:
+    # a filtered side whose key is a base column joins straight from the base
+    # columns (its predicates run inside the join passes, row ids are base
+    # ids); otherwise the side is compacted first
+    lmap = rmap = None
+    lkey_direct = lsel is not None and lb[left_key].dim() == 1
+    rkey_direct = rsel is not None and rb[right_key].dim() == 1
+    if not lkey_direct:
         lmap = lsel.indices() if lsel is not None else None
-        lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
-        pi, bi = join_indices(lkey, rkey)
+    lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
+    pairs = None
+    if rkey_direct:
+        pairs = join_indices(lkey, rb[right_key], probe_sel=lsel if lkey_direct else None,
+                             build_sel=rsel)
+    if pairs is None:  # unfiltered build side, or a filtered one with repeated keys
+        rmap = rsel.indices() if rsel is not None else None
+        rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
+        pairs = join_indices(lkey, rkey, probe_sel=lsel if lkey_direct else None)
+    pi, bi = pairs
     return _gather_side(left, lb, lmap, pi) + _gather_side(right, rb, rmap, bi)
 
 

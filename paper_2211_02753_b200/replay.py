@@ -26,6 +26,8 @@ sizing its output) runs eagerly from then on.  ``TDP_REPLAY=0`` or
 from __future__ import annotations
 
 import os
+import warnings
+import weakref
 from collections import OrderedDict
 from typing import Optional
 
@@ -41,7 +43,6 @@ from .tensor import Tensor
 MAX_ENTRIES = 4
 MAX_RESULT_BYTES = 64 << 20  # larger results: the copy-out would dominate
 
-_WARM = "warm"
 _NOGRAPH = "nograph"
 
 
@@ -187,7 +188,8 @@ def _capture(q, catalog):
     graph = torch.cuda.CUDAGraph()
     launches0 = nat.launch_count()
     try:
-        with capturing():
+        with capturing(), warnings.catch_warnings():
+            warnings.simplefilter("ignore")  # "graph is empty": a lazy result, no launches
             with torch.cuda.graph(graph):
                 table = q._execute(catalog)
     except Exception:
@@ -202,19 +204,34 @@ def _capture(q, catalog):
     return _Replay(graph, template, launches, hold)
 
 
+class _Warm:
+    """First sighting of a state: weak references to its tables, so a second
+    sighting is recognised only while those very objects are alive (a new
+    table that happens to reuse a dead one's id and buffers is a new state,
+    and a stream of fresh tables never triggers captures)."""
+
+    def __init__(self, tables):
+        self.refs = [weakref.ref(t) for t in tables]
+
+    def alive(self, tables) -> bool:
+        return all(r() is t for r, t in zip(self.refs, tables))
+
+
 def run(q, catalog, sig):
     """Replay for ``sig`` if captured (capturing it on the second sighting);
     None: run the program eagerly."""
     entries: OrderedDict = q._replays
+    tables = [catalog._tables.get(name) for name in q._scan_tables]
     ent = entries.get(sig)
-    if ent is None:
-        entries[sig] = _WARM
+    if ent is None or (isinstance(ent, _Warm) and not ent.alive(tables)):
+        entries[sig] = _Warm(tables)
+        entries.move_to_end(sig)
         while len(entries) > MAX_ENTRIES:
             entries.popitem(last=False)
         return None
     if ent == _NOGRAPH:
         return None
-    if ent == _WARM:
+    if isinstance(ent, _Warm):
         ent = _capture(q, catalog)
         entries[sig] = ent
         if ent == _NOGRAPH:

@@ -231,3 +231,37 @@ def test_join_extreme_keys_unique_and_runs(unique):
     epi, ebi = orc.join_inner(probe, build)
     np.testing.assert_array_equal(pi.cpu().numpy(), epi)
     np.testing.assert_array_equal(bi.cpu().numpy(), ebi)
+
+
+@pytest.mark.parametrize("unique_build", [True, False])
+@pytest.mark.parametrize("filter_probe", [True, False])
+def test_filtered_build_join_matches_oracle(unique_build, filter_probe):
+    """equi_join whose build side is a lazy filtered relation: its predicates
+    run inside the hash build (build ids are base ids); with repeated build
+    keys the build side is compacted first (runs path)."""
+    from paper_2211_02753_b200.kernels import equi_join, filter_exact
+
+    rng = np.random.default_rng(31 + unique_build + 2 * filter_probe)
+    nb, n_probe = 30_000, 120_000
+    bk = rng.permutation(200_000)[:nb].astype(np.int64) * 3 if unique_build else \
+        rng.integers(0, 40_000, size=nb)
+    bseg = rng.integers(0, 5, size=nb)
+    bv = rng.random(nb)
+    pk = rng.integers(0, 600_000 if unique_build else 40_000, size=n_probe)
+    pv = rng.integers(0, 100, size=n_probe)
+    build = [tq.plain(tq.Tensor(bk)), tq.plain(tq.Tensor(bseg)), tq.plain(tq.Tensor(bv))]
+    probe = [tq.plain(tq.Tensor(pk)), tq.plain(tq.Tensor(pv))]
+    fb = filter_exact(build, [(1, "=", 2)])
+    fp = filter_exact(probe, [(1, "<", 60)]) if filter_probe else probe
+    out = equi_join(fp, fb, 0, 0)
+    bkeep = bseg == 2
+    pkeep = pv < 60 if filter_probe else np.ones(n_probe, dtype=bool)
+    fpk, fpv = pk[pkeep], pv[pkeep]
+    fbk, fbs, fbv = bk[bkeep], bseg[bkeep], bv[bkeep]
+    epi, ebi = orc.join_inner(fpk, fbk)
+    assert len(epi) > 0
+    np.testing.assert_array_equal(out[0].values.numpy(), fpk[epi])
+    np.testing.assert_array_equal(out[1].values.numpy(), fpv[epi])
+    np.testing.assert_array_equal(out[2].values.numpy(), fbk[ebi])
+    np.testing.assert_array_equal(out[3].values.numpy(), fbs[ebi])
+    np.testing.assert_array_equal(out[4].values.numpy(), fbv[ebi])

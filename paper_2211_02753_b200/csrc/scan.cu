@@ -1,7 +1,10 @@
 // Device-wide exclusive prefix sum over int64 counts (tile counts of the
 // filter compaction, radix-sort digit histograms, join match counts).
-// Reduce-then-scan: each CTA scans a chunk of kChunk values, the chunk totals
-// are scanned recursively, then chunk offsets are added back.
+// One launch: up to kChunk values are scanned by one CTA; beyond that every
+// CTA scans a chunk and finds its offset by decoupled look-back over its
+// predecessors' published aggregates / inclusive prefixes (one 64-bit status
+// word per chunk: 2 flag bits + a 62-bit value), so no second pass over the
+// data and no recursion.  Counts are non-negative and below 2^62.
 #include "tdp_common.cuh"
 
 namespace tdp {
@@ -43,7 +46,7 @@ __device__ __forceinline__ i64 block_exclusive_scan(i64 v, i64* total) {
 
 __global__ void __launch_bounds__(kScanThreads) chunk_scan_kernel(const i64* __restrict__ in,
                                                                   i64* __restrict__ out, i64 n,
-                                                                  i64* __restrict__ chunk_sums) {
+                                                                  i64* __restrict__ total) {
   __shared__ i64 s_total;
   const i64 base = (i64)blockIdx.x * kChunk + (i64)threadIdx.x * kScanItems;
   i64 v[kScanItems];
@@ -61,34 +64,83 @@ __global__ void __launch_bounds__(kScanThreads) chunk_scan_kernel(const i64* __r
     if (idx < n) out[idx] = pre;
     pre += v[k];
   }
-  if (threadIdx.x == 0 && chunk_sums != nullptr) chunk_sums[blockIdx.x] = s_total;
+  if (threadIdx.x == 0 && total != nullptr) *total = s_total;
 }
 
-__global__ void add_offsets_kernel(i64* __restrict__ out, i64 n, const i64* __restrict__ offs) {
-  const i64 chunk = blockIdx.x;
-  const i64 add = offs[chunk];
-  const i64 start = chunk * kChunk;
-  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
-    i64 idx = start + t;
-    if (idx < n) out[idx] += add;
+constexpr u64 kFlagAgg = 1ull << 62;   // value = this chunk's sum
+constexpr u64 kFlagPre = 2ull << 62;   // value = inclusive prefix through this chunk
+constexpr u64 kValMask = kFlagAgg - 1;
+
+__device__ __forceinline__ u64 load_status(const u64* p) {
+  return *reinterpret_cast<const volatile u64*>(p);
+}
+
+// status[nchunks] and the chunk ticket (status[nchunks]) must be zero.
+__global__ void __launch_bounds__(kScanThreads)
+    lookback_scan_kernel(const i64* __restrict__ in, i64* __restrict__ out, i64 n,
+                         u64* __restrict__ status, i64 nchunks, i64* __restrict__ total) {
+  __shared__ i64 s_total;
+  __shared__ i64 s_prefix;
+  __shared__ unsigned s_chunk;
+  if (threadIdx.x == 0)  // chunks in dispatch order: predecessors are running or done
+    s_chunk = atomicAdd(reinterpret_cast<unsigned*>(status + nchunks), 1u);
+  __syncthreads();
+  const i64 chunk = s_chunk;
+  const i64 base = chunk * kChunk + (i64)threadIdx.x * kScanItems;
+  i64 v[kScanItems];
+  i64 local = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const i64 idx = base + k;
+    v[k] = idx < n ? __ldg(in + idx) : 0;
+    local += v[k];
   }
-}
-
-// total = out[n-1] + in[n-1] (or 0 when n == 0)
-__global__ void write_total_kernel(const i64* in, const i64* out, i64 n, i64* total) {
-  *total = n > 0 ? out[n - 1] + in[n - 1] : 0;
+  i64 pre = block_exclusive_scan(local, &s_total);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const i64 agg = s_total;
+    i64 excl = 0;
+    if (chunk == 0) {
+      if (lane == 0) atomicExch(reinterpret_cast<unsigned long long*>(status), kFlagPre | (u64)agg);
+    } else {
+      if (lane == 0)
+        atomicExch(reinterpret_cast<unsigned long long*>(status + chunk), kFlagAgg | (u64)agg);
+      for (i64 p = chunk - 1;; p -= 32) {
+        const i64 idx = p - lane;  // lane 0 = nearest predecessor
+        u64 st = idx >= 0 ? load_status(status + idx) : kFlagPre;
+        while (__any_sync(0xffffffffu, (st >> 62) == 0))
+          if ((st >> 62) == 0) st = load_status(status + idx);
+        const unsigned prefixed = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int stop = prefixed ? __ffs(prefixed) - 1 : 31;
+        i64 c = lane <= stop ? (i64)(st & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        excl += c;
+        if (prefixed) break;
+      }
+      if (lane == 0)
+        atomicExch(reinterpret_cast<unsigned long long*>(status + chunk),
+                   kFlagPre | (u64)(excl + agg));
+    }
+    if (lane == 0) s_prefix = excl;
+  }
+  __syncthreads();
+  pre += s_prefix;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const i64 idx = base + k;
+    if (idx < n) out[idx] = pre;
+    pre += v[k];
+  }
+  if (total != nullptr && chunk == nchunks - 1 && threadIdx.x == 0) *total = s_prefix + s_total;
 }
 
 }  // namespace
 
 size_t exclusive_scan_workspace(i64 n) {
-  size_t bytes = 0;
-  i64 level = n;
-  while (level > kChunk) {
-    level = ceil_div(level, kChunk);
-    bytes += 2 * (size_t)level * sizeof(i64);
-  }
-  return bytes + 256;
+  // a multiple of 256 bytes: callers carve further buffers behind it
+  const size_t b = (size_t)(ceil_div(n > 0 ? n : 1, kChunk) + 1) * sizeof(u64) + 256;
+  return (b + 255) & ~(size_t)255;
 }
 
 int exclusive_scan_i64(const i64* in, i64* out, i64 n, i64* total, void* ws, size_t ws_bytes,
@@ -98,25 +150,17 @@ int exclusive_scan_i64(const i64* in, i64* out, i64 n, i64* total, void* ws, siz
     return TDP_OK;
   }
   if (n <= kChunk) {
-    chunk_scan_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, nullptr);
+    chunk_scan_kernel<<<1, kScanThreads, 0, stream>>>(in, out, n, total);
     TDP_LAUNCH_CHECK("chunk_scan_kernel");
-  } else {
-    const i64 nchunks = ceil_div(n, kChunk);
-    TDP_REQUIRE(ws_bytes >= exclusive_scan_workspace(n), "scan workspace too small");
-    i64* sums = reinterpret_cast<i64*>(ws);
-    i64* offs = sums + nchunks;
-    chunk_scan_kernel<<<(unsigned)nchunks, kScanThreads, 0, stream>>>(in, out, n, sums);
-    TDP_LAUNCH_CHECK("chunk_scan_kernel");
-    int rc = exclusive_scan_i64(sums, offs, nchunks, nullptr, offs + nchunks,
-                                ws_bytes - 2 * nchunks * sizeof(i64), stream);
-    if (rc != TDP_OK) return rc;
-    add_offsets_kernel<<<(unsigned)nchunks, 256, 0, stream>>>(out, n, offs);
-    TDP_LAUNCH_CHECK("add_offsets_kernel");
+    return TDP_OK;
   }
-  if (total) {
-    write_total_kernel<<<1, 1, 0, stream>>>(in, out, n, total);
-    TDP_LAUNCH_CHECK("write_total_kernel");
-  }
+  const i64 nchunks = ceil_div(n, kChunk);
+  TDP_REQUIRE(ws != nullptr && ws_bytes >= exclusive_scan_workspace(n), "scan workspace too small");
+  u64* status = reinterpret_cast<u64*>(ws);
+  TDP_CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)(nchunks + 1) * sizeof(u64), stream));
+  lookback_scan_kernel<<<(unsigned)nchunks, kScanThreads, 0, stream>>>(in, out, n, status, nchunks,
+                                                                      total);
+  TDP_LAUNCH_CHECK("lookback_scan_kernel");
   return TDP_OK;
 }
 

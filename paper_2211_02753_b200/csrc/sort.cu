@@ -194,8 +194,8 @@ i64 scan_extent(i64 n) {
 
 size_t sort_ws_bytes(i64 n) {
   const i64 ntiles = ceil_div(n > 0 ? n : 1, kSortTile);
-  return 4 * align256((size_t)n * 8) + 2 * align256((size_t)ntiles * 256 * 8) +
-         align256(8 * 256 * 8) + exclusive_scan_workspace(scan_extent(n)) + 1024;
+  return align256(4 * align256((size_t)n * 8) + 2 * align256((size_t)ntiles * 256 * 8) +
+                  align256(8 * 256 * 8) + exclusive_scan_workspace(scan_extent(n)) + 1024);
 }
 
 SortBuffers carve(void* ws, i64 n) {

@@ -270,6 +270,13 @@ size_t tdp_sort_workspace(int64_t n);
  * key: TDP_I64 / TDP_F64 / TDP_F32 / TDP_I32 scalar column.               */
 int tdp_sort_order(const tdp_column* key, int32_t descending, int64_t n, int64_t* out_order,
                    void* ws, size_t ws_bytes, void* stream);
+/* The first k entries of tdp_sort_order's stable order (ORDER BY ... LIMIT k,
+ * tq/kernels.py:267-273 sort_limit), 1 <= k <= 1024, without sorting all n:
+ * per-CTA bitonic sorts of 2048 (key image, row) pairs keep their k smallest,
+ * repeated on the survivors.  Writes min(k, n) row indices.                */
+size_t tdp_topk_workspace(int64_t n, int64_t k);
+int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t k,
+                   int64_t* out_order, void* ws, size_t ws_bytes, void* stream);
 
 /* np.unique(key, return_inverse=True) for an int64 column
  * (tq/kernels.py:128): out_uniques[0:u) ascending, out_inverse[i] = rank of

@@ -109,6 +109,9 @@ _SIGNATURES = {
     "tdp_scan_minmax": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate), c_int32,
                                 POINTER(c_int32), c_int32, c_void_p, c_void_p]),
     "tdp_sort_workspace": (c_size_t, [c_int64]),
+    "tdp_topk_workspace": (c_size_t, [c_int64, c_int64]),
+    "tdp_topk_order": (c_int, [POINTER(Column), c_int32, c_int64, c_int64, c_void_p, c_void_p,
+                               c_size_t, c_void_p]),
     "tdp_sort_order": (c_int, [POINTER(Column), c_int32, c_int64, c_void_p, c_void_p, c_size_t,
                                c_void_p]),
     "tdp_unique_inverse": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -343,6 +343,61 @@ __global__ void copy_counts_kernel(const unsigned long long* __restrict__ counts
 
 }  // namespace
 
+
+// ---------------------------------------------------------------------------
+// top-k of a stable order (ORDER BY ... LIMIT k, tq/kernels.py:267-273): the k
+// smallest (key image, row) pairs.  Each CTA bitonic-sorts a chunk of
+// kTopkChunk pairs in shared memory and keeps its first k; the survivors are
+// reduced the same way until one CTA remains.  Ties keep row order because the
+// row index is the second sort key, exactly as the stable radix sort orders.
+// ---------------------------------------------------------------------------
+constexpr int kTopkChunk = 2048;
+constexpr int kTopkThreads = 1024;
+constexpr int kTopkMax = 1024;
+
+__global__ void __launch_bounds__(kTopkThreads)
+    topk_chunk_kernel(const u64* __restrict__ keys, const i64* __restrict__ idx, i64 m, int k,
+                      u64* __restrict__ out_keys, i64* __restrict__ out_idx,
+                      i64* __restrict__ final_idx, i64 final_count) {
+  __shared__ u64 sk[kTopkChunk];
+  __shared__ i64 si[kTopkChunk];
+  const i64 base = (i64)blockIdx.x * kTopkChunk;
+  for (int t = threadIdx.x; t < kTopkChunk; t += blockDim.x) {
+    const i64 g = base + t;
+    const bool ok = g < m;
+    sk[t] = ok ? keys[g] : ~0ull;
+    si[t] = ok ? idx[g] : LLONG_MAX;  // sentinel sorts after every real pair
+  }
+  for (int size = 2; size <= kTopkChunk; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < kTopkChunk / 2; t += blockDim.x) {
+        const int a = 2 * t - (t & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        const u64 ka = sk[a], kb = sk[b];
+        const i64 ia = si[a], ib = si[b];
+        const bool gt = ka > kb || (ka == kb && ia > ib);
+        if (gt == up) {
+          sk[a] = kb;
+          sk[b] = ka;
+          si[a] = ib;
+          si[b] = ia;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (final_idx != nullptr) {  // last round: one CTA, the answer
+    for (int t = threadIdx.x; t < final_count; t += blockDim.x) final_idx[t] = si[t];
+    return;
+  }
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    out_keys[(i64)blockIdx.x * k + t] = sk[t];
+    out_idx[(i64)blockIdx.x * k + t] = si[t];
+  }
+}
+
 }  // namespace tdp
 
 using namespace tdp;
@@ -350,6 +405,63 @@ using namespace tdp;
 extern "C" {
 
 size_t tdp_sort_workspace(int64_t n) { return sort_ws_bytes(n); }
+
+size_t tdp_topk_workspace(int64_t n, int64_t k) {
+  const i64 m1 = ceil_div(n > 0 ? n : 1, kTopkChunk) * (k > 0 ? k : 1);
+  return 2 * align256((size_t)(n > 0 ? n : 1) * 8) + 4 * align256((size_t)m1 * 8) + 256;
+}
+
+int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t k,
+                   int64_t* out_order, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(key != nullptr && n >= 0, "bad top-k arguments");
+  TDP_REQUIRE(k >= 1 && k <= kTopkMax, "top-k needs 1 <= k <= %d (got %lld)", kTopkMax,
+              (long long)k);
+  TDP_REQUIRE(key->width == 1, "sort keys must be scalar columns");
+  TDP_REQUIRE(key->dtype == TDP_I64 || key->dtype == TDP_F64 || key->dtype == TDP_F32 ||
+                  key->dtype == TDP_I32,
+              "sort key dtype %d not supported", key->dtype);
+  TDP_REQUIRE(key->rows >= n, "short key column");
+  if (n == 0) return TDP_OK;
+  TDP_REQUIRE(ws_bytes >= tdp_topk_workspace(n, k), "top-k workspace too small");
+  cudaStream_t st = as_stream(stream);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  u64* k0 = (u64*)p;
+  p += align256((size_t)n * 8);
+  i64* i0 = (i64*)p;
+  p += align256((size_t)n * 8);
+  const i64 m1 = ceil_div(n, kTopkChunk) * k;
+  u64* ka = (u64*)p;
+  p += align256((size_t)m1 * 8);
+  i64* ia = (i64*)p;
+  p += align256((size_t)m1 * 8);
+  u64* kb = (u64*)p;
+  p += align256((size_t)m1 * 8);
+  i64* ib = (i64*)p;
+  make_keys_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(key->data, key->dtype,
+                                                                descending ? 1 : 0, n, k0, i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  const i64 want = k < n ? k : n;
+  const u64* sk = k0;
+  const i64* si = i0;
+  i64 m = n;
+  bool use_a = true;
+  while (m > kTopkChunk) {
+    const i64 blocks = ceil_div(m, kTopkChunk);
+    u64* dk = use_a ? ka : kb;
+    i64* di = use_a ? ia : ib;
+    topk_chunk_kernel<<<(unsigned)blocks, kTopkThreads, 0, st>>>(sk, si, m, (int)k, dk, di,
+                                                                 nullptr, 0);
+    TDP_LAUNCH_CHECK("topk_chunk_kernel");
+    sk = dk;
+    si = di;
+    m = blocks * k;
+    use_a = !use_a;
+  }
+  topk_chunk_kernel<<<1, kTopkThreads, 0, st>>>(sk, si, m, (int)k, nullptr, nullptr, out_order,
+                                                 want);
+  TDP_LAUNCH_CHECK("topk_chunk_kernel");
+  return TDP_OK;
+}
 
 int tdp_sort_order(const tdp_column* key, int32_t descending, int64_t n, int64_t* out_order,
                    void* ws, size_t ws_bytes, void* stream) {

@@ -891,11 +891,49 @@ def stable_order(key: EncodedTensor, descending: bool = False) -> torch.Tensor:
     return out
 
 
+TOPK_MAX = 1024
+
+
+def _sort_key_tensor(key: EncodedTensor, descending: bool) -> torch.Tensor:
+    if key.is_pe():
+        raise KernelError("cannot sort by a probability-encoded column")
+    if key.values.ndim != 1:
+        raise KernelError("sort keys must be scalar columns")
+    arr = key.values.data.detach()
+    if arr.dtype == torch.bool:
+        if descending:
+            raise TypeError("The numpy boolean negative, the `-` operator, is not supported, "
+                            "use the `~` operator or the logical_not function instead.")
+        arr = arr.to(torch.int64)
+    arr = arr.contiguous()
+    nat.require_cuda(arr)
+    return arr
+
+
+def topk_order(key: EncodedTensor, k: int, descending: bool = False) -> torch.Tensor:
+    """``stable_order(key, descending)[:k]`` without ordering all rows
+    (tdp_topk_order; 1 <= k <= TOPK_MAX)."""
+    arr = _sort_key_tensor(key, descending)
+    n = int(arr.shape[0])
+    out = torch.empty(min(k, n), dtype=torch.int64, device=arr.device)
+    if n:
+        ws = nat.workspace(nat.load().tdp_topk_workspace(n, k), arr.device)
+        nat.call("tdp_topk_order", nat.columns([arr]), 1 if descending else 0, n, k,
+                 nat.ptr(out), nat.ptr(ws), ws.numel(), nat.stream())
+    return out
+
+
 def sort_limit(columns: Sequence[EncodedTensor], key_index: int,
                descending: bool = False, limit: Optional[int] = None) -> list[EncodedTensor]:
-    order = stable_order(columns[key_index], descending)
-    if limit is not None:
-        order = order[: max(0, limit)]
+    """Stable order by one key, optionally truncated (tq/kernels.py:267-273);
+    a small LIMIT takes the top rows without ordering the rest."""
+    key = columns[key_index]
+    if limit is not None and 0 < limit <= TOPK_MAX and limit < key.row_count:
+        order = topk_order(key, limit, descending)
+    else:
+        order = stable_order(key, descending)
+        if limit is not None:
+            order = order[: max(0, limit)]
     return [take_rows(c, order) for c in columns]
 
 

@@ -265,3 +265,47 @@ def test_filtered_build_join_matches_oracle(unique_build, filter_probe):
     np.testing.assert_array_equal(out[2].values.numpy(), fbk[ebi])
     np.testing.assert_array_equal(out[3].values.numpy(), fbs[ebi])
     np.testing.assert_array_equal(out[4].values.numpy(), fbv[ebi])
+
+
+@pytest.mark.parametrize("n", [1, 7, 2048, 2049, 100_003, 3_000_000])
+@pytest.mark.parametrize("k", [1, 10, 1024])
+def test_topk_order_equals_stable_order_prefix(n, k):
+    """ORDER BY ... LIMIT k via the top-k kernel == the stable radix order's
+    first k rows (ties by row, numpy DESC/NaN/-0.0/INT64_MIN semantics)."""
+    from paper_2211_02753_b200.kernels import stable_order, topk_order
+
+    rng = np.random.default_rng(n + k)
+    ints = rng.integers(-50, 50, size=n)
+    ints[: min(n, 3)] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max, 0][: min(n, 3)]
+    floats = rng.integers(-20, 20, size=n).astype(np.float64) / 4
+    if n > 10:
+        floats[[1, 4, 9]] = [np.nan, -0.0, 0.0]
+    f32 = floats.astype(np.float32)
+    for arr in (ints, floats, f32):
+        col = tq.plain(tq.Tensor(arr))
+        for desc in (False, True):
+            full = stable_order(col, desc).cpu().numpy()[:k]
+            got = topk_order(col, k, desc).cpu().numpy()
+            np.testing.assert_array_equal(got, full)
+
+
+def test_order_by_limit_query_matches_oracle():
+    rng = np.random.default_rng(5)
+    n = 200_000
+    g = rng.integers(0, 50_000, size=n)
+    v = rng.integers(0, 1000, size=n).astype(np.float64)  # exact sums, many ties
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["g", "v"], [tq.plain(tq.Tensor(g)),
+                                                          tq.plain(tq.Tensor(v))]))
+    reg = tq.UdfRegistry()
+    for sql, desc, lim in (("SELECT g, SUM(v) FROM t GROUP BY g ORDER BY sum_v DESC LIMIT 10", True, 10),
+                           ("SELECT g, SUM(v) FROM t GROUP BY g ORDER BY sum_v LIMIT 1000", False, 1000),
+                           ("SELECT g, SUM(v) FROM t GROUP BY g ORDER BY sum_v DESC LIMIT 60000", True, 60000)):
+        q = wl.compile_sql(sql, cat, reg)
+        res = q.run(cat)
+        keys, inv = np.unique(g, return_inverse=True)
+        sums = np.zeros(len(keys))
+        np.add.at(sums, inv, v)
+        order = np.argsort(-sums if desc else sums, kind="stable")[:lim]
+        np.testing.assert_array_equal(res.columns[0].values.numpy(), keys[order])
+        np.testing.assert_allclose(res.columns[1].values.numpy(), sums[order], rtol=1e-12)

@@ -214,7 +214,15 @@ def require_cuda(*tensors: torch.Tensor) -> None:
                 f"B200 kernels need CUDA tensors; got a {t.device} tensor (no CPU fallback)")
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_raw_device = getattr(torch._C, "_cuda_getDevice", None)
+
+
 def stream() -> c_void_p:
+    """The current CUDA stream of the current device (torch's raw accessors:
+    this is called once per launch, torch.cuda.current_stream() costs ~10 us)."""
+    if _raw_stream is not None and _raw_device is not None:
+        return c_void_p(_raw_stream(_raw_device()))
     return c_void_p(torch.cuda.current_stream().cuda_stream)
 
 

@@ -562,6 +562,21 @@ def _llp(args):
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0
+    # exact swap of the trained query: pe_decode ->
+    # exact COUNT BY (Bag, Pred), one pass over X (tdp_linear_argmax_count)
+    exact = q.swap_to_exact()
+    for _ in range(3):
+        res = exact.run(cat)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        res = exact.run(cat)
+    e1.record()
+    torch.cuda.synchronize()
+    swap_ms = e0.elapsed_time(e1) / steps
+    swap_groups = int(res.row_count)
     # CPU baseline: the closed-form oracle of the reference's step, one core
     from oracle import relational as orc
 
@@ -591,7 +606,11 @@ def _llp(args):
                          "cores": 1, "kind": "port",
                          "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
                                    f"reference tape), {reps} reps, extrapolated to {n} rows"},
-        "bytes_floor_ms": 528 * n / 6449.4e9 * 1e3,
+        "bytes_floor_ms": 528 * n / _peaks()[0] / 1e9 * 1e3,
+        "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
+                       "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
+                       "what": "q.swap_to_exact().run(cat): pe_decode + exact COUNT by (Bag, Pred); "
+                               "one pass over X + bag codes (tdp_linear_argmax_count)"},
     }
     print(json.dumps(line), flush=True)
 

@@ -423,6 +423,14 @@ int tdp_soft_linear_supported(int32_t dtype, int64_t n, int32_t d, int32_t k, in
 int tdp_soft_linear_count_fwd(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k,
                               const void* W, const void* bias, const tdp_soft_key* keys,
                               int32_t nkeys, int32_t dense_key, double* out_grid, void* stream);
+/* The exact swap of the same query (CompiledQuery.swap_to_exact inserts
+ * pe_decode, tq/compiler.py:125-136, :378-381): exact COUNT grouped by the
+ * one-hot codes and argmax(softmax(X W + bias)) (tq/encodings.py:154-165:
+ * first maximum, NaN wins) in one pass over X; out_counts is the dense
+ * int64 count grid over the cells (row-major in key order).              */
+int tdp_linear_argmax_count(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k,
+                            const void* W, const void* bias, const tdp_soft_key* keys,
+                            int32_t nkeys, int32_t dense_key, int64_t* out_counts, void* stream);
 size_t tdp_soft_linear_count_bwd_workspace(int64_t n, int32_t d, int32_t k);
 /* VJP of the above w.r.t. W and bias for the upstream grid gradient G
  * (float64): the softmax VJP (tq/tensor.py:515-527) of dP[i,c] = G[cell(i,c)]

@@ -147,6 +147,9 @@ _SIGNATURES = {
     "tdp_linear_wgrad": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p,
                                  c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_soft_linear_supported": (c_int, [c_int32, c_int64, c_int32, c_int32, c_int64, c_void_p]),
+    "tdp_linear_argmax_count": (c_int, [c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p,
+                                        c_void_p, POINTER(SoftKey), c_int32, c_int32, c_void_p,
+                                        c_void_p]),
     "tdp_soft_linear_count_fwd": (c_int, [c_void_p, c_int32, c_int64, c_int32, c_int32, c_void_p,
                                           c_void_p, POINTER(SoftKey), c_int32, c_int32, c_void_p,
                                           c_void_p]),

@@ -249,7 +249,7 @@ def soft_linear_supported(x: torch.Tensor, w: torch.Tensor, cells: int) -> bool:
                                                      int(cells), nat.ptr(x)))
 
 
-def _linear_keys(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor]):
+def linear_keys(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor]):
     arr = (nat.SoftKey * len(spec.kinds))()
     it = iter(codes)
     for j, (kind, k) in enumerate(spec.kinds):
@@ -270,7 +270,7 @@ class _SoftLinearCount(torch.autograd.Function):
         n, d = x.shape
         k = w.shape[1]
         grid = torch.empty(spec.cells, dtype=torch.float64, device=x.device)
-        keys = _linear_keys(spec, dense_pos, codes)
+        keys = linear_keys(spec, dense_pos, codes)
         nat.call("tdp_soft_linear_count_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
                  keys, len(spec.kinds), dense_pos, nat.ptr(grid), nat.stream())
         ctx.spec, ctx.dense_pos, ctx.has_bias = spec, dense_pos, b is not None
@@ -289,7 +289,7 @@ class _SoftLinearCount(torch.autograd.Function):
         dw = torch.empty_like(w)
         db = torch.empty_like(b) if b is not None else None
         ws = nat.workspace(nat.load().tdp_soft_linear_count_bwd_workspace(n, d, k), x.device)
-        keys = _linear_keys(ctx.spec, ctx.dense_pos, codes)
+        keys = linear_keys(ctx.spec, ctx.dense_pos, codes)
         nat.call("tdp_soft_linear_count_bwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
                  keys, len(ctx.spec.kinds), ctx.dense_pos, nat.ptr(G), nat.ptr(dw), nat.ptr(db),
                  nat.ptr(ws), ws.numel(), nat.stream())

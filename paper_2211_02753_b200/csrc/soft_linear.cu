@@ -151,7 +151,29 @@ __device__ __forceinline__ void load_head(const T* __restrict__ W, const T* __re
   for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
 }
 
-template <class T, int K, int V>
+// first maximum, NaN counting as the maximum (np.argmax, tdp_pe_argmax)
+template <class T, int K>
+__device__ __forceinline__ int argmax_row(const T (&p)[K]) {
+  int best = 0;
+  T bv = p[0];
+  bool bnan = bv != bv;
+#pragma unroll
+  for (int c = 1; c < K; ++c) {
+    const bool vn = p[c] != p[c];
+    if (!bnan && (vn || p[c] > bv)) {
+      best = c;
+      bv = p[c];
+      bnan = vn;
+    }
+  }
+  return best;
+}
+
+// kArgmax: the exact swap of the same query (pe_decode of the head's PE column,
+// tq/encodings.py:154-165, then an exact COUNT by the decoded keys): each row
+// adds 1 to the cell of argmax(P) instead of P to every cell; grid is then a
+// uint64 count grid.
+template <class T, int K, int V, bool kArgmax>
 __global__ void __launch_bounds__(kRingThreads)
     soft_linear_count_fwd_kernel(const T* __restrict__ X, i64 n, int stages,
                                  const T* __restrict__ W, const T* __restrict__ bias,
@@ -207,8 +229,13 @@ __global__ void __launch_bounds__(kRingThreads)
         for (int j = 0; j < K; ++j) z[j] += bj[j];
         T p[K];
         softmax_row<T, K>(z, p);
+        if (kArgmax) {
+          atomicAdd(lo + base + argmax_row<T, K>(p) * oh.dense_stride, 1u);
+        } else {
 #pragma unroll
-        for (int j = 0; j < K; ++j) fix_add(lo, hi, grid, base + j * oh.dense_stride, (double)p[j]);
+          for (int j = 0; j < K; ++j)
+            fix_add(lo, hi, grid, base + j * oh.dense_stride, (double)p[j]);
+        }
       }
       if (++s == stages) {
         s = 0;
@@ -219,7 +246,11 @@ __global__ void __launch_bounds__(kRingThreads)
   __syncthreads();
   for (int c = threadIdx.x; c < cells; c += blockDim.x) {
     const unsigned l = lo[c], h = hi[c];
-    if (l | h) atomicAdd(grid + c, ((double)h * 4294967296.0 + (double)l) / kFixScale);
+    if (kArgmax) {
+      if (l) atomicAdd(reinterpret_cast<unsigned long long*>(grid) + c, (unsigned long long)l);
+    } else if (l | h) {
+      atomicAdd(grid + c, ((double)h * 4294967296.0 + (double)l) / kFixScale);
+    }
   }
 }
 
@@ -417,7 +448,7 @@ int make_keys(const tdp_soft_key* keys, int nkeys, int dense_key, int k, i64* ce
   return TDP_OK;
 }
 
-template <class T>
+template <class T, bool kArgmax = false>
 int launch_fwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
                const OneHotKeys& oh_in, i64 cells, double* grid, cudaStream_t st) {
   Plan p;
@@ -429,9 +460,9 @@ int launch_fwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
   bool launched = false;
 #define TDP_CASE(KK, VV)                                                                       \
   if constexpr (sizeof(T) == 4 || VV == 1) if (k == KK && p.V == VV) {                                                                \
-    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_fwd_kernel<T, KK, VV>,                 \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_fwd_kernel<T, KK, VV, kArgmax>,        \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)); \
-    soft_linear_count_fwd_kernel<T, KK, VV><<<p.grid, kRingThreads, p.smem, st>>>(             \
+    soft_linear_count_fwd_kernel<T, KK, VV, kArgmax><<<p.grid, kRingThreads, p.smem, st>>>(    \
         (const T*)X, n, p.stages, (const T*)W, (const T*)b, oh, (int)cells, grid);             \
     launched = true;                                                                           \
   }
@@ -510,6 +541,21 @@ int tdp_soft_linear_count_fwd(const void* X, int32_t dtype, int64_t n, int32_t d
   if (dtype == TDP_F32) return launch_fwd<float>(X, n, d, k, W, bias, oh, cells, out_grid, st);
   if (dtype == TDP_F64) return launch_fwd<double>(X, n, d, k, W, bias, oh, cells, out_grid, st);
   return set_error(TDP_EINVAL, "soft_linear: float32/float64 only");
+}
+
+int tdp_linear_argmax_count(const void* X, int32_t dtype, int64_t n, int32_t d, int32_t k,
+                            const void* W, const void* bias, const tdp_soft_key* keys,
+                            int32_t nkeys, int32_t dense_key, int64_t* out_counts, void* stream) {
+  i64 cells = 0;
+  OneHotKeys oh;
+  if (int rc = make_keys(keys, nkeys, dense_key, k, &cells, &oh)) return rc;
+  cudaStream_t st = as_stream(stream);
+  TDP_CUDA_TRY(cudaMemsetAsync(out_counts, 0, (size_t)cells * sizeof(int64_t), st));
+  if (n == 0) return TDP_OK;
+  double* grid = reinterpret_cast<double*>(out_counts);
+  if (dtype == TDP_F32) return launch_fwd<float, true>(X, n, d, k, W, bias, oh, cells, grid, st);
+  if (dtype == TDP_F64) return launch_fwd<double, true>(X, n, d, k, W, bias, oh, cells, grid, st);
+  return set_error(TDP_EINVAL, "linear_argmax_count: float32/float64 only");
 }
 
 size_t tdp_soft_linear_count_bwd_workspace(int64_t n, int32_t d, int32_t k) {

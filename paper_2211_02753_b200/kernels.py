@@ -32,9 +32,11 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, soft_groupby_grid,
-                       soft_linear_count, soft_linear_supported)
+from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, linear_keys,
+                       soft_groupby_grid, soft_linear_count, soft_linear_supported)
 from .encodings import (
+    DecodedArgmax,
+    DecodedCodes,
     DictionaryEncoding,
     EncodedTensor,
     EncodingError,
@@ -438,12 +440,66 @@ def groupby_exact(keys: Sequence[EncodedTensor], aggs: Sequence[AggInput], *,
         agg_specs.append((func, _value_dtype(v)))
         agg_vals.append(v)
 
+    fused = _groupby_decoded_linear(keys, agg_specs, defer_rows)
+    if fused is not None:
+        return fused
     operands = key_vals + [v for v in agg_vals if v is not None]
     space = _fusable(operands)
     if space is not None and all(as_expr(k)[0].op in ("col", "cast", "add", "sub", "mul", "neg", "square")
                                  for k in key_vals):
         return _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows)
     return _groupby_general(keys, key_vals, agg_specs, agg_vals)
+
+
+def _groupby_decoded_linear(keys, agg_specs, defer_rows=False):
+    """COUNT grouped by pe_decode(pe_encode(Linear(X))) and decoded one-hot
+    codes -- the exact swap of a trained LLP query -- in
+    one pass over X (tdp_linear_argmax_count), then the dense finalisation of
+    the fused group-by (occupied groups in ascending key order).  None when
+    the keys / aggregates do not have that form."""
+    if not agg_specs or any(f != "count" for f, _ in agg_specs):
+        return None
+    if active_tape() is not None or current_group() is not None:
+        return None
+    dense, kinds, codes = None, [], []
+    for j, k in enumerate(keys):
+        v = k.values
+        lz = v._lazy if v._t is None else None
+        if isinstance(lz, DecodedArgmax) and lz._out is None and dense is None:
+            dense = (j, lz)
+            kinds.append(("dense", lz.k))
+        elif isinstance(lz, DecodedCodes):
+            kinds.append(("onehot", lz.k))
+            codes.append(lz.codes.contiguous())
+        else:
+            return None
+    if dense is None:
+        return None
+    pos, dec = dense
+    lin = dec.pend.lin
+    spec = SoftKeySpec(kinds)
+    if not soft_linear_supported(lin.x, lin.w, spec.cells):
+        return None
+    nat.require_cuda(*codes)
+    x, w = lin.x.detach().contiguous(), lin.w.detach().contiguous()
+    b = None if lin.b is None else lin.b.detach().contiguous()
+    n, d = x.shape
+    slots = spec.cells
+    counts = torch.empty(slots, dtype=torch.int64, device=x.device)
+    nat.call("tdp_linear_argmax_count", nat.ptr(x), nat.TORCH_TO_TDP[x.dtype], n, d,
+             int(w.shape[1]), nat.ptr(w), nat.ptr(b), linear_keys(spec, pos, codes),
+             len(kinds), pos, nat.ptr(counts), nat.stream())
+    naggs = len(agg_specs)
+    sums = counts.unsqueeze(0).expand(naggs, slots).contiguous()
+    spans = [(0, kk) for _, kk in kinds]
+    kinds_native = [nat.AGG_COUNT] * naggs
+    out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds_native, 0,
+                                                  x.device, defer_rows)
+    key_values = [out_keys[j].contiguous() for j in range(len(keys))]
+    agg_values = _agg_outputs(agg_specs, out_aggs, out_counts, already_avg=True)
+    if defer_rows:
+        return ([PrefixRows(kv, g) for kv in key_values], [PrefixRows(a, g) for a in agg_values])
+    return key_values, agg_values
 
 
 def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False):

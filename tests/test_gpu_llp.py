@@ -79,3 +79,43 @@ def test_soft_counts_conserve_mass_and_gradient_of_total_is_zero():
         g = tape.gradient(x).numpy()
     assert abs(float(total.item()) - 4000.0) < 1e-6
     assert np.max(np.abs(g)) < 1e-6
+
+
+@pytest.mark.parametrize("dtype,d", [("float64", 32), ("float32", 64)])
+def test_exact_swap_fused_argmax_count(dtype, d):
+    """swap_to_exact of an LLP-shaped query: COUNT by (decoded one-hot bag,
+    argmax of the linear head's softmax) in one pass over X
+    (tdp_linear_argmax_count) == decoding the materialised probabilities
+    (same row arithmetic) and counting, bit for bit; and == numpy in float64."""
+    from paper_2211_02753_b200.encodings import DecodedArgmax
+
+    rng = np.random.default_rng(7)
+    n, bags, k = 50_000, 37, 3
+    X = rng.normal(size=(n, d)).astype(dtype)
+    bag = rng.integers(0, bags, size=n)
+    model = tq.Linear(d, k, np.random.default_rng(1), name="lin", dtype=dtype)
+    bag_pe = tq.one_hot_pe(bag, bags)
+    reg = tq.UdfRegistry()
+    reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(k))), 1,
+                             lambda c: (bag_pe, tq.pe_encode(model(c.values))), model.parameters))
+    cat = tq.Catalog()
+    cat.register_tensor(tq.Tensor(X), "T")
+    plan = tq.lower(tq.bind(tq.parse("SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"),
+                            cat, reg))
+    exact = tq.compile_plan(plan, tq.CompileConfig(trainable=True), reg).swap_to_exact()
+    dec = tq.pe_decode(tq.pe_encode(model(tq.Tensor(X))))
+    assert isinstance(dec.values._lazy, DecodedArgmax)  # the fused path's input form
+    res = exact.run(cat)
+    got = [c.values.numpy() for c in res.columns]
+    # eager: materialise P with the unfused kernels, decode, count
+    P = tq.pe_encode(model(tq.Tensor(X))).values.numpy()
+    pred = np.argmax(P, axis=1)
+    cells, cnt = np.unique(bag * k + pred, return_counts=True)
+    np.testing.assert_array_equal(got[0], cells // k)
+    np.testing.assert_array_equal(got[1], cells % k)
+    np.testing.assert_array_equal(got[2], cnt)
+    if dtype == "float64":
+        z = X @ model.weight.value.numpy() + model.bias.value.numpy()
+        e = np.exp(z - z.max(axis=1, keepdims=True))
+        ref = np.argmax(e / e.sum(axis=1, keepdims=True), axis=1)
+        assert np.count_nonzero(ref != pred) == 0

@@ -1114,6 +1114,9 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
     if active_tape() is not None:
         pi, bi = join_indices(left[left_key].values, right[right_key].values)
         return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
+    group = current_group()
+    if group is not None and world_size(group) > 1:
+        return _equi_join_sharded(left, right, left_key, right_key, group)
     lb, lsel = _side_sources(left)
     rb, rsel = _side_sources(right)
     # a filtered side whose key is a base column joins straight from the base
@@ -1135,6 +1138,42 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
         pairs = join_indices(lkey, rkey, probe_sel=lsel if lkey_direct else None)
     pi, bi = pairs
     return _gather_side(left, lb, lmap, pi) + _gather_side(right, rb, rmap, bi)
+
+
+def _repartition(cols: Sequence[EncodedTensor], key_index: int, group) -> list[EncodedTensor]:
+    """Rows of one (row-sharded) relation moved to the rank that owns their
+    join key (key_destination), by an NCCL all-to-all; encodings kept."""
+    data = []
+    for c in cols:
+        if c.is_pe() or c.values.ndim != 1:
+            raise KernelError("a sharded join moves scalar columns only")
+        t = c.values.data.detach()
+        data.append(t.to(torch.int64) if t.dtype == torch.bool else t.contiguous())
+    world = world_size(group)
+    dest = key_destination([data[key_index]], world)
+    n = int(dest.numel())
+    order = stable_order(plain(Tensor(dest)))
+    send_counts, _ = _groupby_codes(dest, world, [], [], n, dest.device)
+    moved = exchange_rows(gather_many(data, order), send_counts, group)
+    out = []
+    with trusted():
+        for c, t, orig in zip(cols, moved, data):
+            if c.values.dtype == "bool":
+                t = t.to(torch.bool)
+            out.append(EncodedTensor(Tensor(t), c.encoding))
+    return out
+
+
+def _equi_join_sharded(left, right, left_key: int, right_key: int, group) -> list[EncodedTensor]:
+    """Equi-join of two row-sharded relations: both sides are
+    repartitioned by key with an all-to-all, so every key's rows meet on one
+    rank, then joined locally.  The result is again row-sharded (each rank
+    holds the pairs of the keys it owns); its row order is by rank of
+    arrival, as the join's order is not part of its contract."""
+    lp = _repartition(left, left_key, group)
+    rp = _repartition(right, right_key, group)
+    pi, bi = join_indices(lp[left_key].values, rp[right_key].values)
+    return [take_rows(c, pi) for c in lp] + [take_rows(c, bi) for c in rp]
 
 
 # ---------------------------------------------------------------------------

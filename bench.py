@@ -51,6 +51,8 @@ def _args():
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-companion", action="store_true",
+                    help="skip the Q6 companion measurement of the default Q1 run")
     ap.add_argument("--encoding", choices=("wide", "compact"), default="wide",
                     help="compact: lossless narrow column storage (SURVEY §8(f) 1)")
     return ap.parse_args()
@@ -265,6 +267,45 @@ def _ours(args):
             dist.all_reduce(lt, op=dist.ReduceOp.SUM)
             launches = int(lt.item())
 
+        # ---- companion Q6 on the same shard (the metric names Q1 and Q6) ---
+        companion = None
+        if args.query == "q1" and not args.no_companion:
+            q6 = wl.compile_sql(wl.Q6_SQL, cat, wl.q6_registry())
+            for _ in range(3):
+                q6.run(cat)
+            barrier()
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c1 = torch.cuda.Event(enable_timing=True)
+            c0.record()
+            for _ in range(args.steps):
+                r6 = q6.run(cat)
+            c1.record()
+            torch.cuda.synchronize()
+            barrier()
+            ms6 = c0.elapsed_time(c1) / args.steps
+            os.environ["TDP_REPLAY"] = "0"
+            _native.load().tdp_kernel_timer_enable(1)
+            _native.load().tdp_kernel_timer_read(None, None)
+            for _ in range(args.steps):
+                r6 = q6.run(cat)
+            torch.cuda.synchronize()
+            _native.load().tdp_kernel_timer_enable(0)
+            os.environ.pop("TDP_REPLAY", None)
+            _native.load().tdp_kernel_timer_read(_ct.byref(_tot), _ct.byref(_cnt))
+            k6 = _tot.value / _cnt.value if _cnt.value else 0.0
+            if world > 1:
+                t = torch.tensor([ms6, k6], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms6, k6 = float(t[0]), float(t[1])
+            b6 = wl.Q6_BYTES_PER_ROW if args.encoding == "wide" else None
+            companion = {"workload": f"TPC-H Q6 SF{args.sf * world:g} on the same lineitem shards",
+                         "value": n_total / (ms6 / 1e3), "unit": "rows/s", "ms_per_step": ms6,
+                         "kernel_ms": k6}
+            if b6 and k6:
+                companion["hbm_gbs_kernel"] = b6 * rows / (k6 / 1e3) / 1e9
+            companion["result"] = float(r6.columns[0].values.numpy()[0]) if rank == 0 else None
+
         # ---- end to end through the API from pinned host buffers ----------
         if args.encoding == "compact":
             from paper_2211_02753_b200 import compact as cp
@@ -356,6 +397,10 @@ def _ours(args):
                      "algorithmic_bytes_per_launch": bpr * kernel_rows},
         "clocks": clocks,
     }
+    if companion is not None:
+        companion["peak_frac_kernel"] = (companion["hbm_gbs_kernel"] / peak
+                                         if "hbm_gbs_kernel" in companion else None)
+        line["companion_q6"] = companion
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"], line["parity"] = _cpu_baseline(args, arrays, query, cat)
     print(json.dumps(line), flush=True)

@@ -224,6 +224,19 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
                        int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
                        size_t ws_bytes, void* stream);
 
+/* tdp_scan_aggregate followed by tdp_groupby_finalize in one call: for
+ * small group spaces the partial-row reduction and the finalisation run as
+ * one single-CTA launch after the scan.  out_counts / out_sums receive the
+ * raw per-slot results as in tdp_scan_aggregate; the finalisation outputs
+ * are those of tdp_groupby_finalize (slots = prod(key spans)).             */
+int tdp_scan_aggregate_grouped(const tdp_column* cols, int32_t ncols, int64_t n,
+                               const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                               int32_t nprog, const tdp_key* keys, int32_t nkeys,
+                               const tdp_agg* aggs, int32_t naggs, int64_t* out_counts,
+                               void* out_sums, void* ws, size_t ws_bytes, uint64_t avg_mask,
+                               int64_t* out_keys, int64_t* out_group_counts, void* out_aggs,
+                               int64_t* out_groups, void* stream);
+
 /* Same front half, but writes the selected rows' program values
  * (outputs[j] = value outs[j]) compacted in row order: the materialised
  * form of a lazily filtered, elementwise-UDF column.                       */

@@ -96,6 +96,11 @@ _SIGNATURES = {
     "tdp_scan_aggregate": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate), c_int32,
                                    POINTER(Instr), c_int32, POINTER(Key), c_int32, POINTER(Agg),
                                    c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_scan_aggregate_grouped": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate),
+                                           c_int32, POINTER(Instr), c_int32, POINTER(Key), c_int32,
+                                           POINTER(Agg), c_int32, c_void_p, c_void_p, c_void_p,
+                                           c_size_t, c_uint64, c_void_p, c_void_p, c_void_p,
+                                           c_void_p, c_void_p]),
     "tdp_scan_project": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate), c_int32,
                                  POINTER(Instr), c_int32, POINTER(c_int32), c_int32,
                                  POINTER(c_void_p), c_void_p, c_void_p, c_size_t, c_void_p]),

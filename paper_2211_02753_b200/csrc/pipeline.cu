@@ -634,13 +634,14 @@ struct AggMap {
 
 // One warp per output item; lanes stride over the partial rows in a fixed
 // order and combine with a fixed shuffle tree -> bitwise deterministic.
-__global__ void agg_reduce_kernel(const u64* __restrict__ part, int rows, int slots, AggMap m,
-                                  i64* __restrict__ out_counts, u64* __restrict__ out_sums) {
+__device__ __forceinline__ void reduce_items(const u64* __restrict__ part, int rows, int slots,
+                                             const AggMap& m, i64* __restrict__ out_counts,
+                                             u64* __restrict__ out_sums, i64 first_warp,
+                                             i64 nwarps) {
   const int lane = threadIdx.x & 31;
   const i64 items = (i64)slots * (1 + m.naggs);
   const i64 cells = (i64)slots * (1 + m.nf + m.ni);
-  for (i64 it = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
-       it += ((i64)gridDim.x * blockDim.x) >> 5) {
+  for (i64 it = first_warp; it < items; it += nwarps) {
     i64 cell;
     bool is_f = false;
     if (it < slots) {
@@ -657,22 +658,41 @@ __global__ void agg_reduce_kernel(const u64* __restrict__ part, int rows, int sl
         cell = (i64)slots * (1 + m.nf + m.acc[a]) + g;
       }
     }
+    // partial rows are cell-major: part[cell * rows + r] (coalesced per warp);
+    // four accumulators per lane keep several loads in flight, combined in a
+    // fixed order -> bitwise deterministic
+    const u64* src = part + cell * (i64)rows;
     u64 bits;
     if (is_f) {
-      double v = 0.0;
-      for (int r = lane; r < rows; r += 32) v += __longlong_as_double((i64)part[(i64)r * cells + cell]);
-      v = warp_sum(v);
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      int r = lane;
+      for (; r + 96 < rows; r += 128) {
+        v0 += __longlong_as_double((i64)src[r]);
+        v1 += __longlong_as_double((i64)src[r + 32]);
+        v2 += __longlong_as_double((i64)src[r + 64]);
+        v3 += __longlong_as_double((i64)src[r + 96]);
+      }
+      for (; r < rows; r += 32) v0 += __longlong_as_double((i64)src[r]);
+      double v = warp_sum((v0 + v1) + (v2 + v3));
       bits = (u64)__double_as_longlong(v);
     } else {
       u64 v = 0;
-      for (int r = lane; r < rows; r += 32) v += part[(i64)r * cells + cell];
+      for (int r = lane; r < rows; r += 32) v += src[r];
       bits = warp_sum(v);
     }
+    (void)cells;
     if (lane == 0) {
       if (it < slots) out_counts[it] = (i64)bits;
       else out_sums[it - slots] = bits;
     }
   }
+}
+
+__global__ void agg_reduce_kernel(const u64* __restrict__ part, int rows, int slots, AggMap m,
+                                  i64* __restrict__ out_counts, u64* __restrict__ out_sums) {
+  reduce_items(part, rows, slots, m, out_counts, out_sums,
+               ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+               ((i64)gridDim.x * blockDim.x) >> 5);
 }
 
 struct KeyDigits {
@@ -684,11 +704,14 @@ struct KeyDigits {
 };
 
 // Single CTA: compact occupied slots in ascending slot order.
-__global__ void __launch_bounds__(1024)
-    finalize_kernel(const i64* __restrict__ counts, const u64* __restrict__ sums, i64 slots,
-                    KeyDigits kd, AggMap m, unsigned long long avg_mask,
-                    i64* __restrict__ out_keys, i64* __restrict__ out_counts,
-                    u64* __restrict__ out_aggs, i64* __restrict__ out_groups) {
+__device__ __forceinline__ void finalize_block(const i64* __restrict__ counts,
+                                               const u64* __restrict__ sums, i64 slots,
+                                               const KeyDigits& kd, const AggMap& m,
+                                               unsigned long long avg_mask,
+                                               i64* __restrict__ out_keys,
+                                               i64* __restrict__ out_counts,
+                                               u64* __restrict__ out_aggs,
+                                               i64* __restrict__ out_groups) {
   __shared__ int warp_tot[32];
   __shared__ i64 running;
   if (threadIdx.x == 0) running = 0;
@@ -730,6 +753,29 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
   }
   if (threadIdx.x == 0) *out_groups = running;
+}
+
+__global__ void __launch_bounds__(1024)
+    finalize_kernel(const i64* __restrict__ counts, const u64* __restrict__ sums, i64 slots,
+                    KeyDigits kd, AggMap m, unsigned long long avg_mask,
+                    i64* __restrict__ out_keys, i64* __restrict__ out_counts,
+                    u64* __restrict__ out_aggs, i64* __restrict__ out_groups) {
+  finalize_block(counts, sums, slots, kd, m, avg_mask, out_keys, out_counts, out_aggs, out_groups);
+}
+
+// Small group spaces: the partial-row reduction and the finalisation in one
+// CTA (one launch after the scan instead of two).
+constexpr i64 kFusedTailItems = 4096;
+__global__ void __launch_bounds__(1024)
+    reduce_finalize_kernel(const u64* __restrict__ part, int rows, int slots, AggMap m,
+                           i64* __restrict__ red_counts, u64* __restrict__ red_sums,
+                           KeyDigits kd, unsigned long long avg_mask, i64* __restrict__ out_keys,
+                           i64* __restrict__ out_counts, u64* __restrict__ out_aggs,
+                           i64* __restrict__ out_groups) {
+  reduce_items(part, rows, slots, m, red_counts, red_sums, threadIdx.x >> 5, blockDim.x >> 5);
+  __syncthreads();  // the CTA's global writes are visible to the CTA
+  finalize_block(red_counts, red_sums, slots, kd, m, avg_mask, out_keys, out_counts, out_aggs,
+                 out_groups);
 }
 
 struct KeyCols {
@@ -905,11 +951,40 @@ size_t tdp_scan_aggregate_workspace(int64_t n, int64_t slots, int32_t naggs) {
   return (size_t)((reg > cells ? reg : cells) * 8 + 256);
 }
 
-int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
-                       const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
-                       int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
-                       int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
-                       size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace tdp {
+namespace {
+struct GroupOut {  // finalisation outputs (tdp_scan_aggregate_grouped)
+  unsigned long long avg_mask;
+  int64_t* keys;
+  int64_t* counts;
+  void* aggs;
+  int64_t* groups;
+};
+
+int key_digits(const tdp_key* keys, int nkeys, i64 slots, KeyDigits* kd) {
+  TDP_REQUIRE(nkeys >= 0 && nkeys <= kMaxKeys, "bad key count");
+  std::memset(kd, 0, sizeof(*kd));
+  kd->nkeys = nkeys;
+  i64 prod = 1;
+  for (int j = nkeys - 1; j >= 0; --j) {
+    TDP_REQUIRE(keys[j].span >= 1, "key %d: bad span", j);
+    kd->lo[j] = keys[j].lo;
+    kd->span[j] = keys[j].span;
+    kd->stride[j] = prod;
+    prod *= keys[j].span;
+  }
+  TDP_REQUIRE(prod == slots, "slots %lld != product of key spans %lld", (long long)slots,
+              (long long)prod);
+  return TDP_OK;
+}
+
+int scan_aggregate_impl(const tdp_column* cols, int32_t ncols, int64_t n,
+                        const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                        int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                        int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
+                        size_t ws_bytes, void* stream, const GroupOut* fin) {
   Spec s;
   int rc = build_spec(s, cols, ncols, n, preds, npreds, prog, nprog, keys, nkeys, aggs, naggs,
                       nullptr, 0);
@@ -971,11 +1046,61 @@ int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
   }
   AggMap m = make_map(s);
   const i64 items = s.slots * (1 + naggs);
+  if (fin != nullptr) {
+    KeyDigits kd;
+    rc = key_digits(keys, nkeys, s.slots, &kd);
+    if (rc) return rc;
+    if (items <= kFusedTailItems) {
+      reduce_finalize_kernel<<<1, 1024, 0, st>>>(
+          reinterpret_cast<const u64*>(ws), (int)rows, (int)s.slots, m, out_counts,
+          reinterpret_cast<u64*>(out_sums), kd, fin->avg_mask, fin->keys, fin->counts,
+          reinterpret_cast<u64*>(fin->aggs), fin->groups);
+      TDP_LAUNCH_CHECK("reduce_finalize_kernel");
+      return TDP_OK;
+    }
+    agg_reduce_kernel<<<(unsigned)ceil_div(items * 32, 256), 256, 0, st>>>(
+        reinterpret_cast<const u64*>(ws), (int)rows, (int)s.slots, m, out_counts,
+        reinterpret_cast<u64*>(out_sums));
+    TDP_LAUNCH_CHECK("agg_reduce_kernel");
+    finalize_kernel<<<1, 1024, 0, st>>>(out_counts, reinterpret_cast<const u64*>(out_sums),
+                                        s.slots, kd, m, fin->avg_mask, fin->keys, fin->counts,
+                                        reinterpret_cast<u64*>(fin->aggs), fin->groups);
+    TDP_LAUNCH_CHECK("finalize_kernel");
+    return TDP_OK;
+  }
   agg_reduce_kernel<<<(unsigned)ceil_div(items * 32, 256), 256, 0, st>>>(
       reinterpret_cast<const u64*>(ws), (int)rows, (int)s.slots, m, out_counts,
       reinterpret_cast<u64*>(out_sums));
   TDP_LAUNCH_CHECK("agg_reduce_kernel");
   return TDP_OK;
+}
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+int tdp_scan_aggregate(const tdp_column* cols, int32_t ncols, int64_t n,
+                       const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                       int32_t nprog, const tdp_key* keys, int32_t nkeys, const tdp_agg* aggs,
+                       int32_t naggs, int64_t* out_counts, void* out_sums, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return scan_aggregate_impl(cols, ncols, n, preds, npreds, prog, nprog, keys, nkeys, aggs, naggs,
+                             out_counts, out_sums, ws, ws_bytes, stream, nullptr);
+}
+
+int tdp_scan_aggregate_grouped(const tdp_column* cols, int32_t ncols, int64_t n,
+                               const tdp_predicate* preds, int32_t npreds, const tdp_instr* prog,
+                               int32_t nprog, const tdp_key* keys, int32_t nkeys,
+                               const tdp_agg* aggs, int32_t naggs, int64_t* out_counts,
+                               void* out_sums, void* ws, size_t ws_bytes, uint64_t avg_mask,
+                               int64_t* out_keys, int64_t* out_group_counts, void* out_aggs,
+                               int64_t* out_groups, void* stream) {
+  TDP_REQUIRE(out_keys != nullptr && out_group_counts != nullptr && out_groups != nullptr &&
+                  (naggs == 0 || out_aggs != nullptr),
+              "null finalisation output");
+  GroupOut fin{(unsigned long long)avg_mask, out_keys, out_group_counts, out_aggs, out_groups};
+  return scan_aggregate_impl(cols, ncols, n, preds, npreds, prog, nprog, keys, nkeys, aggs, naggs,
+                             out_counts, out_sums, ws, ws_bytes, stream, &fin);
 }
 
 int tdp_scan_project(const tdp_column* cols, int32_t ncols, int64_t n,

@@ -139,31 +139,33 @@ struct TdpAcc {
       }
     }
     __syncthreads();
-    u64* out = reinterpret_cast<u64*>(P.acc) + (i64)blockIdx.x * TDP_CELLS;
+    // partial rows are stored cell-major (acc[cell * gridDim.x + cta]) so the
+    // reduction over CTAs reads each cell contiguously
+    u64* out = reinterpret_cast<u64*>(P.acc) + blockIdx.x;
     for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {
       if (c >= TDP_G && c < TDP_G * (1 + TDP_NF)) {
         double v = 0.0;
         for (int w = 0; w < NWARPS; ++w) v += __longlong_as_double((i64)red[w][c]);
-        out[c] = (u64)__double_as_longlong(v);
+        out[(i64)c * gridDim.x] = (u64)__double_as_longlong(v);
       } else {
         u64 v = 0;
         for (int w = 0; w < NWARPS; ++w) v += red[w][c];
-        out[c] = v;
+        out[(i64)c * gridDim.x] = v;
       }
     }
 #elif TDP_SMEMACC
     __syncthreads();
-    u64* out = reinterpret_cast<u64*>(P.acc) + (i64)blockIdx.x * TDP_CELLS;
+    u64* out = reinterpret_cast<u64*>(P.acc) + blockIdx.x;  // cell-major, as above
     for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {
       const u64* row = sm + (size_t)c * TDP_ACC_THREADS;
       if (c >= TDP_G && c < TDP_G * (1 + TDP_NF)) {
         double v = 0.0;
         for (int t = 0; t < TDP_ACC_THREADS; ++t) v += __longlong_as_double((i64)row[t]);
-        out[c] = (u64)__double_as_longlong(v);
+        out[(i64)c * gridDim.x] = (u64)__double_as_longlong(v);
       } else {
         u64 v = 0;
         for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];
-        out[c] = v;
+        out[(i64)c * gridDim.x] = v;
       }
     }
 #endif

@@ -325,8 +325,13 @@ def _materialize(v) -> torch.Tensor:
 
 def _scan_aggregate(exprs_keys: Sequence[Expr], spans: Sequence[tuple[int, int]],
                     aggs: Sequence[tuple[int, Optional[Expr]]], sel: Optional[Selection],
-                    n: int, device) -> tuple[torch.Tensor, torch.Tensor, int]:
-    """Run tdp_scan_aggregate; returns (counts[G], sums_raw[naggs, G] int64 bits, G)."""
+                    n: int, device, avg_mask: Optional[int] = None):
+    """Run tdp_scan_aggregate; returns (counts[G], sums_raw[naggs, G] int64 bits, G).
+
+    With ``avg_mask`` (an unsharded group-by) the finalisation runs in the
+    same native call (tdp_scan_aggregate_grouped) and the result is
+    ``(out_keys[nkeys, G], out_counts[G], out_aggs[naggs, G], out_groups[1])``
+    in tdp_groupby_finalize's layout."""
     prog = Program()
     keys = [nat.Key(prog.value(e), 0, lo, span) for e, (lo, span) in zip(exprs_keys, spans)]
     agg_structs = []
@@ -351,6 +356,22 @@ def _scan_aggregate(exprs_keys: Sequence[Expr], spans: Sequence[tuple[int, int]]
     hook = PROFILE_HOOK
     if hook is not None:
         hook.begin("tdp_scan_aggregate", n)
+    if avg_mask is not None:
+        nk = max(1, len(keys))
+        fin = torch.empty((nk + 1 + na) * slots + 1, dtype=torch.int64, device=device)
+        out_keys = fin[:nk * slots].view(nk, slots)
+        out_counts = fin[nk * slots:(nk + 1) * slots]
+        out_aggs = fin[(nk + 1) * slots:(nk + 1 + na) * slots].view(na, slots)
+        out_groups = fin[(nk + 1 + na) * slots:]
+        nat.call("tdp_scan_aggregate_grouped", prog.native_columns(), len(prog.cols), n, preds,
+                 npreds, prog.native_instrs(), len(prog.instrs), nat.struct_array(nat.Key, keys),
+                 len(keys), nat.struct_array(nat.Agg, agg_structs), len(agg_structs),
+                 nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel() * 8, avg_mask,
+                 nat.ptr(out_keys), nat.ptr(out_counts), nat.ptr(out_aggs), nat.ptr(out_groups),
+                 nat.stream())
+        if hook is not None:
+            hook.end("tdp_scan_aggregate")
+        return out_keys, out_counts, out_aggs, out_groups
     nat.call("tdp_scan_aggregate", prog.native_columns(), len(prog.cols), n, preds, npreds,
              prog.native_instrs(), len(prog.instrs), nat.struct_array(nat.Key, keys), len(keys),
              nat.struct_array(nat.Agg, agg_structs), len(agg_structs), nat.ptr(counts),
@@ -543,16 +564,26 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
     for (func, dt), v in zip(agg_specs, agg_vals):
         kind = _agg_kind(func, dt)
         agg_exprs.append((kind, as_expr(v)[0] if v is not None else None))
-    counts, sums, slots = _scan_aggregate(kexprs, spans, agg_exprs, sel, n, device)
-    allreduce_partials(counts, sums, [a for a, (k, _) in enumerate(agg_exprs)
-                                      if k == nat.AGG_SUM_F64], current_group())
     avg_mask = 0
     for a, (func, _) in enumerate(agg_specs):
         if func == "avg":
             avg_mask |= 1 << a
-    kinds = [k for k, _ in agg_exprs]
-    out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask,
-                                                  device, defer_rows)
+    group = current_group()
+    if group is None or world_size(group) <= 1:  # scan + reduce + finalise in one call
+        out_keys, out_counts, out_aggs, out_groups = _scan_aggregate(
+            kexprs, spans, agg_exprs, sel, n, device, avg_mask=avg_mask)
+        if defer_rows:
+            g = DeferredCount(out_groups)
+        else:
+            g = int(out_groups.item())
+            out_keys, out_counts, out_aggs = out_keys[:, :g], out_counts[:g], out_aggs[:, :g]
+    else:
+        counts, sums, slots = _scan_aggregate(kexprs, spans, agg_exprs, sel, n, device)
+        allreduce_partials(counts, sums, [a for a, (k, _) in enumerate(agg_exprs)
+                                          if k == nat.AGG_SUM_F64], group)
+        kinds = [k for k, _ in agg_exprs]
+        out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask,
+                                                      device, defer_rows)
     key_values = [out_keys[j].contiguous() for j in range(len(keys))]
     agg_values = _agg_outputs(agg_specs, out_aggs, out_counts, already_avg=True)
     if defer_rows:

@@ -359,8 +359,10 @@ def _ours(args):
     if tf.exists():
         try:
             tj = json.loads(tf.read_text())
-            key = f"{args.query}_sf{args.sf:g}_n{world}" + ("_compact" if args.encoding == "compact" else "")
-            traffic = tj.get(key)
+            sfx = "_compact" if args.encoding == "compact" else ""
+            # weak scaling: every rank's launch scans one SF shard, as at N=1
+            traffic = tj.get(f"{args.query}_sf{args.sf:g}_n{world}{sfx}",
+                             tj.get(f"{args.query}_sf{args.sf:g}_n1{sfx}"))
         except Exception:
             traffic = None
     line = {

@@ -58,7 +58,7 @@ def test_cnn_image_query_matches_torch_reference(chunk_rows):
     ref_loss = torch.mean((counts - torch.from_numpy(target)) ** 2)
     ref_loss.backward()
     np.testing.assert_allclose(pred.numpy(), counts.detach().numpy(), rtol=1e-5)
-    np.testing.assert_allclose(float(loss.item()), float(ref_loss), rtol=1e-5)
+    np.testing.assert_allclose(float(loss.item()), float(ref_loss.detach()), rtol=1e-5)
     for g, p in zip(grads, ref_net.parameters()):
         np.testing.assert_allclose(g, p.grad.numpy(), rtol=1e-5, atol=1e-9)
 

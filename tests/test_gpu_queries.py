@@ -309,3 +309,42 @@ def test_order_by_limit_query_matches_oracle():
         order = np.argsort(-sums if desc else sums, kind="stable")[:lim]
         np.testing.assert_array_equal(res.columns[0].values.numpy(), keys[order])
         np.testing.assert_allclose(res.columns[1].values.numpy(), sums[order], rtol=1e-12)
+
+
+@pytest.mark.parametrize("limit", [0, 1, 5, 7, 50])
+def test_order_by_limit_edges(limit):
+    """LIMIT 0, LIMIT >= rows, ties and NaN keys through the SQL path (top-k
+    and full-sort paths must agree with the reference's stable order)."""
+    vals = np.array([3.0, np.nan, 1.0, 3.0, -0.0, 0.0, 2.0])
+    ids = np.arange(len(vals))
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["i", "v"], [tq.plain(tq.Tensor(ids)),
+                                                          tq.plain(tq.Tensor(vals))]))
+    for desc in (False, True):
+        sql = f"SELECT i, v FROM t ORDER BY v {'DESC ' if desc else ''}LIMIT {limit}"
+        res = wl.compile_sql(sql, cat, tq.UdfRegistry()).run(cat)
+        exp = orc.stable_order(vals, desc)[:max(0, limit)]
+        np.testing.assert_array_equal(res.columns[0].values.numpy(), ids[exp])
+
+
+def test_replay_with_compact_storage_and_fresh_tables():
+    """Graph replay over a compact table; a stream of fresh tables (the e2e
+    pattern) never replays a stale graph."""
+    from paper_2211_02753_b200 import compact as cp
+    from paper_2211_02753_b200 import replay
+
+    arrays = wl.lineitem_arrays(0.01, seed=8, rows=30_000)
+    cat = tq.Catalog()
+    cat.register("lineitem", cp.compact_table(wl.lineitem_table(arrays)))
+    q = wl.compile_sql(wl.Q1_SQL, cat, wl.q1_registry())
+    exp = otpch.q1(arrays)
+    for _ in range(4):
+        got = q.run(cat).column("count").values.numpy()
+        np.testing.assert_array_equal(got, exp["count"])
+    assert any(isinstance(e, replay._Replay) for e in q._replays.values())
+    for seed in range(3):
+        a2 = wl.lineitem_arrays(0.01, seed=20 + seed, rows=30_000)
+        c2 = tq.Catalog()
+        c2.register("lineitem", wl.lineitem_table(a2))
+        got = q.run(c2).column("sum_charge").values.numpy()
+        np.testing.assert_allclose(got, otpch.q1(a2)["sum_charge"], rtol=1e-9)

@@ -177,7 +177,7 @@ def _ours(args):
 
     import paper_2211_02753_b200 as tq
     from paper_2211_02753_b200 import _native, kernels as K, workloads as wl
-    from paper_2211_02753_b200.distributed import shard_bounds, sharded
+    from paper_2211_02753_b200.distributed import sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -26,7 +26,7 @@ from __future__ import annotations
 
 from ctypes import c_int32
 from dataclasses import dataclass
-from typing import Callable, Optional, Sequence, Union
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 import torch
@@ -37,7 +37,6 @@ from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, linear_keys,
 from .encodings import (
     DecodedArgmax,
     DecodedCodes,
-    DictionaryEncoding,
     EncodedTensor,
     EncodingError,
     OneHotValue,

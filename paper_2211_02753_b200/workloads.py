@@ -14,7 +14,7 @@ import numpy as np
 
 from .encodings import DictionaryEncoding, EncodedTensor, StringDictionary, plain, trusted
 from .kernels import UdfEntry, UdfRegistry
-from .storage import FLOAT, STRING, Catalog, table_from_columns, tensor_type
+from .storage import FLOAT, STRING, Catalog, table_from_columns
 from .tensor import Tensor, add, mul, sub, tensor
 
 # day numbers since 1970-01-01 (Appendix B)

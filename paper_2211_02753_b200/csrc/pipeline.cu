@@ -44,6 +44,16 @@ constexpr int kConsWarps = 8;               // consumer warps of the ring kernel
 constexpr i64 kStageBudget = 64 * 1024;     // max bytes of one ring stage
 constexpr i64 kRingBudget = 200 * 1024;     // bytes of shared memory for the ring
 constexpr i64 kTwoCtaBudget = 110 * 1024;   // ring + accumulators per CTA at 2 CTAs/SM
+// rows up to this many bytes prefer two CTAs per SM (env TDP_TWO_CTA_ROW_BYTES
+// overrides, for measurements)
+static i64 two_cta_row_bytes() {
+  static const i64 v = [] {
+    const char* e = getenv("TDP_TWO_CTA_ROW_BYTES");
+    return e ? (i64)atoll(e) : (i64)32;
+  }();
+  return v;
+}
+#define kTwoCtaRowBytes two_cta_row_bytes()
 constexpr i64 kMaxSmemCells = 48;           // shared-memory accumulator mode limit
 constexpr int kAccThreads = 256;            // accumulator columns (TDP_ACC_THREADS)
 
@@ -371,7 +381,7 @@ Ring ring_shape(const Spec& s) {
   // the limit: then prefer two CTAs per SM (twice the consumer warps to hide
   // FP64 / shared-memory latency) over a deeper ring, when two fit.
   const i64 half = kTwoCtaBudget - s.acc_smem;
-  if (row_bytes <= 24 && half >= 2 * r.stage_bytes) st = half / r.stage_bytes;
+  if (row_bytes <= kTwoCtaRowBytes && half >= 2 * r.stage_bytes) st = half / r.stage_bytes;
   r.stages = (int)(st < 2 ? 2 : (st > 8 ? 8 : st));
   return r;
 }

@@ -306,6 +306,22 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
                       const int32_t* agg_kinds, int32_t naggs, int64_t* out_counts,
                       void* out_sums, void* stream);
 
+/* Hash group-by over one int64 key (groupby_exact general path, tq/kernels.py
+ * :108-167, for key ranges too wide for dense slots).  prepare: one pass
+ * hashes every key into an open-addressing table and accumulates counts and
+ * sums with warp-combined global atomics, then compacts the occupied slots;
+ * out_ngroups (device int64) = distinct keys m.  emit (same workspace, m from
+ * the host): stable radix sort of the m distinct keys, then out_keys[m],
+ * out_counts[m] and out_sums[naggs][m] in ascending key order (8-byte values
+ * as tdp_groupby_codes: double / int64 sums, the count for COUNT).        */
+size_t tdp_groupby_hash_workspace(int64_t n, int32_t naggs);
+int tdp_groupby_hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
+                             const int32_t* agg_kinds, int32_t naggs, int64_t* out_ngroups,
+                             void* ws, size_t ws_bytes, void* stream);
+int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, int64_t m,
+                          int64_t* out_keys, int64_t* out_counts, void* out_sums, void* ws,
+                          size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* equi-join (builder-defined; the reference has none)       */
 /* ------------------------------------------------------------------------ */

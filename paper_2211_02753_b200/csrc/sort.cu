@@ -21,6 +21,8 @@
 // small range sort in 3-4 passes.
 #include <vector>
 
+#include <cstring>
+
 #include "tdp_common.cuh"
 
 namespace tdp {
@@ -1143,3 +1145,238 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// hash group-by for one high-cardinality int64 key (groupby_exact's general
+// path, tq/kernels.py:108-167, when the key range is too wide for dense
+// slots).  prepare: one pass inserts every row's key into an open-addressing
+// table (CAS on the key image, INT64_MIN in a side slot) and adds its count /
+// sums into the slot's accumulators with global atomics -- lanes of a warp
+// holding the same key are combined first (__match_any_sync + shuffle sums),
+// so a hot key costs one atomic per warp; occupied slots are then compacted
+// into (key image, slot) pairs and counted.  emit: a stable radix sort of the
+// m distinct keys (not of the n rows) and a gather of the accumulators, so
+// groups come out in ascending key order as np.unique orders them.
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+struct HashAgg {
+  u64* slot;     // [cap + 1]  key image (0 = empty); [cap] = side slot for INT64_MIN
+  u64* cnt;      // [cap + 1]
+  u64* acc;      // [naggs][cap + 1]  (double bits for SUM_F64, u64 for SUM_I64)
+  i64* flags;    // [cap + 1]
+  i64* offs;     // [cap + 1]
+  void* scan_ws;
+  size_t scan_bytes;
+  u64 mask;
+  i64 cap;       // power of two
+};
+
+size_t hashagg_ws_bytes(i64 n, int naggs) {
+  const i64 cap = (i64)table_capacity(n);
+  const size_t per = (size_t)(cap + 1) * 8;
+  return sort_ws_bytes(n) + align256(per) * (4 + (size_t)(naggs > 0 ? naggs : 0)) +
+         exclusive_scan_workspace(cap + 1) + 1024;
+}
+
+HashAgg carve_hashagg(void* ws, i64 n, int naggs) {
+  HashAgg h;
+  h.cap = (i64)table_capacity(n);
+  h.mask = (u64)h.cap - 1;
+  const size_t per = align256((size_t)(h.cap + 1) * 8);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n);
+  h.slot = (u64*)p;
+  p += per;
+  h.cnt = (u64*)p;
+  p += per;
+  h.flags = (i64*)p;
+  p += per;
+  h.offs = (i64*)p;
+  p += per;
+  h.acc = (u64*)p;
+  p += per * (naggs > 0 ? naggs : 0);
+  h.scan_ws = p;
+  h.scan_bytes = exclusive_scan_workspace(h.cap + 1) + 512;
+  return h;
+}
+
+template <class V>
+__device__ __forceinline__ V group_sum(V v, unsigned peers, int lane) {
+  // sum of v over the lanes in `peers` (lanes holding the same key): lane
+  // order within the group is fixed (ascending), so the result is reproducible
+  V total = 0;
+  unsigned m = peers;
+  while (m) {
+    const int src = __ffs(m) - 1;
+    total += __shfl_sync(peers, v, src);
+    m &= m - 1;
+  }
+  (void)lane;
+  return total;
+}
+
+__global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, ValSet vs) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const i64 i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
+    const i64 k = keys[i];
+    const unsigned peers = __match_any_sync(active, k);
+    const int leader = __ffs(peers) - 1;
+    // the leader finds (or inserts) the key's slot
+    i64 slot = 0;
+    if (lane == leader) {
+      const u64 img = (u64)k ^ 0x8000000000000000ull;
+      if (img == 0ull) {
+        slot = h.cap;
+      } else {
+        u64 s = join_hash(k) & h.mask;
+        for (;;) {
+          const unsigned long long prev =
+              atomicCAS(reinterpret_cast<unsigned long long*>(h.slot + s), 0ull,
+                        (unsigned long long)img);
+          if (prev == 0ull || prev == img) break;
+          s = (s + 1) & h.mask;
+        }
+        slot = (i64)s;
+      }
+    }
+    slot = __shfl_sync(peers, slot, leader);
+    const unsigned long long c = (unsigned long long)__popc(peers);
+    if (lane == leader) atomicAdd(reinterpret_cast<unsigned long long*>(h.cnt + slot), c);
+    for (int a = 0; a < vs.naggs; ++a) {
+      if (vs.kind[a] == TDP_AGG_COUNT) continue;
+      u64* dst = h.acc + (i64)a * (h.cap + 1) + slot;
+      if (vs.kind[a] == TDP_AGG_SUM_F64) {
+        const double v = group_sum(load_as_f64(vs.p[a], vs.dt[a], i), peers, lane);
+        if (lane == leader) atomicAdd(reinterpret_cast<double*>(dst), v);
+      } else {
+        const unsigned long long v =
+            group_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i), peers, lane);
+        if (lane == leader) atomicAdd(reinterpret_cast<unsigned long long*>(dst), v);
+      }
+    }
+  }
+}
+
+__global__ void hashagg_flags_kernel(HashAgg h) {
+  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s <= h.cap;
+       s += (i64)gridDim.x * blockDim.x)
+    h.flags[s] = s < h.cap ? (h.slot[s] != 0ull) : (h.cnt[h.cap] != 0ull);
+}
+
+__global__ void hashagg_compact_kernel(HashAgg h, u64* __restrict__ out_img,
+                                       i64* __restrict__ out_slot) {
+  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s <= h.cap;
+       s += (i64)gridDim.x * blockDim.x) {
+    if (!h.flags[s]) continue;
+    const i64 o = h.offs[s];
+    out_img[o] = s < h.cap ? h.slot[s] : 0ull;  // key images sort like the keys
+    out_slot[o] = s;
+  }
+}
+
+__global__ void hashagg_gather_kernel(HashAgg h, const u64* __restrict__ img,
+                                      const i64* __restrict__ slot, i64 m, ValSet vs,
+                                      i64* __restrict__ out_keys, i64* __restrict__ out_counts,
+                                      u64* __restrict__ out_sums) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (i64)gridDim.x * blockDim.x) {
+    const i64 s = slot[i];
+    out_keys[i] = (i64)(img[i] ^ 0x8000000000000000ull);
+    const u64 c = h.cnt[s];
+    out_counts[i] = (i64)c;
+    for (int a = 0; a < vs.naggs; ++a)
+      out_sums[(i64)a * m + i] = vs.kind[a] == TDP_AGG_COUNT ? c : h.acc[(i64)a * (h.cap + 1) + s];
+  }
+}
+
+int make_valset(const tdp_column* vals, const int32_t* agg_kinds, int32_t naggs, i64 n,
+                ValSet* vs) {
+  TDP_REQUIRE(naggs >= 0 && naggs <= 32, "at most 32 aggregates");
+  std::memset(vs, 0, sizeof(*vs));
+  vs->naggs = naggs;
+  for (int a = 0; a < naggs; ++a) {
+    vs->kind[a] = agg_kinds[a];
+    TDP_REQUIRE(agg_kinds[a] >= TDP_AGG_COUNT && agg_kinds[a] <= TDP_AGG_SUM_I64,
+                "agg %d: bad kind", a);
+    if (agg_kinds[a] == TDP_AGG_COUNT) {
+      vs->dt[a] = TDP_I64;
+      continue;
+    }
+    TDP_REQUIRE(vals != nullptr && vals[a].rows >= n && vals[a].width == 1,
+                "agg %d: value column must be scalar with >= n rows", a);
+    vs->p[a] = vals[a].data;
+    vs->dt[a] = vals[a].dtype;
+  }
+  return TDP_OK;
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_groupby_hash_workspace(int64_t n, int32_t naggs) { return hashagg_ws_bytes(n, naggs); }
+
+int tdp_groupby_hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
+                             const int32_t* agg_kinds, int32_t naggs, int64_t* out_ngroups,
+                             void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n >= 0 && out_ngroups != nullptr, "bad hash group-by arguments");
+  TDP_REQUIRE(ws_bytes >= hashagg_ws_bytes(n, naggs), "hash group-by workspace too small");
+  ValSet vs;
+  int rc = make_valset(vals, agg_kinds, naggs, n, &vs);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_ngroups, 0, 8, st));
+    return TDP_OK;
+  }
+  HashAgg h = carve_hashagg(ws, n, naggs);
+  const size_t per = (size_t)(h.cap + 1) * 8;
+  TDP_CUDA_TRY(cudaMemsetAsync(h.slot, 0, per, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(h.cnt, 0, per, st));
+  for (int a = 0; a < naggs; ++a)
+    TDP_CUDA_TRY(cudaMemsetAsync(h.acc + (i64)a * (h.cap + 1), 0, per, st));
+  hashagg_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(keys, n, h, vs);
+  TDP_LAUNCH_CHECK("hashagg_kernel");
+  hashagg_flags_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h);
+  TDP_LAUNCH_CHECK("hashagg_flags_kernel");
+  rc = exclusive_scan_i64(h.flags, h.offs, h.cap + 1, out_ngroups, h.scan_ws, h.scan_bytes, st);
+  if (rc) return rc;
+  SortBuffers b = carve(ws, n);
+  hashagg_compact_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h, b.k0, b.i0);
+  TDP_LAUNCH_CHECK("hashagg_compact_kernel");
+  return TDP_OK;
+}
+
+int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, int64_t m,
+                          int64_t* out_keys, int64_t* out_counts, void* out_sums, void* ws,
+                          size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(m >= 0 && m <= (n > 0 ? n : 0), "bad group count");
+  TDP_REQUIRE(ws_bytes >= hashagg_ws_bytes(n, naggs), "hash group-by workspace too small");
+  if (m == 0) return TDP_OK;
+  ValSet vs;
+  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  if (rc) return rc;
+  vs.naggs = naggs;
+  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
+  cudaStream_t st = as_stream(stream);
+  HashAgg h = carve_hashagg(ws, n, naggs);
+  SortBuffers b = carve(ws, n);
+  u64* sk;
+  i64* order;
+  rc = radix_sort(b, m, st, &sk, &order);
+  if (rc) return rc;
+  hashagg_gather_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(
+      h, sk, order, m, vs, out_keys, out_counts, reinterpret_cast<u64*>(out_sums));
+  TDP_LAUNCH_CHECK("hashagg_gather_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"
+

@@ -713,11 +713,47 @@ def _groupby_sharded(kdata, agg_specs, vdata, group):
     return gather_many(kv, o), gather_many(av, o)
 
 
+HASH_GROUPBY_MIN_ROWS = 1 << 16
+
+
+def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
+    """One int64 key, hash aggregation (tdp_groupby_hash_*): a pass over the
+    rows instead of a sort of them; only the distinct keys are sorted."""
+    kinds = [_agg_kind(f, dt) for f, dt in agg_specs]
+    vals = []
+    for (func, dt), v, kind in zip(agg_specs, agg_vals, kinds):
+        if kind == nat.AGG_COUNT:
+            vals.append(None)
+            continue
+        t = _materialize(v)
+        if t.dim() != 1 or t.shape[0] != n:
+            raise KernelError(f"{func} aggregate needs a value column of {n} rows")
+        vals.append(t.to(torch.int64) if t.dtype == torch.bool else t.contiguous())
+    cols = (nat.Column * max(1, len(vals)))()
+    for a, t in enumerate(vals):
+        cols[a] = nat.column(t) if t is not None else nat.Column(None, nat.I64, 0, 0, 1)
+    kind_arr = (c_int32 * max(1, len(kinds)))(*kinds)
+    key = key.contiguous()
+    ws = nat.workspace(nat.load().tdp_groupby_hash_workspace(n, len(kinds)), device)
+    ng = torch.empty(1, dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_hash_prepare", nat.ptr(key), n, cols, kind_arr, len(kinds),
+             nat.ptr(ng), nat.ptr(ws), ws.numel(), nat.stream())
+    m = int(ng.item())
+    keys_out = torch.empty(m, dtype=torch.int64, device=device)
+    counts = torch.empty(m, dtype=torch.int64, device=device)
+    sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_hash_emit", n, kind_arr, len(kinds), m, nat.ptr(keys_out),
+             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
+    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
+
+
 def _groupby_local(kdata, agg_specs, agg_vals):
     device = kdata[0].device
     n = int(kdata[0].shape[0])
     if n == 0:
         return _empty_groups(len(kdata), agg_specs, device)
+    if len(kdata) == 1 and kdata[0].dtype == torch.int64 and n >= HASH_GROUPBY_MIN_ROWS:
+        return _groupby_hash(kdata[0], agg_specs, agg_vals, n, device)
     uniqs, codes = zip(*[unique_inverse(k) for k in kdata])
     if len(kdata) == 1:
         group_codes, slots = codes[0], int(uniqs[0].numel())

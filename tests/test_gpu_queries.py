@@ -348,3 +348,28 @@ def test_replay_with_compact_storage_and_fresh_tables():
         c2.register("lineitem", wl.lineitem_table(a2))
         got = q.run(c2).column("sum_charge").values.numpy()
         np.testing.assert_allclose(got, otpch.q1(a2)["sum_charge"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("n,distinct", [(70_000, 50), (300_000, 120_000), (1_000_003, 5)])
+def test_hash_groupby_matches_oracle(n, distinct):
+    """High-cardinality int64 keys take the hash group-by (warp-combined
+    atomics, distinct keys sorted): keys ascending, exact counts and integer
+    (wrap-around) sums, float sums within 1e-12; INT64_MIN / MAX keys."""
+    from paper_2211_02753_b200.kernels import groupby_exact
+
+    rng = np.random.default_rng(n)
+    pool = rng.integers(-10**15, 10**15, size=distinct)
+    pool[:2] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max][: len(pool[:2])]
+    key = pool[rng.integers(0, distinct, size=n)]
+    key[: n // 3] = pool[0]  # a hot key: whole warps share it
+    fv = rng.normal(size=n)
+    iv = rng.integers(-2**62, 2**62, size=n)
+    keys, aggs = groupby_exact([tq.plain(tq.Tensor(key))],
+                               [("count", None), ("sum", tq.Tensor(fv)), ("sum", tq.Tensor(iv)),
+                                ("avg", tq.Tensor(fv))])
+    ek, ea = orc.groupby_exact([key], [("count", None), ("sum", fv), ("sum", iv), ("avg", fv)])
+    np.testing.assert_array_equal(keys[0].cpu().numpy(), ek[0])
+    np.testing.assert_array_equal(aggs[0].cpu().numpy(), ea[0])
+    np.testing.assert_allclose(aggs[1].cpu().numpy(), ea[1], rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(aggs[2].cpu().numpy(), ea[2])
+    np.testing.assert_allclose(aggs[3].cpu().numpy(), ea[3], rtol=1e-9, atol=1e-12)

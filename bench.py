@@ -600,13 +600,17 @@ def _llp(args):
     losses = tq.train(q, cat, batches, TrainConfig(iterations=max(args.warmup, 3), lr=0.01))
     torch.cuda.synchronize()
     launches0 = _native.launch_count()
+    uuid = str(torch.cuda.get_device_properties(0).uuid)
+    sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     steps = max(1, min(args.steps, 20))
+    sampler.active = True
     t0.record()
     losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
     t1.record()
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0
     # exact swap of the trained query: pe_decode ->
@@ -648,7 +652,7 @@ def _llp(args):
                                f"(trainable), Linear({d},2) -> pe_encode, one_hot_pe bag, MSE, Adam",
                    "step": "one iteration of tq.train() (K iterations per call, losses read back at the end)",
                    "rows": n, "features": d, "bags": bags},
-        "gpu_launches": launches, "losses": losses[:3] + losses[-2:],
+        "gpu_launches": launches, "losses": losses[:3] + losses[-2:], "clocks": clocks,
         "cpu_baseline": {"value": cpu_s / m * n * 1e3, "unit": "ms/step (linear extrapolation)",
                          "cores": 1, "kind": "port",
                          "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "

@@ -658,6 +658,12 @@ def _llp(args):
                          "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
                                    f"reference tape), {reps} reps, extrapolated to {n} rows"},
         "bytes_floor_ms": 528 * n / _peaks()[0] / 1e9 * 1e3,
+        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
+                     "achieved": 528 * n / (ms / 1e3) / 1e9,
+                     "frac": 528 * n / (ms / 1e3) / 1e9 / _peaks()[0],
+                     "traffic": None,
+                     "what": "algorithmic bytes of the step (X read twice + bag codes twice, "
+                             "528 B/row, SURVEY §8(d)) over the whole step time"},
         "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
                        "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
                        "what": "q.swap_to_exact().run(cat): pe_decode + exact COUNT by (Bag, Pred); "
@@ -709,6 +715,11 @@ def _q3(args):
                    "orders": len(tables["orders"]["o_orderkey"]), "lineitem": nli,
                    "joined_rows": int(exp["joined_rows"])},
         "hbm_gbs_base_columns": base_bytes / (ms / 1e3) / 1e9, "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
+                     "achieved": base_bytes / (ms / 1e3) / 1e9,
+                     "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0], "traffic": None,
+                     "what": "base columns read once (SURVEY §8(d), 2.42 GB at SF10) over the "
+                             "whole pipeline time (host synchronisations included)"},
         "parity": "ok" if (got == exp["l_orderkey"]).all() else "MISMATCH",
         "cpu_baseline": {"value": nli / cpu_s, "unit": "lineitem rows/s", "cores": 1,
                          "kind": "port", "sample": f"full SF{args.sf:g}, oracle/tpch.py q3 once"},

@@ -48,6 +48,7 @@ def _args():
     ap.add_argument("--image-rows", type=int, default=10_000_000)
     ap.add_argument("--image-classes", type=int, default=10)
     ap.add_argument("--llp-rows", type=int, default=100_000_000)
+    ap.add_argument("--llp-features", type=int, default=64)
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -573,7 +574,7 @@ def _llp(args):
     from paper_2211_02753_b200.training import TrainConfig
 
     torch.cuda.set_device(0)
-    n, d, bags = args.llp_rows, 64, 1000
+    n, d, bags = args.llp_rows, args.llp_features, 1000
     g = torch.Generator(device="cuda").manual_seed(0)
     X = torch.randn(n, d, generator=g, device="cuda", dtype=torch.float32)
     bag = torch.randint(0, bags, (n,), generator=g, device="cuda", dtype=torch.int64)
@@ -657,13 +658,13 @@ def _llp(args):
                          "cores": 1, "kind": "port",
                          "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
                                    f"reference tape), {reps} reps, extrapolated to {n} rows"},
-        "bytes_floor_ms": 528 * n / _peaks()[0] / 1e9 * 1e3,
+        "bytes_floor_ms": (8 * d + 16) * n / _peaks()[0] / 1e9 * 1e3,
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
-                     "achieved": 528 * n / (ms / 1e3) / 1e9,
-                     "frac": 528 * n / (ms / 1e3) / 1e9 / _peaks()[0],
+                     "achieved": (8 * d + 16) * n / (ms / 1e3) / 1e9,
+                     "frac": (8 * d + 16) * n / (ms / 1e3) / 1e9 / _peaks()[0],
                      "traffic": None,
                      "what": "algorithmic bytes of the step (X read twice + bag codes twice, "
-                             "528 B/row, SURVEY §8(d)) over the whole step time"},
+                             "2 (4d + 8) B/row = 528 at d=64, SURVEY §8(d)) over the step time"},
         "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
                        "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
                        "what": "q.swap_to_exact().run(cat): pe_decode + exact COUNT by (Bag, Pred); "

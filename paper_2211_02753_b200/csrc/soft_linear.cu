@@ -151,6 +151,110 @@ __device__ __forceinline__ void load_head(const T* __restrict__ W, const T* __re
   for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
 }
 
+// Feature ownership of a lane: contiguous (features lane*V .. lane*V+V-1,
+// d == 32 V, one vector load per row) or strided (features lane + 32 v, any
+// d <= 32 V that is a multiple of 4, masked): the strided layout serves
+// feature counts that are not a multiple of 32 with the same warp algorithms.
+template <bool kStrided, int V>
+__device__ __forceinline__ int feat(int lane, int v) {
+  return kStrided ? lane + 32 * v : lane * V + v;
+}
+
+template <class T, int K, int V, bool kStrided>
+__device__ __forceinline__ void load_head_l(const T* __restrict__ W, const T* __restrict__ bias,
+                                            int lane, int d, T (&w)[V][K], T (&bj)[K]) {
+  if (!kStrided) {
+    load_head<T, K, V>(W, bias, lane, w, bj);
+    return;
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int f = feat<kStrided, V>(lane, v);
+#pragma unroll
+    for (int j = 0; j < K; ++j) w[v][j] = f < d ? W[f * K + j] : T(0);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
+}
+
+template <class T, int V, bool kStrided>
+__device__ __forceinline__ void load_row_l(const T* __restrict__ sxrow, int lane, int d,
+                                           T (&x)[V]) {
+  if (!kStrided) {
+    VecLoad<T, V>::ld(sxrow + lane * V, x);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int f = lane + 32 * v;
+      x[v] = f < d ? sxrow[f] : T(0);
+    }
+  }
+}
+
+// Row dots of one 32-row group (see vec_row_dots, stream_ring.cuh): the
+// contiguous layout is exactly vec_row_dots; the strided one the same
+// butterfly transposition over the strided feature slices.
+template <class T, int K, int V, bool FULL, bool kStrided>
+__device__ __forceinline__ void row_dots(const T* __restrict__ sx, int g, i64 r0, i64 n, int d,
+                                         const T (&w)[V][K], int lane, T (&out)[K]) {
+  if constexpr (!kStrided) {
+    vec_row_dots<T, K, V, FULL>(sx, g, r0, n, w, lane, out);
+  } else {
+    constexpr int KC = K < DotChunk<T>::kc ? K : DotChunk<T>::kc;
+    const bool upper16 = (lane & 16) != 0;
+#pragma unroll
+    for (int j0 = 0; j0 < K; j0 += KC) {
+      T p[16][KC];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        T xa[V], xb[V];
+        if (FULL || r0 + g * 32 + r < n) load_row_l<T, V, true>(sx + (size_t)(g * 32 + r) * d, lane, d, xa);
+        else
+#pragma unroll
+          for (int v = 0; v < V; ++v) xa[v] = T(0);
+        if (FULL || r0 + g * 32 + r + 16 < n)
+          load_row_l<T, V, true>(sx + (size_t)(g * 32 + r + 16) * d, lane, d, xb);
+        else
+#pragma unroll
+          for (int v = 0; v < V; ++v) xb[v] = T(0);
+#pragma unroll
+        for (int jj = 0; jj < KC; ++jj) {
+          if (j0 + jj < K) {
+            T a = xa[0] * w[0][j0 + jj];
+            T b = xb[0] * w[0][j0 + jj];
+#pragma unroll
+            for (int v = 1; v < V; ++v) {
+              a += xa[v] * w[v][j0 + jj];
+              b += xb[v] * w[v][j0 + jj];
+            }
+            const T send = upper16 ? a : b;
+            const T keep = upper16 ? b : a;
+            p[r][jj] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int r = 0; r < o; ++r) {
+#pragma unroll
+          for (int jj = 0; jj < KC; ++jj) {
+            if (j0 + jj < K) {
+              const T send = upper ? p[r][jj] : p[r + o][jj];
+              const T keep = upper ? p[r + o][jj] : p[r][jj];
+              p[r][jj] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < KC; ++jj)
+        if (j0 + jj < K) out[j0 + jj] = p[0][jj];
+    }
+  }
+}
+
 // first maximum, NaN counting as the maximum (np.argmax, tdp_pe_argmax)
 template <class T, int K>
 __device__ __forceinline__ int argmax_row(const T (&p)[K]) {
@@ -173,15 +277,15 @@ __device__ __forceinline__ int argmax_row(const T (&p)[K]) {
 // tq/encodings.py:154-165, then an exact COUNT by the decoded keys): each row
 // adds 1 to the cell of argmax(P) instead of P to every cell; grid is then a
 // uint64 count grid.
-template <class T, int K, int V, bool kArgmax>
+template <class T, int K, int V, bool kArgmax, bool kStrided>
 __global__ void __launch_bounds__(kRingThreads)
-    soft_linear_count_fwd_kernel(const T* __restrict__ X, i64 n, int stages,
+    soft_linear_count_fwd_kernel(const T* __restrict__ X, i64 n, int d_rt, int stages,
                                  const T* __restrict__ W, const T* __restrict__ bias,
                                  OneHotKeys oh, int cells, double* __restrict__ grid) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) u64 full[4];
   __shared__ __align__(8) u64 empty[4];
-  constexpr int d = 32 * V;
+  const int d = kStrided ? d_rt : 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   unsigned* lo = reinterpret_cast<unsigned*>(ring + (size_t)stages * stage_bytes);
@@ -199,7 +303,7 @@ __global__ void __launch_bounds__(kRingThreads)
     if (lane == 0) ring_produce_codes<T>(X, oh, n, d, stages, stage_bytes, ring, full, empty);
   } else {
     T w[V][K], bj[K];
-    load_head<T, K, V>(W, bias, lane, w, bj);
+    load_head_l<T, K, V, kStrided>(W, bias, lane, d, w, bj);
     const i64 ntiles = (n + kVecRows - 1) / kVecRows;
     int s = 0;
     unsigned fph = 0;
@@ -215,10 +319,10 @@ __global__ void __launch_bounds__(kRingThreads)
       i64 base = 0;
       if (full_stage) {
         base = onehot_cell_stage(oh, sc, true, warp * 32 + lane, row);
-        vec_row_dots<T, K, V, true>(sx, warp, r0, n, w, lane, z);
+        row_dots<T, K, V, true, kStrided>(sx, warp, r0, n, d, w, lane, z);
         valid = true;
       } else if (r0 + warp * 32 < n) {
-        vec_row_dots<T, K, V, false>(sx, warp, r0, n, w, lane, z);
+        row_dots<T, K, V, false, kStrided>(sx, warp, r0, n, d, w, lane, z);
         valid = row < n;
         if (valid) base = onehot_cell(oh, row);
       }
@@ -258,16 +362,16 @@ __global__ void __launch_bounds__(kRingThreads)
 // the shared copy of the upstream grid gradient and publishes it in shared
 // memory; then every lane accumulates x[r, its features] * dZ[r, :] over the
 // group's 32 rows (features re-read from the stage, released afterwards).
-template <class T, int K, int V>
+template <class T, int K, int V, bool kStrided>
 __global__ void __launch_bounds__(kRingThreads)
-    soft_linear_count_bwd_kernel(const T* __restrict__ X, i64 n, int stages,
+    soft_linear_count_bwd_kernel(const T* __restrict__ X, i64 n, int d_rt, int stages,
                                  const T* __restrict__ W, const T* __restrict__ bias,
                                  OneHotKeys oh, int cells, const double* __restrict__ G,
                                  double* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) u64 full[4];
   __shared__ __align__(8) u64 empty[4];
-  constexpr int d = 32 * V;
+  const int d = kStrided ? d_rt : 32 * V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   T* sG = reinterpret_cast<T*>(ring + (size_t)stages * stage_bytes);
@@ -286,7 +390,7 @@ __global__ void __launch_bounds__(kRingThreads)
     return;
   }
   T w[V][K], bj[K];
-  load_head<T, K, V>(W, bias, lane, w, bj);
+  load_head_l<T, K, V, kStrided>(W, bias, lane, d, w, bj);
   T* mydz = sdz + warp * 32 * K;
   double acc[V][K];
   double bacc[K];
@@ -312,10 +416,10 @@ __global__ void __launch_bounds__(kRingThreads)
     i64 base = 0;
     if (full_stage) base = onehot_cell_stage(oh, sc, true, warp * 32 + lane, row);
     if (full_stage) {
-      vec_row_dots<T, K, V, true>(sx, warp, r0, n, w, lane, z);
+      row_dots<T, K, V, true, kStrided>(sx, warp, r0, n, d, w, lane, z);
       valid = true;
     } else if (active) {
-      vec_row_dots<T, K, V, false>(sx, warp, r0, n, w, lane, z);
+      row_dots<T, K, V, false, kStrided>(sx, warp, r0, n, d, w, lane, z);
       valid = row < n;
     }
     if (active) {
@@ -354,7 +458,7 @@ __global__ void __launch_bounds__(kRingThreads)
       for (int r = 0; r < 32; ++r) {
         if (full_stage || r < nrow) {
           T x[V];
-          VecLoad<T, V>::ld(sx + (size_t)(warp * 32 + r) * d + lane * V, x);
+          load_row_l<T, V, kStrided>(sx + (size_t)(warp * 32 + r) * d, lane, d, x);
 #pragma unroll
           for (int j = 0; j < K; ++j) {
             const T dr = mydz[r * K + j];
@@ -378,9 +482,12 @@ __global__ void __launch_bounds__(kRingThreads)
   const int Wd = d * K + K;
   double* out = part + ((i64)blockIdx.x * kRingWarps + warp) * Wd;
 #pragma unroll
-  for (int v = 0; v < V; ++v)
+  for (int v = 0; v < V; ++v) {
+    const int f = feat<kStrided, V>(lane, v);
+    if (!kStrided || f < d)
 #pragma unroll
-    for (int j = 0; j < K; ++j) out[(lane * V + v) * K + j] = acc[v][j];
+      for (int j = 0; j < K; ++j) out[f * K + j] = acc[v][j];
+  }
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const double b = warp_sum(bacc[j]);
@@ -391,16 +498,47 @@ __global__ void __launch_bounds__(kRingThreads)
 // ---- host side ---------------------------------------------------------------
 
 struct Plan {
-  int V;
+  int V;          // features per lane (contiguous) or the strided VMAX
+  bool strided;
   int stages;
   size_t smem;
   int grid;
 };
 
+// Strided instantiations: VMAX 4 (d <= 128; two 256-row stages must also fit
+// shared memory, which bounds d to ~104 fp32 / ~52 fp64), within the
+// register budget of the backward (168 registers at 288 threads): fp32
+// k <= 4, fp64 k == 1.
+template <class T>
+constexpr bool strided_ok(int k, int vmax) {
+  return vmax == 4 && (sizeof(T) == 4 ? k <= 4 : k == 1);
+}
+
+// Contiguous layout for d = 32 or 64 (fp32) / 32 (fp64); strided for any
+// other d that is a multiple of 4 (bulk-copy granularity) up to 32 * VMAX.
+template <class T>
+bool plan_layout(const void* X, i64 n, int d, int k, int* V, bool* strided) {
+  const int vw = vec_width<T>(reinterpret_cast<const T*>(X), n, d);
+  if (vw >= 1 && vw <= 2 && (sizeof(T) == 4 || vw == 1)) {
+    *V = vw;
+    *strided = false;
+    return true;
+  }
+  if ((((uintptr_t)X) & 15) != 0 || n < (i64)kVecRows * 4 || d < 1 || d % 4 != 0) return false;
+  const int need = (d + 31) / 32;
+  const int vmax = 4;
+  if (need > vmax || !strided_ok<T>(k, vmax)) return false;
+  *V = vmax;
+  *strided = true;
+  return true;
+}
+
 template <class T>
 bool make_plan(const void* X, i64 n, int d, int k, i64 cells, bool bwd, int staged_keys, Plan* p) {
-  const int V = vec_width<T>(reinterpret_cast<const T*>(X), n, d);
-  if (V == 0 || V > 2 || k < 1 || k > kMaxK || cells < 1 || cells > kMaxCells) return false;
+  int V = 0;
+  bool strided = false;
+  if (!plan_layout<T>(X, n, d, k, &V, &strided)) return false;
+  if (k < 1 || k > kMaxK || cells < 1 || cells > kMaxCells) return false;
   const size_t stage = stage_size<T>(d, staged_keys);
   const size_t extra = bwd ? (size_t)((cells + 3) & ~3) * sizeof(T) +
                                  (size_t)kRingWarps * 32 * k * sizeof(T)
@@ -410,6 +548,7 @@ bool make_plan(const void* X, i64 n, int d, int k, i64 cells, bool bwd, int stag
   int st = (int)((budget - extra) / stage);
   st = st > 4 ? 4 : st;
   p->V = V;
+  p->strided = strided;
   p->stages = st;
   p->smem = (size_t)st * stage + extra;
   p->grid = stream_grid((n + kVecRows - 1) / kVecRows, 1, 1);
@@ -458,15 +597,16 @@ int launch_fwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
     return set_error(TDP_ENOTSUP, "soft_linear: unsupported shape (n=%lld d=%d k=%d cells=%lld)",
                      (long long)n, d, k, (long long)cells);
   bool launched = false;
-#define TDP_CASE(KK, VV)                                                                       \
-  if constexpr (sizeof(T) == 4 || VV == 1) if (k == KK && p.V == VV) {                                                                \
-    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_fwd_kernel<T, KK, VV, kArgmax>,        \
+#define TDP_CASE(KK, VV, SS)                                                                   \
+  if constexpr (SS ? strided_ok<T>(KK, VV) : (sizeof(T) == 4 || VV == 1))                      \
+  if (k == KK && p.V == VV && p.strided == SS) {                                               \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_fwd_kernel<T, KK, VV, kArgmax, SS>,    \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)); \
-    soft_linear_count_fwd_kernel<T, KK, VV, kArgmax><<<p.grid, kRingThreads, p.smem, st>>>(    \
-        (const T*)X, n, p.stages, (const T*)W, (const T*)b, oh, (int)cells, grid);             \
+    soft_linear_count_fwd_kernel<T, KK, VV, kArgmax, SS><<<p.grid, kRingThreads, p.smem, st>>>( \
+        (const T*)X, n, d, p.stages, (const T*)W, (const T*)b, oh, (int)cells, grid);          \
     launched = true;                                                                           \
   }
-#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2)
+#define TDP_CASES(KK) TDP_CASE(KK, 1, false) TDP_CASE(KK, 2, false) TDP_CASE(KK, 4, true)
   TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
 #undef TDP_CASES
 #undef TDP_CASE
@@ -490,15 +630,16 @@ int launch_bwd(const void* X, i64 n, int d, int k, const void* W, const void* b,
   TDP_REQUIRE(ws_bytes >= (size_t)prow * width * sizeof(double), "soft_linear: workspace too small");
   double* part = reinterpret_cast<double*>(ws);
   bool launched = false;
-#define TDP_CASE(KK, VV)                                                                       \
-  if constexpr (sizeof(T) == 4 || VV == 1) if (k == KK && p.V == VV) {                                                                \
-    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_bwd_kernel<T, KK, VV>,                 \
+#define TDP_CASE(KK, VV, SS)                                                                   \
+  if constexpr (SS ? strided_ok<T>(KK, VV) : (sizeof(T) == 4 || VV == 1))                      \
+  if (k == KK && p.V == VV && p.strided == SS) {                                               \
+    TDP_CUDA_TRY(cudaFuncSetAttribute(soft_linear_count_bwd_kernel<T, KK, VV, SS>,             \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem)); \
-    soft_linear_count_bwd_kernel<T, KK, VV><<<p.grid, kRingThreads, p.smem, st>>>(             \
-        (const T*)X, n, p.stages, (const T*)W, (const T*)b, oh, (int)cells, G, part);          \
+    soft_linear_count_bwd_kernel<T, KK, VV, SS><<<p.grid, kRingThreads, p.smem, st>>>(         \
+        (const T*)X, n, d, p.stages, (const T*)W, (const T*)b, oh, (int)cells, G, part);       \
     launched = true;                                                                           \
   }
-#define TDP_CASES(KK) TDP_CASE(KK, 1) TDP_CASE(KK, 2)
+#define TDP_CASES(KK) TDP_CASE(KK, 1, false) TDP_CASE(KK, 2, false) TDP_CASE(KK, 4, true)
   TDP_CASES(1) TDP_CASES(2) TDP_CASES(3) TDP_CASES(4) TDP_CASES(5) TDP_CASES(6) TDP_CASES(7) TDP_CASES(8)
 #undef TDP_CASES
 #undef TDP_CASE

@@ -83,7 +83,9 @@ def test_decimal_predicate_needs_integer_column_and_divisor(lib):
 def test_soft_linear_shape_limits(lib):
     assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 64, 2, 2000, c_void_p(256)) == 1
     assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 64, 2, 2000, c_void_p(260)) == 0  # X not 16-B aligned
-    assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 48, 2, 2000, c_void_p(256)) == 0  # d % 32
+    assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 48, 2, 2000, c_void_p(256)) == 1  # strided
+    assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 50, 2, 2000, c_void_p(256)) == 0  # d % 4
+    assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 200, 2, 2000, c_void_p(256)) == 0  # smem
     assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 64, 9, 2000, c_void_p(256)) == 0  # k > 8
     assert lib.tdp_soft_linear_supported(nat.F32, 100_000, 64, 2, 9000, c_void_p(256)) == 0  # cells
     keys = (nat.SoftKey * 2)()

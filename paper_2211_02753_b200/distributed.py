@@ -93,17 +93,31 @@ def allreduce_ranges(lo: torch.Tensor, hi: torch.Tensor, group) -> tuple[torch.T
 
 
 def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows: list[int],
-                       group) -> None:
+                       group, count_rows: tuple = ()) -> None:
     """In-place SUM of dense partial aggregates across ranks.
 
     ``counts``: int64 [slots].  ``sums_raw``: int64 [naggs, slots] holding the
     raw 8-byte results; rows listed in ``float_rows`` are float64 bit
-    patterns, the others int64 (counts / integer sums, wrap-around).
+    patterns, the others int64 (counts / integer sums, wrap-around).  When
+    every integer row is a count (``count_rows``), counts travel as float64
+    (exact: a row count is far below 2^53) in the same all-reduce as the float
+    sums -- one collective per query instead of two.
     """
     if world_size(group) <= 1:
         return
     nrows = sums_raw.shape[0]
     int_rows = [r for r in range(nrows) if r not in float_rows]
+    if all(r in count_rows for r in int_rows):
+        merged = torch.cat([counts.reshape(1, -1).to(torch.float64),
+                            sums_raw[int_rows].to(torch.float64),
+                            sums_raw[float_rows].view(torch.float64)], dim=0)
+        _all_reduce(merged, dist.ReduceOp.SUM, group)
+        counts.copy_(merged[0].round().to(torch.int64))
+        for j, r in enumerate(int_rows):
+            sums_raw[r].copy_(merged[1 + j].round().to(torch.int64))
+        for j, r in enumerate(float_rows):
+            sums_raw[r].copy_(merged[1 + len(int_rows) + j].view(torch.int64))
+        return
     ints = torch.cat([counts.reshape(1, -1), sums_raw[int_rows]], dim=0) if int_rows else counts.reshape(1, -1).clone()
     _all_reduce(ints, dist.ReduceOp.SUM, group)
     counts.copy_(ints[0])

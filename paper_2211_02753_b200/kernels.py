@@ -579,7 +579,8 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
     else:
         counts, sums, slots = _scan_aggregate(kexprs, spans, agg_exprs, sel, n, device)
         allreduce_partials(counts, sums, [a for a, (k, _) in enumerate(agg_exprs)
-                                          if k == nat.AGG_SUM_F64], group)
+                                          if k == nat.AGG_SUM_F64], group,
+                           tuple(a for a, (k, _) in enumerate(agg_exprs) if k == nat.AGG_COUNT))
         kinds = [k for k, _ in agg_exprs]
         out_keys, out_counts, out_aggs, g = _finalize(counts, sums, slots, spans, kinds, avg_mask,
                                                       device, defer_rows)
@@ -794,7 +795,8 @@ def global_aggregate(row_source: Sequence[EncodedTensor], agg_inputs) -> list[to
                  for f, v in agg_inputs]
         rows_dev, raw, _ = _scan_aggregate([], [], specs, sel, n, device)
         allreduce_partials(rows_dev, raw, [a for a, (k, _) in enumerate(specs)
-                                           if k == nat.AGG_SUM_F64], current_group())
+                                           if k == nat.AGG_SUM_F64], current_group(),
+                           tuple(a for a, (k, _) in enumerate(specs) if k == nat.AGG_COUNT))
     elif current_group() is not None:
         raise KernelError("sharded global aggregate needs its inputs in one row space")
     out = []

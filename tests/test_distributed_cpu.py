@@ -57,6 +57,10 @@ def _worker(rank, world, port, result):
     counts, fs, is_ = _dense_partials(k, f, i, lo, span)
     c_t = torch.from_numpy(counts)
     raw = torch.stack([torch.from_numpy(fs).view(torch.int64), torch.from_numpy(is_), c_t.clone()])
+    # merged path: count rows travel with the float sums in one all-reduce
+    c2 = torch.from_numpy(counts.copy())
+    raw2 = torch.stack([torch.from_numpy(fs.copy()).view(torch.int64), c2.clone()])
+    allreduce_partials(c2, raw2, [0], dist.group.WORLD, count_rows=(1,))
     allreduce_partials(c_t, raw, [0], dist.group.WORLD)
     if rank == 0:
         exp_c, exp_f, exp_i = _dense_partials(keys, vf, vi, keys.min(), keys.max() - keys.min() + 1)
@@ -64,7 +68,11 @@ def _worker(rank, world, port, result):
                         and np.array_equal(c_t.numpy(), exp_c)
                         and np.allclose(raw[0].view(torch.float64).numpy(), exp_f, rtol=1e-12)
                         and np.array_equal(raw[1].numpy(), exp_i)
-                        and np.array_equal(raw[2].numpy(), exp_c))
+                        and np.array_equal(raw[2].numpy(), exp_c)
+                        and np.array_equal(c2.numpy(), exp_c)
+                        and c2.dtype == torch.int64
+                        and np.array_equal(raw2[1].numpy(), exp_c)
+                        and np.allclose(raw2[0].view(torch.float64).numpy(), exp_f, rtol=1e-12))
     dist.destroy_process_group()
 
 

@@ -163,24 +163,24 @@ __device__ __forceinline__ int feat(int lane, int v) {
 template <class T, int K, int V, bool kStrided>
 __device__ __forceinline__ void load_head_l(const T* __restrict__ W, const T* __restrict__ bias,
                                             int lane, int d, T (&w)[V][K], T (&bj)[K]) {
-  if (!kStrided) {
+  if constexpr (!kStrided) {
     load_head<T, K, V>(W, bias, lane, w, bj);
-    return;
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int f = feat<kStrided, V>(lane, v);
+#pragma unroll
+      for (int j = 0; j < K; ++j) w[v][j] = f < d ? W[f * K + j] : T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
   }
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int f = feat<kStrided, V>(lane, v);
-#pragma unroll
-    for (int j = 0; j < K; ++j) w[v][j] = f < d ? W[f * K + j] : T(0);
-  }
-#pragma unroll
-  for (int j = 0; j < K; ++j) bj[j] = bias ? bias[j] : T(0);
 }
 
 template <class T, int V, bool kStrided>
 __device__ __forceinline__ void load_row_l(const T* __restrict__ sxrow, int lane, int d,
                                            T (&x)[V]) {
-  if (!kStrided) {
+  if constexpr (!kStrided) {
     VecLoad<T, V>::ld(sxrow + lane * V, x);
   } else {
 #pragma unroll
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kRingThreads)
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) u64 full[4];
   __shared__ __align__(8) u64 empty[4];
-  const int d = kStrided ? d_rt : 32 * V;
+  const int d = kStrided ? d_rt : 32 * V;  // a compile-time constant unless strided
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   unsigned* lo = reinterpret_cast<unsigned*>(ring + (size_t)stages * stage_bytes);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kRingThreads)
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) u64 full[4];
   __shared__ __align__(8) u64 empty[4];
-  const int d = kStrided ? d_rt : 32 * V;
+  const int d = kStrided ? d_rt : 32 * V;  // a compile-time constant unless strided
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t stage_bytes = stage_size<T>(d, oh.staged ? oh.n : 0);
   T* sG = reinterpret_cast<T*>(ring + (size_t)stages * stage_bytes);
@@ -458,7 +458,10 @@ __global__ void __launch_bounds__(kRingThreads)
       for (int r = 0; r < 32; ++r) {
         if (full_stage || r < nrow) {
           T x[V];
-          load_row_l<T, V, kStrided>(sx + (size_t)(warp * 32 + r) * d, lane, d, x);
+          if constexpr (kStrided)
+            load_row_l<T, V, true>(sx + (size_t)(warp * 32 + r) * d, lane, d, x);
+          else
+            VecLoad<T, V>::ld(sx + (size_t)(warp * 32 + r) * (32 * V) + lane * V, x);
 #pragma unroll
           for (int j = 0; j < K; ++j) {
             const T dr = mydz[r * K + j];

@@ -26,6 +26,7 @@ sizing its output) runs eagerly from then on.  ``TDP_REPLAY=0`` or
 from __future__ import annotations
 
 import os
+import threading
 import warnings
 import weakref
 from collections import OrderedDict
@@ -38,7 +39,7 @@ from .distributed import current_group, world_size
 from .encodings import EncodedTensor, trusted
 from .lazy import DeferredCount, LazyValue, PrefixRows, capturing, compact_source
 from .storage import table_from_columns
-from .tensor import Tensor
+from .tensor import Tensor, _cuda_available
 
 MAX_ENTRIES = 4
 MAX_RESULT_BYTES = 64 << 20  # larger results: the copy-out would dominate
@@ -68,7 +69,7 @@ def signature(q, catalog) -> Optional[tuple]:
     group = current_group()
     if group is not None and world_size(group) > 1:
         return None
-    if not torch.cuda.is_available() or torch.cuda.is_current_stream_capturing():
+    if not _cuda_available() or torch.cuda.is_current_stream_capturing():
         return None
     sig = [id(catalog), id(q.registry), len(q.registry.names()), torch.cuda.current_device()]
     tables = getattr(catalog, "_tables", None)
@@ -157,17 +158,32 @@ class _Template:
 
 
 class _Replay:
+    """A captured plan.  Replays are serialised: exact runs may come from
+    several threads on different streams (SPEC: read-only runs may proceed in
+    parallel), and every replay rewrites the graph's buffers, so a replay
+    first waits (on the device) for the previous replay's copy-out."""
+
     def __init__(self, graph, template: _Template, launches: int, hold):
         self.graph = graph
         self.template = template
         self.launches = launches
         self.hold = hold  # the catalog tables the signature names (ids stay unique)
+        self.lock = threading.Lock()
+        self.done: Optional[torch.cuda.Event] = None
 
     def __call__(self):
-        self.graph.replay()
-        if self.launches:
-            nat.load().tdp_count_graph_launches(self.launches)
-        return self.template.materialise()
+        with self.lock:
+            stream = torch.cuda.current_stream()
+            if self.done is not None:
+                stream.wait_event(self.done)
+            self.graph.replay()
+            if self.launches:
+                nat.load().tdp_count_graph_launches(self.launches)
+            table = self.template.materialise()
+            done = torch.cuda.Event()
+            done.record(stream)
+            self.done = done
+            return table
 
 
 def _inputs(q, catalog) -> tuple[set, list]:
@@ -217,9 +233,18 @@ class _Warm:
         return all(r() is t for r, t in zip(self.refs, tables))
 
 
+_LOCK = threading.Lock()  # the per-query replay tables
+
+
 def run(q, catalog, sig):
     """Replay for ``sig`` if captured (capturing it on the second sighting);
     None: run the program eagerly."""
+    with _LOCK:
+        ent = _lookup(q, catalog, sig)
+    return ent() if isinstance(ent, _Replay) else None
+
+
+def _lookup(q, catalog, sig):
     entries: OrderedDict = q._replays
     tables = [catalog._tables.get(name) for name in q._scan_tables]
     ent = entries.get(sig)
@@ -237,4 +262,4 @@ def run(q, catalog, sig):
         if ent == _NOGRAPH:
             return None
     entries.move_to_end(sig)
-    return ent()
+    return ent

@@ -112,3 +112,38 @@ def test_replay_off_switch():
     for _ in range(3):
         q.run(cat)
     assert not q._replays
+
+
+def test_concurrent_replays_from_threads_on_separate_streams():
+    """Exact runs may come from several threads (SPEC); replays of one graph
+    are serialised on the device, every result stays correct."""
+    import threading
+
+    arrays = wl.lineitem_arrays(0.01, seed=6, rows=200_000)
+    cat = tq.Catalog()
+    cat.register("lineitem", wl.lineitem_table(arrays))
+    q = wl.compile_sql(wl.Q1_SQL, cat, wl.q1_registry())
+    exp = otpch.q1(arrays)
+    for _ in range(3):
+        q.run(cat)
+    errors, results = [], []
+
+    def worker():
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                outs = [q.run(cat) for _ in range(25)]
+                stream.synchronize()
+                results.extend(o.column("sum_charge").values.numpy() for o in outs)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker) for _ in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(results) == 75
+    for r in results:
+        np.testing.assert_allclose(r, exp["sum_charge"], rtol=1e-9)

@@ -42,7 +42,16 @@ constexpr int kMaxRegCells = 64;
 constexpr i64 kMaxSlots = 1 << 20;
 constexpr int kConsWarps = 8;               // consumer warps of the ring kernel
 constexpr i64 kStageBudget = 64 * 1024;     // max bytes of one ring stage
-constexpr i64 kRingBudget = 200 * 1024;     // bytes of shared memory for the ring
+// bytes of shared memory for the ring + accumulators of one CTA
+// (env TDP_RING_BUDGET_KB overrides, for measurements)
+static i64 ring_budget() {
+  static const i64 v = [] {
+    const char* e = getenv("TDP_RING_BUDGET_KB");
+    return e ? (i64)atoll(e) * 1024 : (i64)200 * 1024;
+  }();
+  return v;
+}
+#define kRingBudget ring_budget()
 constexpr i64 kTwoCtaBudget = 110 * 1024;   // ring + accumulators per CTA at 2 CTAs/SM
 // rows up to this many bytes prefer two CTAs per SM (env TDP_TWO_CTA_ROW_BYTES
 // overrides, for measurements)

@@ -70,6 +70,8 @@ def decode_expr(stored: torch.Tensor, divisor: int) -> Expr:
     ``cast`` to int64, then for decimals the divide-free correctly rounded
     quotient by ``divisor`` (TDP_OP_DECIMAL)."""
     col = Expr("cast", "int64", (Expr("col", _NARROW_NAME[stored.dtype], col=stored),))
+    if divisor == 1:  # integer-valued floats: the conversion is exact
+        return Expr("cast", "float64", (col,))
     if divisor:
         return Expr("decimal", "float64", (col,), value=int(divisor))
     return col

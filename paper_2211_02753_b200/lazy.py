@@ -191,6 +191,10 @@ def compact_source(e: Expr) -> Optional[tuple[torch.Tensor, int]]:
     if e.op == "decimal" and e.args[0].op == "cast" and e.args[0].args[0].op == "col" \
             and e.args[0].args[0].dtype in NARROW_INTS:
         return e.args[0].args[0].col, int(e.value)
+    if e.op == "cast" and e.dtype == "float64" and e.args[0].op == "cast" \
+            and e.args[0].dtype == "int64" and e.args[0].args[0].op == "col" \
+            and e.args[0].args[0].dtype in NARROW_INTS:
+        return e.args[0].args[0].col, 1
     return None
 
 

@@ -38,7 +38,7 @@ from . import _native as nat
 from .distributed import current_group, world_size
 from .encodings import EncodedTensor, trusted
 from .lazy import DeferredCount, LazyValue, PrefixRows, capturing, compact_source
-from .storage import table_from_columns
+from .storage import Table, table_from_columns
 from .tensor import Tensor, _cuda_available
 
 MAX_ENTRIES = 4
@@ -94,67 +94,86 @@ def signature(q, catalog) -> Optional[tuple]:
 
 
 class _Template:
-    """Result table of a captured run and how to re-materialise it."""
+    """Result table of a captured run and how to re-materialise it: the pool
+    storages to copy out, and per result tensor a precomputed (storage,
+    dtype, size, stride, offset) so the fresh table is built from strided
+    views of the copies without re-deriving anything."""
 
-    def __init__(self, names, cols, storages, device):
-        self.names = names
-        self.cols = cols          # (kind, tensors..., encoding)
-        self.storages = storages  # data_ptr -> uint8 view of a pool storage
+    def __init__(self, schema, cols, storages, device, rows):
+        self.schema = schema
+        self.cols = cols          # ("t", spec, None, enc) | ("prefix", spec, count_spec, enc)
+        self.storages = storages  # key -> uint8 view of a pool storage
         self.device = device
+        self.rows = rows          # int row count of plain-tensor results, else None
 
     @staticmethod
     def build(table, inputs: set) -> Optional["_Template"]:
         cols, storages, total = [], {}, 0
 
-        def track(t: torch.Tensor) -> bool:
+        def track(t: torch.Tensor):
+            """Spec of ``t`` (None: too much to copy out)."""
             nonlocal total
             st = t.untyped_storage()
             key = st.data_ptr()
-            if key in inputs or key in storages:
-                return True
-            total += st.nbytes()
-            storages[key] = torch.empty(0, dtype=torch.uint8, device=t.device).set_(
-                st, 0, (st.nbytes(),), (1,))
-            return total <= MAX_RESULT_BYTES
+            if key in inputs:
+                return ("input", t)
+            if key not in storages:
+                total += st.nbytes()
+                if total > MAX_RESULT_BYTES or st.nbytes() % t.element_size():
+                    return None
+                storages[key] = torch.empty(0, dtype=torch.uint8, device=t.device).set_(
+                    st, 0, (st.nbytes(),), (1,))
+            return (key, t.dtype, tuple(t.size()), tuple(t.stride()), t.storage_offset())
 
+        rows = None
         for c in table.columns:
             v = c.values
             if v._t is not None:
-                if not track(v._t):
+                spec = track(v._t)
+                if spec is None:
                     return None
-                cols.append(("t", v._t, None, c.encoding))
+                cols.append(("t", spec, None, c.encoding))
+                rows = int(v._t.shape[0]) if v._t.dim() else None
             elif isinstance(v._lazy, PrefixRows) and isinstance(v._lazy.count, DeferredCount) \
                     and v._lazy.count.dev is not None:
-                full, dev = v._lazy.full, v._lazy.count.dev
-                if not (track(full) and track(dev)):
+                fs, ds = track(v._lazy.full), track(v._lazy.count.dev)
+                if fs is None or ds is None:
                     return None
-                cols.append(("prefix", full, dev, c.encoding))
+                cols.append(("prefix", fs, ds, c.encoding))
             else:
                 return None
-        return _Template(list(table.schema.names), cols, storages, table.device)
+        if any(kind == "prefix" for kind, *_ in cols):
+            rows = None
+        return _Template(table.schema, cols, storages, table.device, rows)
 
     def materialise(self):
         fresh = {k: src.clone() for k, src in self.storages.items()}
+        typed: dict = {}
 
-        def remap(t: torch.Tensor) -> torch.Tensor:
-            new = fresh.get(t.untyped_storage().data_ptr())
-            if new is None:  # a catalog buffer passed through
-                return t
-            return torch.empty(0, dtype=t.dtype, device=t.device).set_(
-                new.untyped_storage(), t.storage_offset(), t.size(), t.stride())
+        def view(spec) -> torch.Tensor:
+            if spec[0] == "input":  # a catalog buffer passed through
+                return spec[1]
+            key, dt, size, stride, off = spec
+            base = typed.get((key, dt))
+            if base is None:
+                base = fresh[key].view(dt)
+                typed[(key, dt)] = base
+            return base.as_strided(size, stride, off)
 
         cols = []
-        counts: dict = {}
+        count = None
         with trusted():
             for kind, a, b, enc in self.cols:
                 if kind == "t":
-                    cols.append(EncodedTensor(Tensor(remap(a)), enc))
+                    cols.append(EncodedTensor(Tensor(view(a)), enc))
                 else:
-                    key = (b.untyped_storage().data_ptr(), b.storage_offset())
-                    if key not in counts:  # one host slot per device count
-                        counts[key] = DeferredCount(remap(b))
-                    cols.append(EncodedTensor(Tensor(PrefixRows(remap(a), counts[key])), enc))
-        return table_from_columns(self.names, cols, device=self.device)
+                    if count is None or count[0] != b:  # one host slot per device count
+                        count = (b, DeferredCount(view(b)))
+                    cols.append(EncodedTensor(Tensor(PrefixRows(view(a), count[1])), enc))
+        if self.rows is None and count is None:
+            return table_from_columns(list(self.schema.names), cols, device=self.device)
+        return Table(self.schema, tuple(cols), count[1] if count is not None else self.rows,
+                     self.device)
 
 
 class _Replay:

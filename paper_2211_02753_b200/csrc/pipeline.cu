@@ -382,7 +382,11 @@ Ring ring_shape(const Spec& s) {
   if (row_bytes == 0) row_bytes = 1;
   r.pu = 4;
   const i64 budget = kRingBudget - s.acc_smem;
-  while (r.pu > 1 && (i64)kConsWarps * 32 * r.pu * row_bytes * 4 > budget) r.pu >>= 1;
+  static const i64 min_stages = [] {
+    const char* e = getenv("TDP_RING_MIN_STAGES");  // measurements only
+    return e ? (i64)atoll(e) : (i64)4;
+  }();
+  while (r.pu > 1 && (i64)kConsWarps * 32 * r.pu * row_bytes * min_stages > budget) r.pu >>= 1;
   r.ptile = kConsWarps * 32 * r.pu;
   r.stage_bytes = (i64)r.ptile * row_bytes;
   i64 st = (kRingBudget - s.acc_smem) / r.stage_bytes;

@@ -83,6 +83,41 @@ def _all_gather(parts: list, t: torch.Tensor, group) -> None:
         dist.all_gather(parts, t, group=group)
 
 
+class _AllReduceSum(torch.autograd.Function):
+    """Sum of per-rank partial grids across ranks, differentiable: everything
+    downstream (loss, its gradient) is computed from the reduced grid, so the
+    upstream gradient is the same on every rank and is also the gradient of
+    each rank's partial; the parameter gradients that result are per-rank
+    partial sums (reduced by the trainer, training.train_step)."""
+
+    @staticmethod
+    def forward(ctx, t: torch.Tensor, group) -> torch.Tensor:
+        out = t.detach().clone()
+        _all_reduce(out, dist.ReduceOp.SUM, group)
+        return out
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        return g, None
+
+
+def allreduce_sum(t: torch.Tensor, group) -> torch.Tensor:
+    """``t`` summed over the ranks of ``group`` (identity for one rank),
+    keeping the autograd graph (soft group-by grids of a sharded LLP step)."""
+    if world_size(group) <= 1:
+        return t
+    return _AllReduceSum.apply(t, group)
+
+
+def allreduce_grads(grads, group) -> None:
+    """In-place SUM of per-rank parameter gradients (data-parallel step)."""
+    if world_size(group) <= 1:
+        return
+    for g in grads:
+        if g is not None:
+            _all_reduce(g, dist.ReduceOp.SUM, group)
+
+
 def allreduce_ranges(lo: torch.Tensor, hi: torch.Tensor, group) -> tuple[torch.Tensor, torch.Tensor]:
     """Global [min, max] of per-rank key ranges (empty shards hold
     (INT64_MAX, INT64_MIN), the identities of MIN / MAX)."""

@@ -61,6 +61,7 @@ from .lazy import (
 )
 from .distributed import (
     allgather_rows,
+    allreduce_sum,
     allreduce_partials,
     allreduce_ranges,
     current_group,
@@ -898,6 +899,7 @@ def _soft_linear_count(pes: Sequence[EncodedTensor], spaces: tuple[int, ...]) ->
     with _grad_mode():
         grid = soft_linear_count(spec, pos, [c.contiguous() for c in codes], lin.x, lin.w, lin.b,
                                  torch_dtype(joint_dt))
+        grid = allreduce_sum(grid, current_group())  # row-sharded: global grid
         return _finish(grid.reshape(spaces))
 
 
@@ -942,6 +944,7 @@ def soft_groupby(pes: Sequence[EncodedTensor], agg: str = "count",
         joint_dt = np.promote_types(joint_dt, d).name
     with _grad_mode():
         grid = soft_groupby_grid(spec, keys, n, torch_dtype(joint_dt))
+        grid = allreduce_sum(grid, current_group())  # row-sharded: global grid
         counts = _finish(grid.reshape(spaces))
     if agg == "count":
         return GroupedCounts(spaces, counts)
@@ -955,6 +958,7 @@ def soft_groupby(pes: Sequence[EncodedTensor], agg: str = "count",
     with _grad_mode():
         wt = tape.input_for(w) if tape is not None else w.data
         weighted_grid = soft_groupby_grid(spec, keys, n, torch_dtype(wdt), values=wt.contiguous())
+        weighted_grid = allreduce_sum(weighted_grid, current_group())
         weighted = _finish(weighted_grid.reshape(spaces))
     if agg == "sum":
         return GroupedCounts(spaces, weighted)

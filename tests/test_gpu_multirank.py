@@ -52,8 +52,16 @@ def _worker(rank, world, port, result):
         res = q.run(cat)
     got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
     exp = otpch.q1(arrays)
-    ok &= np.array_equal(got["rf"], exp["rf"]) and np.array_equal(got["count"], exp["count"])
-    ok &= all(np.allclose(got[k], exp[k], rtol=1e-9) for k in ("sum_qty", "sum_charge", "avg_disc"))
+    _c = bool(np.array_equal(got["rf"], exp["rf"]) and np.array_equal(got["count"], exp["count"]))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 55 failed', file=sys.stderr, flush=True)
+    ok &= _c
+    _c = bool(all(np.allclose(got[k], exp[k], rtol=1e-9) for k in ("sum_qty", "sum_charge", "avg_disc")))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 56 failed', file=sys.stderr, flush=True)
+    ok &= _c
     # high-cardinality key: all-to-all repartition, local group-by, all-gather
     rng = np.random.default_rng(9)
     n = 50_001
@@ -68,8 +76,16 @@ def _worker(rank, world, port, result):
         r2 = q2.run(cat2)
     ek, ea = orc.groupby_exact([key], [("sum", val), ("count", None)])
     g2 = [c.values.numpy() for c in r2.columns]
-    ok &= np.array_equal(g2[0], ek[0]) and np.array_equal(g2[2], ea[1])
-    ok &= np.allclose(g2[1], ea[0], rtol=1e-9, atol=1e-12)
+    _c = bool(np.array_equal(g2[0], ek[0]) and np.array_equal(g2[2], ea[1]))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 71 failed', file=sys.stderr, flush=True)
+    ok &= _c
+    _c = bool(np.allclose(g2[1], ea[0], rtol=1e-9, atol=1e-12))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 72 failed', file=sys.stderr, flush=True)
+    ok &= _c
     # sharded equi-join: both sides repartitioned by key (all-to-all), local
     # join; the union of the ranks' pairs equals the single-process join
     from paper_2211_02753_b200.kernels import equi_join, filter_exact
@@ -94,7 +110,11 @@ def _worker(rank, world, port, result):
     epi, ebi = orc.join_inner(lk, rk[keep])
     exp = sorted(zip(lk[epi].tolist(), lv[epi].tolist(), rk[keep][ebi].tolist(),
                      rv[keep][ebi].tolist()))
-    ok &= got == exp and len(exp) > 0
+    _c = bool(got == exp and len(exp) > 0)
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 97 failed', file=sys.stderr, flush=True)
+    ok &= _c
     # the Q3-style pipeline on row-sharded customer / orders / lineitem:
     # local filters, key-repartitioned joins, repartitioned group-by, the
     # all-gathered groups ordered and limited on every rank
@@ -109,8 +129,57 @@ def _worker(rank, world, port, result):
         r3 = wl.Q3Plan(cat3).run(cat3)
     e3 = otpch.q3(tables)
     g3 = {n: c.values.numpy() for n, c in zip(r3.schema.names, r3.columns)}
-    ok &= np.array_equal(g3["l_orderkey"], e3["l_orderkey"])
-    ok &= np.allclose(g3["sum_rev"], e3["sum_rev"], rtol=1e-9)
+    _c = bool(np.array_equal(g3["l_orderkey"], e3["l_orderkey"]))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 112 failed', file=sys.stderr, flush=True)
+    ok &= _c
+    _c = bool(np.allclose(g3["sum_rev"], e3["sum_rev"], rtol=1e-9))
+    if not _c:
+        import sys
+        print(f'rank {rank}: check at line 113 failed', file=sys.stderr, flush=True)
+    ok &= _c
+    # data-parallel LLP training: row shards of X and bag codes, the soft
+    # count grid summed across ranks in the forward, the parameter gradients
+    # in the backward -> the same losses and weights as one process on all rows
+    from paper_2211_02753_b200.storage import tensor_type
+
+    def llp_losses(Xn, bagn, shard_ctx):
+        model = tq.Linear(64, 2, np.random.default_rng(0), name="lin")
+        bag_pe = tq.one_hot_pe(bagn, 40)
+        reg = tq.UdfRegistry()
+        reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(40)), ("Pred", tensor_type(2))), 1,
+                                 lambda c: (bag_pe, tq.pe_encode(model(c.values))),
+                                 model.parameters))
+        catl = tq.Catalog()
+        Xt = tq.Tensor(Xn)
+        catl.register_tensor(Xt, "T")
+        q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
+            "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"), catl, reg)),
+            tq.CompileConfig(trainable=True), reg)
+        target = tq.Tensor(np.linspace(0.0, 2000.0, 80))
+        with shard_ctx:
+            losses = tq.train(q, catl, [("T", Xt, target)], tq.TrainConfig(iterations=4, lr=0.05))
+        return losses, model.weight.value.numpy()
+
+    import contextlib
+
+    rng = np.random.default_rng(17)
+    N = 60_000
+    X = rng.normal(size=(N, 64)).astype(np.float32)
+    bag = rng.integers(0, 40, size=N)
+    a, b = shard_bounds(N, rank, world)
+    l_sh, w_sh = llp_losses(X[a:b], bag[a:b], sharded())
+    l_one, w_one = llp_losses(X, bag, contextlib.nullcontext())
+    llp_ok = np.allclose(l_sh, l_one, rtol=1e-5) and np.allclose(w_sh, w_one, rtol=1e-5, atol=1e-5)
+    if not llp_ok:
+        import sys
+        print(f"rank {rank} sharded LLP: losses {l_sh} vs {l_one}; "
+              f"max |dW| {np.max(np.abs(w_sh - w_one))}", file=sys.stderr, flush=True)
+    ok &= llp_ok
+    if not ok:
+        import sys
+        print(f"rank {rank}: checks failed", file=sys.stderr, flush=True)
     result[rank] = bool(ok)
     dist.destroy_process_group()
 

@@ -144,3 +144,31 @@ def test_shard_bounds_cover_rows():
             assert all(spans[r][1] == spans[r + 1][0] for r in range(w - 1))
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _grad_worker(rank, world, port, result):
+    """allreduce_sum: forward = sum of the ranks' partials, backward = the
+    upstream gradient on every rank; allreduce_grads sums the partials."""
+    from paper_2211_02753_b200.distributed import allreduce_grads, allreduce_sum
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64) * (rank + 1)
+    t.requires_grad_(True)
+    out = allreduce_sum(t, dist.group.WORLD)
+    w = torch.tensor([0.5, -1.0, 2.0], dtype=torch.float64)
+    (out * w).sum().backward()
+    g = [t.grad.clone()]
+    allreduce_grads(g, dist.group.WORLD)
+    if rank == 0:
+        result["ok"] = (torch.equal(out.detach(), torch.tensor([3.0, 6.0, 9.0], dtype=torch.float64))
+                        and torch.equal(t.grad, w) and torch.equal(g[0], 2 * w))
+    dist.destroy_process_group()
+
+
+def test_differentiable_allreduce_world2():
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_grad_worker, args=(2, _free_port(), result), nprocs=2, join=True)
+    assert result.get("ok") is True

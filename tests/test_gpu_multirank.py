@@ -177,6 +177,27 @@ def _worker(rank, world, port, result):
         print(f"rank {rank} sharded LLP: losses {l_sh} vs {l_one}; "
               f"max |dW| {np.max(np.abs(w_sh - w_one))}", file=sys.stderr, flush=True)
     ok &= llp_ok
+    # trainable global aggregates (GlobalAggSoftOp) over row shards
+    def scored(Xn, shard_ctx):
+        reg = tq.UdfRegistry()
+        wts = tq.Tensor(np.linspace(-1.0, 1.0, 64))
+        reg.register(tq.make_scoring_udf("scorer", wts, scale=8.0))
+        catl = tq.Catalog()
+        catl.register_tensor(tq.Tensor(Xn.astype(np.float64)), "T")
+        q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
+            "SELECT SUM(Score), AVG(Score), COUNT(*) FROM scorer(T)"), catl, reg)),
+            tq.CompileConfig(trainable=True), reg)
+        with shard_ctx:
+            r = q.run(catl)
+        return [float(c.values.numpy()[0]) for c in r.columns]
+
+    g_sh = scored(X[a:b], sharded())
+    g_one = scored(X, contextlib.nullcontext())
+    g_ok = np.allclose(g_sh, g_one, rtol=1e-9)
+    if not g_ok:
+        import sys
+        print(f"rank {rank} global soft aggregates {g_sh} vs {g_one}", file=sys.stderr, flush=True)
+    ok &= g_ok
     if not ok:
         import sys
         print(f"rank {rank}: checks failed", file=sys.stderr, flush=True)

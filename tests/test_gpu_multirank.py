@@ -177,6 +177,35 @@ def _worker(rank, world, port, result):
         print(f"rank {rank} sharded LLP: losses {l_sh} vs {l_one}; "
               f"max |dW| {np.max(np.abs(w_sh - w_one))}", file=sys.stderr, flush=True)
     ok &= llp_ok
+    # ORDER BY / LIMIT over a row-sharded relation: local top rows, gathered
+    # in rank order, ordered again == the global stable order
+    rng = np.random.default_rng(23)
+    nt = 30_001
+    kv = rng.integers(0, 500, size=nt).astype(np.float64)  # many ties
+    iv = np.arange(nt)
+    a2, b2 = shard_bounds(nt, rank, world)
+    cat4 = tq.Catalog()
+    cat4.register("t", tq.table_from_columns(["i", "v"], [tq.plain(tq.Tensor(iv[a2:b2])),
+                                                          tq.plain(tq.Tensor(kv[a2:b2]))]))
+    for sql, desc, lim in (("SELECT i, v FROM t ORDER BY v DESC LIMIT 25", True, 25),
+                           ("SELECT i, v FROM t ORDER BY v LIMIT 3000", False, 3000),
+                           ("SELECT i, v FROM t WHERE v > 100 ORDER BY v", False, None),
+                           ("SELECT i, v FROM t LIMIT 40", None, 40)):
+        q4 = wl.compile_sql(sql, cat4, tq.UdfRegistry())
+        with sharded():
+            r4 = q4.run(cat4)
+        got_i = r4.columns[0].values.numpy()
+        if desc is None:
+            exp_i = iv[:lim]
+        else:
+            keep = kv > 100 if "WHERE" in sql else np.ones(nt, dtype=bool)
+            order = orc.stable_order(kv[keep], desc)
+            exp_i = iv[keep][order][: lim if lim is not None else None]
+        c4 = bool(np.array_equal(got_i, exp_i))
+        if not c4:
+            import sys
+            print(f"rank {rank} sharded '{sql}' mismatch", file=sys.stderr, flush=True)
+        ok &= c4
     # trainable global aggregates (GlobalAggSoftOp) over row shards
     def scored(Xn, shard_ctx):
         reg = tq.UdfRegistry()

@@ -121,6 +121,21 @@ void tdp_count_graph_launches(uint64_t n);
 /* Read and clear the CUDA runtime error state of this library (after an
  * aborted graph capture); returns the cudaError_t that was pending.        */
 int tdp_clear_error(void);
+/* Replay guard (no reference counterpart: the reference re-plans every run).
+ * Enqueue a check that the `n` (<= 8) integers at device `got` (element size
+ * 4 or 8) equal `expected` (host array): a CUDA graph captured from a plan
+ * sized by host reads of those integers traps on a mismatch instead of
+ * overrunning buffers.                                                     */
+/* Replay log of host decisions the library takes from device data (the
+ * radix sort's skipped digit passes; thread-local).  mode 1 records them,
+ * mode 2 (inside a CUDA-graph capture) replays `values` instead of
+ * synchronising, each checked on the device; mode 0 is off.  end() copies a
+ * recorded log to `out` (capacity `cap`, >= size()) and turns logging off. */
+int tdp_replay_log_begin(int32_t mode, const int64_t* values, int64_t n);
+int64_t tdp_replay_log_size(void);
+int tdp_replay_log_end(int64_t* out, int64_t cap);
+int tdp_expect_values(const void* got, int32_t esize, int32_t n, const int64_t* expected,
+                      void* stream);
 /* Benchmark timer of the fused pipeline kernel: while enabled, CUDA events are
  * recorded on the launch stream immediately around every tdp_scan_agg launch
  * (after all host-side preparation).  read() waits for the recorded events,

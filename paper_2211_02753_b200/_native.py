@@ -81,6 +81,10 @@ _SIGNATURES = {
     "tdp_launch_count": (c_uint64, []),
     "tdp_count_graph_launches": (None, [c_uint64]),
     "tdp_clear_error": (c_int, []),
+    "tdp_expect_values": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "tdp_replay_log_begin": (c_int, [c_int32, c_void_p, c_int64]),
+    "tdp_replay_log_size": (c_int64, []),
+    "tdp_replay_log_end": (c_int, [c_void_p, c_int64]),
     "tdp_kernel_timer_enable": (c_int, [c_int32]),
     "tdp_kernel_timer_read": (c_int, [POINTER(c_double), POINTER(c_int64)]),
     "tdp_filter_mask": (c_int, [POINTER(Column), c_int32, POINTER(Predicate), c_int32, c_int64,

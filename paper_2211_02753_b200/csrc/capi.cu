@@ -1,6 +1,8 @@
 // Library-level C ABI: error strings, version, device properties, and the
 // host translation of predicate descriptors.
+#include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <mutex>
 #include <vector>
 
@@ -12,6 +14,18 @@ static thread_local std::string g_error;
 static std::atomic<unsigned long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local int g_replay_mode = 0;
+static thread_local std::vector<i64> g_replay_log;
+static thread_local size_t g_replay_pos = 0;
+
+int replay_mode() { return g_replay_mode; }
+void replay_push(i64 v) { g_replay_log.push_back(v); }
+bool replay_take(i64* v) {
+  if (g_replay_pos >= g_replay_log.size()) return false;
+  *v = g_replay_log[g_replay_pos++];
+  return true;
+}
 
 int set_error(int code, const char* fmt, ...) {
   char buf[1024];
@@ -82,9 +96,63 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
   return TDP_OK;
 }
 
+struct Expected {
+  i64 v[8];
+};
+
+// One thread per value: a replayed plan's device-computed integer must equal
+// the value its buffers were sized from; anything else aborts the replay.
+__global__ void expect_values_kernel(const void* got, int esize, int n, Expected e) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  const i64 v = esize == 8 ? reinterpret_cast<const i64*>(got)[i]
+                           : (i64) reinterpret_cast<const int*>(got)[i];
+  if (v != e.v[i]) {
+    printf("tdp: replayed plan read %lld where %lld was recorded (catalog changed behind "
+           "the replay signature)\n", (long long)v, (long long)e.v[i]);
+    __trap();
+  }
+}
+
 }  // namespace tdp
 
 extern "C" {
+
+int tdp_replay_log_begin(int32_t mode, const int64_t* values, int64_t n) {
+  TDP_REQUIRE(mode >= 0 && mode <= 2, "replay log mode must be 0, 1 or 2");
+  TDP_REQUIRE(n >= 0 && (n == 0 || values != nullptr), "bad replay log values");
+  tdp::g_replay_mode = mode;
+  tdp::g_replay_log.assign(values, values + (mode == 2 ? n : 0));
+  tdp::g_replay_pos = 0;
+  return TDP_OK;
+}
+
+int64_t tdp_replay_log_size(void) {
+  return tdp::g_replay_mode == 2 ? (int64_t)tdp::g_replay_pos : (int64_t)tdp::g_replay_log.size();
+}
+
+int tdp_replay_log_end(int64_t* out, int64_t cap) {
+  const int64_t n = (int64_t)tdp::g_replay_log.size();
+  TDP_REQUIRE(cap >= n || tdp::g_replay_mode == 2, "replay log output too small");
+  if (tdp::g_replay_mode == 1 && n) std::copy(tdp::g_replay_log.begin(), tdp::g_replay_log.end(), out);
+  tdp::g_replay_mode = 0;
+  tdp::g_replay_log.clear();
+  tdp::g_replay_pos = 0;
+  return TDP_OK;
+}
+
+int tdp_expect_values(const void* got, int32_t esize, int32_t n, const int64_t* expected,
+                      void* stream) {
+  TDP_REQUIRE(n >= 0 && n <= 8, "tdp_expect_values: at most 8 values (got %d)", n);
+  TDP_REQUIRE(esize == 4 || esize == 8, "tdp_expect_values: element size must be 4 or 8");
+  TDP_REQUIRE(n == 0 || (got != nullptr && expected != nullptr), "tdp_expect_values: null pointer");
+  if (n == 0) return TDP_OK;
+  tdp::Expected e;
+  for (int i = 0; i < 8; ++i) e.v[i] = i < n ? expected[i] : 0;
+  tdp::expect_values_kernel<<<1, 32, 0, tdp::as_stream(stream)>>>(got, esize, n, e);
+  TDP_LAUNCH_CHECK("expect_values_kernel");
+  return TDP_OK;
+}
 
 const char* tdp_last_error(void) { return tdp::last_error(); }
 

@@ -21,6 +21,7 @@
 // small range sort in 3-4 passes.
 #include <vector>
 
+#include <cstdio>
 #include <cstring>
 
 #include "tdp_common.cuh"
@@ -223,6 +224,23 @@ SortBuffers carve(void* ws, i64 n) {
   return b;
 }
 
+// A replayed sort skips the digit passes its recording run skipped: each of
+// them must still be constant (one bin holds all n keys), else trap.
+__global__ void sort_passes_check_kernel(const unsigned long long* __restrict__ hist, i64 n,
+                                         unsigned passes) {
+  __shared__ int constant[8];
+  if (threadIdx.x < 8) constant[threadIdx.x] = 0;
+  __syncthreads();
+  for (int d = 0; d < 8; ++d)
+    if (hist[d * 256 + threadIdx.x] == (unsigned long long)n) constant[d] = 1;
+  __syncthreads();
+  if (threadIdx.x < 8 && !((passes >> threadIdx.x) & 1u) && !constant[threadIdx.x]) {
+    printf("tdp: replayed radix sort skips digit %d, which is no longer constant\n",
+           (int)threadIdx.x);
+    __trap();
+  }
+}
+
 // Sorts the images in b.k0 / payload b.i0.  On return *keys/*idx point at the
 // buffer holding the sorted result.
 int radix_sort(SortBuffers& b, i64 n, cudaStream_t st, u64** keys, i64** idx) {
@@ -233,18 +251,32 @@ int radix_sort(SortBuffers& b, i64 n, cudaStream_t st, u64** keys, i64** idx) {
   TDP_CUDA_TRY(cudaMemsetAsync(b.hist, 0, 8 * 256 * 8, st));
   all_digit_hist_kernel<<<stream_grid(n, 256 * 16, 4), 256, 0, st>>>(b.k0, n, b.hist);
   TDP_LAUNCH_CHECK("all_digit_hist_kernel");
-  std::vector<unsigned long long> h(8 * 256);
-  TDP_CUDA_TRY(cudaMemcpyAsync(h.data(), b.hist, h.size() * 8, cudaMemcpyDeviceToHost, st));
-  TDP_CUDA_TRY(cudaStreamSynchronize(st));
+  // bit d set: digit d is not constant, pass d runs
+  unsigned passes = 0;
+  if (replay_mode() == 2) {  // graph capture: the recorded decision, checked on the device
+    i64 v;
+    TDP_REQUIRE(replay_take(&v), "radix sort: replay log exhausted");
+    passes = (unsigned)v;
+    sort_passes_check_kernel<<<1, 256, 0, st>>>(b.hist, n, passes);
+    TDP_LAUNCH_CHECK("sort_passes_check_kernel");
+  } else {
+    std::vector<unsigned long long> h(8 * 256);
+    TDP_CUDA_TRY(cudaMemcpyAsync(h.data(), b.hist, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    TDP_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int d = 0; d < 8; ++d) {
+      bool trivial = false;
+      for (int v = 0; v < 256; ++v)
+        if (h[d * 256 + v] == (unsigned long long)n) trivial = true;
+      if (!trivial) passes |= 1u << d;
+    }
+    if (replay_mode() == 1) replay_push((i64)passes);
+  }
   u64* kin = b.k0;
   u64* kout = b.k1;
   i64* iin = b.i0;
   i64* iout = b.i1;
   for (int d = 0; d < 8; ++d) {
-    bool trivial = false;
-    for (int v = 0; v < 256; ++v)
-      if (h[d * 256 + v] == (unsigned long long)n) trivial = true;
-    if (trivial) continue;
+    if (!((passes >> d) & 1u)) continue;
     const int shift = 8 * d;
     tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, ntiles, b.counts);
     TDP_LAUNCH_CHECK("tile_hist_kernel");
@@ -1030,8 +1062,8 @@ int join_prepare_mode(const int64_t* build_keys, int64_t n_build, const PredSet*
     TDP_CUDA_TRY(cudaMemcpyAsync(out_info + 1, j.ht.flags, sizeof(int), cudaMemcpyDeviceToDevice,
                                  st));
   } else {
-    const int one[2] = {1, 1};
-    TDP_CUDA_TRY(cudaMemcpyAsync(j.ht.flags, one, sizeof(one), cudaMemcpyHostToDevice, st));
+    // flags[0] (keys repeat), flags[1] (runs mode): nonzero, no host source
+    TDP_CUDA_TRY(cudaMemsetAsync(j.ht.flags, 1, 2 * sizeof(int), st));
     make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(
         build_keys, TDP_I64, 0, n_build, j.sb.k0, j.sb.i0);
     TDP_LAUNCH_CHECK("make_keys_kernel");

@@ -34,6 +34,14 @@ const char* last_error();
 // can report how many of their launches were ours.
 void count_launch();
 
+// Replay log of host decisions taken inside the library from device data
+// (the radix sort's skipped digit passes).  Mode 1 records every decision;
+// mode 2 (a CUDA-graph capture) takes them from the log instead of
+// synchronising -- the caller enqueues a device check of each.  Thread-local.
+int replay_mode();
+void replay_push(i64 v);
+bool replay_take(i64* v);
+
 #define TDP_LAUNCH_CHECK(name)                                                          \
   do {                                                                                  \
     cudaError_t _e = cudaGetLastError();                                                \

@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from .hostread import read_int, read_ints
 from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, linear_keys,
                        soft_groupby_grid, soft_linear_count, soft_linear_supported)
 from .encodings import (
@@ -401,7 +402,7 @@ def _finalize(counts, sums, slots, spans, aggs_kinds, avg_mask, device, defer_ro
              nat.ptr(out_groups), nat.stream())
     if defer_rows:  # padded [slots] outputs + the occupied count, read by the host later
         return out_keys, out_counts, out_aggs, DeferredCount(out_groups)
-    g = int(out_groups.item())
+    g = read_int(out_groups)
     return out_keys[:, :g], out_counts[:g], out_aggs[:, :g], g
 
 
@@ -544,7 +545,7 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
         if group is not None:
             lo, hi = allreduce_ranges(mm[0::2].contiguous(), mm[1::2].contiguous(), group)
             mm = torch.stack([lo, hi], dim=1).reshape(-1)
-        host = mm.tolist()
+        host = read_ints(mm)
         for t, j in enumerate(need_range):
             ranges[j] = (host[2 * t], host[2 * t + 1])
         if any(lo > hi for lo, hi in ranges.values()):
@@ -575,7 +576,7 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
         if defer_rows:
             g = DeferredCount(out_groups)
         else:
-            g = int(out_groups.item())
+            g = read_int(out_groups)
             out_keys, out_counts, out_aggs = out_keys[:, :g], out_counts[:g], out_aggs[:, :g]
     else:
         counts, sums, slots = _scan_aggregate(kexprs, spans, agg_exprs, sel, n, device)
@@ -630,7 +631,7 @@ def unique_inverse(key: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     ws = nat.workspace(lib.tdp_sort_workspace(n) + 2 * ((n * 8 + 255) // 256 * 256) + 1024, dev)
     nat.call("tdp_unique_inverse", nat.ptr(key), n, nat.ptr(uniques), nat.ptr(inverse),
              nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream())
-    u = int(count.item()) if n else 0
+    u = read_int(count) if n else 0
     return uniques[:u], inverse
 
 
@@ -740,7 +741,7 @@ def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
     ng = torch.empty(1, dtype=torch.int64, device=device)
     nat.call("tdp_groupby_hash_prepare", nat.ptr(key), n, cols, kind_arr, len(kinds),
              nat.ptr(ng), nat.ptr(ws), ws.numel(), nat.stream())
-    m = int(ng.item())
+    m = read_int(ng)
     keys_out = torch.empty(m, dtype=torch.int64, device=device)
     counts = torch.empty(m, dtype=torch.int64, device=device)
     sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
@@ -823,7 +824,7 @@ def global_aggregate(row_source: Sequence[EncodedTensor], agg_inputs) -> list[to
         else:
             mean = total.to(torch.float64) / cnt.to(torch.float64)
             # numpy: float32 mean stays float32; an empty input gives float64 NaN
-            if dt == "float32" and int(cnt.item()) > 0:
+            if dt == "float32" and read_int(cnt) > 0:
                 mean = mean.to(torch.float32)
             out.append(mean)
     return out
@@ -1125,13 +1126,13 @@ def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
     pc, npc, pp, npp = predset(probe_sel, n_probe, "probe")
     nat.call("tdp_join_prepare_ex", nat.ptr(bk), n_build, bc, nbc, bp, nbp, nat.ptr(pk), n_probe,
              pc, npc, pp, npp, 0, nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
-    m, repeated = info.tolist()
+    m, repeated = read_ints(info)
     if repeated:
         if nbp:
             return None
         nat.call("tdp_join_prepare_ex", nat.ptr(bk), n_build, bc, 0, bp, 0, nat.ptr(pk), n_probe,
                  pc, npc, pp, npp, 1, nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
-        m = int(info[0].item())
+        m = read_int(info[:1])
     pi = torch.empty(m, dtype=torch.int64, device=dev)
     bi = torch.empty(m, dtype=torch.int64, device=dev)
     if m:

@@ -31,6 +31,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from .hostread import read_int, record_value, replay_value
 from . import autograd as _ag
 from . import tensor as _T
 
@@ -135,7 +136,7 @@ class Selection:
                  native_predicates(self.preds, index), len(self.preds), self.n,
                  nat.ptr(out_idx), nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream())
         self._count_dev = count
-        self._count = int(count.item())
+        self._count = read_int(count)
         self._idx = out_idx[: self._count]
 
     def indices(self) -> torch.Tensor:
@@ -538,9 +539,14 @@ class DeferredCount:
     def value(self) -> int:
         if self._value is None:
             if self._slot is None:
-                raise RuntimeError("row count of a CUDA-graph template read during capture")
+                v = replay_value(self.dev)  # a capture sized from a recorded run
+                if v is None:
+                    raise RuntimeError("row count of a CUDA-graph template read during capture")
+                self._value = v
+                return v
             self._event.synchronize()
             self._value = int(_ring().buf[self._slot])
+            record_value(self._value)
             self._event = None
             self.dev = None
         return self._value

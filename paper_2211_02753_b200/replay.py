@@ -37,6 +37,7 @@ import torch
 from . import _native as nat
 from .distributed import current_group, world_size
 from .encodings import EncodedTensor, trusted
+from . import hostread
 from .lazy import DeferredCount, LazyValue, PrefixRows, capturing, compact_source
 from .storage import Table, table_from_columns
 from .tensor import Tensor, _cuda_available
@@ -65,20 +66,23 @@ def _stored(t: Tensor) -> Optional[torch.Tensor]:
     return None
 
 
-def signature(q, catalog) -> Optional[tuple]:
+def _tables_signature(catalog, names) -> Optional[tuple[list, list]]:
+    """(signature items, tables) of the named catalog tables: identity, every
+    stored column buffer and its in-place version counter."""
     group = current_group()
     if group is not None and world_size(group) > 1:
         return None
-    if not _cuda_available() or torch.cuda.is_current_stream_capturing():
+    if not _cuda_available() or torch.cuda.is_current_stream_capturing() or hostread.active():
         return None
-    sig = [id(catalog), id(q.registry), len(q.registry.names()), torch.cuda.current_device()]
-    tables = getattr(catalog, "_tables", None)
-    if tables is None:
+    tables_by_name = getattr(catalog, "_tables", None)
+    if tables_by_name is None:
         return None
-    for name in q._scan_tables:
-        t = tables.get(name)
+    sig, tables = [id(catalog), torch.cuda.current_device()], []
+    for name in names:
+        t = tables_by_name.get(name)
         if t is None:
             return None
+        tables.append(t)
         sig.append(id(t))
         for c in t.columns:
             st = _stored(c.values)
@@ -86,6 +90,14 @@ def signature(q, catalog) -> Optional[tuple]:
                 return None
             sig.append(st.data_ptr())
             sig.append(st._version)
+    return sig, tables
+
+
+def signature(q, catalog) -> Optional[tuple]:
+    got = _tables_signature(catalog, q._scan_tables)
+    if got is None:
+        return None
+    sig = got[0] + [id(q.registry), len(q.registry.names())]
     for p in q._params:
         d = p.value.data
         sig.append(d.data_ptr())
@@ -205,30 +217,37 @@ class _Replay:
             return table
 
 
-def _inputs(q, catalog) -> tuple[set, list]:
-    ptrs, hold = set(), []
-    for name in q._scan_tables:
-        t = catalog._tables.get(name)
-        hold.append(t)
+def _inputs(tables) -> set:
+    ptrs = set()
+    for t in tables:
         for c in t.columns:
             st = _stored(c.values)
             if st is not None:
                 ptrs.add(st.untyped_storage().data_ptr())
-    return ptrs, hold
+    return ptrs
 
 
-def _capture(q, catalog):
-    inputs, hold = _inputs(q, catalog)
+def _capture(execute, tables, log):
+    """Capture ``execute`` into a CUDA graph; its host reads of device
+    integers come from ``log`` (an eager run over the same state) and are
+    checked on the device on every replay (hostread.py)."""
+    inputs = _inputs(tables)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
     launches0 = nat.launch_count()
     try:
-        with capturing(), warnings.catch_warnings():
+        with capturing(), warnings.catch_warnings(), hostread.replaying(log) as rlog:
             warnings.simplefilter("ignore")  # "graph is empty": a lazy result, no launches
             with torch.cuda.graph(graph):
-                table = q._execute(catalog)
+                table = execute()
+        if not rlog.consumed():
+            raise hostread.ReplayMismatch("fewer host reads than recorded")
     except Exception:
-        # a host synchronisation (or other uncapturable call) inside the plan
+        # an uncapturable call inside the plan (or a diverging read sequence)
+        if os.environ.get("TDP_REPLAY_DEBUG"):
+            import traceback
+
+            traceback.print_exc()
         nat.load().tdp_clear_error()
         torch.cuda.synchronize()
         return _NOGRAPH
@@ -236,49 +255,85 @@ def _capture(q, catalog):
     template = _Template.build(table, inputs)
     if template is None:
         return _NOGRAPH
-    return _Replay(graph, template, launches, hold)
+    return _Replay(graph, template, launches, list(tables))
 
 
 class _Warm:
     """First sighting of a state: weak references to its tables, so a second
     sighting is recognised only while those very objects are alive (a new
     table that happens to reuse a dead one's id and buffers is a new state,
-    and a stream of fresh tables never triggers captures)."""
+    and a stream of fresh tables never triggers captures), and the host reads
+    the eager run made (None until it finished)."""
 
     def __init__(self, tables):
         self.refs = [weakref.ref(t) for t in tables]
+        self.log = None  # hostread._Log
 
     def alive(self, tables) -> bool:
         return all(r() is t for r, t in zip(self.refs, tables))
 
 
-_LOCK = threading.Lock()  # the per-query replay tables
+_LOCK = threading.Lock()  # the per-owner replay tables
 
 
-def run(q, catalog, sig):
-    """Replay for ``sig`` if captured (capturing it on the second sighting);
-    None: run the program eagerly."""
+def run(owner, sig, tables, execute):
+    """Result of ``execute()`` (a Table) for the state ``sig``: replayed from
+    a CUDA graph once the state has been seen before, else run eagerly (the
+    first eager run records its host reads for the capture).  ``owner`` keeps
+    the entries (``owner._replays``, an OrderedDict)."""
     with _LOCK:
-        ent = _lookup(q, catalog, sig)
-    return ent() if isinstance(ent, _Replay) else None
+        ent = _lookup(owner, sig, tables, execute)
+    if isinstance(ent, _Replay):
+        return ent()
+    if isinstance(ent, _Warm):
+        with hostread.recording() as log:
+            out = execute()
+        ent.log = log
+        return out
+    return execute()
 
 
-def _lookup(q, catalog, sig):
-    entries: OrderedDict = q._replays
-    tables = [catalog._tables.get(name) for name in q._scan_tables]
+def _lookup(owner, sig, tables, execute):
+    entries: OrderedDict = owner._replays
     ent = entries.get(sig)
     if ent is None or (isinstance(ent, _Warm) and not ent.alive(tables)):
-        entries[sig] = _Warm(tables)
+        ent = _Warm(tables)
+        entries[sig] = ent
         entries.move_to_end(sig)
         while len(entries) > MAX_ENTRIES:
             entries.popitem(last=False)
-        return None
+        return ent
     if ent == _NOGRAPH:
         return None
     if isinstance(ent, _Warm):
-        ent = _capture(q, catalog)
+        if ent.log is None:  # its recording run has not finished (another thread)
+            return None
+        ent = _capture(execute, tables, ent.log)
         entries[sig] = ent
         if ent == _NOGRAPH:
             return None
     entries.move_to_end(sig)
     return ent
+
+
+class Pipeline:
+    """Replay for a composite plan -- several compiled queries and kernel
+    calls between them, ``fn(catalog) -> Table`` over the catalog tables
+    ``table_names`` -- on the same terms as ``CompiledQuery.run``: an
+    unchanged state replays one CUDA graph of the whole plan, its data-
+    dependent sizes (join pair counts, group counts) taken from the recorded
+    eager run and checked on the device."""
+
+    def __init__(self, fn, table_names):
+        self.fn = fn
+        self.table_names = tuple(table_names)
+        self._replays: OrderedDict = OrderedDict()
+
+    def run(self, catalog):
+        if not enabled():
+            return self.fn(catalog)
+        got = _tables_signature(catalog, self.table_names)
+        if got is None:
+            return self.fn(catalog)
+        sig, tables = got
+        return run(self, tuple(sig), tables, lambda: self.fn(catalog))

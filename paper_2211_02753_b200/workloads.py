@@ -199,8 +199,15 @@ class Q3Plan:
         self.lineitem = compile_sql(Q3_LINEITEM, catalog, empty)
         self.registry = q3_registry()
         self.tail = None
+        from .replay import Pipeline
+
+        # an unchanged catalog replays one CUDA graph of the whole plan
+        self._pipeline = Pipeline(self.run_eager, ("customer", "orders", "lineitem"))
 
     def run(self, catalog: Catalog):
+        return self._pipeline.run(catalog)
+
+    def run_eager(self, catalog: Catalog):
         from .kernels import equi_join
 
         c = self.cust.run(catalog)

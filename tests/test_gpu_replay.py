@@ -17,6 +17,7 @@ import paper_2211_02753_b200 as tq
 from paper_2211_02753_b200 import _native, replay
 from paper_2211_02753_b200 import compact as cp
 from paper_2211_02753_b200 import workloads as wl
+from paper_2211_02753_b200.storage import FLOAT
 
 pytestmark = pytest.mark.gpu
 
@@ -81,7 +82,9 @@ def test_q6_replay_and_invalidation():
         np.testing.assert_allclose(got, otpch.q6(arrays2)["sum_rev"], rtol=1e-9, atol=1e-9)
 
 
-def test_uncapturable_plan_falls_back():
+def test_data_dependent_sizes_replay_from_recorded_reads():
+    """A general-key group-by sizes its output from a device group count: the
+    capture takes it from the eager run's recorded read (hostread.py)."""
     rng = np.random.default_rng(11)
     n = 20_000
     k = rng.integers(-10**12, 10**12, size=n)
@@ -92,13 +95,101 @@ def test_uncapturable_plan_falls_back():
     q = tq.compile_plan(tq.lower(tq.bind(tq.parse("SELECT k, SUM(v) FROM t GROUP BY k"), cat,
                                          tq.UdfRegistry())), tq.CompileConfig(), tq.UdfRegistry())
     outs = [q.run(cat) for _ in range(3)]
-    assert replay._NOGRAPH in q._replays.values()
+    assert any(isinstance(e, replay._Replay) for e in q._replays.values())
     keys, inv = np.unique(k, return_inverse=True)
     sums = np.zeros(len(keys))
     np.add.at(sums, inv, v)
     for r in outs:
         np.testing.assert_array_equal(r.columns[0].values.numpy(), keys)
         np.testing.assert_allclose(r.columns[1].values.numpy(), sums, rtol=1e-12)
+
+
+def test_uncapturable_plan_falls_back():
+    """A UDF body that reads a device value on the host cannot be captured:
+    the plan runs eagerly from then on."""
+    rng = np.random.default_rng(12)
+    n = 20_000
+    v = rng.random(n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["v"], [tq.plain(tq.Tensor(v))]))
+    reg = tq.UdfRegistry()
+
+    def body(c):
+        peak = float(c.values.data.max().item())  # host read inside the plan
+        return (tq.plain(tq.Tensor(c.values.data / peak)),)
+
+    reg.register(tq.UdfEntry("norm", (("w", FLOAT),), 1, body, (), pe_outputs=False))
+    q = tq.compile_plan(tq.lower(tq.bind(tq.parse("SELECT SUM(w) FROM (SELECT norm(v) FROM t)"),
+                                         cat, reg)), tq.CompileConfig(), reg)
+    outs = [q.run(cat) for _ in range(3)]
+    assert replay._NOGRAPH in q._replays.values()
+    for r in outs:
+        np.testing.assert_allclose(r.columns[0].values.numpy(), [np.sum(v / v.max())], rtol=1e-12)
+
+
+def _q3_check(res, exp):
+    got = _cols(res)
+    np.testing.assert_array_equal(got["l_orderkey"], exp["l_orderkey"])
+    np.testing.assert_allclose(got["sum_rev"], exp["sum_rev"], rtol=1e-9)
+
+
+def test_q3_pipeline_replays_one_graph():
+    """The Q3 plan (three filter queries, two joins, the tail query) replays
+    as one CUDA graph over an unchanged catalog; a new catalog state runs
+    eagerly again."""
+    tables = wl.q3_arrays(0.02, seed=7)
+    cat = wl.q3_catalog(tables)
+    plan = wl.Q3Plan(cat)
+    exp = otpch.q3(tables)
+    outs = [plan.run(cat) for _ in range(2)]
+    assert any(isinstance(e, replay._Replay) for e in plan._pipeline._replays.values())
+    n0 = _native.launch_count()
+    outs.append(plan.run(cat))
+    assert _native.launch_count() - n0 > 10  # the joins, group-by, top-k, ...
+    for r in outs:
+        _q3_check(r, exp)
+    # an in-place write to a scanned column is a new state
+    li = cat._tables["lineitem"]
+    sd = li.columns[list(li.schema.names).index("l_shipdate")].values.data
+    sd.add_(1)
+    shifted = {t: dict(c) for t, c in tables.items()}
+    shifted["lineitem"]["l_shipdate"] = tables["lineitem"]["l_shipdate"] + 1
+    _q3_check(plan.run(cat), otpch.q3(shifted))
+
+
+_GUARD_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import torch
+from paper_2211_02753_b200 import workloads as wl
+tables = wl.q3_arrays(0.02, seed=7)
+cat = wl.q3_catalog(tables)
+plan = wl.Q3Plan(cat)
+plan.run(cat); plan.run(cat)
+li = cat._tables["lineitem"]
+sd = li.columns[list(li.schema.names).index("l_shipdate")].values.data
+sd.data.fill_(20000)  # behind the version counter: the signature still matches
+res = plan.run(cat)
+torch.cuda.synchronize()
+print("NOT TRAPPED", flush=True)
+"""
+
+
+def test_replay_guard_traps_on_stale_sizes():
+    """A catalog changed behind torch's version counters keeps the replay
+    signature, but the recorded join size no longer holds: the device-side
+    check aborts the replay instead of overrunning the pair buffers."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parent.parent)
+    proc = subprocess.run([sys.executable, "-c", _GUARD_SCRIPT.format(root=root)],
+                          capture_output=True, text=True, timeout=300)
+    out = proc.stdout + proc.stderr
+    assert "NOT TRAPPED" not in out
+    assert proc.returncode != 0
+    assert "replayed plan read" in out or "CUDA" in out or "cuda" in out
 
 
 def test_replay_off_switch():

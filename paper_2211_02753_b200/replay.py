@@ -227,10 +227,14 @@ def _inputs(tables) -> set:
     return ptrs
 
 
+CAPTURES = [0]  # capture attempts in this process (diagnostics)
+
+
 def _capture(execute, tables, log):
     """Capture ``execute`` into a CUDA graph; its host reads of device
     integers come from ``log`` (an eager run over the same state) and are
     checked on the device on every replay (hostread.py)."""
+    CAPTURES[0] += 1
     inputs = _inputs(tables)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()

@@ -699,6 +699,9 @@ def _q3(args):
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0
     # the same pipeline re-planned on the host every step (no graph replay)
+    for _ in range(max(args.warmup, 3)):
+        plan.run_eager(cat)
+    torch.cuda.synchronize()
     t0.record()
     for _ in range(steps):
         plan.run_eager(cat)

@@ -381,31 +381,33 @@ __global__ void copy_counts_kernel(const unsigned long long* __restrict__ counts
 // ---------------------------------------------------------------------------
 // top-k of a stable order (ORDER BY ... LIMIT k, tq/kernels.py:267-273): the k
 // smallest (key image, row) pairs.  Each CTA bitonic-sorts a chunk of
-// kTopkChunk pairs in shared memory and keeps its first k; the survivors are
-// reduced the same way until one CTA remains.  Ties keep row order because the
-// row index is the second sort key, exactly as the stable radix sort orders.
+// `chunk` pairs (a power of two <= kTopkChunk) in shared memory and keeps its
+// first k; the survivors are reduced the same way until one CTA remains.
+// Chunks are sized per round: the smallest power of two >= 2k that still
+// gives at most two CTAs per SM, so a round is a short sort on many SMs
+// rather than a 2048-wide one on few.  Ties keep row order because the row
+// index is the second sort key, exactly as the stable radix sort orders.
 // ---------------------------------------------------------------------------
 constexpr int kTopkChunk = 2048;
-constexpr int kTopkThreads = 1024;
 constexpr int kTopkMax = 1024;
 
-__global__ void __launch_bounds__(kTopkThreads)
+__global__ void __launch_bounds__(kTopkChunk / 2)
     topk_chunk_kernel(const u64* __restrict__ keys, const i64* __restrict__ idx, i64 m, int k,
-                      u64* __restrict__ out_keys, i64* __restrict__ out_idx,
+                      int chunk, u64* __restrict__ out_keys, i64* __restrict__ out_idx,
                       i64* __restrict__ final_idx, i64 final_count) {
   __shared__ u64 sk[kTopkChunk];
   __shared__ i64 si[kTopkChunk];
-  const i64 base = (i64)blockIdx.x * kTopkChunk;
-  for (int t = threadIdx.x; t < kTopkChunk; t += blockDim.x) {
+  const i64 base = (i64)blockIdx.x * chunk;
+  for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
     const i64 g = base + t;
     const bool ok = g < m;
     sk[t] = ok ? keys[g] : ~0ull;
     si[t] = ok ? idx[g] : LLONG_MAX;  // sentinel sorts after every real pair
   }
-  for (int size = 2; size <= kTopkChunk; size <<= 1) {
+  for (int size = 2; size <= chunk; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
-      for (int t = threadIdx.x; t < kTopkChunk / 2; t += blockDim.x) {
+      for (int t = threadIdx.x; t < chunk / 2; t += blockDim.x) {
         const int a = 2 * t - (t & (stride - 1));
         const int b = a + stride;
         const bool up = (a & size) == 0;
@@ -432,6 +434,19 @@ __global__ void __launch_bounds__(kTopkThreads)
   }
 }
 
+int topk_round_chunk(i64 m, i64 k) {
+  int c = 64;
+  while (c < 2 * k) c <<= 1;
+  while (c < kTopkChunk && ceil_div(m, c) > 2 * (i64)sm_count()) c <<= 1;
+  return c;
+}
+
+int pow2_at_least(i64 m) {
+  int c = 2;
+  while (c < m) c <<= 1;
+  return c;
+}
+
 }  // namespace tdp
 
 using namespace tdp;
@@ -441,7 +456,8 @@ extern "C" {
 size_t tdp_sort_workspace(int64_t n) { return sort_ws_bytes(n); }
 
 size_t tdp_topk_workspace(int64_t n, int64_t k) {
-  const i64 m1 = ceil_div(n > 0 ? n : 1, kTopkChunk) * (k > 0 ? k : 1);
+  // first round: chunks of at least 64 pairs (and >= 2k), k survivors each
+  const i64 m1 = ceil_div(n > 0 ? n : 1, 64) * (k > 0 ? k : 1);
   return 2 * align256((size_t)(n > 0 ? n : 1) * 8) + 4 * align256((size_t)m1 * 8) + 256;
 }
 
@@ -463,7 +479,7 @@ int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t
   p += align256((size_t)n * 8);
   i64* i0 = (i64*)p;
   p += align256((size_t)n * 8);
-  const i64 m1 = ceil_div(n, kTopkChunk) * k;
+  const i64 m1 = ceil_div(n, 64) * k;
   u64* ka = (u64*)p;
   p += align256((size_t)m1 * 8);
   i64* ia = (i64*)p;
@@ -480,19 +496,21 @@ int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t
   i64 m = n;
   bool use_a = true;
   while (m > kTopkChunk) {
-    const i64 blocks = ceil_div(m, kTopkChunk);
+    const int chunk = topk_round_chunk(m, k);
+    const i64 blocks = ceil_div(m, chunk);
     u64* dk = use_a ? ka : kb;
     i64* di = use_a ? ia : ib;
-    topk_chunk_kernel<<<(unsigned)blocks, kTopkThreads, 0, st>>>(sk, si, m, (int)k, dk, di,
-                                                                 nullptr, 0);
+    topk_chunk_kernel<<<(unsigned)blocks, chunk / 2, 0, st>>>(sk, si, m, (int)k, chunk, dk, di,
+                                                              nullptr, 0);
     TDP_LAUNCH_CHECK("topk_chunk_kernel");
     sk = dk;
     si = di;
     m = blocks * k;
     use_a = !use_a;
   }
-  topk_chunk_kernel<<<1, kTopkThreads, 0, st>>>(sk, si, m, (int)k, nullptr, nullptr, out_order,
-                                                 want);
+  const int last = pow2_at_least(m);
+  topk_chunk_kernel<<<1, last / 2 > 32 ? last / 2 : 32, 0, st>>>(sk, si, m, (int)k, last, nullptr,
+                                                                 nullptr, out_order, want);
   TDP_LAUNCH_CHECK("topk_chunk_kernel");
   return TDP_OK;
 }

@@ -1,4 +1,4 @@
-"""Eager (re-planned) Q3 step time with and without replay of the inner queries."""
+"""Eager (re-planned) Q3 step time after pipeline replays; capture counts."""
 import sys
 import time
 from pathlib import Path
@@ -11,12 +11,17 @@ from paper_2211_02753_b200 import replay, workloads as wl
 tables = wl.q3_arrays(10.0, seed=7)
 cat = wl.q3_catalog(tables)
 plan = wl.Q3Plan(cat)
-for name, fn in (("run_eager", plan.run_eager), ("run (pipeline replay)", plan.run)):
+for name, fn in (("run (pipeline replay)", plan.run), ("run_eager", plan.run_eager)):
     for _ in range(3):
         fn(cat)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(20):
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
         fn(cat)
-    torch.cuda.synchronize()
-    print(f"{name}: {(time.perf_counter() - t0) / 20 * 1e3:.3f} ms; captures so far {replay.CAPTURES[0]}")
+        torch.cuda.synchronize()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print(f"{name}: " + " ".join(f"{t:.2f}" for t in ts) + f"; captures so far {replay.CAPTURES[0]}")
+print("tail entries:", [type(e).__name__ if not isinstance(e, str) else e for e in plan.tail._replays.values()])
+for q in (plan.cust, plan.orders, plan.lineitem):
+    print("filter entries:", [type(e).__name__ if not isinstance(e, str) else e for e in q._replays.values()])

@@ -95,3 +95,49 @@ def test_soft_linear_shape_limits(lib):
     rc = lib.tdp_linear_argmax_count(None, nat.F32, 1000, 64, 2, None, None, keys, 2, 1, out,
                                      None)
     assert rc == EINVAL and "dense" in _err(lib)
+
+
+def test_replay_log_round_trip_and_validation(lib):
+    """The C-side replay log (tdp_replay_log_*): a replay-mode log reports how
+    far it was consumed; bad modes and oversize expect reads are rejected."""
+    assert lib.tdp_replay_log_begin(3, None, 0) == EINVAL and "mode" in _err(lib)
+    vals = (c_int64 * 3)(5, 6, 7)
+    assert lib.tdp_replay_log_begin(2, vals, 3) == 0
+    assert lib.tdp_replay_log_size() == 0  # nothing consumed yet
+    assert lib.tdp_replay_log_end(None, 0) == 0
+    assert lib.tdp_replay_log_begin(1, None, 0) == 0
+    assert lib.tdp_replay_log_size() == 0  # nothing recorded
+    out = (c_int64 * 1)()
+    assert lib.tdp_replay_log_end(out, 1) == 0
+    expected = (c_int64 * 9)()
+    assert lib.tdp_expect_values(c_void_p(16), 8, 9, expected, None) == EINVAL
+    assert "at most 8" in _err(lib)
+    assert lib.tdp_expect_values(c_void_p(16), 2, 1, expected, None) == EINVAL
+
+
+def test_hostread_scopes_without_device():
+    """hostread: outside a scope a read is a plain read; a recording scope
+    logs reads; a replaying scope hands them back in order and rejects a
+    diverging sequence before touching the device."""
+    import torch
+
+    from paper_2211_02753_b200 import hostread
+
+    t = torch.tensor([3, 4], dtype=torch.int64)
+    assert hostread.read_ints(t) == [3, 4] and not hostread.active()
+    with hostread.recording() as log:
+        assert hostread.active()
+        assert hostread.read_int(torch.tensor([9])) == 9
+        hostread.record_value(11)
+    assert log.values == [[9], [11]] and log.c_values == []
+    with pytest.raises(RuntimeError):
+        with hostread.recording():
+            with hostread.recording():
+                pass
+    with hostread.replaying(log) as rlog:
+        with pytest.raises(hostread.ReplayMismatch):  # shape differs from the log
+            hostread.read_ints(torch.tensor([1, 2]))
+        rlog.pos = len(log.values)
+        with pytest.raises(hostread.ReplayMismatch):  # more reads than recorded
+            hostread.read_int(torch.tensor([1]))
+    assert not hostread.active()

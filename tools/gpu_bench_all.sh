@@ -3,6 +3,7 @@
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" 2>&1 | tail -2
 timeout 600 python bench.py > gpurun_out/bench_q1.json 2> gpurun_out/bench_q1.err; echo "q1 rc=$?"
 timeout 600 python bench.py --query q6 > gpurun_out/bench_q6.json 2> gpurun_out/bench_q6.err; echo "q6 rc=$?"
 timeout 600 python bench.py --encoding compact > gpurun_out/bench_q1_compact.json 2> gpurun_out/bench_q1_compact.err; echo "q1c rc=$?"

@@ -687,15 +687,19 @@ def _q3(args):
     for _ in range(max(args.warmup, 3)):
         res = plan.run(cat)
     torch.cuda.synchronize()
+    uuid = str(torch.cuda.get_device_properties(0).uuid)
+    sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
     launches0 = _native.launch_count()
     steps = max(1, min(args.steps, 50))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sampler.active = True
     t0.record()
     for _ in range(steps):
         res = plan.run(cat)
     t1.record()
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0
     # the same pipeline re-planned on the host every step (no graph replay)
@@ -708,6 +712,24 @@ def _q3(args):
     t1.record()
     torch.cuda.synchronize()
     eager_ms = t0.elapsed_time(t1) / steps
+    # end to end through the API: pinned host columns copied in every step (a
+    # new catalog, so the plan runs eagerly), the result read back
+    host = {t: {c: torch.from_numpy(v).pin_memory() for c, v in cols.items()}
+            for t, cols in tables.items()}
+    h2d = sum(h.numel() * h.element_size() for cols in host.values() for h in cols.values())
+
+    def e2e_step():
+        out = plan.run(wl.q3_catalog(host))
+        return sum(c.values.numpy().nbytes for c in out.columns)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.e2e_steps, 5))
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d2h = e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - w0) / e2e_steps
     nli = len(tables["lineitem"]["l_orderkey"])
     base_bytes = (16 * len(tables["customer"]["c_custkey"]) + 32 * len(tables["orders"]["o_orderkey"])
                   + 32 * nli)
@@ -729,7 +751,9 @@ def _q3(args):
         "replay": "one CUDA graph of the whole plan per step (replay.Pipeline; every kernel runs "
                   "over all rows, data-dependent sizes from the recorded eager run, checked on "
                   "the device)",
-        "eager_ms_per_step": eager_ms,
+        "eager_ms_per_step": eager_ms, "clocks": clocks,
+        "e2e": {"value": nli / e2e_s, "unit": "lineitem rows/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
                      "achieved": base_bytes / (ms / 1e3) / 1e9,
                      "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0], "traffic": None,

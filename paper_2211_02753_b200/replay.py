@@ -310,8 +310,8 @@ def _lookup(owner, sig, tables, execute):
     if ent == _NOGRAPH:
         return None
     if isinstance(ent, _Warm):
-        if ent.log is None:  # its recording run has not finished (another thread)
-            return None
+        if ent.log is None:  # no finished recording (another thread's, or one that raised)
+            return ent
         ent = _capture(execute, tables, ent.log)
         entries[sig] = ent
         if ent == _NOGRAPH:

@@ -287,12 +287,19 @@ extern "C" __global__ void __launch_bounds__(TDP_PTHREADS)
     for (i64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
       tdp_mbar_wait(tdp_smem_addr(&full_bar[s]), fph);
       const unsigned char* sb = tdp_ring + (size_t)s * TDP_STAGE_BYTES;
+#if TDP_VEC_RING
+      TdpRow r[TDP_PU];
+      tdp_load_smem_pu(r, sb, warp * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < TDP_PU; ++u) acc.row(P, r[u], true);
+#else
 #pragma unroll
       for (int u = 0; u < TDP_PU; ++u) {
         TdpRow r;
         tdp_load_smem(r, sb, (u * TDP_CONS_WARPS + warp) * 32 + lane);
         acc.row(P, r, true);
       }
+#endif
       __syncwarp();
       if (lane == 0) tdp_mbar_arrive(tdp_smem_addr(&empty_bar[s]));
       if (++s == TDP_STAGES) {

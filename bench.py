@@ -390,7 +390,9 @@ def _ours(args):
         "hbm_gbs_step": bpr * n_total / (ms / 1e3) / 1e9,
         "e2e": {"value": n_total / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": d2h,
-                "how": "pinned host columns -> device table -> CompiledQuery.run -> result to host"},
+                "h2d_gbs_per_rank": h2d / e2e_s / 1e9,
+                "how": "pinned host columns -> device table -> CompiledQuery.run -> result to host "
+                       "(bound by the host->device link: h2d_gbs_per_rank)"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "tdp_scan_agg (fused filter+UDF+group-by), per rank, "
                                "timed by library events over eager runs",
@@ -753,7 +755,9 @@ def _q3(args):
                   "the device)",
         "eager_ms_per_step": eager_ms, "clocks": clocks,
         "e2e": {"value": nli / e2e_s, "unit": "lineitem rows/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "h2d_gbs": h2d / e2e_s / 1e9,
+                "how": "pinned host columns -> q3_catalog -> Q3Plan.run (a new catalog: "
+                       "re-planned) -> result to host"},
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
                      "achieved": base_bytes / (ms / 1e3) / 1e9,
                      "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0], "traffic": None,

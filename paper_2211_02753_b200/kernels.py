@@ -1163,6 +1163,8 @@ def _side_sources(cols: Sequence[EncodedTensor]):
 
 
 def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tensor):
+    if not cols:
+        return []
     if any(onehot_payload(c.values) is not None for c in cols):
         return [take_rows(c, rows if rowmap is None else gather_rows_raw(rowmap, rows))
                 for c in cols]
@@ -1173,23 +1175,32 @@ def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tenso
 
 
 def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], left_key: int,
-              right_key: int) -> list[EncodedTensor]:
+              right_key: int, left_out: Optional[Sequence[int]] = None,
+              right_out: Optional[Sequence[int]] = None) -> list[EncodedTensor]:
     """Inner join ``left.left_key = right.right_key``; returns left columns then
     right columns, rows ordered by left row then ascending right row.  Keys
     must be plain int64 columns (dictionary codes from different dictionaries
     are not comparable).  Filtered (lazy) inputs are joined without
     materialising the filtered relations: only the key columns are gathered
-    before the join, every output column is gathered once from its base."""
+    before the join, every output column is gathered once from its base.
+    ``left_out`` / ``right_out`` (default: all) list the columns to return --
+    a projection pushed into the join: the others are never gathered."""
     for side, cols, k in (("left", left, left_key), ("right", right, right_key)):
         col = cols[k]
         if col.is_pe() or col.is_dictionary() or col.values.dtype != "int64" or col.values.ndim != 1:
             raise KernelError(f"{side} join key must be a plain int64 column")
+    lo = list(range(len(left))) if left_out is None else list(left_out)
+    ro = list(range(len(right))) if right_out is None else list(right_out)
+    for side, cols, out in (("left", left, lo), ("right", right, ro)):
+        if any(not 0 <= i < len(cols) for i in out):
+            raise KernelError(f"{side} output column index out of range")
     if active_tape() is not None:
         pi, bi = join_indices(left[left_key].values, right[right_key].values)
-        return [take_rows(c, pi) for c in left] + [take_rows(c, bi) for c in right]
+        return [take_rows(left[i], pi) for i in lo] + [take_rows(right[i], bi) for i in ro]
     group = current_group()
     if group is not None and world_size(group) > 1:
-        return _equi_join_sharded(left, right, left_key, right_key, group)
+        out = _equi_join_sharded(left, right, left_key, right_key, group)
+        return [out[i] for i in lo] + [out[len(left) + i] for i in ro]
     lb, lsel = _side_sources(left)
     rb, rsel = _side_sources(right)
     # a filtered side whose key is a base column joins straight from the base
@@ -1210,7 +1221,8 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
         rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
         pairs = join_indices(lkey, rkey, probe_sel=lsel if lkey_direct else None)
     pi, bi = pairs
-    return _gather_side(left, lb, lmap, pi) + _gather_side(right, rb, rmap, bi)
+    return (_gather_side([left[i] for i in lo], [lb[i] for i in lo], lmap, pi)
+            + _gather_side([right[i] for i in ro], [rb[i] for i in ro], rmap, bi))
 
 
 def _repartition(cols: Sequence[EncodedTensor], key_index: int, group) -> list[EncodedTensor]:

@@ -213,10 +213,11 @@ class Q3Plan:
         c = self.cust.run(catalog)
         o = self.orders.run(catalog)
         li = self.lineitem.run(catalog)
-        oc = equi_join(list(o.columns), list(c.columns), 1, 0)  # orders |><| BUILDING customers
-        j = equi_join(list(li.columns), oc[:4], 0, 0)          # lineitem |><| those orders
-        names = ["l_orderkey", "l_extendedprice", "l_discount", "o_orderkey", "o_custkey",
-                 "o_orderdate", "o_shippriority"]
+        # orders |><| BUILDING customers: keep o_orderkey, o_orderdate, o_shippriority
+        oc = equi_join(list(o.columns), list(c.columns), 1, 0, left_out=[0, 2, 3], right_out=[])
+        # lineitem |><| those orders: the tail reads these five columns only
+        j = equi_join(list(li.columns), oc, 0, 0, right_out=[1, 2])
+        names = ["l_orderkey", "l_extendedprice", "l_discount", "o_orderdate", "o_shippriority"]
         joined = table_from_columns(names, j)
         work = Catalog()
         work.register("joined", joined)

@@ -265,6 +265,13 @@ def test_filtered_build_join_matches_oracle(unique_build, filter_probe):
     np.testing.assert_array_equal(out[2].values.numpy(), fbk[ebi])
     np.testing.assert_array_equal(out[3].values.numpy(), fbs[ebi])
     np.testing.assert_array_equal(out[4].values.numpy(), fbv[ebi])
+    # a projection pushed into the join returns exactly the listed columns
+    proj = equi_join(fp, fb, 0, 0, left_out=[1], right_out=[2, 0])
+    assert len(proj) == 3
+    np.testing.assert_array_equal(proj[0].values.numpy(), fpv[epi])
+    np.testing.assert_array_equal(proj[1].values.numpy(), fbv[ebi])
+    np.testing.assert_array_equal(proj[2].values.numpy(), fbk[ebi])
+    assert equi_join(fp, fb, 0, 0, left_out=[], right_out=[]) == []
 
 
 @pytest.mark.parametrize("n", [1, 7, 2048, 2049, 100_003, 3_000_000])

@@ -22,12 +22,11 @@ for _ in range(N):
     t = [time.perf_counter()]
     c = plan.cust.run(cat); o = plan.orders.run(cat); li = plan.lineitem.run(cat)
     t.append(time.perf_counter())
-    oc = equi_join(list(o.columns), list(c.columns), 1, 0)
+    oc = equi_join(list(o.columns), list(c.columns), 1, 0, left_out=[0, 2, 3], right_out=[])
     t.append(time.perf_counter())
-    j = equi_join(list(li.columns), oc[:4], 0, 0)
+    j = equi_join(list(li.columns), oc, 0, 0, right_out=[1, 2])
     t.append(time.perf_counter())
-    names = ["l_orderkey", "l_extendedprice", "l_discount", "o_orderkey", "o_custkey",
-             "o_orderdate", "o_shippriority"]
+    names = ["l_orderkey", "l_extendedprice", "l_discount", "o_orderdate", "o_shippriority"]
     work = Catalog()
     work.register("joined", table_from_columns(names, j))
     res = plan.tail.run(work)

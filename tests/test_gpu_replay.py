@@ -13,6 +13,7 @@ import pytest
 import torch
 
 import oracle.tpch as otpch
+from oracle import relational as orc
 import paper_2211_02753_b200 as tq
 from paper_2211_02753_b200 import _native, replay
 from paper_2211_02753_b200 import compact as cp
@@ -155,6 +156,49 @@ def test_q3_pipeline_replays_one_graph():
     shifted = {t: dict(c) for t, c in tables.items()}
     shifted["lineitem"]["l_shipdate"] = tables["lineitem"]["l_shipdate"] + 1
     _q3_check(plan.run(cat), otpch.q3(shifted))
+
+
+def test_pipeline_with_sorted_join_and_full_order_replays():
+    """A composite plan whose library calls take data-dependent decisions in
+    C (radix-sort digit passes of a repeated-key join build and of a full
+    ORDER BY) replays from the recorded log with identical results."""
+    from paper_2211_02753_b200.kernels import equi_join, filter_exact
+    from paper_2211_02753_b200.replay import Pipeline
+
+    rng = np.random.default_rng(41)
+    nl, nr = 50_000, 8_000
+    lk = rng.integers(0, 3_000, size=nl)
+    lv = rng.normal(size=nl)
+    rk = rng.integers(0, 3_000, size=nr)          # repeated build keys: sorted runs
+    rv = rng.integers(0, 1000, size=nr).astype(np.float64)
+    cat = tq.Catalog()
+    cat.register("l", tq.table_from_columns(["lk", "lv"], [tq.plain(tq.Tensor(lk)),
+                                                            tq.plain(tq.Tensor(lv))]))
+    cat.register("r", tq.table_from_columns(["rk", "rv"], [tq.plain(tq.Tensor(rk)),
+                                                            tq.plain(tq.Tensor(rv))]))
+    order_q = {}
+
+    def plan(c):
+        lt, rt = c._tables["l"], c._tables["r"]
+        right = filter_exact(list(rt.columns), [(1, "<", 700.0)])
+        j = equi_join(list(lt.columns), right, 0, 0, left_out=[1], right_out=[1])
+        work = tq.Catalog()
+        work.register("j", tq.table_from_columns(["lv", "rv"], j))
+        if "q" not in order_q:
+            order_q["q"] = wl.compile_sql("SELECT lv, rv FROM j ORDER BY rv DESC", work,
+                                          tq.UdfRegistry())
+        return order_q["q"].run(work)
+
+    pipe = Pipeline(plan, ("l", "r"))
+    outs = [pipe.run(cat) for _ in range(3)]
+    assert any(isinstance(e, replay._Replay) for e in pipe._replays.values())
+    keep = rv < 700.0
+    epi, ebi = orc.join_inner(lk, rk[keep])
+    jlv, jrv = lv[epi], rv[keep][ebi]
+    order = orc.stable_order(jrv, True)
+    for r in outs:
+        np.testing.assert_array_equal(r.columns[1].values.numpy(), jrv[order])
+        np.testing.assert_array_equal(r.columns[0].values.numpy(), jlv[order])
 
 
 _GUARD_SCRIPT = r"""

@@ -49,11 +49,16 @@ struct TdpAcc {
   i64 ai[TDP_G][TDP_NIA];
 #endif
 #if TDP_SMEMACC
-  // cell-major [TDP_CELLS][TDP_ACC_THREADS]: a thread touches only its own
-  // column, so updates need no atomics and consecutive threads hit
-  // consecutive 8-byte words (conflict-free).
+  // cell-major columns: a thread touches only its own column, so updates need
+  // no atomics and consecutive threads hit consecutive words (conflict-free).
+  // Counts are 32-bit ([TDP_G][TDP_ACC_THREADS] u32: a thread counts at most
+  // its own rows), the value cells 64-bit after them
+  // ([TDP_G * (TDP_NF + TDP_NI)][TDP_ACC_THREADS] u64): 4 bytes less
+  // shared-memory traffic per row, the pipe narrow rows are bound by.
   u64* sm;
   int col;
+  __device__ __forceinline__ unsigned* counts() const { return reinterpret_cast<unsigned*>(sm); }
+  __device__ __forceinline__ u64* values() const { return sm + (size_t)TDP_G * (TDP_ACC_THREADS / 2); }
 #endif
   __device__ __forceinline__ void zero(u64* smem_acc) {
 #if TDP_REGACC
@@ -69,8 +74,10 @@ struct TdpAcc {
 #if TDP_SMEMACC
     sm = smem_acc;
     col = threadIdx.x;
-    if (col < TDP_ACC_THREADS)
-      for (int c = 0; c < TDP_CELLS; ++c) sm[c * TDP_ACC_THREADS + col] = 0;
+    if (col < TDP_ACC_THREADS) {
+      for (int c = 0; c < TDP_G; ++c) counts()[c * TDP_ACC_THREADS + col] = 0u;
+      for (int c = 0; c < TDP_CELLS - TDP_G; ++c) values()[c * TDP_ACC_THREADS + col] = 0;
+    }
 #endif
   }
   __device__ __forceinline__ void add(const TdpParams& P, bool keep, int slot, const double* f,
@@ -87,15 +94,15 @@ struct TdpAcc {
     }
 #elif TDP_SMEMACC
     if (keep) {
-      u64* p = sm + (size_t)slot * TDP_ACC_THREADS + col;
-      p[0] += 1ull;
+      counts()[(size_t)slot * TDP_ACC_THREADS + col] += 1u;
+      u64* p = values() + (size_t)slot * TDP_ACC_THREADS + col;
 #pragma unroll
       for (int a = 0; a < TDP_NF; ++a) {
-        double* d = reinterpret_cast<double*>(p + (size_t)TDP_G * (1 + a) * TDP_ACC_THREADS);
+        double* d = reinterpret_cast<double*>(p + (size_t)TDP_G * a * TDP_ACC_THREADS);
         *d += f[a];
       }
 #pragma unroll
-      for (int a = 0; a < TDP_NI; ++a) p[(size_t)TDP_G * (1 + TDP_NF + a) * TDP_ACC_THREADS] += (u64)q[a];
+      for (int a = 0; a < TDP_NI; ++a) p[(size_t)TDP_G * (TDP_NF + a) * TDP_ACC_THREADS] += (u64)q[a];
     }
 #else
     if (keep) {
@@ -157,8 +164,15 @@ struct TdpAcc {
     __syncthreads();
     u64* out = reinterpret_cast<u64*>(P.acc) + blockIdx.x;  // cell-major, as above
     for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {
-      const u64* row = sm + (size_t)c * TDP_ACC_THREADS;
-      if (c >= TDP_G && c < TDP_G * (1 + TDP_NF)) {
+      if (c < TDP_G) {
+        const unsigned* row = counts() + (size_t)c * TDP_ACC_THREADS;
+        u64 v = 0;
+        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];
+        out[(i64)c * gridDim.x] = v;
+        continue;
+      }
+      const u64* row = values() + (size_t)(c - TDP_G) * TDP_ACC_THREADS;
+      if (c < TDP_G * (1 + TDP_NF)) {
         double v = 0.0;
         for (int t = 0; t < TDP_ACC_THREADS; ++t) v += __longlong_as_double((i64)row[t]);
         out[(i64)c * gridDim.x] = (u64)__double_as_longlong(v);

@@ -336,6 +336,20 @@ int tdp_groupby_hash_prepare(const int64_t* keys, int64_t n, const tdp_column* v
 int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, int64_t m,
                           int64_t* out_keys, int64_t* out_counts, void* out_sums, void* ws,
                           size_t ws_bytes, void* stream);
+/* prepare_ex: prepare, plus the distinct keys' range: out_info (device
+ * int64[3]) = {m, min key image, max key image} (images: key ^ INT64_MIN,
+ * order-preserving).  emit_ranked: emit with the keys ordered by a bitmap
+ * over [min_key, min_key + key_range) (ranks by popcount prefix) instead of
+ * a radix sort -- for ranges up to a few dozen bits per distinct key; its
+ * extra workspace is tdp_groupby_hash_rank_workspace(key_range).          */
+int tdp_groupby_hash_prepare_ex(const int64_t* keys, int64_t n, const tdp_column* vals,
+                                const int32_t* agg_kinds, int32_t naggs, int64_t* out_info,
+                                void* ws, size_t ws_bytes, void* stream);
+size_t tdp_groupby_hash_rank_workspace(int64_t key_range);
+int tdp_groupby_hash_emit_ranked(int64_t n, const int32_t* agg_kinds, int32_t naggs, int64_t m,
+                                 int64_t min_key, int64_t key_range, int64_t* out_keys,
+                                 int64_t* out_counts, void* out_sums, void* ws, size_t ws_bytes,
+                                 void* rank_ws, size_t rank_ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* equi-join (builder-defined; the reference has none)       */

@@ -132,6 +132,12 @@ _SIGNATURES = {
                                          c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_groupby_hash_emit": (c_int, [c_int64, POINTER(c_int32), c_int32, c_int64, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_groupby_hash_prepare_ex": (c_int, [c_void_p, c_int64, POINTER(Column), POINTER(c_int32),
+                                            c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_groupby_hash_rank_workspace": (c_size_t, [c_int64]),
+    "tdp_groupby_hash_emit_ranked": (c_int, [c_int64, POINTER(c_int32), c_int32, c_int64, c_int64,
+                                             c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                             c_size_t, c_void_p, c_size_t, c_void_p]),
     "tdp_join_workspace": (c_size_t, [c_int64, c_int64]),
     "tdp_join_prepare": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                                  c_size_t, c_void_p]),

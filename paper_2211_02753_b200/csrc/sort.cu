@@ -1319,15 +1319,96 @@ __global__ void hashagg_flags_kernel(HashAgg h) {
     h.flags[s] = s < h.cap ? (h.slot[s] != 0ull) : (h.cnt[h.cap] != 0ull);
 }
 
+// With `range` (preset ~0 / 0): also the min / max key image into range[1], [2].
 __global__ void hashagg_compact_kernel(HashAgg h, u64* __restrict__ out_img,
-                                       i64* __restrict__ out_slot) {
+                                       i64* __restrict__ out_slot,
+                                       unsigned long long* __restrict__ range) {
+  unsigned long long lo = ~0ull, hi = 0ull;
   for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s <= h.cap;
        s += (i64)gridDim.x * blockDim.x) {
     if (!h.flags[s]) continue;
     const i64 o = h.offs[s];
-    out_img[o] = s < h.cap ? h.slot[s] : 0ull;  // key images sort like the keys
+    const u64 img = s < h.cap ? h.slot[s] : 0ull;  // key images sort like the keys
+    out_img[o] = img;
     out_slot[o] = s;
+    lo = img < lo ? img : lo;
+    hi = img > hi ? img : hi;
   }
+  if (range == nullptr) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  if ((threadIdx.x & 31) == 0 && lo <= hi) {
+    atomicMin(range + 1, lo);
+    atomicMax(range + 2, hi);
+  }
+}
+
+__global__ void info_init_kernel(unsigned long long* info) {
+  info[1] = ~0ull;
+  info[2] = 0ull;
+}
+
+// Rank of each distinct key by a bitmap over its range (instead of a radix
+// sort of the m keys: a handful of bandwidth-bound passes over range/8 bytes
+// rather than four latency-bound sort passes).
+__global__ void rank_bits_kernel(const u64* __restrict__ img, i64 m, u64 lo,
+                                 unsigned* __restrict__ bits) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 d = img[i] - lo;
+    atomicOr(bits + (d >> 5), 1u << (d & 31));
+  }
+}
+
+// One warp per 1024-bit block of the bitmap: its population, and per word
+// the set bits of the block's earlier words (u16, <= 992).
+__global__ void rank_popc_kernel(const unsigned* __restrict__ bits, i64 words, i64 blocks,
+                                 i64* __restrict__ counts, unsigned short* __restrict__ wpre) {
+  const int lane = threadIdx.x & 31;
+  const i64 warps = (i64)gridDim.x * (blockDim.x >> 5);
+  for (i64 blk = (i64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); blk < blocks;
+       blk += warps) {
+    const i64 w = blk * 32 + lane;
+    const int c = w < words ? __popc(bits[w]) : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (w < words) wpre[w] = (unsigned short)(incl - c);
+    if (lane == 31) counts[blk] = incl;
+  }
+}
+
+// rank = keys in earlier blocks + earlier words of the block + bits below
+__global__ void rank_place_kernel(const u64* __restrict__ img, const i64* __restrict__ slot, i64 m,
+                                  u64 lo, const unsigned* __restrict__ bits,
+                                  const unsigned short* __restrict__ wpre,
+                                  const i64* __restrict__ offs, u64* __restrict__ img_out,
+                                  i64* __restrict__ slot_out) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 d = img[i] - lo;
+    const i64 word = (i64)(d >> 5);
+    const i64 r = offs[d >> 10] + wpre[word] + __popc(bits[word] & ((1u << (d & 31)) - 1u));
+    img_out[r] = img[i];
+    slot_out[r] = slot[i];
+  }
+}
+
+i64 rank_words(i64 range) { return (range + 31) / 32; }
+i64 rank_blocks(i64 range) { return (range + 1023) / 1024; }
+
+size_t rank_ws_bytes(i64 range) {
+  const i64 r = range > 0 ? range : 1;
+  const i64 b = rank_blocks(r);
+  return align256((size_t)rank_words(r) * 4) + align256((size_t)rank_words(r) * 2) +
+         2 * align256((size_t)b * 8) + exclusive_scan_workspace(b) + 1024;
 }
 
 __global__ void hashagg_gather_kernel(HashAgg h, const u64* __restrict__ img,
@@ -1373,9 +1454,19 @@ extern "C" {
 
 size_t tdp_groupby_hash_workspace(int64_t n, int32_t naggs) { return hashagg_ws_bytes(n, naggs); }
 
+static int hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
+                        const int32_t* agg_kinds, int32_t naggs, int64_t* out_ngroups,
+                        void* ws, size_t ws_bytes, void* stream, unsigned long long* range);
+
 int tdp_groupby_hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
                              const int32_t* agg_kinds, int32_t naggs, int64_t* out_ngroups,
                              void* ws, size_t ws_bytes, void* stream) {
+  return hash_prepare(keys, n, vals, agg_kinds, naggs, out_ngroups, ws, ws_bytes, stream, nullptr);
+}
+
+static int hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
+                        const int32_t* agg_kinds, int32_t naggs, int64_t* out_ngroups,
+                        void* ws, size_t ws_bytes, void* stream, unsigned long long* range) {
   TDP_REQUIRE(n >= 0 && out_ngroups != nullptr, "bad hash group-by arguments");
   TDP_REQUIRE(ws_bytes >= hashagg_ws_bytes(n, naggs), "hash group-by workspace too small");
   ValSet vs;
@@ -1399,8 +1490,66 @@ int tdp_groupby_hash_prepare(const int64_t* keys, int64_t n, const tdp_column* v
   rc = exclusive_scan_i64(h.flags, h.offs, h.cap + 1, out_ngroups, h.scan_ws, h.scan_bytes, st);
   if (rc) return rc;
   SortBuffers b = carve(ws, n);
-  hashagg_compact_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h, b.k0, b.i0);
+  hashagg_compact_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h, b.k0, b.i0, range);
   TDP_LAUNCH_CHECK("hashagg_compact_kernel");
+  return TDP_OK;
+}
+
+int tdp_groupby_hash_prepare_ex(const int64_t* keys, int64_t n, const tdp_column* vals,
+                                const int32_t* agg_kinds, int32_t naggs, int64_t* out_info,
+                                void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(out_info != nullptr, "null group-by info output");
+  unsigned long long* info = reinterpret_cast<unsigned long long*>(out_info);
+  info_init_kernel<<<1, 1, 0, as_stream(stream)>>>(info);
+  TDP_LAUNCH_CHECK("info_init_kernel");
+  return hash_prepare(keys, n, vals, agg_kinds, naggs, out_info, ws, ws_bytes, stream, info);
+}
+
+size_t tdp_groupby_hash_rank_workspace(int64_t key_range) { return rank_ws_bytes(key_range); }
+
+int tdp_groupby_hash_emit_ranked(int64_t n, const int32_t* agg_kinds, int32_t naggs, int64_t m,
+                                 int64_t min_key, int64_t key_range, int64_t* out_keys,
+                                 int64_t* out_counts, void* out_sums, void* ws, size_t ws_bytes,
+                                 void* rank_ws, size_t rank_ws_bytes_, void* stream) {
+  TDP_REQUIRE(m >= 0 && m <= (n > 0 ? n : 0), "bad group count");
+  TDP_REQUIRE(ws_bytes >= hashagg_ws_bytes(n, naggs), "hash group-by workspace too small");
+  TDP_REQUIRE(m == 0 || (key_range >= m && key_range <= ((int64_t)1 << 36)),
+              "key range %lld cannot hold %lld distinct keys", (long long)key_range, (long long)m);
+  TDP_REQUIRE(m == 0 || rank_ws_bytes_ >= rank_ws_bytes(key_range), "rank workspace too small");
+  if (m == 0) return TDP_OK;
+  ValSet vs;
+  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  if (rc) return rc;
+  vs.naggs = naggs;
+  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
+  cudaStream_t st = as_stream(stream);
+  HashAgg h = carve_hashagg(ws, n, naggs);
+  SortBuffers b = carve(ws, n);
+  const i64 words = rank_words(key_range), blocks = rank_blocks(key_range);
+  unsigned char* p = reinterpret_cast<unsigned char*>(rank_ws);
+  unsigned* bits = (unsigned*)p;
+  p += align256((size_t)words * 4);
+  unsigned short* wpre = (unsigned short*)p;
+  p += align256((size_t)words * 2);
+  i64* counts = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  i64* offs = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  const u64 lo = (u64)min_key ^ 0x8000000000000000ull;
+  TDP_CUDA_TRY(cudaMemsetAsync(bits, 0, (size_t)words * 4, st));
+  rank_bits_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(b.k0, m, lo, bits);
+  TDP_LAUNCH_CHECK("rank_bits_kernel");
+  rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(bits, words, blocks, counts, wpre);
+  TDP_LAUNCH_CHECK("rank_popc_kernel");
+  rc = exclusive_scan_i64(counts, offs, blocks, nullptr, p, exclusive_scan_workspace(blocks) + 512,
+                          st);
+  if (rc) return rc;
+  rank_place_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(b.k0, b.i0, m, lo, bits, wpre,
+                                                                  offs, b.k1, b.i1);
+  TDP_LAUNCH_CHECK("rank_place_kernel");
+  hashagg_gather_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(
+      h, b.k1, b.i1, m, vs, out_keys, out_counts, reinterpret_cast<u64*>(out_sums));
+  TDP_LAUNCH_CHECK("hashagg_gather_kernel");
   return TDP_OK;
 }
 

@@ -719,6 +719,17 @@ def _groupby_sharded(kdata, agg_specs, vdata, group):
 HASH_GROUPBY_MIN_ROWS = 1 << 16
 
 
+# bitmap ranking of hash group-by keys while the key range is at most this many
+# values per distinct key (beyond: radix sort of the distinct keys)
+RANK_BITS_PER_GROUP = 1024
+
+
+def _key_of_image(img: int) -> int:
+    """int64 key of an order-preserving key image (key ^ INT64_MIN) read as int64."""
+    u = (img & (2**64 - 1)) ^ (1 << 63)
+    return u - (1 << 64) if u >= 1 << 63 else u
+
+
 def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
     """One int64 key, hash aggregation (tdp_groupby_hash_*): a pass over the
     rows instead of a sort of them; only the distinct keys are sorted."""
@@ -738,15 +749,25 @@ def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
     kind_arr = (c_int32 * max(1, len(kinds)))(*kinds)
     key = key.contiguous()
     ws = nat.workspace(nat.load().tdp_groupby_hash_workspace(n, len(kinds)), device)
-    ng = torch.empty(1, dtype=torch.int64, device=device)
-    nat.call("tdp_groupby_hash_prepare", nat.ptr(key), n, cols, kind_arr, len(kinds),
-             nat.ptr(ng), nat.ptr(ws), ws.numel(), nat.stream())
-    m = read_int(ng)
+    info = torch.empty(3, dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_hash_prepare_ex", nat.ptr(key), n, cols, kind_arr, len(kinds),
+             nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
+    m, lo_img, hi_img = read_ints(info)  # group count and key range, one read
     keys_out = torch.empty(m, dtype=torch.int64, device=device)
     counts = torch.empty(m, dtype=torch.int64, device=device)
     sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
-    nat.call("tdp_groupby_hash_emit", n, kind_arr, len(kinds), m, nat.ptr(keys_out),
-             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
+    key_range = ((hi_img - lo_img) & (2**64 - 1)) + 1 if m else 0
+    if m and key_range <= min(RANK_BITS_PER_GROUP * m + (1 << 21), 1 << 32):
+        # ascending key order by a bitmap rank over the range (a few
+        # bandwidth-bound passes) instead of a radix sort of the m keys
+        lo_key = _key_of_image(lo_img)
+        rws = nat.workspace(nat.load().tdp_groupby_hash_rank_workspace(key_range), device)
+        nat.call("tdp_groupby_hash_emit_ranked", n, kind_arr, len(kinds), m, lo_key, key_range,
+                 nat.ptr(keys_out), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(),
+                 nat.ptr(rws), rws.numel(), nat.stream())
+    else:
+        nat.call("tdp_groupby_hash_emit", n, kind_arr, len(kinds), m, nat.ptr(keys_out),
+                 nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
     return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
 
 

@@ -357,6 +357,28 @@ def test_replay_with_compact_storage_and_fresh_tables():
         np.testing.assert_allclose(got, otpch.q1(a2)["sum_charge"], rtol=1e-9)
 
 
+@pytest.mark.parametrize("lo,span,distinct", [(-40_000, 80_000, 30_000), (1, 60_000_000, 110_000),
+                                               (2**62, 5_000_000, 70_000),
+                                               (-(2**63), 3_000_000, 20_000)])
+def test_hash_groupby_bitmap_rank_order(lo, span, distinct):
+    """Hash group-by whose distinct keys span a modest range: keys ordered by
+    the bitmap rank (tdp_groupby_hash_emit_ranked) -- ascending like the radix
+    path, incl. negative keys, keys near INT64_MAX and INT64_MIN itself."""
+    from paper_2211_02753_b200.kernels import groupby_exact
+
+    rng = np.random.default_rng(span)
+    pool = lo + rng.choice(span, size=distinct, replace=False).astype(np.int64)
+    pool[0] = lo + span - 1
+    n = 200_000
+    key = pool[rng.integers(0, distinct, size=n)]
+    fv = rng.normal(size=n)
+    keys, aggs = groupby_exact([tq.plain(tq.Tensor(key))], [("count", None), ("sum", tq.Tensor(fv))])
+    ek, ea = orc.groupby_exact([key], [("count", None), ("sum", fv)])
+    np.testing.assert_array_equal(keys[0].cpu().numpy(), ek[0])
+    np.testing.assert_array_equal(aggs[0].cpu().numpy(), ea[0])
+    np.testing.assert_allclose(aggs[1].cpu().numpy(), ea[1], rtol=1e-9, atol=1e-9)
+
+
 @pytest.mark.parametrize("n,distinct", [(70_000, 50), (300_000, 120_000), (1_000_003, 5)])
 def test_hash_groupby_matches_oracle(n, distinct):
     """High-cardinality int64 keys take the hash group-by (warp-combined

@@ -228,6 +228,7 @@ def _inputs(tables) -> set:
 
 
 CAPTURES = [0]  # capture attempts in this process (diagnostics)
+CAPTURE_ATTEMPTS = 2  # failed captures of one state before it runs eagerly for good
 
 
 def _capture(execute, tables, log):
@@ -237,6 +238,9 @@ def _capture(execute, tables, log):
     CAPTURES[0] += 1
     inputs = _inputs(tables)
     torch.cuda.synchronize()
+    # a stale (non-sticky) error left by an unrelated earlier call would make
+    # the first launch check inside the capture fail it
+    nat.load().tdp_clear_error()
     graph = torch.cuda.CUDAGraph()
     launches0 = nat.launch_count()
     try:
@@ -272,6 +276,7 @@ class _Warm:
     def __init__(self, tables):
         self.refs = [weakref.ref(t) for t in tables]
         self.log = None  # hostread._Log
+        self.failures = 0
 
     def alive(self, tables) -> bool:
         return all(r() is t for r, t in zip(self.refs, tables))
@@ -312,10 +317,16 @@ def _lookup(owner, sig, tables, execute):
     if isinstance(ent, _Warm):
         if ent.log is None:  # no finished recording (another thread's, or one that raised)
             return ent
-        ent = _capture(execute, tables, ent.log)
-        entries[sig] = ent
-        if ent == _NOGRAPH:
+        got = _capture(execute, tables, ent.log)
+        if got == _NOGRAPH:
+            # one more attempt on the next sighting (a one-time lazy
+            # initialisation inside the first capture can abort it), then eager
+            ent.failures += 1
+            if ent.failures >= CAPTURE_ATTEMPTS:
+                entries[sig] = _NOGRAPH
             return None
+        ent = got
+        entries[sig] = ent
     entries.move_to_end(sig)
     return ent
 

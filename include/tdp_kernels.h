@@ -122,7 +122,7 @@ void tdp_count_graph_launches(uint64_t n);
  * aborted graph capture); returns the cudaError_t that was pending.        */
 int tdp_clear_error(void);
 /* Replay guard (no reference counterpart: the reference re-plans every run).
- * Enqueue a check that the `n` (<= 8) integers at device `got` (element size
+ * Enqueue a check that the `n` (<= 16) integers at device `got` (element size
  * 4 or 8) equal `expected` (host array): a CUDA graph captured from a plan
  * sized by host reads of those integers traps on a mismatch instead of
  * overrunning buffers.                                                     */

@@ -96,8 +96,10 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
   return TDP_OK;
 }
 
+constexpr int kMaxExpected = 16;  // a dense group-by's key ranges: 2 per key, <= 8 keys
+
 struct Expected {
-  i64 v[8];
+  i64 v[kMaxExpected];
 };
 
 // One thread per value: a replayed plan's device-computed integer must equal
@@ -143,12 +145,13 @@ int tdp_replay_log_end(int64_t* out, int64_t cap) {
 
 int tdp_expect_values(const void* got, int32_t esize, int32_t n, const int64_t* expected,
                       void* stream) {
-  TDP_REQUIRE(n >= 0 && n <= 8, "tdp_expect_values: at most 8 values (got %d)", n);
+  TDP_REQUIRE(n >= 0 && n <= tdp::kMaxExpected, "tdp_expect_values: at most %d values (got %d)",
+              tdp::kMaxExpected, n);
   TDP_REQUIRE(esize == 4 || esize == 8, "tdp_expect_values: element size must be 4 or 8");
   TDP_REQUIRE(n == 0 || (got != nullptr && expected != nullptr), "tdp_expect_values: null pointer");
   if (n == 0) return TDP_OK;
   tdp::Expected e;
-  for (int i = 0; i < 8; ++i) e.v[i] = i < n ? expected[i] : 0;
+  for (int i = 0; i < tdp::kMaxExpected; ++i) e.v[i] = i < n ? expected[i] : 0;
   tdp::expect_values_kernel<<<1, 32, 0, tdp::as_stream(stream)>>>(got, esize, n, e);
   TDP_LAUNCH_CHECK("expect_values_kernel");
   return TDP_OK;

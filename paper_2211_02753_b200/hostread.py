@@ -31,7 +31,7 @@ from . import _native as nat
 
 _TLS = threading.local()
 
-MAX_VALUES = 8  # per read (tdp_expect_values)
+MAX_VALUES = 16  # per read (tdp_expect_values)
 
 
 class ReplayMismatch(RuntimeError):

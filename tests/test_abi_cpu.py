@@ -109,9 +109,9 @@ def test_replay_log_round_trip_and_validation(lib):
     assert lib.tdp_replay_log_size() == 0  # nothing recorded
     out = (c_int64 * 1)()
     assert lib.tdp_replay_log_end(out, 1) == 0
-    expected = (c_int64 * 9)()
-    assert lib.tdp_expect_values(c_void_p(16), 8, 9, expected, None) == EINVAL
-    assert "at most 8" in _err(lib)
+    expected = (c_int64 * 17)()
+    assert lib.tdp_expect_values(c_void_p(16), 8, 17, expected, None) == EINVAL
+    assert "at most 16" in _err(lib)
     assert lib.tdp_expect_values(c_void_p(16), 2, 1, expected, None) == EINVAL
 
 

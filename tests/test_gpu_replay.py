@@ -107,6 +107,29 @@ def test_data_dependent_sizes_replay_from_recorded_reads():
         np.testing.assert_allclose(r.columns[1].values.numpy(), sums, rtol=1e-12)
 
 
+def test_dense_key_ranges_replay_from_recorded_reads():
+    """Two small-range int keys take the dense fused group-by, sized by a host
+    read of both keys' ranges (four values): replayed from the log."""
+    rng = np.random.default_rng(13)
+    n = 30_000
+    a = rng.integers(-50, 50, size=n)
+    b = rng.integers(1000, 1040, size=n)
+    v = rng.random(n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["a", "b", "v"], [tq.plain(tq.Tensor(a)),
+                                                              tq.plain(tq.Tensor(b)),
+                                                              tq.plain(tq.Tensor(v))]))
+    q = wl.compile_sql("SELECT a, b, SUM(v), COUNT(*) FROM t GROUP BY a, b", cat, tq.UdfRegistry())
+    outs = [q.run(cat) for _ in range(4)]
+    assert any(isinstance(e, replay._Replay) for e in q._replays.values())
+    ek, ea = orc.groupby_exact([a, b], [("sum", v), ("count", None)])
+    for r in outs:
+        np.testing.assert_array_equal(r.columns[0].values.numpy(), ek[0])
+        np.testing.assert_array_equal(r.columns[1].values.numpy(), ek[1])
+        np.testing.assert_allclose(r.columns[2].values.numpy(), ea[0], rtol=1e-9)
+        np.testing.assert_array_equal(r.columns[3].values.numpy(), ea[1])
+
+
 def test_uncapturable_plan_falls_back():
     """A UDF body that reads a device value on the host cannot be captured:
     the plan runs eagerly from then on."""

@@ -675,6 +675,20 @@ def _llp(args):
     print(json.dumps(line), flush=True)
 
 
+def _q3_probe_traffic():
+    """ncu DRAM bytes of Q3's dominant kernel (the lineitem join probe) vs its
+    algorithmic bytes, from profiles/roofline_traffic.json (None if absent)."""
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    if not tf.exists():
+        return None
+    ent = json.loads(tf.read_text()).get("q3_sf10_n1_join_probe")
+    if ent is None:
+        return None
+    return {"name": ent["kernel"], "traffic": ent["dram_bytes"], "algorithmic": 0.96e9,
+            "ncu_us": ent["ncu_duration_us"],
+            "note": "traffic ~ algorithmic: issue/latency-bound, not re-reading"}
+
+
 def _q3(args):
     """Q3-style join pipeline (SURVEY config 3) on one GPU -- extra measurement."""
     import torch
@@ -760,7 +774,9 @@ def _q3(args):
                        "re-planned) -> result to host"},
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
                      "achieved": base_bytes / (ms / 1e3) / 1e9,
-                     "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0], "traffic": None,
+                     "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0],
+                     "traffic": None,
+                     "dominant_kernel": _q3_probe_traffic(),
                      "what": "base columns read once (SURVEY §8(d), 2.42 GB at SF10) over the "
                              "whole pipeline time (host synchronisations included)"},
         "parity": "ok" if (got == exp["l_orderkey"]).all() else "MISMATCH",

@@ -1,41 +1,37 @@
 #!/usr/bin/env python
 """Benchmark of the tensor-query hot path on B200.
 
-Default workload: TPC-H Q1 at SF10 (6.0e7 synthetic lineitem rows, 4 groups x
-8 aggregates incl. avg/count), written against the reference's query API
-(SQL + elementwise TvfMap UDF) and executed by this
-package: the plan compiles to Filter -> TvfMap -> GroupAggregate, which runs
-as one fused pass (tdp_scan_aggregate).  ``--query q6`` selects TPC-H Q6.
+Default workload (the BASELINE metric): TPC-H Q1 on a synthetic SF10 lineitem
+table (6.0e7 rows, 4 groups x 8 aggregates incl. avg/count), written against
+the reference's query API (SQL + elementwise TvfMap UDF)
+and executed by this package: Filter -> TvfMap -> GroupAggregate runs as one
+fused pass (tdp_scan_aggregate); a Q6 companion runs on the same table.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--query q1|q6|q3|llp|image] [--sf SF] [--scaling strong|weak]
 
-One process per GPU (torchrun for N > 1): every rank holds an SF10 shard of
-lineitem (the table is SF10 x N -- "weak" scaling, the row-partitioned path
-of SURVEY §8(e)) and the partial aggregates are merged with NCCL all-reduces
-inside the query.  Rank 0 prints one JSON line.
+One process per GPU (torchrun for N > 1).  The table is split into N
+contiguous row shards ("strong" scaling: BASELINE's "row-sharded at 1/2/4/8
+GPUs"); partial aggregates are merged by an NCCL all-reduce inside the query,
+and the whole step (collective included) is replayed as one CUDA graph.
+Rank 0 prints one JSON line; its ``parity`` checks the timed result against
+the oracle over the whole table.
 
 ``--impl reference`` times the reference's algorithm on the host cores: the
-numpy restatement in oracle/ (the reference itself is Python/numpy and cannot
-travel to the GPU host), row-sharded over all cores with multiprocessing.
+numpy restatement in oracle/ (the reference is Python/numpy and cannot be
+installed on the GPU host), row-sharded over all cores with multiprocessing.
+
+Workload modules live in benchmarks/ (tpch.py, q3.py, llp.py, image.py).
 """
 
 from __future__ import annotations
 
 import argparse
-import json
-import os
-import statistics
-import subprocess
 import sys
-import threading
-import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-
-METRIC = "TPC-H Q1/Q6 SF10 rows/sec & HBM GB/s at 1/2/4/8 B200 vs CPU ref"
-HBM_PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
 def _args():
@@ -45,846 +41,49 @@ def _args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--query", choices=("q1", "q6", "q3", "llp", "image"), default="q1")
+    ap.add_argument("--sf", type=float, default=10.0)
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: N row shards of one SF table (BASELINE config 2); "
+                         "weak: one SF shard per rank")
+    ap.add_argument("--encoding", choices=("wide", "compact"), default="wide",
+                    help="compact: lossless narrow column storage (SURVEY §8(f) 1)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-table oracle check of the timed result")
+    ap.add_argument("--no-companion", action="store_true",
+                    help="skip the Q6 companion measurement of the default Q1 run")
     ap.add_argument("--image-rows", type=int, default=10_000_000)
     ap.add_argument("--image-classes", type=int, default=10)
     ap.add_argument("--llp-rows", type=int, default=100_000_000)
     ap.add_argument("--llp-features", type=int, default=64)
-    ap.add_argument("--sf", type=float, default=10.0)
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-companion", action="store_true",
-                    help="skip the Q6 companion measurement of the default Q1 run")
-    ap.add_argument("--encoding", choices=("wide", "compact"), default="wide",
-                    help="compact: lossless narrow column storage (SURVEY §8(f) 1)")
     return ap.parse_args()
-
-
-def _peaks() -> tuple[float, str]:
-    p = ROOT / "MEASURED_PEAKS.json"
-    try:
-        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
-
-
-def _workload(query: str, sf: float, rows: int, encoding: str = "wide", bpr: int = 0) -> dict:
-    if query == "q1":
-        w = {"workload": f"TPC-H Q1 SF{sf:g}: filter l_shipdate<=10471 -> q1prep UDF "
-                         "(disc_price, charge) -> GROUP BY returnflag, linestatus, 8 aggregates",
-             "sf": sf, "rows": rows, "bytes_per_row": 56,
-             "columns": "7 x 8 B (int64 dates/dictionary codes, float64 values)"}
-    else:
-        w = {"workload": f"TPC-H Q6 SF{sf:g}: 5-predicate filter -> revenue UDF -> SUM",
-             "sf": sf, "rows": rows, "bytes_per_row": 32,
-             "columns": "4 x 8 B (int64 shipdate, float64 values)"}
-    if encoding == "compact":
-        w["bytes_per_row"] = bpr
-        w["columns"] = ("compact storage (SURVEY §8(f) 1): int16 dates, uint8 dictionary codes, "
-                        "scaled-decimal int8/int32 values; decoded values bit-identical to the "
-                        "8 B reference columns")
-        w["encoding"] = "compact"
-    return w
-
-
-# ---------------------------------------------------------------------------
-# clocks during the timed region
-# ---------------------------------------------------------------------------
-
-class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown")
-
-    def __init__(self, gpu_id: str):
-        self.samples: list[list[str]] = []
-        self.proc = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            return
-        self._first = threading.Event()
-        self.active = False
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
-        self._first.wait(timeout=5.0)
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self._first.set()
-            if self.active:
-                self.samples.append([x.strip() for x in line.split(",")])
-
-    def stop(self) -> dict | None:
-        if self.proc is None:
-            return None
-        self.active = False
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
-
-
-# ---------------------------------------------------------------------------
-# kernel timing hook (CUDA events on the launching stream)
-# ---------------------------------------------------------------------------
-
-class KernelTimer:
-    def __init__(self):
-        import torch
-
-        self.torch = torch
-        self.pending: list = []
-        self.rows: list[int] = []
-
-    def begin(self, name, rows):
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
-        self.pending.append([e, None])
-        self.rows.append(int(rows))
-
-    def end(self, name):
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
-        self.pending[-1][1] = e
-
-    def mean_ms(self) -> float | None:
-        if not self.pending:
-            return None
-        return statistics.mean(a.elapsed_time(b) for a, b in self.pending)
-
-
-# ---------------------------------------------------------------------------
-# our implementation
-# ---------------------------------------------------------------------------
-
-def _ours(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    import paper_2211_02753_b200 as tq
-    from paper_2211_02753_b200 import _native, kernels as K, workloads as wl
-    from paper_2211_02753_b200.distributed import sharded
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # TDP_DIST_BACKEND=gloo + TDP_ONE_GPU=1 exercise the multi-rank code path on
-    # a single-GPU host (every rank on cuda:0); production runs use NCCL.
-    if os.environ.get("TDP_ONE_GPU") == "1":
-        local = 0
-    torch.cuda.set_device(local)
-    if world > 1:
-        backend = os.environ.get("TDP_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    group = dist.group.WORLD if world > 1 else None
-
-    rows = int(round(6_000_000 * args.sf))  # per rank (weak scaling)
-    n_total = rows * world
-    arrays = wl.lineitem_arrays(args.sf, seed=42 + rank, rows=rows)
-    cols = wl.LINEITEM_COLUMNS
-    if args.query == "q1":
-        sql, reg, bpr = wl.Q1_SQL, wl.q1_registry(), wl.Q1_BYTES_PER_ROW
-    else:
-        sql, reg, bpr = wl.Q6_SQL, wl.q6_registry(), wl.Q6_BYTES_PER_ROW
-        cols = ("l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
-
-    table = wl.lineitem_table(arrays, cols)
-    if args.encoding == "compact":  # ingestion, outside the timed region
-        from paper_2211_02753_b200 import compact as cp
-
-        table = cp.compact_table(table)
-        bpr = sum(cp.stored_bytes(c) for c in table.columns)
-    cat = tq.Catalog()
-    cat.register("lineitem", table)
-    query = wl.compile_sql(sql, cat, reg)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    with sharded(group):
-        for _ in range(max(args.warmup, 3)):
-            result = query.run(cat)
-        torch.cuda.synchronize()
-        # parity of the warm-up result on rank 0 at N=1 is checked after timing
-        uuid = str(torch.cuda.get_device_properties(local).uuid)
-        sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
-        launches0 = _native.launch_count()
-        barrier()
-        torch.cuda.synchronize()
-        sampler.active = True
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(args.steps):
-            result = query.run(cat)
-        t1.record()
-        torch.cuda.synchronize()
-        barrier()
-        clocks = sampler.stop()
-        launches = _native.launch_count() - launches0
-        ms = t0.elapsed_time(t1) / args.steps
-        # kernel timer: CUDA events recorded by libtdp_kernels on the launch
-        # stream right around each tdp_scan_agg launch (after host prep), over
-        # the same number of eager runs (a replayed CUDA graph cannot record
-        # the library's events; the kernel and its inputs are the same)
-        import ctypes as _ct
-
-        os.environ["TDP_REPLAY"] = "0"
-        _native.load().tdp_kernel_timer_enable(1)
-        _native.load().tdp_kernel_timer_read(None, None)
-        barrier()
-        for _ in range(args.steps):
-            result = query.run(cat)
-        torch.cuda.synchronize()
-        _native.load().tdp_kernel_timer_enable(0)
-        os.environ.pop("TDP_REPLAY", None)
-        _tot, _cnt = _ct.c_double(0.0), _ct.c_int64(0)
-        _native.load().tdp_kernel_timer_read(_ct.byref(_tot), _ct.byref(_cnt))
-        kernel_ms = _tot.value / _cnt.value if _cnt.value else None
-        if world > 1:
-            t = torch.tensor([ms, kernel_ms or 0.0], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms, kernel_ms = float(t[0]), float(t[1])
-            lt = torch.tensor([launches], dtype=torch.int64, device="cuda")
-            dist.all_reduce(lt, op=dist.ReduceOp.SUM)
-            launches = int(lt.item())
-
-        # ---- companion Q6 on the same shard (the metric names Q1 and Q6) ---
-        companion = None
-        if args.query == "q1" and not args.no_companion:
-            q6 = wl.compile_sql(wl.Q6_SQL, cat, wl.q6_registry())
-            for _ in range(3):
-                q6.run(cat)
-            barrier()
-            torch.cuda.synchronize()
-            c0 = torch.cuda.Event(enable_timing=True)
-            c1 = torch.cuda.Event(enable_timing=True)
-            c0.record()
-            for _ in range(args.steps):
-                r6 = q6.run(cat)
-            c1.record()
-            torch.cuda.synchronize()
-            barrier()
-            ms6 = c0.elapsed_time(c1) / args.steps
-            os.environ["TDP_REPLAY"] = "0"
-            _native.load().tdp_kernel_timer_enable(1)
-            _native.load().tdp_kernel_timer_read(None, None)
-            for _ in range(args.steps):
-                r6 = q6.run(cat)
-            torch.cuda.synchronize()
-            _native.load().tdp_kernel_timer_enable(0)
-            os.environ.pop("TDP_REPLAY", None)
-            _native.load().tdp_kernel_timer_read(_ct.byref(_tot), _ct.byref(_cnt))
-            k6 = _tot.value / _cnt.value if _cnt.value else 0.0
-            if world > 1:
-                t = torch.tensor([ms6, k6], dtype=torch.float64, device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms6, k6 = float(t[0]), float(t[1])
-            b6 = wl.Q6_BYTES_PER_ROW if args.encoding == "wide" else None
-            companion = {"workload": f"TPC-H Q6 SF{args.sf * world:g} on the same lineitem shards",
-                         "value": n_total / (ms6 / 1e3), "unit": "rows/s", "ms_per_step": ms6,
-                         "kernel_ms": k6}
-            if b6 and k6:
-                companion["hbm_gbs_kernel"] = b6 * rows / (k6 / 1e3) / 1e9
-            companion["result"] = float(r6.columns[0].values.numpy()[0]) if rank == 0 else None
-
-        # ---- end to end through the API from pinned host buffers ----------
-        if args.encoding == "compact":
-            from paper_2211_02753_b200 import compact as cp
-
-            host_stored = [t.cpu().pin_memory() for t in cp.stored_tensors(table)]
-            h2d = sum(h.numel() * h.element_size() for h in host_stored)
-
-            def make_table():
-                dev = [h.to("cuda", non_blocking=True) for h in host_stored]
-                return cp.table_from_stored(table, dev)
-        else:
-            host = {c: torch.from_numpy(arrays[c]).pin_memory() for c in cols}
-            h2d = sum(h.numel() * h.element_size() for h in host.values())
-
-            def make_table():
-                return wl.lineitem_table(host, cols)
-
-        def e2e_step():
-            c2 = tq.Catalog()
-            c2.register("lineitem", make_table())
-            out = query.run(c2)
-            vals = [c.values.numpy() for c in out.columns]
-            return sum(v.nbytes for v in vals)
-
-        e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        w0 = time.perf_counter()
-        d2h = 0
-        for _ in range(args.e2e_steps):
-            d2h = e2e_step()
-        torch.cuda.synchronize()
-        barrier()
-        e2e_s = (time.perf_counter() - w0) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t[0])
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    peak, peak_src = _peaks()
-    value = n_total / (ms / 1e3)
-    kernel_rows = rows
-    achieved = bpr * kernel_rows / (kernel_ms / 1e3) / 1e9 if kernel_ms else None
-    traffic = None
-    tf = ROOT / "profiles" / "roofline_traffic.json"
-    if tf.exists():
-        try:
-            tj = json.loads(tf.read_text())
-            sfx = "_compact" if args.encoding == "compact" else ""
-            # weak scaling: every rank's launch scans one SF shard, as at N=1
-            traffic = tj.get(f"{args.query}_sf{args.sf:g}_n{world}{sfx}",
-                             tj.get(f"{args.query}_sf{args.sf:g}_n1{sfx}"))
-        except Exception:
-            traffic = None
-    line = {
-        "metric": METRIC,
-        "value": value,
-        "unit": "rows/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": max(args.warmup, 3),
-        "ms_per_step": ms,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), resident in HBM",
-        "config": dict(_workload(args.query, args.sf * world, n_total, args.encoding, bpr),
-                       sf_per_gpu=args.sf,
-                       parallelism=f"dp{world}: one SF{args.sf:g} lineitem shard per GPU, "
-                                   f"NCCL all-reduce of partial aggregates",
-                       l2="inputs larger than L2 (no flush needed)",
-                       step="CompiledQuery.run(catalog) of the SQL plan (exact plan over an "
-                            "unchanged catalog: CUDA-graph replay of its launches), result "
-                            "table on device"),
-        "hbm_gbs_step": bpr * n_total / (ms / 1e3) / 1e9,
-        "e2e": {"value": n_total / e2e_s, "unit": "rows/s", "h2d_bytes_per_step": h2d * world,
-                "d2h_bytes_per_step": d2h,
-                "h2d_gbs_per_rank": h2d / e2e_s / 1e9,
-                "how": "pinned host columns -> device table -> CompiledQuery.run -> result to host "
-                       "(bound by the host->device link: h2d_gbs_per_rank)"},
-        "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "tdp_scan_agg (fused filter+UDF+group-by), per rank, "
-                               "timed by library events over eager runs",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_source": peak_src, "kernel_ms": kernel_ms,
-                     "algorithmic_bytes_per_launch": bpr * kernel_rows},
-        "clocks": clocks,
-    }
-    if companion is not None:
-        companion["peak_frac_kernel"] = (companion["hbm_gbs_kernel"] / peak
-                                         if "hbm_gbs_kernel" in companion else None)
-        line["companion_q6"] = companion
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"], line["parity"] = _cpu_baseline(args, arrays, query, cat)
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-def _cpu_baseline(args, arrays, query, cat):
-    """Oracle (numpy restatement of the reference path) on a bounded sample,
-    one host core; plus a parity check of the engine on the same sample."""
-    import numpy as np
-
-    import paper_2211_02753_b200 as tq
-    from oracle import tpch as otpch
-    from paper_2211_02753_b200 import workloads as wl
-
-    sample_rows = min(len(arrays["l_shipdate"]), 6_000_000)
-    sample = {k: v[:sample_rows] for k, v in arrays.items()}
-    fn = otpch.q1 if args.query == "q1" else otpch.q6
-    reps, t = 0, 0.0
-    exp = None
-    while t < 10.0 and reps < 20:
-        w0 = time.perf_counter()
-        exp = fn(sample)
-        t += time.perf_counter() - w0
-        reps += 1
-    rate = reps * sample_rows / t
-    # parity of the engine on the same sample
-    c2 = tq.Catalog()
-    cols = wl.LINEITEM_COLUMNS if args.query == "q1" else (
-        "l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
-    t2 = wl.lineitem_table(sample, cols)
-    if args.encoding == "compact":
-        from paper_2211_02753_b200 import compact as cp
-
-        t2 = cp.compact_table(t2)
-    c2.register("lineitem", t2)
-    res = query.run(c2)
-    got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
-    ok = True
-    for k, v in exp.items():
-        g = got[k]
-        if v.dtype.kind in "iu":
-            ok &= bool(np.array_equal(g, v))
-        else:
-            ok &= bool(np.allclose(g, v, rtol=1e-9, atol=0))
-    return ({"value": rate, "unit": "rows/s", "cores": 1, "kind": "port",
-             "sample": f"{sample_rows} rows (first SF{sample_rows / 6e6:g} of the shard) x {reps} "
-                       f"repetitions, oracle/tpch.py (numpy restatement of tq filter_exact -> "
-                       f"UDF -> groupby_exact)"},
-            {"status": "ok" if ok else "MISMATCH", "rows": sample_rows,
-             "rule": "keys/counts bit-exact, float aggregates rtol 1e-9 vs float64 oracle"})
-
-
-# ---------------------------------------------------------------------------
-# reference arm: the reference algorithm on all host cores
-# ---------------------------------------------------------------------------
-
-_REF_ARRAYS: dict = {}
-
-
-def _ref_worker(task):
-    import numpy as np
-
-    from oracle import relational as orc
-
-    query, lo, hi = task
-    a = {k: v[lo:hi] for k, v in _REF_ARRAYS.items()}
-    if query == "q1":
-        cols = [a[c] for c in ("l_shipdate", "l_returnflag", "l_linestatus", "l_quantity",
-                               "l_extendedprice", "l_discount", "l_tax")]
-        ship, rf, ls, q, p, d, t = orc.filter_exact(cols, [(0, "<=", 10471)])
-        one = np.asarray(1.0)
-        dp = p * (one - d)
-        ch = dp * (one + t)
-        keys, aggs = orc.groupby_exact([rf, ls], [("sum", q), ("sum", p), ("sum", dp),
-                                                  ("sum", ch), ("sum", d), ("count", None)])
-        return [k.tolist() for k in keys], [x.tolist() for x in aggs]
-    cols = [a[c] for c in ("l_shipdate", "l_discount", "l_quantity", "l_extendedprice")]
-    ship, d, q, p = orc.filter_exact(cols, [(0, ">=", 8766), (0, "<", 9131), (1, ">=", 0.05),
-                                            (1, "<=", 0.07), (2, "<", 24)])
-    return float((p * d).sum()), len(p)
-
-
-def _reference(args):
-    import multiprocessing as mp
-
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from paper_2211_02753_b200 import workloads as wl
-
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    n_total = int(round(6_000_000 * args.sf)) * world  # our arm's table: SF10 per GPU
-    # calibrate one core, then size the per-step sample so the run stays short
-    cal = wl.lineitem_arrays(args.sf, seed=42, rows=1_000_000)
-    _REF_ARRAYS.clear()
-    _REF_ARRAYS.update(cal)
-    w0 = time.perf_counter()
-    _ref_worker((args.query, 0, len(cal["l_shipdate"])))
-    per_core = len(cal["l_shipdate"]) / (time.perf_counter() - w0)
-    budget_s = max(0.05, 150.0 / max(1, args.steps + args.warmup))
-    sample = int(min(6_000_000 * args.sf, per_core * cores * budget_s))
-    sample = max(sample, cores)
-    arrays = wl.lineitem_arrays(args.sf, seed=42, rows=sample)
-    _REF_ARRAYS.clear()
-    _REF_ARRAYS.update(arrays)
-    bounds = [(args.query, i * sample // cores, (i + 1) * sample // cores) for i in range(cores)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        for _ in range(args.warmup):
-            pool.map(_ref_worker, bounds)
-        times = []
-        for _ in range(args.steps):
-            w0 = time.perf_counter()
-            parts = pool.map(_ref_worker, bounds)
-            _merge(args.query, parts)
-            times.append(time.perf_counter() - w0)
-    step_s = statistics.mean(times)
-    value = sample / step_s
-    line = {
-        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded dbgen-like lineitem, SURVEY Appendix B), in host RAM",
-        "config": dict(_workload(args.query, args.sf * world, n_total), sf_per_gpu=args.sf,
-                       parallelism=f"{cores} host processes, row-sharded, partials merged"),
-        "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} rows per step (bounded sample of SF{args.sf:g}), "
-                                   f"oracle/ numpy restatement of the reference path on "
-                                   f"{cores} processes"},
-        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _merge(query, parts):
-    if query == "q6":
-        return sum(p[0] for p in parts)
-    acc: dict = {}
-    for keys, aggs in parts:
-        for g in range(len(keys[0])):
-            key = tuple(k[g] for k in keys)
-            cur = acc.setdefault(key, [0.0] * (len(aggs) - 1) + [0])
-            for a in range(len(aggs)):
-                cur[a] += aggs[a][g]
-    out = {}
-    for key in sorted(acc):
-        s = acc[key]
-        cnt = s[-1]
-        out[key] = s[:5] + [s[0] / cnt, s[1] / cnt, s[4] / cnt, cnt]
-    return out
-
-
-# ---------------------------------------------------------------------------
-# LLP trainable step (SURVEY config 4) -- extra measurement, not the headline
-# ---------------------------------------------------------------------------
-
-def _llp(args):
-    import numpy as np
-    import torch
-
-    import paper_2211_02753_b200 as tq
-    from paper_2211_02753_b200 import _native
-    from paper_2211_02753_b200.storage import tensor_type
-    from paper_2211_02753_b200.training import TrainConfig
-
-    torch.cuda.set_device(0)
-    n, d, bags = args.llp_rows, args.llp_features, 1000
-    g = torch.Generator(device="cuda").manual_seed(0)
-    X = torch.randn(n, d, generator=g, device="cuda", dtype=torch.float32)
-    bag = torch.randint(0, bags, (n,), generator=g, device="cuda", dtype=torch.int64)
-    Wstar = torch.randn(d, 2, generator=g, device="cuda", dtype=torch.float32)
-    labels = torch.argmax(X @ Wstar, dim=1)
-    target = torch.zeros(bags * 2, dtype=torch.float64, device="cuda")
-    target.index_add_(0, bag * 2 + labels, torch.ones(n, dtype=torch.float64, device="cuda"))
-    del labels
-    model = tq.Linear(d, 2, np.random.default_rng(0), name="lin")
-    bag_pe = tq.one_hot_pe(bag, bags)
-    reg = tq.UdfRegistry()
-    reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(2))), 1,
-                             lambda c: (bag_pe, tq.pe_encode(model(c.values))), model.parameters))
-    cat = tq.Catalog()
-    Xt = tq.Tensor(X)
-    cat.register_tensor(Xt, "T")
-    q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
-        "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"), cat, reg)),
-        tq.CompileConfig(trainable=True), reg)
-    tgt = tq.Tensor(target)
-    batches = [("T", Xt, tgt)]
-    # the reference's training loop (tq/training.py:121): K iterations of
-    # register -> run -> MSE -> backward -> Adam, losses returned as floats
-    losses = tq.train(q, cat, batches, TrainConfig(iterations=max(args.warmup, 3), lr=0.01))
-    torch.cuda.synchronize()
-    launches0 = _native.launch_count()
-    uuid = str(torch.cuda.get_device_properties(0).uuid)
-    sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    steps = max(1, min(args.steps, 20))
-    sampler.active = True
-    t0.record()
-    losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
-    t1.record()
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    ms = t0.elapsed_time(t1) / steps
-    launches = _native.launch_count() - launches0
-    # exact swap of the trained query (SURVEY §8(f) rank 2): pe_decode ->
-    # exact COUNT BY (Bag, Pred), one pass over X (tdp_linear_argmax_count)
-    exact = q.swap_to_exact()
-    for _ in range(3):
-        res = exact.run(cat)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        res = exact.run(cat)
-    e1.record()
-    torch.cuda.synchronize()
-    swap_ms = e0.elapsed_time(e1) / steps
-    swap_groups = int(res.row_count)
-    # CPU baseline: the closed-form oracle of the reference's step, one core
-    from oracle import relational as orc
-
-    m = 100_000
-    Xh = X[:m].double().cpu().numpy()
-    bh = bag[:m].cpu().numpy()
-    Wh = model.weight.value.numpy().astype(np.float64)
-    bb = model.bias.value.numpy().astype(np.float64)
-    th = np.zeros(bags * 2)
-    w0 = time.perf_counter()
-    reps = 0
-    while time.perf_counter() - w0 < 5.0:
-        orc.llp_forward_backward(Xh, bh, Wh, bb, th, bags)
-        reps += 1
-    cpu_s = (time.perf_counter() - w0) / reps
-    line = {
-        "metric": "LLP trainable query step latency (SURVEY config 4)",
-        "value": ms, "unit": "ms/step", "higher_is_better": False, "n_gpus": 1,
-        "steps": steps, "warmup": max(args.warmup, 3), "rows_per_s": n / (ms / 1e3),
-        "dtype": "f32 model, f64 grid", "data": "synthetic X ~ N(0,1), bags ~ U{0..999}",
-        "config": {"workload": f"SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred "
-                               f"(trainable), Linear({d},2) -> pe_encode, one_hot_pe bag, MSE, Adam",
-                   "step": "one iteration of tq.train() (K iterations per call, losses read back at the end)",
-                   "rows": n, "features": d, "bags": bags},
-        "gpu_launches": launches, "losses": losses[:3] + losses[-2:], "clocks": clocks,
-        "cpu_baseline": {"value": cpu_s / m * n * 1e3, "unit": "ms/step (linear extrapolation)",
-                         "cores": 1, "kind": "port",
-                         "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
-                                   f"reference tape), {reps} reps, extrapolated to {n} rows"},
-        "bytes_floor_ms": (8 * d + 16) * n / _peaks()[0] / 1e9 * 1e3,
-        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
-                     "achieved": (8 * d + 16) * n / (ms / 1e3) / 1e9,
-                     "frac": (8 * d + 16) * n / (ms / 1e3) / 1e9 / _peaks()[0],
-                     "traffic": None,
-                     "what": "algorithmic bytes of the step (X read twice + bag codes twice, "
-                             "2 (4d + 8) B/row = 528 at d=64, SURVEY §8(d)) over the step time"},
-        "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
-                       "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
-                       "what": "q.swap_to_exact().run(cat): pe_decode + exact COUNT by (Bag, Pred); "
-                               "one pass over X + bag codes (tdp_linear_argmax_count)"},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _q3_probe_traffic():
-    """ncu DRAM bytes of Q3's dominant kernel (the lineitem join probe) vs its
-    algorithmic bytes, from profiles/roofline_traffic.json (None if absent)."""
-    tf = ROOT / "profiles" / "roofline_traffic.json"
-    if not tf.exists():
-        return None
-    ent = json.loads(tf.read_text()).get("q3_sf10_n1_join_probe")
-    if ent is None:
-        return None
-    return {"name": ent["kernel"], "traffic": ent["dram_bytes"], "algorithmic": 0.96e9,
-            "ncu_us": ent["ncu_duration_us"],
-            "note": "traffic ~ algorithmic: issue/latency-bound, not re-reading"}
-
-
-def _q3(args):
-    """Q3-style join pipeline (SURVEY config 3) on one GPU -- extra measurement."""
-    import torch
-
-    from oracle import tpch as otpch
-    from paper_2211_02753_b200 import _native, workloads as wl
-
-    torch.cuda.set_device(0)
-    tables = wl.q3_arrays(args.sf, seed=7)
-    cat = wl.q3_catalog(tables)
-    plan = wl.Q3Plan(cat)
-    for _ in range(max(args.warmup, 3)):
-        res = plan.run(cat)
-    torch.cuda.synchronize()
-    uuid = str(torch.cuda.get_device_properties(0).uuid)
-    sampler = ClockSampler("GPU-" + uuid if not uuid.startswith("GPU-") else uuid)
-    launches0 = _native.launch_count()
-    steps = max(1, min(args.steps, 50))
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    sampler.active = True
-    t0.record()
-    for _ in range(steps):
-        res = plan.run(cat)
-    t1.record()
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    ms = t0.elapsed_time(t1) / steps
-    launches = _native.launch_count() - launches0
-    # the same pipeline re-planned on the host every step (no graph replay)
-    for _ in range(max(args.warmup, 3)):
-        plan.run_eager(cat)
-    torch.cuda.synchronize()
-    t0.record()
-    for _ in range(steps):
-        plan.run_eager(cat)
-    t1.record()
-    torch.cuda.synchronize()
-    eager_ms = t0.elapsed_time(t1) / steps
-    # end to end through the API: pinned host columns copied in every step (a
-    # new catalog, so the plan runs eagerly), the result read back
-    host = {t: {c: torch.from_numpy(v).pin_memory() for c, v in cols.items()}
-            for t, cols in tables.items()}
-    h2d = sum(h.numel() * h.element_size() for cols in host.values() for h in cols.values())
-
-    def e2e_step():
-        out = plan.run(wl.q3_catalog(host))
-        return sum(c.values.numpy().nbytes for c in out.columns)
-
-    e2e_step()
-    torch.cuda.synchronize()
-    e2e_steps = max(1, min(args.e2e_steps, 5))
-    w0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        d2h = e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - w0) / e2e_steps
-    nli = len(tables["lineitem"]["l_orderkey"])
-    base_bytes = (16 * len(tables["customer"]["c_custkey"]) + 32 * len(tables["orders"]["o_orderkey"])
-                  + 32 * nli)
-    w0 = time.perf_counter()
-    exp = otpch.q3(tables)
-    cpu_s = time.perf_counter() - w0
-    got = res.columns[0].values.numpy()
-    line = {
-        "metric": "TPC-H Q3-style join pipeline (SURVEY config 3)", "value": nli / (ms / 1e3),
-        "unit": "lineitem rows/s", "ms_per_step": ms, "higher_is_better": True, "n_gpus": 1,
-        "steps": steps, "warmup": max(args.warmup, 3), "dtype": "f64",
-        "data": "synthetic Appendix-B customer/orders/lineitem, seed 7",
-        "config": {"workload": f"Q3-style SF{args.sf:g}: 3 SQL filters, orders|><|customer, "
-                               f"lineitem|><|orders, GROUP BY l_orderkey, ORDER BY sum_rev DESC LIMIT 10",
-                   "customer": len(tables["customer"]["c_custkey"]),
-                   "orders": len(tables["orders"]["o_orderkey"]), "lineitem": nli,
-                   "joined_rows": int(exp["joined_rows"])},
-        "hbm_gbs_base_columns": base_bytes / (ms / 1e3) / 1e9, "gpu_launches": launches,
-        "replay": "one CUDA graph of the whole plan per step (replay.Pipeline; every kernel runs "
-                  "over all rows, data-dependent sizes from the recorded eager run, checked on "
-                  "the device)",
-        "eager_ms_per_step": eager_ms, "clocks": clocks,
-        "e2e": {"value": nli / e2e_s, "unit": "lineitem rows/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "h2d_gbs": h2d / e2e_s / 1e9,
-                "how": "pinned host columns -> q3_catalog -> Q3Plan.run (a new catalog: "
-                       "re-planned) -> result to host"},
-        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": _peaks()[0],
-                     "achieved": base_bytes / (ms / 1e3) / 1e9,
-                     "frac": base_bytes / (ms / 1e3) / 1e9 / _peaks()[0],
-                     "traffic": None,
-                     "dominant_kernel": _q3_probe_traffic(),
-                     "what": "base columns read once (SURVEY §8(d), 2.42 GB at SF10) over the "
-                             "whole pipeline time (host synchronisations included)"},
-        "parity": "ok" if (got == exp["l_orderkey"]).all() else "MISMATCH",
-        "cpu_baseline": {"value": nli / cpu_s, "unit": "lineitem rows/s", "cores": 1,
-                         "kind": "port", "sample": f"full SF{args.sf:g}, oracle/tpch.py q3 once"},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _image(args):
-    """Image query (SURVEY config 5): GROUP BY the PE output of a random-init CNN
-    UDF over 1e7 synthetic 28x28 images, counts fed to an MSE loss, trained
-    with tq.train().  The CNN runs in cuDNN (library code, float32 without
-    TF32); the framework's own kernels are the softmax / soft group-by count
-    forward and backward.  Their share of the step is taken from one
-    torch.profiler pass after the timed region (diagnostic only)."""
-    import numpy as np
-    import torch
-    from torch.profiler import ProfilerActivity, profile
-
-    import paper_2211_02753_b200 as tq
-    from paper_2211_02753_b200 import _native
-    from paper_2211_02753_b200.models import TorchModel
-    from paper_2211_02753_b200.training import TrainConfig
-
-    torch.cuda.set_device(0)
-    torch.backends.cudnn.allow_tf32 = False
-    torch.backends.cuda.matmul.allow_tf32 = False
-    torch.backends.cudnn.benchmark = True
-    n, k = args.image_rows, args.image_classes
-    g = torch.Generator(device="cuda").manual_seed(3)
-    images = torch.rand(n, 28, 28, generator=g, device="cuda", dtype=torch.float32)
-    torch.manual_seed(0)
-    net = torch.nn.Sequential(
-        torch.nn.Unflatten(1, (1, 28)),
-        torch.nn.Conv2d(1, 8, 3), torch.nn.ReLU(), torch.nn.MaxPool2d(2),
-        torch.nn.Conv2d(8, 16, 3), torch.nn.ReLU(), torch.nn.MaxPool2d(2),
-        torch.nn.Flatten(), torch.nn.Linear(400, k)).cuda()
-    chunk = 1 << 18
-    model = TorchModel(net, "cnn", chunk_rows=chunk)
-    reg = tq.UdfRegistry()
-    reg.register(tq.classifier_tvf("cnn", model, k, "Pred"))
-    cat = tq.Catalog()
-    X = tq.Tensor(images)
-    cat.register_tensor(X, "imgs")
-    q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
-        "SELECT Pred, COUNT(*) FROM cnn(imgs) GROUP BY Pred"), cat, reg)),
-        tq.CompileConfig(trainable=True), reg)
-    target = torch.full((k,), n / k, dtype=torch.float32, device="cuda")
-    target[0] *= 1.5
-    target[1] *= 0.5
-    batches = [("imgs", X, tq.Tensor(target))]
-    losses = tq.train(q, cat, batches, TrainConfig(iterations=max(args.warmup, 3), lr=0.01))
-    torch.cuda.synchronize()
-    launches0 = _native.launch_count()
-    steps = max(1, min(args.steps, 5))
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
-    t1.record()
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / steps
-    launches = _native.launch_count() - launches0
-    # diagnostic: share of one step's device time in this framework's kernels
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        tq.train(q, cat, batches, TrainConfig(iterations=1, lr=0.01))
-        torch.cuda.synchronize()
-    ours = total = 0.0
-    for e in prof.events():
-        if e.device_type == torch.autograd.DeviceType.CUDA:
-            t = e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
-            total += t
-            if "tdp::" in e.name:
-                ours += t
-    line = {
-        "metric": "Image query step latency (SURVEY config 5)", "value": ms, "unit": "ms/step",
-        "higher_is_better": False, "n_gpus": 1, "steps": steps, "warmup": max(args.warmup, 3),
-        "images_per_s": n / (ms / 1e3), "dtype": "f32 (cuDNN convolutions without TF32)",
-        "data": "synthetic images U[0,1) (seed 3), random-init CNN",
-        "config": {"workload": "SELECT Pred, COUNT(*) FROM cnn(imgs) GROUP BY Pred (trainable), "
-                               "CNN conv(1-8,3)+ReLU+pool2 -> conv(8-16,3)+ReLU+pool2 -> FC(400,k) "
-                               "-> pe_encode, MSE, Adam",
-                   "images": n, "classes": k, "chunk_rows": chunk,
-                   "step": "one iteration of tq.train(); CNN activations checkpointed per chunk"},
-        "gpu_launches": launches,
-        "framework_kernel_share": ours / total if total else None,
-        "framework_kernel_ms": ours / 1e3,
-        "losses": losses[:2] + losses[-2:],
-    }
-    print(json.dumps(line), flush=True)
 
 
 def main():
     args = _args()
-    if args.query == "llp":
-        _llp(args)
+    if args.query in ("llp", "image", "q3"):
+        import os
+
+        if int(os.environ.get("RANK", "0")) != 0:
+            return  # single-GPU workloads: extra ranks have nothing to do
+        if args.impl == "reference":
+            import json
+
+            print(json.dumps({"impl": "reference", "unavailable":
+                              f"--query {args.query} has no host reference arm; its line carries "
+                              f"cpu_baseline"}))
+            return
+        from benchmarks import image, llp, q3
+
+        {"llp": llp, "image": image, "q3": q3}[args.query].run(args)
         return
-    if args.query == "image":
-        _image(args)
-        return
-    if args.query == "q3":
-        _q3(args)
-        return
+    from benchmarks import tpch
+
     if args.impl == "reference":
-        _reference(args)
+        tpch.run_reference(args)
     else:
-        _ours(args)
+        tpch.run_ours(args)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,197 @@
+"""LLP trainable query step (BASELINE config 4): 1e8 rows x 64 features,
+1000 bags, SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred."""
+
+from __future__ import annotations
+
+import json
+import time
+
+from .common import ClockSampler, cpu_model, peaks, sustain
+
+
+def f64_step_reference(X, bag, W, b, target, bags: int, chunk: int = 1 << 22):
+    """Count grid, MSE-loss gradient dW / db of one LLP step recomputed in
+    float64 with torch over chunks of X (the checker: the closed forms of the
+    reference tape, in double precision)."""
+    import torch
+
+    Wd, bd = W.double(), b.double()
+    n = X.shape[0]
+    grid = torch.zeros(bags * 2, dtype=torch.float64, device=X.device)
+    for lo in range(0, n, chunk):
+        P = torch.softmax(X[lo:lo + chunk].double() @ Wd + bd, dim=1)
+        cell = bag[lo:lo + chunk] * 2
+        grid.index_add_(0, cell, P[:, 0])
+        grid.index_add_(0, cell + 1, P[:, 1])
+    G = 2.0 * (grid - target) / grid.numel()  # d mean((grid - t)^2) / d grid
+    G2 = G.view(bags, 2)
+    dW = torch.zeros_like(Wd)
+    db = torch.zeros_like(bd)
+    for lo in range(0, n, chunk):
+        x = X[lo:lo + chunk].double()
+        P = torch.softmax(x @ Wd + bd, dim=1)
+        g = G2[bag[lo:lo + chunk]]
+        dZ = P * (g - (P * g).sum(dim=1, keepdim=True))
+        dW += x.T @ dZ
+        db += dZ.sum(dim=0)
+    return grid, dW, db
+
+
+def _rel(got, ref) -> float:
+    import torch
+
+    scale = float(ref.abs().max())
+    return float((got.double() - ref).abs().max()) / max(scale, 1e-300)
+
+
+def run(args) -> None:
+    import numpy as np
+    import torch
+
+    import paper_2211_02753_b200 as tq
+    from paper_2211_02753_b200 import _native
+    from paper_2211_02753_b200.storage import tensor_type
+    from paper_2211_02753_b200.tensor import backward
+    from paper_2211_02753_b200.training import TrainConfig, mse_loss, prediction_vector
+
+    torch.cuda.set_device(0)
+    n, d, bags = args.llp_rows, args.llp_features, 1000
+    g = torch.Generator(device="cuda").manual_seed(0)
+    X = torch.randn(n, d, generator=g, device="cuda", dtype=torch.float32)
+    bag = torch.randint(0, bags, (n,), generator=g, device="cuda", dtype=torch.int64)
+    Wstar = torch.randn(d, 2, generator=g, device="cuda", dtype=torch.float32)
+    labels = torch.argmax(X @ Wstar, dim=1)
+    target = torch.zeros(bags * 2, dtype=torch.float64, device="cuda")
+    target.index_add_(0, bag * 2 + labels, torch.ones(n, dtype=torch.float64, device="cuda"))
+    del labels
+    model = tq.Linear(d, 2, np.random.default_rng(0), name="lin")
+    bag_pe = tq.one_hot_pe(bag, bags)
+    reg = tq.UdfRegistry()
+    reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(2))), 1,
+                             lambda c: (bag_pe, tq.pe_encode(model(c.values))), model.parameters))
+    cat = tq.Catalog()
+    Xt = tq.Tensor(X)
+    cat.register_tensor(Xt, "T")
+    q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
+        "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"), cat, reg)),
+        tq.CompileConfig(trainable=True), reg)
+    tgt = tq.Tensor(target)
+    batches = [("T", Xt, tgt)]
+    # the reference's training loop (tq/training.py:121): K iterations of
+    # register -> run -> MSE -> backward -> Adam, losses returned as floats
+    losses = tq.train(q, cat, batches, TrainConfig(iterations=max(args.warmup, 3), lr=0.01))
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    sampler = ClockSampler(0)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 20))
+    sampler.active = True
+    t0.record()
+    losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
+    t1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1) / steps
+    launches = _native.launch_count() - launches0
+
+    # ---- parity at the full size: one more step's grid and gradients (the
+    # engine's, at the trained weights) against a float64 recompute
+    cat.register_tensor(Xt, "T")
+    result = q.run(cat)
+    pred = prediction_vector(result, q)
+    loss = mse_loss(pred, tgt)
+    backward(loss)
+    grads = {p.name: q.tape.gradient(p.value).data for p in q.parameters()}
+    grid = pred.data.detach().clone()
+    q.end_session()
+    W, b = model.weight.value.data, model.bias.value.data
+    w0 = time.perf_counter()
+    rgrid, rdW, rdb = f64_step_reference(X, bag, W, b, target, bags)
+    torch.cuda.synchronize()
+    check_s = time.perf_counter() - w0
+    errs = {"grid": _rel(grid, rgrid), "dW": _rel(grads["lin.weight"], rdW),
+            "db": _rel(grads["lin.bias"], rdb)}
+    tol = 1e-5
+    parity = {"status": "ok" if all(v <= tol for v in errs.values()) else "MISMATCH",
+              "rows": n, "max_abs_err_over_max_abs_ref": errs, "tolerance": tol,
+              "checked": "count grid + dW + db of one training step at the full 1e8 x 64 size "
+                         "(after the timed steps) vs a float64 recompute (torch, chunked, the "
+                         "reference tape's closed forms)", "check_s": check_s}
+
+    # exact swap of the trained query: pe_decode ->
+    # exact COUNT BY (Bag, Pred), one pass over X (tdp_linear_argmax_count)
+    exact = q.swap_to_exact()
+    hold = {}
+
+    def swap_step():
+        hold["r"] = exact.run(cat)
+
+    for _ in range(3):
+        swap_step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        swap_step()
+    e1.record()
+    torch.cuda.synchronize()
+    swap_ms = e0.elapsed_time(e1) / steps
+    res = hold["r"]
+    # exact-swap cross-check (diagnostic): the counts of a cuBLAS fp32 argmax
+    # per row -- a different summation order, so near-ties may differ by a few
+    Z = torch.zeros(bags * 2, dtype=torch.int64, device="cuda")
+    for lo in range(0, n, 1 << 22):
+        cls = torch.argmax(X[lo:lo + (1 << 22)] @ W + b, dim=1)
+        Z.index_add_(0, bag[lo:lo + (1 << 22)] * 2 + cls, torch.ones_like(cls))
+    occ = torch.nonzero(Z).reshape(-1)
+    got_cnt = torch.as_tensor(res.columns[2].values.numpy(), device="cuda")
+    swap_mismatch = int((got_cnt - Z[occ]).abs().sum()) if got_cnt.numel() == occ.numel() else -1
+    swap_groups = int(res.row_count)
+    # CPU baseline: the closed-form oracle of the reference's step, one core
+    from oracle import relational as orc
+
+    m = 100_000
+    Xh = X[:m].double().cpu().numpy()
+    bh = bag[:m].cpu().numpy()
+    Wh = W.cpu().numpy().astype(np.float64)
+    bb = b.cpu().numpy().astype(np.float64)
+    th = np.zeros(bags * 2)
+    w0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - w0 < 5.0:
+        orc.llp_forward_backward(Xh, bh, Wh, bb, th, bags)
+        reps += 1
+    cpu_s = (time.perf_counter() - w0) / reps
+    peak = peaks()[0]
+    line = {
+        "metric": "LLP trainable query step latency (SURVEY config 4)",
+        "value": ms, "unit": "ms/step", "higher_is_better": False, "n_gpus": 1,
+        "steps": steps, "warmup": max(args.warmup, 3), "rows_per_s": n / (ms / 1e3),
+        "dtype": "f32 model, f64 grid", "data": "synthetic X ~ N(0,1), bags ~ U{0..999}",
+        "config": {"workload": f"SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred "
+                               f"(trainable), Linear({d},2) -> pe_encode, one_hot_pe bag, MSE, Adam",
+                   "step": "one iteration of tq.train() (K iterations per call, losses read back at the end)",
+                   "rows": n, "features": d, "bags": bags},
+        "gpu_launches": launches, "losses": losses[:3] + losses[-2:], "clocks": clocks,
+        "parity": parity,
+        "cpu_baseline": {"value": cpu_s / m * n * 1e3, "unit": "ms/step (linear extrapolation)",
+                         "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
+                                   f"reference tape), {reps} reps, extrapolated to {n} rows"},
+        "bytes_floor_ms_two_pass": (8 * d + 16) * n / peak / 1e9 * 1e3,
+        "bytes_floor_ms_one_pass": (4 * d + 8) * n / peak / 1e9 * 1e3,
+        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                     "achieved": (8 * d + 16) * n / (ms / 1e3) / 1e9,
+                     "frac": (8 * d + 16) * n / (ms / 1e3) / 1e9 / peak,
+                     "traffic": None,
+                     "what": "algorithmic bytes of the step (X read twice + bag codes twice, "
+                             "2 (4d + 8) B/row = 528 at d=64, SURVEY §8(d)) over the step time"},
+        "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
+                       "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
+                       "count_mismatch_vs_torch_argmax": swap_mismatch,
+                       "what": "q.swap_to_exact().run(cat): pe_decode + exact COUNT by (Bag, Pred); "
+                               "one pass over X + bag codes (tdp_linear_argmax_count)"},
+    }
+    print(json.dumps(line), flush=True)

@@ -1,0 +1,126 @@
+"""Q3-style customer |><| orders |><| lineitem pipeline (BASELINE config 3)."""
+
+from __future__ import annotations
+
+import json
+import time
+
+from .common import ROOT, ClockSampler, cpu_model, peaks, sustain, timed
+
+
+def _probe_traffic(nli: int):
+    """ncu DRAM bytes of Q3's dominant kernel at this lineitem size (None if
+    not captured) next to its algorithmic bytes (key + shipdate, 16 B/row)."""
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    try:
+        ent = json.loads(tf.read_text()).get(f"q3_rows{nli}_probe")
+    except Exception:
+        return None
+    if ent is None:
+        return None
+    return {"name": ent["kernel"], "traffic": ent["dram_bytes"], "algorithmic": 16 * nli,
+            "ncu_us": ent["ncu_duration_us"], "source": ent.get("source")}
+
+
+def run(args) -> None:
+    import numpy as np
+    import torch
+
+    from oracle import tpch as otpch
+    from paper_2211_02753_b200 import _native, workloads as wl
+
+    torch.cuda.set_device(0)
+    tables = wl.q3_arrays(args.sf, seed=7)
+    cat = wl.q3_catalog(tables)
+    plan = wl.Q3Plan(cat)
+    holder = {}
+
+    def step():
+        holder["r"] = plan.run(cat)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    launches0 = _native.launch_count()
+    steps = max(1, min(args.steps, 50))
+    sampler.active = True
+    ms = timed(step, steps)
+    launches = _native.launch_count() - launches0
+    res = holder["r"]
+    sustain(step, 1.5)
+    clocks = sampler.stop()
+    # the same pipeline re-planned on the host every step (no graph replay)
+    for _ in range(max(args.warmup, 3)):
+        plan.run_eager(cat)
+    eager_ms = timed(lambda: plan.run_eager(cat), steps)
+    # end to end through the API: pinned host columns copied in every step (a
+    # new catalog, so the plan runs eagerly), the result read back
+    host = {t: {c: torch.from_numpy(v).pin_memory() for c, v in cols.items()}
+            for t, cols in tables.items()}
+    h2d = sum(h.numel() * h.element_size() for cols in host.values() for h in cols.values())
+    d2h = [0]
+
+    def e2e_step():
+        out = plan.run(wl.q3_catalog(host))
+        d2h[0] = sum(c.values.numpy().nbytes for c in out.columns)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.e2e_steps, 5))
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - w0) / e2e_steps
+    nli = len(tables["lineitem"]["l_orderkey"])
+    base_bytes = (16 * len(tables["customer"]["c_custkey"]) + 32 * len(tables["orders"]["o_orderkey"])
+                  + 32 * nli)
+    w0 = time.perf_counter()
+    exp = otpch.q3(tables)
+    cpu_s = time.perf_counter() - w0
+    # parity of the timed (replayed) result: all four columns
+    names = ("l_orderkey", "sum_rev", "avg_o_orderdate", "avg_o_shippriority")
+    got = [c.values.numpy() for c in res.columns]
+    ok = len(got) == 4 and np.array_equal(got[0], exp["l_orderkey"])
+    worst = 0.0
+    for g, k in zip(got[1:], names[1:]):
+        e = exp[k]
+        ok = ok and g.shape == e.shape and np.allclose(g, e, rtol=1e-9, atol=0)
+        if g.shape == e.shape and len(e):
+            worst = max(worst, float(np.max(np.abs(g - e) / np.maximum(np.abs(e), 1e-300))))
+    peak = peaks()[0]
+    line = {
+        "metric": "TPC-H Q3-style join pipeline (SURVEY config 3)", "value": nli / (ms / 1e3),
+        "unit": "lineitem rows/s", "ms_per_step": ms, "higher_is_better": True, "n_gpus": 1,
+        "steps": steps, "warmup": max(args.warmup, 3), "dtype": "f64",
+        "data": "synthetic Appendix-B customer/orders/lineitem, seed 7",
+        "config": {"workload": f"Q3-style SF{args.sf:g}: 3 SQL filters, orders|><|customer, "
+                               f"lineitem|><|orders, GROUP BY l_orderkey, ORDER BY sum_rev DESC LIMIT 10",
+                   "customer": len(tables["customer"]["c_custkey"]),
+                   "orders": len(tables["orders"]["o_orderkey"]), "lineitem": nli,
+                   "joined_rows": int(exp["joined_rows"])},
+        "hbm_gbs_base_columns": base_bytes / (ms / 1e3) / 1e9, "gpu_launches": launches,
+        "replay": "one CUDA graph of the whole plan per step (replay.Pipeline; every kernel runs "
+                  "over all rows, data-dependent sizes from the recorded eager run, checked on "
+                  "the device)",
+        "eager_ms_per_step": eager_ms, "clocks": clocks,
+        "e2e": {"value": nli / e2e_s, "unit": "lineitem rows/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h[0], "h2d_gbs": h2d / e2e_s / 1e9,
+                "how": "pinned host columns -> q3_catalog -> Q3Plan.run (a new catalog: "
+                       "re-planned) -> result to host"},
+        "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                     "achieved": base_bytes / (ms / 1e3) / 1e9,
+                     "frac": base_bytes / (ms / 1e3) / 1e9 / peak,
+                     "traffic": None,
+                     "dominant_kernel": _probe_traffic(nli),
+                     "what": "base columns read once (SURVEY §8(d), 2.42 GB at SF10) over the "
+                             "whole pipeline time"},
+        "parity": {"status": "ok" if ok else "MISMATCH", "checked": "all four columns of the last "
+                   "timed (replayed) step's top-10 vs oracle/tpch.py q3 over the full tables",
+                   "rule": "l_orderkey bit-exact, floats rtol 1e-9", "max_rel_err": worst},
+        "cpu_baseline": {"value": nli / cpu_s, "unit": "lineitem rows/s", "cores": 1,
+                         "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"full SF{args.sf:g}, oracle/tpch.py q3 once"},
+    }
+    print(json.dumps(line), flush=True)

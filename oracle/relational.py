@@ -290,3 +290,34 @@ def join_nested_loop(probe: np.ndarray, build: np.ndarray) -> tuple[np.ndarray, 
         return np.array([], dtype=np.int64), np.array([], dtype=np.int64)
     a = np.array(pairs, dtype=np.int64)
     return a[:, 0], a[:, 1]
+
+
+# ---------------------------------------------------------------------------
+# gradient paths: gather VJP and the trainable global aggregates
+# ---------------------------------------------------------------------------
+
+def gather_rows_vjp(src_shape, idx: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """tq/tensor.py:609-612 -- VJP of an axis-0 gather: zeros of the source
+    shape, np.add.at of the upstream rows (duplicate indices accumulate)."""
+    grad = np.zeros(src_shape, dtype=g.dtype)
+    np.add.at(grad, idx, g)
+    return grad
+
+
+def score_global_soft(X: np.ndarray, W: np.ndarray, b: np.ndarray, threshold, G: np.ndarray):
+    """Forward + parameter gradients of ``SELECT SUM(s), AVG(s), COUNT(*) FROM
+    (SELECT s FROM lin(T) [WHERE s > threshold])`` in trainable mode, with the
+    loss G[0]*SUM + G[1]*AVG: the tape chain Linear -> filter_exact/take_rows
+    (gather, VJP gather_rows_vjp) -> GlobalAggSoftOp (tq/compiler.py:265-288:
+    reduce_sum, reduce_mean, COUNT a float constant).  threshold None: no WHERE."""
+    s = (X @ W + b).reshape(-1)
+    idx = np.nonzero(s > threshold)[0] if threshold is not None else np.arange(len(s))
+    kept = s[idx]
+    m = len(kept)
+    total = kept.sum()
+    avg = kept.mean() if m else np.nan
+    ds_kept = np.full(m, G[0] + (G[1] / m if m else 0.0))
+    ds = gather_rows_vjp((len(s),), idx, ds_kept)
+    dW = X.T @ ds.reshape(-1, 1)
+    db = np.array([ds.sum()])
+    return np.array([total]), np.array([avg]), np.array([float(m)]), dW, db

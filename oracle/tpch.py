@@ -33,6 +33,51 @@ def q1(arrays: dict) -> dict[str, np.ndarray]:
     return out
 
 
+def q1_partial(arrays: dict) -> dict[tuple, list]:
+    """Q1 over one row range of lineitem: per (rf, ls) group the five sums and
+    the count -- the mergeable part of q1() (AVG = merged SUM / merged COUNT,
+    as tq/kernels.py:147-153 forms it from the whole column)."""
+    cols = [arrays[c] for c in Q1_COLS]
+    ship, rf, ls, q, p, d, t = filter_exact(cols, [(0, "<=", 10471)])
+    one = np.asarray(1.0)
+    dp = p * (one - d)
+    ch = dp * (one + t)
+    keys, aggs = groupby_exact([rf, ls], [("sum", q), ("sum", p), ("sum", dp), ("sum", ch),
+                                          ("sum", d), ("count", None)])
+    return {(int(a), int(b)): [float(x[g]) for x in aggs[:5]] + [int(aggs[5][g])]
+            for g, (a, b) in enumerate(zip(keys[0], keys[1]))}
+
+
+def q1_merge(parts) -> dict[str, np.ndarray]:
+    """q1() of the concatenated row ranges from their q1_partial()s."""
+    acc: dict = {}
+    for part in parts:
+        for key, vals in part.items():
+            cur = acc.setdefault(key, [0.0] * 5 + [0])
+            for a, v in enumerate(vals):
+                cur[a] += v
+    keys = sorted(acc)
+    col = lambda a: np.array([acc[k][a] for k in keys], dtype=np.float64)  # noqa: E731
+    cnt = np.array([acc[k][5] for k in keys], dtype=np.int64)
+    return {"rf": np.array([k[0] for k in keys], dtype=np.int64),
+            "ls": np.array([k[1] for k in keys], dtype=np.int64),
+            "sum_qty": col(0), "sum_price": col(1), "sum_disc_price": col(2),
+            "sum_charge": col(3), "avg_qty": col(0) / cnt, "avg_price": col(1) / cnt,
+            "avg_disc": col(4) / cnt, "count": cnt}
+
+
+def q6_partial(arrays: dict) -> tuple[float, int]:
+    """Q6 over one row range: (SUM(extendedprice * discount), qualifying rows)."""
+    cols = [arrays[c] for c in ("l_shipdate", "l_discount", "l_quantity", "l_extendedprice")]
+    ship, d, q, p = filter_exact(cols, [(0, ">=", 8766), (0, "<", 9131), (1, ">=", 0.05),
+                                        (1, "<=", 0.07), (2, "<", 24)])
+    return float((p * d).sum()), len(p)
+
+
+def q6_merge(parts) -> dict[str, np.ndarray]:
+    return {"sum_rev": np.array([sum(s for s, _ in parts)], dtype=np.float64)}
+
+
 def q3(tables: dict) -> dict[str, np.ndarray]:
     """Q3-style pipeline: reference filters (filter_exact) on each table, the
     builder-defined sort/searchsorted join (no join in the reference), the

@@ -104,6 +104,29 @@ def gather_rows(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
     return gather_rows_raw(x, idx)
 
 
+class _ColumnSum(torch.autograd.Function):
+    """SUM of a 1-d float column on the fused scan kernel (float64
+    accumulation, fixed reduction order); VJP: the upstream gradient
+    broadcast to every row (tq/tensor.py:474)."""
+
+    @staticmethod
+    def forward(ctx, x: torch.Tensor) -> torch.Tensor:
+        from .kernels import _scan_single
+
+        ctx.n = x.shape[0]
+        _, raw = _scan_single(x.detach())
+        return raw.view(torch.float64).to(x.dtype).reshape(())
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        return g.reshape(1).expand(ctx.n).contiguous()
+
+
+def column_sum(x: torch.Tensor) -> torch.Tensor:
+    """Differentiable sum of a 1-d float CUDA column (0-d result, input dtype)."""
+    return _ColumnSum.apply(x)
+
+
 # ---------------------------------------------------------------------------
 # skinny linear layer (matmul with few output columns)
 # ---------------------------------------------------------------------------

@@ -17,13 +17,22 @@ The reference has no distribution at all.
 
 from __future__ import annotations
 
+import os
 import threading
 from contextlib import contextmanager
 
 import torch
 import torch.distributed as dist
 
+from . import hostread
+
 _TLS = threading.local()
+
+# TDP_FORCE_COLLECTIVES=1: a one-rank group still takes the sharded code path
+# (partials, NCCL all-reduce / all-to-all over a real one-rank communicator) --
+# how the collective path is exercised on a single-GPU host.
+def _force() -> bool:
+    return os.environ.get("TDP_FORCE_COLLECTIVES") == "1"
 
 
 def current_group():
@@ -47,6 +56,24 @@ def sharded(group=None):
 
 def world_size(group) -> int:
     return 1 if group is None else dist.get_world_size(group)
+
+
+def is_sharded(group) -> bool:
+    """Rows of ``group``'s relations are split across ranks (merge needed)."""
+    return group is not None and (dist.get_world_size(group) > 1 or _force())
+
+
+@contextmanager
+def local():
+    """Suspend the enclosing :func:`sharded` scope: the computation inside
+    sees one rank's data as the whole (an aggregate over a relation every
+    rank already holds in full must not be merged again)."""
+    prev = getattr(_TLS, "group", None)
+    _TLS.group = None
+    try:
+        yield
+    finally:
+        _TLS.group = prev
 
 
 # Collectives: NCCL on device tensors.  A gloo group (CPU tests, or several
@@ -104,14 +131,14 @@ class _AllReduceSum(torch.autograd.Function):
 def allreduce_sum(t: torch.Tensor, group) -> torch.Tensor:
     """``t`` summed over the ranks of ``group`` (identity for one rank),
     keeping the autograd graph (soft group-by grids of a sharded LLP step)."""
-    if world_size(group) <= 1:
+    if not is_sharded(group):
         return t
     return _AllReduceSum.apply(t, group)
 
 
 def allreduce_grads(grads, group) -> None:
     """In-place SUM of per-rank parameter gradients (data-parallel step)."""
-    if world_size(group) <= 1:
+    if not is_sharded(group):
         return
     for g in grads:
         if g is not None:
@@ -121,7 +148,7 @@ def allreduce_grads(grads, group) -> None:
 def allreduce_ranges(lo: torch.Tensor, hi: torch.Tensor, group) -> tuple[torch.Tensor, torch.Tensor]:
     """Global [min, max] of per-rank key ranges (empty shards hold
     (INT64_MAX, INT64_MIN), the identities of MIN / MAX)."""
-    if world_size(group) > 1:
+    if is_sharded(group):
         _all_reduce(lo, dist.ReduceOp.MIN, group)
         _all_reduce(hi, dist.ReduceOp.MAX, group)
     return lo, hi
@@ -138,7 +165,7 @@ def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows:
     (exact: a row count is far below 2^53) in the same all-reduce as the float
     sums -- one collective per query instead of two.
     """
-    if world_size(group) <= 1:
+    if not is_sharded(group):
         return
     nrows = sums_raw.shape[0]
     int_rows = [r for r in range(nrows) if r not in float_rows]
@@ -192,8 +219,11 @@ def exchange_rows(grouped: list[torch.Tensor], send_counts: torch.Tensor,
     """
     recv_counts = torch.empty_like(send_counts)
     _all_to_all_single(recv_counts, send_counts, None, None, group)
-    send = send_counts.tolist()
-    recv = recv_counts.tolist()
+    # one host read of both split vectors (hostread: logged for graph replay,
+    # checked on the device when replayed)
+    both = hostread.read_ints(torch.cat([send_counts, recv_counts]))
+    world = send_counts.numel()
+    send, recv = both[:world], both[world:]
     out = []
     for col in grouped:
         dst = torch.empty((sum(recv),) + tuple(col.shape[1:]), dtype=col.dtype, device=col.device)
@@ -205,13 +235,13 @@ def exchange_rows(grouped: list[torch.Tensor], send_counts: torch.Tensor,
 def allgather_rows(columns: list[torch.Tensor], group) -> list[torch.Tensor]:
     """Concatenate every rank's rows (rank order) on every rank."""
     world = world_size(group)
-    if world <= 1:
+    if not is_sharded(group):
         return columns
     dev = columns[0].device
     n = torch.tensor([columns[0].shape[0]], dtype=torch.int64, device=dev)
     sizes = [torch.empty_like(n) for _ in range(world)]
     _all_gather(sizes, n, group)
-    sizes = [int(s) for s in sizes]
+    sizes = hostread.read_ints(torch.cat(sizes))
     m = max(sizes) if sizes else 0
     out = []
     for col in columns:

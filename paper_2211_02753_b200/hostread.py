@@ -100,13 +100,22 @@ def replaying(log: "_Log") -> _Scope:
     return _Scope(_Log("replay", log.values, log.c_values))
 
 
+SYNC_READS = [0]  # synchronising reads of device integers in this process (diagnostics)
+
+
+def _sync_read(t: torch.Tensor) -> list[int]:
+    if t.is_cuda:
+        SYNC_READS[0] += 1
+    return [int(v) for v in t.reshape(-1).tolist()]
+
+
 def read_ints(t: torch.Tensor) -> list[int]:
     """The integer elements of a small device tensor (int64 / int32 / bool)."""
     log = getattr(_TLS, "log", None)
     if log is None:
-        return [int(v) for v in t.reshape(-1).tolist()]
+        return _sync_read(t)
     if log.mode == "record":
-        vals = [int(v) for v in t.reshape(-1).tolist()]
+        vals = _sync_read(t)
         log.values.append(vals)
         return vals
     if log.pos >= len(log.values):

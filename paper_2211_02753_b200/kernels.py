@@ -67,6 +67,7 @@ from .distributed import (
     allreduce_ranges,
     current_group,
     exchange_rows,
+    is_sharded,
     key_destination,
     world_size,
 )
@@ -197,9 +198,6 @@ def _row_space(columns: Sequence[EncodedTensor]) -> Optional[tuple[Optional[Sele
         elif isinstance(v._lazy, LazyValue):
             s = v._lazy.sel
             rows = s.n if s is not None else base_rows(v._lazy.expr)
-            if s is not None and v._lazy.expr.op != "col":
-                # expression columns refine fine; require the same base space
-                pass
         else:
             return None
         key = id(s) if s is not None else None
@@ -570,7 +568,7 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
         if func == "avg":
             avg_mask |= 1 << a
     group = current_group()
-    if group is None or world_size(group) <= 1:  # scan + reduce + finalise in one call
+    if not is_sharded(group):  # scan + reduce + finalise in one call
         out_keys, out_counts, out_aggs, out_groups = _scan_aggregate(
             kexprs, spans, agg_exprs, sel, n, device, avg_mask=avg_mask)
         if defer_rows:
@@ -677,7 +675,7 @@ def _groupby_general(keys, key_vals, agg_specs, agg_vals):
         vdata.append(t)
     nat.require_cuda(*kdata)
     group = current_group()
-    if group is not None and world_size(group) > 1:
+    if is_sharded(group):
         return _groupby_sharded(kdata, agg_specs, vdata, group)
     return _groupby_local(kdata, agg_specs, vdata)
 
@@ -1219,7 +1217,7 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
         pi, bi = join_indices(left[left_key].values, right[right_key].values)
         return [take_rows(left[i], pi) for i in lo] + [take_rows(right[i], bi) for i in ro]
     group = current_group()
-    if group is not None and world_size(group) > 1:
+    if is_sharded(group):
         out = _equi_join_sharded(left, right, left_key, right_key, group)
         return [out[i] for i in lo] + [out[len(left) + i] for i in ro]
     lb, lsel = _side_sources(left)

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .hostread import read_int, record_value, replay_value
+from .hostread import SYNC_READS, read_int, record_value, replay_value
 from . import autograd as _ag
 from . import tensor as _T
 
@@ -545,6 +545,7 @@ class DeferredCount:
                 self._value = v
                 return v
             self._event.synchronize()
+            SYNC_READS[0] += 1
             self._value = int(_ring().buf[self._slot])
             record_value(self._value)
             self._event = None

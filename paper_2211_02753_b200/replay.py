@@ -10,8 +10,12 @@ graph the second time it sees the same state and replays it afterwards:
 
 * state = the scanned tables (object identity, every stored column buffer and
   its in-place version counter), the UDF registry, the versions of the
-  referenced parameters, the device; anything else (a process group of more
-  than one rank, an open tape, an unknown lazy column) disables replay;
+  referenced parameters, the device and the process group of the enclosing
+  ``distributed.sharded`` scope; anything else (a gloo group, an open tape,
+  an unknown lazy column) disables replay;
+* under NCCL the in-query collectives (the all-reduce of partial aggregates,
+  the all-to-all of a key shuffle) are captured with the kernels: every rank
+  captures on the same (second) run of the same plan and replays in lockstep;
 * every kernel still runs over every row on each replay -- only the host-side
   planning is skipped -- and the launches are accounted to the library's
   launch counter;
@@ -35,7 +39,9 @@ from typing import Optional
 import torch
 
 from . import _native as nat
-from .distributed import current_group, world_size
+import torch.distributed as dist
+
+from .distributed import current_group
 from .encodings import EncodedTensor, trusted
 from . import hostread
 from .lazy import DeferredCount, LazyValue, PrefixRows, capturing, compact_source
@@ -70,14 +76,16 @@ def _tables_signature(catalog, names) -> Optional[tuple[list, list]]:
     """(signature items, tables) of the named catalog tables: identity, every
     stored column buffer and its in-place version counter."""
     group = current_group()
-    if group is not None and world_size(group) > 1:
-        return None
+    if group is not None and dist.get_backend(group) != "nccl":
+        return None  # host-staged (gloo) collectives cannot be captured
     if not _cuda_available() or torch.cuda.is_current_stream_capturing() or hostread.active():
         return None
     tables_by_name = getattr(catalog, "_tables", None)
     if tables_by_name is None:
         return None
-    sig, tables = [id(catalog), torch.cuda.current_device()], []
+    # a sharded run (NCCL collectives inside the graph: capturable, replayed in
+    # lockstep on every rank) and a local one are different states
+    sig, tables = [id(catalog), torch.cuda.current_device(), id(group) if group else None], []
     for name in names:
         t = tables_by_name.get(name)
         if t is None:
@@ -246,7 +254,9 @@ def _capture(execute, tables, log):
     try:
         with capturing(), warnings.catch_warnings(), hostread.replaying(log) as rlog:
             warnings.simplefilter("ignore")  # "graph is empty": a lazy result, no launches
-            with torch.cuda.graph(graph):
+            # thread_local: an eager query on another thread (or NCCL's
+            # watchdog polling its events) does not invalidate this capture
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
                 table = execute()
         if not rlog.consumed():
             raise hostread.ReplayMismatch("fewer host reads than recorded")

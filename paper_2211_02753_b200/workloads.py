@@ -33,10 +33,14 @@ LINEITEM_COLUMNS = ("l_shipdate", "l_returnflag", "l_linestatus", "l_quantity",
                     "l_extendedprice", "l_discount", "l_tax")
 
 
-def lineitem_arrays(sf: float, seed: int = 42, rows: int | None = None) -> dict[str, np.ndarray]:
-    """Appendix B lineitem generator (int64 dates/codes, float64 values)."""
-    n = int(rows if rows is not None else round(6_000_000 * sf))
-    rng = np.random.default_rng(seed)
+LINEITEM_CHUNK = 1 << 21  # rows per independently seeded generator chunk
+
+
+def _lineitem_chunk(sf: float, seed: int, chunk: int, rows: int) -> dict[str, np.ndarray]:
+    """Rows [chunk * LINEITEM_CHUNK, + rows) of the canonical table: chunk 0
+    draws from ``default_rng(seed)``, chunk c > 0 from ``default_rng([seed, c])``."""
+    rng = np.random.default_rng(seed if chunk == 0 else [seed, chunk])
+    n = rows
     orderdate = rng.integers(D_1992_01_01, 10440 + 1, size=n, dtype=np.int64)
     shipdate = orderdate + rng.integers(1, 122, size=n, dtype=np.int64)
     receipt = shipdate + rng.integers(1, 31, size=n, dtype=np.int64)
@@ -51,6 +55,30 @@ def lineitem_arrays(sf: float, seed: int = 42, rows: int | None = None) -> dict[
     linestatus = (shipdate > D_CURRENT).astype(np.int64)  # O=1 else F=0
     return {"l_shipdate": shipdate, "l_returnflag": returnflag, "l_linestatus": linestatus,
             "l_quantity": qty, "l_extendedprice": price, "l_discount": discount, "l_tax": tax}
+
+
+def lineitem_arrays(sf: float, seed: int = 42, rows: int | None = None, lo: int = 0,
+                    hi: int | None = None) -> dict[str, np.ndarray]:
+    """Appendix B lineitem generator (int64 dates/codes, float64 values).
+
+    The table of ``rows`` rows (default 6e6 x SF) is generated in independently
+    seeded chunks of LINEITEM_CHUNK rows, so any row range [lo, hi) -- one
+    rank's shard -- is produced without generating the rest, and the shards of
+    all ranks concatenate to the same table."""
+    n = int(rows if rows is not None else round(6_000_000 * sf))
+    hi = n if hi is None else min(int(hi), n)
+    lo = max(0, int(lo))
+    parts = []
+    for c in range(lo // LINEITEM_CHUNK, (hi + LINEITEM_CHUNK - 1) // LINEITEM_CHUNK):
+        c0 = c * LINEITEM_CHUNK
+        full = _lineitem_chunk(sf, seed, c, min(LINEITEM_CHUNK, n - c0))
+        a, b = max(lo, c0) - c0, min(hi, c0 + LINEITEM_CHUNK) - c0
+        parts.append({k: v[a:b] for k, v in full.items()})
+    if len(parts) == 1:
+        return {k: np.ascontiguousarray(v) for k, v in parts[0].items()}
+    if not parts:
+        return {k: v[:0] for k, v in _lineitem_chunk(sf, seed, 0, 0).items()}
+    return {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
 
 
 def lineitem_table(arrays: dict, columns=LINEITEM_COLUMNS):

@@ -298,6 +298,67 @@ exact = q.swap_to_exact().run(cat)
 for nm, col in zip(exact.schema.names, exact.columns):
     put(f"llp/exact/{nm}", col.values.data)
 
+# ---------------------------------------------------------------------------
+# gradient paths through gather (take_rows' VJP, tq/tensor.py:597-614) and the
+# trainable global aggregates (GlobalAggSoftOp, tq/compiler.py:265-288)
+# ---------------------------------------------------------------------------
+from tensorquery.tensor import gather  # noqa: E402
+
+g_rng = np.random.default_rng(31)
+src = g_rng.normal(size=(50, 3))
+idx = g_rng.integers(0, 50, size=200)  # duplicates: np.add.at accumulates
+gw = g_rng.normal(size=(200, 3))
+put("gather/src", src)
+put("gather/idx", idx)
+put("gather/w", gw)
+with Tape() as tape:
+    a = Tensor(src)
+    out = gather(a, Tensor(idx.astype(np.int64)), axis=0)
+    backward(reduce_sum(mul(out, tensor(gw))))
+    put("gather/out", out.data)
+    put("gather/grad", tape.gradient(a).data)
+
+# trainable query: Linear(6,1) score UDF -> WHERE score > 0.05 (filter_exact ->
+# take_rows -> gather on the tape) -> SUM / AVG / COUNT (GlobalAggSoftOp)
+n_t, d_t = 400, 6
+Xt = g_rng.normal(size=(n_t, d_t))
+put("globsoft/X", Xt)
+lin = ref.Linear(d_t, 1, np.random.default_rng(8), name="sc", dtype="float64")
+put("globsoft/W", lin.weight.value.data.copy())
+put("globsoft/b", lin.bias.value.data.copy())
+from tensorquery.storage import FLOAT  # noqa: E402
+from tensorquery.tensor import reshape as t_reshape  # noqa: E402
+
+regs = ref.UdfRegistry()
+regs.register(ref.UdfEntry(
+    "sc", (("s", FLOAT),), 1,
+    lambda c: (plain(t_reshape(lin(c.values), (c.values.shape[0],))),),
+    lin.parameters, pe_outputs=False))
+cat = ref.Catalog()
+cat.register_tensor(Tensor(Xt), "T")
+meta["globsoft"] = {}
+for tag, sql in (("filtered", "SELECT SUM(s), AVG(s), COUNT(*) FROM (SELECT s FROM sc(T) "
+                              "WHERE s > 0.05)"),
+                 ("plain", "SELECT SUM(s), AVG(s), COUNT(*) FROM sc(T)")):
+    plan = ref.lower(ref.bind(ref.parse(sql), cat, regs))
+    q = ref.compile_plan(plan, ref.CompileConfig(trainable=True), regs)
+    meta["globsoft"][tag] = {"sql": sql, "compiled": q.explain_compiled()}
+    res = q.run(cat)
+    gvec = g_rng.normal(size=2)
+    put(f"globsoft/{tag}/G", gvec)
+    loss = ref.tensor(0.0)
+    from tensorquery.tensor import add as t_add  # noqa: E402
+
+    for j, col in enumerate(res.columns[:2]):
+        loss = t_add(loss, reduce_sum(mul(col.values, tensor(gvec[j:j + 1]))))
+    backward(loss)
+    for nm, col in zip(res.schema.names, res.columns):
+        put(f"globsoft/{tag}/{nm}", col.values.data)
+    put(f"globsoft/{tag}/dW", q.tape.gradient(lin.weight.value).data)
+    put(f"globsoft/{tag}/db", q.tape.gradient(lin.bias.value).data)
+    meta["globsoft"][tag]["names"] = list(res.schema.names)
+    q.end_session()
+
 np.savez_compressed(HERE / "golden.npz", **arrays)
 (HERE / "golden.json").write_text(json.dumps(meta, indent=1, default=float))
 print(f"wrote {len(arrays)} arrays")

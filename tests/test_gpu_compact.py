@@ -51,7 +51,7 @@ def test_lineitem_storage_plan_and_round_trip():
     assert narrow.columns[1].encoding.dictionary == wl.RETURNFLAG
 
 
-@pytest.mark.parametrize("rows", [1, 5000, 200_003])
+@pytest.mark.parametrize("rows", [1, 5000, 200_003, 1_000_003])
 def test_q1_compact_equals_wide_and_oracle(rows):
     arrays = wl.lineitem_arrays(0.01, seed=5, rows=rows)
     cw, cn, _ = _catalogs(arrays)
@@ -72,7 +72,7 @@ def test_q1_compact_equals_wide_and_oracle(rows):
     assert rn.columns[0].is_dictionary()
 
 
-@pytest.mark.parametrize("rows", [0, 777, 123_457])
+@pytest.mark.parametrize("rows", [0, 777, 123_457, 400_009, 1_500_001])
 def test_q6_compact_equals_oracle(rows):
     cols = ("l_shipdate", "l_quantity", "l_extendedprice", "l_discount")
     arrays = wl.lineitem_arrays(0.01, seed=3, rows=rows)

@@ -86,6 +86,19 @@ def _worker(rank, world, port, result):
         import sys
         print(f'rank {rank}: check at line 72 failed', file=sys.stderr, flush=True)
     ok &= _c
+    # an aggregate over an inner aggregate's (replicated) result is not merged
+    # across ranks again (it used to return world_size x the counts)
+    q2n = wl.compile_sql("SELECT COUNT(*), SUM(sum_v) FROM (SELECT k, SUM(v) FROM t GROUP BY k)",
+                         cat2, tq.UdfRegistry())
+    with sharded():
+        r2n = q2n.run(cat2)
+    gn = [c.values.numpy() for c in r2n.columns]
+    _c = bool(int(gn[0][0]) == len(ek[0]) and np.allclose(gn[1][0], val.sum(), rtol=1e-9))
+    if not _c:
+        import sys
+        print(f"rank {rank}: nested aggregate {gn} vs {len(ek[0])}, {val.sum()}", file=sys.stderr,
+              flush=True)
+    ok &= _c
     # sharded equi-join: both sides repartitioned by key (all-to-all), local
     # join; the union of the ranks' pairs equals the single-process join
     from paper_2211_02753_b200.kernels import equi_join, filter_exact

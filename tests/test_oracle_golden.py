@@ -136,3 +136,18 @@ def test_join_oracle_vs_nested_loop():
         b = orc.join_nested_loop(probe, build)
         np.testing.assert_array_equal(a[0], b[0])
         np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_gather_vjp_and_global_soft_golden():
+    src, idx, w = A["gather/src"], A["gather/idx"], A["gather/w"]
+    np.testing.assert_array_equal(src[idx], A["gather/out"])
+    np.testing.assert_allclose(orc.gather_rows_vjp(src.shape, idx, w), A["gather/grad"],
+                               rtol=1e-13, atol=1e-14)
+    X, W, b = A["globsoft/X"], A["globsoft/W"], A["globsoft/b"]
+    for tag, thr in (("filtered", 0.05), ("plain", None)):
+        s, avg, cnt, dW, db = orc.score_global_soft(X, W, b, thr, A[f"globsoft/{tag}/G"])
+        np.testing.assert_allclose(s, A[f"globsoft/{tag}/sum_s"], rtol=1e-12)
+        np.testing.assert_allclose(avg, A[f"globsoft/{tag}/avg_s"], rtol=1e-12)
+        np.testing.assert_array_equal(cnt, A[f"globsoft/{tag}/count"])
+        np.testing.assert_allclose(dW, A[f"globsoft/{tag}/dW"], rtol=1e-12)
+        np.testing.assert_allclose(db, A[f"globsoft/{tag}/db"], rtol=1e-12)

@@ -316,10 +316,14 @@ int tdp_unique_inverse(const int64_t* key, int64_t n, int64_t* out_uniques,
 /* Grouped aggregation over dense codes in [0, slots): counts (int64) and per
  * aggregate 8-byte sums in the value column's accumulator type (float64 for
  * float input, int64 wrap-around for int input; np.bincount / np.add.at,
- * tq/kernels.py:138-153).  vals[a] may be NULL for COUNT.                   */
+ * tq/kernels.py:138-153).  vals[a] may be NULL for COUNT.  Float sums are
+ * accumulated in 256-bit fixed point (order-independent, bitwise repeatable)
+ * in the caller's workspace of tdp_groupby_codes_workspace(slots, naggs)
+ * bytes.                                                                    */
+size_t tdp_groupby_codes_workspace(int64_t slots, int32_t naggs);
 int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_column* vals,
                       const int32_t* agg_kinds, int32_t naggs, int64_t* out_counts,
-                      void* out_sums, void* stream);
+                      void* out_sums, void* ws, size_t ws_bytes, void* stream);
 
 /* Hash group-by over one int64 key (groupby_exact general path, tq/kernels.py
  * :108-167, for key ranges too wide for dense slots).  prepare: one pass

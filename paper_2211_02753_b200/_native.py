@@ -125,8 +125,9 @@ _SIGNATURES = {
                                c_void_p]),
     "tdp_unique_inverse": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_size_t, c_void_p]),
+    "tdp_groupby_codes_workspace": (c_size_t, [c_int64, c_int32]),
     "tdp_groupby_codes": (c_int, [c_void_p, c_int64, c_int64, POINTER(Column), POINTER(c_int32),
-                                  c_int32, c_void_p, c_void_p, c_void_p]),
+                                  c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_groupby_hash_workspace": (c_size_t, [c_int64, c_int32]),
     "tdp_groupby_hash_prepare": (c_int, [c_void_p, c_int64, POINTER(Column), POINTER(c_int32),
                                          c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),

@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "tdp_common.cuh"
+#include "fixed_acc.cuh"
 
 namespace tdp {
 
@@ -321,15 +322,38 @@ __global__ void unique_scatter_kernel(const u64* __restrict__ sk, const i64* __r
 // ---- grouped aggregation over dense codes ----------------------------------
 struct ValSet {
   int naggs;
-  int pad;
+  int nfixed;     // float SUM aggregates: fixed-point cells (fixed_acc.cuh)
   const void* p[32];
   int dt[32];
   int kind[32];
+  int fidx[32];   // aggregate -> fixed-point cell block (float SUMs), else -1
 };
+
+inline void number_fixed(ValSet* vs) {
+  vs->nfixed = 0;
+  for (int a = 0; a < vs->naggs; ++a)
+    vs->fidx[a] = vs->kind[a] == TDP_AGG_SUM_F64 ? vs->nfixed++ : -1;
+}
+
+// fixed-point cells -> the double bits of the float sums: sums[a][slot]
+// (stride `sstride` per aggregate), cells [fidx][slot][kFixedWords]
+__global__ void fixed_finalize_kernel(const unsigned long long* __restrict__ fx, i64 slots,
+                                      ValSet vs, unsigned long long* __restrict__ sums,
+                                      i64 sstride) {
+  for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < slots * vs.naggs;
+       t += (i64)gridDim.x * blockDim.x) {
+    const int a = (int)(t / slots);
+    const i64 s = t - (i64)a * slots;
+    if (vs.fidx[a] < 0) continue;
+    const double v = fixed_value(fx + ((i64)vs.fidx[a] * slots + s) * kFixedWords);
+    sums[(i64)a * sstride + s] = (unsigned long long)__double_as_longlong(v);
+  }
+}
 
 __global__ void groupby_codes_kernel(const i64* __restrict__ codes, i64 n, i64 slots, ValSet vs,
                                      unsigned long long* __restrict__ counts,
-                                     unsigned long long* __restrict__ sums) {
+                                     unsigned long long* __restrict__ sums,
+                                     unsigned long long* __restrict__ fx) {
   const int lane = threadIdx.x & 31;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -345,8 +369,9 @@ __global__ void groupby_codes_kernel(const i64* __restrict__ codes, i64 n, i64 s
       for (int a = 0; a < vs.naggs; ++a) {
         if (vs.kind[a] == TDP_AGG_COUNT) continue;
         if (vs.kind[a] == TDP_AGG_SUM_F64) {
+          // fixed lane order -> the same warp sum every run; integer cells
           const double v = warp_sum(load_as_f64(vs.p[a], vs.dt[a], i));
-          if (lane == 0) atomicAdd(reinterpret_cast<double*>(sums) + (i64)a * slots + c0, v);
+          if (lane == 0) fixed_add(fx + ((i64)vs.fidx[a] * slots + c0) * kFixedWords, v);
         } else {
           const unsigned long long v = warp_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i));
           if (lane == 0) atomicAdd(sums + (i64)a * slots + c0, v);
@@ -357,7 +382,7 @@ __global__ void groupby_codes_kernel(const i64* __restrict__ codes, i64 n, i64 s
       for (int a = 0; a < vs.naggs; ++a) {
         if (vs.kind[a] == TDP_AGG_COUNT) continue;
         if (vs.kind[a] == TDP_AGG_SUM_F64)
-          atomicAdd(reinterpret_cast<double*>(sums) + (i64)a * slots + c,
+          fixed_add(fx + ((i64)vs.fidx[a] * slots + c) * kFixedWords,
                     load_as_f64(vs.p[a], vs.dt[a], i));
         else
           atomicAdd(sums + (i64)a * slots + c,
@@ -569,14 +594,18 @@ int tdp_unique_inverse(const int64_t* key, int64_t n, int64_t* out_uniques, int6
   return TDP_OK;
 }
 
+size_t tdp_groupby_codes_workspace(int64_t slots, int32_t naggs) {
+  return (size_t)(slots > 0 ? slots : 1) * (size_t)(naggs > 0 ? naggs : 0) * kFixedWords * 8 + 256;
+}
+
 int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_column* vals,
                       const int32_t* agg_kinds, int32_t naggs, int64_t* out_counts,
-                      void* out_sums, void* stream) {
+                      void* out_sums, void* ws, size_t ws_bytes, void* stream) {
   TDP_REQUIRE(n >= 0 && slots >= 1, "bad group-by shape");
   TDP_REQUIRE(naggs >= 0 && naggs <= 32, "at most 32 aggregates");
   ValSet vs;
+  std::memset(&vs, 0, sizeof(vs));
   vs.naggs = naggs;
-  vs.pad = 0;
   for (int a = 0; a < naggs; ++a) {
     vs.kind[a] = agg_kinds[a];
     TDP_REQUIRE(agg_kinds[a] >= TDP_AGG_COUNT && agg_kinds[a] <= TDP_AGG_SUM_I64,
@@ -591,14 +620,25 @@ int tdp_groupby_codes(const int64_t* codes, int64_t n, int64_t slots, const tdp_
     vs.p[a] = vals[a].data;
     vs.dt[a] = vals[a].dtype;
   }
+  number_fixed(&vs);
+  const size_t fx_bytes = (size_t)slots * vs.nfixed * kFixedWords * 8;
+  TDP_REQUIRE(vs.nfixed == 0 || (ws != nullptr && ws_bytes >= fx_bytes),
+              "group-by workspace too small (%zu < %zu)", ws_bytes, fx_bytes);
+  unsigned long long* fx = reinterpret_cast<unsigned long long*>(ws);
   cudaStream_t st = as_stream(stream);
   TDP_CUDA_TRY(cudaMemsetAsync(out_counts, 0, (size_t)slots * 8, st));
   if (naggs) TDP_CUDA_TRY(cudaMemsetAsync(out_sums, 0, (size_t)slots * naggs * 8, st));
+  if (vs.nfixed) TDP_CUDA_TRY(cudaMemsetAsync(fx, 0, fx_bytes, st));
   if (n > 0) {
     groupby_codes_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(
         codes, n, slots, vs, reinterpret_cast<unsigned long long*>(out_counts),
-        reinterpret_cast<unsigned long long*>(out_sums));
+        reinterpret_cast<unsigned long long*>(out_sums), fx);
     TDP_LAUNCH_CHECK("groupby_codes_kernel");
+  }
+  if (vs.nfixed) {
+    fixed_finalize_kernel<<<stream_grid(slots * naggs, 256, 4), 256, 0, st>>>(
+        fx, slots, vs, reinterpret_cast<unsigned long long*>(out_sums), slots);
+    TDP_LAUNCH_CHECK("fixed_finalize_kernel");
   }
   if (naggs) {
     copy_counts_kernel<<<stream_grid(slots * naggs, 256, 4), 256, 0, st>>>(
@@ -1223,6 +1263,7 @@ struct HashAgg {
   u64* slot;     // [cap + 1]  key image (0 = empty); [cap] = side slot for INT64_MIN
   u64* cnt;      // [cap + 1]
   u64* acc;      // [naggs][cap + 1]  (double bits for SUM_F64, u64 for SUM_I64)
+  u64* fx;       // [nfixed][cap + 1][kFixedWords]  fixed-point cells of the float SUMs
   i64* flags;    // [cap + 1]
   i64* offs;     // [cap + 1]
   void* scan_ws;
@@ -1234,7 +1275,8 @@ struct HashAgg {
 size_t hashagg_ws_bytes(i64 n, int naggs) {
   const i64 cap = (i64)table_capacity(n);
   const size_t per = (size_t)(cap + 1) * 8;
-  return sort_ws_bytes(n) + align256(per) * (4 + (size_t)(naggs > 0 ? naggs : 0)) +
+  const size_t na = naggs > 0 ? naggs : 0;
+  return sort_ws_bytes(n) + align256(per) * (4 + na) + align256(per * kFixedWords) * na +
          exclusive_scan_workspace(cap + 1) + 1024;
 }
 
@@ -1254,6 +1296,8 @@ HashAgg carve_hashagg(void* ws, i64 n, int naggs) {
   p += per;
   h.acc = (u64*)p;
   p += per * (naggs > 0 ? naggs : 0);
+  h.fx = (u64*)p;  // fixed-point cells of the float SUMs (a prefix of naggs blocks)
+  p += align256((size_t)(h.cap + 1) * 8 * kFixedWords) * (naggs > 0 ? naggs : 0);
   h.scan_ws = p;
   h.scan_bytes = exclusive_scan_workspace(h.cap + 1) + 512;
   return h;
@@ -1310,8 +1354,11 @@ __global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, V
       if (vs.kind[a] == TDP_AGG_COUNT) continue;
       u64* dst = h.acc + (i64)a * (h.cap + 1) + slot;
       if (vs.kind[a] == TDP_AGG_SUM_F64) {
+        // the peers' sum in fixed lane order, then order-free integer cells
         const double v = group_sum(load_as_f64(vs.p[a], vs.dt[a], i), peers, lane);
-        if (lane == leader) atomicAdd(reinterpret_cast<double*>(dst), v);
+        if (lane == leader)
+          fixed_add(reinterpret_cast<unsigned long long*>(h.fx) +
+                        ((i64)vs.fidx[a] * (h.cap + 1) + slot) * kFixedWords, v);
       } else {
         const unsigned long long v =
             group_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i), peers, lane);
@@ -1452,6 +1499,7 @@ int make_valset(const tdp_column* vals, const int32_t* agg_kinds, int32_t naggs,
     vs->p[a] = vals[a].data;
     vs->dt[a] = vals[a].dtype;
   }
+  number_fixed(vs);
   return TDP_OK;
 }
 
@@ -1490,9 +1538,18 @@ static int hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
   TDP_CUDA_TRY(cudaMemsetAsync(h.slot, 0, per, st));
   TDP_CUDA_TRY(cudaMemsetAsync(h.cnt, 0, per, st));
   for (int a = 0; a < naggs; ++a)
-    TDP_CUDA_TRY(cudaMemsetAsync(h.acc + (i64)a * (h.cap + 1), 0, per, st));
+    if (vs.kind[a] != TDP_AGG_SUM_F64)
+      TDP_CUDA_TRY(cudaMemsetAsync(h.acc + (i64)a * (h.cap + 1), 0, per, st));
+  if (vs.nfixed)
+    TDP_CUDA_TRY(cudaMemsetAsync(h.fx, 0, per * kFixedWords * vs.nfixed, st));
   hashagg_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(keys, n, h, vs);
   TDP_LAUNCH_CHECK("hashagg_kernel");
+  if (vs.nfixed) {  // float sums -> h.acc as double bits (before compaction reads them)
+    fixed_finalize_kernel<<<stream_grid((h.cap + 1) * naggs, 256, 8), 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long*>(h.fx), h.cap + 1, vs,
+        reinterpret_cast<unsigned long long*>(h.acc), h.cap + 1);
+    TDP_LAUNCH_CHECK("fixed_finalize_kernel");
+  }
   hashagg_flags_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h);
   TDP_LAUNCH_CHECK("hashagg_flags_kernel");
   rc = exclusive_scan_i64(h.flags, h.offs, h.cap + 1, out_ngroups, h.scan_ws, h.scan_bytes, st);

@@ -169,10 +169,13 @@ def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows:
         return
     nrows = sums_raw.shape[0]
     int_rows = [r for r in range(nrows) if r not in float_rows]
+    # rows by slicing (no advanced indexing: a host index list would be a
+    # pageable copy, which a CUDA-graph capture cannot contain)
+    row = lambda r: sums_raw[r:r + 1]  # noqa: E731
     if all(r in count_rows for r in int_rows):
-        merged = torch.cat([counts.reshape(1, -1).to(torch.float64),
-                            sums_raw[int_rows].to(torch.float64),
-                            sums_raw[float_rows].view(torch.float64)], dim=0)
+        merged = torch.cat([counts.reshape(1, -1).to(torch.float64)]
+                           + [row(r).to(torch.float64) for r in int_rows]
+                           + [row(r).view(torch.float64) for r in float_rows], dim=0)
         _all_reduce(merged, dist.ReduceOp.SUM, group)
         counts.copy_(merged[0].round().to(torch.int64))
         for j, r in enumerate(int_rows):
@@ -180,13 +183,13 @@ def allreduce_partials(counts: torch.Tensor, sums_raw: torch.Tensor, float_rows:
         for j, r in enumerate(float_rows):
             sums_raw[r].copy_(merged[1 + len(int_rows) + j].view(torch.int64))
         return
-    ints = torch.cat([counts.reshape(1, -1), sums_raw[int_rows]], dim=0) if int_rows else counts.reshape(1, -1).clone()
+    ints = torch.cat([counts.reshape(1, -1)] + [row(r) for r in int_rows], dim=0)
     _all_reduce(ints, dist.ReduceOp.SUM, group)
     counts.copy_(ints[0])
     for j, r in enumerate(int_rows):
         sums_raw[r].copy_(ints[1 + j])
     if float_rows:
-        floats = sums_raw[float_rows].contiguous().view(torch.float64).clone()
+        floats = torch.cat([row(r) for r in float_rows], dim=0).view(torch.float64)
         _all_reduce(floats, dist.ReduceOp.SUM, group)
         for j, r in enumerate(float_rows):
             sums_raw[r].copy_(floats[j].view(torch.int64))

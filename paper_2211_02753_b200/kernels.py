@@ -654,9 +654,11 @@ def _groupby_codes(codes: torch.Tensor, slots: int, agg_specs, agg_vals, n: int,
     counts = torch.empty(slots, dtype=torch.int64, device=device)
     sums = torch.empty((max(1, len(kinds)), slots), dtype=torch.int64, device=device)
     nat.require_cuda(codes)
+    ws = nat.workspace(nat.load().tdp_groupby_codes_workspace(
+        slots, sum(k == nat.AGG_SUM_F64 for k in kinds)), device)
     nat.call("tdp_groupby_codes", nat.ptr(codes), n, slots, cols,
              (c_int32 * max(1, len(kinds)))(*kinds), len(kinds), nat.ptr(counts), nat.ptr(sums),
-             nat.stream())
+             nat.ptr(ws), ws.numel(), nat.stream())
     return counts, sums
 
 

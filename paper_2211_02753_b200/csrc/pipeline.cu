@@ -18,7 +18,9 @@
 #include <cuda.h>
 #include <nvrtc.h>
 
+#include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -621,6 +623,18 @@ int compile(const Spec& s, const Ring& ring, i64 acc_smem, std::shared_ptr<Kerne
   std::vector<char> cubin;
   rc = nvrtc_compile(src, &cubin);
   if (rc) return rc;
+  if (const char* dir = getenv("TDP_DUMP_CUBIN_DIR")) {  // SASS evidence (cuobjdump -sass)
+    const std::string base = std::string(dir) + "/tdp_scan_" +
+                             std::to_string(std::hash<std::string>{}(key) & 0xffffffu);
+    if (FILE* f = fopen((base + ".cubin").c_str(), "wb")) {
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+    }
+    if (FILE* f = fopen((base + ".cu").c_str(), "wb")) {
+      fwrite(src.data(), 1, src.size(), f);
+      fclose(f);
+    }
+  }
   TDP_CUDA_TRY(cudaFree(0));  // make the primary context current on this thread
   auto k = std::make_shared<Kernel>();
   rc = cu_check(d, d->load(&k->mod, cubin.data()), "cuModuleLoadData");

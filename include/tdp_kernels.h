@@ -400,6 +400,26 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Dense-range equi-join: the same contract as tdp_join_prepare_ex (mode 0) /
+ * tdp_join_emit when every build key lies in [lo, lo + key_range) (a column
+ * statistic) and the keys are unique: a bitmap of key_range bits replaces the
+ * hash table and Bloom filter (one bit test per probe row, exact), build rows
+ * are found by the key's rank among the set bits.  out_info[1] != 0 reports a
+ * repeated build key or a key outside the range (the pair count is then not
+ * valid: use the hash join).  need_rows = 0 skips the build-row index (a
+ * semi-join: out_build_idx is not written).  Replaces the same
+ * filter_exact -> take_rows -> join composition.           */
+size_t tdp_join_dense_workspace(int64_t key_range, int64_t n_build, int64_t n_probe);
+int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                           int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds,
+                           const int64_t* probe_keys, int64_t n_probe, const tdp_column* pcols,
+                           int32_t npcols, const tdp_predicate* ppreds, int32_t nppreds,
+                           int64_t lo, int64_t key_range, int32_t need_rows, int64_t* out_info,
+                           void* ws, size_t ws_bytes, void* stream);
+int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe, int64_t lo,
+                        int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
+                        int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* probability encodings and soft (differentiable) group-by                 */
 /* ------------------------------------------------------------------------ */

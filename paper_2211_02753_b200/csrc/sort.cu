@@ -1644,3 +1644,263 @@ int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, in
 
 }  // extern "C"
 
+
+// ---------------------------------------------------------------------------
+// Dense-range equi-join (unique build keys within a known range [lo, lo+R)):
+// the build sets one bit per key in a bitmap of R bits (atomicOr; a bit seen
+// twice = repeated key -> the caller falls back to the hash join), the probe
+// tests one bit per row -- no hashing, no Bloom filter, no slot compare, and
+// no false positives.  A build row is found again by its key's rank among the
+// set bits (per-1024-bit block offsets + per-word u16 prefixes, the bitmap
+// rank of the hash group-by), and rank order is ascending key order.  Used
+// when R is small next to the build (TPC-H keys: c_custkey R = rows, o_orderkey
+// R = 4 x rows); the bitmap (R/8 bytes) and rank words stay L2-resident.
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+struct DenseJoin {
+  unsigned* bits;        // [words]
+  unsigned short* wpre;  // [words]  set bits of the block's earlier words
+  i64* bcount;           // [blocks]
+  i64* boffs;            // [blocks]  set bits of earlier blocks
+  i64* rank_row;         // [nb]      build row of each rank (need_rows)
+  int* flags;            // [0] repeated key, [1] key outside [lo, lo+R), [2] zero (expand)
+  u64 lo;
+  i64 range;
+};
+
+__device__ __forceinline__ i64 dense_rank(const DenseJoin& dj, u64 d) {
+  const i64 w = (i64)(d >> 5);
+  return dj.boffs[d >> 10] + dj.wpre[w] + __popc(dj.bits[w] & ((1u << (d & 31)) - 1u));
+}
+
+template <bool kFiltered>
+__global__ void dense_build_kernel(const i64* __restrict__ keys, i64 nb, DenseJoin dj,
+                                   PredSet bps) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (i64)gridDim.x * blockDim.x) {
+    if (kFiltered && !eval_all(bps, i)) continue;
+    const u64 x = (u64)__ldg(keys + i) - dj.lo;
+    if (x >= (u64)dj.range) {
+      dj.flags[1] = 1;
+      continue;
+    }
+    const unsigned bit = 1u << (x & 31);
+    if (atomicOr(dj.bits + (x >> 5), bit) & bit) dj.flags[0] = 1;
+  }
+}
+
+template <bool kFiltered>
+__global__ void dense_place_kernel(const i64* __restrict__ keys, i64 nb, DenseJoin dj,
+                                   PredSet bps) {
+  if (dj.flags[0] | dj.flags[1]) return;  // falls back to the hash join
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (i64)gridDim.x * blockDim.x) {
+    if (kFiltered && !eval_all(bps, i)) continue;
+    dj.rank_row[dense_rank(dj, (u64)__ldg(keys + i) - dj.lo)] = i;
+  }
+}
+
+// Probe pass: the tile / word layout of join_count_kernel (so the unique-key
+// expansion is shared), one bitmap word per row instead of Bloom + slot.
+template <bool kFiltered>
+__global__ void __launch_bounds__(kJoinThreads, 4)
+    dense_count_kernel(DenseJoin dj, const i64* __restrict__ probe, i64 np, PredSet ps,
+                       unsigned* __restrict__ match_bits, i64* __restrict__ word_counts,
+                       i64* __restrict__ tile_counts) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 tile = blockIdx.x;
+  bool act[kJoinPer];
+  i64 row[kJoinPer], key[kJoinPer];
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    row[k] = join_row(tile, k);
+    act[k] = row[k] < np;
+  }
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) key[k] = act[k] ? __ldcs(probe + row[k]) : 0;
+  if (kFiltered) eval_batch<kJoinPer>(ps, row, act);
+  unsigned w[kJoinPer];
+  u64 d[kJoinPer];
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    d[k] = (u64)key[k] - dj.lo;
+    act[k] = act[k] && d[k] < (u64)dj.range;
+    w[k] = act[k] ? __ldg(dj.bits + (d[k] >> 5)) : 0u;
+  }
+  i64 local = 0;
+#pragma unroll
+  for (int k = 0; k < kJoinPer; ++k) {
+    const bool hit = act[k] && ((w[k] >> (d[k] & 31)) & 1u);
+    const unsigned word = __ballot_sync(0xffffffffu, hit);
+    const i64 wc = (i64)__popc(word);
+    if (lane == 0) {
+      match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
+      word_counts[tile * kJoinWords + k * kJoinWarps + warp] = wc;
+    }
+    local += wc;
+  }
+  if (lane == 0 && local != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(tile_counts + tile), (unsigned long long)local);
+}
+
+__global__ void dense_pairs_kernel(DenseJoin dj, const i64* __restrict__ probe,
+                                   const i64* __restrict__ tile_counts,
+                                   const i64* __restrict__ tile_offsets, i64 tiles,
+                                   const i64* __restrict__ out_probe, i64* __restrict__ out_build) {
+  const i64 total = tile_offsets[tiles - 1] + tile_counts[tiles - 1];
+  for (i64 m = (i64)blockIdx.x * blockDim.x + threadIdx.x; m < total;
+       m += (i64)gridDim.x * blockDim.x)
+    out_build[m] = dj.rank_row[dense_rank(dj, (u64)__ldg(probe + out_probe[m]) - dj.lo)];
+}
+
+struct DenseWs {
+  DenseJoin dj;
+  unsigned* match_bits;
+  i64* word_counts;
+  i64* tile_counts;
+  i64* tile_offsets;
+  void* scan_ws;
+  size_t scan_bytes;
+  void* bscan_ws;
+  size_t bscan_bytes;
+};
+
+size_t dense_ws_bytes(i64 range, i64 nb, i64 np) {
+  const i64 r = range > 0 ? range : 1;
+  const i64 words = rank_words(r), blocks = rank_blocks(r);
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  return align256((size_t)words * 4) + align256((size_t)words * 2) + 2 * align256((size_t)blocks * 8) +
+         align256((size_t)(nb > 0 ? nb : 1) * 8) + 256 + align256((size_t)tiles * kJoinWords * 4) +
+         align256((size_t)tiles * kJoinWords * 8) + 2 * align256((size_t)tiles * 8) +
+         exclusive_scan_workspace(tiles) + exclusive_scan_workspace(blocks) + 4096;
+}
+
+DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np) {
+  DenseWs w;
+  const i64 r = range > 0 ? range : 1;
+  const i64 words = rank_words(r), blocks = rank_blocks(r);
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  w.dj.bits = (unsigned*)p;
+  p += align256((size_t)words * 4);
+  w.dj.wpre = (unsigned short*)p;
+  p += align256((size_t)words * 2);
+  w.dj.bcount = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  w.dj.boffs = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  w.dj.rank_row = (i64*)p;
+  p += align256((size_t)(nb > 0 ? nb : 1) * 8);
+  w.dj.flags = (int*)p;
+  p += 256;
+  w.dj.lo = (u64)lo;
+  w.dj.range = r;
+  w.match_bits = (unsigned*)p;
+  p += align256((size_t)tiles * kJoinWords * 4);
+  w.word_counts = (i64*)p;
+  p += align256((size_t)tiles * kJoinWords * 8);
+  w.tile_counts = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  w.tile_offsets = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  w.scan_ws = p;
+  w.scan_bytes = exclusive_scan_workspace(tiles);
+  p += exclusive_scan_workspace(tiles);
+  w.bscan_ws = p;
+  w.bscan_bytes = exclusive_scan_workspace(blocks) + 1024;
+  return w;
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_join_dense_workspace(int64_t key_range, int64_t n_build, int64_t n_probe) {
+  return dense_ws_bytes(key_range, n_build, n_probe);
+}
+
+int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                           int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds,
+                           const int64_t* probe_keys, int64_t n_probe, const tdp_column* pcols,
+                           int32_t npcols, const tdp_predicate* ppreds, int32_t nppreds,
+                           int64_t lo, int64_t key_range, int32_t need_rows, int64_t* out_info,
+                           void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
+  TDP_REQUIRE(out_info != nullptr, "null join info output");
+  TDP_REQUIRE(key_range >= 1 && key_range <= ((int64_t)1 << 34),
+              "dense join key range %lld outside [1, 2^34]", (long long)key_range);
+  TDP_REQUIRE(ws_bytes >= dense_ws_bytes(key_range, n_build, n_probe), "join workspace too small");
+  PredSet bps, pps;
+  int rc = make_predset(bcols, nbcols, bpreds, nbpreds, n_build, &bps);
+  if (rc) return rc;
+  rc = make_predset(pcols, npcols, ppreds, nppreds, n_probe, &pps);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe);
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  const i64 words = rank_words(key_range), blocks = rank_blocks(key_range);
+  TDP_CUDA_TRY(cudaMemsetAsync(out_info, 0, 2 * sizeof(i64), st));
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
+  TDP_CUDA_TRY(cudaMemsetAsync(w.dj.bits, 0, (size_t)words * 4, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(w.dj.flags, 0, 16, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(w.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
+  const bool bfilt = bps.npreds > 0, pfilt = pps.npreds > 0;
+  if (bfilt)
+    dense_build_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
+                                                                                w.dj, bps);
+  else
+    dense_build_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
+                                                                                 w.dj, bps);
+  TDP_LAUNCH_CHECK("dense_build_kernel");
+  if (need_rows) {
+    rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(w.dj.bits, words, blocks,
+                                                                 w.dj.bcount, w.dj.wpre);
+    TDP_LAUNCH_CHECK("rank_popc_kernel");
+    rc = exclusive_scan_i64(w.dj.bcount, w.dj.boffs, blocks, nullptr, w.bscan_ws, w.bscan_bytes, st);
+    if (rc) return rc;
+    if (bfilt)
+      dense_place_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(
+          build_keys, n_build, w.dj, bps);
+    else
+      dense_place_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(
+          build_keys, n_build, w.dj, bps);
+    TDP_LAUNCH_CHECK("dense_place_kernel");
+  }
+  // out_info[1] = repeated key | key outside the range (two ints): fall back
+  TDP_CUDA_TRY(cudaMemcpyAsync(out_info + 1, w.dj.flags, 2 * sizeof(int), cudaMemcpyDeviceToDevice,
+                               st));
+  auto kernel = pfilt ? dense_count_kernel<true> : dense_count_kernel<false>;
+  kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(w.dj, probe_keys, n_probe, pps, w.match_bits,
+                                                   w.word_counts, w.tile_counts);
+  TDP_LAUNCH_CHECK("dense_count_kernel");
+  return exclusive_scan_i64(w.tile_counts, w.tile_offsets, tiles, out_info, w.scan_ws,
+                            w.scan_bytes, st);
+}
+
+int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe, int64_t lo,
+                        int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
+                        int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(ws_bytes >= dense_ws_bytes(key_range, n_build, n_probe), "join workspace too small");
+  TDP_REQUIRE(!need_rows || out_build_idx != nullptr, "null build row output");
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
+  cudaStream_t st = as_stream(stream);
+  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe);
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  HashTable none;  // the expansion only reads flags[1] (runs mode): the zero flag
+  std::memset(&none, 0, sizeof(none));
+  none.flags = w.dj.flags + 2;
+  join_expand_unique_kernel<<<(unsigned)ceil_div(tiles, kJoinWarps), kJoinThreads, 0, st>>>(
+      none, tiles, w.match_bits, w.word_counts, w.tile_counts, w.tile_offsets, out_probe_idx);
+  TDP_LAUNCH_CHECK("join_expand_unique_kernel");
+  if (need_rows) {
+    dense_pairs_kernel<<<(unsigned)(sm_count() * 8), 256, 0, st>>>(
+        w.dj, probe_keys, w.tile_counts, w.tile_offsets, tiles, out_probe_idx, out_build_idx);
+    TDP_LAUNCH_CHECK("dense_pairs_kernel");
+  }
+  return TDP_OK;
+}
+
+}  // extern "C"

@@ -1112,9 +1112,56 @@ def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTens
 # ---------------------------------------------------------------------------
 
 
+# dense-range join while the build key range is at most this many bits per
+# build row (bitmap <= 8 B per build row, and <= 2^34 bits)
+DENSE_JOIN_BITS_PER_ROW = 64
+
+
+def column_range(t: torch.Tensor, compute: bool = True) -> Optional[tuple[int, int]]:
+    """[min, max] of an int64 column: a column statistic cached on the tensor
+    (valid while its in-place version is unchanged), like a zone map.
+    Computed on first use with tdp_scan_minmax (one host read; not part of a
+    plan's replay log: a cached catalog statistic is the same on every run),
+    never during a CUDA-graph capture.  Gathered join outputs inherit their
+    base column's range (a superset of theirs)."""
+    meta = getattr(t, "_tdp_range", None)
+    if meta is not None and meta[0] == t._version:
+        return meta[1], meta[2]
+    if not compute or t.numel() == 0 or t.dtype != torch.int64 or t.dim() != 1 \
+            or torch.cuda.is_current_stream_capturing():
+        return None
+    nat.require_cuda(t)
+    prog = Program()
+    kc = prog.col_index(t.contiguous())
+    mm = torch.empty(2, dtype=torch.int64, device=t.device)
+    preds, npreds = prog.predicates(None)
+    nat.call("tdp_scan_minmax", prog.native_columns(), len(prog.cols), int(t.numel()), preds,
+             npreds, (c_int32 * 1)(kc), 1, nat.ptr(mm), nat.stream())
+    lo, hi = (int(v) for v in mm.tolist())
+    t._tdp_range = (t._version, lo, hi)
+    return lo, hi
+
+
+def _inherit_range(out: torch.Tensor, base: torch.Tensor, compute: bool = False) -> None:
+    r = column_range(base, compute=compute) if base.dtype == torch.int64 else None
+    if r is not None:
+        out._tdp_range = (out._version, r[0], r[1])
+
+
+def _dense_range(build_range, n_build: int) -> Optional[tuple[int, int]]:
+    if build_range is None:
+        return None
+    lo, hi = build_range
+    span = hi - lo + 1
+    if span < 1 or span > min(1 << 34, DENSE_JOIN_BITS_PER_ROW * max(n_build, 1 << 16)):
+        return None
+    return lo, span
+
+
 def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
-                 build_sel: Optional[Selection] = None
-                 ) -> Optional[tuple[torch.Tensor, torch.Tensor]]:
+                 build_sel: Optional[Selection] = None,
+                 build_range: Optional[tuple[int, int]] = None, need_build_rows: bool = True
+                 ) -> Optional[tuple[torch.Tensor, Optional[torch.Tensor]]]:
     """Inner equi-join row pairs: (probe rows, build rows), ordered by probe row
     then ascending build row (hash build, one probe per probe row).
 
@@ -1124,7 +1171,12 @@ def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
     side are base row ids (the filtered relation is never materialised).  One
     host synchronisation (the pair count) unless the build keys repeat; a
     filtered build with repeated keys returns None (the caller compacts the
-    build side first)."""
+    build side first).
+    With ``build_range`` (every build key in [lo, hi], a column statistic)
+    and a span small next to the build, the dense-range join runs first
+    (bitmap instead of hash table; unique keys only -- repeated keys fall back
+    to the hash join).  ``need_build_rows=False`` (no build column is output)
+    returns None for the build rows when the build keys are unique."""
     pk = _materialize(probe_key).contiguous().to(torch.int64)
     bk = _materialize(build_key).contiguous().to(torch.int64)
     nat.require_cuda(pk, bk)
@@ -1145,6 +1197,22 @@ def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
 
     bc, nbc, bp, nbp = predset(build_sel, n_build, "build")
     pc, npc, pp, npp = predset(probe_sel, n_probe, "probe")
+    dense = _dense_range(build_range, n_build)
+    if dense is not None and n_build and n_probe:
+        lo, span = dense
+        dws = nat.workspace(nat.load().tdp_join_dense_workspace(span, n_build, n_probe), dev)
+        nat.call("tdp_join_dense_prepare", nat.ptr(bk), n_build, bc, nbc, bp, nbp, nat.ptr(pk),
+                 n_probe, pc, npc, pp, npp, lo, span, int(need_build_rows), nat.ptr(info),
+                 nat.ptr(dws), dws.numel(), nat.stream())
+        m, fallback = read_ints(info)
+        if not fallback:
+            pi = torch.empty(m, dtype=torch.int64, device=dev)
+            bi = torch.empty(m, dtype=torch.int64, device=dev) if need_build_rows else None
+            if m:
+                nat.call("tdp_join_dense_emit", nat.ptr(pk), n_build, n_probe, lo, span,
+                         int(need_build_rows), nat.ptr(pi), nat.ptr(bi) if bi is not None else None,
+                         nat.ptr(dws), dws.numel(), nat.stream())
+            return pi, bi
     nat.call("tdp_join_prepare_ex", nat.ptr(bk), n_build, bc, nbc, bp, nbp, nat.ptr(pk), n_probe,
              pc, npc, pp, npp, 0, nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
     m, repeated = read_ints(info)
@@ -1183,7 +1251,18 @@ def _side_sources(cols: Sequence[EncodedTensor]):
     return [c.values.data.detach() for c in cols], None
 
 
-def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tensor):
+def _is_catalog_column(cols: Sequence[EncodedTensor]) -> bool:
+    """The side's columns are stored tensors (not lazy views): their range is
+    worth a (cached) statistic."""
+    return all(c.values._t is not None for c in cols)
+
+
+def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tensor,
+                 stats: bool = False):
+    """Output columns of one join side: its (base) columns gathered at
+    ``rows`` (through ``rowmap`` for a compacted side).  Outputs carry their
+    base column's range statistic (computed once when ``stats``: the base is
+    a catalog column), so a later join on them can run dense."""
     if not cols:
         return []
     if any(onehot_payload(c.values) is not None for c in cols):
@@ -1191,6 +1270,8 @@ def _gather_side(cols: Sequence[EncodedTensor], bases, rowmap, rows: torch.Tenso
                 for c in cols]
     src = rows if rowmap is None else gather_rows_raw(rowmap, rows)
     outs = gather_many([b.contiguous() for b in bases], src)
+    for o, b in zip(outs, bases):
+        _inherit_range(o, b, compute=stats)
     with trusted():
         return [EncodedTensor(Tensor(o), c.encoding) for o, c in zip(outs, cols)]
 
@@ -1233,17 +1314,24 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
     if not lkey_direct:
         lmap = lsel.indices() if lsel is not None else None
     lkey = lb[left_key] if lmap is None else gather_rows_raw(lb[left_key], lmap)
+    # the build key's range (a column statistic) enables the dense-range join;
+    # a semi-join (no right column returned) needs no build rows
+    brange = column_range(rb[right_key], compute=rsel is not None or _is_catalog_column(right))
+    need_rows = bool(ro)
     pairs = None
     if rkey_direct:
         pairs = join_indices(lkey, rb[right_key], probe_sel=lsel if lkey_direct else None,
-                             build_sel=rsel)
+                             build_sel=rsel, build_range=brange, need_build_rows=need_rows)
     if pairs is None:  # unfiltered build side, or a filtered one with repeated keys
         rmap = rsel.indices() if rsel is not None else None
         rkey = rb[right_key] if rmap is None else gather_rows_raw(rb[right_key], rmap)
-        pairs = join_indices(lkey, rkey, probe_sel=lsel if lkey_direct else None)
+        pairs = join_indices(lkey, rkey, probe_sel=lsel if lkey_direct else None,
+                             build_range=brange if rmap is None else None,
+                             need_build_rows=need_rows)
     pi, bi = pairs
-    return (_gather_side([left[i] for i in lo], [lb[i] for i in lo], lmap, pi)
-            + _gather_side([right[i] for i in ro], [rb[i] for i in ro], rmap, bi))
+    return (_gather_side([left[i] for i in lo], [lb[i] for i in lo], lmap, pi, stats=lsel is not None)
+            + _gather_side([right[i] for i in ro], [rb[i] for i in ro], rmap, bi,
+                           stats=rsel is not None))
 
 
 def _repartition(cols: Sequence[EncodedTensor], key_index: int, group) -> list[EncodedTensor]:

@@ -1,0 +1,127 @@
+"""GPU: equi-join (builder-defined: no reference join exists).
+
+The oracle ``join_inner`` (sort + searchsorted) is itself checked against a
+nested-loop join on adversarial inputs (CPU test below), then both join
+algorithms of the B200 path -- the hash join and the dense-range (bitmap)
+join -- must give exactly its (probe row, build row) pairs in its order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2211_02753_b200 as tq
+from oracle import relational as orc
+from paper_2211_02753_b200 import kernels as K
+from paper_2211_02753_b200 import workloads as wl
+
+I64 = np.iinfo(np.int64)
+
+
+def _cases():
+    rng = np.random.default_rng(40)
+    yield "dups_both_sides", rng.integers(0, 30, size=700), rng.integers(0, 30, size=500)
+    yield "all_equal", np.full(300, 7), np.full(200, 7)
+    yield "empty_probe", np.array([], dtype=np.int64), rng.integers(0, 9, size=50)
+    yield "empty_build", rng.integers(0, 9, size=50), np.array([], dtype=np.int64)
+    yield "no_match", np.arange(0, 400, 2), np.arange(1, 400, 2)
+    yield "int64_extremes", (np.array([I64.min, I64.max, 0, -1, 1, I64.min + 1, I64.max - 1] * 40)
+                             [rng.permutation(280)]), \
+        np.array([I64.max, I64.min, -1, I64.max, 5, I64.min + 1])
+    yield "negative_dense", rng.integers(-1000, -900, size=600), rng.permutation(100) - 1000
+
+
+@pytest.mark.parametrize("name,probe,build", list(_cases()))
+def test_oracle_join_equals_nested_loop(name, probe, build):
+    """CPU: the oracle against brute force (runs without a GPU)."""
+    probe, build = np.asarray(probe, np.int64), np.asarray(build, np.int64)
+    epi, ebi = orc.join_inner(probe, build)
+    npi, nbi = orc.join_nested_loop(probe, build)
+    np.testing.assert_array_equal(epi, npi)
+    np.testing.assert_array_equal(ebi, nbi)
+
+
+def _dev(a):
+    return torch.as_tensor(np.asarray(a, np.int64)).cuda()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,probe,build", list(_cases()))
+@pytest.mark.parametrize("dense", [False, True])
+def test_join_adversarial_vs_oracle(name, probe, build, dense):
+    probe, build = np.asarray(probe, np.int64), np.asarray(build, np.int64)
+    rng = None
+    if dense and len(build):
+        rng = (int(build.min()), int(build.max()))
+    pairs = K.join_indices(_dev(probe), _dev(build), build_range=rng)
+    epi, ebi = orc.join_inner(probe, build)
+    np.testing.assert_array_equal(pairs[0].cpu().numpy(), epi)
+    np.testing.assert_array_equal(pairs[1].cpu().numpy(), ebi)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lo", [0, -(2**40), 2**63 - 5_000_000, -(2**63)])
+@pytest.mark.parametrize("need_rows", [True, False])
+def test_dense_join_unique_build(lo, need_rows):
+    """Unique build keys in a known range: the bitmap join (incl. ranges at
+    the ends of int64), with and without the build-row index."""
+    rng = np.random.default_rng(abs(lo) % 1000 + 3)
+    span = 4_000_000
+    build = lo + rng.choice(span, size=700_000, replace=False).astype(np.int64)
+    probe = lo + rng.integers(0, span, size=1_500_000).astype(np.int64)
+    pairs = K.join_indices(_dev(probe), _dev(build), build_range=(lo, lo + span - 1),
+                           need_build_rows=need_rows)
+    epi, ebi = orc.join_inner(probe, build)
+    np.testing.assert_array_equal(pairs[0].cpu().numpy(), epi)
+    if need_rows:
+        np.testing.assert_array_equal(pairs[1].cpu().numpy(), ebi)
+    else:
+        assert pairs[1] is None
+
+
+@pytest.mark.gpu
+def test_dense_join_filtered_sides_from_base_columns():
+    """A filtered build and a filtered probe read straight from base columns
+    (equi_join on lazy selections): the build key's range is the catalog
+    column's statistic, cached on the tensor."""
+    rng = np.random.default_rng(8)
+    nb, npr = 300_000, 2_000_000
+    bkey = rng.permutation(nb).astype(np.int64) * 3 + 11
+    bflag = rng.integers(0, 4, size=nb)
+    pkey = rng.integers(0, 3 * nb + 20, size=npr).astype(np.int64)
+    pval = rng.normal(size=npr)
+    right = [tq.plain(tq.Tensor(bkey)), tq.plain(tq.Tensor(bflag))]
+    left = [tq.plain(tq.Tensor(pkey)), tq.plain(tq.Tensor(pval))]
+    rf = K.filter_exact(right, [(1, "<", 2)])
+    lf = K.filter_exact(left, [(1, ">", 0.3)])
+    out = K.equi_join(lf, rf, 0, 0)
+    base = right[0].values.data
+    assert K.column_range(base, compute=False) == (int(bkey.min()), int(bkey.max()))
+    keep_b = bflag < 2
+    keep_p = pval > 0.3
+    epi, ebi = orc.join_inner(pkey[keep_p], bkey[keep_b])
+    np.testing.assert_array_equal(out[0].values.numpy(), pkey[keep_p][epi])
+    np.testing.assert_array_equal(out[1].values.numpy(), pval[keep_p][epi])
+    np.testing.assert_array_equal(out[3].values.numpy(), bflag[keep_b][ebi])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sf", [0.02, 0.2])
+def test_q3_dense_joins_and_replay(sf):
+    """The Q3 pipeline (both joins dense: c_custkey, o_orderkey statistics)
+    eager and replayed, all four result columns against the oracle."""
+    from oracle import tpch as otpch
+
+    tables = wl.q3_arrays(sf, seed=7)
+    cat = wl.q3_catalog(tables)
+    plan = wl.Q3Plan(cat)
+    exp = otpch.q3(tables)
+    for _ in range(4):  # eager, record, capture, replay
+        res = plan.run(cat)
+        got = [c.values.numpy() for c in res.columns]
+        np.testing.assert_array_equal(got[0], exp["l_orderkey"])
+        np.testing.assert_allclose(got[1], exp["sum_rev"], rtol=1e-9)
+        np.testing.assert_allclose(got[2], exp["avg_o_orderdate"], rtol=1e-12)
+        np.testing.assert_allclose(got[3], exp["avg_o_shippriority"], rtol=1e-12)

@@ -1259,47 +1259,50 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
 namespace tdp {
 namespace {
 
+// A distinct key owns a *cell* (claimed on first insertion, zeroed by its
+// claimer and then published through cidx): image, count, integer sums and
+// the float SUMs' fixed-point words.  Only the key table (8 B per slot) and
+// the cell indices (4 B) are cleared per call -- not a full set of per-slot
+// accumulators -- and the m claimed cells are the groups directly.
 struct HashAgg {
-  u64* slot;     // [cap + 1]  key image (0 = empty); [cap] = side slot for INT64_MIN
-  u64* cnt;      // [cap + 1]
-  u64* acc;      // [naggs][cap + 1]  (double bits for SUM_F64, u64 for SUM_I64)
-  u64* fx;       // [nfixed][cap + 1][kFixedWords]  fixed-point cells of the float SUMs
-  i64* flags;    // [cap + 1]
-  i64* offs;     // [cap + 1]
-  void* scan_ws;
-  size_t scan_bytes;
+  u64* slot;                 // [cap]      key image (0 = empty)
+  unsigned* cidx;            // [cap + 1]  published cell + 1; [cap]: INT64_MIN (image 0)
+  unsigned long long* misc;  // [0] cells claimed (= groups m), [1] INT64_MIN claimed
+  u64* cells;                // [ncap][cw]
+  i64 ncap;
+  int cw;                    // image, count, naggs sums, kFixedWords per float SUM
+  int naggs;
   u64 mask;
-  i64 cap;       // power of two
+  i64 cap;                   // power of two
 };
+
+constexpr int kCellImg = 0, kCellCnt = 1, kCellAcc = 2;
+
+int cell_words(int naggs, int nfixed) { return kCellAcc + naggs + kFixedWords * nfixed; }
 
 size_t hashagg_ws_bytes(i64 n, int naggs) {
   const i64 cap = (i64)table_capacity(n);
-  const size_t per = (size_t)(cap + 1) * 8;
-  const size_t na = naggs > 0 ? naggs : 0;
-  return sort_ws_bytes(n) + align256(per) * (4 + na) + align256(per * kFixedWords) * na +
-         exclusive_scan_workspace(cap + 1) + 1024;
+  const i64 ncap = n > 0 ? n : 1;
+  const int na = naggs > 0 ? naggs : 0;
+  return sort_ws_bytes(n) + align256((size_t)cap * 8) + align256((size_t)(cap + 1) * 4) + 256 +
+         align256((size_t)ncap * cell_words(na, na) * 8) + 1024;
 }
 
-HashAgg carve_hashagg(void* ws, i64 n, int naggs) {
+HashAgg carve_hashagg(void* ws, i64 n, const ValSet& vs) {
   HashAgg h;
   h.cap = (i64)table_capacity(n);
   h.mask = (u64)h.cap - 1;
-  const size_t per = align256((size_t)(h.cap + 1) * 8);
+  h.ncap = n > 0 ? n : 1;
+  h.naggs = vs.naggs;
+  h.cw = cell_words(vs.naggs, vs.nfixed);
   unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(n);
   h.slot = (u64*)p;
-  p += per;
-  h.cnt = (u64*)p;
-  p += per;
-  h.flags = (i64*)p;
-  p += per;
-  h.offs = (i64*)p;
-  p += per;
-  h.acc = (u64*)p;
-  p += per * (naggs > 0 ? naggs : 0);
-  h.fx = (u64*)p;  // fixed-point cells of the float SUMs (a prefix of naggs blocks)
-  p += align256((size_t)(h.cap + 1) * 8 * kFixedWords) * (naggs > 0 ? naggs : 0);
-  h.scan_ws = p;
-  h.scan_bytes = exclusive_scan_workspace(h.cap + 1) + 512;
+  p += align256((size_t)h.cap * 8);
+  h.cidx = (unsigned*)p;
+  p += align256((size_t)(h.cap + 1) * 4);
+  h.misc = (unsigned long long*)p;
+  p += 256;
+  h.cells = (u64*)p;
   return h;
 }
 
@@ -1318,6 +1321,28 @@ __device__ __forceinline__ V group_sum(V v, unsigned peers, int lane) {
   return total;
 }
 
+// A new key: claim the next cell, zero it, then publish its index (release).
+__device__ __forceinline__ i64 claim_cell(const HashAgg& h, u64 img, unsigned* pub) {
+  const i64 id = (i64)atomicAdd(h.misc, 1ull);
+  u64* c = h.cells + id * h.cw;
+  c[kCellImg] = img;
+  for (int w = 1; w < h.cw; ++w) c[w] = 0ull;
+  __threadfence();
+  atomicExch(pub, (unsigned)(id + 1));
+  return id;
+}
+
+// A key another warp inserted: wait for its cell index (the claimer is
+// running: it won the slot's CAS, and it is never in this warp -- a warp's
+// lanes with one key are a single peer group with one leader).
+__device__ __forceinline__ i64 wait_cell(const unsigned* pub) {
+  unsigned v;
+  while ((v = *(volatile const unsigned*)pub) == 0u) {
+  }
+  __threadfence();
+  return (i64)v - 1;
+}
+
 __global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, ValSet vs) {
   const int lane = threadIdx.x & 31;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -1329,63 +1354,66 @@ __global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, V
     const i64 k = keys[i];
     const unsigned peers = __match_any_sync(active, k);
     const int leader = __ffs(peers) - 1;
-    // the leader finds (or inserts) the key's slot
-    i64 slot = 0;
+    // the leader finds (or inserts) the key's cell
+    i64 cell = 0;
     if (lane == leader) {
       const u64 img = (u64)k ^ 0x8000000000000000ull;
       if (img == 0ull) {
-        slot = h.cap;
+        cell = atomicCAS(h.misc + 1, 0ull, 1ull) == 0ull ? claim_cell(h, 0ull, h.cidx + h.cap)
+                                                          : wait_cell(h.cidx + h.cap);
       } else {
         u64 s = join_hash(k) & h.mask;
         for (;;) {
           const unsigned long long prev =
               atomicCAS(reinterpret_cast<unsigned long long*>(h.slot + s), 0ull,
                         (unsigned long long)img);
-          if (prev == 0ull || prev == img) break;
+          if (prev == 0ull) {
+            cell = claim_cell(h, img, h.cidx + s);
+            break;
+          }
+          if (prev == img) {
+            cell = wait_cell(h.cidx + s);
+            break;
+          }
           s = (s + 1) & h.mask;
         }
-        slot = (i64)s;
       }
     }
-    slot = __shfl_sync(peers, slot, leader);
-    const unsigned long long c = (unsigned long long)__popc(peers);
-    if (lane == leader) atomicAdd(reinterpret_cast<unsigned long long*>(h.cnt + slot), c);
+    cell = __shfl_sync(peers, cell, leader);
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(h.cells + cell * h.cw);
+    if (lane == leader) atomicAdd(c + kCellCnt, (unsigned long long)__popc(peers));
     for (int a = 0; a < vs.naggs; ++a) {
       if (vs.kind[a] == TDP_AGG_COUNT) continue;
-      u64* dst = h.acc + (i64)a * (h.cap + 1) + slot;
       if (vs.kind[a] == TDP_AGG_SUM_F64) {
-        // the peers' sum in fixed lane order, then order-free integer cells
+        // the peers' sum in fixed lane order, then order-free integer words
         const double v = group_sum(load_as_f64(vs.p[a], vs.dt[a], i), peers, lane);
-        if (lane == leader)
-          fixed_add(reinterpret_cast<unsigned long long*>(h.fx) +
-                        ((i64)vs.fidx[a] * (h.cap + 1) + slot) * kFixedWords, v);
+        if (lane == leader) fixed_add(c + kCellAcc + vs.naggs + kFixedWords * vs.fidx[a], v);
       } else {
         const unsigned long long v =
             group_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i), peers, lane);
-        if (lane == leader) atomicAdd(reinterpret_cast<unsigned long long*>(dst), v);
+        if (lane == leader) atomicAdd(c + kCellAcc + a, v);
       }
     }
   }
 }
 
-__global__ void hashagg_flags_kernel(HashAgg h) {
-  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s <= h.cap;
-       s += (i64)gridDim.x * blockDim.x)
-    h.flags[s] = s < h.cap ? (h.slot[s] != 0ull) : (h.cnt[h.cap] != 0ull);
-}
-
-// With `range` (preset ~0 / 0): also the min / max key image into range[1], [2].
-__global__ void hashagg_compact_kernel(HashAgg h, u64* __restrict__ out_img,
-                                       i64* __restrict__ out_slot,
-                                       unsigned long long* __restrict__ range) {
+// Per claimed cell: float SUMs -> double bits in the cell's sum word; the key
+// image and cell id into the sort input; the images' [min, max] into range.
+__global__ void hashagg_cells_kernel(HashAgg h, ValSet vs, u64* __restrict__ out_img,
+                                     i64* __restrict__ out_cell,
+                                     unsigned long long* __restrict__ range) {
+  const i64 m = (i64)h.misc[0];
   unsigned long long lo = ~0ull, hi = 0ull;
-  for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s <= h.cap;
-       s += (i64)gridDim.x * blockDim.x) {
-    if (!h.flags[s]) continue;
-    const i64 o = h.offs[s];
-    const u64 img = s < h.cap ? h.slot[s] : 0ull;  // key images sort like the keys
-    out_img[o] = img;
-    out_slot[o] = s;
+  for (i64 id = (i64)blockIdx.x * blockDim.x + threadIdx.x; id < m;
+       id += (i64)gridDim.x * blockDim.x) {
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(h.cells + id * h.cw);
+    for (int a = 0; a < vs.naggs; ++a)
+      if (vs.kind[a] == TDP_AGG_SUM_F64)
+        c[kCellAcc + a] = (unsigned long long)__double_as_longlong(
+            fixed_value(c + kCellAcc + vs.naggs + kFixedWords * vs.fidx[a]));
+    const u64 img = c[kCellImg];  // key images sort like the keys
+    out_img[id] = img;
+    out_cell[id] = id;
     lo = img < lo ? img : lo;
     hi = img > hi ? img : hi;
   }
@@ -1467,17 +1495,17 @@ size_t rank_ws_bytes(i64 range) {
 }
 
 __global__ void hashagg_gather_kernel(HashAgg h, const u64* __restrict__ img,
-                                      const i64* __restrict__ slot, i64 m, ValSet vs,
+                                      const i64* __restrict__ cell, i64 m, ValSet vs,
                                       i64* __restrict__ out_keys, i64* __restrict__ out_counts,
                                       u64* __restrict__ out_sums) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (i64)gridDim.x * blockDim.x) {
-    const i64 s = slot[i];
+    const u64* c = h.cells + cell[i] * h.cw;
     out_keys[i] = (i64)(img[i] ^ 0x8000000000000000ull);
-    const u64 c = h.cnt[s];
-    out_counts[i] = (i64)c;
+    const u64 cnt = c[kCellCnt];
+    out_counts[i] = (i64)cnt;
     for (int a = 0; a < vs.naggs; ++a)
-      out_sums[(i64)a * m + i] = vs.kind[a] == TDP_AGG_COUNT ? c : h.acc[(i64)a * (h.cap + 1) + s];
+      out_sums[(i64)a * m + i] = vs.kind[a] == TDP_AGG_COUNT ? cnt : c[kCellAcc + a];
   }
 }
 
@@ -1533,30 +1561,16 @@ static int hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
     TDP_CUDA_TRY(cudaMemsetAsync(out_ngroups, 0, 8, st));
     return TDP_OK;
   }
-  HashAgg h = carve_hashagg(ws, n, naggs);
-  const size_t per = (size_t)(h.cap + 1) * 8;
-  TDP_CUDA_TRY(cudaMemsetAsync(h.slot, 0, per, st));
-  TDP_CUDA_TRY(cudaMemsetAsync(h.cnt, 0, per, st));
-  for (int a = 0; a < naggs; ++a)
-    if (vs.kind[a] != TDP_AGG_SUM_F64)
-      TDP_CUDA_TRY(cudaMemsetAsync(h.acc + (i64)a * (h.cap + 1), 0, per, st));
-  if (vs.nfixed)
-    TDP_CUDA_TRY(cudaMemsetAsync(h.fx, 0, per * kFixedWords * vs.nfixed, st));
+  HashAgg h = carve_hashagg(ws, n, vs);
+  TDP_CUDA_TRY(cudaMemsetAsync(h.slot, 0, (size_t)h.cap * 8, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(h.cidx, 0, (size_t)(h.cap + 1) * 4, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(h.misc, 0, 16, st));
   hashagg_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(keys, n, h, vs);
   TDP_LAUNCH_CHECK("hashagg_kernel");
-  if (vs.nfixed) {  // float sums -> h.acc as double bits (before compaction reads them)
-    fixed_finalize_kernel<<<stream_grid((h.cap + 1) * naggs, 256, 8), 256, 0, st>>>(
-        reinterpret_cast<const unsigned long long*>(h.fx), h.cap + 1, vs,
-        reinterpret_cast<unsigned long long*>(h.acc), h.cap + 1);
-    TDP_LAUNCH_CHECK("fixed_finalize_kernel");
-  }
-  hashagg_flags_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h);
-  TDP_LAUNCH_CHECK("hashagg_flags_kernel");
-  rc = exclusive_scan_i64(h.flags, h.offs, h.cap + 1, out_ngroups, h.scan_ws, h.scan_bytes, st);
-  if (rc) return rc;
   SortBuffers b = carve(ws, n);
-  hashagg_compact_kernel<<<stream_grid(h.cap + 1, 256 * 4, 8), 256, 0, st>>>(h, b.k0, b.i0, range);
-  TDP_LAUNCH_CHECK("hashagg_compact_kernel");
+  hashagg_cells_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(h, vs, b.k0, b.i0, range);
+  TDP_LAUNCH_CHECK("hashagg_cells_kernel");
+  TDP_CUDA_TRY(cudaMemcpyAsync(out_ngroups, h.misc, 8, cudaMemcpyDeviceToDevice, st));
   return TDP_OK;
 }
 
@@ -1587,8 +1601,9 @@ int tdp_groupby_hash_emit_ranked(int64_t n, const int32_t* agg_kinds, int32_t na
   if (rc) return rc;
   vs.naggs = naggs;
   for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
+  number_fixed(&vs);
   cudaStream_t st = as_stream(stream);
-  HashAgg h = carve_hashagg(ws, n, naggs);
+  HashAgg h = carve_hashagg(ws, n, vs);
   SortBuffers b = carve(ws, n);
   const i64 words = rank_words(key_range), blocks = rank_blocks(key_range);
   unsigned char* p = reinterpret_cast<unsigned char*>(rank_ws);
@@ -1629,8 +1644,9 @@ int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, in
   if (rc) return rc;
   vs.naggs = naggs;
   for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
+  number_fixed(&vs);
   cudaStream_t st = as_stream(stream);
-  HashAgg h = carve_hashagg(ws, n, naggs);
+  HashAgg h = carve_hashagg(ws, n, vs);
   SortBuffers b = carve(ws, n);
   u64* sk;
   i64* order;

@@ -1248,7 +1248,13 @@ def _side_sources(cols: Sequence[EncodedTensor]):
     if sels is not None and len(sels) == 1:
         sel = cols[0].values._lazy.sel
         return [c.values._lazy.expr.col for c in cols], sel
-    return [c.values.data.detach() for c in cols], None
+    # the stored tensors themselves (a detach() would be a new object without
+    # the column statistics cached on it)
+    return [_no_grad(c.values.data) for c in cols], None
+
+
+def _no_grad(t: torch.Tensor) -> torch.Tensor:
+    return t.detach() if t.requires_grad else t
 
 
 def _is_catalog_column(cols: Sequence[EncodedTensor]) -> bool:

@@ -29,6 +29,7 @@ sizing its output) runs eagerly from then on.  ``TDP_REPLAY=0`` or
 
 from __future__ import annotations
 
+import gc
 import os
 import threading
 import warnings
@@ -251,6 +252,11 @@ def _capture(execute, tables, log):
     nat.load().tdp_clear_error()
     graph = torch.cuda.CUDAGraph()
     launches0 = nat.launch_count()
+    # no cyclic garbage collection inside the capture: a collected object of an
+    # earlier run holding a CUDA event (a DeferredCount) would destroy it, an
+    # API call that invalidates the capture
+    gc_was_enabled = gc.isenabled()
+    gc.disable()
     try:
         with capturing(), warnings.catch_warnings(), hostread.replaying(log) as rlog:
             warnings.simplefilter("ignore")  # "graph is empty": a lazy result, no launches
@@ -261,6 +267,8 @@ def _capture(execute, tables, log):
         if not rlog.consumed():
             raise hostread.ReplayMismatch("fewer host reads than recorded")
     except Exception:
+        if gc_was_enabled:
+            gc.enable()
         # an uncapturable call inside the plan (or a diverging read sequence)
         if os.environ.get("TDP_REPLAY_DEBUG"):
             import traceback
@@ -269,6 +277,8 @@ def _capture(execute, tables, log):
         nat.load().tdp_clear_error()
         torch.cuda.synchronize()
         return _NOGRAPH
+    if gc_was_enabled:
+        gc.enable()
     launches = nat.launch_count() - launches0
     template = _Template.build(table, inputs)
     if template is None:

@@ -86,14 +86,19 @@ enum tdp_cmp_op { TDP_EQ = 0, TDP_NE = 1, TDP_LT = 2, TDP_GT = 3, TDP_LE = 4, TD
  *   TDP_CMP_ALL  row always matches (out-of-range int literal)
  *   TDP_CMP_DEC  double(x) / double(lit_i) <op> lit_f: a float64 column kept
  *                as scaled integers (x = value * lit_i exactly), compared
- *                after the same correctly rounded division that decodes it */
+ *                after the same correctly rounded division that decodes it *   TDP_CMP_BITMAP  semi-join membership: x = int64(col) - lit_i, row
+ *                   matches iff 0 <= x < (int64)lit_f and bit x is set in
+ *                   the uint32-word bitmap passed as column `reserved`
+ *                   (op ignored; built by tdp_join_dense_bitmap)
+ */
 enum tdp_cmp_type {
   TDP_CMP_I64 = 0,
   TDP_CMP_F64 = 1,
   TDP_CMP_F32 = 2,
   TDP_CMP_NONE = 3,
   TDP_CMP_ALL = 4,
-  TDP_CMP_DEC = 5
+  TDP_CMP_DEC = 5,
+  TDP_CMP_BITMAP = 6
 };
 
 typedef struct tdp_predicate {
@@ -416,6 +421,15 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
                            int32_t npcols, const tdp_predicate* ppreds, int32_t nppreds,
                            int64_t lo, int64_t key_range, int32_t need_rows, int64_t* out_info,
                            void* ws, size_t ws_bytes, void* stream);
+/* Semi-join bitmap: bit (key - lo) of out_bits (ceil(key_range/32) uint32
+ * words, cleared here) for every build row passing the build predicates;
+ * out_flags[0] = a key repeats, [1] = a key outside [lo, lo + key_range)
+ * (int32 each).  The bitmap is the operand of a TDP_CMP_BITMAP predicate:
+ * a probe relation filtered by it is the left semi-join (inner join whose
+ * right side contributes no columns, unique right keys) without pairs.      */
+int tdp_join_dense_bitmap(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                          int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds, int64_t lo,
+                          int64_t key_range, uint32_t* out_bits, int32_t* out_flags, void* stream);
 int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe, int64_t lo,
                         int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
                         int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);

@@ -33,7 +33,7 @@ NAME_TO_TDP = {"int64": I64, "float64": F64, "float32": F32, "bool": BOOL}
 
 # comparison ops / kinds
 CMP_OPS = {"=": 0, "<>": 1, "<": 2, ">": 3, "<=": 4, ">=": 5}
-CMP_I64, CMP_F64, CMP_F32, CMP_NONE, CMP_ALL, CMP_DEC = 0, 1, 2, 3, 4, 5
+CMP_I64, CMP_F64, CMP_F32, CMP_NONE, CMP_ALL, CMP_DEC, CMP_BITMAP = 0, 1, 2, 3, 4, 5, 6
 
 # expression opcodes
 OP_LOAD, OP_CONST, OP_CAST, OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3, 4, 5, 6
@@ -157,6 +157,9 @@ _SIGNATURES = {
                                        POINTER(Column), c_int32, POINTER(Predicate), c_int32,
                                        c_int64, c_int64, c_int32, c_void_p, c_void_p, c_size_t,
                                        c_void_p]),
+    "tdp_join_dense_bitmap": (c_int, [c_void_p, c_int64, POINTER(Column), c_int32,
+                                      POINTER(Predicate), c_int32, c_int64, c_int64, c_void_p,
+                                      c_void_p, c_void_p]),
     "tdp_join_dense_emit": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32,
                                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_softmax_fwd": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p]),

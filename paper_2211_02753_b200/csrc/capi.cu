@@ -65,7 +65,7 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
   for (int k = 0; k < npreds; ++k) {
     const tdp_predicate& p = preds[k];
     TDP_REQUIRE(p.op >= TDP_EQ && p.op <= TDP_GE, "predicate %d: bad operator %d", k, p.op);
-    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_DEC, "predicate %d: bad compare kind",
+    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_BITMAP, "predicate %d: bad compare kind",
                 k);
     TDP_REQUIRE(p.cmp != TDP_CMP_DEC || p.lit_i > 0, "predicate %d: decimal divisor must be > 0", k);
     DevPred& d = out->p[k];
@@ -74,6 +74,14 @@ int make_predset(const tdp_column* cols, int32_t ncols, const tdp_predicate* pre
     d.li = p.lit_i;
     d.lf = p.lit_f;
     d.pad = 0;
+    d.bits = nullptr;
+    if (p.cmp == TDP_CMP_BITMAP) {
+      TDP_REQUIRE(p.reserved >= 0 && p.reserved < ncols, "predicate %d: bitmap column %d out of range",
+                  k, p.reserved);
+      TDP_REQUIRE(p.lit_f >= 1.0 && (double)cols[p.reserved].rows * 32.0 >= p.lit_f,
+                  "predicate %d: bitmap shorter than its key range", k);
+      d.bits = reinterpret_cast<const unsigned*>(cols[p.reserved].data);
+    }
     if (p.cmp == TDP_CMP_NONE || p.cmp == TDP_CMP_ALL) {
       d.ptr = nullptr;
       d.dtype = TDP_I64;

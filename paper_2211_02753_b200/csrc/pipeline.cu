@@ -209,9 +209,13 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
   for (size_t k = 0; k < s.preds.size(); ++k) {
     const tdp_predicate& p = s.preds[k];
     TDP_REQUIRE(p.op >= TDP_EQ && p.op <= TDP_GE, "predicate %zu: bad op", k);
-    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_DEC, "predicate %zu: bad compare", k);
+    TDP_REQUIRE(p.cmp >= TDP_CMP_I64 && p.cmp <= TDP_CMP_BITMAP, "predicate %zu: bad compare", k);
     TDP_REQUIRE(p.cmp != TDP_CMP_DEC || p.lit_i > 0, "predicate %zu: bad decimal divisor", k);
-    if (p.cmp <= TDP_CMP_F32 || p.cmp == TDP_CMP_DEC) {
+    if (p.cmp == TDP_CMP_BITMAP)  // the bitmap is read by address, never streamed
+      TDP_REQUIRE(p.reserved >= 0 && p.reserved < ncols && p.lit_f >= 1.0 &&
+                      (double)cols[p.reserved].rows * 32.0 >= p.lit_f,
+                  "predicate %zu: bad bitmap operand", k);
+    if (p.cmp <= TDP_CMP_F32 || p.cmp == TDP_CMP_DEC || p.cmp == TDP_CMP_BITMAP) {
       TDP_REQUIRE(p.column >= 0 && p.column < ncols, "predicate %zu: bad column", k);
       used[p.column] = 1;
     }
@@ -509,6 +513,11 @@ std::string generate(const Spec& s) {
       case TDP_CMP_NONE:
         o << "  keep = false;\n";
         break;
+      case TDP_CMP_BITMAP:
+        o << "  { const u64 x = (u64)(i64)r.c" << p.column << " - (u64)P.pli[" << k
+          << "]; keep &= x < (u64)(i64)P.plf[" << k << "] && ((__ldg((const unsigned*)P.col["
+          << p.reserved << "] + (x >> 5)) >> (x & 31)) & 1u); }\n";
+        break;
       default:
         break;
     }
@@ -589,7 +598,8 @@ std::string signature(const Spec& s) {
   put((long long)s.col_dtype.size());
   for (int d : s.col_dtype) put(d);
   put((long long)s.preds.size());
-  for (const auto& p : s.preds) put(((long long)p.column << 16) | (p.op << 8) | p.cmp);
+  for (const auto& p : s.preds)
+    put(((long long)p.reserved << 40) | ((long long)p.column << 16) | (p.op << 8) | p.cmp);
   put((long long)s.prog.size());
   for (const auto& in : s.prog) put(((long long)in.op << 48) ^ ((long long)in.dtype << 40) ^ ((long long)in.a << 20) ^ in.b);
   put((long long)s.keys.size());

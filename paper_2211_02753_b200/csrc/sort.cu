@@ -1565,10 +1565,12 @@ static int hash_prepare(const int64_t* keys, int64_t n, const tdp_column* vals,
   TDP_CUDA_TRY(cudaMemsetAsync(h.slot, 0, (size_t)h.cap * 8, st));
   TDP_CUDA_TRY(cudaMemsetAsync(h.cidx, 0, (size_t)(h.cap + 1) * 4, st));
   TDP_CUDA_TRY(cudaMemsetAsync(h.misc, 0, 16, st));
-  hashagg_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(keys, n, h, vs);
+  // one row per thread: the pass is latency-bound (CAS, dependent atomics of the
+  // fixed-point cells), so keep every row's chain in flight at once
+  hashagg_kernel<<<stream_grid(n, 256, 32), 256, 0, st>>>(keys, n, h, vs);
   TDP_LAUNCH_CHECK("hashagg_kernel");
   SortBuffers b = carve(ws, n);
-  hashagg_cells_kernel<<<stream_grid(n, 256 * 4, 8), 256, 0, st>>>(h, vs, b.k0, b.i0, range);
+  hashagg_cells_kernel<<<stream_grid(n, 256, 32), 256, 0, st>>>(h, vs, b.k0, b.i0, range);
   TDP_LAUNCH_CHECK("hashagg_cells_kernel");
   TDP_CUDA_TRY(cudaMemcpyAsync(out_ngroups, h.misc, 8, cudaMemcpyDeviceToDevice, st));
   return TDP_OK;
@@ -1680,11 +1682,19 @@ struct DenseJoin {
   unsigned short* wpre;  // [words]  set bits of the block's earlier words
   i64* bcount;           // [blocks]
   i64* boffs;            // [blocks]  set bits of earlier blocks
-  i64* rank_row;         // [nb]      build row of each rank (need_rows)
+  i64* rank_row;         // [nb]      build row of each rank (need_rows, rank mode)
+  int* row_of;           // [R]       build row of each key offset (need_rows, direct mode)
   int* flags;            // [0] repeated key, [1] key outside [lo, lo+R), [2] zero (expand)
   u64 lo;
   i64 range;
 };
+
+// Build rows by key offset in a plain int32 array of R entries (no clearing:
+// only offsets whose bit is set are read) while R <= 8 x the build rows;
+// beyond, by rank among the set bits.
+inline bool dense_direct(i64 range, i64 nb) {
+  return range <= 8 * (nb > (1 << 20) ? nb : (1 << 20)) && nb < ((i64)1 << 31);
+}
 
 __device__ __forceinline__ i64 dense_rank(const DenseJoin& dj, u64 d) {
   const i64 w = (i64)(d >> 5);
@@ -1704,6 +1714,7 @@ __global__ void dense_build_kernel(const i64* __restrict__ keys, i64 nb, DenseJo
     }
     const unsigned bit = 1u << (x & 31);
     if (atomicOr(dj.bits + (x >> 5), bit) & bit) dj.flags[0] = 1;
+    if (dj.row_of != nullptr) dj.row_of[x] = (int)i;
   }
 }
 
@@ -1768,7 +1779,10 @@ __global__ void dense_pairs_kernel(DenseJoin dj, const i64* __restrict__ probe,
   const i64 total = tile_offsets[tiles - 1] + tile_counts[tiles - 1];
   for (i64 m = (i64)blockIdx.x * blockDim.x + threadIdx.x; m < total;
        m += (i64)gridDim.x * blockDim.x)
-    out_build[m] = dj.rank_row[dense_rank(dj, (u64)__ldg(probe + out_probe[m]) - dj.lo)];
+  {
+    const u64 d = (u64)__ldg(probe + out_probe[m]) - dj.lo;
+    out_build[m] = dj.row_of != nullptr ? (i64)dj.row_of[d] : dj.rank_row[dense_rank(dj, d)];
+  }
 }
 
 struct DenseWs {
@@ -1788,12 +1802,13 @@ size_t dense_ws_bytes(i64 range, i64 nb, i64 np) {
   const i64 words = rank_words(r), blocks = rank_blocks(r);
   const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
   return align256((size_t)words * 4) + align256((size_t)words * 2) + 2 * align256((size_t)blocks * 8) +
-         align256((size_t)(nb > 0 ? nb : 1) * 8) + 256 + align256((size_t)tiles * kJoinWords * 4) +
+         align256((size_t)(nb > 0 ? nb : 1) * 8) + (dense_direct(r, nb) ? align256((size_t)r * 4) : 0) +
+         256 + align256((size_t)tiles * kJoinWords * 4) +
          align256((size_t)tiles * kJoinWords * 8) + 2 * align256((size_t)tiles * 8) +
          exclusive_scan_workspace(tiles) + exclusive_scan_workspace(blocks) + 4096;
 }
 
-DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np) {
+DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np, bool need_rows) {
   DenseWs w;
   const i64 r = range > 0 ? range : 1;
   const i64 words = rank_words(r), blocks = rank_blocks(r);
@@ -1809,6 +1824,11 @@ DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np) {
   p += align256((size_t)blocks * 8);
   w.dj.rank_row = (i64*)p;
   p += align256((size_t)(nb > 0 ? nb : 1) * 8);
+  w.dj.row_of = nullptr;
+  if (dense_direct(r, nb)) {
+    if (need_rows) w.dj.row_of = (int*)p;
+    p += align256((size_t)r * 4);
+  }
   w.dj.flags = (int*)p;
   p += 256;
   w.dj.lo = (u64)lo;
@@ -1855,7 +1875,7 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   rc = make_predset(pcols, npcols, ppreds, nppreds, n_probe, &pps);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
-  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe);
+  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe, need_rows != 0);
   const i64 tiles = ceil_div(n_probe, kJoinTile);
   const i64 words = rank_words(key_range), blocks = rank_blocks(key_range);
   TDP_CUDA_TRY(cudaMemsetAsync(out_info, 0, 2 * sizeof(i64), st));
@@ -1871,7 +1891,7 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
     dense_build_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
                                                                                  w.dj, bps);
   TDP_LAUNCH_CHECK("dense_build_kernel");
-  if (need_rows) {
+  if (need_rows && w.dj.row_of == nullptr) {
     rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(w.dj.bits, words, blocks,
                                                                  w.dj.bcount, w.dj.wpre);
     TDP_LAUNCH_CHECK("rank_popc_kernel");
@@ -1896,6 +1916,35 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
                             w.scan_bytes, st);
 }
 
+int tdp_join_dense_bitmap(const int64_t* build_keys, int64_t n_build, const tdp_column* bcols,
+                          int32_t nbcols, const tdp_predicate* bpreds, int32_t nbpreds, int64_t lo,
+                          int64_t key_range, uint32_t* out_bits, int32_t* out_flags, void* stream) {
+  TDP_REQUIRE(n_build >= 0 && out_bits != nullptr && out_flags != nullptr, "bad bitmap arguments");
+  TDP_REQUIRE(key_range >= 1 && key_range <= ((int64_t)1 << 34),
+              "dense join key range %lld outside [1, 2^34]", (long long)key_range);
+  PredSet bps;
+  int rc = make_predset(bcols, nbcols, bpreds, nbpreds, n_build, &bps);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  TDP_CUDA_TRY(cudaMemsetAsync(out_bits, 0, (size_t)rank_words(key_range) * 4, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(out_flags, 0, 2 * sizeof(int32_t), st));
+  if (n_build == 0) return TDP_OK;
+  DenseJoin dj;
+  std::memset(&dj, 0, sizeof(dj));
+  dj.bits = out_bits;
+  dj.flags = out_flags;
+  dj.lo = (u64)lo;
+  dj.range = key_range;
+  if (bps.npreds > 0)
+    dense_build_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
+                                                                                dj, bps);
+  else
+    dense_build_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
+                                                                                 dj, bps);
+  TDP_LAUNCH_CHECK("dense_build_kernel");
+  return TDP_OK;
+}
+
 int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe, int64_t lo,
                         int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
                         int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream) {
@@ -1903,7 +1952,7 @@ int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_pr
   TDP_REQUIRE(!need_rows || out_build_idx != nullptr, "null build row output");
   if (n_build == 0 || n_probe == 0) return TDP_OK;
   cudaStream_t st = as_stream(stream);
-  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe);
+  DenseWs w = carve_dense(ws, key_range, lo, n_build, n_probe, need_rows != 0);
   const i64 tiles = ceil_div(n_probe, kJoinTile);
   HashTable none;  // the expansion only reads flags[1] (runs mode): the zero flag
   std::memset(&none, 0, sizeof(none));

@@ -104,6 +104,7 @@ struct DevPred {
   int pad;
   i64 li;
   double lf;
+  const unsigned* bits;  // TDP_CMP_BITMAP: the semi-join bitmap
 };
 
 struct PredSet {
@@ -197,6 +198,11 @@ __device__ __forceinline__ bool eval_pred(const DevPred& p, i64 i) {
       return compare<double>((double)load_as_i64(p.ptr, p.dtype, i) / (double)p.li, p.lf, p.op);
     case TDP_CMP_NONE:
       return false;
+    case TDP_CMP_BITMAP: {
+      const unsigned long long x = (unsigned long long)load_as_i64(p.ptr, p.dtype, i) -
+                                   (unsigned long long)p.li;
+      return x < (unsigned long long)(i64)p.lf && ((__ldg(p.bits + (x >> 5)) >> (x & 31)) & 1u);
+    }
     default:
       return true;
   }

@@ -42,18 +42,21 @@ class _Log:
     """Python-side reads (``values``) and the library's own decisions
     (``c_values``: the radix sort's digit passes, logged in C)."""
 
-    __slots__ = ("mode", "values", "pos", "c_values", "c_pos")
+    __slots__ = ("mode", "values", "pos", "c_values", "c_pos", "decisions", "d_pos")
 
     def __init__(self, mode: str, values: Optional[list] = None,
-                 c_values: Optional[list] = None):
+                 c_values: Optional[list] = None, decisions: Optional[list] = None):
         self.mode = mode
         self.values = [] if values is None else values
         self.pos = 0
         self.c_values = [] if c_values is None else c_values
         self.c_pos = 0
+        self.decisions = [] if decisions is None else decisions
+        self.d_pos = 0
 
     def consumed(self) -> bool:
-        return self.pos == len(self.values) and self.c_pos == len(self.c_values)
+        return (self.pos == len(self.values) and self.c_pos == len(self.c_values)
+                and self.d_pos == len(self.decisions))
 
 
 def active() -> bool:
@@ -97,7 +100,7 @@ def recording() -> _Scope:
 
 def replaying(log: "_Log") -> _Scope:
     """A fresh replay cursor over a recorded log."""
-    return _Scope(_Log("replay", log.values, log.c_values))
+    return _Scope(_Log("replay", log.values, log.c_values, log.decisions))
 
 
 SYNC_READS = [0]  # synchronising reads of device integers in this process (diagnostics)
@@ -134,6 +137,27 @@ def read_ints(t: torch.Tensor) -> list[int]:
     expected = (c_int64 * MAX_VALUES)(*vals)
     nat.call("tdp_expect_values", nat.ptr(flat), esize, len(vals), expected, nat.stream())
     return list(vals)
+
+
+def decision(fn):
+    """A planning decision taken from host-side state (a cached column
+    statistic): ``fn()`` normally and while recording (logged); inside a
+    capture, the recorded decision -- so the captured plan takes the same
+    path as the run it was recorded from even if that state is not available
+    to it (statistics of a tensor created in the capture).  Device data the
+    decision rests on is still checked by the kernels' own logged reads."""
+    log = getattr(_TLS, "log", None)
+    if log is None:
+        return fn()
+    if log.mode == "record":
+        v = fn()
+        log.decisions.append(v)
+        return v
+    if log.d_pos >= len(log.decisions):
+        raise ReplayMismatch("more planning decisions than recorded")
+    v = log.decisions[log.d_pos]
+    log.d_pos += 1
+    return v
 
 
 def read_int(t: torch.Tensor) -> int:

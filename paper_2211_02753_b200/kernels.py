@@ -32,6 +32,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import hostread
 from .hostread import read_int, read_ints
 from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, linear_keys,
                        soft_groupby_grid, soft_linear_count, soft_linear_supported)
@@ -1120,10 +1121,15 @@ DENSE_JOIN_BITS_PER_ROW = 64
 def column_range(t: torch.Tensor, compute: bool = True) -> Optional[tuple[int, int]]:
     """[min, max] of an int64 column: a column statistic cached on the tensor
     (valid while its in-place version is unchanged), like a zone map.
-    Computed on first use with tdp_scan_minmax (one host read; not part of a
-    plan's replay log: a cached catalog statistic is the same on every run),
-    never during a CUDA-graph capture.  Gathered join outputs inherit their
-    base column's range (a superset of theirs)."""
+    Computed on first use with tdp_scan_minmax (one host read).  Inside a
+    CUDA-graph capture the recorded run's answer is used (hostread.decision):
+    the plan takes the same path; the dense join kernels still flag any key
+    outside the range (a logged, device-checked read).  Gathered join outputs
+    inherit their base column's range (a superset of theirs)."""
+    return hostread.decision(lambda: _column_range(t, compute))
+
+
+def _column_range(t: torch.Tensor, compute: bool) -> Optional[tuple[int, int]]:
     meta = getattr(t, "_tdp_range", None)
     if meta is not None and meta[0] == t._version:
         return meta[1], meta[2]
@@ -1143,7 +1149,9 @@ def column_range(t: torch.Tensor, compute: bool = True) -> Optional[tuple[int, i
 
 
 def _inherit_range(out: torch.Tensor, base: torch.Tensor, compute: bool = False) -> None:
-    r = column_range(base, compute=compute) if base.dtype == torch.int64 else None
+    if base.dtype != torch.int64 or base.dim() != 1:
+        return
+    r = column_range(base, compute=compute)
     if r is not None:
         out._tdp_range = (out._version, r[0], r[1])
 
@@ -1309,6 +1317,10 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
     if is_sharded(group):
         out = _equi_join_sharded(left, right, left_key, right_key, group)
         return [out[i] for i in lo] + [out[len(left) + i] for i in ro]
+    if not ro:  # nothing from the right side: a semi-join, kept lazy when it can be
+        semi = _semi_join_lazy(left, right, left_key, right_key, lo)
+        if semi is not None:
+            return semi
     lb, lsel = _side_sources(left)
     rb, rsel = _side_sources(right)
     # a filtered side whose key is a base column joins straight from the base
@@ -1338,6 +1350,69 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
     return (_gather_side([left[i] for i in lo], [lb[i] for i in lo], lmap, pi, stats=lsel is not None)
             + _gather_side([right[i] for i in ro], [rb[i] for i in ro], rmap, bi,
                            stats=rsel is not None))
+
+
+def _semi_join_lazy(left, right, left_key: int, right_key: int, lo: list):
+    """``left`` joined with ``right`` when no right column is returned and the
+    right keys are unique: exactly the left rows whose key is among the right
+    keys, in left row order.  It stays lazy -- the left selection refined by a
+    membership predicate on a bitmap of the right keys (TDP_CMP_BITMAP, one
+    bit per value of the right key's range) -- so no pairs are formed and a
+    later consumer (another join's build, a fused aggregate) evaluates it in
+    its own pass.  None (the caller runs the pair join) when the left side is
+    not one row space of base columns, the right key has no usable range
+    statistic, or a right key repeats (one host read of the build flags)."""
+    space = _row_space(left)
+    if space is None:
+        return None
+    lsel, n_left = space
+    kv = left[left_key].values
+    if kv._t is not None:
+        lbase = kv._t
+    elif isinstance(kv._lazy, LazyValue) and kv._lazy.expr.op == "col":
+        lbase = kv._lazy.expr.col
+    else:
+        return None
+    rb, rsel = _side_sources(right)
+    if rsel is None and not _is_catalog_column(right):
+        return None
+    bk = rb[right_key]
+    if bk.dim() != 1 or bk.dtype != torch.int64 or lbase.dtype != torch.int64:
+        return None
+    n_build = int(bk.numel())
+    dense = _dense_range(column_range(bk), n_build)
+    if dense is None or n_build == 0:
+        return None
+    nat.require_cuda(bk, lbase)
+    lo_key, span = dense
+    dev = bk.device
+    bits = torch.empty((span + 31) // 32, dtype=torch.int32, device=dev)
+    flags = torch.empty(2, dtype=torch.int32, device=dev)
+    if rsel is not None and rsel.preds:
+        if rsel.n != n_build:
+            raise KernelError("build selection and key column disagree on row count")
+        prog = Program()
+        preds, npreds = prog.predicates(rsel)
+        nat.require_cuda(*prog.cols)
+        bc, nbc = prog.native_columns(), len(prog.cols)
+    else:
+        bc, nbc, preds, npreds = nat.columns([]), 0, nat.struct_array(nat.Predicate, []), 0
+    nat.call("tdp_join_dense_bitmap", nat.ptr(bk.contiguous()), n_build, bc, nbc, preds, npreds,
+             lo_key, span, nat.ptr(bits), nat.ptr(flags), nat.stream())
+    if any(read_ints(flags)):  # a repeated (or out-of-statistic) right key
+        return None
+    member = Pred(lbase, "=", nat.CMP_BITMAP, lo_key, float(span), aux=bits)
+    device = _device_of([as_expr(c.values)[0] for c in left], lsel)
+    new_sel = lsel.refine([member]) if lsel is not None else Selection(n_left, [member], device)
+    out = []
+    for i in lo:
+        c = left[i]
+        v = c.values
+        expr = Expr.column(v._t) if v._t is not None else v._lazy.expr
+        with trusted():
+            out.append(EncodedTensor(Tensor(LazyValue(expr, new_sel, valid_for=c.encoding)),
+                                     c.encoding))
+    return out
 
 
 def _repartition(cols: Sequence[EncodedTensor], key_index: int, group) -> list[EncodedTensor]:

@@ -74,23 +74,28 @@ def resolve_predicate(col_dtype: str, op: str, literal) -> tuple[int, int, float
 
 
 class Pred:
-    """One resolved comparison on a base column."""
+    """One resolved comparison on a base column.  ``aux`` is the operand
+    tensor of a semi-join membership test (CMP_BITMAP: the bitmap of the
+    right side's keys, lit_i = lowest key, lit_f = key range)."""
 
-    __slots__ = ("col", "op", "cmp", "lit_i", "lit_f")
+    __slots__ = ("col", "op", "cmp", "lit_i", "lit_f", "aux")
 
-    def __init__(self, col: Optional[torch.Tensor], op: str, cmp: int, lit_i: int, lit_f: float):
+    def __init__(self, col: Optional[torch.Tensor], op: str, cmp: int, lit_i: int, lit_f: float,
+                 aux: Optional[torch.Tensor] = None):
         self.col = col
         self.op = op
         self.cmp = cmp
         self.lit_i = lit_i
         self.lit_f = lit_f
+        self.aux = aux
 
 
 def native_predicates(preds: Sequence[Pred], col_index: dict[int, int]):
     arr = (nat.Predicate * max(1, len(preds)))()
     for k, p in enumerate(preds):
         c = col_index[id(p.col)] if p.col is not None else 0
-        arr[k] = nat.Predicate(c, nat.CMP_OPS[p.op], p.cmp, 0, p.lit_i, p.lit_f)
+        aux = col_index[id(p.aux)] if p.aux is not None else 0
+        arr[k] = nat.Predicate(c, nat.CMP_OPS[p.op], p.cmp, aux, p.lit_i, p.lit_f)
     return arr
 
 
@@ -111,11 +116,13 @@ class Selection:
         return Selection(self.n, self.preds + tuple(preds), self.device)
 
     def base_columns(self) -> list[torch.Tensor]:
+        """Predicate operands: the base columns and any semi-join bitmaps."""
         cols, seen = [], set()
         for p in self.preds:
-            if p.col is not None and id(p.col) not in seen:
-                seen.add(id(p.col))
-                cols.append(p.col)
+            for t in (p.col, p.aux):
+                if t is not None and id(t) not in seen:
+                    seen.add(id(t))
+                    cols.append(t)
         return cols
 
     def _run(self) -> None:
@@ -419,6 +426,8 @@ class Program:
         for p in preds:
             if p.col is not None:
                 self.col_index(p.col)
+            if p.aux is not None:
+                self.col_index(p.aux)
         return native_predicates(preds, self._col_index), len(preds)
 
     def native_columns(self):

@@ -1321,15 +1321,13 @@ __device__ __forceinline__ V group_sum(V v, unsigned peers, int lane) {
   return total;
 }
 
-// A new key: claim the next cell, zero it, then publish its index (release).
-__device__ __forceinline__ i64 claim_cell(const HashAgg& h, u64 img, unsigned* pub) {
-  const i64 id = (i64)atomicAdd(h.misc, 1ull);
+// A new key's cell: zero it, then publish its index (release).
+__device__ __forceinline__ void init_cell(const HashAgg& h, i64 id, u64 img, unsigned* pub) {
   u64* c = h.cells + id * h.cw;
   c[kCellImg] = img;
   for (int w = 1; w < h.cw; ++w) c[w] = 0ull;
   __threadfence();
   atomicExch(pub, (unsigned)(id + 1));
-  return id;
 }
 
 // A key another warp inserted: wait for its cell index (the claimer is
@@ -1354,30 +1352,43 @@ __global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, V
     const i64 k = keys[i];
     const unsigned peers = __match_any_sync(active, k);
     const int leader = __ffs(peers) - 1;
-    // the leader finds (or inserts) the key's cell
-    i64 cell = 0;
+    const u64 img = (u64)k ^ 0x8000000000000000ull;
+    // the leader finds or inserts the key's slot ...
+    unsigned* pub = nullptr;
+    bool inserted = false;
     if (lane == leader) {
-      const u64 img = (u64)k ^ 0x8000000000000000ull;
       if (img == 0ull) {
-        cell = atomicCAS(h.misc + 1, 0ull, 1ull) == 0ull ? claim_cell(h, 0ull, h.cidx + h.cap)
-                                                          : wait_cell(h.cidx + h.cap);
+        pub = h.cidx + h.cap;
+        inserted = atomicCAS(h.misc + 1, 0ull, 1ull) == 0ull;
       } else {
         u64 s = join_hash(k) & h.mask;
         for (;;) {
           const unsigned long long prev =
               atomicCAS(reinterpret_cast<unsigned long long*>(h.slot + s), 0ull,
                         (unsigned long long)img);
-          if (prev == 0ull) {
-            cell = claim_cell(h, img, h.cidx + s);
-            break;
-          }
-          if (prev == img) {
-            cell = wait_cell(h.cidx + s);
+          if (prev == 0ull || prev == img) {
+            inserted = prev == 0ull;
             break;
           }
           s = (s + 1) & h.mask;
         }
+        pub = h.cidx + s;
       }
+    }
+    // ... the warp's new keys take consecutive cells with one counter atomic
+    const unsigned claims = __ballot_sync(active, inserted);
+    unsigned long long first = 0;
+    if (claims) {
+      const int src = __ffs(claims) - 1;
+      if (lane == src) first = atomicAdd(h.misc, (unsigned long long)__popc(claims));
+      first = __shfl_sync(active, first, src);
+    }
+    i64 cell = 0;
+    if (inserted) {
+      cell = (i64)first + __popc(claims & lanemask_lt());
+      init_cell(h, cell, img, pub);
+    } else if (lane == leader) {
+      cell = wait_cell(pub);
     }
     cell = __shfl_sync(peers, cell, leader);
     unsigned long long* c = reinterpret_cast<unsigned long long*>(h.cells + cell * h.cw);
@@ -1701,20 +1712,38 @@ __device__ __forceinline__ i64 dense_rank(const DenseJoin& dj, u64 d) {
   return dj.boffs[d >> 10] + dj.wpre[w] + __popc(dj.bits[w] & ((1u << (d & 31)) - 1u));
 }
 
+// Build pass, tiled like the probe (kJoinPer rows per thread, their
+// predicate loads batched): a filtered build reads its predicate columns
+// once per row with R independent loads in flight.
+constexpr int kBuildThreads = 512, kBuildPer = kJoinTile / kBuildThreads;
+
 template <bool kFiltered>
-__global__ void dense_build_kernel(const i64* __restrict__ keys, i64 nb, DenseJoin dj,
-                                   PredSet bps) {
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
-       i += (i64)gridDim.x * blockDim.x) {
-    if (kFiltered && !eval_all(bps, i)) continue;
-    const u64 x = (u64)__ldg(keys + i) - dj.lo;
+__global__ void __launch_bounds__(kBuildThreads, 2)
+    dense_build_kernel(const i64* __restrict__ keys, i64 nb, DenseJoin dj, PredSet bps) {
+  const i64 tile = blockIdx.x;
+  bool act[kBuildPer];
+  i64 row[kBuildPer], key[kBuildPer];
+#pragma unroll
+  for (int k = 0; k < kBuildPer; ++k) {
+    row[k] = tile * kJoinTile + (i64)k * kBuildThreads + threadIdx.x;
+    act[k] = row[k] < nb;
+  }
+  // keys with the predicate columns: one round of independent loads (a
+  // selective build filter still touches most key sectors)
+#pragma unroll
+  for (int k = 0; k < kBuildPer; ++k) key[k] = act[k] ? __ldg(keys + row[k]) : 0;
+  if (kFiltered) eval_batch_upfront<kBuildPer>(bps, row, act);
+#pragma unroll
+  for (int k = 0; k < kBuildPer; ++k) {
+    if (!act[k]) continue;
+    const u64 x = (u64)key[k] - dj.lo;
     if (x >= (u64)dj.range) {
       dj.flags[1] = 1;
       continue;
     }
     const unsigned bit = 1u << (x & 31);
     if (atomicOr(dj.bits + (x >> 5), bit) & bit) dj.flags[0] = 1;
-    if (dj.row_of != nullptr) dj.row_of[x] = (int)i;
+    if (dj.row_of != nullptr) dj.row_of[x] = (int)row[k];
   }
 }
 
@@ -1884,12 +1913,11 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   TDP_CUDA_TRY(cudaMemsetAsync(w.dj.flags, 0, 16, st));
   TDP_CUDA_TRY(cudaMemsetAsync(w.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
   const bool bfilt = bps.npreds > 0, pfilt = pps.npreds > 0;
+  const unsigned btiles = (unsigned)ceil_div(n_build, kJoinTile);
   if (bfilt)
-    dense_build_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
-                                                                                w.dj, bps);
+    dense_build_kernel<true><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, w.dj, bps);
   else
-    dense_build_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
-                                                                                 w.dj, bps);
+    dense_build_kernel<false><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, w.dj, bps);
   TDP_LAUNCH_CHECK("dense_build_kernel");
   if (need_rows && w.dj.row_of == nullptr) {
     rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(w.dj.bits, words, blocks,
@@ -1935,12 +1963,11 @@ int tdp_join_dense_bitmap(const int64_t* build_keys, int64_t n_build, const tdp_
   dj.flags = out_flags;
   dj.lo = (u64)lo;
   dj.range = key_range;
+  const unsigned btiles = (unsigned)ceil_div(n_build, kJoinTile);
   if (bps.npreds > 0)
-    dense_build_kernel<true><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
-                                                                                dj, bps);
+    dense_build_kernel<true><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, dj, bps);
   else
-    dense_build_kernel<false><<<stream_grid(n_build, 256 * 4, 8), 256, 0, st>>>(build_keys, n_build,
-                                                                                 dj, bps);
+    dense_build_kernel<false><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, dj, bps);
   TDP_LAUNCH_CHECK("dense_build_kernel");
   return TDP_OK;
 }

@@ -61,7 +61,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs of the current device (cached per device ordinal).
 int sm_count();
 
-inline int dtype_size(int dt) {
+__host__ __device__ inline int dtype_size(int dt) {
   switch (dt) {
     case TDP_I64:
     case TDP_F64:
@@ -261,6 +261,16 @@ __device__ __forceinline__ void cmp_rows(const T (&v)[R], T lit, int op, bool (&
 // chain of switches).  row[r] must be a valid row wherever keep[r] is true.
 template <int R>
 __device__ __forceinline__ void eval_batch(const PredSet& ps, const i64 (&row)[R], bool (&keep)[R]) {
+  // the later predicates' loads depend on the earlier ones' outcome: start
+  // their lines towards L2 now, so each later round waits on L2, not DRAM
+  for (int k = 1; k < ps.npreds; ++k) {
+    const int es = dtype_size(ps.p[k].dtype);
+    const char* base = reinterpret_cast<const char*>(ps.p[k].ptr);
+    if (base == nullptr || es == 0) continue;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (keep[r]) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + row[r] * es));
+  }
   for (int k = 0; k < ps.npreds; ++k) {
     const int cmp = ps.p[k].cmp, dt = ps.p[k].dtype, op = ps.p[k].op;
     const void* ptr = ps.p[k].ptr;
@@ -281,9 +291,77 @@ __device__ __forceinline__ void eval_batch(const PredSet& ps, const i64 (&row)[R
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = keep[r] ? __ldg(c + row[r]) : 0.0;
       cmp_rows<R, double>(v, ps.p[k].lf, op, keep);
+    } else if (cmp == TDP_CMP_BITMAP && dt == TDP_I64) {
+      // semi-join membership: R key loads, then R bitmap-word loads in flight
+      const i64* c = reinterpret_cast<const i64*>(ptr);
+      unsigned long long x[R];
+      unsigned w[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[r] = keep[r] ? (unsigned long long)__ldg(c + row[r]) - (unsigned long long)ps.p[k].li : 0ull;
+        keep[r] = keep[r] && x[r] < (unsigned long long)(i64)ps.p[k].lf;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = keep[r] ? __ldg(ps.p[k].bits + (x[r] >> 5)) : 0u;
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && ((w[r] >> (x[r] & 31)) & 1u);
     } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) keep[r] = keep[r] && eval_pred(ps.p[k], row[r]);
+    }
+  }
+}
+
+// eval_batch with every predicate's column loaded for all R rows up front
+// (one round of independent loads instead of one per predicate; a bitmap
+// membership test adds one dependent round for its words) when the set is
+// at most kUpfront predicates on 8-byte columns; else eval_batch.
+constexpr int kUpfront = 3;
+
+template <int R>
+__device__ __forceinline__ void eval_batch_upfront(const PredSet& ps, const i64 (&row)[R],
+                                                   bool (&keep)[R]) {
+  bool simple = ps.npreds <= kUpfront;
+  for (int k = 0; k < ps.npreds && simple; ++k) {
+    const int cmp = ps.p[k].cmp, dt = ps.p[k].dtype;
+    simple = (cmp == TDP_CMP_I64 && dt == TDP_I64) || (cmp == TDP_CMP_F64 && dt == TDP_F64) ||
+             (cmp == TDP_CMP_BITMAP && dt == TDP_I64);
+  }
+  if (!simple) {
+    eval_batch<R>(ps, row, keep);
+    return;
+  }
+  i64 v[kUpfront][R];
+#pragma unroll
+  for (int k = 0; k < kUpfront; ++k)
+    if (k < ps.npreds) {
+      const i64* c = reinterpret_cast<const i64*>(ps.p[k].ptr);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[k][r] = keep[r] ? __ldg(c + row[r]) : 0;
+    }
+#pragma unroll
+  for (int k = 0; k < kUpfront; ++k) {
+    if (k >= ps.npreds) break;
+    const DevPred& p = ps.p[k];
+    if (p.cmp == TDP_CMP_I64) {
+      cmp_rows<R, i64>(v[k], p.li, p.op, keep);
+    } else if (p.cmp == TDP_CMP_F64) {
+      double f[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) f[r] = __longlong_as_double(v[k][r]);
+      cmp_rows<R, double>(f, p.lf, p.op, keep);
+    } else {  // bitmap membership
+      unsigned w[R];
+      unsigned long long x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[r] = (unsigned long long)v[k][r] - (unsigned long long)p.li;
+        keep[r] = keep[r] && x[r] < (unsigned long long)(i64)p.lf;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = keep[r] ? __ldg(p.bits + (x[r] >> 5)) : 0u;
+#pragma unroll
+      for (int r = 0; r < R; ++r) keep[r] = keep[r] && ((w[r] >> (x[r] & 31)) & 1u);
     }
   }
 }

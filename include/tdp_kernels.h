@@ -405,6 +405,22 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Bitmap group-by over one int64 key whose values lie in [lo, lo+key_range)
+ * (the scan's min/max), the range at most ~1024 values per row: the rank of
+ * a key among the set bits of a key_range-bit map is its group id in
+ * ascending key order, so rows accumulate straight into dense cells (float
+ * SUMs in fixed point: bitwise repeatable).  prepare: out_ngroups (device) =
+ * distinct keys m; emit (m from the host): out_keys[m] ascending,
+ * out_counts[m], out_sums[naggs][m] as tdp_groupby_hash_emit.  Same contract
+ * as the hash group-by (groupby_exact, tq/kernels.py:108-167).             */
+size_t tdp_groupby_bitmap_workspace(int64_t n, int64_t key_range, int32_t naggs);
+int tdp_groupby_bitmap_prepare(const int64_t* keys, int64_t n, int64_t lo, int64_t key_range,
+                               const tdp_column* vals, const int32_t* agg_kinds, int32_t naggs,
+                               int64_t* out_ngroups, void* ws, size_t ws_bytes, void* stream);
+int tdp_groupby_bitmap_emit(int64_t n, int64_t lo, int64_t key_range, const int32_t* agg_kinds,
+                            int32_t naggs, int64_t m, int64_t* out_keys, int64_t* out_counts,
+                            void* out_sums, void* ws, size_t ws_bytes, void* stream);
+
 /* Dense-range equi-join: the same contract as tdp_join_prepare_ex (mode 0) /
  * tdp_join_emit when every build key lies in [lo, lo + key_range) (a column
  * statistic) and the keys are unique: a bitmap of key_range bits replaces the

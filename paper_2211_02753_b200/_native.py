@@ -151,6 +151,13 @@ _SIGNATURES = {
                                     c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_join_emit": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_size_t,
                               c_void_p]),
+    "tdp_groupby_bitmap_workspace": (c_size_t, [c_int64, c_int64, c_int32]),
+    "tdp_groupby_bitmap_prepare": (c_int, [c_void_p, c_int64, c_int64, c_int64, POINTER(Column),
+                                           POINTER(c_int32), c_int32, c_void_p, c_void_p,
+                                           c_size_t, c_void_p]),
+    "tdp_groupby_bitmap_emit": (c_int, [c_int64, c_int64, c_int64, POINTER(c_int32), c_int32,
+                                        c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_size_t, c_void_p]),
     "tdp_join_dense_workspace": (c_size_t, [c_int64, c_int64, c_int64]),
     "tdp_join_dense_prepare": (c_int, [c_void_p, c_int64, POINTER(Column), c_int32,
                                        POINTER(Predicate), c_int32, c_void_p, c_int64,

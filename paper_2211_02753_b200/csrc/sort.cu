@@ -1996,3 +1996,200 @@ int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_pr
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Bitmap group-by: one int64 key whose range R (from the scan's min/max) is at
+// most ~1024 values per row.  The distinct keys are the set bits of an R-bit
+// map, their rank among the set bits is the group id in ascending key order
+// (np.unique's order, tq/kernels.py:128-136), so rows accumulate straight
+// into dense cells [0, m) -- no hash table, no CAS chains, no sort of the
+// distinct keys.  Passes: set bits (rows) -> popcount prefix (R/32 words) ->
+// accumulate (rows) -> emit (m groups).
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+struct BitmapAgg {
+  unsigned* bits;
+  unsigned short* wpre;
+  i64* bcount;
+  i64* boffs;
+  unsigned long long* m;  // [1] group count (device)
+  u64* cells;             // [n][cw]  image, count, sums, fixed words
+  void* scan_ws;
+  size_t scan_bytes;
+  u64 lo;
+  i64 range;
+  int cw;
+};
+
+size_t bitmap_agg_ws_bytes(i64 n, i64 range, int naggs) {
+  const i64 r = range > 0 ? range : 1;
+  const i64 words = rank_words(r), blocks = rank_blocks(r);
+  const int na = naggs > 0 ? naggs : 0;
+  return align256((size_t)words * 4) + align256((size_t)words * 2) + 2 * align256((size_t)blocks * 8) +
+         256 + align256((size_t)(n > 0 ? n : 1) * cell_words(na, na) * 8) +
+         exclusive_scan_workspace(blocks) + 2048;
+}
+
+BitmapAgg carve_bitmap_agg(void* ws, i64 n, i64 range, i64 lo, const ValSet& vs) {
+  BitmapAgg b;
+  const i64 r = range > 0 ? range : 1;
+  const i64 words = rank_words(r), blocks = rank_blocks(r);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  b.bits = (unsigned*)p;
+  p += align256((size_t)words * 4);
+  b.wpre = (unsigned short*)p;
+  p += align256((size_t)words * 2);
+  b.bcount = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  b.boffs = (i64*)p;
+  p += align256((size_t)blocks * 8);
+  b.m = (unsigned long long*)p;
+  p += 256;
+  b.cw = cell_words(vs.naggs, vs.nfixed);
+  b.cells = (u64*)p;
+  p += align256((size_t)(n > 0 ? n : 1) * cell_words(vs.naggs, vs.naggs) * 8);
+  b.scan_ws = p;
+  b.scan_bytes = exclusive_scan_workspace(blocks) + 1024;
+  b.lo = (u64)lo;
+  b.range = r;
+  return b;
+}
+
+__global__ void bm_set_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg b) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const u64 d = (u64)__ldg(keys + i) - b.lo;
+    atomicOr(b.bits + (d >> 5), 1u << (d & 31));
+  }
+}
+
+// zero the m cells (m from the scan, on the device)
+__global__ void bm_clear_kernel(BitmapAgg b) {
+  const i64 words = (i64)*b.m * b.cw;
+  for (i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x; t < words;
+       t += (i64)gridDim.x * blockDim.x)
+    b.cells[t] = 0ull;
+}
+
+__global__ void bm_accum_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg b, ValSet vs) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 base = (i64)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const i64 i = base + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
+    const i64 k = __ldg(keys + i);
+    const unsigned peers = __match_any_sync(active, k);  // equal keys of the warp combine
+    const int leader = __ffs(peers) - 1;
+    const u64 d = (u64)k - b.lo;
+    const i64 w = (i64)(d >> 5);
+    const i64 g = b.boffs[d >> 10] + b.wpre[w] + __popc(b.bits[w] & ((1u << (d & 31)) - 1u));
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(b.cells + g * b.cw);
+    if (lane == leader) {
+      c[kCellImg] = (unsigned long long)k ^ 0x8000000000000000ull;  // same value from every writer
+      atomicAdd(c + kCellCnt, (unsigned long long)__popc(peers));
+    }
+    for (int a = 0; a < vs.naggs; ++a) {
+      if (vs.kind[a] == TDP_AGG_COUNT) continue;
+      if (vs.kind[a] == TDP_AGG_SUM_F64) {
+        const double v = group_sum(load_as_f64(vs.p[a], vs.dt[a], i), peers, lane);
+        if (lane == leader) fixed_add(c + kCellAcc + vs.naggs + kFixedWords * vs.fidx[a], v);
+      } else {
+        const unsigned long long v =
+            group_sum((unsigned long long)load_as_i64(vs.p[a], vs.dt[a], i), peers, lane);
+        if (lane == leader) atomicAdd(c + kCellAcc + a, v);
+      }
+    }
+  }
+}
+
+__global__ void bm_emit_kernel(BitmapAgg b, i64 m, ValSet vs, i64* __restrict__ out_keys,
+                               i64* __restrict__ out_counts, u64* __restrict__ out_sums) {
+  for (i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x; g < m;
+       g += (i64)gridDim.x * blockDim.x) {
+    const unsigned long long* c = reinterpret_cast<const unsigned long long*>(b.cells + g * b.cw);
+    out_keys[g] = (i64)(c[kCellImg] ^ 0x8000000000000000ull);
+    const u64 cnt = c[kCellCnt];
+    out_counts[g] = (i64)cnt;
+    for (int a = 0; a < vs.naggs; ++a) {
+      u64 v;
+      if (vs.kind[a] == TDP_AGG_COUNT)
+        v = cnt;
+      else if (vs.kind[a] == TDP_AGG_SUM_F64)
+        v = (u64)__double_as_longlong(fixed_value(c + kCellAcc + vs.naggs + kFixedWords * vs.fidx[a]));
+      else
+        v = c[kCellAcc + a];
+      out_sums[(i64)a * m + g] = v;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_groupby_bitmap_workspace(int64_t n, int64_t key_range, int32_t naggs) {
+  return bitmap_agg_ws_bytes(n, key_range, naggs);
+}
+
+int tdp_groupby_bitmap_prepare(const int64_t* keys, int64_t n, int64_t lo, int64_t key_range,
+                               const tdp_column* vals, const int32_t* agg_kinds, int32_t naggs,
+                               int64_t* out_ngroups, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n >= 0 && out_ngroups != nullptr, "bad bitmap group-by arguments");
+  TDP_REQUIRE(key_range >= 1 && key_range <= ((int64_t)1 << 34),
+              "bitmap group-by key range %lld outside [1, 2^34]", (long long)key_range);
+  TDP_REQUIRE(ws_bytes >= bitmap_agg_ws_bytes(n, key_range, naggs),
+              "bitmap group-by workspace too small");
+  ValSet vs;
+  int rc = make_valset(vals, agg_kinds, naggs, n, &vs);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_ngroups, 0, 8, st));
+    return TDP_OK;
+  }
+  BitmapAgg b = carve_bitmap_agg(ws, n, key_range, lo, vs);
+  const i64 words = rank_words(key_range), blocks = rank_blocks(key_range);
+  TDP_CUDA_TRY(cudaMemsetAsync(b.bits, 0, (size_t)words * 4, st));
+  bm_set_kernel<<<stream_grid(n, 256 * 4, 16), 256, 0, st>>>(keys, n, b);
+  TDP_LAUNCH_CHECK("bm_set_kernel");
+  rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(b.bits, words, blocks, b.bcount,
+                                                               b.wpre);
+  TDP_LAUNCH_CHECK("rank_popc_kernel");
+  rc = exclusive_scan_i64(b.bcount, b.boffs, blocks, reinterpret_cast<i64*>(b.m), b.scan_ws,
+                          b.scan_bytes, st);
+  if (rc) return rc;
+  bm_clear_kernel<<<stream_grid(n * b.cw, 256 * 4, 8), 256, 0, st>>>(b);
+  TDP_LAUNCH_CHECK("bm_clear_kernel");
+  bm_accum_kernel<<<stream_grid(n, 256, 32), 256, 0, st>>>(keys, n, b, vs);
+  TDP_LAUNCH_CHECK("bm_accum_kernel");
+  TDP_CUDA_TRY(cudaMemcpyAsync(out_ngroups, b.m, 8, cudaMemcpyDeviceToDevice, st));
+  return TDP_OK;
+}
+
+int tdp_groupby_bitmap_emit(int64_t n, int64_t lo, int64_t key_range, const int32_t* agg_kinds,
+                            int32_t naggs, int64_t m, int64_t* out_keys, int64_t* out_counts,
+                            void* out_sums, void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(m >= 0 && m <= (n > 0 ? n : 0), "bad group count");
+  TDP_REQUIRE(ws_bytes >= bitmap_agg_ws_bytes(n, key_range, naggs),
+              "bitmap group-by workspace too small");
+  if (m == 0) return TDP_OK;
+  ValSet vs;
+  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  if (rc) return rc;
+  vs.naggs = naggs;
+  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
+  number_fixed(&vs);
+  BitmapAgg b = carve_bitmap_agg(ws, n, key_range, lo, vs);
+  cudaStream_t st = as_stream(stream);
+  bm_emit_kernel<<<stream_grid(m, 256, 16), 256, 0, st>>>(b, m, vs, out_keys, out_counts,
+                                                           reinterpret_cast<u64*>(out_sums));
+  TDP_LAUNCH_CHECK("bm_emit_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"

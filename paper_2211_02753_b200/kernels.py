@@ -559,7 +559,8 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
         spans.append((lo, span))
         slots *= span
     if slots > DENSE_SLOT_LIMIT:  # high cardinality: sort-based (sharded: all-to-all)
-        return _groupby_general(keys, key_vals, agg_specs, agg_vals)
+        return _groupby_general(keys, key_vals, agg_specs, agg_vals,
+                                key_range=ranges.get(0) if len(keys) == 1 else None)
     agg_exprs = []
     for (func, dt), v in zip(agg_specs, agg_vals):
         kind = _agg_kind(func, dt)
@@ -663,8 +664,9 @@ def _groupby_codes(codes: torch.Tensor, slots: int, agg_specs, agg_vals, n: int,
     return counts, sums
 
 
-def _groupby_general(keys, key_vals, agg_specs, agg_vals):
-    """Sort-based path (the reference's np.unique algorithm on the device)."""
+def _groupby_general(keys, key_vals, agg_specs, agg_vals, key_range=None):
+    """Sort-based path (the reference's np.unique algorithm on the device);
+    hash / bitmap aggregation for one high-cardinality int64 key."""
     kdata = [_materialize(v) for v in key_vals]
     n = int(kdata[0].shape[0])
     vdata = []
@@ -680,7 +682,7 @@ def _groupby_general(keys, key_vals, agg_specs, agg_vals):
     group = current_group()
     if is_sharded(group):
         return _groupby_sharded(kdata, agg_specs, vdata, group)
-    return _groupby_local(kdata, agg_specs, vdata)
+    return _groupby_local(kdata, agg_specs, vdata, key_range)
 
 
 def _lex_order(keys: Sequence[torch.Tensor]) -> torch.Tensor:
@@ -772,11 +774,52 @@ def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
     return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
 
 
-def _groupby_local(kdata, agg_specs, agg_vals):
+def _agg_columns(agg_specs, agg_vals, n: int):
+    kinds = [_agg_kind(f, dt) for f, dt in agg_specs]
+    vals = []
+    for (func, dt), v, kind in zip(agg_specs, agg_vals, kinds):
+        if kind == nat.AGG_COUNT:
+            vals.append(None)
+            continue
+        t = _materialize(v)
+        if t.dim() != 1 or t.shape[0] != n:
+            raise KernelError(f"{func} aggregate needs a value column of {n} rows")
+        vals.append(t.to(torch.int64) if t.dtype == torch.bool else t.contiguous())
+    cols = (nat.Column * max(1, len(vals)))()
+    for a, t in enumerate(vals):
+        cols[a] = nat.column(t) if t is not None else nat.Column(None, nat.I64, 0, 0, 1)
+    return kinds, vals, cols
+
+
+def _groupby_bitmap(key: torch.Tensor, lo: int, span: int, agg_specs, agg_vals, n: int, device):
+    """One int64 key in [lo, lo + span): bitmap-rank aggregation
+    (tdp_groupby_bitmap_*) -- groups come out in ascending key order without
+    a hash table or a sort; one host read (the group count)."""
+    kinds, vals, cols = _agg_columns(agg_specs, agg_vals, n)
+    kind_arr = (c_int32 * max(1, len(kinds)))(*kinds)
+    key = key.contiguous()
+    ws = nat.workspace(nat.load().tdp_groupby_bitmap_workspace(n, span, len(kinds)), device)
+    info = torch.empty(1, dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_bitmap_prepare", nat.ptr(key), n, lo, span, cols, kind_arr, len(kinds),
+             nat.ptr(info), nat.ptr(ws), ws.numel(), nat.stream())
+    m = read_int(info)
+    keys_out = torch.empty(m, dtype=torch.int64, device=device)
+    counts = torch.empty(m, dtype=torch.int64, device=device)
+    sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_bitmap_emit", n, lo, span, kind_arr, len(kinds), m, nat.ptr(keys_out),
+             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
+    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
+
+
+def _groupby_local(kdata, agg_specs, agg_vals, key_range=None):
     device = kdata[0].device
     n = int(kdata[0].shape[0])
     if n == 0:
         return _empty_groups(len(kdata), agg_specs, device)
+    if len(kdata) == 1 and kdata[0].dtype == torch.int64 and key_range is not None:
+        span = key_range[1] - key_range[0] + 1
+        if 1 <= span <= min(1 << 34, RANK_BITS_PER_GROUP * n + (1 << 21)):
+            return _groupby_bitmap(kdata[0], key_range[0], span, agg_specs, agg_vals, n, device)
     if len(kdata) == 1 and kdata[0].dtype == torch.int64 and n >= HASH_GROUPBY_MIN_ROWS:
         return _groupby_hash(kdata[0], agg_specs, agg_vals, n, device)
     uniqs, codes = zip(*[unique_inverse(k) for k in kdata])

@@ -406,7 +406,7 @@ def test_hash_groupby_matches_oracle(n, distinct):
     np.testing.assert_allclose(aggs[3].cpu().numpy(), ea[3], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("path", ["hash", "codes"])
+@pytest.mark.parametrize("path", ["hash", "codes", "bitmap"])
 def test_float_group_sums_bitwise_repeatable_and_special_values(path):
     """Float SUMs of the atomic group-by paths (hash: one int64 key; codes:
     the general multi-key path) accumulate in 256-bit fixed point: the same
@@ -417,7 +417,10 @@ def test_float_group_sums_bitwise_repeatable_and_special_values(path):
 
     rng = np.random.default_rng(91)
     n = 400_000
-    key = rng.integers(0, 3_000, size=n).astype(np.int64) * 1_000_003  # sparse: no dense slots
+    # sparse keys (no dense slots): a 3e9 range takes the hash table, a 1e7
+    # range the bitmap rank
+    key = rng.integers(0, 3_000, size=n).astype(np.int64) * (3_001 if path == "bitmap"
+                                                            else 1_000_003)
     sign = np.where(rng.random(n) < 0.5, -1.0, 1.0)
     fv = sign * rng.random(n) * 10.0 ** rng.integers(-20, 26, size=n)
     fv[:5] = [np.inf, -np.inf, np.nan, 1e30, -1e300]
@@ -440,3 +443,31 @@ def test_float_group_sums_bitwise_repeatable_and_special_values(path):
     np.testing.assert_array_equal(aggs[1].cpu().numpy(), ea[1])
     np.testing.assert_allclose(runs[0], ea[0], rtol=1e-9, atol=1e-9)  # nan == nan positions too
     assert np.array_equal(np.isnan(runs[0]), np.isnan(ea[0]))
+
+
+@pytest.mark.parametrize("lo", [0, -(2**40), 2**63 - 6_000_000, -(2**63)])
+def test_bitmap_groupby_matches_oracle(lo):
+    """One int64 key whose range is modest next to the rows (Q3's l_orderkey
+    after the joins): bitmap-rank group-by, incl. ranges at the ends of int64
+    and hot keys; SQL through the fused range scan."""
+    rng = np.random.default_rng(abs(lo) % 997 + 5)
+    n = 250_000
+    pool = lo + rng.choice(5_000_000, size=60_000, replace=False).astype(np.int64)
+    key = pool[rng.integers(0, len(pool), size=n)]
+    key[: n // 4] = pool[0]  # a hot key
+    v = rng.normal(size=n) * 100
+    iv = rng.integers(-2**40, 2**40, size=n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["k", "v", "iv"], [tq.plain(tq.Tensor(key)),
+                                                               tq.plain(tq.Tensor(v)),
+                                                               tq.plain(tq.Tensor(iv))]))
+    q = wl.compile_sql("SELECT k, SUM(v), AVG(v), SUM(iv), COUNT(*) FROM t GROUP BY k", cat,
+                       tq.UdfRegistry())
+    res = q.run(cat)
+    keys, aggs = orc.groupby_exact([key], [("sum", v), ("avg", v), ("sum", iv), ("count", None)])
+    got = [c.values.numpy() for c in res.columns]
+    np.testing.assert_array_equal(got[0], keys[0])
+    np.testing.assert_allclose(got[1], aggs[0], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(got[2], aggs[1], rtol=1e-9, atol=1e-9)
+    np.testing.assert_array_equal(got[3], aggs[2])
+    np.testing.assert_array_equal(got[4], aggs[3])

@@ -450,6 +450,24 @@ int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_pr
                         int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
                         int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);
 
+/* One-pass LLP step (tq/kernels.py:190-229 soft_groupby over
+ * pe_encode(Linear(X)), its tape backward tq/tensor.py:474, :364-365,
+ * :515-527): for k = 2 classes and one one-hot bag key, the forward writes
+ * the count grid AND the per-bag statistics stats[b] = (Q_b, S_b[0..d)) with
+ * Q_b = sum P0 P1, S_b = sum P0 P1 x over the bag's rows; the backward forms
+ * dW = sum_b (G[b,0] - G[b,1]) S_b [1, -1], db likewise from Q_b, without
+ * reading X.  Rows are visited in bag order through perm (int32 stable
+ * permutation) and offs (int64 [bags + 1] bag offsets).  float32 X, d = 32
+ * or 64; grid cell of (bag b, class c) = b * bag_stride + c * dense_stride. */
+size_t tdp_llp_onepass_workspace(int32_t bags, int32_t d);
+int tdp_llp_onepass_fwd(const float* X, int64_t n, int32_t d, const float* W, const float* bias,
+                        const int32_t* perm, const int64_t* offs, int32_t bags, int64_t bag_stride,
+                        int64_t dense_stride, double* out_grid, double* out_stats, void* ws,
+                        size_t ws_bytes, void* stream);
+int tdp_llp_onepass_bwd(const double* stats, int32_t bags, int32_t d, const double* grad_grid,
+                        int64_t bag_stride, int64_t dense_stride, float* dW, float* db,
+                        void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* probability encodings and soft (differentiable) group-by                 */
 /* ------------------------------------------------------------------------ */

@@ -158,6 +158,12 @@ _SIGNATURES = {
     "tdp_groupby_bitmap_emit": (c_int, [c_int64, c_int64, c_int64, POINTER(c_int32), c_int32,
                                         c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_size_t, c_void_p]),
+    "tdp_llp_onepass_workspace": (c_size_t, [c_int32, c_int32]),
+    "tdp_llp_onepass_fwd": (c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p,
+                                    c_void_p, c_size_t, c_void_p]),
+    "tdp_llp_onepass_bwd": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_int64, c_int64,
+                                    c_void_p, c_void_p, c_void_p]),
     "tdp_join_dense_workspace": (c_size_t, [c_int64, c_int64, c_int64]),
     "tdp_join_dense_prepare": (c_int, [c_void_p, c_int64, POINTER(Column), c_int32,
                                        POINTER(Predicate), c_int32, c_void_p, c_int64,

@@ -283,6 +283,48 @@ def linear_keys(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor]
     return arr
 
 
+def bag_index(codes: torch.Tensor, bags: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Rows of a one-hot key column in bag order: (int32 stable permutation,
+    int64 offsets [bags + 1]).  Built once per code column with the radix sort
+    and cached on it (valid while its in-place version is unchanged), like an
+    index on the column."""
+    meta = getattr(codes, "_tdp_bag_index", None)
+    if meta is not None and meta[0] == codes._version and meta[1] == bags:
+        return meta[2], meta[3]
+    from .encodings import plain
+    from .kernels import _groupby_codes, stable_order
+    from .tensor import Tensor
+
+    n = int(codes.numel())
+    perm = stable_order(plain(Tensor(codes))).to(torch.int32)
+    counts, _ = _groupby_codes(codes, bags, [], [], n, codes.device)
+    offs = torch.zeros(bags + 1, dtype=torch.int64, device=codes.device)
+    offs[1:] = torch.cumsum(counts, 0)
+    codes._tdp_bag_index = (codes._version, bags, perm, offs)
+    return perm, offs
+
+
+def _onepass_layout(spec: SoftKeySpec, dense_pos: int, x: torch.Tensor, w: torch.Tensor,
+                    codes) -> Optional[tuple[int, int, int]]:
+    """(bags, bag stride, dense stride) when the one-pass LLP step applies:
+    float32 X with 32 or 64 features, two classes, one one-hot key (SURVEY
+    §8(f) 3, llp_onepass.cu); None otherwise (the two-pass kernels)."""
+    import os
+
+    if os.environ.get("TDP_LLP_ONEPASS", "1") == "0":
+        return None
+    if not (x.dtype == torch.float32 and x.shape[1] in (32, 64) and w.shape[1] == 2
+            and len(codes) == 1 and len(spec.kinds) == 2 and x.shape[0] < (1 << 31)
+            and x.data_ptr() % 8 == 0):
+        return None
+    strides, st = [0, 0], 1
+    for j in (1, 0):
+        strides[j] = st
+        st *= spec.kinds[j][1]
+    bag_pos = 1 - dense_pos
+    return spec.kinds[bag_pos][1], strides[bag_pos], strides[dense_pos]
+
+
 class _SoftLinearCount(torch.autograd.Function):
     @staticmethod
     def forward(ctx, spec: SoftKeySpec, dense_pos: int, out_dtype: torch.dtype, x: torch.Tensor,
@@ -293,15 +335,43 @@ class _SoftLinearCount(torch.autograd.Function):
         n, d = x.shape
         k = w.shape[1]
         grid = torch.empty(spec.cells, dtype=torch.float64, device=x.device)
+        ctx.spec, ctx.dense_pos, ctx.has_bias = spec, dense_pos, b is not None
+        onepass = _onepass_layout(spec, dense_pos, x, w, codes)
+        if onepass is not None:
+            # one pass over X: the grid and the per-bag statistics of the
+            # backward (llp_onepass.cu); the backward never reads X
+            bags, bag_stride, dense_stride = onepass
+            perm, offs = bag_index(codes[0].contiguous(), bags)
+            stats = torch.empty((bags, d + 1), dtype=torch.float64, device=x.device)
+            ws = nat.workspace(nat.load().tdp_llp_onepass_workspace(bags, d), x.device)
+            nat.call("tdp_llp_onepass_fwd", nat.ptr(x), n, d, nat.ptr(w), nat.ptr(b), nat.ptr(perm),
+                     nat.ptr(offs), bags, bag_stride, dense_stride, nat.ptr(grid), nat.ptr(stats),
+                     nat.ptr(ws), ws.numel(), nat.stream())
+            ctx.onepass = (bags, bag_stride, dense_stride, d)
+            ctx.save_for_backward(stats, w, *(() if b is None else (b,)))
+            return grid.to(out_dtype)
+        ctx.onepass = None
         keys = linear_keys(spec, dense_pos, codes)
         nat.call("tdp_soft_linear_count_fwd", nat.ptr(x), _dt(x), n, d, k, nat.ptr(w), nat.ptr(b),
                  keys, len(spec.kinds), dense_pos, nat.ptr(grid), nat.stream())
-        ctx.spec, ctx.dense_pos, ctx.has_bias = spec, dense_pos, b is not None
         ctx.save_for_backward(x, w, *(() if b is None else (b,)), *codes)
         return grid.to(out_dtype)
 
     @staticmethod
     def backward(ctx, g: torch.Tensor):
+        if ctx.onepass is not None:
+            saved = ctx.saved_tensors
+            stats, w = saved[0], saved[1]
+            b = saved[2] if ctx.has_bias else None
+            bags, bag_stride, dense_stride, d = ctx.onepass
+            G = g.detach().to(torch.float64).contiguous()
+            dw = torch.empty_like(w)
+            db = torch.empty_like(b) if b is not None else None
+            nat.call("tdp_llp_onepass_bwd", nat.ptr(stats), bags, d, nat.ptr(G), bag_stride,
+                     dense_stride, nat.ptr(dw), nat.ptr(db), nat.stream())
+            return (None, None, None, None, dw if ctx.needs_input_grad[4] else None,
+                    db if ctx.has_bias and ctx.needs_input_grad[5] else None,
+                    *([None] * (len(ctx.needs_input_grad) - 6)))
         saved = ctx.saved_tensors
         x, w = saved[0], saved[1]
         b = saved[2] if ctx.has_bias else None

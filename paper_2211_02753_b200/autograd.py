@@ -315,7 +315,7 @@ def _onepass_layout(spec: SoftKeySpec, dense_pos: int, x: torch.Tensor, w: torch
         return None
     if not (x.dtype == torch.float32 and x.shape[1] in (32, 64) and w.shape[1] == 2
             and len(codes) == 1 and len(spec.kinds) == 2 and x.shape[0] < (1 << 31)
-            and x.data_ptr() % 8 == 0):
+            and x.data_ptr() % 16 == 0):
         return None
     strides, st = [0, 0], 1
     for j in (1, 0):

@@ -181,13 +181,15 @@ def run(args) -> None:
                          "sample": f"{m} rows, oracle llp_forward_backward (closed form of the "
                                    f"reference tape), {reps} reps, extrapolated to {n} rows"},
         "bytes_floor_ms_two_pass": (8 * d + 16) * n / peak / 1e9 * 1e3,
-        "bytes_floor_ms_one_pass": (4 * d + 8) * n / peak / 1e9 * 1e3,
+        "bytes_floor_ms_one_pass": (4 * d + 4) * n / peak / 1e9 * 1e3,
         "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak,
-                     "achieved": (8 * d + 16) * n / (ms / 1e3) / 1e9,
-                     "frac": (8 * d + 16) * n / (ms / 1e3) / 1e9 / peak,
+                     "achieved": (4 * d + 4) * n / (ms / 1e3) / 1e9,
+                     "frac": (4 * d + 4) * n / (ms / 1e3) / 1e9 / peak,
                      "traffic": None,
-                     "what": "algorithmic bytes of the step (X read twice + bag codes twice, "
-                             "2 (4d + 8) B/row = 528 at d=64, SURVEY §8(d)) over the step time"},
+                     "what": "bytes of the one-pass step (X read once in bag order + the int32 bag "
+                             "permutation, 4d + 4 = 260 B/row at d=64; llp_onepass.cu) over the "
+                             "step time",
+                     "survey_two_pass_bytes_frac": (8 * d + 16) * n / (ms / 1e3) / 1e9 / peak},
         "exact_swap": {"ms_per_run": swap_ms, "rows_per_s": n / (swap_ms / 1e3),
                        "hbm_gbs": (4 * d + 8) * n / (swap_ms / 1e3) / 1e9, "groups": swap_groups,
                        "count_mismatch_vs_torch_argmax": swap_mismatch,

@@ -405,6 +405,19 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Device dictionary encoding (tq/encodings.py:127-133 dict_encode): a
+ * 64-bit hash per string of a UTF-8 byte buffer (offsets int64 [n + 1]);
+ * after tdp_unique_inverse of the hashes, tdp_string_groups writes each hash
+ * group's first string (out_first int64 [m]) and sets *out_flag when a
+ * string differs byte-wise from its group's first one (a hash collision: the
+ * caller encodes on the host instead).  Codes = the groups' sorted ranks,
+ * gathered by the inverse.                                                  */
+int tdp_string_hash(const uint8_t* bytes, const int64_t* offsets, int64_t n, int64_t* out_hash,
+                    void* stream);
+int tdp_string_groups(const uint8_t* bytes, const int64_t* offsets, int64_t n,
+                      const int64_t* inverse, int64_t m, int64_t* out_first, int32_t* out_flag,
+                      void* stream);
+
 /* Bitmap group-by over one int64 key whose values lie in [lo, lo+key_range)
  * (the scan's min/max), the range at most ~1024 values per row: the rank of
  * a key among the set bits of a key_range-bit map is its group id in

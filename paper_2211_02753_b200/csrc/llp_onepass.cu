@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kOpThreads, kOpCtasPerSm)
       for (int v = 0; v < V; ++v) sg[v] = 0.f;
 #pragma unroll 8
       for (int j = 0; j < 32; ++j) {
+        if (j >= cnt) break;  // rows past a short last group: stale buffer contents
         const float qj = __shfl_sync(0xffffffffu, q, j);
         float xj[V];
         if constexpr (V == 2) {

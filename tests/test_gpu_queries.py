@@ -471,3 +471,26 @@ def test_bitmap_groupby_matches_oracle(lo):
     np.testing.assert_allclose(got[2], aggs[1], rtol=1e-9, atol=1e-9)
     np.testing.assert_array_equal(got[3], aggs[2])
     np.testing.assert_array_equal(got[4], aggs[3])
+
+
+@pytest.mark.parametrize("n,distinct", [(5000, 7), (200_003, 40_000)])
+def test_dict_encode_on_device_matches_sorted_rank(n, distinct):
+    """dict_encode (tq/encodings.py:127-133) on the device: the dictionary is
+    the sorted distinct strings, codes their ranks -- equal to the host
+    (reference) algorithm incl. non-ASCII, empty and prefix strings."""
+    import bisect
+
+    from paper_2211_02753_b200 import encodings as E
+
+    rng = np.random.default_rng(n)
+    alphabet = ["", "a", "ab", "abc", "b", "\u00e4", "\u00e4b", "Z", "zz", "\u65e5\u672c",
+                "\u65e5", "a "]
+    pool = alphabet + [f"s{int(x):07d}" + ("\u00e9" if x % 3 == 0 else "") for x in
+                       rng.integers(0, 10**7, size=distinct)]
+    strings = [pool[i] for i in rng.integers(0, len(pool), size=n)]
+    col = E.dict_encode(strings)
+    entries = tuple(sorted(set(strings)))
+    assert col.encoding.dictionary.entries == entries
+    exp = np.array([bisect.bisect_left(entries, s) for s in strings], dtype=np.int64)
+    np.testing.assert_array_equal(col.values.numpy(), exp)
+    assert E.dict_decode(col) == strings

@@ -122,7 +122,10 @@ def test_fused_soft_linear_count(dtype, d, k, oh, dense_pos):
     # contiguous layout; the strided layout sums the row dots in another
     # order) and matching gradients
     cgrid, cdw, cdb = _run(X, W, b, codes, ks, dense_pos, G, dtype, fuse=False)
-    if _contiguous(dtype, d):
+    onepass = dtype == "float32" and k == 2 and len(oh) == 1 and d in (32, 64)
+    if onepass:  # llp_onepass.cu: float64 sums of the probabilities, not 2^-30 fixed point
+        np.testing.assert_allclose(grid, cgrid, rtol=1e-8, atol=n * 2.0**-31)
+    elif _contiguous(dtype, d):
         np.testing.assert_array_equal(grid, cgrid)
     else:
         np.testing.assert_allclose(grid, cgrid, rtol=1e-6 if dtype == "float32" else 1e-13,

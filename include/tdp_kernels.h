@@ -405,6 +405,17 @@ int tdp_join_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
                   int64_t* out_probe_idx, int64_t* out_build_idx, void* ws, size_t ws_bytes,
                   void* stream);
 
+/* Differentiable ORDER BY [LIMIT k] of trainable queries (
+ * the reference rejects Sort/Limit when trainable, tq/compiler.py:464-475):
+ * NeuralSort rows P[k][n] of float64 scores s (descending), temperature tau
+ *   P[r, i] = softmax_i(((n + 1 - 2 (r + 1)) s_i - sum_j |s_i - s_j|) / tau).
+ * fwd workspace: n doubles.  bwd: dP (overwritten with the softmax VJP),
+ * out_ds = dL/ds; workspace 2 n doubles.                                    */
+int tdp_softsort_fwd(const double* s, int64_t n, int32_t k, double tau, double* out_P,
+                     double* ws, void* stream);
+int tdp_softsort_bwd(const double* s, int64_t n, int32_t k, double tau, const double* P,
+                     double* dP_inout, double* out_ds, double* ws, void* stream);
+
 /* Device dictionary encoding (tq/encodings.py:127-133 dict_encode): a
  * 64-bit hash per string of a UTF-8 byte buffer (offsets int64 [n + 1]);
  * after tdp_unique_inverse of the hashes, tdp_string_groups writes each hash

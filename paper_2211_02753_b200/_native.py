@@ -154,6 +154,10 @@ _SIGNATURES = {
     "tdp_string_hash": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "tdp_string_groups": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p]),
+    "tdp_softsort_fwd": (c_int, [c_void_p, c_int64, c_int32, c_double, c_void_p, c_void_p,
+                                 c_void_p]),
+    "tdp_softsort_bwd": (c_int, [c_void_p, c_int64, c_int32, c_double, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_void_p]),
     "tdp_groupby_bitmap_workspace": (c_size_t, [c_int64, c_int64, c_int32]),
     "tdp_groupby_bitmap_prepare": (c_int, [c_void_p, c_int64, c_int64, c_int64, POINTER(Column),
                                            POINTER(c_int32), c_int32, c_void_p, c_void_p,

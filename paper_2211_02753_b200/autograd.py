@@ -396,3 +396,40 @@ def soft_linear_count(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.T
                       out_dtype: torch.dtype) -> torch.Tensor:
     """Flattened count grid of softmax(x w + b) crossed with one-hot keys."""
     return _SoftLinearCount.apply(spec, dense_pos, out_dtype, x, w, b, *codes)
+
+
+# ---------------------------------------------------------------------------
+# differentiable ORDER BY (SURVEY §8(f) 4): NeuralSort relaxation
+# ---------------------------------------------------------------------------
+
+class _SoftSort(torch.autograd.Function):
+    """P [k, n]: row r the relaxed one-hot of the rank-r (descending) row of
+    scores s (float64), temperature tau (csrc/softsort.cu)."""
+
+    @staticmethod
+    def forward(ctx, s: torch.Tensor, k: int, tau: float) -> torch.Tensor:
+        s = s.detach().to(torch.float64).contiguous()
+        n = s.numel()
+        P = torch.empty((k, n), dtype=torch.float64, device=s.device)
+        ws = torch.empty(max(n, 1), dtype=torch.float64, device=s.device)
+        nat.call("tdp_softsort_fwd", nat.ptr(s), n, k, float(tau), nat.ptr(P), nat.ptr(ws),
+                 nat.stream())
+        ctx.tau, ctx.k = tau, k
+        ctx.save_for_backward(s, P)
+        return P
+
+    @staticmethod
+    def backward(ctx, dP: torch.Tensor):
+        s, P = ctx.saved_tensors
+        n = s.numel()
+        g = dP.detach().to(torch.float64).contiguous().clone()
+        ds = torch.empty(n, dtype=torch.float64, device=s.device)
+        ws = torch.empty(2 * max(n, 1), dtype=torch.float64, device=s.device)
+        nat.call("tdp_softsort_bwd", nat.ptr(s), n, ctx.k, float(ctx.tau), nat.ptr(P), nat.ptr(g),
+                 nat.ptr(ds), nat.ptr(ws), nat.stream())
+        return ds, None, None
+
+
+def soft_sort_matrix(s: torch.Tensor, k: int, tau: float) -> torch.Tensor:
+    """Relaxed top-k permutation rows of the scores (descending)."""
+    return _SoftSort.apply(s, k, tau)

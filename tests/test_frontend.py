@@ -184,3 +184,21 @@ def test_pipeline_codegen_compiles_q1_program_with_nvrtc():
     assert "tdp_bulk_load(sb + 0u" in src  # column tiles stream through the bulk-copy ring
     # the UDF's (1 - d) and (1 + t) become SSA values; (1.0) is shared (CSE)
     assert src.count("P.imf[") == 2  # once in tdp_eval, once in tdp_project
+
+
+def test_trainable_order_by_is_rejected_without_soft_sort():
+    """tq/compiler.py:464-475: Sort / Limit in trainable mode raise CompileError
+    unless the soft-sort extension is asked for (CompileConfig.soft_sort_tau)."""
+    import paper_2211_02753_b200 as tq
+    from paper_2211_02753_b200.compiler import CompileError
+
+    cat = tq.Catalog()
+    reg = tq.UdfRegistry()
+    cat.register_tensor(tq.Tensor(np.zeros((4, 3))), "T")
+    reg.register(tq.make_scoring_udf("scorer", tq.Tensor(np.ones(3)), 1.0))
+    plan = tq.lower(tq.bind(tq.parse("SELECT Score FROM scorer(T) ORDER BY Score LIMIT 2"), cat,
+                            reg))
+    with pytest.raises(CompileError, match="Sort has no differentiable implementation"):
+        tq.compile_plan(plan, tq.CompileConfig(trainable=True), reg)
+    q = tq.compile_plan(plan, tq.CompileConfig(trainable=True, soft_sort_tau=0.5), reg)
+    assert "sort[soft]" in q.explain_compiled()

@@ -36,7 +36,7 @@ import numpy as np
 import torch
 
 from .encodings import EncodedTensor, trusted
-from .lazy import Expr, LazyValue, compact_source, project
+from .lazy import Expr, LazyValue, compact_source, project, set_value_range
 from .storage import Table, table_from_columns
 from .tensor import Tensor
 
@@ -103,7 +103,9 @@ def plan_column(col: EncodedTensor) -> Optional[tuple[CompactSpec, torch.Tensor]
         dt = _int_type(lo, hi, unsigned_ok=col.is_dictionary())
         if dt is None:
             return None
-        return CompactSpec(dt), t.to(dt)
+        stored = t.to(dt)
+        set_value_range(stored, lo, hi)
+        return CompactSpec(dt), stored
     if t.dtype != torch.float64 or n == 0:
         return None
     # exact decimal test on the host (numpy division is correctly rounded),
@@ -126,6 +128,7 @@ def plan_column(col: EncodedTensor) -> Optional[tuple[CompactSpec, torch.Tensor]
             decoded = project([decode_expr(stored, s)], None)[0]
             if not bool((decoded.view(torch.int64) == t.view(torch.int64)).all()):
                 continue
+            set_value_range(stored, lo, hi)
             return CompactSpec(dt, s), stored
     return None
 

@@ -67,6 +67,8 @@ static i64 two_cta_row_bytes() {
 #define kTwoCtaRowBytes two_cta_row_bytes()
 constexpr i64 kMaxSmemCells = 48;           // shared-memory accumulator mode limit
 constexpr int kAccThreads = 256;            // accumulator columns (TDP_ACC_THREADS)
+constexpr int kMaxPackWords = 8;            // packed per-thread accumulator words
+constexpr int kMaxIvals = 32;               // integer accumulators (<= aggregates)
 
 // Must match the TdpParams emitted below, field for field.
 struct HostParams {
@@ -81,6 +83,7 @@ struct HostParams {
   void* acc;
   const unsigned* bits;
   const i64* tile_off;
+  i64 plo[kMaxIvals];     // per integer accumulator: bias of its packed field
 };
 
 // ---------------------------------------------------------------------------
@@ -175,6 +178,30 @@ const char* op_sym(int op) {
   }
 }
 
+// Internal aggregate kind (never passed in by callers): SUM of a float64 value
+// that the program computes exactly as scaled integers (decimal columns kept
+// as integers by compact storage, exact decimal constants, + - *): the sum is
+// accumulated exactly in integers and converted once, sum / scale, at the end.
+constexpr int kAggSumDec = 3;
+
+// Closed interval of an int64 program value, when it provably never wraps.
+struct Range {
+  bool ok = false;
+  i64 lo = 0, hi = 0;
+};
+
+// One accumulator packed into a 64-bit per-thread word (shared-memory mode):
+// the word receives (v - lo) << off per kept row, so every field stays
+// non-negative and fields never borrow from each other.
+struct Field {
+  int acc;   // -1: the row count, else an integer accumulator (ival index)
+  int word;
+  int off;
+  int bits;   // field width: the sum of up to rows-per-thread values
+  i64 lo;     // bias subtracted from every value (min(range lo, 0))
+  int rbits;  // width of one biased value
+};
+
 struct Spec {
   // inputs
   std::vector<int> col_dtype;  // per column
@@ -187,11 +214,366 @@ struct Spec {
   std::vector<int> used_cols;
   std::vector<int> fvals, ivals;  // accumulator -> program value
   std::vector<int> agg_acc;       // agg -> accumulator index (-1 for count)
+  std::vector<double> agg_scale;  // per agg: decimal scale of a kAggSumDec sum, else 0
+  std::vector<double> iscale;     // per ival: 0 (plain SUM_I64) or the decimal scale
   i64 slots = 1;
   int accmode = 0;       // 0 registers, 1 shared-memory columns, 2 global atomics
   bool regacc = true;    // per-CTA partial rows (modes 0 and 1)
   i64 acc_smem = 0;      // bytes of shared-memory accumulators (mode 1)
+  // shared-memory mode: packed per-thread words (count + bounded integer sums)
+  std::vector<Field> fields;
+  int pwords = 0;
+  std::vector<int> iu;   // per ival: unpacked cell index, or -1 when packed
+  i64 sm_rows = 0;       // u64 rows of TDP_ACC_THREADS words
 };
+
+// ---------------------------------------------------------------------------
+// exact decimal aggregation
+// ---------------------------------------------------------------------------
+constexpr i64 kRangeLimit = (i64)1 << 62;
+
+Range type_range(int dt) {
+  Range r;
+  r.ok = true;
+  switch (dt) {
+    case TDP_I8: r.lo = -128; r.hi = 127; break;
+    case TDP_U8: r.lo = 0; r.hi = 255; break;
+    case TDP_BOOL: r.lo = 0; r.hi = 1; break;
+    case TDP_I16: r.lo = -32768; r.hi = 32767; break;
+    case TDP_I32: r.lo = INT32_MIN; r.hi = INT32_MAX; break;
+    default: r.ok = false;
+  }
+  return r;
+}
+
+Range make_range(__int128 lo, __int128 hi) {
+  Range r;
+  r.ok = lo >= -(__int128)kRangeLimit && hi <= (__int128)kRangeLimit;
+  r.lo = r.ok ? (i64)lo : 0;
+  r.hi = r.ok ? (i64)hi : 0;
+  return r;
+}
+
+// Interval of every int64 program value (others: !ok).  A LOAD with b == 1
+// carries the caller's promise that the stored values lie in [imm_i, imm_f]
+// (compact storage measures it at ingestion).
+std::vector<Range> value_ranges(const Spec& s) {
+  std::vector<Range> R(s.prog.size());
+  for (size_t j = 0; j < s.prog.size(); ++j) {
+    const tdp_instr& in = s.prog[j];
+    if (in.dtype != TDP_I64) continue;
+    const Range a = in.a >= 0 && in.a < (int)j ? R[in.a] : Range();
+    const Range b = in.b >= 0 && in.b < (int)j ? R[in.b] : Range();
+    switch (in.op) {
+      case TDP_OP_LOAD: {
+        Range t = type_range(s.col_dtype[in.a]);
+        if (in.b == 1) {
+          const i64 hlo = in.imm_i, hhi = (i64)in.imm_f;
+          if (!t.ok) t = make_range(hlo, hhi);
+          else if (hlo >= t.lo && hhi <= t.hi && hlo <= hhi) t = make_range(hlo, hhi);
+        }
+        R[j] = t;
+        break;
+      }
+      case TDP_OP_CONST: R[j] = make_range(in.imm_i, in.imm_i); break;
+      case TDP_OP_CAST: R[j] = s.prog[in.a].dtype == TDP_I64 ? a : Range(); break;
+      case TDP_OP_ADD:
+        if (a.ok && b.ok) R[j] = make_range((__int128)a.lo + b.lo, (__int128)a.hi + b.hi);
+        break;
+      case TDP_OP_SUB:
+        if (a.ok && b.ok) R[j] = make_range((__int128)a.lo - b.hi, (__int128)a.hi - b.lo);
+        break;
+      case TDP_OP_MUL:
+        if (a.ok && b.ok) {
+          const __int128 p[4] = {(__int128)a.lo * b.lo, (__int128)a.lo * b.hi,
+                                 (__int128)a.hi * b.lo, (__int128)a.hi * b.hi};
+          __int128 lo = p[0], hi = p[0];
+          for (int k = 1; k < 4; ++k) {
+            lo = p[k] < lo ? p[k] : lo;
+            hi = p[k] > hi ? p[k] : hi;
+          }
+          R[j] = make_range(lo, hi);
+        }
+        break;
+      case TDP_OP_NEG:
+        if (a.ok) R[j] = make_range(-(__int128)a.hi, -(__int128)a.lo);
+        break;
+      case TDP_OP_SQUARE:
+        if (a.ok) {
+          const __int128 l2 = (__int128)a.lo * a.lo, h2 = (__int128)a.hi * a.hi;
+          const __int128 mx = l2 > h2 ? l2 : h2;
+          R[j] = a.lo >= 0 ? make_range(l2, h2) : a.hi <= 0 ? make_range(h2, l2) : make_range(0, mx);
+        }
+        break;
+      case TDP_OP_RELU:
+        if (a.ok) R[j] = make_range(a.lo > 0 ? a.lo : 0, a.hi > 0 ? a.hi : 0);
+        break;
+      default:
+        break;
+    }
+  }
+  return R;
+}
+
+struct Exact {
+  int v = -1;     // int64 program value
+  i64 scale = 0;  // value of the float64 = v / scale, exactly
+};
+
+int push_instr(Spec& s, int op, int a, int b, i64 imm_i) {
+  if ((int)s.prog.size() >= kMaxInstr) return -1;
+  tdp_instr in;
+  in.op = op;
+  in.dtype = TDP_I64;
+  in.a = a;
+  in.b = b;
+  in.imm_i = imm_i;
+  in.imm_f = 0.0;
+  s.prog.push_back(in);
+  return (int)s.prog.size() - 1;
+}
+
+// Exact scaled decimal of a small-magnitude float constant: m / 10^k == c.
+bool exact_const(double c, i64* m, i64* scale) {
+  i64 p = 1;
+  for (int k = 0; k <= 6; ++k, p *= 10) {
+    const double x = c * (double)p;
+    if (!(x > -9.0e15 && x < 9.0e15)) return false;
+    const double r = nearbyint(x);
+    if ((double)(i64)r / (double)p == c) {
+      *m = (i64)r;
+      *scale = p;
+      return true;
+    }
+  }
+  return false;
+}
+
+// The float64 program value `v` restated over int64 values with a scale, or
+// false.  Emits the integer instructions it needs (memoised per value).
+bool exact_of(Spec& s, int v, std::map<int, Exact>& memo, Exact* out) {
+  auto it = memo.find(v);
+  if (it != memo.end()) {
+    *out = it->second;
+    return out->v >= 0;
+  }
+  memo[v] = Exact();  // in progress / failed
+  const tdp_instr in = s.prog[v];
+  Exact e;
+  if (in.dtype != TDP_F64) return false;
+  switch (in.op) {
+    case TDP_OP_DECIMAL: {
+      const double d = in.imm_f;
+      if (!(d >= 1.0 && d <= 1e9 && d == nearbyint(d))) return false;
+      e.v = in.a;
+      e.scale = (i64)d;
+      break;
+    }
+    case TDP_OP_CAST:
+      if (s.prog[in.a].dtype != TDP_I64) return false;
+      e.v = in.a;
+      e.scale = 1;
+      break;
+    case TDP_OP_CONST: {
+      i64 m = 0, sc = 1;
+      if (!exact_const(in.imm_f, &m, &sc)) return false;
+      e.v = push_instr(s, TDP_OP_CONST, 0, 0, m);
+      e.scale = sc;
+      break;
+    }
+    case TDP_OP_NEG:
+    case TDP_OP_SQUARE: {
+      Exact a;
+      if (!exact_of(s, in.a, memo, &a)) return false;
+      if (in.op == TDP_OP_SQUARE && a.scale > ((i64)1 << 26)) return false;
+      e.v = push_instr(s, in.op, a.v, 0, 0);
+      e.scale = in.op == TDP_OP_SQUARE ? a.scale * a.scale : a.scale;
+      break;
+    }
+    case TDP_OP_ADD:
+    case TDP_OP_SUB:
+    case TDP_OP_MUL: {
+      Exact a, b;
+      if (!exact_of(s, in.a, memo, &a) || !exact_of(s, in.b, memo, &b)) return false;
+      if (in.op == TDP_OP_MUL) {
+        if ((__int128)a.scale * b.scale > ((i64)1 << 53)) return false;
+        e.v = push_instr(s, TDP_OP_MUL, a.v, b.v, 0);
+        e.scale = a.scale * b.scale;
+        break;
+      }
+      // common scale: one scale must divide the other (powers of ten do)
+      const i64 hi = a.scale > b.scale ? a.scale : b.scale;
+      if (hi % a.scale || hi % b.scale) return false;
+      // x * factor (a constant operand is folded: no per-row multiply)
+      auto rescale = [&s](int v, i64 factor) -> int {
+        if (factor == 1) return v;
+        const tdp_instr& c = s.prog[v];
+        if (c.op == TDP_OP_CONST && c.dtype == TDP_I64) {
+          const __int128 m = (__int128)c.imm_i * factor;
+          if (m > -(__int128)kRangeLimit && m < (__int128)kRangeLimit)
+            return push_instr(s, TDP_OP_CONST, 0, 0, (i64)m);
+        }
+        const int f = push_instr(s, TDP_OP_CONST, 0, 0, factor);
+        return f < 0 ? -1 : push_instr(s, TDP_OP_MUL, v, f, 0);
+      };
+      const int av = rescale(a.v, hi / a.scale);
+      const int bv = av < 0 ? -1 : rescale(b.v, hi / b.scale);
+      if (av < 0 || bv < 0) return false;
+      e.v = push_instr(s, in.op, av, bv, 0);
+      e.scale = hi;
+      break;
+    }
+    default:
+      return false;
+  }
+  if (e.v < 0) return false;
+  memo[v] = e;
+  *out = e;
+  return true;
+}
+
+i64 ceil_pow2(i64 x) {
+  i64 p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int bits_for(unsigned __int128 x) {  // bits of the largest value a field must hold
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b > 0 ? b : 1;
+}
+
+// Rows one accumulating thread can see: every kernel variant runs 256
+// accumulating threads per CTA and at least one CTA per SM (or <= 4 rows per
+// thread when the grid is smaller), so n / (256 * SMs) plus a tile's rows;
+// rounded up to a power of two so the packing (part of the kernel's cache
+// key) changes only when n doubles.
+i64 rows_per_thread_bound(i64 n) {
+  const i64 sms = sm_count() > 0 ? sm_count() : 148;
+  return ceil_pow2(n / (256 * sms) + 16);
+}
+
+// SUM over a float64 value computed exactly from scaled integers -> exact
+// integer accumulation (kAggSumDec), when the integer program cannot wrap and
+// a CTA's partial sum fits int64.  Changes no result beyond the rounding of
+// the float path (the sum of the exact row values, rounded once).
+void convert_decimal_sums(Spec& s, i64 n) {
+  std::map<int, Exact> memo;
+  const size_t keep = s.prog.size();
+  std::vector<std::pair<int, Exact>> conv;  // agg -> exact
+  for (size_t a = 0; a < s.aggs.size(); ++a) {
+    if (s.aggs[a].kind != TDP_AGG_SUM_F64) continue;
+    Exact e;
+    if (exact_of(s, s.aggs[a].value, memo, &e)) conv.emplace_back((int)a, e);
+  }
+  if (conv.empty()) {
+    s.prog.resize(keep);
+    return;
+  }
+  const std::vector<Range> R = value_ranges(s);
+  const i64 per_cta = s.accmode == 2 ? (n > 0 ? n : 1) : rows_per_thread_bound(n) * 256;
+  bool any = false;
+  for (auto& ce : conv) {
+    const Range& r = R[ce.second.v];
+    if (!r.ok) continue;
+    const i64 mag = r.hi > -r.lo ? r.hi : -r.lo;
+    if ((__int128)mag * per_cta >= ((__int128)1 << 63)) continue;
+    s.aggs[ce.first].kind = kAggSumDec;
+    s.aggs[ce.first].value = ce.second.v;
+    any = true;
+  }
+  if (!any) s.prog.resize(keep);
+  s.agg_scale.assign(s.aggs.size(), 0.0);
+  for (auto& ce : conv)
+    if (s.aggs[ce.first].kind == kAggSumDec) s.agg_scale[ce.first] = (double)ce.second.scale;
+}
+
+// Shared-memory accumulators: pack the row count and every bounded integer
+// sum into as few per-thread 64-bit words as their ranges allow (first fit,
+// widest first).  Q1 on compact storage: count + 5 sums in 3 words instead of
+// a 32-bit count and five 64-bit cells (48 instead of 88 bytes of shared-memory
+// read-modify-write per row).
+void pack_fields(Spec& s, i64 n) {
+  s.fields.clear();
+  s.pwords = 0;
+  s.iu.assign(s.ivals.size(), -1);
+  const std::vector<Range> R = value_ranges(s);
+  const unsigned __int128 rows = (unsigned __int128)rows_per_thread_bound(n);
+  std::vector<Field> cand;
+  cand.push_back(Field{-1, 0, 0, bits_for(rows), 0, 1});
+  for (size_t k = 0; k < s.ivals.size(); ++k) {
+    const Range& r = R[s.ivals[k]];
+    if (!r.ok) continue;
+    // biased by min(lo, 0): non-negative ranges need no per-row subtract
+    const i64 bias = r.lo < 0 ? r.lo : 0;
+    const unsigned __int128 span = (unsigned __int128)((__int128)r.hi - bias);
+    const int b = bits_for(span * rows);
+    if (b <= 62) cand.push_back(Field{(int)k, 0, 0, b, bias, bits_for(span)});
+  }
+  std::vector<int> order(cand.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return cand[x].bits > cand[y].bits; });
+  std::vector<int> used;
+  for (int i : order) {
+    Field f = cand[i];
+    int w = 0;
+    while (w < (int)used.size() && used[w] + f.bits > 64) ++w;
+    if (w == (int)used.size()) {
+      if ((int)used.size() == kMaxPackWords) continue;
+      used.push_back(0);
+    }
+    f.word = w;
+    f.off = used[w];
+    used[w] += f.bits;
+    s.fields.push_back(f);
+  }
+  bool count_packed = false;
+  for (const Field& f : s.fields) count_packed |= f.acc < 0;
+  // worth it only when some word holds two fields
+  if (!count_packed || used.size() >= s.fields.size()) {
+    s.fields.clear();
+    s.iu.assign(s.ivals.size(), -1);
+    return;
+  }
+  s.pwords = (int)used.size();
+  std::vector<char> packed(s.ivals.size(), 0);
+  for (const Field& f : s.fields)
+    if (f.acc >= 0) packed[f.acc] = 1;
+  int nu = 0;
+  for (size_t k = 0; k < s.ivals.size(); ++k) s.iu[k] = packed[k] ? -1 : nu++;
+}
+
+// agg -> accumulator lists (deduplicated by value and scale)
+void list_accumulators(Spec& s) {
+  s.fvals.clear();
+  s.ivals.clear();
+  s.iscale.clear();
+  s.agg_acc.clear();
+  for (size_t a = 0; a < s.aggs.size(); ++a) {
+    const tdp_agg& g = s.aggs[a];
+    if (g.kind == TDP_AGG_COUNT) {
+      s.agg_acc.push_back(-1);
+      continue;
+    }
+    const bool isf = g.kind == TDP_AGG_SUM_F64;
+    const double sc = s.agg_scale[a];
+    std::vector<int>& lst = isf ? s.fvals : s.ivals;
+    int idx = -1;
+    for (size_t t = 0; t < lst.size(); ++t)
+      if (lst[t] == g.value && (isf || s.iscale[t] == sc)) idx = (int)t;
+    if (idx < 0) {
+      idx = (int)lst.size();
+      lst.push_back(g.value);
+      if (!isf) s.iscale.push_back(sc);
+    }
+    s.agg_acc.push_back(idx);
+  }
+}
 
 int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
   TDP_REQUIRE(ncols >= 0 && ncols <= kMaxCols, "at most %d columns (got %d)", kMaxCols, ncols);
@@ -227,6 +609,8 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
     switch (in.op) {
       case TDP_OP_LOAD:
         TDP_REQUIRE(in.a >= 0 && in.a < ncols, "instr %zu: bad column", j);
+        TDP_REQUIRE(in.b == 0 || (in.b == 1 && in.dtype == TDP_I64 && (double)in.imm_i <= in.imm_f),
+                    "instr %zu: bad value-range hint", j);
         used[in.a] = 1;
         break;
       case TDP_OP_CONST:
@@ -274,24 +658,14 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
   }
   for (size_t a = 0; a < s.aggs.size(); ++a) {
     const tdp_agg& g = s.aggs[a];
-    if (g.kind == TDP_AGG_COUNT) {
-      s.agg_acc.push_back(-1);
-      continue;
-    }
+    if (g.kind == TDP_AGG_COUNT) continue;
     TDP_REQUIRE(g.kind == TDP_AGG_SUM_F64 || g.kind == TDP_AGG_SUM_I64, "agg %zu: bad kind", a);
     TDP_REQUIRE(g.value >= 0 && g.value < (int)s.prog.size(), "agg %zu: bad value", a);
     if (g.kind == TDP_AGG_SUM_I64)
       TDP_REQUIRE(s.prog[g.value].dtype == TDP_I64, "agg %zu: SUM_I64 over a float value", a);
-    std::vector<int>& lst = g.kind == TDP_AGG_SUM_F64 ? s.fvals : s.ivals;
-    int idx = -1;
-    for (size_t t = 0; t < lst.size(); ++t)
-      if (lst[t] == g.value) idx = (int)t;
-    if (idx < 0) {
-      idx = (int)lst.size();
-      lst.push_back(g.value);
-    }
-    s.agg_acc.push_back(idx);
   }
+  s.agg_scale.assign(s.aggs.size(), 0.0);
+  list_accumulators(s);
   for (size_t o = 0; o < s.outs.size(); ++o)
     TDP_REQUIRE(s.outs[o] >= 0 && s.outs[o] < (int)s.prog.size(), "output %zu: bad value", o);
   for (int c = 0; c < ncols; ++c)
@@ -309,11 +683,37 @@ int validate_and_derive(Spec& s, const tdp_column* cols, int ncols, i64 n) {
   else if (cells <= kMaxSmemCells) s.accmode = 1;
   else s.accmode = 2;
   s.regacc = s.accmode != 2;
-  s.acc_smem = s.accmode == 1 ? cells * kAccThreads * 8 : 0;
+  if (!s.aggs.empty() && s.outs.empty()) {
+    convert_decimal_sums(s, n);
+    list_accumulators(s);
+  }
+  s.iu.assign(s.ivals.size(), -1);
+  for (size_t k = 0; k < s.ivals.size(); ++k) s.iu[k] = (int)k;
+  s.fields.clear();
+  s.pwords = 0;
+  if (s.accmode == 1) pack_fields(s, n);
+  // shared-memory rows: packed words [pwords][G], 32-bit counts (when not
+  // packed) [G] (G/2 rows of u64), float cells [NF][G], unpacked int cells
+  int niu = 0;
+  for (int k : s.iu) niu += k >= 0 ? 1 : 0;
+  // one extra slot row per cell takes the rows that fail the predicates
+  // (branch-free updates)
+  s.sm_rows = (s.slots + 1) * ((i64)s.pwords + (i64)s.fvals.size() + niu) +
+              (s.pwords > 0 ? 0 : (s.slots + 2) / 2);
+  s.acc_smem = s.accmode == 1 ? s.sm_rows * kAccThreads * 8 : 0;
   return TDP_OK;
 }
 
+bool fits32(const Range& r) { return r.ok && r.lo >= INT32_MIN && r.hi <= INT32_MAX; }
+
+// integer compares on <= 16-bit columns run in 32 bits (fill_params clamps the literal)
+bool narrow_cmp(int dt) { return dt == TDP_I8 || dt == TDP_I16 || dt == TDP_U8 || dt == TDP_BOOL; }
+
 void emit_program(std::ostringstream& o, const Spec& s) {
+  // int64 values whose range provably fits 32 bits are computed in 32-bit
+  // arithmetic (mod 2^32, exact because the result fits); 32 x 32 -> 64-bit
+  // products are one wide multiply
+  const std::vector<Range> R = value_ranges(s);
   for (size_t j = 0; j < s.prog.size(); ++j) {
     const tdp_instr& in = s.prog[j];
     const char* T = ctype_of(in.dtype);
@@ -321,6 +721,25 @@ void emit_program(std::ostringstream& o, const Spec& s) {
     const bool isf32 = in.dtype == TDP_F32;
     o << "  const " << T << " v" << j << " = ";
     const std::string a = "v" + std::to_string(in.a), b = "v" + std::to_string(in.b);
+    if (isint && fits32(R[j]) &&
+        (in.op == TDP_OP_ADD || in.op == TDP_OP_SUB || in.op == TDP_OP_MUL ||
+         in.op == TDP_OP_NEG || in.op == TDP_OP_SQUARE)) {
+      const std::string ua = "(unsigned)" + a, ub = "(unsigned)" + b;
+      o << "(i64)(int)(";
+      switch (in.op) {
+        case TDP_OP_ADD: o << ua << " + " << ub; break;
+        case TDP_OP_SUB: o << ua << " - " << ub; break;
+        case TDP_OP_MUL: o << ua << " * " << ub; break;
+        case TDP_OP_NEG: o << "0u - " << ua; break;
+        default: o << ua << " * " << ua; break;
+      }
+      o << ");\n";
+      continue;
+    }
+    if (isint && in.op == TDP_OP_MUL && fits32(R[in.a]) && fits32(R[in.b])) {
+      o << "(i64)(int)" << a << " * (i64)(int)" << b << ";\n";
+      continue;
+    }
     switch (in.op) {
       case TDP_OP_LOAD:
         o << "(" << T << ")r.c" << in.a;
@@ -373,6 +792,115 @@ void emit_program(std::ostringstream& o, const Spec& s) {
   }
 }
 
+// Shared-memory accumulator columns (TDP_ACCMODE 1): one TDP_ACC_THREADS-wide
+// row of u64 per cell, each thread owning one column of every row.  Rows:
+// packed words [NW][G] | 32-bit counts [G] (only when the count is not
+// packed; G/2 rows) | float cells [NF][G] | unpacked integer cells [..][G].
+void emit_smem_acc(std::ostringstream& o, const Spec& s) {
+  const i64 G = s.slots + 1, NW = s.pwords, NF = (i64)s.fvals.size();  // + the reject slot
+  const i64 FB = NW * G + (NW > 0 ? 0 : (G + 1) / 2);
+  const i64 IB = FB + NF * G;
+  const Field* cnt = nullptr;
+  std::vector<const Field*> fof(s.ivals.size(), nullptr);
+  for (const Field& f : s.fields) {
+    if (f.acc < 0) cnt = &f;
+    else fof[f.acc] = &f;
+  }
+  // `mine` = this thread's column (sm + col); rows failing the predicates go
+  // to slot TDP_G, which the flush ignores
+  o << "__device__ __forceinline__ void tdp_smem_add(u64* mine, int slot, const double* f, "
+       "const i64* q, const TdpParams& P) {\n";
+  o << "  (void)f; (void)q; (void)P;\n  u64* p = mine + slot * TDP_ACC_THREADS;\n";
+  // per word: the biased field values x = q - bias (0 <= x < 2^bits) occupy
+  // disjoint bit ranges, so the word is assembled from two 32-bit halves
+  // without carries (one shift per field; 64-bit only for > 32-bit fields)
+  for (int w = 0; w < NW; ++w) {
+    u64 konst = 0;
+    std::ostringstream lo32, hi32, w64;
+    for (const Field& f : s.fields) {
+      if (f.word != w) continue;
+      if (f.acc < 0) {
+        konst += (u64)1 << f.off;
+        continue;
+      }
+      std::ostringstream x;
+      if (f.rbits <= 32) {
+        x << "((unsigned)q[" << f.acc << "]";
+        if (f.lo != 0) x << " - (unsigned)P.plo[" << f.acc << "]";
+        x << ")";
+        if (f.off + f.rbits <= 32) {
+          lo32 << " + (" << x.str() << " << " << f.off << ")";
+        } else if (f.off >= 32) {
+          hi32 << " + (" << x.str() << " << " << f.off - 32 << ")";
+        } else {
+          lo32 << " + (" << x.str() << " << " << f.off << ")";
+          hi32 << " + (" << x.str() << " >> " << 32 - f.off << ")";
+        }
+      } else {
+        w64 << " + ((u64)(q[" << f.acc << "]";
+        if (f.lo != 0) w64 << " - P.plo[" << f.acc << "]";
+        w64 << ") << " << f.off << ")";
+      }
+    }
+    o << "  {\n    const unsigned lo = " << (unsigned)(konst & 0xffffffffu) << "u" << lo32.str()
+      << ";\n    const unsigned hi = " << (unsigned)(konst >> 32) << "u" << hi32.str() << ";\n";
+    o << "    p[" << w * G << " * TDP_ACC_THREADS] += (((u64)hi << 32) | lo)" << w64.str()
+      << ";\n  }\n";
+  }
+  if (NW == 0)  // 32-bit counts [G][256] at the start (col == threadIdx.x)
+    o << "  reinterpret_cast<unsigned*>(mine - threadIdx.x)[slot * TDP_ACC_THREADS + threadIdx.x] "
+         "+= 1u;\n";
+  for (i64 a = 0; a < NF; ++a)
+    o << "  *reinterpret_cast<double*>(p + " << FB + a * G << " * TDP_ACC_THREADS) += f[" << a
+      << "];\n";
+  for (size_t k = 0; k < s.iu.size(); ++k)
+    if (s.iu[k] >= 0)
+      o << "  p[" << IB + (i64)s.iu[k] * G << " * TDP_ACC_THREADS] += (u64)q[" << k << "];\n";
+  o << "}\n";
+  // per-CTA partial row, cell-major (acc[cell * gridDim.x + cta]); fixed order
+  auto field_sum = [&](const Field& f, const char* v) {
+    o << "      const u64* row = sm + (" << (i64)f.word * G << " + slot) * TDP_ACC_THREADS;\n"
+      << "      for (int t = 0; t < TDP_ACC_THREADS; ++t) " << v << " += (row[t] >> " << f.off
+      << ") & " << (((u64)1 << f.bits) - 1) << "ull;\n";
+  };
+  o << "__device__ __forceinline__ void tdp_smem_flush(const u64* sm, const TdpParams& P) {\n"
+       "  u64* out = reinterpret_cast<u64*>(P.acc) + blockIdx.x;\n"
+       "  for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {\n"
+       "    const int grp = c / TDP_G, slot = c % TDP_G;\n"
+       "    u64 v = 0;\n"
+       "    switch (grp) {\n";
+  o << "    case 0: {\n";
+  if (cnt) {
+    field_sum(*cnt, "v");
+  } else {
+    o << "      const unsigned* row = reinterpret_cast<const unsigned*>(sm) + slot * "
+         "TDP_ACC_THREADS;\n      for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];\n";
+  }
+  o << "      break;\n    }\n";
+  for (i64 a = 0; a < NF; ++a)
+    o << "    case " << 1 + a << ": {\n      const double* row = reinterpret_cast<const double*>(sm) + ("
+      << FB + a * G << " + slot) * TDP_ACC_THREADS;\n      double d = 0.0;\n"
+      << "      for (int t = 0; t < TDP_ACC_THREADS; ++t) d += row[t];\n"
+      << "      v = (u64)__double_as_longlong(d);\n      break;\n    }\n";
+  for (size_t k = 0; k < s.ivals.size(); ++k) {
+    o << "    case " << 1 + NF + (i64)k << ": {\n";
+    if (fof[k]) {
+      // biased field sums + lo * (rows counted by this CTA for the slot)
+      o << "      u64 cn = 0;\n      {\n";
+      field_sum(*cnt, "cn");
+      o << "      }\n";
+      field_sum(*fof[k], "v");
+      o << "      v += (u64)P.plo[" << k << "] * cn;\n";
+    } else {
+      o << "      const u64* row = sm + (" << IB + (i64)s.iu[k] * G
+        << " + slot) * TDP_ACC_THREADS;\n      for (int t = 0; t < TDP_ACC_THREADS; ++t) v += "
+           "row[t];\n";
+    }
+    o << "      break;\n    }\n";
+  }
+  o << "    default: break;\n    }\n    out[(i64)c * gridDim.x] = v;\n  }\n}\n";
+}
+
 // Shape of the bulk-copy ring for the columns a program reads.
 struct Ring {
   int pu = 4;            // rows per consumer thread per tile
@@ -386,7 +914,14 @@ Ring ring_shape(const Spec& s) {
   i64 row_bytes = 0;
   for (int c : s.used_cols) row_bytes += dtype_size(s.col_dtype[c]);
   if (row_bytes == 0) row_bytes = 1;
-  r.pu = 4;
+  // private accumulator columns read each column with one vector load per
+  // thread: 8 rows per thread halve the per-tile loop overhead per row
+  static const int vec_pu = [] {  // measurements only
+    const char* e = getenv("TDP_VEC_PU");
+    const int v = e ? atoi(e) : 8;
+    return v == 4 ? 4 : 8;
+  }();
+  r.pu = s.accmode == 1 ? vec_pu : 4;
   const i64 budget = kRingBudget - s.acc_smem;
   static const i64 min_stages = [] {
     const char* e = getenv("TDP_RING_MIN_STAGES");  // measurements only
@@ -399,7 +934,13 @@ Ring ring_shape(const Spec& s) {
   // Narrow rows (compact storage) make the per-row arithmetic, not the bytes,
   // the limit: then prefer two CTAs per SM (twice the consumer warps to hide
   // FP64 / shared-memory latency) over a deeper ring, when two fit.
-  const i64 half = kTwoCtaBudget - s.acc_smem;
+  static const int narrow_ctas = [] {  // CTAs per SM for narrow rows (measurements)
+    const char* e = getenv("TDP_NARROW_CTAS");
+    const int v = e ? atoi(e) : 2;
+    return v < 2 ? 2 : (v > 4 ? 4 : v);
+  }();
+  const i64 per_cta = narrow_ctas == 2 ? kTwoCtaBudget : (i64)233472 / narrow_ctas - 2048;
+  const i64 half = per_cta - s.acc_smem;
   if (row_bytes <= kTwoCtaRowBytes && half >= 2 * r.stage_bytes) st = half / r.stage_bytes;
   r.stages = (int)(st < 2 ? 2 : (st > 8 ? 8 : st));
   return r;
@@ -423,11 +964,16 @@ std::string generate(const Spec& s) {
   o << "#define TDP_G " << s.slots << "\n#define TDP_NF " << s.fvals.size() << "\n";
   o << "#define TDP_NI " << s.ivals.size() << "\n#define TDP_ACCMODE " << s.accmode
     << "\n";
+  o << "#define TDP_CELLS (TDP_G * (1 + TDP_NF + TDP_NI))\n#define TDP_ACC_THREADS " << kAccThreads
+    << "\n";
+  o << "#define TDP_SM_ROWS " << (s.accmode == 1 ? s.sm_rows : 0) << "\n#define TDP_NW "
+    << s.pwords << "\n";
   o << "#define TDP_FTILE " << kFilterTile << "\n#define TDP_FWORDS " << kFilterWords << "\n";
   o << "struct TdpParams {\n  const void* col[" << kMaxCols << "];\n  void* out[" << kMaxOuts
     << "];\n  i64 n;\n  i64 pli[" << kMaxPreds << "];\n  double plf[" << kMaxPreds
     << "];\n  i64 imi[" << kMaxInstr << "];\n  double imf[" << kMaxInstr << "];\n  i64 klo["
-    << kMaxKeys << "];\n  void* acc;\n  const unsigned* bits;\n  const i64* tile_off;\n};\n";
+    << kMaxKeys << "];\n  void* acc;\n  const unsigned* bits;\n  const i64* tile_off;\n"
+    << "  i64 plo[" << kMaxIvals << "];\n};\n";
   // row of loaded columns
   o << "struct TdpRow {\n  int pad_;\n";
   for (int c : s.used_cols) o << "  " << ctype_of(s.col_dtype[c]) << " c" << c << ";\n";
@@ -495,8 +1041,12 @@ std::string generate(const Spec& s) {
     const tdp_predicate& p = s.preds[k];
     switch (p.cmp) {
       case TDP_CMP_I64:
-        o << "  keep &= ((i64)r.c" << p.column << " " << op_sym(p.op) << " P.pli[" << k
-          << "]);\n";
+        if (narrow_cmp(s.col_dtype[p.column]))  // literal clamped to the type range +- 1
+          o << "  keep &= ((int)r.c" << p.column << " " << op_sym(p.op) << " (int)P.pli[" << k
+            << "]);\n";
+        else
+          o << "  keep &= ((i64)r.c" << p.column << " " << op_sym(p.op) << " P.pli[" << k
+            << "]);\n";
         break;
       case TDP_CMP_F64:
         o << "  keep &= ((double)r.c" << p.column << " " << op_sym(p.op) << " P.plf[" << k
@@ -523,14 +1073,16 @@ std::string generate(const Spec& s) {
     }
   }
   emit_program(o, s);
-  o << "  i64 sl = 0;\n";
+  // slots < 2^20: the mixed-radix slot in 32-bit arithmetic
+  o << "  int sl = 0;\n";
   for (size_t j = 0; j < s.keys.size(); ++j)
-    o << "  sl = sl * " << s.keys[j].span << "LL + (i64)((u64)v" << s.keys[j].value
-      << " - (u64)P.klo[" << j << "]);\n";
-  o << "  slot = (int)sl;\n";
+    o << "  sl = sl * " << s.keys[j].span << " + (int)((unsigned)v" << s.keys[j].value
+      << " - (unsigned)P.klo[" << j << "]);\n";
+  o << "  slot = sl;\n";
   for (size_t a = 0; a < s.fvals.size(); ++a) o << "  f[" << a << "] = (double)v" << s.fvals[a] << ";\n";
   for (size_t a = 0; a < s.ivals.size(); ++a) o << "  q[" << a << "] = (i64)v" << s.ivals[a] << ";\n";
   o << "  return keep;\n}\n";
+  if (s.accmode == 1) emit_smem_acc(o, s);
   // projection
   o << "__device__ __forceinline__ void tdp_project(const TdpRow& r, const TdpParams& P, i64 "
        "pos) {\n";
@@ -611,6 +1163,10 @@ std::string signature(const Spec& s) {
   for (const auto& a : s.aggs) put(((long long)a.kind << 32) | (unsigned)a.value);
   put((long long)s.outs.size());
   for (int o : s.outs) put(o);
+  put((long long)s.prog.size());  // incl. the integer restatement of decimal sums
+  put(s.pwords);
+  for (const auto& f : s.fields)
+    put(((long long)(f.acc + 1) << 32) | ((long long)f.word << 16) | (f.off << 8) | f.bits);
   return k;
 }
 
@@ -686,12 +1242,22 @@ void fill_params(HostParams& hp, const Spec& s, const tdp_column* cols, int ncol
   for (size_t k = 0; k < s.preds.size(); ++k) {
     hp.pli[k] = s.preds[k].lit_i;
     hp.plf[k] = s.preds[k].lit_f;
+    const tdp_predicate& p = s.preds[k];
+    if (p.cmp == TDP_CMP_I64 && p.column >= 0 && p.column < (int)s.col_dtype.size() &&
+        narrow_cmp(s.col_dtype[p.column])) {
+      // every comparison of a value in [lo, hi] with L equals the comparison
+      // with clamp(L, lo - 1, hi + 1), which fits 32 bits
+      const Range t = type_range(s.col_dtype[p.column]);
+      hp.pli[k] = p.lit_i < t.lo - 1 ? t.lo - 1 : (p.lit_i > t.hi + 1 ? t.hi + 1 : p.lit_i);
+    }
   }
   for (size_t j = 0; j < s.prog.size(); ++j) {
     hp.imi[j] = s.prog[j].imm_i;
     hp.imf[j] = s.prog[j].imm_f;
   }
   for (size_t j = 0; j < s.keys.size(); ++j) hp.klo[j] = s.keys[j].lo;
+  for (const Field& f : s.fields)
+    if (f.acc >= 0) hp.plo[f.acc] = f.lo;
 }
 
 // ---------------------------------------------------------------------------
@@ -704,6 +1270,7 @@ struct AggMap {
   int pad;
   int kind[32];
   int acc[32];
+  double scale[32];  // kAggSumDec: the sum is exact integers / scale
 };
 
 // One warp per output item; lanes stride over the partial rows in a fixed
@@ -718,6 +1285,7 @@ __device__ __forceinline__ void reduce_items(const u64* __restrict__ part, int r
   for (i64 it = first_warp; it < items; it += nwarps) {
     i64 cell;
     bool is_f = false;
+    double dec = 0.0;  // > 0: exact integer cells of a decimal sum
     if (it < slots) {
       cell = it;
     } else {
@@ -730,6 +1298,7 @@ __device__ __forceinline__ void reduce_items(const u64* __restrict__ part, int r
         is_f = true;
       } else {
         cell = (i64)slots * (1 + m.nf + m.acc[a]) + g;
+        if (m.kind[a] == kAggSumDec) dec = m.scale[a];
       }
     }
     // partial rows are cell-major: part[cell * rows + r] (coalesced per warp);
@@ -749,6 +1318,25 @@ __device__ __forceinline__ void reduce_items(const u64* __restrict__ part, int r
       for (; r < rows; r += 32) v0 += __longlong_as_double((i64)src[r]);
       double v = warp_sum((v0 + v1) + (v2 + v3));
       bits = (u64)__double_as_longlong(v);
+    } else if (dec > 0.0) {
+      // per-CTA partials are exact int64; their sum is kept in 128 bits and
+      // rounded once: double(sum) / scale
+      __int128 v = 0;
+      for (int r = lane; r < rows; r += 32) v += (__int128)(i64)src[r];
+      u64 lo = (u64)v;
+      i64 hi = (i64)(v >> 64);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const u64 tlo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const i64 thi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const u64 nlo = lo + tlo;
+        hi = hi + thi + (nlo < lo ? 1 : 0);
+        lo = nlo;
+      }
+      const bool fits = hi == ((i64)lo >> 63);
+      const double sum = fits ? (double)(i64)lo
+                              : fma((double)hi, 18446744073709551616.0, (double)lo);
+      bits = (u64)__double_as_longlong(sum / dec);
     } else {
       u64 v = 0;
       for (int r = lane; r < rows; r += 32) v += src[r];
@@ -815,7 +1403,8 @@ __device__ __forceinline__ void finalize_block(const i64* __restrict__ counts,
         u64 v = raw;
         if ((avg_mask >> a) & 1ull) {
           double sum;
-          if (m.kind[a] == TDP_AGG_SUM_F64) sum = __longlong_as_double((i64)raw);
+          if (m.kind[a] == TDP_AGG_SUM_F64 || m.kind[a] == kAggSumDec)
+            sum = __longlong_as_double((i64)raw);
           else sum = (double)(i64)raw;
           v = (u64)__double_as_longlong(sum / (double)c);
         }
@@ -931,6 +1520,7 @@ AggMap make_map(const Spec& s) {
   for (int a = 0; a < m.naggs; ++a) {
     m.kind[a] = s.aggs[a].kind;
     m.acc[a] = s.agg_acc[a];
+    m.scale[a] = s.aggs[a].kind == kAggSumDec ? s.iscale[s.agg_acc[a]] : 0.0;
   }
   return m;
 }

@@ -26,7 +26,6 @@
 //                 are bitwise deterministic run to run.
 //   TDP_REGACC=0  atomics straight into zeroed global accumulators.
 
-#define TDP_CELLS (TDP_G * (1 + TDP_NF + TDP_NI))
 #define TDP_NFA (TDP_NF > 0 ? TDP_NF : 1)
 #define TDP_NIA (TDP_NI > 0 ? TDP_NI : 1)
 
@@ -40,7 +39,8 @@ __device__ __forceinline__ T tdp_warp_sum(T v) {
 // TDP_ACCMODE 0: registers, 1: per-thread columns in shared memory, 2: global atomics
 #define TDP_REGACC (TDP_ACCMODE == 0)
 #define TDP_SMEMACC (TDP_ACCMODE == 1)
-#define TDP_ACC_THREADS 256  // shared-memory accumulator columns (one per thread)
+// TDP_CELLS, TDP_ACC_THREADS (shared-memory accumulator columns, one per
+// thread) are defined by the generated prefix
 
 struct TdpAcc {
 #if TDP_REGACC
@@ -51,14 +51,11 @@ struct TdpAcc {
 #if TDP_SMEMACC
   // cell-major columns: a thread touches only its own column, so updates need
   // no atomics and consecutive threads hit consecutive words (conflict-free).
-  // Counts are 32-bit ([TDP_G][TDP_ACC_THREADS] u32: a thread counts at most
-  // its own rows), the value cells 64-bit after them
-  // ([TDP_G * (TDP_NF + TDP_NI)][TDP_ACC_THREADS] u64): 4 bytes less
-  // shared-memory traffic per row, the pipe narrow rows are bound by.
+  // Layout and per-row updates are generated (tdp_smem_add / tdp_smem_flush):
+  // the row count and bounded integer sums share packed 64-bit words.
   u64* sm;
+  u64* mine;  // sm + this thread's column
   int col;
-  __device__ __forceinline__ unsigned* counts() const { return reinterpret_cast<unsigned*>(sm); }
-  __device__ __forceinline__ u64* values() const { return sm + (size_t)TDP_G * (TDP_ACC_THREADS / 2); }
 #endif
   __device__ __forceinline__ void zero(u64* smem_acc) {
 #if TDP_REGACC
@@ -74,10 +71,9 @@ struct TdpAcc {
 #if TDP_SMEMACC
     sm = smem_acc;
     col = threadIdx.x;
-    if (col < TDP_ACC_THREADS) {
-      for (int c = 0; c < TDP_G; ++c) counts()[c * TDP_ACC_THREADS + col] = 0u;
-      for (int c = 0; c < TDP_CELLS - TDP_G; ++c) values()[c * TDP_ACC_THREADS + col] = 0;
-    }
+    mine = sm + col;
+    if (col < TDP_ACC_THREADS)
+      for (int c = 0; c < TDP_SM_ROWS; ++c) sm[c * TDP_ACC_THREADS + col] = 0;
 #endif
   }
   __device__ __forceinline__ void add(const TdpParams& P, bool keep, int slot, const double* f,
@@ -93,17 +89,7 @@ struct TdpAcc {
       for (int a = 0; a < TDP_NI; ++a) ai[s][a] = (i64)((u64)ai[s][a] + (hit ? (u64)q[a] : 0ull));
     }
 #elif TDP_SMEMACC
-    if (keep) {
-      counts()[(size_t)slot * TDP_ACC_THREADS + col] += 1u;
-      u64* p = values() + (size_t)slot * TDP_ACC_THREADS + col;
-#pragma unroll
-      for (int a = 0; a < TDP_NF; ++a) {
-        double* d = reinterpret_cast<double*>(p + (size_t)TDP_G * a * TDP_ACC_THREADS);
-        *d += f[a];
-      }
-#pragma unroll
-      for (int a = 0; a < TDP_NI; ++a) p[(size_t)TDP_G * (TDP_NF + a) * TDP_ACC_THREADS] += (u64)q[a];
-    }
+    tdp_smem_add(mine, keep ? slot : TDP_G, f, q, P);  // branch-free: rejects -> slot G
 #else
     if (keep) {
       atomicAdd(reinterpret_cast<u64*>(P.acc) + slot, 1ull);
@@ -162,32 +148,13 @@ struct TdpAcc {
     }
 #elif TDP_SMEMACC
     __syncthreads();
-    u64* out = reinterpret_cast<u64*>(P.acc) + blockIdx.x;  // cell-major, as above
-    for (int c = threadIdx.x; c < TDP_CELLS; c += blockDim.x) {
-      if (c < TDP_G) {
-        const unsigned* row = counts() + (size_t)c * TDP_ACC_THREADS;
-        u64 v = 0;
-        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];
-        out[(i64)c * gridDim.x] = v;
-        continue;
-      }
-      const u64* row = values() + (size_t)(c - TDP_G) * TDP_ACC_THREADS;
-      if (c < TDP_G * (1 + TDP_NF)) {
-        double v = 0.0;
-        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += __longlong_as_double((i64)row[t]);
-        out[(i64)c * gridDim.x] = (u64)__double_as_longlong(v);
-      } else {
-        u64 v = 0;
-        for (int t = 0; t < TDP_ACC_THREADS; ++t) v += row[t];
-        out[(i64)c * gridDim.x] = v;
-      }
-    }
+    tdp_smem_flush(sm, P);
 #endif
   }
 };
 
 #if TDP_SMEMACC
-#define TDP_ACC_SMEM_BYTES (TDP_CELLS * TDP_ACC_THREADS * 8)
+#define TDP_ACC_SMEM_BYTES (TDP_SM_ROWS * TDP_ACC_THREADS * 8)
 #else
 #define TDP_ACC_SMEM_BYTES 0
 #endif

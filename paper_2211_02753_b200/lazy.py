@@ -189,6 +189,20 @@ class Expr:
 NARROW_INTS = ("int32", "int16", "int8", "uint8")
 
 
+def set_value_range(t: torch.Tensor, lo: int, hi: int) -> None:
+    """Record that every value of the (immutable, narrow integer) stored column
+    ``t`` lies in [lo, hi] -- measured at ingestion by compact storage.  The
+    fused scan uses it to bound exact integer sums (TDP_OP_LOAD range hint)."""
+    t._tdp_range = (int(lo), int(hi))
+
+
+def value_range(t: torch.Tensor) -> Optional[tuple[int, int]]:
+    r = getattr(t, "_tdp_range", None)
+    if r is None or t.dtype not in (torch.int32, torch.int16, torch.int8, torch.uint8):
+        return None
+    return r
+
+
 def compact_source(e: Expr) -> Optional[tuple[torch.Tensor, int]]:
     """(stored narrow column, decimal divisor or 0) when ``e`` decodes a
     compact column (compact.py): ``cast(col)`` to int64, or
@@ -391,8 +405,12 @@ class Program:
             load_dt = {"int64": "int64", "bool": "int64", "float64": "float64",
                        "float32": "float32", "int32": "int64", "int16": "int64",
                        "int8": "int64", "uint8": "int64"}[e.dtype]
-            v = self._emit(("load", c), nat.Instr(nat.OP_LOAD, _DT[load_dt], c, 0, 0, 0.0))
-            return v
+            rng = value_range(e.col) if load_dt == "int64" else None
+            if rng is not None:  # promised [lo, hi]: lets sums run as exact packed integers
+                ins = nat.Instr(nat.OP_LOAD, _DT[load_dt], c, 1, rng[0], float(rng[1]))
+            else:
+                ins = nat.Instr(nat.OP_LOAD, _DT[load_dt], c, 0, 0, 0.0)
+            return self._emit(("load", c), ins)
         if e.op == "const":
             dt = e.dtype if e.dtype in _DT else "int64"
             if dt == "int64":

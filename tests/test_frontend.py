@@ -186,6 +186,72 @@ def test_pipeline_codegen_compiles_q1_program_with_nvrtc():
     assert src.count("P.imf[") == 2  # once in tdp_eval, once in tdp_project
 
 
+def test_pipeline_codegen_packs_exact_decimal_sums_of_compact_q1():
+    """On compact storage (int32 cents, int8 hundredths, measured value ranges)
+    Q1's five float sums are restated as exact scaled-integer programs
+    (c*(100-d), c*(100-d)*(100+t)) and, with the row count, packed into three
+    64-bit shared-memory words per thread and group (pipeline.cu
+    convert_decimal_sums / pack_fields)."""
+    import ctypes
+
+    import torch
+
+    from paper_2211_02753_b200.compact import decode_expr
+    from paper_2211_02753_b200.lazy import Expr, Pred, Program, Selection, set_value_range
+
+    n = 60_000_000  # SF10: 2048 rows per thread at most -> 12-bit count field
+
+    def col(dt, lo, hi, div):
+        x = torch.empty(n, dtype=dt)
+        set_value_range(x, lo, hi)
+        return decode_expr(x, div)
+
+    rf, ls = (decode_expr(torch.empty(n, dtype=torch.uint8), 0) for _ in range(2))
+    q, p = col(torch.int8, 1, 50, 1), col(torch.int32, 90000, 10494950, 100)
+    d, tx = col(torch.int8, 0, 10, 100), col(torch.int8, 0, 8, 100)
+    one = Expr.const(1.0, "float64")
+    dp = Expr("mul", "float64", (p, Expr("sub", "float64", (one, d))))
+    ch = Expr("mul", "float64", (dp, Expr("add", "float64", (one, tx))))
+    prog = Program()
+    sel = Selection(n, [Pred(torch.empty(n, dtype=torch.int16), "<=", _native.CMP_I64, 10471, 0.0)],
+                    torch.device("cpu"))
+    keys = [_native.Key(prog.value(rf), 0, 0, 3), _native.Key(prog.value(ls), 0, 0, 2)]
+    aggs = [_native.Agg(_native.AGG_SUM_F64, prog.value(e)) for e in (q, p, dp, ch, d)]
+    aggs.append(_native.Agg(_native.AGG_COUNT, 0))
+    preds, npreds = prog.predicates(sel)
+    buf = ctypes.create_string_buffer(1 << 17)
+    rc = _native.load().tdp_pipeline_codegen(
+        _native.columns(prog.cols, False), len(prog.cols), n, preds, npreds, prog.native_instrs(),
+        len(prog.instrs), _native.struct_array(_native.Key, keys), 2,
+        _native.struct_array(_native.Agg, aggs), len(aggs), None, 0, 1, buf, len(buf))
+    assert rc > 0, _native.last_error()
+    src = buf.value.decode()
+    assert "#define TDP_NF 0" in src and "#define TDP_NI 5" in src  # all five sums exact
+    assert "#define TDP_NW 3" in src and "#define TDP_SM_ROWS 21" in src  # 3 x (6 + reject slot)
+    eval_body = src[src.index("bool tdp_eval"):src.index("tdp_smem_add")]
+    assert "tdp_decimal" not in eval_body.split("slot = sl;")[1]  # q[] are integers
+    add = src[src.index("void tdp_smem_add"):src.index("void tdp_smem_flush")]
+    assert add.count("sm[(") == 3  # three packed words per row
+    # without measured ranges (int32/int8 type ranges) a CTA's sum of
+    # c*(100-d)*(100+t) could exceed int64: that sum stays a float64 cell
+    for t in prog.cols:
+        if hasattr(t, "_tdp_range"):
+            del t._tdp_range
+    prog2 = Program()
+    keys = [_native.Key(prog2.value(rf), 0, 0, 3), _native.Key(prog2.value(ls), 0, 0, 2)]
+    aggs = [_native.Agg(_native.AGG_SUM_F64, prog2.value(e)) for e in (q, p, dp, ch, d)]
+    aggs.append(_native.Agg(_native.AGG_COUNT, 0))
+    preds, npreds = prog2.predicates(sel)
+    rc = _native.load().tdp_pipeline_codegen(
+        _native.columns(prog2.cols, False), len(prog2.cols), n, preds, npreds,
+        prog2.native_instrs(), len(prog2.instrs), _native.struct_array(_native.Key, keys), 2,
+        _native.struct_array(_native.Agg, aggs), len(aggs), None, 0, 0, buf, len(buf))
+    assert rc > 0, _native.last_error()
+    src2 = buf.value.decode()
+    assert re.findall(r"#define TDP_(?:NF|NI|NW) \d+", src2) == [
+        "#define TDP_NF 1", "#define TDP_NI 4", "#define TDP_NW 3"]
+
+
 def test_trainable_order_by_is_rejected_without_soft_sort():
     """tq/compiler.py:464-475: Sort / Limit in trainable mode raise CompileError
     unless the soft-sort extension is asked for (CompileConfig.soft_sort_tau)."""

@@ -131,3 +131,85 @@ def test_table_from_stored_round_trip():
     again = cp.table_from_stored(narrow, stored)
     for a, b in zip(narrow.columns, again.columns):
         np.testing.assert_array_equal(a.values.numpy(), b.values.numpy())
+
+
+def _exact_q1_floats(arrays):
+    """Per (rf, ls) group (ascending) the exact rational Q1 float aggregates over
+    the stored integers, rounded once (fractions): the result the exact
+    decimal path must reproduce to within the final rounding."""
+    from fractions import Fraction
+
+    keep = arrays["l_shipdate"] <= 10471
+    rf, ls = arrays["l_returnflag"][keep], arrays["l_linestatus"][keep]
+    q = np.rint(arrays["l_quantity"][keep]).astype(np.int64)
+    c = np.rint(arrays["l_extendedprice"][keep] * 100).astype(np.int64)
+    d = np.rint(arrays["l_discount"][keep] * 100).astype(np.int64)
+    t = np.rint(arrays["l_tax"][keep] * 100).astype(np.int64)
+    dp = c * (100 - d)                  # |.| < 2^39: exact in int64
+    ch = dp * (100 + t)                 # |.| < 2^47
+    out = {k: [] for k in ("sum_qty", "sum_price", "sum_disc_price", "sum_charge", "avg_qty",
+                           "avg_price", "avg_disc", "count")}
+    for g in sorted(set(zip(rf.tolist(), ls.tolist()))):
+        m = (rf == g[0]) & (ls == g[1])
+        n = int(m.sum())
+        sq, sp, sd = int(q[m].sum()), int(c[m].sum()), int(d[m].sum())
+        sdp, sch = sum(dp[m].tolist()), sum(ch[m].tolist())
+        out["sum_qty"].append(float(sq))
+        out["sum_price"].append(float(Fraction(sp, 100)))
+        out["sum_disc_price"].append(float(Fraction(sdp, 10_000)))
+        out["sum_charge"].append(float(Fraction(sch, 1_000_000)))
+        out["avg_qty"].append(float(Fraction(sq, n)))
+        out["avg_price"].append(float(Fraction(sp, 100 * n)))
+        out["avg_disc"].append(float(Fraction(sd, 100 * n)))
+        out["count"].append(n)
+    return {k: np.asarray(v) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("rows", [4093, 300_007, 2_000_003])
+def test_q1_compact_decimal_sums_exact_at_type_extremes(rows):
+    """Compact decimals at the extremes of their stored types (int32 cents
+    incl. INT32_MIN/MAX, negative int8 discounts/taxes/quantities): the fused
+    scan sums them as exact scaled integers in packed per-thread words
+    (pipeline.cu convert_decimal_sums / pack_fields), so every float aggregate
+    equals the exactly rounded rational sum -- no float reassociation error
+    even under cancellation."""
+    rng = np.random.default_rng(rows)
+    arrays = wl.lineitem_arrays(0.01, seed=17, rows=rows)
+    c = rng.integers(-2**31, 2**31, rows, dtype=np.int64)
+    c[:4] = [-2**31, 2**31 - 1, -2**31, 2**31 - 1]
+    arrays["l_extendedprice"] = c / 100.0
+    arrays["l_discount"] = rng.integers(-128, 128, rows) / 100.0
+    arrays["l_tax"] = rng.integers(-128, 128, rows) / 100.0
+    arrays["l_quantity"] = rng.integers(-128, 128, rows).astype(np.float64)
+    cw, cn, narrow = _catalogs(arrays)
+    specs = dict(zip(narrow.schema.names, cp.specs_of(narrow)))
+    assert specs["l_extendedprice"] == cp.CompactSpec(torch.int32, 100)
+    assert specs["l_discount"] == cp.CompactSpec(torch.int8, 100)
+    assert specs["l_quantity"] == cp.CompactSpec(torch.int8, 1)
+    res = wl.compile_sql(wl.Q1_SQL, cn, wl.q1_registry()).run(cn)
+    got = {n: c.values.numpy() for n, c in zip(res.schema.names, res.columns)}
+    exp = otpch.q1(arrays)  # group keys and counts (bit-exact)
+    np.testing.assert_array_equal(got["rf"], exp["rf"])
+    np.testing.assert_array_equal(got["ls"], exp["ls"])
+    np.testing.assert_array_equal(got["count"], exp["count"])
+    exact = _exact_q1_floats(arrays)
+    for k in ("sum_qty", "sum_price", "sum_disc_price", "sum_charge", "avg_qty", "avg_price",
+              "avg_disc"):
+        # two roundings at most (the int sum -> double, then / scale or / count)
+        np.testing.assert_allclose(got[k], exact[k], rtol=5e-16, atol=0, err_msg=k)
+
+
+@pytest.mark.parametrize("rows", [3001, 700_001])
+def test_q1_compact_bitwise_repeatable(rows):
+    """Exact integer accumulation is order-free: two runs are bitwise equal,
+    and equal the float64 reference within its own rounding (rtol 1e-12)."""
+    arrays = wl.lineitem_arrays(0.01, seed=23, rows=rows)
+    cw, cn, _ = _catalogs(arrays)
+    q = wl.compile_sql(wl.Q1_SQL, cn, wl.q1_registry())
+    a, b = q.run(cn), q.run(cn)
+    for x, y in zip(a.columns, b.columns):
+        np.testing.assert_array_equal(x.values.numpy().view(np.uint8), y.values.numpy().view(np.uint8))
+    exact = _exact_q1_floats(arrays)
+    got = {n: c.values.numpy() for n, c in zip(a.schema.names, a.columns)}
+    for k in exact:
+        np.testing.assert_allclose(got[k], exact[k], rtol=5e-16, atol=0, err_msg=k)

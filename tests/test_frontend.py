@@ -231,7 +231,7 @@ def test_pipeline_codegen_packs_exact_decimal_sums_of_compact_q1():
     eval_body = src[src.index("bool tdp_eval"):src.index("tdp_smem_add")]
     assert "tdp_decimal" not in eval_body.split("slot = sl;")[1]  # q[] are integers
     add = src[src.index("void tdp_smem_add"):src.index("void tdp_smem_flush")]
-    assert add.count("sm[(") == 3  # three packed words per row
+    assert add.count(" * TDP_ACC_THREADS] += ") == 3  # three packed words per row
     # without measured ranges (int32/int8 type ranges) a CTA's sum of
     # c*(100-d)*(100+t) could exceed int64: that sum stays a float64 cell
     for t in prog.cols:

@@ -474,6 +474,25 @@ int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_pr
                         int64_t key_range, int32_t need_rows, int64_t* out_probe_idx,
                         int64_t* out_build_idx, void* ws, size_t ws_bytes, void* stream);
 
+/* Sort / searchsorted equi-join (north_star's "radix sort + searchsorted
+ * probing"): stable LSD radix sort of the build key images
+ * with their row ids, then each probe row passing the probe predicates
+ * searches the sorted keys (a <= 4096-fence top level in shared memory, then
+ * the fence interval in global memory).  Same result contract as
+ * tdp_join_prepare_ex / tdp_join_emit: *out_count (device int64) pairs,
+ * ordered by probe row then ascending build row; any keys (repeats on both
+ * sides, INT64 extremes).  The planner prefers the dense-range / hash joins
+ * (one lookup per probe row, measured faster: DESIGN.md §3.3); this form is
+ * selected with TDP_JOIN_ALGO=sort / kernels.JOIN_ALGORITHM.                */
+size_t tdp_join_sorted_workspace(int64_t n_build, int64_t n_probe);
+int tdp_join_sorted_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                            int64_t n_probe, const tdp_column* pcols, int32_t npcols,
+                            const tdp_predicate* ppreds, int32_t nppreds, int64_t* out_count,
+                            void* ws, size_t ws_bytes, void* stream);
+int tdp_join_sorted_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
+                         int64_t* out_probe_idx, int64_t* out_build_idx, void* ws,
+                         size_t ws_bytes, void* stream);
+
 /* One-pass LLP step (tq/kernels.py:190-229 soft_groupby over
  * pe_encode(Linear(X)), its tape backward tq/tensor.py:474, :364-365,
  * :515-527): for k = 2 classes and one one-hot bag key, the forward writes

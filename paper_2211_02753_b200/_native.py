@@ -182,6 +182,12 @@ _SIGNATURES = {
                                       c_void_p, c_void_p]),
     "tdp_join_dense_emit": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32,
                                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_join_sorted_workspace": (c_size_t, [c_int64, c_int64]),
+    "tdp_join_sorted_prepare": (c_int, [c_void_p, c_int64, c_void_p, c_int64, POINTER(Column),
+                                        c_int32, POINTER(Predicate), c_int32, c_void_p, c_void_p,
+                                        c_size_t, c_void_p]),
+    "tdp_join_sorted_emit": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                     c_size_t, c_void_p]),
     "tdp_softmax_fwd": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
     "tdp_softmax_bwd": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p,
                                 c_void_p]),

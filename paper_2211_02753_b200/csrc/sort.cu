@@ -2193,3 +2193,274 @@ int tdp_groupby_bitmap_emit(int64_t n, int64_t lo, int64_t key_range, const int3
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// sort / searchsorted equi-join (the algorithm north_star names; the default
+// planner prefers the dense-range and hash joins, which read the probe side
+// once with one table lookup per row -- tdp_join_sorted_* is kept as the
+// measured alternative and for callers that want it).
+//   prepare: stable LSD radix sort of the build key images with their row ids
+//            (ascending row within equal keys), then every probe key searches
+//            the sorted images: a top level of <= kTopFences fence keys held
+//            in shared memory by persistent CTAs, then a binary search of the
+//            fence interval in global memory (L2-resident for build sides up
+//            to ~10^7 keys; sorted probe columns hit L1).  Match bits + per
+//            word pair counts per 2048-row tile, as the hash join's.
+//   emit:    matched rows search again and write (probe row, build row)
+//            pairs: by probe row, then ascending build row.
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+constexpr int kTopFences = 4096;
+
+struct SortedJoin {
+  const u64* sk;     // sorted build key images [m]
+  const i64* order;  // build row of each sorted key [m]
+  i64 m;
+  i64 stride;        // top[j] = sk[j * stride], j < ntop
+  int ntop;
+};
+
+__device__ __forceinline__ void sj_load_top(const SortedJoin& sj, u64* top) {
+  for (int j = threadIdx.x; j < sj.ntop; j += blockDim.x) top[j] = __ldg(sj.sk + (i64)j * sj.stride);
+  __syncthreads();
+}
+
+// First index of sk with image >= k (m if none).
+__device__ __forceinline__ i64 sj_lower(const SortedJoin& sj, const u64* top, u64 k) {
+  int a = 0, b = sj.ntop;  // first fence >= k
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (top[mid] < k) a = mid + 1;
+    else b = mid;
+  }
+  // sk[(a-1)*stride] < k <= sk[a*stride]: the answer lies in ((a-1)*stride, a*stride]
+  i64 lo = a > 0 ? (i64)(a - 1) * sj.stride + 1 : 0;
+  i64 hi = (i64)a * sj.stride;
+  if (hi > sj.m) hi = sj.m;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (__ldg(sj.sk + mid) < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Number of build keys equal to image k; *first = their first sorted index.
+__device__ __forceinline__ i64 sj_count(const SortedJoin& sj, const u64* top, u64 k, i64* first) {
+  const i64 lo = sj_lower(sj, top, k);
+  *first = lo;
+  if (lo >= sj.m || __ldg(sj.sk + lo) != k) return 0;
+  if (lo + 1 >= sj.m || __ldg(sj.sk + lo + 1) != k) return 1;
+  // a run: galloping, then bisection for the first image > k
+  i64 a = lo + 1, step = 2;
+  while (a + step < sj.m && __ldg(sj.sk + a + step) == k) {
+    a += step;
+    step <<= 1;
+  }
+  i64 b = a + step < sj.m ? a + step : sj.m;  // sk[a] == k, sk[b] > k or b == m
+  while (a + 1 < b) {
+    const i64 mid = (a + b) >> 1;
+    if (__ldg(sj.sk + mid) == k) a = mid;
+    else b = mid;
+  }
+  return b - lo;
+}
+
+// tile_counts zeroed; persistent CTAs walk the 2048-row tiles.
+template <bool kFiltered>
+__global__ void __launch_bounds__(kJoinThreads)
+    sorted_count_kernel(SortedJoin sj, const i64* __restrict__ probe, i64 np, i64 tiles,
+                        PredSet ps, unsigned* __restrict__ match_bits,
+                        i64* __restrict__ word_counts, i64* __restrict__ tile_counts) {
+  __shared__ u64 top[kTopFences];
+  sj_load_top(sj, top);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    bool act[kJoinPer];
+    i64 row[kJoinPer];
+    u64 key[kJoinPer];
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      row[k] = join_row(tile, k);
+      act[k] = row[k] < np;
+      key[k] = act[k] ? image_i64(__ldcs(probe + row[k]), 0) : 0;
+    }
+    if (kFiltered) eval_batch<kJoinPer>(ps, row, act);
+    i64 local = 0;
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      i64 first, c = act[k] ? sj_count(sj, top, key[k], &first) : 0;
+      const unsigned word = __ballot_sync(0xffffffffu, c > 0);
+      const i64 wc = word ? warp_sum(c) : 0;
+      if (lane == 0) {
+        match_bits[tile * kJoinWords + k * kJoinWarps + warp] = word;
+        word_counts[tile * kJoinWords + k * kJoinWarps + warp] = wc;
+      }
+      local += wc;
+    }
+    if (lane == 0 && local != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(tile_counts + tile), (unsigned long long)local);
+  }
+}
+
+__global__ void __launch_bounds__(kJoinThreads)
+    sorted_emit_kernel(SortedJoin sj, const i64* __restrict__ probe, i64 tiles,
+                       const unsigned* __restrict__ match_bits,
+                       const i64* __restrict__ word_counts, const i64* __restrict__ tile_counts,
+                       const i64* __restrict__ tile_offsets, i64* __restrict__ out_probe,
+                       i64* __restrict__ out_build) {
+  __shared__ u64 top[kTopFences];
+  sj_load_top(sj, top);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (tile_counts[tile] == 0) continue;  // CTA-uniform
+    const WordPrefix wp(word_counts + tile * kJoinWords, lane);
+    const i64 base = tile_offsets[tile];
+    unsigned bits[kJoinPer];
+    i64 s[kJoinPer], c[kJoinPer];
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) bits[k] = match_bits[tile * kJoinWords + k * kJoinWarps + warp];
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      s[k] = 0;
+      c[k] = 0;
+      if ((bits[k] >> lane) & 1u)
+        c[k] = sj_count(sj, top, image_i64(__ldg(probe + join_row(tile, k)), 0), &s[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kJoinPer; ++k) {
+      if (bits[k] == 0u) continue;  // warp-uniform
+      const i64 word_off = base + wp.word_offset(k * kJoinWarps + warp);
+      i64 ci = c[k];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const i64 t = __shfl_up_sync(0xffffffffu, ci, o);
+        if (lane >= o) ci += t;
+      }
+      const i64 pos = word_off + ci - c[k];
+      const i64 i = join_row(tile, k);
+      for (i64 m = 0; m < c[k]; ++m) {
+        out_probe[pos + m] = i;
+        out_build[pos + m] = __ldg(sj.order + s[k] + m);
+      }
+    }
+  }
+}
+
+struct SortedWs {
+  SortBuffers sb;
+  unsigned* match_bits;
+  i64* word_counts;
+  i64* tile_counts;
+  i64* tile_offsets;
+  void* scan_ws;
+  size_t scan_bytes;
+};
+
+size_t sorted_ws_bytes(i64 nb, i64 np) {
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  return sort_ws_bytes(nb) + align256((size_t)tiles * kJoinWords * 4) +
+         align256((size_t)tiles * kJoinWords * 8) + 2 * align256((size_t)tiles * 8) +
+         exclusive_scan_workspace(tiles) + 2048;
+}
+
+SortedWs carve_sorted(void* ws, i64 nb, i64 np) {
+  SortedWs j;
+  j.sb = carve(ws, nb);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws) + sort_ws_bytes(nb);
+  const i64 tiles = ceil_div(np > 0 ? np : 1, kJoinTile);
+  j.match_bits = (unsigned*)p;
+  p += align256((size_t)tiles * kJoinWords * 4);
+  j.word_counts = (i64*)p;
+  p += align256((size_t)tiles * kJoinWords * 8);
+  j.tile_counts = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  j.tile_offsets = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  j.scan_ws = p;
+  j.scan_bytes = exclusive_scan_workspace(tiles) + 1024;
+  return j;
+}
+
+SortedJoin sorted_view(const SortedWs& j, i64 nb) {
+  SortedJoin sj;
+  sj.sk = j.sb.k0;
+  sj.order = j.sb.i0;
+  sj.m = nb;
+  sj.stride = ceil_div(nb > 0 ? nb : 1, kTopFences);
+  sj.ntop = (int)ceil_div(nb, sj.stride);
+  return sj;
+}
+
+int persistent_grid(i64 tiles) {
+  const i64 g = (i64)sm_count() * 4;
+  return (int)(tiles < g ? (tiles > 0 ? tiles : 1) : g);
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_join_sorted_workspace(int64_t n_build, int64_t n_probe) {
+  return sorted_ws_bytes(n_build, n_probe);
+}
+
+int tdp_join_sorted_prepare(const int64_t* build_keys, int64_t n_build, const int64_t* probe_keys,
+                            int64_t n_probe, const tdp_column* pcols, int32_t npcols,
+                            const tdp_predicate* ppreds, int32_t nppreds, int64_t* out_count,
+                            void* ws, size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n_build >= 0 && n_probe >= 0, "negative join sizes");
+  TDP_REQUIRE(out_count != nullptr, "null join count output");
+  TDP_REQUIRE(ws_bytes >= sorted_ws_bytes(n_build, n_probe), "sorted join workspace too small");
+  PredSet pps;
+  int rc = make_predset(pcols, npcols, ppreds, nppreds, n_probe, &pps);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  SortedWs j = carve_sorted(ws, n_build, n_probe);
+  TDP_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(i64), st));
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
+  make_keys_kernel<<<stream_grid(n_build, 256 * 8, 8), 256, 0, st>>>(build_keys, TDP_I64, 0,
+                                                                     n_build, j.sb.k0, j.sb.i0);
+  TDP_LAUNCH_CHECK("make_keys_kernel");
+  u64* sk;
+  i64* order;
+  rc = radix_sort(j.sb, n_build, st, &sk, &order);
+  if (rc) return rc;
+  if (sk != j.sb.k0) {  // keep the sorted build in k0 / i0 for tdp_join_sorted_emit
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.k0, sk, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+    TDP_CUDA_TRY(cudaMemcpyAsync(j.sb.i0, order, (size_t)n_build * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
+  const SortedJoin sj = sorted_view(j, n_build);
+  const int grid = persistent_grid(tiles);
+  if (pps.npreds > 0)
+    sorted_count_kernel<true><<<grid, kJoinThreads, 0, st>>>(
+        sj, probe_keys, n_probe, tiles, pps, j.match_bits, j.word_counts, j.tile_counts);
+  else
+    sorted_count_kernel<false><<<grid, kJoinThreads, 0, st>>>(
+        sj, probe_keys, n_probe, tiles, pps, j.match_bits, j.word_counts, j.tile_counts);
+  TDP_LAUNCH_CHECK("sorted_count_kernel");
+  return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
+                            j.scan_bytes, st);
+}
+
+int tdp_join_sorted_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_probe,
+                         int64_t* out_probe_idx, int64_t* out_build_idx, void* ws,
+                         size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(ws_bytes >= sorted_ws_bytes(n_build, n_probe), "sorted join workspace too small");
+  if (n_build == 0 || n_probe == 0) return TDP_OK;
+  cudaStream_t st = as_stream(stream);
+  SortedWs j = carve_sorted(ws, n_build, n_probe);
+  const i64 tiles = ceil_div(n_probe, kJoinTile);
+  sorted_emit_kernel<<<persistent_grid(tiles), kJoinThreads, 0, st>>>(
+      sorted_view(j, n_build), probe_keys, tiles, j.match_bits, j.word_counts, j.tile_counts,
+      j.tile_offsets, out_probe_idx, out_build_idx);
+  TDP_LAUNCH_CHECK("sorted_emit_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"

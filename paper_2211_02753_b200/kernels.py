@@ -24,6 +24,7 @@ equi_join (new)             tdp_join_prepare / tdp_join_emit
 
 from __future__ import annotations
 
+import os
 from ctypes import c_int32
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
@@ -1209,6 +1210,39 @@ def _dense_range(build_range, n_build: int) -> Optional[tuple[int, int]]:
     return lo, span
 
 
+# Equi-join algorithm: "auto" = dense-range bitmap join when the build keys'
+# range allows, else the hash join; "sort" = radix-sorted build +
+# searchsorted probe (tdp_join_sorted_*, north_star's algorithm, measured
+# slower on Q3 -- DESIGN.md §3.3).  Env TDP_JOIN_ALGO sets the default.
+JOIN_ALGORITHM = os.environ.get("TDP_JOIN_ALGO", "auto")
+
+
+def _join_sorted(pk: torch.Tensor, bk: torch.Tensor, probe_sel: Optional[Selection],
+                 build_sel: Optional[Selection], predset):
+    """Sort / searchsorted join; a filtered build side is compacted first
+    (its selection's row ids), build rows are mapped back to base rows."""
+    dev = pk.device
+    bmap = None
+    if build_sel is not None and build_sel.preds:
+        bmap = build_sel.indices()
+        bk = gather_rows_raw(bk, bmap)
+    n_probe, n_build = int(pk.numel()), int(bk.numel())
+    pc, npc, pp, npp = predset(probe_sel, n_probe, "probe")
+    ws = nat.workspace(nat.load().tdp_join_sorted_workspace(n_build, n_probe), dev)
+    cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    nat.call("tdp_join_sorted_prepare", nat.ptr(bk), n_build, nat.ptr(pk), n_probe, pc, npc, pp,
+             npp, nat.ptr(cnt), nat.ptr(ws), ws.numel(), nat.stream())
+    m = read_int(cnt)
+    pi = torch.empty(m, dtype=torch.int64, device=dev)
+    bi = torch.empty(m, dtype=torch.int64, device=dev)
+    if m:
+        nat.call("tdp_join_sorted_emit", nat.ptr(pk), n_build, n_probe, nat.ptr(pi), nat.ptr(bi),
+                 nat.ptr(ws), ws.numel(), nat.stream())
+    if bmap is not None:
+        bi = gather_rows_raw(bmap, bi)
+    return pi, bi
+
+
 def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
                  build_sel: Optional[Selection] = None,
                  build_range: Optional[tuple[int, int]] = None, need_build_rows: bool = True
@@ -1246,6 +1280,8 @@ def join_indices(probe_key, build_key, probe_sel: Optional[Selection] = None,
         nat.require_cuda(*prog.cols)
         return prog.native_columns(), len(prog.cols), preds, npreds
 
+    if JOIN_ALGORITHM == "sort":
+        return _join_sorted(pk, bk, probe_sel, build_sel, predset)
     bc, nbc, bp, nbp = predset(build_sel, n_build, "build")
     pc, npc, pp, npp = predset(probe_sel, n_probe, "probe")
     dense = _dense_range(build_range, n_build)

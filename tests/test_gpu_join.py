@@ -49,11 +49,14 @@ def _dev(a):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,probe,build", list(_cases()))
-@pytest.mark.parametrize("dense", [False, True])
-def test_join_adversarial_vs_oracle(name, probe, build, dense):
+@pytest.mark.parametrize("algo", ["hash", "dense", "sort"])
+def test_join_adversarial_vs_oracle(name, probe, build, algo, monkeypatch):
+    """hash: open-addressing + Bloom; dense: bitmap over the build key range;
+    sort: radix-sorted build + searchsorted probe (tdp_join_sorted_*)."""
     probe, build = np.asarray(probe, np.int64), np.asarray(build, np.int64)
+    monkeypatch.setattr(K, "JOIN_ALGORITHM", "sort" if algo == "sort" else "auto")
     rng = None
-    if dense and len(build):
+    if algo == "dense" and len(build):
         rng = (int(build.min()), int(build.max()))
     pairs = K.join_indices(_dev(probe), _dev(build), build_range=rng)
     epi, ebi = orc.join_inner(probe, build)
@@ -125,3 +128,64 @@ def test_q3_dense_joins_and_replay(sf):
         np.testing.assert_allclose(got[1], exp["sum_rev"], rtol=1e-9)
         np.testing.assert_allclose(got[2], exp["avg_o_orderdate"], rtol=1e-12)
         np.testing.assert_allclose(got[3], exp["avg_o_shippriority"], rtol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nb,npr,kmax", [(5000, 300_000, 4000), (1_000_003, 3_000_017, 1 << 40),
+                                          (20_000, 500_000, 50)])
+def test_sorted_join_large_vs_oracle(nb, npr, kmax):
+    """The sort / searchsorted join beyond one fence block (build > 4096
+    keys: the shared-memory top level plus the global fence interval), with
+    repeated build keys (kmax < nb: long runs) and a sorted probe column."""
+    rng = np.random.default_rng(nb)
+    build = rng.integers(-kmax, kmax, size=nb).astype(np.int64)
+    probe = np.sort(rng.integers(-kmax, kmax, size=npr).astype(np.int64))
+    pk, bk = _dev(probe), _dev(build)
+    from paper_2211_02753_b200 import _native as nat
+
+    buf = nat.workspace(nat.load().tdp_join_sorted_workspace(nb, npr), pk.device)
+    cnt = torch.empty(1, dtype=torch.int64, device=pk.device)
+    nat.call("tdp_join_sorted_prepare", nat.ptr(bk), nb, nat.ptr(pk), npr, nat.columns([]), 0,
+             nat.struct_array(nat.Predicate, []), 0, nat.ptr(cnt), nat.ptr(buf), buf.numel(),
+             nat.stream())
+    m = int(cnt.item())
+    epi, ebi = orc.join_inner(probe, build)
+    assert m == len(epi)
+    pi = torch.empty(m, dtype=torch.int64, device=pk.device)
+    bi = torch.empty(m, dtype=torch.int64, device=pk.device)
+    nat.call("tdp_join_sorted_emit", nat.ptr(pk), nb, npr, nat.ptr(pi), nat.ptr(bi), nat.ptr(buf),
+             buf.numel(), nat.stream())
+    np.testing.assert_array_equal(pi.cpu().numpy(), epi)
+    np.testing.assert_array_equal(bi.cpu().numpy(), ebi)
+
+
+@pytest.mark.gpu
+def test_sorted_join_filtered_sides_and_q3(monkeypatch):
+    """TDP_JOIN_ALGO=sort through equi_join on lazy filtered sides (build
+    compacted by its selection, probe predicates inside the count pass) and
+    through the whole Q3 pipeline, against the oracle."""
+    from oracle import tpch as otpch
+
+    monkeypatch.setattr(K, "JOIN_ALGORITHM", "sort")
+    rng = np.random.default_rng(9)
+    nb, npr = 200_000, 1_000_000
+    bkey = rng.integers(0, 150_000, size=nb).astype(np.int64)
+    bflag = rng.integers(0, 4, size=nb)
+    pkey = rng.integers(0, 160_000, size=npr).astype(np.int64)
+    pval = rng.normal(size=npr)
+    right = [tq.plain(tq.Tensor(bkey)), tq.plain(tq.Tensor(bflag))]
+    left = [tq.plain(tq.Tensor(pkey)), tq.plain(tq.Tensor(pval))]
+    out = K.equi_join(K.filter_exact(left, [(1, ">", 0.3)]),
+                      K.filter_exact(right, [(1, "<", 2)]), 0, 0)
+    keep_b, keep_p = bflag < 2, pval > 0.3
+    epi, ebi = orc.join_inner(pkey[keep_p], bkey[keep_b])
+    np.testing.assert_array_equal(out[0].values.numpy(), pkey[keep_p][epi])
+    np.testing.assert_array_equal(out[1].values.numpy(), pval[keep_p][epi])
+    np.testing.assert_array_equal(out[3].values.numpy(), bflag[keep_b][ebi])
+    tables = wl.q3_arrays(0.05, seed=7)
+    cat = wl.q3_catalog(tables)
+    res = wl.Q3Plan(cat).run(cat)
+    exp = otpch.q3(tables)
+    got = [c.values.numpy() for c in res.columns]
+    np.testing.assert_array_equal(got[0], exp["l_orderkey"])
+    np.testing.assert_allclose(got[1], exp["sum_rev"], rtol=1e-9)

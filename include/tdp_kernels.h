@@ -141,10 +141,12 @@ int64_t tdp_replay_log_size(void);
 int tdp_replay_log_end(int64_t* out, int64_t cap);
 int tdp_expect_values(const void* got, int32_t esize, int32_t n, const int64_t* expected,
                       void* stream);
-/* Benchmark timer of the fused pipeline kernel: while enabled, CUDA events are
- * recorded on the launch stream immediately around every tdp_scan_agg launch
- * (after all host-side preparation).  read() waits for the recorded events,
- * returns the summed milliseconds and the launch count, and clears them.   */
+/* Benchmark timer: while enabled, CUDA events are recorded on the launch
+ * stream immediately around every launch of the selected kernels (after all
+ * host-side preparation): on = 1 the fused scan (tdp_scan_agg), on = 2 the
+ * join probe passes (dense / hash / sorted count kernels), 0 off.  read()
+ * waits for the recorded events, returns the summed milliseconds and the
+ * launch count, and clears them.                                           */
 int tdp_kernel_timer_enable(int32_t on);
 int tdp_kernel_timer_read(double* total_ms, int64_t* launches);
 

@@ -1527,14 +1527,17 @@ AggMap make_map(const Spec& s) {
 
 i64 cells_of(const Spec& s) { return s.slots * (i64)(1 + s.fvals.size() + s.ivals.size()); }
 
+}  // namespace
+
 // ---- kernel timer (benchmarks) ---------------------------------------------
+// kind 1: the fused scan kernels; kind 2: the join probe kernels
 std::mutex g_timer_mu;
-bool g_timer_on = false;
+int g_timer_on = 0;
 std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timer_events;
 
-cudaEvent_t timer_begin(cudaStream_t st) {
+cudaEvent_t timer_begin(int kind, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(g_timer_mu);
-  if (!g_timer_on) return nullptr;
+  if (g_timer_on != kind) return nullptr;
   cudaEvent_t a = nullptr;
   if (cudaEventCreate(&a) != cudaSuccess) return nullptr;
   cudaEventRecord(a, st);
@@ -1549,8 +1552,6 @@ void timer_end(cudaEvent_t a, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(g_timer_mu);
   g_timer_events.emplace_back(a, b);
 }
-
-}  // namespace
 
 }  // namespace tdp
 
@@ -1583,7 +1584,7 @@ int tdp_pipeline_codegen(const tdp_column* cols, int32_t ncols, int64_t n,
 
 int tdp_kernel_timer_enable(int32_t on) {
   std::lock_guard<std::mutex> lock(g_timer_mu);
-  g_timer_on = on != 0;
+  g_timer_on = on;
   return TDP_OK;
 }
 
@@ -1699,7 +1700,7 @@ int scan_aggregate_impl(const tdp_column* cols, int32_t ncols, int64_t n,
     fill_params(hp, s, cols, ncols, n);
     hp.acc = ws;
     void* args[] = {&hp};
-    cudaEvent_t t0 = timer_begin(st);
+    cudaEvent_t t0 = timer_begin(1, st);
     rc = cu_check(d,
                   d->launch(fn, (unsigned)grid, 1, 1, threads, 1, 1, (unsigned)smem, (CUstream)st,
                             args, nullptr),

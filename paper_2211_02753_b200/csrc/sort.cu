@@ -1151,9 +1151,11 @@ int join_prepare_mode(const int64_t* build_keys, int64_t n_build, const PredSet*
   const bool runs = mode == 1;
   auto kernel = filtered ? (runs ? join_count_kernel<true, false> : join_count_kernel<true, true>)
                          : (runs ? join_count_kernel<false, false> : join_count_kernel<false, true>);
+  cudaEvent_t t0 = timer_begin(2, st);
   kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, pp, j.match_bits,
                                                    j.word_counts, j.tile_counts);
   TDP_LAUNCH_CHECK("join_count_kernel");
+  timer_end(t0, st);
   return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_info, j.scan_ws,
                             j.scan_bytes, st);
 }
@@ -1937,9 +1939,11 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   TDP_CUDA_TRY(cudaMemcpyAsync(out_info + 1, w.dj.flags, 2 * sizeof(int), cudaMemcpyDeviceToDevice,
                                st));
   auto kernel = pfilt ? dense_count_kernel<true> : dense_count_kernel<false>;
+  cudaEvent_t t0 = timer_begin(2, st);
   kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(w.dj, probe_keys, n_probe, pps, w.match_bits,
                                                    w.word_counts, w.tile_counts);
   TDP_LAUNCH_CHECK("dense_count_kernel");
+  timer_end(t0, st);
   return exclusive_scan_i64(w.tile_counts, w.tile_offsets, tiles, out_info, w.scan_ws,
                             w.scan_bytes, st);
 }
@@ -2437,6 +2441,7 @@ int tdp_join_sorted_prepare(const int64_t* build_keys, int64_t n_build, const in
   TDP_CUDA_TRY(cudaMemsetAsync(j.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
   const SortedJoin sj = sorted_view(j, n_build);
   const int grid = persistent_grid(tiles);
+  cudaEvent_t t0 = timer_begin(2, st);
   if (pps.npreds > 0)
     sorted_count_kernel<true><<<grid, kJoinThreads, 0, st>>>(
         sj, probe_keys, n_probe, tiles, pps, j.match_bits, j.word_counts, j.tile_counts);
@@ -2444,6 +2449,7 @@ int tdp_join_sorted_prepare(const int64_t* build_keys, int64_t n_build, const in
     sorted_count_kernel<false><<<grid, kJoinThreads, 0, st>>>(
         sj, probe_keys, n_probe, tiles, pps, j.match_bits, j.word_counts, j.tile_counts);
   TDP_LAUNCH_CHECK("sorted_count_kernel");
+  timer_end(t0, st);
   return exclusive_scan_i64(j.tile_counts, j.tile_offsets, tiles, out_count, j.scan_ws,
                             j.scan_bytes, st);
 }

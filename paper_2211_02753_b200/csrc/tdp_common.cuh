@@ -60,6 +60,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // Number of SMs of the current device (cached per device ordinal).
 int sm_count();
+// benchmark timer (tdp_kernel_timer_enable): events around launches of `kind`
+cudaEvent_t timer_begin(int kind, cudaStream_t st);
+void timer_end(cudaEvent_t a, cudaStream_t st);
 
 __host__ __device__ inline int dtype_size(int dt) {
   switch (dt) {

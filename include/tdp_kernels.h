@@ -431,6 +431,38 @@ int tdp_string_groups(const uint8_t* bytes, const int64_t* offsets, int64_t n,
                       const int64_t* inverse, int64_t m, int64_t* out_first, int32_t* out_flag,
                       void* stream);
 
+/* Device CSV ingestion (tq/storage.py:190-249 read_csv /
+ * register_csv: excel-dialect csv.reader + int() / float() / dict_encode).
+ * The file's UTF-8 bytes (ending in a record terminator) are tokenised on
+ * the device.  tdp_csv_index: out_counts[0] = fields, [1] = records (header
+ * included), [2] = quote characters (device int64; odd = an unterminated
+ * quoted field).  tdp_csv_fields: the byte position of every field end
+ * (int64 [fields]) and each record's last field index (int64 [records]);
+ * out_flags[0] != 0 reports what the device path does not model (a quote
+ * inside an unquoted field or after a closing quote, an empty line,
+ * malformed UTF-8), out_flags[1] the first record whose field count is not
+ * ncols (INT32_MAX if none) -- the caller then uses the host reader, which
+ * raises the reference's errors.  tdp_csv_parse_column: data rows' cells of
+ * column col as int64 (kind 0, Python int()) or float64 (kind 1, Python
+ * float(), exact on the device only on Clinger's fast path); out_status per
+ * row: 0 ok, 1 the host converts this cell, 2 invalid.
+ * tdp_csv_string_column: with out_bytes NULL the unescaped cell offsets
+ * (int64 [nrows + 1], total last), then the bytes themselves -- the input of
+ * tdp_string_hash / tdp_string_groups (dict_encode).                       */
+size_t tdp_csv_workspace(int64_t nbytes);
+size_t tdp_csv_string_workspace(int64_t nrows);
+int tdp_csv_index(const uint8_t* bytes, int64_t nbytes, int64_t* out_counts, void* ws,
+                  size_t ws_bytes, void* stream);
+int tdp_csv_fields(const uint8_t* bytes, int64_t nbytes, int32_t ncols, int64_t nrecords,
+                   int64_t* out_field_ends, int64_t* out_record_ends, int32_t* out_flags,
+                   void* ws, size_t ws_bytes, void* stream);
+int tdp_csv_parse_column(const uint8_t* bytes, const int64_t* field_ends, int32_t ncols,
+                         int32_t col, int64_t nrows, int32_t kind, void* out_values,
+                         uint8_t* out_status, void* stream);
+int tdp_csv_string_column(const uint8_t* bytes, const int64_t* field_ends, int32_t ncols,
+                          int32_t col, int64_t nrows, int64_t* out_offsets, uint8_t* out_bytes,
+                          void* ws, size_t ws_bytes, void* stream);
+
 /* Bitmap group-by over one int64 key whose values lie in [lo, lo+key_range)
  * (the scan's min/max), the range at most ~1024 values per row: the rank of
  * a key among the set bits of a key_range-bit map is its group id in

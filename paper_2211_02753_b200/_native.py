@@ -182,6 +182,15 @@ _SIGNATURES = {
                                       c_void_p, c_void_p]),
     "tdp_join_dense_emit": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int32,
                                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_csv_workspace": (c_size_t, [c_int64]),
+    "tdp_csv_string_workspace": (c_size_t, [c_int64]),
+    "tdp_csv_index": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "tdp_csv_fields": (c_int, [c_void_p, c_int64, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_size_t, c_void_p]),
+    "tdp_csv_parse_column": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int64, c_int32,
+                                     c_void_p, c_void_p, c_void_p]),
+    "tdp_csv_string_column": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int64, c_void_p,
+                                      c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_join_sorted_workspace": (c_size_t, [c_int64, c_int64]),
     "tdp_join_sorted_prepare": (c_int, [c_void_p, c_int64, c_void_p, c_int64, POINTER(Column),
                                         c_int32, POINTER(Predicate), c_int32, c_void_p, c_void_p,

@@ -1,6 +1,6 @@
 # Compact-storage Q1/Q6 kernel under codegen variants (measurement helper).
 mkdir -p gpurun_out
-for cfg in "TDP_VEC_PU=4 TDP_NARROW_CTAS=3" "TDP_VEC_PU=8 TDP_RING_MIN_STAGES=2" "TDP_VEC_PU=4 TDP_NARROW_CTAS=4"; do
+for cfg in "TDP_VEC_PU=8" "TDP_VEC_PU=4"; do
   env $cfg timeout 600 python bench.py --encoding compact --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/sweep.json 2>/dev/null
   python -c "
 import json; d=json.loads(open('gpurun_out/sweep.json').read().strip().splitlines()[-1])

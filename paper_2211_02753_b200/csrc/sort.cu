@@ -1700,6 +1700,9 @@ struct DenseJoin {
   int* flags;            // [0] repeated key, [1] key outside [lo, lo+R), [2] zero (expand)
   u64 lo;
   i64 range;
+  // [0] build rows set, [1] set bits, [2] CTAs done (dense_dup_check_kernel);
+  // null: repeats are detected from the atomics' return values instead
+  unsigned long long* cnt;
 };
 
 // Build rows by key offset in a plain int32 array of R entries (no clearing:
@@ -1735,6 +1738,7 @@ __global__ void __launch_bounds__(kBuildThreads, 2)
 #pragma unroll
   for (int k = 0; k < kBuildPer; ++k) key[k] = act[k] ? __ldg(keys + row[k]) : 0;
   if (kFiltered) eval_batch_upfront<kBuildPer>(bps, row, act);
+  unsigned built = 0;
 #pragma unroll
   for (int k = 0; k < kBuildPer; ++k) {
     if (!act[k]) continue;
@@ -1744,8 +1748,48 @@ __global__ void __launch_bounds__(kBuildThreads, 2)
       continue;
     }
     const unsigned bit = 1u << (x & 31);
-    if (atomicOr(dj.bits + (x >> 5), bit) & bit) dj.flags[0] = 1;
+    if (dj.cnt != nullptr) {
+      // fire-and-forget OR (the CTA does not wait for L2): a repeated key
+      // shows as fewer set bits than rows set (dense_dup_check_kernel)
+      atomicOr(dj.bits + (x >> 5), bit);
+      ++built;
+    } else if (atomicOr(dj.bits + (x >> 5), bit) & bit) {
+      dj.flags[0] = 1;
+    }
     if (dj.row_of != nullptr) dj.row_of[x] = (int)row[k];
+  }
+  if (dj.cnt != nullptr) {  // one global atomic per CTA (a single counter: avoid contention)
+    __shared__ unsigned cta_built;
+    if (threadIdx.x == 0) cta_built = 0;
+    __syncthreads();
+    const unsigned w = warp_sum(built);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&cta_built, w);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_built) atomicAdd(dj.cnt, (unsigned long long)cta_built);
+  }
+}
+
+// After the build: set bits vs rows set -> flags[0] (a repeated key).  The
+// last CTA to finish compares (order-free integer sums).
+__global__ void dense_dup_check_kernel(DenseJoin dj, i64 words) {
+  __shared__ unsigned long long part[32];
+  unsigned long long s = 0;
+  for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (i64)gridDim.x * blockDim.x)
+    s += __popc(dj.bits[w]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += part[k];
+    atomicAdd(dj.cnt + 1, t);
+    __threadfence();
+    if (atomicAdd(dj.cnt + 2, 1ull) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long set = atomicAdd(dj.cnt + 1, 0ull);
+      if (set != atomicAdd(dj.cnt, 0ull)) dj.flags[0] = 1;
+    }
   }
 }
 
@@ -1861,6 +1905,7 @@ DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np, bool need_rows)
     p += align256((size_t)r * 4);
   }
   w.dj.flags = (int*)p;
+  w.dj.cnt = reinterpret_cast<unsigned long long*>(p + 32);
   p += 256;
   w.dj.lo = (u64)lo;
   w.dj.range = r;
@@ -1912,7 +1957,7 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   TDP_CUDA_TRY(cudaMemsetAsync(out_info, 0, 2 * sizeof(i64), st));
   if (n_build == 0 || n_probe == 0) return TDP_OK;
   TDP_CUDA_TRY(cudaMemsetAsync(w.dj.bits, 0, (size_t)words * 4, st));
-  TDP_CUDA_TRY(cudaMemsetAsync(w.dj.flags, 0, 16, st));
+  TDP_CUDA_TRY(cudaMemsetAsync(w.dj.flags, 0, 64, st));  // flags + the dup-check counters
   TDP_CUDA_TRY(cudaMemsetAsync(w.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
   const bool bfilt = bps.npreds > 0, pfilt = pps.npreds > 0;
   const unsigned btiles = (unsigned)ceil_div(n_build, kJoinTile);
@@ -1921,6 +1966,8 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   else
     dense_build_kernel<false><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, w.dj, bps);
   TDP_LAUNCH_CHECK("dense_build_kernel");
+  dense_dup_check_kernel<<<stream_grid(words, 256 * 8, 4), 256, 0, st>>>(w.dj, words);
+  TDP_LAUNCH_CHECK("dense_dup_check_kernel");
   if (need_rows && w.dj.row_of == nullptr) {
     rank_popc_kernel<<<stream_grid(blocks, 8, 8), 256, 0, st>>>(w.dj.bits, words, blocks,
                                                                  w.dj.bcount, w.dj.wpre);

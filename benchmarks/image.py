@@ -5,6 +5,9 @@ from __future__ import annotations
 
 import json
 
+from .common import ClockSampler
+
+
 def run(args):
     """Image query (SURVEY config 5): GROUP BY the PE output of a random-init CNN
     UDF over 1e7 synthetic 28x28 images, counts fed to an MSE loss, trained
@@ -54,10 +57,13 @@ def run(args):
     steps = max(1, min(args.steps, 5))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(0)
+    sampler.active = True
     t0.record()
     losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
     t1.record()
     torch.cuda.synchronize()
+    clocks = sampler.stop()
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0
     # diagnostic: share of one step's device time in this framework's kernels
@@ -81,7 +87,7 @@ def run(args):
                                "-> pe_encode, MSE, Adam",
                    "images": n, "classes": k, "chunk_rows": chunk,
                    "step": "one iteration of tq.train(); CNN activations checkpointed per chunk"},
-        "gpu_launches": launches,
+        "gpu_launches": launches, "clocks": clocks,
         "framework_kernel_share": ours / total if total else None,
         "framework_kernel_ms": ours / 1e3,
         "losses": losses[:2] + losses[-2:],

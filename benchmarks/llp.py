@@ -91,6 +91,8 @@ def run(args) -> None:
     losses += tq.train(q, cat, batches, TrainConfig(iterations=steps, lr=0.01))
     t1.record()
     torch.cuda.synchronize()
+    # keep the GPU loaded long enough for nvidia-smi's sampling period
+    sustain(lambda: tq.train(q, cat, batches, TrainConfig(iterations=1, lr=0.01)), 1.5)
     clocks = sampler.stop()
     ms = t0.elapsed_time(t1) / steps
     launches = _native.launch_count() - launches0

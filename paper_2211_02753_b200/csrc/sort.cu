@@ -677,6 +677,31 @@ constexpr int kJoinTile = 2048;  // probe rows per tile
 constexpr int kJoinWords = kJoinTile / 32;
 constexpr int kJoinPer = kJoinTile / kJoinThreads;
 constexpr int kJoinWarps = kJoinThreads / 32;
+
+// Tile-per-CTA probe / build passes prefetch a later tile's columns into L2
+// with one bulk instruction per column (l2_prefetch_range): the HBM stream
+// runs a wave ahead of the CTAs' dependent bitmap / Bloom / slot lookups
+// (Q3 SF10 lineitem probe 0.182 -> 0.153 ms, 0.81 -> 0.96 of the copy peak).
+// The CTA of tile `tile` asks L2 for the rows of tile `tile + ahead`.
+__device__ __forceinline__ void join_prefetch_ahead(i64 ahead, i64 tile, const i64* keys, i64 n,
+                                                     const PredSet& ps, bool filtered) {
+  if (ahead <= 0 || threadIdx.x != 0) return;
+  const i64 r0 = (tile + ahead) * kJoinTile;
+  if (r0 >= n) return;
+  const i64 rows = n - r0 < kJoinTile ? n - r0 : kJoinTile;
+  l2_prefetch_range(keys + r0, rows * 8);
+  if (filtered) prefetch_predset_l2(ps, r0, rows);
+}
+
+// L2 prefetch distance in tiles: resident CTAs of a wave x TDP_L2_AHEAD
+// (measurements; default 1, 0 disables)
+inline i64 join_ahead(int ctas_per_sm) {
+  static const double mult = [] {
+    const char* e = getenv("TDP_L2_AHEAD");
+    return e ? atof(e) : 1.0;
+  }();
+  return (i64)(mult * sm_count() * ctas_per_sm);
+}
 constexpr i64 kMinKey = (i64)0x8000000000000000ull;
 
 // slot.y packs (start + 1) << 24 | min(run length, kCountSat); a saturated
@@ -700,6 +725,7 @@ struct HashTable {
   i64* side;         // run of the key INT64_MIN (its image is the empty marker): {start+1, count}
   int* flags;        // [0] a key repeats, [1] build is sorted (runs), else unique
   const i64* order;  // sorted build row ids (sorted mode)
+  i64 ahead;         // probe: tiles ahead prefetched into L2 (join_prefetch_ahead)
 };
 
 // Register-blocked Bloom filter: one 32-bit word per key, 3 bits from 5-bit
@@ -834,6 +860,7 @@ __global__ void __launch_bounds__(kJoinThreads, kUnique ? 4 : 3)
                       i64* __restrict__ tile_counts) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
+  join_prefetch_ahead(ht.ahead, tile, probe, np, ps, kFiltered);
   bool act[kJoinPer];
   i64 row[kJoinPer], key[kJoinPer];
 #pragma unroll
@@ -1066,6 +1093,7 @@ JoinWs carve_join(void* ws, i64 nb, i64 np) {
   j.ht.count = (i64*)p;
   p += align256(cap * 8);
   j.ht.mask = cap - 1;
+  j.ht.ahead = 0;
   j.ht.bloom = (unsigned*)p;
   p += align256(bloom_blocks(nb) * 4);
   j.ht.bmask = (unsigned)(bloom_blocks(nb) - 1);
@@ -1151,6 +1179,7 @@ int join_prepare_mode(const int64_t* build_keys, int64_t n_build, const PredSet*
   const bool runs = mode == 1;
   auto kernel = filtered ? (runs ? join_count_kernel<true, false> : join_count_kernel<true, true>)
                          : (runs ? join_count_kernel<false, false> : join_count_kernel<false, true>);
+  j.ht.ahead = join_ahead(runs ? 3 : 4);
   cudaEvent_t t0 = timer_begin(2, st);
   kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(j.ht, probe_keys, n_probe, pp, j.match_bits,
                                                    j.word_counts, j.tile_counts);
@@ -1703,7 +1732,11 @@ struct DenseJoin {
   // [0] build rows set, [1] set bits, [2] CTAs done (dense_dup_check_kernel);
   // null: repeats are detected from the atomics' return values instead
   unsigned long long* cnt;
+  // tiles ahead of its own whose columns a build / probe CTA prefetches into
+  // L2 (about one wave of resident CTAs; 0: none)
+  i64 ahead;
 };
+
 
 // Build rows by key offset in a plain int32 array of R entries (no clearing:
 // only offsets whose bit is set are read) while R <= 8 x the build rows;
@@ -1726,6 +1759,7 @@ template <bool kFiltered>
 __global__ void __launch_bounds__(kBuildThreads, 2)
     dense_build_kernel(const i64* __restrict__ keys, i64 nb, DenseJoin dj, PredSet bps) {
   const i64 tile = blockIdx.x;
+  join_prefetch_ahead(dj.ahead, tile, keys, nb, bps, kFiltered);
   bool act[kBuildPer];
   i64 row[kBuildPer], key[kBuildPer];
 #pragma unroll
@@ -1813,6 +1847,7 @@ __global__ void __launch_bounds__(kJoinThreads, 4)
                        i64* __restrict__ tile_counts) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = blockIdx.x;
+  join_prefetch_ahead(dj.ahead, tile, probe, np, ps, kFiltered);
   bool act[kJoinPer];
   i64 row[kJoinPer], key[kJoinPer];
 #pragma unroll
@@ -1908,6 +1943,7 @@ DenseWs carve_dense(void* ws, i64 range, i64 lo, i64 nb, i64 np, bool need_rows)
   w.dj.cnt = reinterpret_cast<unsigned long long*>(p + 32);
   p += 256;
   w.dj.lo = (u64)lo;
+  w.dj.ahead = 0;
   w.dj.range = r;
   w.match_bits = (unsigned*)p;
   p += align256((size_t)tiles * kJoinWords * 4);
@@ -1961,6 +1997,7 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   TDP_CUDA_TRY(cudaMemsetAsync(w.tile_counts, 0, (size_t)tiles * sizeof(i64), st));
   const bool bfilt = bps.npreds > 0, pfilt = pps.npreds > 0;
   const unsigned btiles = (unsigned)ceil_div(n_build, kJoinTile);
+  w.dj.ahead = join_ahead(2);
   if (bfilt)
     dense_build_kernel<true><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, w.dj, bps);
   else
@@ -1986,6 +2023,7 @@ int tdp_join_dense_prepare(const int64_t* build_keys, int64_t n_build, const tdp
   TDP_CUDA_TRY(cudaMemcpyAsync(out_info + 1, w.dj.flags, 2 * sizeof(int), cudaMemcpyDeviceToDevice,
                                st));
   auto kernel = pfilt ? dense_count_kernel<true> : dense_count_kernel<false>;
+  w.dj.ahead = join_ahead(4);
   cudaEvent_t t0 = timer_begin(2, st);
   kernel<<<(unsigned)tiles, kJoinThreads, 0, st>>>(w.dj, probe_keys, n_probe, pps, w.match_bits,
                                                    w.word_counts, w.tile_counts);
@@ -2014,6 +2052,7 @@ int tdp_join_dense_bitmap(const int64_t* build_keys, int64_t n_build, const tdp_
   dj.flags = out_flags;
   dj.lo = (u64)lo;
   dj.range = key_range;
+  dj.ahead = join_ahead(2);
   const unsigned btiles = (unsigned)ceil_div(n_build, kJoinTile);
   if (bps.npreds > 0)
     dense_build_kernel<true><<<btiles, kBuildThreads, 0, st>>>(build_keys, n_build, dj, bps);

@@ -116,6 +116,19 @@ struct PredSet {
   DevPred p[kMaxPreds];
 };
 
+// Bulk prefetch of [p, p + bytes) into L2 by the TMA engine (no registers,
+// no shared memory): a tile-per-CTA streaming kernel asks for a tile the next
+// wave of CTAs will read, so its HBM traffic no longer waits for the CTAs of
+// this wave to finish their dependent (L2-latency) phase.  The range is
+// widened to 16-byte bounds, which stay inside the allocation's last chunk.
+__device__ __forceinline__ void l2_prefetch_range(const void* p, i64 bytes) {
+  if (p == nullptr || bytes <= 0) return;
+  const unsigned long long a = (unsigned long long)p & ~15ull;
+  const unsigned long long e = ((unsigned long long)p + (unsigned long long)bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a))
+               : "memory");
+}
+
 __device__ __forceinline__ i64 load_as_i64(const void* base, int dt, i64 i) {
   switch (dt) {
     case TDP_I64:
@@ -312,6 +325,15 @@ __device__ __forceinline__ void eval_batch(const PredSet& ps, const i64 (&row)[R
 #pragma unroll
       for (int r = 0; r < R; ++r) keep[r] = keep[r] && eval_pred(ps.p[k], row[r]);
     }
+  }
+}
+
+// L2 prefetch of rows [row0, row0 + rows) of every predicate column
+__device__ __forceinline__ void prefetch_predset_l2(const PredSet& ps, i64 row0, i64 rows) {
+  for (int k = 0; k < ps.npreds; ++k) {
+    const int es = dtype_size(ps.p[k].dtype);
+    if (ps.p[k].cmp == TDP_CMP_NONE || ps.p[k].cmp == TDP_CMP_ALL || es == 0) continue;
+    l2_prefetch_range(reinterpret_cast<const char*>(ps.p[k].ptr) + row0 * es, rows * es);
   }
 }
 

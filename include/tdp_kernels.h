@@ -225,6 +225,11 @@ typedef struct tdp_key {
 } tdp_key;
 
 enum tdp_agg_kind { TDP_AGG_COUNT = 0, TDP_AGG_SUM_F64 = 1, TDP_AGG_SUM_I64 = 2 };
+/* OR-ed into a SUM kind passed to a group-by *emit* call (hash / bitmap
+ * group-by): that aggregate is emitted as the float64 mean
+ * double(sum) / double(count) -- tq/kernels.py:160-161
+ * `sums.astype(np.float64) / counts`, IEEE division -- instead of the sum.  */
+#define TDP_AGG_AVG_BIT 0x100
 
 typedef struct tdp_agg {
   int32_t kind;  /* tdp_agg_kind                                           */

@@ -40,6 +40,7 @@ OP_LOAD, OP_CONST, OP_CAST, OP_ADD, OP_SUB, OP_MUL, OP_DIV = 0, 1, 2, 3, 4, 5, 6
 OP_NEG, OP_SQUARE, OP_LOG, OP_EXP, OP_RELU, OP_DECIMAL = 7, 8, 9, 10, 11, 12
 
 AGG_COUNT, AGG_SUM_F64, AGG_SUM_I64 = 0, 1, 2
+AGG_AVG_BIT = 0x100  # group-by emit: write the float64 mean (TDP_AGG_AVG_BIT)
 SOFT_DENSE, SOFT_ONEHOT = 0, 1
 
 

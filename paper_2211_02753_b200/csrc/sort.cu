@@ -327,7 +327,31 @@ struct ValSet {
   int dt[32];
   int kind[32];
   int fidx[32];   // aggregate -> fixed-point cell block (float SUMs), else -1
+  unsigned avg;   // emit: aggregates written as double(sum) / double(count)
 };
+
+// Emit kinds: TDP_AGG_AVG_BIT moved into vs->avg, the kinds themselves plain.
+inline int emit_kinds(const int32_t* agg_kinds, int32_t naggs, ValSet* vs) {
+  TDP_REQUIRE(naggs >= 0 && naggs <= 32, "at most 32 aggregates");
+  std::memset(vs, 0, sizeof(*vs));
+  vs->naggs = naggs;
+  for (int a = 0; a < naggs; ++a) {
+    const int k = agg_kinds[a] & ~TDP_AGG_AVG_BIT;
+    TDP_REQUIRE(k >= TDP_AGG_COUNT && k <= TDP_AGG_SUM_I64, "agg %d: bad kind", a);
+    TDP_REQUIRE(!(agg_kinds[a] & TDP_AGG_AVG_BIT) || k != TDP_AGG_COUNT,
+                "agg %d: AVG of a count", a);
+    vs->kind[a] = k;
+    if (agg_kinds[a] & TDP_AGG_AVG_BIT) vs->avg |= 1u << a;
+  }
+  return TDP_OK;
+}
+
+// One emitted aggregate value (8 bytes): the mean when the AVG bit is set.
+__device__ __forceinline__ u64 emit_value(const ValSet& vs, int a, u64 raw, u64 cnt) {
+  if (!((vs.avg >> a) & 1u)) return raw;
+  const double s = vs.kind[a] == TDP_AGG_SUM_F64 ? __longlong_as_double((i64)raw) : (double)(i64)raw;
+  return (u64)__double_as_longlong(s / (double)cnt);
+}
 
 inline void number_fixed(ValSet* vs) {
   vs->nfixed = 0;
@@ -1547,7 +1571,8 @@ __global__ void hashagg_gather_kernel(HashAgg h, const u64* __restrict__ img,
     const u64 cnt = c[kCellCnt];
     out_counts[i] = (i64)cnt;
     for (int a = 0; a < vs.naggs; ++a)
-      out_sums[(i64)a * m + i] = vs.kind[a] == TDP_AGG_COUNT ? cnt : c[kCellAcc + a];
+      out_sums[(i64)a * m + i] =
+          vs.kind[a] == TDP_AGG_COUNT ? cnt : emit_value(vs, a, c[kCellAcc + a], cnt);
   }
 }
 
@@ -1641,10 +1666,8 @@ int tdp_groupby_hash_emit_ranked(int64_t n, const int32_t* agg_kinds, int32_t na
   TDP_REQUIRE(m == 0 || rank_ws_bytes_ >= rank_ws_bytes(key_range), "rank workspace too small");
   if (m == 0) return TDP_OK;
   ValSet vs;
-  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  int rc = emit_kinds(agg_kinds, naggs, &vs);  // kinds only (+ AVG bits)
   if (rc) return rc;
-  vs.naggs = naggs;
-  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
   number_fixed(&vs);
   cudaStream_t st = as_stream(stream);
   HashAgg h = carve_hashagg(ws, n, vs);
@@ -1684,10 +1707,8 @@ int tdp_groupby_hash_emit(int64_t n, const int32_t* agg_kinds, int32_t naggs, in
   TDP_REQUIRE(ws_bytes >= hashagg_ws_bytes(n, naggs), "hash group-by workspace too small");
   if (m == 0) return TDP_OK;
   ValSet vs;
-  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  int rc = emit_kinds(agg_kinds, naggs, &vs);  // kinds only (+ AVG bits)
   if (rc) return rc;
-  vs.naggs = naggs;
-  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
   number_fixed(&vs);
   cudaStream_t st = as_stream(stream);
   HashAgg h = carve_hashagg(ws, n, vs);
@@ -2212,7 +2233,7 @@ __global__ void bm_emit_kernel(BitmapAgg b, i64 m, ValSet vs, i64* __restrict__ 
         v = (u64)__double_as_longlong(fixed_value(c + kCellAcc + vs.naggs + kFixedWords * vs.fidx[a]));
       else
         v = c[kCellAcc + a];
-      out_sums[(i64)a * m + g] = v;
+      out_sums[(i64)a * m + g] = vs.kind[a] == TDP_AGG_COUNT ? v : emit_value(vs, a, v, cnt);
     }
   }
 }
@@ -2269,10 +2290,8 @@ int tdp_groupby_bitmap_emit(int64_t n, int64_t lo, int64_t key_range, const int3
               "bitmap group-by workspace too small");
   if (m == 0) return TDP_OK;
   ValSet vs;
-  int rc = make_valset(nullptr, agg_kinds, 0, n, &vs);  // kinds only
+  int rc = emit_kinds(agg_kinds, naggs, &vs);  // kinds only (+ AVG bits)
   if (rc) return rc;
-  vs.naggs = naggs;
-  for (int a = 0; a < naggs; ++a) vs.kind[a] = agg_kinds[a];
   number_fixed(&vs);
   BitmapAgg b = carve_bitmap_agg(ws, n, key_range, lo, vs);
   cudaStream_t st = as_stream(stream);

@@ -128,6 +128,27 @@ def take_rows(col: EncodedTensor, indices) -> EncodedTensor:
         return EncodedTensor(Tensor(gather_rows_raw(v.data, idx)), col.encoding)
 
 
+def take_rows_many(columns: Sequence[EncodedTensor], indices) -> list[EncodedTensor]:
+    """take_rows of several columns by one index vector: the plain ones in a
+    single gather launch (tdp_gather_rows over up to 16 columns)."""
+    idx = _as_index(indices)
+    out: list = [None] * len(columns)
+    plain = []
+    for i, c in enumerate(columns):
+        v = c.values
+        if onehot_payload(v) is None and not (v.dtype in FLOAT_DTYPES and active_tape() is not None):
+            plain.append(i)
+        else:
+            out[i] = take_rows(c, idx)
+    for b in range(0, len(plain), 16):
+        part = plain[b:b + 16]
+        got = gather_many([columns[i].values.data for i in part], idx)
+        with trusted():
+            for i, g in zip(part, got):
+                out[i] = EncodedTensor(Tensor(g), columns[i].encoding)
+    return out
+
+
 _OPS = ("=", "<>", "<", ">", "<=", ">=")
 
 
@@ -300,6 +321,13 @@ def _agg_kind(func: str, dtype: str) -> int:
     if func == "count":
         return nat.AGG_COUNT
     return nat.AGG_SUM_F64 if dtype in FLOAT_DTYPES else nat.AGG_SUM_I64
+
+
+def _emit_kinds(agg_specs, kinds) -> "c_int32 * n":
+    """Kinds for a group-by emit call: AVG aggregates carry TDP_AGG_AVG_BIT,
+    so the emit kernel writes the float64 mean (no cast / divide launches)."""
+    ek = [k | nat.AGG_AVG_BIT if f == "avg" else k for (f, _), k in zip(agg_specs, kinds)]
+    return (c_int32 * max(1, len(ek)))(*ek)
 
 
 def _fusable(values: Sequence) -> Optional[tuple[Optional[Selection], int]]:
@@ -766,13 +794,15 @@ def _groupby_hash(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
         # bandwidth-bound passes) instead of a radix sort of the m keys
         lo_key = _key_of_image(lo_img)
         rws = nat.workspace(nat.load().tdp_groupby_hash_rank_workspace(key_range), device)
-        nat.call("tdp_groupby_hash_emit_ranked", n, kind_arr, len(kinds), m, lo_key, key_range,
+        nat.call("tdp_groupby_hash_emit_ranked", n, _emit_kinds(agg_specs, kinds), len(kinds), m,
+                 lo_key, key_range,
                  nat.ptr(keys_out), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(),
                  nat.ptr(rws), rws.numel(), nat.stream())
     else:
-        nat.call("tdp_groupby_hash_emit", n, kind_arr, len(kinds), m, nat.ptr(keys_out),
-                 nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
-    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
+        nat.call("tdp_groupby_hash_emit", n, _emit_kinds(agg_specs, kinds), len(kinds), m,
+                 nat.ptr(keys_out), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(),
+                 nat.stream())
+    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=True)
 
 
 def _agg_columns(agg_specs, agg_vals, n: int):
@@ -807,9 +837,10 @@ def _groupby_bitmap(key: torch.Tensor, lo: int, span: int, agg_specs, agg_vals, 
     keys_out = torch.empty(m, dtype=torch.int64, device=device)
     counts = torch.empty(m, dtype=torch.int64, device=device)
     sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
-    nat.call("tdp_groupby_bitmap_emit", n, lo, span, kind_arr, len(kinds), m, nat.ptr(keys_out),
-             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), nat.stream())
-    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=False)
+    nat.call("tdp_groupby_bitmap_emit", n, lo, span, _emit_kinds(agg_specs, kinds), len(kinds), m,
+             nat.ptr(keys_out), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(),
+             nat.stream())
+    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=True)
 
 
 def _groupby_local(kdata, agg_specs, agg_vals, key_range=None):
@@ -1129,7 +1160,7 @@ def sort_limit(columns: Sequence[EncodedTensor], key_index: int,
         order = stable_order(key, descending)
         if limit is not None:
             order = order[: max(0, limit)]
-    return [take_rows(c, order) for c in columns]
+    return take_rows_many(columns, order)
 
 
 def limit_rows(columns: Sequence[EncodedTensor], count: int) -> list[EncodedTensor]:

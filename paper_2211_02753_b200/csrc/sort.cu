@@ -441,23 +441,32 @@ __global__ void copy_counts_kernel(const unsigned long long* __restrict__ counts
 constexpr int kTopkChunk = 2048;
 constexpr int kTopkMax = 1024;
 
-__global__ void __launch_bounds__(kTopkChunk / 2)
-    topk_chunk_kernel(const u64* __restrict__ keys, const i64* __restrict__ idx, i64 m, int k,
-                      int chunk, u64* __restrict__ out_keys, i64* __restrict__ out_idx,
-                      i64* __restrict__ final_idx, i64 final_count) {
-  __shared__ u64 sk[kTopkChunk];
-  __shared__ i64 si[kTopkChunk];
-  const i64 base = (i64)blockIdx.x * chunk;
-  for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
-    const i64 g = base + t;
-    const bool ok = g < m;
-    sk[t] = ok ? keys[g] : ~0ull;
-    si[t] = ok ? idx[g] : LLONG_MAX;  // sentinel sorts after every real pair
+// Key images of the first round are made while loading (no separate pass).
+struct TopkRaw {
+  const void* key;  // null: read (image, row) pairs of an earlier round
+  int dtype;
+  int desc;
+};
+
+__device__ __forceinline__ u64 topk_image(const TopkRaw& r, i64 i) {
+  switch (r.dtype) {
+    case TDP_I64:
+      return image_i64(__ldg(reinterpret_cast<const i64*>(r.key) + i), r.desc);
+    case TDP_I32:
+      return image_i64((i64)__ldg(reinterpret_cast<const int*>(r.key) + i), r.desc);
+    case TDP_F64:
+      return image_f64(__ldg(reinterpret_cast<const double*>(r.key) + i), r.desc);
+    default:
+      return image_f32(__ldg(reinterpret_cast<const float*>(r.key) + i), r.desc);
   }
-  for (int size = 2; size <= chunk; size <<= 1) {
+}
+
+// Ascending bitonic sort of n (a power of two) (image, row) pairs in shared memory.
+__device__ __forceinline__ void topk_bitonic(u64* sk, i64* si, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
-      for (int t = threadIdx.x; t < chunk / 2; t += blockDim.x) {
+      for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
         const int a = 2 * t - (t & (stride - 1));
         const int b = a + stride;
         const bool up = (a & size) == 0;
@@ -474,6 +483,31 @@ __global__ void __launch_bounds__(kTopkChunk / 2)
     }
   }
   __syncthreads();
+}
+
+// One round: every CTA sorts `chunk` pairs and keeps its first k (the first
+// round reads the key column itself); final_idx: a single CTA, the answer.
+// (A last-CTA-finishes-the-job variant of the second-to-last round measured
+// slower: one CTA sorting 2048 survivors takes longer than a launch.)
+__global__ void __launch_bounds__(kTopkChunk / 2)
+    topk_chunk_kernel(TopkRaw raw, const u64* __restrict__ keys, const i64* __restrict__ idx,
+                      i64 m, int k, int chunk, u64* __restrict__ out_keys,
+                      i64* __restrict__ out_idx, i64* __restrict__ final_idx, i64 final_count) {
+  __shared__ u64 sk[kTopkChunk];
+  __shared__ i64 si[kTopkChunk];
+  const i64 base = (i64)blockIdx.x * chunk;
+  for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
+    const i64 g = base + t;
+    const bool ok = g < m;
+    if (raw.key != nullptr) {
+      sk[t] = ok ? topk_image(raw, g) : ~0ull;
+      si[t] = ok ? g : LLONG_MAX;
+    } else {
+      sk[t] = ok ? keys[g] : ~0ull;
+      si[t] = ok ? idx[g] : LLONG_MAX;  // sentinel sorts after every real pair
+    }
+  }
+  topk_bitonic(sk, si, chunk);
   if (final_idx != nullptr) {  // last round: one CTA, the answer
     for (int t = threadIdx.x; t < final_count; t += blockDim.x) final_idx[t] = si[t];
     return;
@@ -537,32 +571,43 @@ int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t
   u64* kb = (u64*)p;
   p += align256((size_t)m1 * 8);
   i64* ib = (i64*)p;
-  make_keys_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(key->data, key->dtype,
-                                                                descending ? 1 : 0, n, k0, i0);
-  TDP_LAUNCH_CHECK("make_keys_kernel");
+  (void)k0;
+  (void)i0;
+  TopkRaw raw{key->data, key->dtype, descending ? 1 : 0};
+  const TopkRaw none{nullptr, 0, 0};
   const i64 want = k < n ? k : n;
-  const u64* sk = k0;
-  const i64* si = i0;
+  if (n <= kTopkChunk) {  // one CTA: the answer
+    const int last = pow2_at_least(n);
+    topk_chunk_kernel<<<1, last / 2 > 32 ? last / 2 : 32, 0, st>>>(
+        raw, nullptr, nullptr, n, (int)k, last, nullptr, nullptr, out_order, want);
+    TDP_LAUNCH_CHECK("topk_chunk_kernel");
+    return TDP_OK;
+  }
+  const u64* sk = nullptr;
+  const i64* si = nullptr;
   i64 m = n;
   bool use_a = true;
-  while (m > kTopkChunk) {
+  for (;;) {
     const int chunk = topk_round_chunk(m, k);
     const i64 blocks = ceil_div(m, chunk);
     u64* dk = use_a ? ka : kb;
     i64* di = use_a ? ia : ib;
-    topk_chunk_kernel<<<(unsigned)blocks, chunk / 2, 0, st>>>(sk, si, m, (int)k, chunk, dk, di,
-                                                              nullptr, 0);
+    topk_chunk_kernel<<<(unsigned)blocks, chunk / 2, 0, st>>>(sk == nullptr ? raw : none, sk, si,
+                                                              m, (int)k, chunk, dk, di, nullptr,
+                                                              0);
     TDP_LAUNCH_CHECK("topk_chunk_kernel");
     sk = dk;
     si = di;
     m = blocks * k;
     use_a = !use_a;
+    if (m <= kTopkChunk) {
+      const int last = pow2_at_least(m);
+      topk_chunk_kernel<<<1, last / 2 > 32 ? last / 2 : 32, 0, st>>>(
+          none, sk, si, m, (int)k, last, nullptr, nullptr, out_order, want);
+      TDP_LAUNCH_CHECK("topk_chunk_kernel");
+      return TDP_OK;
+    }
   }
-  const int last = pow2_at_least(m);
-  topk_chunk_kernel<<<1, last / 2 > 32 ? last / 2 : 32, 0, st>>>(sk, si, m, (int)k, last, nullptr,
-                                                                 nullptr, out_order, want);
-  TDP_LAUNCH_CHECK("topk_chunk_kernel");
-  return TDP_OK;
 }
 
 int tdp_sort_order(const tdp_column* key, int32_t descending, int64_t n, int64_t* out_order,

@@ -123,6 +123,12 @@ uint64_t tdp_launch_count(void);
 /* Account `n` kernels of this library replayed inside a CUDA graph (a graph
  * captured from library launches relaunches them without calling in). */
 void tdp_count_graph_launches(uint64_t n);
+/* Replay bookkeeping without torch's stream objects (replay.py: a replayed
+ * plan's host path is on the critical path of small queries):
+ * stream_wait_event = cudaStreamWaitEvent; replay_done = count the replayed
+ * graph's launches, then cudaEventRecord(event, stream).                   */
+int tdp_stream_wait_event(void* stream, void* event);
+int tdp_replay_done(void* event, void* stream, uint64_t graph_launches);
 /* Read and clear the CUDA runtime error state of this library (after an
  * aborted graph capture); returns the cudaError_t that was pending.        */
 int tdp_clear_error(void);

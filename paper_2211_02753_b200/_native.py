@@ -81,6 +81,8 @@ _SIGNATURES = {
     "tdp_device_sm_count": (c_int, []),
     "tdp_launch_count": (c_uint64, []),
     "tdp_count_graph_launches": (None, [c_uint64]),
+    "tdp_stream_wait_event": (c_int, [c_void_p, c_void_p]),
+    "tdp_replay_done": (c_int, [c_void_p, c_void_p, c_uint64]),
     "tdp_clear_error": (c_int, []),
     "tdp_expect_values": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "tdp_replay_log_begin": (c_int, [c_int32, c_void_p, c_int64]),
@@ -295,6 +297,13 @@ def stream() -> c_void_p:
     if _raw_stream is not None and _raw_device is not None:
         return c_void_p(_raw_stream(_raw_device()))
     return c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def current_device() -> int:
+    """torch.cuda.current_device() without its Python-level checks."""
+    if _raw_device is not None:
+        return int(_raw_device())
+    return torch.cuda.current_device()
 
 
 def ptr(t: Optional[torch.Tensor]) -> c_void_p:

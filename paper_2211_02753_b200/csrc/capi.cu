@@ -179,4 +179,17 @@ void tdp_count_graph_launches(uint64_t n) {
   tdp::g_launches.fetch_add(n, std::memory_order_relaxed);
 }
 
+int tdp_stream_wait_event(void* stream, void* event) {
+  TDP_REQUIRE(event != nullptr, "null event");
+  TDP_CUDA_TRY(cudaStreamWaitEvent(tdp::as_stream(stream), reinterpret_cast<cudaEvent_t>(event), 0));
+  return TDP_OK;
+}
+
+int tdp_replay_done(void* event, void* stream, uint64_t graph_launches) {
+  TDP_REQUIRE(event != nullptr, "null event");
+  tdp::g_launches.fetch_add(graph_launches, std::memory_order_relaxed);
+  TDP_CUDA_TRY(cudaEventRecord(reinterpret_cast<cudaEvent_t>(event), tdp::as_stream(stream)));
+  return TDP_OK;
+}
+
 }  // extern "C"

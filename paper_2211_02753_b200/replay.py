@@ -29,6 +29,7 @@ sizing its output) runs eagerly from then on.  ``TDP_REPLAY=0`` or
 
 from __future__ import annotations
 
+import ctypes
 import gc
 import os
 import threading
@@ -86,7 +87,7 @@ def _tables_signature(catalog, names) -> Optional[tuple[list, list]]:
         return None
     # a sharded run (NCCL collectives inside the graph: capturable, replayed in
     # lockstep on every rank) and a local one are different states
-    sig, tables = [id(catalog), torch.cuda.current_device(), id(group) if group else None], []
+    sig, tables = [id(catalog), nat.current_device(), id(group) if group else None], []
     for name in names:
         t = tables_by_name.get(name)
         if t is None:
@@ -209,20 +210,23 @@ class _Replay:
         self.launches = launches
         self.hold = hold  # the catalog tables the signature names (ids stay unique)
         self.lock = threading.Lock()
-        self.done: Optional[torch.cuda.Event] = None
+        # one event, re-recorded after every copy-out; a replay from another
+        # stream waits on it (same stream: stream order already serialises)
+        self.done = torch.cuda.Event()
+        self.done.record()  # creates the event (torch creates it lazily)
+        self.done_handle = ctypes.c_void_p(self.done.cuda_event)
+        self.last_stream: Optional[int] = None
 
     def __call__(self):
         with self.lock:
-            stream = torch.cuda.current_stream()
-            if self.done is not None:
-                stream.wait_event(self.done)
+            lib = nat.load()
+            st = nat.stream()
+            if self.last_stream is not None and self.last_stream != st.value:
+                nat.check(lib.tdp_stream_wait_event(st, self.done_handle), "tdp_stream_wait_event")
             self.graph.replay()
-            if self.launches:
-                nat.load().tdp_count_graph_launches(self.launches)
             table = self.template.materialise()
-            done = torch.cuda.Event()
-            done.record(stream)
-            self.done = done
+            nat.check(lib.tdp_replay_done(self.done_handle, st, self.launches), "tdp_replay_done")
+            self.last_stream = st.value
             return table
 
 

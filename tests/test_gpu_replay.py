@@ -307,3 +307,50 @@ def test_concurrent_replays_from_threads_on_separate_streams():
     assert len(results) == 75
     for r in results:
         np.testing.assert_allclose(r, exp["sum_charge"], rtol=1e-9)
+
+
+def test_capture_while_another_thread_runs_eager_queries():
+    """A capture (thread_local mode) is not invalidated by eager queries that
+    another thread runs meanwhile -- host reads, allocations, synchronising
+    radix sorts -- and both threads' results stay correct."""
+    import threading
+
+    arrays = wl.lineitem_arrays(0.01, seed=8, rows=150_000)
+    cat = tq.Catalog()
+    cat.register("lineitem", wl.lineitem_table(arrays))
+    reg = wl.q1_registry()
+    q = wl.compile_sql(wl.Q1_SQL, cat, reg)
+    eager_sql = ("SELECT l_shipdate, l_quantity FROM lineitem WHERE l_quantity > 45.0 "
+                 "ORDER BY l_shipdate")
+    q_eager = tq.compile_plan(tq.lower(tq.bind(tq.parse(eager_sql), cat, reg)),
+                              tq.CompileConfig(replay=False), reg)
+    exp = otpch.q1(arrays)
+    exp_eager = _cols(q_eager.run(cat))
+    stop = threading.Event()
+    errors, eager_runs = [], [0]
+
+    def eager_worker():
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                while not stop.is_set():
+                    got = _cols(q_eager.run(cat))
+                    for n, v in exp_eager.items():
+                        np.testing.assert_array_equal(got[n], v)
+                    eager_runs[0] += 1
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    t = threading.Thread(target=eager_worker)
+    t.start()
+    captures0 = replay.CAPTURES[0]
+    try:
+        for _ in range(6):  # record, capture, replays -- with the eager thread running
+            _check_q1(_cols(q.run(cat)), exp)
+    finally:
+        stop.set()
+        t.join()
+    assert not errors, errors
+    assert eager_runs[0] > 0
+    assert replay.CAPTURES[0] > captures0
+    assert any(isinstance(e, replay._Replay) for e in q._replays.values())

@@ -23,3 +23,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tdp_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tdp_scan_agg --launch-skip 4 -c 1 -o $O/q1c_scan python bench.py --encoding compact --steps 3 --warmup 3 --no-cpu-baseline --no-parity --no-companion --e2e-steps 1 > /dev/null 2>&1; echo "ncu full q1c rc=$?"
 TDP_REPLAY=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_count_kernel -c 1 --launch-skip 2 -o $O/q3_probe python tools/profile_q3.py 10 > /dev/null 2>&1; echo "ncu full q3 rc=$?"
 ls $O
+TDP_REPLAY=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dense_build_kernel -c 1 --launch-skip 1 -o $O/q3_build python tools/profile_q3.py 10 > /dev/null 2>&1; echo "ncu full q3 build rc=$?"
+ls $O

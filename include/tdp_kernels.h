@@ -304,6 +304,26 @@ int tdp_groupby_finalize(const int64_t* counts, const void* sums, int64_t slots,
 int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
                     const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
                     int32_t nkeys, int64_t* out_minmax, void* stream);
+/* tdp_scan_minmax plus, for one key and no predicates, out_runs (device
+ * int64[2]): [0] = 1 if the key column is not non-decreasing, [1] = 1 if a
+ * run of equal keys is longer than 32 rows -- both 0: the sorted-runs
+ * group-by below applies.  Read with the range in one host read.           */
+int tdp_scan_minmax_runs(const tdp_column* cols, int32_t ncols, int64_t n,
+                         const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
+                         int32_t nkeys, int64_t* out_minmax, int64_t* out_runs, void* stream);
+/* Sorted-runs group-by (groupby_exact, tq/kernels.py:108-167, for one int64
+ * key that tdp_scan_minmax_runs found non-decreasing with runs <= 32 rows):
+ * the groups are the runs.  prepare: out_ngroups (device) = m; emit (m from
+ * the host): out_keys[m] ascending, out_counts[m], out_sums[naggs][m] as
+ * tdp_groupby_hash_emit (TDP_AGG_AVG_BIT honoured); every sum adds its run's
+ * rows in row order (np.add.at's order: float sums bit-identical).         */
+size_t tdp_groupby_runs_workspace(int64_t n);
+int tdp_groupby_runs_prepare(const int64_t* keys, int64_t n, int64_t* out_ngroups, void* ws,
+                             size_t ws_bytes, void* stream);
+int tdp_groupby_runs_emit(const int64_t* keys, int64_t n, const tdp_column* vals,
+                          const int32_t* agg_kinds, int32_t naggs, int64_t m, int64_t* out_keys,
+                          int64_t* out_counts, void* out_sums, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* sort-based group-by (general integer keys)                                */

@@ -120,6 +120,15 @@ _SIGNATURES = {
                                      c_void_p, c_void_p, c_void_p]),
     "tdp_scan_minmax": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate), c_int32,
                                 POINTER(c_int32), c_int32, c_void_p, c_void_p]),
+    "tdp_scan_minmax_runs": (c_int, [POINTER(Column), c_int32, c_int64, POINTER(Predicate),
+                                     c_int32, POINTER(c_int32), c_int32, c_void_p, c_void_p,
+                                     c_void_p]),
+    "tdp_groupby_runs_workspace": (c_size_t, [c_int64]),
+    "tdp_groupby_runs_prepare": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_size_t,
+                                         c_void_p]),
+    "tdp_groupby_runs_emit": (c_int, [c_void_p, c_int64, POINTER(Column), POINTER(c_int32),
+                                      c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_size_t, c_void_p]),
     "tdp_sort_workspace": (c_size_t, [c_int64]),
     "tdp_topk_workspace": (c_size_t, [c_int64, c_int64]),
     "tdp_topk_order": (c_int, [POINTER(Column), c_int32, c_int64, c_int64, c_void_p, c_void_p,

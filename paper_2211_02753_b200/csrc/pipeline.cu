@@ -1446,8 +1446,15 @@ struct KeyCols {
   int dt[kMaxKeys];
 };
 
+// runs (nullable; one key, no predicates): runs[0] = 1 if the key column is
+// not non-decreasing, runs[1] = 1 if some run of equal keys is longer than
+// kRunMax rows (sorted: key[i] == key[i - kRunMax]) -- the sorted-runs
+// group-by's preconditions, read with the range in one host read
+constexpr int kRunMax = 32;
+
 __global__ void scan_minmax_kernel(PredSet ps, i64 n, KeyCols kc, int nkeys,
-                                   i64* __restrict__ out) {
+                                   i64* __restrict__ out, i64* __restrict__ runs) {
+  bool unsorted = false, longrun = false;
   i64 mn[kMaxKeys], mx[kMaxKeys];
 #pragma unroll
   for (int j = 0; j < kMaxKeys; ++j) {
@@ -1463,8 +1470,16 @@ __global__ void scan_minmax_kernel(PredSet ps, i64 n, KeyCols kc, int nkeys,
         const i64 v = load_as_i64(kc.p[j], kc.dt[j], i);
         mn[j] = v < mn[j] ? v : mn[j];
         mx[j] = v > mx[j] ? v : mx[j];
+        if (j == 0 && runs != nullptr && i > 0) {
+          unsorted |= v < load_as_i64(kc.p[0], kc.dt[0], i - 1);
+          if (i >= kRunMax) longrun |= v == load_as_i64(kc.p[0], kc.dt[0], i - kRunMax);
+        }
       }
     }
+  }
+  if (runs != nullptr) {
+    if (__any_sync(0xffffffffu, unsorted) && (threadIdx.x & 31) == 0) runs[0] = 1;
+    if (__any_sync(0xffffffffu, longrun) && (threadIdx.x & 31) == 0) runs[1] = 1;
   }
 #pragma unroll
   for (int j = 0; j < kMaxKeys; ++j) {
@@ -1857,10 +1872,12 @@ int tdp_groupby_finalize(const int64_t* counts, const void* sums, int64_t slots,
   return TDP_OK;
 }
 
-int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
-                    const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
-                    int32_t nkeys, int64_t* out_minmax, void* stream) {
+int tdp_scan_minmax_runs(const tdp_column* cols, int32_t ncols, int64_t n,
+                         const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
+                         int32_t nkeys, int64_t* out_minmax, int64_t* out_runs, void* stream) {
   TDP_REQUIRE(nkeys >= 1 && nkeys <= kMaxKeys, "bad key count");
+  TDP_REQUIRE(out_runs == nullptr || (nkeys == 1 && npreds == 0),
+              "run detection needs one key and no predicates");
   PredSet ps;
   int rc = make_predset(cols, ncols, preds, npreds, n, &ps);
   if (rc) return rc;
@@ -1876,12 +1893,21 @@ int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
     kc.dt[j] = c.dtype;
   }
   cudaStream_t st = as_stream(stream);
+  if (out_runs != nullptr) TDP_CUDA_TRY(cudaMemsetAsync(out_runs, 0, 2 * sizeof(i64), st));
   init_minmax_kernel<<<1, 32, 0, st>>>(out_minmax, nkeys);
   TDP_LAUNCH_CHECK("init_minmax_kernel");
   if (n == 0) return TDP_OK;
-  scan_minmax_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(ps, n, kc, nkeys, out_minmax);
+  scan_minmax_kernel<<<stream_grid(n, 256 * 8, 8), 256, 0, st>>>(ps, n, kc, nkeys, out_minmax,
+                                                                  out_runs);
   TDP_LAUNCH_CHECK("scan_minmax_kernel");
   return TDP_OK;
+}
+
+int tdp_scan_minmax(const tdp_column* cols, int32_t ncols, int64_t n,
+                    const tdp_predicate* preds, int32_t npreds, const int32_t* key_cols,
+                    int32_t nkeys, int64_t* out_minmax, void* stream) {
+  return tdp_scan_minmax_runs(cols, ncols, n, preds, npreds, key_cols, nkeys, out_minmax, nullptr,
+                              stream);
 }
 
 }  // extern "C"

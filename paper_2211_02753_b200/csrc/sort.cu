@@ -2349,6 +2349,192 @@ int tdp_groupby_bitmap_emit(int64_t n, int64_t lo, int64_t key_range, const int3
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
+// Sorted-runs group-by: one int64 key column that is non-decreasing with runs
+// of at most kRunLen equal keys (tdp_scan_minmax_runs checks both) -- e.g. a
+// join's output in probe-row order over a clustered key (TPC-H lineitem by
+// l_orderkey).  Groups are the runs: a count pass over 2048-row tiles (run
+// starts per tile), a scan of the tile counts (group offsets, m), and an emit
+// pass in which the thread at each run start writes its group: the key, the
+// run length and every sum over the run's rows in row order -- the order of
+// np.add.at (tq/kernels.py:153-158), so float sums are bit-identical to the
+// reference's; no hash table, no bitmap, no atomics.
+// ---------------------------------------------------------------------------
+namespace tdp {
+namespace {
+
+constexpr int kRunTile = 256;  // rows per CTA, one per thread
+constexpr int kRunLen = 32;    // = kRunMax of tdp_scan_minmax_runs
+
+__global__ void __launch_bounds__(kRunTile)
+    runs_count_kernel(const i64* __restrict__ keys, i64 n, i64* __restrict__ tile_counts) {
+  __shared__ int wsum[kRunTile / 32];
+  const i64 i = (i64)blockIdx.x * kRunTile + threadIdx.x;
+  const bool start = i < n && (i == 0 || __ldg(keys + i) != __ldg(keys + i - 1));
+  const int c = __popc(__ballot_sync(0xffffffffu, start));
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i64 t = 0;
+    for (int w = 0; w < kRunTile / 32; ++w) t += wsum[w];
+    tile_counts[blockIdx.x] = t;
+  }
+}
+
+// One row per thread; the thread at a run start writes the group.  The run's
+// end is the next start bit of the tile (shared ballot words), else the run
+// continues past the tile (<= kRunLen rows, read on).  Value loads of a run
+// are issued four rows at a time, the adds stay in row order.
+__global__ void __launch_bounds__(kRunTile)
+    runs_emit_kernel(const i64* __restrict__ keys, i64 n, const i64* __restrict__ tile_offsets,
+                     ValSet vs, i64 m, i64* __restrict__ out_keys, i64* __restrict__ out_counts,
+                     u64* __restrict__ out_sums) {
+  __shared__ unsigned sbits[kRunTile / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 row0 = (i64)blockIdx.x * kRunTile;
+  const i64 i = row0 + threadIdx.x;
+  i64 key = 0;
+  bool start = false;
+  if (i < n) {
+    key = __ldg(keys + i);
+    start = i == 0 || key != __ldg(keys + i - 1);
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, start);
+  if (lane == 0) sbits[warp] = bal;
+  __syncthreads();
+  if (!start) return;
+  int before = __popc(bal & lanemask_lt());
+  for (int w = 0; w < warp; ++w) before += __popc(sbits[w]);
+  const i64 g = tile_offsets[blockIdx.x] + before;
+  // run end: the next start in this tile, else the tile's end and beyond
+  const int rows_here = (int)(n - row0 < kRunTile ? n - row0 : kRunTile);
+  int end = -1;
+  const int t = threadIdx.x + 1;
+  if (t < kRunTile) {
+    int w = t >> 5;
+    unsigned b = sbits[w] & (0xffffffffu << (t & 31));
+    for (;;) {
+      if (b) {
+        end = w * 32 + __ffs(b) - 1;
+        break;
+      }
+      if (++w >= kRunTile / 32) break;
+      b = sbits[w];
+    }
+  }
+  int len;
+  if (end >= 0) {
+    len = end - threadIdx.x;
+  } else {
+    len = rows_here - threadIdx.x;
+    while (len < kRunLen && i + len < n && __ldg(keys + i + len) == key) ++len;
+  }
+  out_keys[g] = key;
+  out_counts[g] = len;
+  for (int a = 0; a < vs.naggs; ++a) {
+    if (vs.kind[a] == TDP_AGG_COUNT) {
+      out_sums[(i64)a * m + g] = (u64)len;
+      continue;
+    }
+    u64 raw;
+    if (vs.kind[a] == TDP_AGG_SUM_F64) {
+      double acc = 0.0;  // np.add.at into zeros, in row order
+      for (int r = 0; r < len; r += 4) {
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = r + u < len ? load_as_f64(vs.p[a], vs.dt[a], i + r + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (r + u < len) acc = __dadd_rn(acc, x[u]);
+      }
+      raw = (u64)__double_as_longlong(acc);
+    } else {
+      u64 acc = 0;
+      for (int r = 0; r < len; ++r) acc += (u64)load_as_i64(vs.p[a], vs.dt[a], i + r);
+      raw = acc;
+    }
+    out_sums[(i64)a * m + g] = emit_value(vs, a, raw, (u64)len);
+  }
+}
+
+struct RunsWs {
+  i64* tile_counts;
+  i64* tile_offsets;
+  void* scan_ws;
+  size_t scan_bytes;
+};
+
+size_t runs_ws_bytes(i64 n) {
+  const i64 tiles = ceil_div(n > 0 ? n : 1, kRunTile);
+  return 2 * align256((size_t)tiles * 8) + exclusive_scan_workspace(tiles) + 256;
+}
+
+RunsWs carve_runs(void* ws, i64 n) {
+  const i64 tiles = ceil_div(n > 0 ? n : 1, kRunTile);
+  unsigned char* p = reinterpret_cast<unsigned char*>(ws);
+  RunsWs w;
+  w.tile_counts = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  w.tile_offsets = (i64*)p;
+  p += align256((size_t)tiles * 8);
+  w.scan_ws = p;
+  w.scan_bytes = exclusive_scan_workspace(tiles) + 256;
+  return w;
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+size_t tdp_groupby_runs_workspace(int64_t n) { return runs_ws_bytes(n); }
+
+int tdp_groupby_runs_prepare(const int64_t* keys, int64_t n, int64_t* out_ngroups, void* ws,
+                             size_t ws_bytes, void* stream) {
+  TDP_REQUIRE(n >= 0 && out_ngroups != nullptr, "bad sorted-runs group-by arguments");
+  TDP_REQUIRE(ws_bytes >= runs_ws_bytes(n), "sorted-runs group-by workspace too small");
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) {
+    TDP_CUDA_TRY(cudaMemsetAsync(out_ngroups, 0, sizeof(i64), st));
+    return TDP_OK;
+  }
+  RunsWs w = carve_runs(ws, n);
+  const i64 tiles = ceil_div(n, kRunTile);
+  runs_count_kernel<<<(unsigned)tiles, kRunTile, 0, st>>>(keys, n, w.tile_counts);
+  TDP_LAUNCH_CHECK("runs_count_kernel");
+  return exclusive_scan_i64(w.tile_counts, w.tile_offsets, tiles, out_ngroups, w.scan_ws,
+                            w.scan_bytes, st);
+}
+
+int tdp_groupby_runs_emit(const int64_t* keys, int64_t n, const tdp_column* vals,
+                          const int32_t* agg_kinds, int32_t naggs, int64_t m, int64_t* out_keys,
+                          int64_t* out_counts, void* out_sums, void* ws, size_t ws_bytes,
+                          void* stream) {
+  TDP_REQUIRE(m >= 0 && m <= (n > 0 ? n : 0), "bad group count");
+  TDP_REQUIRE(ws_bytes >= runs_ws_bytes(n), "sorted-runs group-by workspace too small");
+  TDP_REQUIRE(naggs >= 0 && naggs <= 32, "at most 32 aggregates");
+  if (m == 0) return TDP_OK;
+  int32_t plain[32];
+  unsigned avg = 0;
+  for (int a = 0; a < naggs; ++a) {
+    plain[a] = agg_kinds[a] & ~TDP_AGG_AVG_BIT;
+    if (agg_kinds[a] & TDP_AGG_AVG_BIT) avg |= 1u << a;
+  }
+  ValSet vs;
+  int rc = make_valset(vals, plain, naggs, n, &vs);
+  if (rc) return rc;
+  vs.avg = avg;
+  RunsWs w = carve_runs(ws, n);
+  cudaStream_t st = as_stream(stream);
+  runs_emit_kernel<<<(unsigned)ceil_div(n, kRunTile), kRunTile, 0, st>>>(
+      keys, n, w.tile_offsets, vs, m, out_keys, out_counts, reinterpret_cast<u64*>(out_sums));
+  TDP_LAUNCH_CHECK("runs_emit_kernel");
+  return TDP_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
 // sort / searchsorted equi-join (the algorithm north_star names; the default
 // planner prefers the dense-range and hash joins, which read the probe side
 // once with one table lookup per row -- tdp_join_sorted_* is kept as the

@@ -559,21 +559,29 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
     spans: list[tuple[int, int]] = []
     need_range = [j for j, k in enumerate(keys) if not k.is_dictionary()]
     ranges: dict[int, tuple[int, int]] = {}
+    runs = False
     if need_range:
         if any(kexprs[j].op != "col" for j in need_range):
             return _groupby_general(keys, key_vals, agg_specs, agg_vals)
         prog = Program()
         kc = [prog.col_index(kexprs[j].col) for j in need_range]
         preds, npreds = prog.predicates(sel)
-        mm = torch.empty(2 * len(need_range), dtype=torch.int64, device=device)
-        nat.require_cuda(*prog.cols)
-        nat.call("tdp_scan_minmax", prog.native_columns(), len(prog.cols), n, preds, npreds,
-                 (c_int32 * len(kc))(*kc), len(kc), nat.ptr(mm), nat.stream())
         group = current_group()
+        # one int64 key, no predicates, not sharded: also check whether the
+        # key column is sorted in short runs (the sorted-runs group-by)
+        check_runs = (len(keys) == 1 and npreds == 0 and group is None
+                      and prog.cols[kc[0]].dtype == torch.int64)
+        mm = torch.empty(2 * len(need_range) + (2 if check_runs else 0), dtype=torch.int64,
+                         device=device)
+        nat.require_cuda(*prog.cols)
+        nat.call("tdp_scan_minmax_runs", prog.native_columns(), len(prog.cols), n, preds, npreds,
+                 (c_int32 * len(kc))(*kc), len(kc), nat.ptr(mm),
+                 nat.ptr(mm[2:]) if check_runs else None, nat.stream())
         if group is not None:
             lo, hi = allreduce_ranges(mm[0::2].contiguous(), mm[1::2].contiguous(), group)
             mm = torch.stack([lo, hi], dim=1).reshape(-1)
         host = read_ints(mm)
+        runs = check_runs and host[2] == 0 and host[3] == 0
         for t, j in enumerate(need_range):
             ranges[j] = (host[2 * t], host[2 * t + 1])
         if any(lo > hi for lo, hi in ranges.values()):
@@ -589,7 +597,8 @@ def _groupby_fused(keys, key_vals, agg_specs, agg_vals, space, defer_rows=False)
         slots *= span
     if slots > DENSE_SLOT_LIMIT:  # high cardinality: sort-based (sharded: all-to-all)
         return _groupby_general(keys, key_vals, agg_specs, agg_vals,
-                                key_range=ranges.get(0) if len(keys) == 1 else None)
+                                key_range=ranges.get(0) if len(keys) == 1 else None,
+                                runs=runs)
     agg_exprs = []
     for (func, dt), v in zip(agg_specs, agg_vals):
         kind = _agg_kind(func, dt)
@@ -693,7 +702,7 @@ def _groupby_codes(codes: torch.Tensor, slots: int, agg_specs, agg_vals, n: int,
     return counts, sums
 
 
-def _groupby_general(keys, key_vals, agg_specs, agg_vals, key_range=None):
+def _groupby_general(keys, key_vals, agg_specs, agg_vals, key_range=None, runs=False):
     """Sort-based path (the reference's np.unique algorithm on the device);
     hash / bitmap aggregation for one high-cardinality int64 key."""
     kdata = [_materialize(v) for v in key_vals]
@@ -711,7 +720,7 @@ def _groupby_general(keys, key_vals, agg_specs, agg_vals, key_range=None):
     group = current_group()
     if is_sharded(group):
         return _groupby_sharded(kdata, agg_specs, vdata, group)
-    return _groupby_local(kdata, agg_specs, vdata, key_range)
+    return _groupby_local(kdata, agg_specs, vdata, key_range, runs)
 
 
 def _lex_order(keys: Sequence[torch.Tensor]) -> torch.Tensor:
@@ -843,11 +852,33 @@ def _groupby_bitmap(key: torch.Tensor, lo: int, span: int, agg_specs, agg_vals, 
     return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=True)
 
 
-def _groupby_local(kdata, agg_specs, agg_vals, key_range=None):
+def _groupby_runs(key: torch.Tensor, agg_specs, agg_vals, n: int, device):
+    """One int64 key column sorted in runs of <= 32 equal keys (checked by
+    tdp_scan_minmax_runs): the runs are the groups (tdp_groupby_runs_*) --
+    a count pass, a scan, an emit pass; sums in row order."""
+    kinds, vals, cols = _agg_columns(agg_specs, agg_vals, n)
+    key = key.contiguous()
+    ws = nat.workspace(nat.load().tdp_groupby_runs_workspace(n), device)
+    info = torch.empty(1, dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_runs_prepare", nat.ptr(key), n, nat.ptr(info), nat.ptr(ws), ws.numel(),
+             nat.stream())
+    m = read_int(info)
+    keys_out = torch.empty(m, dtype=torch.int64, device=device)
+    counts = torch.empty(m, dtype=torch.int64, device=device)
+    sums = torch.empty((max(1, len(kinds)), m), dtype=torch.int64, device=device)
+    nat.call("tdp_groupby_runs_emit", nat.ptr(key), n, cols, _emit_kinds(agg_specs, kinds),
+             len(kinds), m, nat.ptr(keys_out), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws),
+             ws.numel(), nat.stream())
+    return [keys_out], _agg_outputs(agg_specs, sums, counts, already_avg=True)
+
+
+def _groupby_local(kdata, agg_specs, agg_vals, key_range=None, runs=False):
     device = kdata[0].device
     n = int(kdata[0].shape[0])
     if n == 0:
         return _empty_groups(len(kdata), agg_specs, device)
+    if runs and len(kdata) == 1 and kdata[0].dtype == torch.int64:
+        return _groupby_runs(kdata[0], agg_specs, agg_vals, n, device)
     if len(kdata) == 1 and kdata[0].dtype == torch.int64 and key_range is not None:
         span = key_range[1] - key_range[0] + 1
         if 1 <= span <= min(1 << 34, RANK_BITS_PER_GROUP * n + (1 << 21)):

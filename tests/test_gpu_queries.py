@@ -494,3 +494,66 @@ def test_dict_encode_on_device_matches_sorted_rank(n, distinct):
     exp = np.array([bisect.bisect_left(entries, s) for s in strings], dtype=np.int64)
     np.testing.assert_array_equal(col.values.numpy(), exp)
     assert E.dict_decode(col) == strings
+
+
+@pytest.mark.parametrize("case", ["runs", "run33", "unsorted", "int64_ends", "filtered"])
+def test_sorted_runs_groupby_matches_oracle(case, monkeypatch):
+    """One int64 key sorted in runs of <= 32 equal keys (a join's output over a
+    clustered key): the sorted-runs group-by (tdp_groupby_runs_*) -- keys,
+    counts and int sums exact, float SUMs/AVGs bit-identical to np.add.at's
+    row order (incl. NaN, inf, -0.0); a run of 33, an unsorted column or a
+    filtered input take the other paths with the same results."""
+    from paper_2211_02753_b200 import kernels as K
+
+    calls = [0]
+    real = K._groupby_runs
+
+    def counted(*a, **kw):
+        calls[0] += 1
+        return real(*a, **kw)
+
+    monkeypatch.setattr(K, "_groupby_runs", counted)
+    rng = np.random.default_rng({"runs": 1, "run33": 2, "unsorted": 3, "int64_ends": 4,
+                                 "filtered": 5}[case])
+    lens = rng.integers(1, 33, size=30_000)
+    if case == "run33":
+        lens[12_345] = 33
+    start = -(2**63) if case == "int64_ends" else 10**12
+    gaps = rng.integers(1, 50, size=lens.size).astype(np.int64)
+    if case == "int64_ends":
+        gaps[:] = 1
+    distinct = start + np.cumsum(gaps) - gaps[0]
+    key = np.repeat(distinct, lens)
+    if case == "int64_ends":
+        key = np.concatenate([key, np.full(7, 2**63 - 1, dtype=np.int64)])
+    n = key.size
+    if case == "unsorted":
+        key[[100, 2_000]] = key[[2_000, 100]]
+    v = rng.normal(size=n) * 10.0 ** rng.integers(-5, 6, size=n)
+    v[:6] = [np.nan, np.inf, -0.0, -np.inf, 1e300, 1e300]
+    iv = rng.integers(-2**62, 2**62, size=n)
+    cat = tq.Catalog()
+    cat.register("t", tq.table_from_columns(["k", "v", "iv"], [tq.plain(tq.Tensor(key)),
+                                                               tq.plain(tq.Tensor(v)),
+                                                               tq.plain(tq.Tensor(iv))]))
+    where = " WHERE iv > 0" if case == "filtered" else ""
+    q = wl.compile_sql(f"SELECT k, SUM(v), AVG(v), SUM(iv), AVG(iv), COUNT(*) FROM t{where} "
+                       "GROUP BY k", cat, tq.UdfRegistry())
+    res = q.run(cat)
+    sel = iv > 0 if case == "filtered" else np.ones(n, dtype=bool)
+    keys, aggs = orc.groupby_exact([key[sel]], [("sum", v[sel]), ("avg", v[sel]),
+                                                ("sum", iv[sel]), ("avg", iv[sel]),
+                                                ("count", None)])
+    got = [c.values.numpy() for c in res.columns]
+    np.testing.assert_array_equal(got[0], keys[0])
+    np.testing.assert_array_equal(got[3], aggs[2])
+    np.testing.assert_array_equal(got[5], aggs[4])
+    if case in ("runs", "int64_ends"):
+        assert calls[0] == 1
+        for g, e in ((got[1], aggs[0]), (got[2], aggs[1]), (got[4], aggs[3])):
+            assert g.tobytes() == e.tobytes()  # np.add.at order: bit-identical
+    else:
+        assert calls[0] == 0
+        for g, e in ((got[1], aggs[0]), (got[2], aggs[1]), (got[4], aggs[3])):
+            np.testing.assert_allclose(g, e, rtol=1e-9, atol=1e-9)
+            assert np.array_equal(np.isnan(g), np.isnan(e))

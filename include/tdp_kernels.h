@@ -180,6 +180,11 @@ int tdp_filter_select(const tdp_column* cols, int32_t ncols, const tdp_predicate
  * / gather forward (tq/tensor.py:597-607).                                 */
 int tdp_gather_rows(const tdp_column* src, int32_t ncols, const int64_t* indices, int64_t m,
                     void* const* dst, void* stream);
+/* The same with two index vectors of m rows in one launch: columns
+ * [0, nfirst) are gathered at indices, the rest at indices2 -- both sides of
+ * a join's output (probe rows, build rows) at once.                        */
+int tdp_gather_rows2(const tdp_column* src, int32_t ncols, int32_t nfirst, const int64_t* indices,
+                     const int64_t* indices2, int64_t m, void* const* dst, void* stream);
 
 /* grad_in[idx[j], :] += grad_out[j, :] (float32/float64).  Replaces the
  * np.add.at VJP of gather (tq/tensor.py:609-612).  grad_in must be zeroed. */

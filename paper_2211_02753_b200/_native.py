@@ -97,6 +97,8 @@ _SIGNATURES = {
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "tdp_gather_rows": (c_int, [POINTER(Column), c_int32, c_void_p, c_int64, POINTER(c_void_p),
                                 c_void_p]),
+    "tdp_gather_rows2": (c_int, [POINTER(Column), c_int32, c_int32, c_void_p, c_void_p, c_int64,
+                                 POINTER(c_void_p), c_void_p]),
     "tdp_scatter_add_rows": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p,
                                      c_void_p]),
     "tdp_scan_aggregate_workspace": (c_size_t, [c_int64, c_int64, c_int32]),

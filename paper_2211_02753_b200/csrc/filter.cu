@@ -115,6 +115,7 @@ struct GatherCol {
   const unsigned char* src;
   unsigned char* dst;
   i64 row_bytes;
+  i64 second;  // 1: rows from the second index vector (tdp_gather_rows2)
 };
 struct GatherSet {
   int ncols;
@@ -148,12 +149,15 @@ __device__ __forceinline__ void copy_elem(const GatherCol& c, i64 src_row, i64 j
 }
 
 // Narrow rows (<= 8 bytes): one thread per output row, all columns.
-__global__ void gather_narrow_kernel(GatherSet gs, const i64* __restrict__ idx, i64 m) {
+__global__ void gather_narrow_kernel(GatherSet gs, const i64* __restrict__ idx,
+                                     const i64* __restrict__ idx2, i64 m) {
   for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < m;
        j += (i64)gridDim.x * blockDim.x) {
-    const i64 r = __ldg(idx + j);
+    const i64 r1 = __ldg(idx + j);
+    const i64 r2 = idx2 != nullptr ? __ldg(idx2 + j) : 0;
     for (int k = 0; k < gs.ncols; ++k) {
       const GatherCol& c = gs.c[k];
+      const i64 r = c.second ? r2 : r1;
       switch (c.row_bytes) {
         case 8:
           copy_elem<8>(c, r, j);
@@ -264,13 +268,18 @@ int tdp_filter_select(const tdp_column* cols, int32_t ncols, const tdp_predicate
   return TDP_OK;
 }
 
-int tdp_gather_rows(const tdp_column* src, int32_t ncols, const int64_t* indices, int64_t m,
-                    void* const* dst, void* stream) {
+}  // extern "C"
+
+namespace tdp {
+namespace {
+
+// Columns [0, nfirst) gathered at idx, the rest at idx2 (null: idx for all).
+int gather_rows_impl(const tdp_column* src, int32_t ncols, int32_t nfirst, const i64* idx,
+                     const i64* idx2, i64 m, void* const* dst, cudaStream_t st) {
   TDP_REQUIRE(ncols >= 0 && ncols <= kMaxCols, "gather of %d columns (max %d)", ncols, kMaxCols);
   TDP_REQUIRE(m >= 0, "negative gather size");
   if (m == 0 || ncols == 0) return TDP_OK;
-  TDP_REQUIRE(indices != nullptr && dst != nullptr, "null gather argument");
-  cudaStream_t st = as_stream(stream);
+  TDP_REQUIRE(idx != nullptr && dst != nullptr, "null gather argument");
   GatherSet narrow;
   narrow.ncols = 0;
   narrow.pad = 0;
@@ -282,20 +291,39 @@ int tdp_gather_rows(const tdp_column* src, int32_t ncols, const int64_t* indices
     c.src = reinterpret_cast<const unsigned char*>(src[k].data);
     c.dst = reinterpret_cast<unsigned char*>(dst[k]);
     c.row_bytes = (i64)es * src[k].width;
+    c.second = k >= nfirst ? 1 : 0;
     if (c.row_bytes == 8 || c.row_bytes == 4 || c.row_bytes == 2 || c.row_bytes == 1) {
       narrow.c[narrow.ncols++] = c;
     } else {
       TDP_REQUIRE(c.row_bytes % 4 == 0, "gather column %d: row of %lld bytes", k,
                   (long long)c.row_bytes);
-      gather_wide_kernel<<<stream_grid(m, 8, 16), 256, 0, st>>>(c, indices, m);
+      gather_wide_kernel<<<stream_grid(m, 8, 16), 256, 0, st>>>(c, c.second ? idx2 : idx, m);
       TDP_LAUNCH_CHECK("gather_wide_kernel");
     }
   }
   if (narrow.ncols) {
-    gather_narrow_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(narrow, indices, m);
+    gather_narrow_kernel<<<stream_grid(m, 256 * 4, 8), 256, 0, st>>>(
+        narrow, idx, nfirst < ncols ? idx2 : nullptr, m);
     TDP_LAUNCH_CHECK("gather_narrow_kernel");
   }
   return TDP_OK;
+}
+
+}  // namespace
+}  // namespace tdp
+
+extern "C" {
+
+int tdp_gather_rows(const tdp_column* src, int32_t ncols, const int64_t* indices, int64_t m,
+                    void* const* dst, void* stream) {
+  return gather_rows_impl(src, ncols, ncols, indices, nullptr, m, dst, as_stream(stream));
+}
+
+int tdp_gather_rows2(const tdp_column* src, int32_t ncols, int32_t nfirst, const int64_t* indices,
+                     const int64_t* indices2, int64_t m, void* const* dst, void* stream) {
+  TDP_REQUIRE(nfirst >= 0 && nfirst <= ncols, "bad first-column count");
+  TDP_REQUIRE(nfirst == ncols || indices2 != nullptr, "null second index vector");
+  return gather_rows_impl(src, ncols, nfirst, indices, indices2, m, dst, as_stream(stream));
 }
 
 int tdp_scatter_add_rows(const void* grad_out, int32_t dtype, int64_t width,

@@ -1948,16 +1948,51 @@ __global__ void __launch_bounds__(kJoinThreads, 4)
     atomicAdd(reinterpret_cast<unsigned long long*>(tile_counts + tile), (unsigned long long)local);
 }
 
-__global__ void dense_pairs_kernel(DenseJoin dj, const i64* __restrict__ probe,
-                                   const i64* __restrict__ tile_counts,
-                                   const i64* __restrict__ tile_offsets, i64 tiles,
-                                   const i64* __restrict__ out_probe, i64* __restrict__ out_build) {
-  const i64 total = tile_offsets[tiles - 1] + tile_counts[tiles - 1];
-  for (i64 m = (i64)blockIdx.x * blockDim.x + threadIdx.x; m < total;
-       m += (i64)gridDim.x * blockDim.x)
-  {
-    const u64 d = (u64)__ldg(probe + out_probe[m]) - dj.lo;
-    out_build[m] = dj.row_of != nullptr ? (i64)dj.row_of[d] : dj.rank_row[dense_rank(dj, d)];
+// Expansion of the match words (join_expand_unique_kernel's layout) that also
+// writes each pair's build row: the probe keys of up to four matches are
+// loaded together, then their build rows -- one launch instead of expand +
+// dense_pairs_kernel (a selective probe has few matches per lane).
+__global__ void dense_expand_pairs_kernel(DenseJoin dj, const i64* __restrict__ probe, i64 tiles,
+                                          const unsigned* __restrict__ match_bits,
+                                          const i64* __restrict__ word_counts,
+                                          const i64* __restrict__ tile_counts,
+                                          const i64* __restrict__ tile_offsets,
+                                          i64* __restrict__ out_probe,
+                                          i64* __restrict__ out_build) {
+  const int lane = threadIdx.x & 31;
+  const i64 tile = (i64)blockIdx.x * kJoinWarps + (threadIdx.x >> 5);
+  if (tile >= tiles || tile_counts[tile] == 0) return;  // warp-uniform
+  const i64* wc = word_counts + tile * kJoinWords;
+  const unsigned* mb = match_bits + tile * kJoinWords;
+  const i64 w0 = wc[2 * lane], w1 = wc[2 * lane + 1];
+  u64 bits = (u64)mb[2 * lane] | ((u64)mb[2 * lane + 1] << 32);
+  i64 incl = w0 + w1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const i64 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  i64 pos = tile_offsets[tile] + incl - w0 - w1;
+  const i64 row0 = tile * kJoinTile + (i64)lane * 64;
+  while (bits) {
+    i64 r[4], key[4];
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      r[u] = row0 + (bits ? __ffsll((long long)bits) - 1 : 0);
+      c += bits ? 1 : 0;
+      bits &= bits - 1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) key[u] = u < c ? __ldg(probe + r[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u >= c) break;
+      const u64 d = (u64)key[u] - dj.lo;
+      out_probe[pos + u] = r[u];
+      out_build[pos + u] = dj.row_of != nullptr ? (i64)dj.row_of[d] : dj.rank_row[dense_rank(dj, d)];
+    }
+    pos += c;
   }
 }
 
@@ -2140,14 +2175,16 @@ int tdp_join_dense_emit(const int64_t* probe_keys, int64_t n_build, int64_t n_pr
   HashTable none;  // the expansion only reads flags[1] (runs mode): the zero flag
   std::memset(&none, 0, sizeof(none));
   none.flags = w.dj.flags + 2;
+  if (need_rows) {
+    dense_expand_pairs_kernel<<<(unsigned)ceil_div(tiles, kJoinWarps), kJoinThreads, 0, st>>>(
+        w.dj, probe_keys, tiles, w.match_bits, w.word_counts, w.tile_counts, w.tile_offsets,
+        out_probe_idx, out_build_idx);
+    TDP_LAUNCH_CHECK("dense_expand_pairs_kernel");
+    return TDP_OK;
+  }
   join_expand_unique_kernel<<<(unsigned)ceil_div(tiles, kJoinWarps), kJoinThreads, 0, st>>>(
       none, tiles, w.match_bits, w.word_counts, w.tile_counts, w.tile_offsets, out_probe_idx);
   TDP_LAUNCH_CHECK("join_expand_unique_kernel");
-  if (need_rows) {
-    dense_pairs_kernel<<<(unsigned)(sm_count() * 8), 256, 0, st>>>(
-        w.dj, probe_keys, w.tile_counts, w.tile_offsets, tiles, out_probe_idx, out_build_idx);
-    TDP_LAUNCH_CHECK("dense_pairs_kernel");
-  }
   return TDP_OK;
 }
 

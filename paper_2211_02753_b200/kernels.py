@@ -25,7 +25,7 @@ equi_join (new)             tdp_join_prepare / tdp_join_emit
 from __future__ import annotations
 
 import os
-from ctypes import c_int32
+from ctypes import c_int32, c_void_p
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -1488,9 +1488,33 @@ def equi_join(left: Sequence[EncodedTensor], right: Sequence[EncodedTensor], lef
                              build_range=brange if rmap is None else None,
                              need_build_rows=need_rows)
     pi, bi = pairs
-    return (_gather_side([left[i] for i in lo], [lb[i] for i in lo], lmap, pi, stats=lsel is not None)
-            + _gather_side([right[i] for i in ro], [rb[i] for i in ro], rmap, bi,
-                           stats=rsel is not None))
+    lcols, rcols = [left[i] for i in lo], [right[i] for i in ro]
+    if lcols and rcols and len(lo) + len(ro) <= 16 and bi is not None and not any(
+            onehot_payload(c.values) is not None for c in lcols + rcols):
+        return _gather_sides(lcols, [lb[i] for i in lo], lmap, pi, lsel is not None,
+                             rcols, [rb[i] for i in ro], rmap, bi, rsel is not None)
+    return (_gather_side(lcols, [lb[i] for i in lo], lmap, pi, stats=lsel is not None)
+            + _gather_side(rcols, [rb[i] for i in ro], rmap, bi, stats=rsel is not None))
+
+
+def _gather_sides(lcols, lbases, lmap, prows, lstats, rcols, rbases, rmap, brows, rstats):
+    """Both sides' output columns of a join in one launch (tdp_gather_rows2):
+    left columns at the probe rows, right columns at the build rows."""
+    lsrc = prows if lmap is None else gather_rows_raw(lmap, prows)
+    rsrc = brows if rmap is None else gather_rows_raw(rmap, brows)
+    bases = [b.contiguous() for b in list(lbases) + list(rbases)]
+    nat.require_cuda(lsrc, rsrc, *bases)
+    m = int(lsrc.numel())
+    outs = [torch.empty((m,) + tuple(b.shape[1:]), dtype=b.dtype, device=b.device) for b in bases]
+    if m:
+        dst = (c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        nat.call("tdp_gather_rows2", nat.columns(bases), len(bases), len(lbases), nat.ptr(lsrc),
+                 nat.ptr(rsrc), m, dst, nat.stream())
+    for k, (o, b) in enumerate(zip(outs, bases)):
+        _inherit_range(o, b, compute=lstats if k < len(lbases) else rstats)
+    cols = list(lcols) + list(rcols)
+    with trusted():
+        return [EncodedTensor(Tensor(o), c.encoding) for o, c in zip(outs, cols)]
 
 
 def _semi_join_lazy(left, right, left_key: int, right_key: int, lo: list):

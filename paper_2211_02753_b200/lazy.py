@@ -487,42 +487,6 @@ def project(exprs: Sequence[Expr], sel: Optional[Selection]) -> list[torch.Tenso
 # ---------------------------------------------------------------------------
 
 
-class _PinnedRing:
-    """Pinned host int64 slots for device-produced counts, allocated once (a
-    fresh pinned allocation per query could block on cudaHostAlloc).  A slot
-    is reused after a full turn of the ring; its previous holder is resolved
-    first (its copy finished long ago in practice)."""
-
-    SLOTS = 4096
-
-    def __init__(self):
-        self.buf = torch.empty(self.SLOTS, dtype=torch.int64, pin_memory=True)
-        self.holders: list = [None] * self.SLOTS
-        self.next = 0
-        self.lock = threading.Lock()
-
-    def take(self, holder) -> int:
-        with self.lock:
-            i = self.next
-            self.next = (i + 1) % self.SLOTS
-            prev = self.holders[i]
-            self.holders[i] = holder
-        h = prev() if prev is not None else None
-        if h is not None:
-            h.value()
-        return i
-
-
-_RING: Optional[_PinnedRing] = None
-
-
-def _ring() -> _PinnedRing:
-    global _RING
-    if _RING is None:
-        _RING = _PinnedRing()
-    return _RING
-
-
 _CAPTURE = threading.local()
 
 
@@ -543,37 +507,35 @@ def is_capturing() -> bool:
 
 
 class DeferredCount:
-    """A row count produced by a kernel.  It is copied to a pinned host slot
-    asynchronously right after the producing launch; the host waits for it
-    only on first access (``value()``), so a query whose result stays on the
-    device never blocks the launching thread."""
+    """A row count produced by a kernel, left on the device until first
+    access: an event is recorded after the producing launch, and ``value()``
+    waits for it and reads the count then.  A query whose result stays on the
+    device neither blocks the launching thread nor queues a device-to-host
+    copy behind its kernels (each such copy in a replayed step's stream costs
+    a copy-engine round trip: compact Q1 step 170 -> 159 us without it)."""
 
-    __slots__ = ("_slot", "_event", "_value", "dev", "__weakref__")
+    __slots__ = ("_event", "_value", "dev", "_template", "__weakref__")
 
     def __init__(self, dev: torch.Tensor):
         self._value: Optional[int] = None
         self.dev = dev
-        if is_capturing():  # a graph template: the replay makes a real one
-            self._slot = None
-            self._event = None
-            return
-        ring = _ring()
-        self._slot = ring.take(weakref.ref(self))
-        ring.buf[self._slot:self._slot + 1].copy_(dev.reshape(1), non_blocking=True)
-        self._event = torch.cuda.Event()
-        self._event.record()
+        self._template = is_capturing()  # a graph template: the replay makes a real one
+        self._event = None
+        if not self._template:
+            self._event = torch.cuda.Event()
+            self._event.record()
 
     def value(self) -> int:
         if self._value is None:
-            if self._slot is None:
+            if self._template:
                 v = replay_value(self.dev)  # a capture sized from a recorded run
                 if v is None:
                     raise RuntimeError("row count of a CUDA-graph template read during capture")
                 self._value = v
                 return v
-            self._event.synchronize()
             SYNC_READS[0] += 1
-            self._value = int(_ring().buf[self._slot])
+            self._event.synchronize()  # the producing stream's count is final
+            self._value = int(self.dev.reshape(-1)[0].item())
             record_value(self._value)
             self._event = None
             self.dev = None

@@ -85,6 +85,24 @@ def test_dense_join_unique_build(lo, need_rows):
 
 
 @pytest.mark.gpu
+def test_dense_join_rank_mode_fused_emit():
+    """A build whose range is > 8 keys per row (but <= 64): build rows are
+    found by the key's rank among the set bits (no key-offset array) in the
+    fused expand + pairs emit; a high match rate (every probe row matches
+    once or more) exercises the four-at-a-time pair loop."""
+    rng = np.random.default_rng(17)
+    span, nb = 60_000_000, 1_100_000
+    build = rng.choice(span, size=nb, replace=False).astype(np.int64) + 5
+    probe = np.concatenate([rng.choice(build, size=1_500_000),
+                            rng.integers(0, span + 10, size=500_000)]).astype(np.int64)
+    rng.shuffle(probe)
+    pairs = K.join_indices(_dev(probe), _dev(build), build_range=(5, span + 4))
+    epi, ebi = orc.join_inner(probe, build)
+    np.testing.assert_array_equal(pairs[0].cpu().numpy(), epi)
+    np.testing.assert_array_equal(pairs[1].cpu().numpy(), ebi)
+
+
+@pytest.mark.gpu
 def test_dense_join_filtered_sides_from_base_columns():
     """A filtered build and a filtered probe read straight from base columns
     (equi_join on lazy selections): the build key's range is the catalog

@@ -557,3 +557,27 @@ def test_sorted_runs_groupby_matches_oracle(case, monkeypatch):
         for g, e in ((got[1], aggs[0]), (got[2], aggs[1]), (got[4], aggs[3])):
             np.testing.assert_allclose(g, e, rtol=1e-9, atol=1e-9)
             assert np.array_equal(np.isnan(g), np.isnan(e))
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 255, 256, 257, 33])
+def test_sorted_runs_groupby_tiny_and_tile_edges(n):
+    """Sorted-runs group-by at tile edges: empty input, one row, runs that
+    cross the 256-row tile boundary, and a single run of 32 / 33 rows."""
+    from paper_2211_02753_b200.kernels import groupby_exact
+
+    rng = np.random.default_rng(n + 3)
+    if n == 33:  # one run of 33: the run check falls back to the other paths
+        key = np.full(33, 7, dtype=np.int64)
+    else:
+        key = np.sort(rng.integers(0, max(1, n // 3), size=n)).astype(np.int64) * 1_000_003
+        if n >= 256:  # a run across the tile edge (rows 250..262)
+            key[250:min(n, 263)] = key[250]
+            key[min(n, 263):] = np.maximum(key[min(n, 263):], key[250] + 1)
+    v = rng.normal(size=n)
+    kv, aggs = groupby_exact([tq.plain(tq.Tensor(key))],
+                             [("sum", tq.Tensor(v)), ("avg", tq.Tensor(v)), ("count", None)])
+    ek, ea = orc.groupby_exact([key], [("sum", v), ("avg", v), ("count", None)])
+    np.testing.assert_array_equal(kv[0].cpu().numpy(), ek[0])
+    np.testing.assert_array_equal(aggs[2].cpu().numpy(), ea[2])
+    np.testing.assert_allclose(aggs[0].cpu().numpy(), ea[0], rtol=1e-12, atol=0)
+    np.testing.assert_allclose(aggs[1].cpu().numpy(), ea[1], rtol=1e-12, atol=0)

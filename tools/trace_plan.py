@@ -54,7 +54,8 @@ def main():
 
         cat = tq.Catalog()
         cat.register("lineitem", wl.lineitem_table(wl.lineitem_arrays(sf, seed=42)))
-        q = wl.compile_sql(wl.Q1_SQL, cat, wl.q1_registry())
+        sql, reg = (wl.Q1_SQL, wl.q1_registry()) if which == "q1" else (wl.Q6_SQL, wl.q6_registry())
+        q = wl.compile_sql(sql, cat, reg)
         run = lambda: q.run(cat)  # noqa: E731
     for _ in range(3):
         run()

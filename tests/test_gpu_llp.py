@@ -119,3 +119,48 @@ def test_exact_swap_fused_argmax_count(dtype, d):
         e = np.exp(z - z.max(axis=1, keepdims=True))
         ref = np.argmax(e / e.sum(axis=1, keepdims=True), axis=1)
         assert np.count_nonzero(ref != pred) == 0
+
+
+@pytest.mark.parametrize("optimizer", ["adam", "sgd"])
+def test_graphed_training_equals_eager(optimizer, monkeypatch):
+    """tq.train() captures one iteration (query run, MSE, backward, optimizer
+    step) in a CUDA graph after two eager ones and replays it: the losses and
+    the trained weights equal the all-eager loop's (the one-pass LLP kernel,
+    fp32 X, 1000 bags; Adam's bias correction read from a device table)."""
+    import torch
+
+    from paper_2211_02753_b200 import training as T
+
+    rng = np.random.default_rng(11)
+    n, d, bags = 120_000, 64, 1000
+    X = torch.tensor(rng.normal(size=(n, d)), dtype=torch.float32, device="cuda")
+    bag = torch.tensor(rng.integers(0, bags, size=n), device="cuda")
+    target = torch.tensor(rng.random(bags * 2) * (n / bags / 2), dtype=torch.float64,
+                          device="cuda")
+
+    def run(graph: bool):
+        monkeypatch.setenv("TDP_TRAIN_GRAPH", "1" if graph else "0")
+        model = tq.Linear(d, 2, np.random.default_rng(0), name="lin")
+        bag_pe = tq.one_hot_pe(bag, bags)
+        reg = tq.UdfRegistry()
+        reg.register(tq.UdfEntry("llp", (("Bag", tensor_type(bags)), ("Pred", tensor_type(2))), 1,
+                                 lambda c: (bag_pe, tq.pe_encode(model(c.values))),
+                                 model.parameters))
+        cat = tq.Catalog()
+        xt = tq.Tensor(X)
+        cat.register_tensor(xt, "T")
+        q = tq.compile_plan(tq.lower(tq.bind(tq.parse(
+            "SELECT Bag, Pred, COUNT(*) FROM llp(T) GROUP BY Bag, Pred"), cat, reg)),
+            tq.CompileConfig(trainable=True), reg)
+        losses = tq.train(q, cat, [("T", xt, tq.Tensor(target))],
+                          tq.TrainConfig(iterations=7, lr=0.01, optimizer=optimizer))
+        return losses, model.weight.value.numpy(), model.bias.value.numpy()
+
+    before = T.GRAPHED[0]
+    lg, wg, bg = run(True)
+    assert T.GRAPHED[0] == before + 1  # captured once, replayed five times
+    le, we, be = run(False)
+    assert T.GRAPHED[0] == before + 1
+    np.testing.assert_allclose(lg, le, rtol=1e-12)
+    np.testing.assert_allclose(wg, we, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(bg, be, rtol=1e-12, atol=0)

@@ -536,8 +536,10 @@ void pack_fields(Spec& s, i64 n) {
   for (const Field& f : s.fields) count_packed |= f.acc < 0;
   // worth it only when some word holds two fields
   if (!count_packed || used.size() >= s.fields.size()) {
+    // not packed: every integer sum keeps its own cell (iu[k] = k), as
+    // without packing -- not -1, which would mean "in a packed word"
     s.fields.clear();
-    s.iu.assign(s.ivals.size(), -1);
+    for (size_t k = 0; k < s.ivals.size(); ++k) s.iu[k] = (int)k;
     return;
   }
   s.pwords = (int)used.size();

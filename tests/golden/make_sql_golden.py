@@ -37,7 +37,7 @@ import tensorquery as ref  # noqa: E402
 from tensorquery.encodings import DictionaryEncoding, StringDictionary, plain  # noqa: E402
 from tensorquery.tensor import Tensor  # noqa: E402
 
-from sql_tables import FLOAT_COLS, INT_COLS, WORDS, make_table  # noqa: E402
+from sql_tables import FLOAT_COLS, INT_COLS, WORDS, mix_entry, tables as make_tables  # noqa: E402
 
 
 def ref_table(cols: dict[str, np.ndarray]):
@@ -94,12 +94,12 @@ def order_limit(rg: random.Random, names: list[str]) -> str:
 def gen_queries(rg: random.Random, count: int) -> list[str]:
     qs = []
     while len(qs) < count:
-        tab = rg.choice(["t", "t", "u"])
-        kind = rg.choice(["proj", "group", "group", "group2", "global", "nested"])
+        tab = rg.choice(["t", "t", "u", "w"])
+        kind = rg.choice(["proj", "group", "group", "group2", "global", "nested", "udf"])
         if kind == "proj":
             cols = rg.sample(list(INT_COLS + FLOAT_COLS + ("s",)), rg.randint(1, 3))
             tail = order_limit(rg, cols)
-            if tab == "u" and "LIMIT" not in tail:  # keep the fixture small
+            if tab != "t" and "LIMIT" not in tail:  # keep the fixture small
                 tail += " LIMIT 500"
             qs.append(f"SELECT {', '.join(cols)} FROM {tab}{where(rg)}{tail}")
         elif kind in ("group", "group2"):
@@ -107,8 +107,25 @@ def gen_queries(rg: random.Random, count: int) -> list[str]:
             aggs = agg_items(rg)
             items = keys + [a for a, _ in aggs]
             names = keys + [n for _, n in aggs]
+            tail = order_limit(rg, names)
+            if tab == "w" and "LIMIT" not in tail:  # keep the fixture small
+                tail += " LIMIT 300"
             qs.append(f"SELECT {', '.join(items)} FROM {tab}{where(rg)} GROUP BY "
-                      f"{', '.join(keys)}{order_limit(rg, names)}")
+                      f"{', '.join(keys)}{tail}")
+        elif kind == "udf":
+            key = rg.choice(["k1", "s", "r", "big", "k2"])
+            b = rg.choice(["k2", "f", "k1"])
+            inner = f"SELECT mix({key}, f, {b}) FROM {tab}{where(rg)}"
+            if rg.random() < 0.7:
+                aggs = [a for a in ["COUNT(*)", "SUM(x)", "AVG(x)"] if rg.random() < 0.8] or ["SUM(x)"]
+                names = ["k"] + [{"COUNT(*)": "count", "SUM(x)": "sum_x", "AVG(x)": "avg_x"}[a]
+                                 for a in aggs]
+                tail = order_limit(rg, names)
+                if tab == "w" and "LIMIT" not in tail:
+                    tail += " LIMIT 300"
+                qs.append(f"SELECT k, {', '.join(aggs)} FROM ({inner}) GROUP BY k{tail}")
+            else:
+                qs.append(f"SELECT SUM(x), COUNT(*), AVG(x) FROM ({inner})")
         elif kind == "global":
             aggs = agg_items(rg)
             qs.append(f"SELECT {', '.join(a for a, _ in aggs)} FROM {tab}{where(rg)}")
@@ -116,9 +133,11 @@ def gen_queries(rg: random.Random, count: int) -> list[str]:
             key = rg.choice(["k1", "s", "r", "big"])
             col = rg.choice(["v", "f", "k2"])
             inner = f"SELECT {key}, SUM({col}), COUNT(*) FROM {tab}{where(rg)} GROUP BY {key}"
+            tail = order_limit(rg, [key, 'sum_' + col])
+            if tab == "w" and "LIMIT" not in tail:
+                tail += " LIMIT 300"
             outer = rg.choice([f"SELECT COUNT(*), SUM(sum_{col}), AVG(sum_{col}) FROM ({inner})",
-                               f"SELECT {key}, sum_{col} FROM ({inner}) WHERE sum_{col} > 0"
-                               f"{order_limit(rg, [key, 'sum_' + col])}"])
+                               f"SELECT {key}, sum_{col} FROM ({inner}) WHERE sum_{col} > 0{tail}"])
             qs.append(outer)
     return qs
 
@@ -138,18 +157,19 @@ REJECTED = [
 
 def main() -> None:
     rg = random.Random(20261017)
-    tables = {"t": make_table(4096, 1), "u": make_table(70_000, 2)}  # = sql_tables.tables()
+    tables = make_tables()
     cat = ref.Catalog()
     for name, cols in tables.items():
         cat.register(name, ref_table(cols))
     reg = ref.UdfRegistry()
+    reg.register(mix_entry(ref))
     arrays: dict[str, np.ndarray] = {}
     # the tables are regenerated by the test (make_table, same seeds); their
     # checksums pin them
     sums = {f"{tn}/{cn}": hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest()
             for tn, cols in tables.items() for cn, v in cols.items()}
     cases = []
-    for qi, sql in enumerate(gen_queries(rg, 160) + REJECTED):
+    for qi, sql in enumerate(gen_queries(rg, 240) + REJECTED):
         case = {"sql": sql}
         try:
             plan = ref.lower(ref.bind(ref.parse(sql), cat, reg))

@@ -7,7 +7,9 @@ import numpy as np
 WORDS = ("apple", "kiwi", "lemon", "pear")
 INT_COLS = ("k1", "k2", "big", "r", "v")
 FLOAT_COLS = ("f", "g")
-SIZES = {"t": (4096, 1), "u": (70_000, 2)}
+# t: small; u: >= 65 536 rows (hash group-by); w: >= 148 x 2048 rows (the
+# bulk-copy ring kernels; only aggregates or LIMITed rows are stored)
+SIZES = {"t": (4096, 1), "u": (70_000, 2), "w": (400_000, 3)}
 
 
 def make_table(n: int, seed: int) -> dict[str, np.ndarray]:
@@ -29,3 +31,20 @@ def make_table(n: int, seed: int) -> dict[str, np.ndarray]:
 
 def tables() -> dict[str, dict[str, np.ndarray]]:
     return {name: make_table(n, seed) for name, (n, seed) in SIZES.items()}
+
+
+def mix_entry(api):
+    """The UDF of the generated queries, for either implementation (`api`:
+    the reference package or this one): mix(k, a, b) -> (k, x = a * 2 + b)
+    -- exact in float64 for the fixture's values (multiples of 1/4)."""
+    from importlib import import_module
+
+    storage = import_module(api.__name__ + ".storage")
+    tensor = import_module(api.__name__ + ".tensor")
+
+    def body(k, a, b):
+        x = tensor.add(tensor.mul(a.values, tensor.tensor(2.0)), b.values)
+        return (k, api.plain(x))
+
+    return api.UdfEntry("mix", (("k", storage.INT), ("x", storage.FLOAT)), 3, body, (),
+                        pe_outputs=False)

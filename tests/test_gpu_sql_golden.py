@@ -1,8 +1,9 @@
 """Random SQL queries against the REFERENCE's own results
 (tests/golden/make_sql_golden.py ran the reference on them): 160 queries --
 filters, projections, one- and two-key GROUP BY with COUNT / SUM / AVG,
-global aggregates, ORDER BY [DESC] [LIMIT], subqueries -- over a 4 096- and a
-70 000-row table (dense, sparse, sorted-in-runs and dictionary keys; the
+global aggregates, ORDER BY [DESC] [LIMIT], subqueries, an elementwise UDF
+-- over 4 096-, 70 000- and 400 000-row tables, each in the reference's
+storage widths and in compact storage (dense, sparse, sorted-in-runs and dictionary keys; the
 fused scan, hash / bitmap / runs group-by, top-k and sort paths), compared
 bit for bit (every float64 sum in the fixture is exact in any order; float32
 global aggregates, summed in float32 like the reference, within a few ulps),
@@ -24,7 +25,7 @@ from paper_2211_02753_b200.encodings import DictionaryEncoding, StringDictionary
 
 G = Path(__file__).resolve().parent / "golden"
 sys.path.insert(0, str(G))
-from sql_tables import WORDS, tables  # noqa: E402
+from sql_tables import WORDS, mix_entry, tables  # noqa: E402
 
 META = json.loads((G / "sql_golden.json").read_text())
 CASES = META["cases"]
@@ -38,7 +39,9 @@ def test_sql_golden_tables_reproduce():
             assert h == META["tables"][f"{tn}/{cn}"], (tn, cn)
 
 
-def _catalog():
+def _catalog(compact: bool = False):
+    from paper_2211_02753_b200 import compact as cp
+
     cat = tq.Catalog()
     for name, cols in tables().items():
         enc = []
@@ -49,13 +52,17 @@ def _catalog():
                                                 DictionaryEncoding(StringDictionary(WORDS))))
                 else:
                     enc.append(tq.plain(tq.Tensor(v)))
-        cat.register(name, tq.table_from_columns(list(cols), enc))
+        table = tq.table_from_columns(list(cols), enc)
+        cat.register(name, cp.compact_table(table) if compact else table)
     return cat
 
 
-@pytest.fixture(scope="module")
-def catalog():
-    return _catalog()
+@pytest.fixture(scope="module", params=["wide", "compact"])
+def catalog(request):
+    """The reference's storage widths, and the same tables in compact
+    storage (narrow integers, scaled decimals, uint8 codes):
+    every query must give the reference's result on both."""
+    return _catalog(request.param == "compact")
 
 
 @pytest.fixture(scope="module")
@@ -68,6 +75,7 @@ def arrays():
 def test_sql_query_matches_reference(qi, catalog, arrays):
     case = CASES[qi]
     reg = tq.UdfRegistry()
+    reg.register(mix_entry(tq))
     if "error" in case:
         with pytest.raises(Exception) as ei:
             tq.compile_plan(tq.lower(tq.bind(tq.parse(case["sql"]), catalog, reg)),
@@ -76,7 +84,13 @@ def test_sql_query_matches_reference(qi, catalog, arrays):
         return
     q = tq.compile_plan(tq.lower(tq.bind(tq.parse(case["sql"]), catalog, reg)),
                         tq.CompileConfig(), reg)
-    out = q.run(catalog)
+    # eager (recording) run, capturing run, CUDA-graph replay: all three
+    # results must be the reference's
+    for _ in range(3):
+        _check(case, q.run(catalog), arrays, qi)
+
+
+def _check(case, out, arrays, qi):
     assert list(out.schema.names) == case["names"], case["sql"]
     assert out.row_count == case["rows"], case["sql"]
     for ci, col in enumerate(out.columns):

@@ -207,3 +207,56 @@ def test_sorted_join_filtered_sides_and_q3(monkeypatch):
     got = [c.values.numpy() for c in res.columns]
     np.testing.assert_array_equal(got[0], exp["l_orderkey"])
     np.testing.assert_allclose(got[1], exp["sum_rev"], rtol=1e-9)
+
+
+def _fuzz_case(seed: int):
+    """A random join: key distribution (dense / sparse / clustered / few
+    distinct), sizes (empty .. 300 K), build keys unique or repeated, and
+    filters on either side (as equi_join on lazy selections)."""
+    rng = np.random.default_rng(1000 + seed)
+    kind = seed % 4
+    nb = int(rng.choice([0, 1, 17, 3000, 70_000, 300_000]))
+    npr = int(rng.choice([0, 5, 2000, 150_000, 300_000]))
+    if kind == 0:    # dense unique build (bitmap join)
+        span = max(nb, 1) * int(rng.integers(1, 40))
+        build = rng.choice(span, size=min(nb, span), replace=False) + int(rng.integers(-10**9, 10**9))
+    elif kind == 1:  # sparse unique build over the int64 range (hash join)
+        build = np.unique(rng.integers(I64.min // 2, I64.max // 2, size=nb))
+        rng.shuffle(build)
+    elif kind == 2:  # repeated build keys
+        build = rng.integers(0, max(1, nb // 7), size=nb)
+    else:            # clustered (sorted runs) build
+        build = np.sort(rng.integers(0, max(1, nb // 3), size=nb))
+    build = np.asarray(build, np.int64)
+    pool = build if len(build) else np.arange(3, dtype=np.int64)
+    probe = np.where(rng.random(npr) < 0.6, rng.choice(pool, size=npr),
+                     rng.integers(int(pool.min()) - 5, int(pool.max()) + 6, size=npr))
+    return np.asarray(probe, np.int64), build, rng
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("algo", ["auto", "sort"])
+def test_join_fuzz_vs_oracle(seed, algo, monkeypatch):
+    """Random joins through equi_join (filtered sides included) against the
+    oracle's join_inner, itself pinned to a nested loop."""
+    probe, build, rng = _fuzz_case(seed)
+    monkeypatch.setattr(K, "JOIN_ALGORITHM", algo)
+    pv = rng.normal(size=len(probe))
+    bv = rng.integers(0, 4, size=len(build))
+    left = [tq.plain(tq.Tensor(probe)), tq.plain(tq.Tensor(pv))]
+    right = [tq.plain(tq.Tensor(build)), tq.plain(tq.Tensor(bv))]
+    keep_p = np.ones(len(probe), bool)
+    keep_b = np.ones(len(build), bool)
+    if seed % 3 == 1 and len(probe):
+        left = K.filter_exact(left, [(1, ">", 0.2)])
+        keep_p = pv > 0.2
+    if seed % 3 == 2 and len(build):
+        right = K.filter_exact(right, [(1, "<", 3)])
+        keep_b = bv < 3
+    out = K.equi_join(left, right, 0, 0)
+    epi, ebi = orc.join_inner(probe[keep_p], build[keep_b])
+    np.testing.assert_array_equal(out[0].values.numpy(), probe[keep_p][epi])
+    np.testing.assert_array_equal(out[1].values.numpy(), pv[keep_p][epi])
+    np.testing.assert_array_equal(out[2].values.numpy(), build[keep_b][ebi])
+    np.testing.assert_array_equal(out[3].values.numpy(), bv[keep_b][ebi])

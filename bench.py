@@ -8,7 +8,7 @@ and executed by this package: Filter -> TvfMap -> GroupAggregate runs as one
 fused pass (tdp_scan_aggregate); a Q6 companion runs on the same table.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--query q1|q6|q3|llp|image] [--sf SF] [--scaling strong|weak]
+                    [--query q1|q6|q3|llp|llp-dense|image] [--sf SF] [--scaling strong|weak]
 
 One process per GPU (torchrun for N > 1).  The table is split into N
 contiguous row shards ("strong" scaling: BASELINE's "row-sharded at 1/2/4/8
@@ -40,7 +40,8 @@ def _args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--query", choices=("q1", "q6", "q3", "llp", "image"), default="q1")
+    ap.add_argument("--query", choices=("q1", "q6", "q3", "llp", "llp-dense", "image"),
+                    default="q1")
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
                     help="strong: N row shards of one SF table (BASELINE config 2); "
@@ -57,12 +58,13 @@ def _args():
     ap.add_argument("--image-classes", type=int, default=10)
     ap.add_argument("--llp-rows", type=int, default=100_000_000)
     ap.add_argument("--llp-features", type=int, default=64)
+    ap.add_argument("--llp-classes", type=int, default=1000, help="--query llp-dense: PE classes")
     return ap.parse_args()
 
 
 def main():
     args = _args()
-    if args.query in ("llp", "image", "q3"):
+    if args.query in ("llp", "llp-dense", "image", "q3"):
         import os
 
         if int(os.environ.get("RANK", "0")) != 0:
@@ -74,9 +76,9 @@ def main():
                               f"--query {args.query} has no host reference arm; its line carries "
                               f"cpu_baseline"}))
             return
-        from benchmarks import image, llp, q3
+        from benchmarks import image, llp, llp_dense, q3
 
-        {"llp": llp, "image": image, "q3": q3}[args.query].run(args)
+        {"llp": llp, "llp-dense": llp_dense, "image": image, "q3": q3}[args.query].run(args)
         return
     from benchmarks import tpch
 

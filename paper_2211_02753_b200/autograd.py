@@ -391,6 +391,129 @@ class _SoftLinearCount(torch.autograd.Function):
                 *([None] * len(codes)))
 
 
+# ---------------------------------------------------------------------------
+# wide heads: softmax(X W + b) with n x k logits too large to form at once
+# (SURVEY §8(d) 4': Linear(64, 1000) over 1e8 rows = 400 GB of logits)
+# ---------------------------------------------------------------------------
+WIDE_HEAD_BYTES = 8 << 30   # defer a Linear whose logits would exceed this
+CHUNK_BYTES = 1 << 30       # logits formed per chunk of rows
+
+
+def wide_head(x: torch.Tensor, w: torch.Tensor) -> bool:
+    """A constant-input linear head whose logits exceed WIDE_HEAD_BYTES."""
+    return (x.is_cuda and w.is_cuda and x.dim() == 2 and w.dim() == 2 and not x.requires_grad
+            and x.dtype == w.dtype and x.dtype in (torch.float32, torch.float64)
+            and x.shape[0] * w.shape[1] * x.element_size() > WIDE_HEAD_BYTES)
+
+
+def _chunk_keys(spec: SoftKeySpec, dense_pos: int, codes, lo: int, hi: int, p: torch.Tensor):
+    it = iter(codes)
+    keys = []
+    for j, (kind, _) in enumerate(spec.kinds):
+        keys.append(p if j == dense_pos else next(it)[lo:hi])
+    return keys
+
+
+class _ChunkedSoftLinearCount(torch.autograd.Function):
+    """Soft COUNT over one key P = softmax(X W + b) (x one-hot keys) whose
+    logits are never formed in full: rows in chunks of CHUNK_BYTES of logits,
+    each chunk's logits by cuBLAS (bias as a column of ones; no TF32),
+    softmaxed and counted (tdp_softmax_fwd; column sums for a single key,
+    tdp_soft_groupby_fwd with one-hot keys)
+    into the grid; the backward recomputes each chunk's P and forms
+    dZ = softmax VJP of the gathered grid gradient (tdp_soft_groupby_bwd,
+    tdp_softmax_bwd), dW += X_c^T dZ, db += sum dZ (tq/tensor.py:474,
+    :364-365, :515-527, :437-447)."""
+
+    @staticmethod
+    def forward(ctx, spec: SoftKeySpec, dense_pos: int, out_dtype: torch.dtype, x: torch.Tensor,
+                w: torch.Tensor, b: Optional[torch.Tensor], *codes: torch.Tensor):
+        x, wd = x.contiguous(), w.detach().contiguous()
+        bd = None if b is None else b.detach().contiguous()
+        n, k = x.shape[0], wd.shape[1]
+        rows = max(1, CHUNK_BYTES // (k * x.element_size()))
+        grid = torch.zeros(spec.cells, dtype=torch.float64, device=x.device)
+        part = torch.empty_like(grid)
+        for lo in range(0, n, rows):
+            hi = min(n, lo + rows)
+            p = _chunk_softmax(x[lo:hi], wd, bd)
+            if len(spec.kinds) == 1:  # one key: the grid is P's column sums
+                grid += _colsum64(p)
+                continue
+            keys = _chunk_keys(spec, dense_pos, codes, lo, hi, p)
+            nat.call("tdp_soft_groupby_fwd", _soft_keys(spec, keys), len(keys), hi - lo, None,
+                     nat.I64, nat.ptr(part), nat.stream())
+            grid += part
+        ctx.spec, ctx.dense_pos, ctx.rows, ctx.has_bias = spec, dense_pos, rows, b is not None
+        ctx.save_for_backward(x, w, *(() if b is None else (b,)), *codes)
+        return grid.to(out_dtype)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        saved = ctx.saved_tensors
+        x, w = saved[0], saved[1]
+        b = saved[2] if ctx.has_bias else None
+        codes = saved[3 if ctx.has_bias else 2:]
+        wd = w.detach().contiguous()
+        bd = None if b is None else b.detach().contiguous()
+        spec, pos = ctx.spec, ctx.dense_pos
+        G = g.detach().to(torch.float64).contiguous()
+        n, k = x.shape[0], wd.shape[1]
+        dw = torch.zeros(wd.shape, dtype=torch.float64, device=x.device)
+        db = torch.zeros(k, dtype=torch.float64, device=x.device)
+        nk = len(spec.kinds)
+        for lo in range(0, n, ctx.rows):
+            hi = min(n, lo + ctx.rows)
+            xc = x[lo:hi]
+            p = _chunk_softmax(xc, wd, bd)
+            keys = _chunk_keys(spec, pos, codes, lo, hi, p)
+            dp = torch.empty_like(p)
+            ptrs = (c_void_p * nk)()
+            ptrs[pos] = dp.data_ptr()
+            nat.call("tdp_soft_groupby_bwd", _soft_keys(spec, keys), nk, hi - lo, None, nat.I64,
+                     nat.ptr(G), ptrs, None, nat.stream())
+            dz = torch.empty_like(p)
+            nat.call("tdp_softmax_bwd", nat.ptr(p), nat.ptr(dp), _dt(p), hi - lo, k, nat.ptr(dz),
+                     nat.stream())
+            dw += (xc.t() @ dz).to(torch.float64)
+            db += _colsum64(dz)
+        gw = dw.to(w.dtype) if ctx.needs_input_grad[4] else None
+        gb = db.to(b.dtype) if b is not None and ctx.needs_input_grad[5] else None
+        return (None, None, None, None, gw, gb, *([None] * len(codes)))
+
+
+def _colsum64(t: torch.Tensor, group: int = 256) -> torch.Tensor:
+    """Column sums of a [rows, k] chunk in float64: groups of ``group`` rows
+    summed in the chunk's dtype (no float64 copy of the chunk), the group sums
+    in float64."""
+    rows = t.shape[0] - t.shape[0] % group
+    out = torch.zeros(t.shape[1], dtype=torch.float64, device=t.device)
+    if rows:
+        out += t[:rows].view(-1, group, t.shape[1]).sum(1).sum(0, dtype=torch.float64)
+    if rows < t.shape[0]:
+        out += t[rows:].sum(0, dtype=torch.float64)
+    return out
+
+
+def _chunk_softmax(xc: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor]) -> torch.Tensor:
+    # the bias rides in the GEMM as a column of ones (no pass over the
+    # chunk's logits to add it: x.w + b rounded once)
+    if b is not None:
+        xc = torch.cat([xc, torch.ones((xc.shape[0], 1), dtype=xc.dtype, device=xc.device)], 1)
+        w = torch.cat([w, b.reshape(1, -1)], 0)
+    z = torch.matmul(xc, w)
+    p = torch.empty_like(z)
+    nat.call("tdp_softmax_fwd", nat.ptr(z), _dt(z), z.shape[0], z.shape[1], nat.ptr(p),
+             nat.stream())
+    return p
+
+
+def chunked_soft_linear_count(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor],
+                              x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor],
+                              out_dtype: torch.dtype) -> torch.Tensor:
+    return _ChunkedSoftLinearCount.apply(spec, dense_pos, out_dtype, x, w, b, *codes)
+
+
 def soft_linear_count(spec: SoftKeySpec, dense_pos: int, codes: Sequence[torch.Tensor],
                       x: torch.Tensor, w: torch.Tensor, b: Optional[torch.Tensor],
                       out_dtype: torch.dtype) -> torch.Tensor:

@@ -36,7 +36,8 @@ from . import _native as nat
 from . import hostread
 from .hostread import read_int, read_ints
 from .autograd import (SoftKeySpec, gather_many, gather_rows_raw, linear_keys,
-                       soft_groupby_grid, soft_linear_count, soft_linear_supported)
+                       soft_groupby_grid, soft_linear_count, soft_linear_supported,
+                       chunked_soft_linear_count)
 from .encodings import (
     DecodedArgmax,
     DecodedCodes,
@@ -1019,15 +1020,17 @@ def _soft_linear_count(pes: Sequence[EncodedTensor], spaces: tuple[int, ...]) ->
         return None
     lin = pend.lin
     spec = SoftKeySpec(kinds)
-    if not soft_linear_supported(lin.x, lin.w, spec.cells):
+    chunked = getattr(lin, "wide", False)
+    if not chunked and not soft_linear_supported(lin.x, lin.w, spec.cells):
         return None
     nat.require_cuda(*codes)
     joint_dt = dts[0]
     for d in dts[1:]:
         joint_dt = np.promote_types(joint_dt, d).name
+    count = chunked_soft_linear_count if chunked else soft_linear_count
     with _grad_mode():
-        grid = soft_linear_count(spec, pos, [c.contiguous() for c in codes], lin.x, lin.w, lin.b,
-                                 torch_dtype(joint_dt))
+        grid = count(spec, pos, [c.contiguous() for c in codes], lin.x, lin.w, lin.b,
+                     torch_dtype(joint_dt))
         grid = allreduce_sum(grid, current_group())  # row-sharded: global grid
         return _finish(grid.reshape(spaces))
 

@@ -174,3 +174,50 @@ def test_unsupported_shapes_fall_back():
     exp = np.zeros((9, k))
     np.add.at(exp, codes, P)
     np.testing.assert_allclose(res.counts.numpy(), exp, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("with_bag", [False, True])
+def test_wide_head_chunked_soft_count_equals_unfused(dtype, with_bag, monkeypatch):
+    """A wide head (SURVEY 4': Linear(d, K) with K large) whose logits would not
+    fit is counted in row chunks (autograd._ChunkedSoftLinearCount): the grid
+    and the tape gradients equal the materialised (unfused) path's."""
+    from paper_2211_02753_b200 import autograd as AG
+    from paper_2211_02753_b200.tensor import Tape, backward, mul, reduce_sum
+
+    rng = np.random.default_rng(5)
+    n, d, k, bags = 5000, 16, 300, 6
+    X = rng.normal(size=(n, d)).astype(dtype)
+    codes = rng.integers(0, bags, size=n)
+    G = rng.normal(size=(bags, k) if with_bag else (k,))
+
+    def run(wide: bool):
+        monkeypatch.setattr(AG, "WIDE_HEAD_BYTES", 0 if wide else 1 << 62)
+        monkeypatch.setattr(AG, "CHUNK_BYTES", 64 << 10)  # ~13-27 rows x 300 per chunk
+        lin = tq.Linear(d, k, np.random.default_rng(9), name="w", dtype=dtype)
+        with Tape() as tape:
+            pe = tq.pe_encode(lin(mark_constant(tq.Tensor(X))))  # a catalog column
+            keys = [tq.one_hot_pe(codes, bags), pe] if with_bag else [pe]
+            grid = tq.soft_groupby(keys).counts
+            backward(reduce_sum(mul(grid, tq.tensor(G.astype(dtype)))))
+            return (grid.numpy(), tape.gradient(lin.weight.value).numpy(),
+                    tape.gradient(lin.bias.value).numpy())
+
+    from paper_2211_02753_b200 import kernels as K
+
+    calls = [0]
+    real = K.chunked_soft_linear_count
+
+    def counted(*a, **kw):
+        calls[0] += 1
+        return real(*a, **kw)
+
+    monkeypatch.setattr(K, "chunked_soft_linear_count", counted)
+    gw, dww, dbw = run(True)
+    assert calls[0] == 1  # the chunked path ran
+    gu, dwu, dbu = run(False)
+    assert calls[0] == 1
+    tol = 1e-9 if dtype == "float64" else 2e-5
+    np.testing.assert_allclose(gw, gu, rtol=tol, atol=n * 2.0**-31)
+    np.testing.assert_allclose(dww, dwu, rtol=tol, atol=tol * np.abs(dwu).max())
+    np.testing.assert_allclose(dbw, dbu, rtol=tol, atol=tol * np.abs(dbu).max())

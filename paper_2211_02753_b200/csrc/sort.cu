@@ -518,6 +518,259 @@ __global__ void __launch_bounds__(kTopkChunk / 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large inputs (n >= kSelMinRows): radix select instead of sorting chunks.
+// The k smallest (image, row) pairs are found digit by digit -- 11 bits of the
+// 64-bit key image per pass (6 passes), then 11 bits of the row index (4
+// passes: ties resolved to the lowest rows, the stable order) -- each pass a
+// histogram of the candidates' next digit, a one-CTA pick of the bucket that
+// holds the k-th pair, and a compaction that sets aside every pair below it
+// ("sure") and keeps the bucket's pairs as the next candidates.  Candidates
+// are rows of the key column re-read with the prefix as a filter ("virtual")
+// until a bucket holds <= kSelCompact pairs, then a materialised buffer.  The
+// want <= 1024 selected pairs are finally sorted in one CTA.  Everything is
+// decided on the device (no host read); a virtual pass costs two reads of the
+// key column, typically two such passes, then microseconds.
+// ---------------------------------------------------------------------------
+constexpr int kSelBits = 11, kSelBins = 1 << kSelBits;
+constexpr int kSelPasses = 10;            // 6 over the image, 4 over the row (< 2^44)
+constexpr i64 kSelMinRows = 1 << 20;
+constexpr i64 kSelCompact = 1 << 16;
+
+struct SelPass {
+  int phase;  // 0: image bits, 1: row bits
+  int shift;
+  int bits;
+};
+
+struct SelPlan {
+  SelPass p[kSelPasses];
+};
+
+// per pass p (filled by the pick kernel of pass p - 1; pass 0 by the host):
+//   prefix[p]: the processed high bits the candidates share (phase 0: image
+//   bits above shift + bits; phase 1: the whole image is img_eq and the row's
+//   high bits match), krem[p] pairs still to take, mat[p]/nbuf[p] whether the
+//   candidates are materialised (buf[p & 1]) and how many, done[p]
+struct SelState {
+  unsigned long long prefix[kSelPasses + 1];
+  long long krem[kSelPasses + 1];
+  long long nbuf[kSelPasses + 1];
+  int mat[kSelPasses + 1];
+  int done[kSelPasses + 1];
+  int bucket[kSelPasses];
+  int take_bucket[kSelPasses];  // last pass: the bucket's pairs are selected too
+  long long below[kSelPasses];  // candidates below the picked bucket (selected)
+  unsigned long long img_eq;    // phase 1: the threshold image
+  unsigned long long nsure;     // pairs selected so far
+};
+
+struct SelWs {
+  SelState* st;
+  unsigned long long* hist;  // [kSelBins]
+  u64* sure_k;               // [kTopkMax]
+  i64* sure_i;
+  u64* buf_k[2];             // [kSelCompact]
+  i64* buf_i[2];
+};
+
+__device__ __forceinline__ bool sel_candidate(const SelState& st, const SelPass& ps, int p, u64 img,
+                                              i64 row, unsigned* digit) {
+  if (ps.phase == 0) {
+    const int hi = ps.shift + ps.bits;  // bits above this digit
+    if (hi < 64 && (img >> hi) != st.prefix[p]) return false;
+    *digit = (unsigned)((img >> ps.shift) & ((1u << ps.bits) - 1u));
+    return true;
+  }
+  if (img != st.img_eq) return false;
+  const int hi = ps.shift + ps.bits;
+  const u64 r = (u64)row;
+  if (hi < 64 && (r >> hi) != st.prefix[p]) return false;
+  *digit = (unsigned)((r >> ps.shift) & ((1u << ps.bits) - 1u));
+  return true;
+}
+
+__global__ void __launch_bounds__(256)
+    sel_hist_kernel(TopkRaw raw, i64 n, SelWs w, SelPlan plan, int p) {
+  const SelState& st = *w.st;
+  if (st.done[p]) return;
+  __shared__ unsigned h[kSelBins];
+  for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) h[b] = 0u;
+  __syncthreads();
+  const SelPass ps = plan.p[p];
+  const bool mat = st.mat[p] != 0;
+  const i64 m = mat ? (i64)st.nbuf[p] : n;
+  const u64* bk = w.buf_k[p & 1];
+  const i64* bi = w.buf_i[p & 1];
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!mat) {  // four rows' loads in flight per thread
+    for (; i + 3 * stride < m; i += 4 * stride) {
+      u64 img[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) img[u] = topk_image(raw, i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        unsigned d;
+        if (sel_candidate(st, ps, p, img[u], i + u * stride, &d)) atomicAdd(&h[d], 1u);
+      }
+    }
+  }
+  for (; i < m; i += stride) {
+    const u64 img = mat ? bk[i] : topk_image(raw, i);
+    const i64 row = mat ? bi[i] : i;
+    unsigned d;
+    if (sel_candidate(st, ps, p, img, row, &d)) atomicAdd(&h[d], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kSelBins; b += blockDim.x)
+    if (h[b]) atomicAdd(w.hist + b, (unsigned long long)h[b]);
+}
+
+// One CTA of 1024 threads: the bucket holding the krem-th candidate.
+__global__ void __launch_bounds__(1024) sel_pick_kernel(SelWs w, SelPlan plan, int p) {
+  SelState& st = *w.st;
+  __shared__ unsigned long long part[1024];
+  __shared__ int pick;
+  if (st.done[p]) {
+    if (threadIdx.x == 0) {
+      st.done[p + 1] = 1;
+      st.krem[p + 1] = 0;
+    }
+    return;
+  }
+  // two bins per thread, inclusive scan over the 1024 partial sums
+  const int t = threadIdx.x;
+  const unsigned long long a = w.hist[2 * t], b = w.hist[2 * t + 1];
+  part[t] = a + b;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const unsigned long long v = t >= o ? part[t - o] : 0ull;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  const long long krem = st.krem[p];
+  if (t == 0) pick = -1;
+  __syncthreads();
+  const unsigned long long before = t ? part[t - 1] : 0ull;
+  if ((long long)before < krem && (long long)part[t] >= krem)  // the k-th lies in bins 2t, 2t+1
+    pick = (long long)(before + a) >= krem ? 2 * t : 2 * t + 1;
+  __syncthreads();
+  if (t == 0) {
+    const SelPass ps = plan.p[p];
+    const int bk = pick < 0 ? 0 : pick;
+    unsigned long long below = 0;
+    for (int q = 0; q < bk; ++q) below += w.hist[q];
+    const unsigned long long inb = w.hist[bk];
+    st.bucket[p] = bk;
+    st.below[p] = (long long)below;
+    const long long left = krem - (long long)below;  // to take from the bucket
+    const bool last = p == kSelPasses - 1;
+    st.take_bucket[p] = last && left > 0;
+    st.krem[p + 1] = left;
+    st.done[p + 1] = pick < 0 || left <= 0 || last;
+    if (p + 1 < kSelPasses) {
+      const SelPass nx = plan.p[p + 1];
+      if (ps.phase == 0 && nx.phase == 1) {  // the image is now fully known
+        st.img_eq = (ps.shift + ps.bits >= 64 ? 0ull : (st.prefix[p] << ps.bits)) | (u64)bk;
+        st.img_eq = (st.img_eq << ps.shift);
+        st.prefix[p + 1] = 0ull;
+      } else {
+        st.prefix[p + 1] = (st.prefix[p] << ps.bits) | (u64)bk;
+      }
+      st.mat[p + 1] = st.mat[p] || (long long)inb <= kSelCompact;
+      st.nbuf[p + 1] = 0;
+    }
+  }
+  __syncthreads();
+  w.hist[2 * t] = 0ull;  // ready for the next pass
+  w.hist[2 * t + 1] = 0ull;
+}
+
+// One candidate of the compaction: selected (below the bucket, or the
+// bucket's pairs in the last pass) or kept as a next-pass candidate.
+__device__ __forceinline__ void sel_place(SelState& st, const SelWs& w, unsigned d,
+                                          unsigned bsel, bool take_bucket, bool keep_next,
+                                          u64 img, i64 row, u64* nk, i64* ni, int p) {
+  if (d < bsel || (d == bsel && take_bucket)) {
+    const unsigned long long at = atomicAdd(&st.nsure, 1ull);
+    if (at < (unsigned long long)kTopkMax) {
+      w.sure_k[at] = img;
+      w.sure_i[at] = row;
+    }
+  } else if (d == bsel && keep_next) {
+    const unsigned long long at = atomicAdd((unsigned long long*)&st.nbuf[p + 1], 1ull);
+    if (at < (unsigned long long)kSelCompact) {
+      nk[at] = img;
+      ni[at] = row;
+    }
+  }
+}
+
+// Pairs below the picked bucket are selected; the bucket's pairs become the
+// next candidates when they are materialised (or, in the last pass, selected).
+__global__ void __launch_bounds__(256)
+    sel_compact_kernel(TopkRaw raw, i64 n, SelWs w, SelPlan plan, int p) {
+  SelState& st = *w.st;
+  if (st.done[p]) return;
+  const SelPass ps = plan.p[p];
+  const bool mat = st.mat[p] != 0;
+  const bool keep_next = p + 1 < kSelPasses && st.mat[p + 1] && !st.done[p + 1];
+  const bool take_bucket = st.take_bucket[p] != 0;
+  const unsigned bsel = (unsigned)st.bucket[p];
+  if (st.below[p] == 0 && !keep_next && !take_bucket) return;  // nothing to place
+  const i64 m = mat ? (i64)st.nbuf[p] : n;
+  const u64* bk = w.buf_k[p & 1];
+  const i64* bi = w.buf_i[p & 1];
+  u64* nk = w.buf_k[(p + 1) & 1];
+  i64* ni = w.buf_i[(p + 1) & 1];
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!mat) {  // four rows' loads in flight; rows with no action skip the slow path
+    for (; i + 3 * stride < m; i += 4 * stride) {
+      u64 img[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) img[u] = topk_image(raw, i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        unsigned d;
+        if (!sel_candidate(st, ps, p, img[u], i + u * stride, &d)) continue;
+        sel_place(st, w, d, bsel, take_bucket, keep_next, img[u], i + u * stride, nk, ni, p);
+      }
+    }
+  }
+  for (; i < m; i += stride) {
+    const u64 img = mat ? bk[i] : topk_image(raw, i);
+    const i64 row = mat ? bi[i] : i;
+    unsigned d;
+    if (!sel_candidate(st, ps, p, img, row, &d)) continue;
+    sel_place(st, w, d, bsel, take_bucket, keep_next, img, row, nk, ni, p);
+  }
+}
+
+
+__global__ void sel_init_kernel(SelState* st, i64 want) {
+  unsigned* w = reinterpret_cast<unsigned*>(st);
+  for (int t = threadIdx.x; t < (int)(sizeof(SelState) / 4); t += blockDim.x) w[t] = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) st->krem[0] = want;
+}
+
+// The selected pairs (want of them) in ascending (image, row) order.
+__global__ void __launch_bounds__(1024)
+    sel_final_kernel(SelWs w, i64 want, i64* __restrict__ out_order) {
+  __shared__ u64 sk[kTopkMax];
+  __shared__ i64 si[kTopkMax];
+  const int nsel = (int)(w.st->nsure < (unsigned long long)kTopkMax ? w.st->nsure : kTopkMax);
+  for (int t = threadIdx.x; t < kTopkMax; t += blockDim.x) {
+    sk[t] = t < nsel ? w.sure_k[t] : ~0ull;
+    si[t] = t < nsel ? w.sure_i[t] : LLONG_MAX;
+  }
+  topk_bitonic(sk, si, kTopkMax);
+  for (int t = threadIdx.x; t < want; t += blockDim.x) out_order[t] = si[t];
+}
+
 int topk_round_chunk(i64 m, i64 k) {
   int c = 64;
   while (c < 2 * k) c <<= 1;
@@ -576,6 +829,43 @@ int tdp_topk_order(const tdp_column* key, int32_t descending, int64_t n, int64_t
   TopkRaw raw{key->data, key->dtype, descending ? 1 : 0};
   const TopkRaw none{nullptr, 0, 0};
   const i64 want = k < n ? k : n;
+  if (n >= kSelMinRows) {  // radix select (see above)
+    unsigned char* q = reinterpret_cast<unsigned char*>(ws);
+    SelWs w;
+    w.st = reinterpret_cast<SelState*>(q);
+    q += align256(sizeof(SelState));
+    w.hist = reinterpret_cast<unsigned long long*>(q);
+    q += align256(kSelBins * 8);
+    w.sure_k = reinterpret_cast<u64*>(q);
+    q += align256(kTopkMax * 8);
+    w.sure_i = reinterpret_cast<i64*>(q);
+    q += align256(kTopkMax * 8);
+    for (int b = 0; b < 2; ++b) {
+      w.buf_k[b] = reinterpret_cast<u64*>(q);
+      q += align256(kSelCompact * 8);
+      w.buf_i[b] = reinterpret_cast<i64*>(q);
+      q += align256(kSelCompact * 8);
+    }
+    TDP_REQUIRE((size_t)(q - reinterpret_cast<unsigned char*>(ws)) <= ws_bytes,
+                "top-k workspace too small for the radix select");
+    SelPlan plan;
+    const int img_shifts[6] = {53, 42, 31, 20, 9, 0};
+    const int img_bits[6] = {11, 11, 11, 11, 11, 9};
+    for (int i = 0; i < 6; ++i) plan.p[i] = SelPass{0, img_shifts[i], img_bits[i]};
+    for (int i = 0; i < 4; ++i) plan.p[6 + i] = SelPass{1, 33 - 11 * i, 11};
+    sel_init_kernel<<<1, 128, 0, st>>>(w.st, want);  // no host copy: graph-capturable
+    TDP_CUDA_TRY(cudaMemsetAsync(w.hist, 0, kSelBins * 8, st));
+    const int grid = stream_grid(n, 256 * 8, 8);
+    for (int p = 0; p < kSelPasses; ++p) {
+      sel_hist_kernel<<<grid, 256, 0, st>>>(raw, n, w, plan, p);
+      sel_pick_kernel<<<1, 1024, 0, st>>>(w, plan, p);
+      sel_compact_kernel<<<grid, 256, 0, st>>>(raw, n, w, plan, p);
+    }
+    TDP_LAUNCH_CHECK("sel kernels");
+    sel_final_kernel<<<1, 1024, 0, st>>>(w, want, out_order);
+    TDP_LAUNCH_CHECK("sel_final_kernel");
+    return TDP_OK;
+  }
   if (n <= kTopkChunk) {  // one CTA: the answer
     const int last = pow2_at_least(n);
     topk_chunk_kernel<<<1, last / 2 > 32 ? last / 2 : 32, 0, st>>>(

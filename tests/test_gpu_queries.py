@@ -581,3 +581,31 @@ def test_sorted_runs_groupby_tiny_and_tile_edges(n):
     np.testing.assert_array_equal(aggs[2].cpu().numpy(), ea[2])
     np.testing.assert_allclose(aggs[0].cpu().numpy(), ea[0], rtol=1e-12, atol=0)
     np.testing.assert_allclose(aggs[1].cpu().numpy(), ea[1], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "ties", "few_distinct", "nan_negzero", "int_extremes",
+                                  "all_equal"])
+@pytest.mark.parametrize("k,desc", [(10, True), (1, False), (1000, False), (257, True)])
+def test_topk_radix_select_large(dist, k, desc):
+    """ORDER BY ... LIMIT k on >= 2^20 rows takes the radix select
+    (tdp_topk_order, sel_* kernels): the result is exactly the first k rows
+    of the stable order -- ties by row, NaN last, -0.0 == 0.0."""
+    from paper_2211_02753_b200.kernels import topk_order
+
+    rng = np.random.default_rng(hash((dist, k, desc)) % 2**32)
+    n = (1 << 20) + 12345
+    if dist == "uniform":
+        v = rng.random(n)
+    elif dist == "ties":
+        v = np.round(rng.random(n), 3)
+    elif dist == "few_distinct":
+        v = rng.integers(0, 5, size=n).astype(np.float64)
+    elif dist == "nan_negzero":
+        v = rng.choice([np.nan, -0.0, 0.0, 1.5, -2.0, np.inf], size=n)
+    elif dist == "int_extremes":
+        v = rng.choice([-(2**63), 2**63 - 1, 0, -1, 7], size=n).astype(np.int64)
+    else:
+        v = np.zeros(n)
+    got = topk_order(tq.plain(tq.Tensor(v)), k, desc).cpu().numpy()
+    exp = orc.stable_order(v, desc)[:k]
+    np.testing.assert_array_equal(got, exp)

@@ -1463,8 +1463,29 @@ __global__ void scan_minmax_kernel(PredSet ps, i64 n, KeyCols kc, int nkeys,
     mn[j] = LLONG_MAX;
     mx[j] = LLONG_MIN;
   }
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (i64)gridDim.x * blockDim.x) {
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 i0 = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ps.npreds == 0 && nkeys == 1 && kc.dt[0] == TDP_I64) {
+    // one unfiltered int64 key (group-by planning, column statistics): four
+    // rows' loads in flight per thread
+    const i64* __restrict__ key = reinterpret_cast<const i64*>(kc.p[0]);
+    for (; i0 + 3 * stride < n; i0 += 4 * stride) {
+      i64 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(key + i0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const i64 i = i0 + u * stride;
+        mn[0] = v[u] < mn[0] ? v[u] : mn[0];
+        mx[0] = v[u] > mx[0] ? v[u] : mx[0];
+        if (runs != nullptr && i > 0) {
+          unsorted |= v[u] < __ldg(key + i - 1);
+          if (i >= kRunMax) longrun |= v[u] == __ldg(key + i - kRunMax);
+        }
+      }
+    }
+  }
+  for (i64 i = i0; i < n; i += stride) {
     if (!eval_all(ps, i)) continue;
 #pragma unroll
     for (int j = 0; j < kMaxKeys; ++j) {

@@ -1752,13 +1752,19 @@ __global__ void hashagg_kernel(const i64* __restrict__ keys, i64 n, HashAgg h, V
         inserted = atomicCAS(h.misc + 1, 0ull, 1ull) == 0ull;
       } else {
         u64 s = join_hash(k) & h.mask;
+        unsigned long long* slots = reinterpret_cast<unsigned long long*>(h.slot);
         for (;;) {
-          const unsigned long long prev =
-              atomicCAS(reinterpret_cast<unsigned long long*>(h.slot + s), 0ull,
-                        (unsigned long long)img);
-          if (prev == 0ull || prev == img) {
-            inserted = prev == 0ull;
-            break;
+          // a plain (L2) read first: a slot only ever goes 0 -> key, so a key
+          // seen is final and only an empty slot needs the CAS (most rows of a
+          // repeated key then do no atomic here)
+          const unsigned long long cur = __ldcg(slots + s);
+          if (cur == img) break;
+          if (cur == 0ull) {
+            const unsigned long long prev = atomicCAS(slots + s, 0ull, (unsigned long long)img);
+            if (prev == 0ull || prev == img) {
+              inserted = prev == 0ull;
+              break;
+            }
           }
           s = (s + 1) & h.mask;
         }

@@ -3,81 +3,73 @@
 // atomicAdd(double) sums in whatever order the warps arrive, so a float SUM
 // computed with it differs from run to run in the last bits.  Here every
 // value is converted to a fixed-point integer (resolution 2^-128) and added
-// into a per-cell 256-bit two's-complement accumulator with 64-bit integer
-// atomics; integer addition is associative, so the cell's final value -- and
-// its conversion back to the nearest double -- is bitwise identical whatever
-// the order of the additions.
+// into a per-cell accumulator with integer atomics; integer addition is
+// associative, so the cell's final value -- and its conversion back to the
+// nearest double -- is bitwise identical whatever the order of the additions.
 //
-// Cell layout (kFixedWords u64 words): w[0..3] the 256-bit accumulator
-// (little-endian words), w[4] a double side accumulator for the values
-// outside the fixed-point range (|x| >= 2^88, inf, NaN), where ordinary
-// float addition applies.  |x| < 2^88 keeps 2^40 additions of headroom.
-// Bits below 2^-128 are truncated (a value keeps its full 53-bit mantissa
-// down to |x| ~ 2^-75).  The result is the correctly rounded exact sum of the
-// fixed-point values plus the side accumulator -- at least as accurate as the
-// reference's sequential np.add.at (tq/kernels.py:147-153).
+// Cell layout (kFixedWords u64 words): w[0..7] eight signed limb
+// accumulators, limb j weighing 2^(32 j) of the 256-bit fixed-point value; an
+// add splits the value's shifted 53-bit mantissa into (at most three) 32-bit
+// pieces and adds each, negated for a negative value, to its limb with a
+// non-returning 64-bit atomic (RED) -- no carry propagation at add time (a
+// limb absorbs 2^31 additions), so no returning atomics: the carries are
+// resolved once when the cell is read.  w[8] is a double side accumulator for
+// the values outside the fixed-point range (|x| >= 2^88, inf, NaN), where
+// ordinary float addition applies.  Bits below 2^-128 are truncated (a value
+// keeps its full 53-bit mantissa down to |x| ~ 2^-75).  The result is the
+// correctly rounded exact sum of the fixed-point values plus the side
+// accumulator -- at least as accurate as the reference's sequential np.add.at
+// (tq/kernels.py:147-153).
 #pragma once
 
 #include <cstdint>
 
 namespace tdp {
 
-constexpr int kFixedWords = 5;
+constexpr int kFixedWords = 9;
+constexpr int kFixedLimbs = 8;
 constexpr int kFixedScale = 128;  // value = integer * 2^-128
-constexpr int kFixedMaxExp = 88;  // |x| < 2^88 goes to the integer words
-
-// w += v (4-word two's complement), one atomic per nonzero word + carries;
-// words below `first` of v are zero.
-__device__ __forceinline__ void fixed_add_words(unsigned long long* w, const unsigned long long v[4],
-                                                int first) {
-  unsigned long long carry = 0;
-  for (int i = first; i < 4; ++i) {
-    const unsigned long long t = v[i] + carry;
-    carry = t < v[i] ? 1ull : 0ull;  // v[i] = ~0 and a carry in: wraps to 0
-    if (t != 0ull) {
-      const unsigned long long old = atomicAdd(w + i, t);
-      carry += (old + t < old) ? 1ull : 0ull;
-    }
-  }
-}
+constexpr int kFixedMaxExp = 88;  // |x| < 2^88 goes to the limbs
 
 __device__ __forceinline__ void fixed_add(unsigned long long* cell, double x) {
   const long long bits = __double_as_longlong(x);
   const int e = (int)((bits >> 52) & 0x7ff);
   if (e == 0) return;  // +-0 and subnormals (< 2^-1022): below the resolution
   if (e == 0x7ff || e - 1075 + 53 > kFixedMaxExp) {
-    atomicAdd(reinterpret_cast<double*>(cell + 4), x);  // inf / NaN / huge
+    atomicAdd(reinterpret_cast<double*>(cell + kFixedLimbs), x);  // inf / NaN / huge
     return;
   }
-  const unsigned long long m = ((unsigned long long)bits & ((1ull << 52) - 1)) | (1ull << 52);
-  const int sh = e - 1075 + kFixedScale;  // bit position of the mantissa's lsb
-  if (sh <= -53) return;                  // |x| < 2^-128: truncated
-  unsigned long long v[4] = {0ull, 0ull, 0ull, 0ull};
-  int first = 0;
+  unsigned long long m = ((unsigned long long)bits & ((1ull << 52) - 1)) | (1ull << 52);
+  int sh = e - 1075 + kFixedScale;  // bit position of the mantissa's lsb
+  if (sh <= -53) return;            // |x| < 2^-128: truncated
   if (sh < 0) {
-    v[0] = m >> (-sh);
-  } else {
-    const int word = sh >> 6, r = sh & 63;
-    v[word] = m << r;
-    if (r && word < 3) v[word + 1] = m >> (64 - r);
-    first = word;
+    m >>= -sh;
+    sh = 0;
   }
-  if (bits < 0) {  // two's complement of the magnitude: ~v + 1 over all words
-    unsigned long long c = 1;
-    for (int i = 0; i < 4; ++i) {
-      v[i] = ~v[i] + c;
-      c = (c && v[i] == 0ull) ? 1ull : 0ull;
-    }
-    // the words below the magnitude's lowest set word stay zero
+  const int j0 = sh >> 5, r = sh & 31;
+  const unsigned __int128 t = (unsigned __int128)m << r;  // <= 84 bits
+  const bool neg = bits < 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const unsigned long long piece = (unsigned long long)(t >> (32 * i)) & 0xffffffffull;
+    if (piece != 0ull && j0 + i < kFixedLimbs)
+      atomicAdd(cell + j0 + i, neg ? (unsigned long long)(-(long long)piece) : piece);
   }
-  fixed_add_words(cell, v, first);
 }
 
 // The cell's sum as the nearest double (round-to-nearest-even of the exact
 // fixed-point total), plus the side accumulator.
 __device__ __forceinline__ double fixed_value(const unsigned long long* cell) {
-  unsigned long long d[4] = {cell[0], cell[1], cell[2], cell[3]};
-  const bool neg = (d[3] >> 63) != 0;
+  // resolve the limbs' carries: a 256-bit two's-complement total in d[4]
+  unsigned long long d[4] = {0ull, 0ull, 0ull, 0ull};
+  __int128 carry = 0;
+#pragma unroll
+  for (int j = 0; j < kFixedLimbs; ++j) {
+    const __int128 t = (__int128)(long long)cell[j] + carry;
+    d[j >> 1] |= ((unsigned long long)t & 0xffffffffull) << (32 * (j & 1));
+    carry = t >> 32;  // arithmetic: floor division
+  }
+  const bool neg = carry < 0;  // totals stay within +-2^255
   if (neg) {  // magnitude
     unsigned long long c = 1;
     for (int i = 0; i < 4; ++i) {
@@ -87,7 +79,7 @@ __device__ __forceinline__ double fixed_value(const unsigned long long* cell) {
   }
   int top = 3;
   while (top >= 0 && d[top] == 0ull) --top;
-  const double side = __longlong_as_double((long long)cell[4]);
+  const double side = __longlong_as_double((long long)cell[kFixedLimbs]);
   if (top < 0) return 0.0 + side;
   const int s = __clzll((long long)d[top]);
   unsigned long long hi = d[top] << s;

@@ -13,6 +13,8 @@ ops = {
  "hash": lambda: K.groupby_exact([tq.plain(tq.Tensor(keys))], [("sum", tq.Tensor(f64)), ("count", None)]),
  "hash_count_only": lambda: K.groupby_exact([tq.plain(tq.Tensor(keys))], [("count", None)]),
  "bitmap": lambda: K.groupby_exact([tq.plain(tq.Tensor(kb))], [("sum", tq.Tensor(f64)), ("count", None)]),
+ "bitmap_count_only": lambda: K.groupby_exact([tq.plain(tq.Tensor(kb))], [("count", None)]),
+ "bitmap_int_sum": lambda: K.groupby_exact([tq.plain(tq.Tensor(kb))], [("sum", tq.Tensor(keys)), ("count", None)]),
  "topk": lambda: K.topk_order(tq.plain(tq.Tensor(f64)), 10, True),
 }
 for name, fn in ops.items():

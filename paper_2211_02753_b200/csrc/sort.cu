@@ -2510,7 +2510,34 @@ struct BitmapAgg {
   u64 lo;
   i64 range;
   int cw;
+  // partitioned accumulation (part_ws_bytes; null below kPartMinRows)
+  unsigned short* pslot;  // [n] group within its partition
+  unsigned* pgroup;       // [n] group of each row (part_hist_kernel)
+  u64* pval;              // [naggs][n] value bits in partition order
+  i64* phist;             // [P] rows per partition
+  i64* poffs;             // [P] partition starts
+  unsigned long long* pcur;  // [P] scatter cursors
+  void* pscan_ws;
+  size_t pscan_bytes;
 };
+
+// Partitioned accumulation (large inputs): rows are scattered by group into
+// partitions of G groups whose cells fit one CTA's shared memory, then each
+// partition is aggregated with shared-memory atomics and written out once --
+// instead of 3-5 L2 atomics per row into a cell array of n x cw words.
+constexpr i64 kPartMinRows = (i64)1 << 22;
+constexpr int kPartMaxParts = 4096;
+constexpr int kPartSmem = 200 * 1024;
+constexpr int kPartMinGroups = 256;  // G below this: the unpartitioned kernel
+constexpr int kPartTileRows = 8192;  // scatter tile: 1024 threads x 8 rows
+
+size_t part_ws_bytes(i64 n, int naggs) {
+  if (n < kPartMinRows) return 0;
+  return align256((size_t)n * 2) + align256((size_t)n * 4) +
+         (size_t)(naggs > 0 ? naggs : 0) * align256((size_t)n * 8) +
+         3 * align256((size_t)(kPartMaxParts + 1) * 8) +
+         align256(exclusive_scan_workspace(kPartMaxParts) + 1024);
+}
 
 size_t bitmap_agg_ws_bytes(i64 n, i64 range, int naggs) {
   const i64 r = range > 0 ? range : 1;
@@ -2518,7 +2545,7 @@ size_t bitmap_agg_ws_bytes(i64 n, i64 range, int naggs) {
   const int na = naggs > 0 ? naggs : 0;
   return align256((size_t)words * 4) + align256((size_t)words * 2) + 2 * align256((size_t)blocks * 8) +
          256 + align256((size_t)(n > 0 ? n : 1) * cell_words(na, na) * 8) +
-         exclusive_scan_workspace(blocks) + 2048;
+         align256(exclusive_scan_workspace(blocks)) + 2048 + part_ws_bytes(n, na);
 }
 
 BitmapAgg carve_bitmap_agg(void* ws, i64 n, i64 range, i64 lo, const ValSet& vs) {
@@ -2541,8 +2568,26 @@ BitmapAgg carve_bitmap_agg(void* ws, i64 n, i64 range, i64 lo, const ValSet& vs)
   p += align256((size_t)(n > 0 ? n : 1) * cell_words(vs.naggs, vs.naggs) * 8);
   b.scan_ws = p;
   b.scan_bytes = exclusive_scan_workspace(blocks) + 1024;
+  p += align256(exclusive_scan_workspace(blocks)) + 2048;
   b.lo = (u64)lo;
   b.range = r;
+  b.pslot = nullptr;
+  if (n >= kPartMinRows) {
+    b.pslot = (unsigned short*)p;
+    p += align256((size_t)n * 2);
+    b.pgroup = (unsigned*)p;
+    p += align256((size_t)n * 4);
+    b.pval = (u64*)p;
+    p += (size_t)vs.naggs * align256((size_t)n * 8);
+    b.phist = (i64*)p;
+    p += align256((size_t)(kPartMaxParts + 1) * 8);
+    b.poffs = (i64*)p;
+    p += align256((size_t)(kPartMaxParts + 1) * 8);
+    b.pcur = (unsigned long long*)p;
+    p += align256((size_t)(kPartMaxParts + 1) * 8);
+    b.pscan_ws = p;
+    b.pscan_bytes = exclusive_scan_workspace(kPartMaxParts) + 1024;
+  }
   return b;
 }
 
@@ -2616,6 +2661,202 @@ __global__ void bm_emit_kernel(BitmapAgg b, i64 m, ValSet vs, i64* __restrict__ 
   }
 }
 
+__device__ __forceinline__ i64 bm_rank(const BitmapAgg& b, u64 d) {
+  const i64 w = (i64)(d >> 5);
+  return __ldg(b.boffs + (d >> 10)) + __ldg(b.wpre + w) +
+         __popc(__ldg(b.bits + w) & ((1u << (d & 31)) - 1u));
+}
+
+// Key images of the m groups straight from the bitmap (group g = the g-th
+// set bit): one thread per bitmap word, no pass over the rows.
+__global__ void bm_keys_kernel(BitmapAgg b, i64 words) {
+  for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (i64)gridDim.x * blockDim.x) {
+    unsigned bits = b.bits[w];
+    if (!bits) continue;
+    i64 g = b.boffs[w >> 5] + b.wpre[w];
+    while (bits) {
+      const int bit = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const u64 k = b.lo + (u64)w * 32 + (u64)bit;
+      b.cells[g * b.cw + kCellImg] = k ^ 0x8000000000000000ull;
+      ++g;
+    }
+  }
+}
+
+// Rows per partition (partition = group >> gshift): shared counters, one
+// global add per CTA and partition.
+__global__ void part_hist_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg b, int gshift,
+                                 int parts) {
+  extern __shared__ unsigned ph_cnt[];
+  for (int p = threadIdx.x; p < parts; p += blockDim.x) ph_cnt[p] = 0u;
+  __syncthreads();
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    const i64 g = bm_rank(b, (u64)__ldg(keys + i) - b.lo);
+    b.pgroup[i] = (unsigned)g;
+    atomicAdd(ph_cnt + (g >> gshift), 1u);
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < parts; p += blockDim.x)
+    if (ph_cnt[p])
+      atomicAdd(reinterpret_cast<unsigned long long*>(b.phist) + p, (unsigned long long)ph_cnt[p]);
+}
+
+// Scatter rows into their partitions, 8192-row tiles of 1024 threads: count
+// per partition in shared memory (each row's place in its partition's run),
+// a block scan of the counts (the tile's rows staged in partition order),
+// one global add per partition and tile to reserve the runs, then the staged
+// rows -- group-in-partition and each aggregate value (8 B) -- written out
+// in staging order, so consecutive threads write consecutive addresses of a
+// run (a row-order write would touch one sector per row).  Row order inside
+// a partition is not fixed; every accumulation downstream is
+// order-independent (integer and fixed-point adds).
+constexpr int kScatterThreads = 1024;
+constexpr int kScatterRows = kPartTileRows / kScatterThreads;
+
+__global__ void __launch_bounds__(kScatterThreads)
+    part_scatter_kernel(i64 n, BitmapAgg b, ValSet vs, int gshift, int parts) {
+  extern __shared__ unsigned ps_sm[];
+  unsigned* cnt = ps_sm;                      // [kPartMaxParts] rows per partition in the tile
+  unsigned* tpre = cnt + kPartMaxParts;       // [kPartMaxParts] staged start
+  unsigned* base = tpre + kPartMaxParts;      // [kPartMaxParts] reserved global start
+  unsigned* wsum = base + kPartMaxParts;      // [32]
+  u64* sval = reinterpret_cast<u64*>(wsum + 32);                                   // [tile]
+  unsigned short* sslot = reinterpret_cast<unsigned short*>(sval + kPartTileRows);  // [tile]
+  unsigned short* spart = sslot + kPartTileRows;                                   // [tile]
+  const unsigned gmask = (1u << gshift) - 1u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int p = tid; p < parts; p += kScatterThreads) cnt[p] = 0u;
+  __syncthreads();
+  for (i64 t0 = (i64)blockIdx.x * kPartTileRows; t0 < n; t0 += (i64)gridDim.x * kPartTileRows) {
+    unsigned pp[kScatterRows], gg[kScatterRows];
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r) {
+      const i64 i = t0 + r * kScatterThreads + tid;
+      pp[r] = 0xffffffffu;
+      if (i < n) {
+        const unsigned g = __ldcs(b.pgroup + i);
+        gg[r] = g;
+        pp[r] = g >> gshift;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r)
+      if (pp[r] != 0xffffffffu) gg[r] = (gg[r] & gmask) | atomicAdd(cnt + pp[r], 1u) << 16;
+    __syncthreads();
+    // block exclusive scan of cnt[0, parts): 4 consecutive per thread
+    unsigned c4[4], t = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = tid * 4 + j;
+      c4[j] = p < parts ? cnt[p] : 0u;
+      t += c4[j];
+    }
+    unsigned incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned w = wsum[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += v;
+      }
+      wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    unsigned run = wsum[warp] + incl - t;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = tid * 4 + j;
+      if (p < parts) {
+        tpre[p] = run;
+        if (c4[j]) base[p] = (unsigned)atomicAdd(b.pcur + p, (unsigned long long)c4[j]);
+        cnt[p] = 0u;
+      }
+      run += c4[j];
+    }
+    __syncthreads();
+    // stage: slots and partitions, then one aggregate's values at a time
+    unsigned sidx[kScatterRows];
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r) {
+      if (pp[r] != 0xffffffffu) {
+        sidx[r] = tpre[pp[r]] + (gg[r] >> 16);
+        sslot[sidx[r]] = (unsigned short)(gg[r] & 0xffffu);
+        spart[sidx[r]] = (unsigned short)pp[r];
+      }
+    }
+    const int tile = (int)min((i64)kPartTileRows, n - t0);
+    __syncthreads();
+    for (int s2 = tid; s2 < tile; s2 += kScatterThreads) {
+      const unsigned p = spart[s2];
+      b.pslot[(i64)base[p] + (s2 - tpre[p])] = sslot[s2];
+    }
+    for (int a = 0; a < vs.naggs; ++a) {
+      if (vs.kind[a] == TDP_AGG_COUNT) continue;
+      const bool f = vs.kind[a] == TDP_AGG_SUM_F64;
+#pragma unroll
+      for (int r = 0; r < kScatterRows; ++r) {
+        const i64 i = t0 + r * kScatterThreads + tid;
+        if (pp[r] != 0xffffffffu)
+          sval[sidx[r]] = f ? (u64)__double_as_longlong(load_as_f64(vs.p[a], vs.dt[a], i))
+                            : (u64)load_as_i64(vs.p[a], vs.dt[a], i);
+      }
+      __syncthreads();
+      for (int s2 = tid; s2 < tile; s2 += kScatterThreads) {
+        const unsigned p = spart[s2];
+        b.pval[(i64)a * n + (i64)base[p] + (s2 - tpre[p])] = sval[s2];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+}
+
+// One CTA per partition: its groups' cells (the cell layout minus the key
+// image, `cw - 1` words each) in shared memory, shared-memory atomics per
+// row, then one coalesced write of the cells.
+__global__ void __launch_bounds__(1024)
+    part_agg_kernel(BitmapAgg b, i64 n, ValSet vs, int gshift) {
+  extern __shared__ unsigned long long pa_sm[];
+  const int sw = b.cw - 1;
+  const i64 p = blockIdx.x;
+  const i64 g0 = p << gshift;
+  const i64 m = (i64)*b.m;
+  if (g0 >= m) return;
+  const i64 ng = min((i64)1 << gshift, m - g0);
+  for (i64 w = threadIdx.x; w < ng * sw; w += blockDim.x) pa_sm[w] = 0ull;
+  __syncthreads();
+  const i64 lo = b.poffs[p], hi = lo + b.phist[p];
+  for (i64 i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    unsigned long long* c = pa_sm + (i64)b.pslot[i] * sw;  // c[w] = cell word w + 1
+    atomicAdd(reinterpret_cast<unsigned*>(c + (kCellCnt - 1)), 1u);  // low half: < 2^31 rows
+    for (int a = 0; a < vs.naggs; ++a) {
+      if (vs.kind[a] == TDP_AGG_COUNT) continue;
+      const u64 v = b.pval[(i64)a * n + i];
+      if (vs.kind[a] == TDP_AGG_SUM_F64)
+        fixed_add(c + (kCellAcc - 1) + vs.naggs + kFixedWords * vs.fidx[a],
+                  __longlong_as_double((long long)v));
+      else
+        atomicAdd(c + (kCellAcc - 1) + a, (unsigned long long)v);
+    }
+  }
+  __syncthreads();
+  u64* out = b.cells + g0 * b.cw;
+  for (i64 w = threadIdx.x; w < ng * sw; w += blockDim.x) {
+    const i64 g = w / sw;
+    out[g * b.cw + 1 + (w - g * sw)] = pa_sm[w];
+  }
+}
+
 }  // namespace
 }  // namespace tdp
 
@@ -2652,10 +2893,43 @@ int tdp_groupby_bitmap_prepare(const int64_t* keys, int64_t n, int64_t lo, int64
   rc = exclusive_scan_i64(b.bcount, b.boffs, blocks, reinterpret_cast<i64*>(b.m), b.scan_ws,
                           b.scan_bytes, st);
   if (rc) return rc;
-  bm_clear_kernel<<<stream_grid(n * b.cw, 256 * 4, 8), 256, 0, st>>>(b);
-  TDP_LAUNCH_CHECK("bm_clear_kernel");
-  bm_accum_kernel<<<stream_grid(n, 256, 32), 256, 0, st>>>(keys, n, b, vs);
-  TDP_LAUNCH_CHECK("bm_accum_kernel");
+  // partitioned accumulation: G groups per partition (a power of two whose
+  // cells fit kPartSmem), P partitions over the <= min(n, range) groups
+  int gshift = 15;
+  while (gshift > 0 && ((size_t)1 << gshift) * (size_t)(b.cw - 1) * 8 > (size_t)kPartSmem) --gshift;
+  const i64 gbound = n < key_range ? n : key_range;
+  const i64 parts = (gbound + ((i64)1 << gshift) - 1) >> gshift;
+  const char* part_env = getenv("TDP_GROUPBY_PARTITION");  // A/B tests and measurements
+  const bool part_on = !(part_env && part_env[0] == '0');
+  if (part_on && b.pslot != nullptr && n < ((i64)1 << 31) && ((i64)1 << gshift) >= kPartMinGroups &&
+      parts <= kPartMaxParts) {
+    bm_keys_kernel<<<stream_grid(words, 256, 8), 256, 0, st>>>(b, words);
+    TDP_LAUNCH_CHECK("bm_keys_kernel");
+    TDP_CUDA_TRY(cudaMemsetAsync(b.phist, 0, (size_t)parts * 8, st));
+    part_hist_kernel<<<stream_grid(n, 256 * 16, 8), 256, (size_t)parts * 4, st>>>(keys, n, b, gshift,
+                                                                                  (int)parts);
+    TDP_LAUNCH_CHECK("part_hist_kernel");
+    rc = exclusive_scan_i64(b.phist, b.poffs, parts, nullptr, b.pscan_ws, b.pscan_bytes, st);
+    if (rc) return rc;
+    TDP_CUDA_TRY(cudaMemcpyAsync(b.pcur, b.poffs, (size_t)parts * 8, cudaMemcpyDeviceToDevice, st));
+    const size_t ssm = (size_t)kPartMaxParts * 12 + 128 + (size_t)kPartTileRows * 12;
+    TDP_CUDA_TRY(cudaFuncSetAttribute(part_scatter_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ssm));
+    TDP_CUDA_TRY(cudaFuncSetAttribute(part_agg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kPartSmem));
+    part_scatter_kernel<<<stream_grid(n, kPartTileRows, 1), kScatterThreads, ssm, st>>>(
+        n, b, vs, gshift, (int)parts);
+    TDP_LAUNCH_CHECK("part_scatter_kernel");
+    const size_t asm_ = ((size_t)1 << gshift) * (size_t)(b.cw - 1) * 8;
+    part_agg_kernel<<<(unsigned)parts, 1024, asm_, st>>>(b, n, vs, gshift);
+    TDP_LAUNCH_CHECK("part_agg_kernel");
+  } else {
+    bm_clear_kernel<<<stream_grid(n * b.cw, 256 * 4, 8), 256, 0, st>>>(b);
+    TDP_LAUNCH_CHECK("bm_clear_kernel");
+    bm_accum_kernel<<<stream_grid(n, 256, 32), 256, 0, st>>>(keys, n, b, vs);
+    TDP_LAUNCH_CHECK("bm_accum_kernel");
+  }
   TDP_CUDA_TRY(cudaMemcpyAsync(out_ngroups, b.m, 8, cudaMemcpyDeviceToDevice, st));
   return TDP_OK;
 }

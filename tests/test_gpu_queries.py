@@ -609,3 +609,48 @@ def test_topk_radix_select_large(dist, k, desc):
     got = topk_order(tq.plain(tq.Tensor(v)), k, desc).cpu().numpy()
     exp = orc.stable_order(v, desc)[:k]
     np.testing.assert_array_equal(got, exp)
+
+
+@pytest.mark.parametrize("case", ["many_groups", "hot_key", "int64_ends"])
+def test_bitmap_groupby_partitioned_equals_unpartitioned(case, monkeypatch):
+    """>= 2^22 rows: the bitmap-rank group-by scatters rows into partitions of
+    groups and aggregates each in shared memory (part_*_kernel); its results
+    must be bitwise those of the one-pass atomic kernel (TDP_GROUPBY_PARTITION=0)
+    -- both accumulate exactly (fixed-point floats, wrapping int64) -- and
+    match the oracle."""
+    from paper_2211_02753_b200.kernels import groupby_exact
+
+    rng = np.random.default_rng({"many_groups": 1, "hot_key": 2, "int64_ends": 3}[case])
+    n = (1 << 22) + 12_345
+    if case == "many_groups":
+        key = rng.integers(0, 3_000_000, size=n).astype(np.int64)
+    elif case == "hot_key":
+        key = rng.integers(0, 2_000_000, size=n).astype(np.int64)
+        key[: n * 3 // 4] = 777  # 3/4 of the rows in one group (limb headroom)
+    else:
+        key = (2**63 - 2_500_000 + rng.integers(0, 2_500_000, size=n)).astype(np.int64)
+        key[::7] = 2**63 - 1
+    sign = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    fv = sign * rng.random(n) * 10.0 ** rng.integers(-20, 20, size=n)
+    fv[:3] = [np.inf, -np.inf, np.nan]
+    iv = rng.integers(-2**62, 2**62, size=n)
+    iv[:2] = [-2**63, 2**63 - 1]
+    spec = [("sum", tq.Tensor(fv)), ("avg", tq.Tensor(fv)), ("sum", tq.Tensor(iv)),
+            ("count", None)]
+    col = tq.plain(tq.Tensor(key))
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TDP_GROUPBY_PARTITION", mode)
+        kv, aggs = groupby_exact([col], spec)
+        got[mode] = [kv[0].cpu().numpy()] + [a.cpu().numpy() for a in aggs]
+    for a, b in zip(got["1"], got["0"]):
+        assert a.dtype == b.dtype and a.tobytes() == b.tobytes()
+    ek, ea = orc.groupby_exact([key], [("sum", fv), ("avg", fv), ("sum", iv), ("count", None)])
+    np.testing.assert_array_equal(got["1"][0], ek[0])
+    np.testing.assert_array_equal(got["1"][3], ea[2])
+    np.testing.assert_array_equal(got["1"][4], ea[3])
+    for j in (0, 1):
+        g, e = got["1"][1 + j], ea[j]
+        assert np.array_equal(np.isnan(g), np.isnan(e))
+        ok = ~np.isnan(e)
+        np.testing.assert_allclose(g[ok], e[ok], rtol=1e-7, atol=1e-12)

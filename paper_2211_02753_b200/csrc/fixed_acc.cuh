@@ -31,7 +31,41 @@ constexpr int kFixedLimbs = 8;
 constexpr int kFixedScale = 128;  // value = integer * 2^-128
 constexpr int kFixedMaxExp = 88;  // |x| < 2^88 goes to the limbs
 
+// A signed 64-bit add into a 64-bit word kept as two 32-bit halves (shared
+// memory: 32-bit atomics are native there, 64-bit ones a CAS loop): the low
+// half's returned old value gives this add's carry / borrow into the high
+// half, so the word's total is exact under any interleaving.
+__device__ __forceinline__ void split_add64(unsigned long long* word, unsigned long long x) {
+  unsigned* h = reinterpret_cast<unsigned*>(word);  // [0] low, [1] high (little-endian)
+  const unsigned lo = (unsigned)x;
+  unsigned hi = (unsigned)(x >> 32);
+  if (lo) {
+    const unsigned old = atomicAdd(h, lo);
+    hi += old > 0xffffffffu - lo ? 1u : 0u;  // carry out of the low half
+  }
+  if (hi) atomicAdd(h + 1, hi);
+}
+
+__device__ __forceinline__ void split_sub32(unsigned long long* word, unsigned x) {
+  unsigned* h = reinterpret_cast<unsigned*>(word);
+  const unsigned old = atomicSub(h, x);
+  if (old < x) atomicSub(h + 1, 1u);  // borrow
+}
+
+template <bool kSplit>
+__device__ __forceinline__ void fixed_add_impl(unsigned long long* cell, double x);
+
 __device__ __forceinline__ void fixed_add(unsigned long long* cell, double x) {
+  fixed_add_impl<false>(cell, x);
+}
+
+// fixed_add for a cell in shared memory (32-bit atomics, same words)
+__device__ __forceinline__ void fixed_add_shared(unsigned long long* cell, double x) {
+  fixed_add_impl<true>(cell, x);
+}
+
+template <bool kSplit>
+__device__ __forceinline__ void fixed_add_impl(unsigned long long* cell, double x) {
   const long long bits = __double_as_longlong(x);
   const int e = (int)((bits >> 52) & 0x7ff);
   if (e == 0) return;  // +-0 and subnormals (< 2^-1022): below the resolution
@@ -52,8 +86,16 @@ __device__ __forceinline__ void fixed_add(unsigned long long* cell, double x) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const unsigned long long piece = (unsigned long long)(t >> (32 * i)) & 0xffffffffull;
-    if (piece != 0ull && j0 + i < kFixedLimbs)
-      atomicAdd(cell + j0 + i, neg ? (unsigned long long)(-(long long)piece) : piece);
+    if (piece != 0ull && j0 + i < kFixedLimbs) {
+      if (kSplit) {
+        if (neg)
+          split_sub32(cell + j0 + i, (unsigned)piece);
+        else
+          split_add64(cell + j0 + i, piece);
+      } else {
+        atomicAdd(cell + j0 + i, neg ? (unsigned long long)(-(long long)piece) : piece);
+      }
+    }
   }
 }
 

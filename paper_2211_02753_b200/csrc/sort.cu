@@ -2843,10 +2843,10 @@ __global__ void __launch_bounds__(1024)
       if (vs.kind[a] == TDP_AGG_COUNT) continue;
       const u64 v = b.pval[(i64)a * n + i];
       if (vs.kind[a] == TDP_AGG_SUM_F64)
-        fixed_add(c + (kCellAcc - 1) + vs.naggs + kFixedWords * vs.fidx[a],
-                  __longlong_as_double((long long)v));
+        fixed_add_shared(c + (kCellAcc - 1) + vs.naggs + kFixedWords * vs.fidx[a],
+                         __longlong_as_double((long long)v));
       else
-        atomicAdd(c + (kCellAcc - 1) + a, (unsigned long long)v);
+        split_add64(c + (kCellAcc - 1) + a, (unsigned long long)v);
     }
   }
   __syncthreads();

@@ -2513,6 +2513,7 @@ struct BitmapAgg {
   // partitioned accumulation (part_ws_bytes; null below kPartMinRows)
   unsigned short* pslot;  // [n] group within its partition
   unsigned* pgroup;       // [n] group of each row (part_hist_kernel)
+  u64* prw;               // [words] bits | in-block prefix << 32: one load per rank
   u64* pval;              // [naggs][n] value bits in partition order
   i64* phist;             // [P] rows per partition
   i64* poffs;             // [P] partition starts
@@ -2531,10 +2532,11 @@ constexpr int kPartSmem = 200 * 1024;
 constexpr int kPartMinGroups = 256;  // G below this: the unpartitioned kernel
 constexpr int kPartTileRows = 8192;  // scatter tile: 1024 threads x 8 rows
 
-size_t part_ws_bytes(i64 n, int naggs) {
+size_t part_ws_bytes(i64 n, i64 range, int naggs) {
   if (n < kPartMinRows) return 0;
   return align256((size_t)n * 2) + align256((size_t)n * 4) +
          (size_t)(naggs > 0 ? naggs : 0) * align256((size_t)n * 8) +
+         align256((size_t)rank_words(range) * 8) +
          3 * align256((size_t)(kPartMaxParts + 1) * 8) +
          align256(exclusive_scan_workspace(kPartMaxParts) + 1024);
 }
@@ -2545,7 +2547,7 @@ size_t bitmap_agg_ws_bytes(i64 n, i64 range, int naggs) {
   const int na = naggs > 0 ? naggs : 0;
   return align256((size_t)words * 4) + align256((size_t)words * 2) + 2 * align256((size_t)blocks * 8) +
          256 + align256((size_t)(n > 0 ? n : 1) * cell_words(na, na) * 8) +
-         align256(exclusive_scan_workspace(blocks)) + 2048 + part_ws_bytes(n, na);
+         align256(exclusive_scan_workspace(blocks)) + 2048 + part_ws_bytes(n, r, na);
 }
 
 BitmapAgg carve_bitmap_agg(void* ws, i64 n, i64 range, i64 lo, const ValSet& vs) {
@@ -2587,6 +2589,8 @@ BitmapAgg carve_bitmap_agg(void* ws, i64 n, i64 range, i64 lo, const ValSet& vs)
     p += align256((size_t)(kPartMaxParts + 1) * 8);
     b.pscan_ws = p;
     b.pscan_bytes = exclusive_scan_workspace(kPartMaxParts) + 1024;
+    p += align256(exclusive_scan_workspace(kPartMaxParts) + 1024);
+    b.prw = (u64*)p;
   }
   return b;
 }
@@ -2685,6 +2689,12 @@ __global__ void bm_keys_kernel(BitmapAgg b, i64 words) {
   }
 }
 
+__global__ void rank_pack_kernel(BitmapAgg b, i64 words) {
+  for (i64 w = (i64)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (i64)gridDim.x * blockDim.x)
+    b.prw[w] = (u64)b.bits[w] | (u64)b.wpre[w] << 32;
+}
+
 // Rows per partition (partition = group >> gshift): shared counters, one
 // global add per CTA and partition.
 __global__ void part_hist_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg b, int gshift,
@@ -2694,7 +2704,10 @@ __global__ void part_hist_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg 
   __syncthreads();
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (i64)gridDim.x * blockDim.x) {
-    const i64 g = bm_rank(b, (u64)__ldg(keys + i) - b.lo);
+    const u64 d = (u64)__ldg(keys + i) - b.lo;
+    const u64 rw = __ldg(b.prw + (d >> 5));
+    const i64 g = __ldg(b.boffs + (d >> 10)) + (i64)(rw >> 32) +
+                  __popc((unsigned)rw & ((1u << (d & 31)) - 1u));
     b.pgroup[i] = (unsigned)g;
     atomicAdd(ph_cnt + (g >> gshift), 1u);
   }
@@ -2905,6 +2918,8 @@ int tdp_groupby_bitmap_prepare(const int64_t* keys, int64_t n, int64_t lo, int64
       parts <= kPartMaxParts) {
     bm_keys_kernel<<<stream_grid(words, 256, 8), 256, 0, st>>>(b, words);
     TDP_LAUNCH_CHECK("bm_keys_kernel");
+    rank_pack_kernel<<<stream_grid(words, 256, 8), 256, 0, st>>>(b, words);
+    TDP_LAUNCH_CHECK("rank_pack_kernel");
     TDP_CUDA_TRY(cudaMemsetAsync(b.phist, 0, (size_t)parts * 8, st));
     part_hist_kernel<<<stream_grid(n, 256 * 16, 8), 256, (size_t)parts * 4, st>>>(keys, n, b, gshift,
                                                                                   (int)parts);

@@ -508,8 +508,9 @@ int tdp_csv_string_column(const uint8_t* bytes, const int64_t* field_ends, int32
  * out_counts[m], out_sums[naggs][m] as tdp_groupby_hash_emit.  Same contract
  * as the hash group-by (groupby_exact, tq/kernels.py:108-167).  From 2^22
  * rows on (and <= 4096 partitions of groups) the rows are first scattered
- * into partitions whose cells fit shared memory and aggregated there (same
- * results bit for bit); the workspace then also holds the partitioned rows
+ * into partitions whose cells fit shared memory and aggregated there (every
+ * row added exactly; repeatable bit for bit); the workspace then also holds
+ * the partitioned rows
  * (2 + 4 + 8 x naggs bytes per row).  TDP_GROUPBY_PARTITION=0 disables it. */
 size_t tdp_groupby_bitmap_workspace(int64_t n, int64_t key_range, int32_t naggs);
 int tdp_groupby_bitmap_prepare(const int64_t* keys, int64_t n, int64_t lo, int64_t key_range,

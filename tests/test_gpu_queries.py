@@ -614,10 +614,11 @@ def test_topk_radix_select_large(dist, k, desc):
 @pytest.mark.parametrize("case", ["many_groups", "hot_key", "int64_ends"])
 def test_bitmap_groupby_partitioned_equals_unpartitioned(case, monkeypatch):
     """>= 2^22 rows: the bitmap-rank group-by scatters rows into partitions of
-    groups and aggregates each in shared memory (part_*_kernel); its results
-    must be bitwise those of the one-pass atomic kernel (TDP_GROUPBY_PARTITION=0)
-    -- both accumulate exactly (fixed-point floats, wrapping int64) -- and
-    match the oracle."""
+    groups and aggregates each in shared memory (part_*_kernel); on these
+    inputs its results are bitwise those of the one-pass atomic kernel
+    (TDP_GROUPBY_PARTITION=0) -- fixed-point floats (the one-pass kernel
+    pre-adds a warp's equal keys in double: a last-bit difference in
+    general), wrapping int64 -- and match the oracle."""
     from paper_2211_02753_b200.kernels import groupby_exact
 
     rng = np.random.default_rng({"many_groups": 1, "hot_key": 2, "int64_ends": 3}[case])

@@ -2530,7 +2530,7 @@ constexpr i64 kPartMinRows = (i64)1 << 22;
 constexpr int kPartMaxParts = 4096;
 constexpr int kPartSmem = 200 * 1024;
 constexpr int kPartMinGroups = 256;  // G below this: the unpartitioned kernel
-constexpr int kPartTileRows = 8192;  // scatter tile: 1024 threads x 8 rows
+constexpr int kPartTileRows = 12288;  // scatter tile: 1024 threads x 12 rows
 
 size_t part_ws_bytes(i64 n, i64 range, int naggs) {
   if (n < kPartMinRows) return 0;
@@ -2717,7 +2717,7 @@ __global__ void part_hist_kernel(const i64* __restrict__ keys, i64 n, BitmapAgg 
       atomicAdd(reinterpret_cast<unsigned long long*>(b.phist) + p, (unsigned long long)ph_cnt[p]);
 }
 
-// Scatter rows into their partitions, 8192-row tiles of 1024 threads: count
+// Scatter rows into their partitions, 12288-row tiles of 1024 threads: count
 // per partition in shared memory (each row's place in its partition's run),
 // a block scan of the counts (the tile's rows staged in partition order),
 // one global add per partition and tile to reserve the runs, then the staged
